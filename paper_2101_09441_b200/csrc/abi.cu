@@ -1,0 +1,739 @@
+// abi.cu -- extern "C" entry points for index build, queries and insertion.
+// See include/dbl_b200.h for the contract and the reference function each
+// entry point replaces.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace dbl {
+
+static thread_local std::string g_last_error;
+static uint64_t g_launches = 0;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+uint64_t &launch_counter() { return g_launches; }
+
+dbl_status cuda_fail(cudaError_t e, const char *what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? DBL_E_OOM : DBL_E_CUDA;
+}
+
+dbl_status make_override(dbl_graph *g, const uint32_t *ids, const uint32_t *buckets, uint32_t cnt,
+                         DevBuf &ovr);
+dbl_status query_finish(dbl_graph *g, uint32_t *err_out);
+
+static int grid_for(uint64_t work, int threads = 256, int cap = 148 * 16) {
+    uint64_t b = (work + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > (uint64_t)cap) b = cap;
+    return (int)b;
+}
+
+__global__ void certified_kernel(const uint64_t *__restrict__ rec, uint32_t rw, uint32_t wdl,
+                                 const uint64_t *__restrict__ keys, uint64_t count,
+                                 unsigned long long *out) {
+    const uint32_t H = rw / 2;
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        const uint64_t *ru = rec + (k >> 32) * rw, *rv = rec + (uint32_t)k * (uint64_t)rw;
+        uint64_t acc = 0;
+        for (uint32_t w = 0; w < wdl; ++w) acc |= ru[H + w] & rv[w];  // dl_out[u] & dl_in[v]
+        c += acc != 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+__global__ void pack_pairs_kernel(const uint32_t *__restrict__ u, const uint32_t *__restrict__ v,
+                                  uint64_t count, uint32_t n, uint64_t *__restrict__ keys,
+                                  unsigned long long *err) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t a = u[i], b = v[i];
+        if (a >= n || b >= n) { atomicOr(err, 1ull); a = 0; b = 0; }
+        keys[i] = ((uint64_t)a << 32) | b;
+    }
+}
+
+// family f of a record: (word offset within record, words)
+static void family_span(const dbl_index *idx, int f, uint32_t &off, uint32_t &w) {
+    const uint32_t H = idx->wdl + idx->wbl;
+    switch (f) {
+    case 0: off = 0; w = idx->wdl; break;                 // dl_in
+    case 1: off = H; w = idx->wdl; break;                 // dl_out
+    case 2: off = idx->wdl; w = idx->wbl; break;          // bl_in
+    default: off = H + idx->wdl; w = idx->wbl; break;     // bl_out
+    }
+}
+
+__global__ void gather_family_kernel(const uint64_t *__restrict__ rec, uint32_t rw, uint32_t off, uint32_t w,
+                                     uint32_t n, uint64_t *__restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * w;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = rec[(i / w) * rw + off + i % w];
+}
+
+__global__ void scatter_family_kernel(uint64_t *__restrict__ rec, uint32_t rw, uint32_t off, uint32_t w,
+                                      uint32_t n, const uint64_t *__restrict__ in) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * w;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        rec[(i / w) * rw + off + i % w] = in[i];
+}
+
+__global__ void diff_kernel(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b, uint64_t count,
+                            unsigned long long *out) {
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        c |= a[i] != b[i];
+    if (__any_sync(FULL, c) && (threadIdx.x & 31) == 0) atomicOr(out, 1ull);
+}
+
+__global__ void fill_tail_kernel(uint32_t *__restrict__ ptr, uint32_t from, uint32_t to) {
+    const uint32_t val = ptr[from - 1];
+    for (uint32_t i = from + blockIdx.x * blockDim.x + threadIdx.x; i < to; i += gridDim.x * blockDim.x)
+        ptr[i] = val;
+}
+
+}  // namespace dbl
+
+using namespace dbl;
+
+extern "C" const char *dbl_last_error(void) { return g_last_error.c_str(); }
+extern "C" int dbl_version(void) { return 1; }
+extern "C" uint64_t dbl_kernel_launches(void) { return g_launches; }
+
+static dbl_status check_pair(const dbl_index *idx, const dbl_graph *g) {
+    if (!idx || !g) { set_error("null handle"); return DBL_E_ARG; }
+    if (idx->n != g->n) {
+        set_error("graph has " + std::to_string(g->n) + " vertices but index has " + std::to_string(idx->n));
+        return DBL_E_MISMATCH;
+    }
+    return DBL_OK;
+}
+
+static dbl_status alloc_index(const dbl_graph *g, const dbl_config *cfg, dbl_index **out) {
+    if (cfg->k > g->n) {
+        set_error("k=" + std::to_string(cfg->k) + " exceeds vertex count " + std::to_string(g->n));
+        return DBL_E_CONFIG;
+    }
+    if (cfg->k_prime < 1) { set_error("k_prime must be >= 1"); return DBL_E_CONFIG; }
+    if (cfg->strategy < 0 || cfg->strategy > 3) { set_error("unknown landmark strategy"); return DBL_E_CONFIG; }
+    dbl_index *idx = new dbl_index();
+    idx->device = g->device;
+    idx->n = g->n;
+    idx->cfg = *cfg;
+    idx->wdl = (cfg->k + 63) / 64;
+    idx->wbl = (cfg->k_prime + 63) / 64;
+    idx->rw = 2 * (idx->wdl + idx->wbl);
+    if (idx->wdl > 16 || idx->wbl > 16) {
+        delete idx;
+        set_error("label widths above 1024 bits are not supported");
+        return DBL_E_CONFIG;
+    }
+    dbl_status s;
+    if ((s = idx->rec.ensure((size_t)g->n * idx->rw * 8 + 16)) || (s = idx->landmarks.ensure((size_t)cfg->k * 4 + 4)) ||
+        (s = idx->leaf_flags.ensure((size_t)g->n + 16)) || (s = idx->bucket.ensure((size_t)g->n * 4 + 16))) {
+        dbl_index_free(idx);
+        return s;
+    }
+    *out = idx;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_index_build(const dbl_graph *gc, const dbl_config *cfg, const uint32_t *landmarks,
+                                      const uint8_t *leaf_flags, const uint32_t *bucket,
+                                      const uint32_t *ovr_ids, const uint32_t *ovr_buckets, uint32_t n_ovr,
+                                      dbl_index **out) {
+    if (!gc || !cfg || !out) { set_error("null argument"); return DBL_E_ARG; }
+    *out = nullptr;
+    dbl_graph *g = const_cast<dbl_graph *>(gc);
+    DBL_CUDA(cudaSetDevice(g->device));
+    if (landmarks && cfg->k) {  // LandmarkSet.of + _check_vertex (labels.py:59-63, 279-283)
+        std::vector<uint32_t> seen(landmarks, landmarks + cfg->k);
+        for (uint32_t i = 0; i < cfg->k; ++i)
+            if (landmarks[i] >= g->n) {
+                set_error("vertex " + std::to_string(landmarks[i]) + " outside [0, " + std::to_string(g->n) + ")");
+                return DBL_E_VERTEX_RANGE;
+            }
+        std::sort(seen.begin(), seen.end());
+        if (std::adjacent_find(seen.begin(), seen.end()) != seen.end()) {
+            set_error("landmark vertices must be distinct");
+            return DBL_E_CONFIG;
+        }
+    }
+    dbl_index *idx = nullptr;
+    dbl_status s = alloc_index(g, cfg, &idx);
+    if (s) return s;
+    auto fail = [&](dbl_status st) { dbl_index_free(idx); return st; };
+    if (cfg->k) {
+        if (landmarks) {
+            DBL_CUDA(cudaMemcpyAsync(idx->landmarks.p, landmarks, (size_t)cfg->k * 4, cudaMemcpyHostToDevice, g->stream));
+        } else if ((s = select_landmarks_dev(g, cfg->k, cfg->strategy, idx->landmarks.as<uint32_t>()))) {
+            return fail(s);
+        }
+    }
+    if (g->n) {
+        if (leaf_flags && bucket) {
+            DBL_CUDA(cudaMemcpyAsync(idx->leaf_flags.p, leaf_flags, g->n, cudaMemcpyHostToDevice, g->stream));
+            DBL_CUDA(cudaMemcpyAsync(idx->bucket.p, bucket, (size_t)g->n * 4, cudaMemcpyHostToDevice, g->stream));
+        } else {
+            DevBuf ovr;
+            const uint32_t *dovr = nullptr;
+            if (ovr_ids && n_ovr) {
+                if ((s = make_override(g, ovr_ids, ovr_buckets, n_ovr, ovr))) { ovr.release(); return fail(s); }
+                dovr = ovr.as<uint32_t>();
+            }
+            s = select_leaves_dev(g, cfg->leaf_threshold, cfg->k_prime, cfg->hash_seed, dovr,
+                                  idx->leaf_flags.as<uint8_t>(), idx->bucket.as<uint32_t>());
+            ovr.release();
+            if (s) return fail(s);
+        }
+    }
+    if ((s = run_build(g, idx, nullptr, 0))) return fail(s);
+    *out = idx;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_index_rebuild(const dbl_graph *gc, dbl_index *idx) {
+    dbl_status s = check_pair(idx, gc);
+    if (s) return s;
+    dbl_graph *g = const_cast<dbl_graph *>(gc);
+    DBL_CUDA(cudaSetDevice(g->device));
+    return run_build(g, idx, nullptr, 0);
+}
+
+extern "C" dbl_status dbl_index_build_words(const dbl_graph *gc, dbl_index *idx, const uint32_t *words,
+                                            uint32_t nwords) {
+    dbl_status s = check_pair(idx, gc);
+    if (s) return s;
+    for (uint32_t i = 0; i < nwords; ++i)
+        if (words[i] >= idx->rw) { set_error("record word out of range"); return DBL_E_ARG; }
+    dbl_graph *g = const_cast<dbl_graph *>(gc);
+    DBL_CUDA(cudaSetDevice(g->device));
+    return run_build(g, idx, words, nwords);
+}
+
+extern "C" dbl_status dbl_index_free(dbl_index *idx) {
+    if (!idx) return DBL_OK;
+    cudaSetDevice(idx->device);
+    cudaDeviceSynchronize();
+    idx->rec.release();
+    idx->landmarks.release();
+    idx->leaf_flags.release();
+    idx->bucket.release();
+    delete idx;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_index_info(const dbl_index *idx, uint32_t *n, dbl_config *cfg) {
+    if (!idx) { set_error("null index"); return DBL_E_ARG; }
+    if (n) *n = idx->n;
+    if (cfg) *cfg = idx->cfg;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_index_metadata(const dbl_index *idx, uint32_t *landmarks, uint8_t *leaf_flags,
+                                         uint32_t *bucket) {
+    if (!idx) { set_error("null index"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(idx->device));
+    if (landmarks && idx->cfg.k) DBL_CUDA(cudaMemcpy(landmarks, idx->landmarks.p, (size_t)idx->cfg.k * 4, cudaMemcpyDeviceToHost));
+    if (leaf_flags && idx->n) DBL_CUDA(cudaMemcpy(leaf_flags, idx->leaf_flags.p, idx->n, cudaMemcpyDeviceToHost));
+    if (bucket && idx->n) DBL_CUDA(cudaMemcpy(bucket, idx->bucket.p, (size_t)idx->n * 4, cudaMemcpyDeviceToHost));
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_index_export(const dbl_index *idx, uint64_t *dl_in, uint64_t *dl_out, uint64_t *bl_in,
+                                       uint64_t *bl_out) {
+    if (!idx) { set_error("null index"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(idx->device));
+    uint64_t *outs[4] = {dl_in, dl_out, bl_in, bl_out};
+    DevBuf tmp;
+    for (int f = 0; f < 4; ++f) {
+        uint32_t off, w;
+        family_span(idx, f, off, w);
+        if (!outs[f] || !w || !idx->n) continue;
+        const uint64_t cnt = (uint64_t)idx->n * w;
+        dbl_status s = tmp.ensure(cnt * 8);
+        if (s) return s;
+        gather_family_kernel<<<grid_for(cnt), 256>>>(idx->rec.as<uint64_t>(), idx->rw, off, w, idx->n,
+                                                     tmp.as<uint64_t>());
+        DBL_LAUNCHED();
+        cudaError_t e = cudaMemcpy(outs[f], tmp.p, cnt * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) { tmp.release(); return cuda_fail(e, "export labels"); }
+    }
+    tmp.release();
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_index_import(dbl_index *idx, const uint64_t *dl_in, const uint64_t *dl_out,
+                                       const uint64_t *bl_in, const uint64_t *bl_out) {
+    if (!idx) { set_error("null index"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(idx->device));
+    const uint64_t *ins[4] = {dl_in, dl_out, bl_in, bl_out};
+    DevBuf tmp;
+    for (int f = 0; f < 4; ++f) {
+        uint32_t off, w;
+        family_span(idx, f, off, w);
+        if (!ins[f] || !w || !idx->n) continue;
+        const uint64_t cnt = (uint64_t)idx->n * w;
+        dbl_status s = tmp.ensure(cnt * 8);
+        if (s) return s;
+        cudaError_t e = cudaMemcpy(tmp.p, ins[f], cnt * 8, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { tmp.release(); return cuda_fail(e, "import labels"); }
+        scatter_family_kernel<<<grid_for(cnt), 256>>>(idx->rec.as<uint64_t>(), idx->rw, off, w, idx->n,
+                                                      tmp.as<uint64_t>());
+        DBL_LAUNCHED();
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    tmp.release();
+    if (e != cudaSuccess) return cuda_fail(e, "import labels");
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_index_equal(const dbl_index *a, const dbl_index *b, int *out_equal) {
+    if (!a || !b || !out_equal) { set_error("null argument"); return DBL_E_ARG; }
+    *out_equal = 0;
+    if (a->n != b->n || a->cfg.k != b->cfg.k || a->cfg.k_prime != b->cfg.k_prime) return DBL_OK;
+    if (a->device != b->device) { set_error("indexes live on different devices"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(a->device));
+    DevBuf flag;
+    dbl_status s = flag.ensure(8);
+    if (s) return s;
+    cudaMemset(flag.p, 0, 8);
+    const uint64_t cnt = (uint64_t)a->n * a->rw;
+    if (cnt) {
+        diff_kernel<<<grid_for(cnt), 256>>>(a->rec.as<uint64_t>(), b->rec.as<uint64_t>(), cnt,
+                                            flag.as<unsigned long long>());
+        DBL_LAUNCHED();
+    }
+    unsigned long long h = 1;
+    cudaError_t e = cudaMemcpy(&h, flag.p, 8, cudaMemcpyDeviceToHost);
+    flag.release();
+    if (e != cudaSuccess) return cuda_fail(e, "index_equal");
+    *out_equal = h == 0;
+    return DBL_OK;
+}
+
+static dbl_status grow_buf(DevBuf &b, size_t old_bytes, size_t new_bytes, int fill) {
+    DevBuf nb;
+    dbl_status s = nb.ensure(new_bytes);
+    if (s) return s;
+    if (old_bytes) DBL_CUDA(cudaMemcpy(nb.p, b.p, old_bytes, cudaMemcpyDeviceToDevice));
+    if (new_bytes > old_bytes) DBL_CUDA(cudaMemset(nb.as<char>() + old_bytes, fill, new_bytes - old_bytes));
+    b.release();
+    b = nb;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_index_grow(dbl_index *idx, uint32_t n) {
+    if (!idx) { set_error("null index"); return DBL_E_ARG; }
+    if (n < idx->n) { set_error("index cannot shrink"); return DBL_E_CONFIG; }
+    if (n == idx->n) return DBL_OK;
+    DBL_CUDA(cudaSetDevice(idx->device));
+    dbl_status s;
+    if ((s = grow_buf(idx->rec, (size_t)idx->n * idx->rw * 8, (size_t)n * idx->rw * 8 + 16, 0)) ||
+        (s = grow_buf(idx->leaf_flags, idx->n, (size_t)n + 16, 0)) ||
+        (s = grow_buf(idx->bucket, (size_t)idx->n * 4, (size_t)n * 4 + 16, 0)))
+        return s;
+    idx->n = n;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_graph_add_vertices(dbl_graph *g, uint32_t count) {
+    if (!g) { set_error("null graph"); return DBL_E_ARG; }
+    if (!count) return DBL_OK;
+    if ((uint64_t)g->n + count >= 0xffffffffull) { set_error("vertex count overflow"); return DBL_E_CONFIG; }
+    DBL_CUDA(cudaSetDevice(g->device));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    const uint32_t n0 = g->n, n1 = n0 + count;
+    DevBuf *ptrs[4] = {&g->fptr, &g->rptr, &g->dfptr, &g->drptr};
+    for (int i = 0; i < 4; ++i) {
+        if (i >= 2 && !g->m_delta) { ptrs[i]->release(); continue; }
+        dbl_status s = grow_buf(*ptrs[i], ((size_t)n0 + 1) * 4, ((size_t)n1 + 1) * 4, 0);
+        if (s) return s;
+        fill_tail_kernel<<<grid_for(count), 256>>>(ptrs[i]->as<uint32_t>(), n0 + 1, n1 + 1);
+        DBL_LAUNCHED();
+    }
+    DBL_CUDA(cudaDeviceSynchronize());
+    g->n = n1;
+    for (int d = 0; d < 2; ++d) g->stamp[d].release();
+    g->changed_bits.release();
+    return graph_ensure_traversal(g);
+}
+
+extern "C" dbl_status dbl_index_records(const dbl_index *idx, uint64_t **dev_records, uint32_t *wpr) {
+    if (!idx) { set_error("null index"); return DBL_E_ARG; }
+    if (dev_records) *dev_records = idx->rec.as<uint64_t>();
+    if (wpr) *wpr = idx->rw;
+    return DBL_OK;
+}
+
+// ---------------------------------------------------------------- queries --
+
+static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const uint32_t *u, const uint32_t *v,
+                             uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, dbl_mem mem,
+                             bool sync) {
+    dbl_status s = check_pair(idx, gc);
+    if (s) return s;
+    if (count && (!u || !v || !codes)) { set_error("null argument"); return DBL_E_ARG; }
+    dbl_graph *g = const_cast<dbl_graph *>(gc);
+    DBL_CUDA(cudaSetDevice(g->device));
+    const uint32_t *du = u, *dv = v;
+    uint8_t *dc = codes;
+    uint32_t *dvis = visited;
+    if (mem == DBL_MEM_HOST && count) {
+        if ((s = g->q_in.ensure(count * 8)) || (s = g->q_codes.ensure(count + 16)) ||
+            (visited && (s = g->q_vis.ensure(count * 4))))
+            return s;
+        uint32_t *bu = g->q_in.as<uint32_t>();
+        DBL_CUDA(cudaMemcpyAsync(bu, u, count * 4, cudaMemcpyHostToDevice, g->stream));
+        DBL_CUDA(cudaMemcpyAsync(bu + count, v, count * 4, cudaMemcpyHostToDevice, g->stream));
+        du = bu;
+        dv = bu + count;
+        dc = g->q_codes.as<uint8_t>();
+        dvis = visited ? g->q_vis.as<uint32_t>() : nullptr;
+    }
+    if ((s = run_query(idx, g, du, dv, count, flags, dc, dvis))) return s;
+    if (mem == DBL_MEM_HOST && count) {
+        DBL_CUDA(cudaMemcpyAsync(codes, dc, count, cudaMemcpyDeviceToHost, g->stream));
+        if (visited) DBL_CUDA(cudaMemcpyAsync(visited, dvis, count * 4, cudaMemcpyDeviceToHost, g->stream));
+    }
+    if (!sync) return DBL_OK;
+    uint32_t err = 0;
+    if ((s = query_finish(g, &err))) return s;
+    if (err) { set_error("query vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_query(const dbl_index *idx, const dbl_graph *g, const uint32_t *u, const uint32_t *v,
+                                uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, dbl_mem mem) {
+    return query_impl(idx, g, u, v, count, flags, codes, visited, mem, true);
+}
+
+extern "C" dbl_status dbl_query_async(const dbl_index *idx, const dbl_graph *g, const uint32_t *u,
+                                      const uint32_t *v, uint64_t count, uint32_t flags, uint8_t *codes,
+                                      uint32_t *visited) {
+    return query_impl(idx, g, u, v, count, flags, codes, visited, DBL_MEM_DEVICE, false);
+}
+
+// ---------------------------------------------------------------- updates --
+
+static dbl_status count_certified(dbl_graph *g, const dbl_index *idx, const uint64_t *keys, uint64_t count,
+                                  uint64_t *out) {
+    *out = 0;
+    if (!count || !idx->wdl) return DBL_OK;
+    DevBuf c;
+    dbl_status s = c.ensure(8);
+    if (s) return s;
+    DBL_CUDA(cudaMemsetAsync(c.p, 0, 8, g->stream));
+    certified_kernel<<<grid_for(count), 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->rw, idx->wdl, keys,
+                                                              count, c.as<unsigned long long>());
+    DBL_LAUNCHED();
+    unsigned long long h = 0;
+    DBL_CUDA(cudaMemcpyAsync(&h, c.p, 8, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    c.release();
+    *out = h;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v,
+                                      dbl_update_stats *stats) {
+    dbl_status s = check_pair(idx, g);
+    if (s) return s;
+    if (u >= g->n || v >= g->n) {
+        set_error("vertex " + std::to_string(u >= g->n ? u : v) + " outside [0, " + std::to_string(g->n) + ")");
+        return DBL_E_VERTEX_RANGE;
+    }
+    DBL_CUDA(cudaSetDevice(g->device));
+    dbl_update_stats st{};
+    const uint64_t key = ((uint64_t)u << 32) | v;
+    if ((s = g->scratch_b.ensure(64))) return s;
+    uint64_t *dkey = g->scratch_b.as<uint64_t>();
+    DBL_CUDA(cudaMemcpyAsync(dkey, &key, 8, cudaMemcpyHostToDevice, g->stream));
+    uint64_t cert = 0;  // pre-check on pre-insertion labels, updates.py:123
+    if ((s = count_certified(g, idx, dkey, 1, &cert))) return s;
+    // add_edge (updates.py:124); graph_filter_new/insert_delta use scratch_a..d
+    DevBuf kb;
+    if ((s = kb.ensure(16))) return s;
+    DBL_CUDA(cudaMemcpyAsync(kb.p, &key, 8, cudaMemcpyHostToDevice, g->stream));
+    uint64_t nnew = 0;
+    DevBuf nb;
+    if ((s = nb.ensure(16))) { kb.release(); return s; }
+    s = graph_filter_new(g, kb.as<uint64_t>(), 1, nb.as<uint64_t>(), &nnew);
+    if (!s && nnew) s = graph_insert_delta(g, nb.as<uint64_t>(), nnew);
+    st.inserted = (uint32_t)nnew;
+    if (s || cert) {
+        kb.release();
+        nb.release();
+        if (!s) {
+            st.early_terminated = 1;
+            if (stats) *stats = st;
+        }
+        return s;
+    }
+    uint32_t changed[2], seedc[2], levels = 0;
+    s = run_insert(g, idx, kb.as<uint64_t>(), 1, true, changed, seedc, &levels);
+    kb.release();
+    nb.release();
+    if (s) return s;
+    // _propagate_union dequeues the seed plus every changed non-seed vertex
+    st.visited = (1 + changed[0] - seedc[0]) + (1 + changed[1] - seedc[1]);
+    st.labels_changed = changed[0] + changed[1];
+    if (stats) *stats = st;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
+                                       uint64_t count, dbl_mem mem, dbl_batch_stats *stats) {
+    dbl_status s = check_pair(idx, g);
+    if (s) return s;
+    dbl_batch_stats st{};
+    st.requested = count;
+    if (!count) { if (stats) *stats = st; return DBL_OK; }
+    if (!u || !v) { set_error("null argument"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(g->device));
+    DevBuf in, keys, alt, newk, err;
+    auto cleanup = [&]() { in.release(); keys.release(); alt.release(); newk.release(); err.release(); };
+    if ((s = keys.ensure(count * 8)) || (s = alt.ensure(count * 8)) || (s = newk.ensure(count * 8)) ||
+        (s = err.ensure(8))) { cleanup(); return s; }
+    const uint32_t *du = u, *dv = v;
+    if (mem == DBL_MEM_HOST) {
+        if ((s = in.ensure(count * 8))) { cleanup(); return s; }
+        DBL_CUDA(cudaMemcpyAsync(in.p, u, count * 4, cudaMemcpyHostToDevice, g->stream));
+        DBL_CUDA(cudaMemcpyAsync(in.as<uint32_t>() + count, v, count * 4, cudaMemcpyHostToDevice, g->stream));
+        du = in.as<uint32_t>();
+        dv = du + count;
+    }
+    DBL_CUDA(cudaMemsetAsync(err.p, 0, 8, g->stream));
+    pack_pairs_kernel<<<grid_for(count), 256, 0, g->stream>>>(du, dv, count, g->n, keys.as<uint64_t>(),
+                                                              err.as<unsigned long long>());
+    DBL_LAUNCHED();
+    unsigned long long herr = 0;
+    DBL_CUDA(cudaMemcpyAsync(&herr, err.p, 8, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    if (herr) { cleanup(); set_error("insert vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+    uint64_t *sorted = nullptr;
+    if ((s = sort_keys(g, keys.as<uint64_t>(), alt.as<uint64_t>(), count, key_end_bit(g->n), &sorted))) {
+        cleanup();
+        return s;
+    }
+    // unique (in place into the other buffer)
+    uint64_t *uniq = sorted == keys.as<uint64_t>() ? alt.as<uint64_t>() : keys.as<uint64_t>();
+    {
+        DevBuf nsel;
+        if ((s = nsel.ensure(8))) { cleanup(); return s; }
+        size_t tmp = 0;
+        DBL_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted, uniq, nsel.as<uint64_t>(), (int64_t)count, g->stream));
+        if ((s = g->cub_tmp.ensure(tmp))) { nsel.release(); cleanup(); return s; }
+        DBL_CUDA(cub::DeviceSelect::Unique(g->cub_tmp.p, tmp, sorted, uniq, nsel.as<uint64_t>(), (int64_t)count,
+                                           g->stream));
+        DBL_LAUNCHED();
+        uint64_t nu = 0;
+        DBL_CUDA(cudaMemcpyAsync(&nu, nsel.p, 8, cudaMemcpyDeviceToHost, g->stream));
+        DBL_CUDA(cudaStreamSynchronize(g->stream));
+        nsel.release();
+        count = nu;
+    }
+    if ((s = count_certified(g, idx, uniq, count, &st.certified))) { cleanup(); return s; }
+    uint64_t nnew = 0;
+    if ((s = graph_filter_new(g, uniq, count, newk.as<uint64_t>(), &nnew))) { cleanup(); return s; }
+    st.inserted = nnew;
+    if (nnew) {
+        if ((s = graph_insert_delta(g, newk.as<uint64_t>(), nnew))) { cleanup(); return s; }
+        uint32_t changed[2], seedc[2], levels = 0;
+        if ((s = run_insert(g, idx, newk.as<uint64_t>(), nnew, true, changed, seedc, &levels))) {
+            cleanup();
+            return s;
+        }
+        st.labels_changed = (uint64_t)changed[0] + changed[1];
+        st.levels = levels;
+        if (g->m_delta * 4 > g->m_base + 1024) {
+            if ((s = graph_compact(g))) { cleanup(); return s; }
+            st.delta_merged = 1;
+        }
+    }
+    cleanup();
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    if (stats) *stats = st;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_work_model(const dbl_index *idx, const dbl_graph *gc, uint64_t *V, uint64_t *E,
+                                     uint32_t *levels) {
+    dbl_status s = check_pair(idx, gc);
+    if (s) return s;
+    if (!V || !E || !levels) { set_error("null argument"); return DBL_E_ARG; }
+    dbl_graph *g = const_cast<dbl_graph *>(gc);
+    DBL_CUDA(cudaSetDevice(g->device));
+    return work_model(idx, g, V, E, levels);
+}
+
+// -------------------------------------------------- multi-GPU word shards --
+
+__global__ void pack_words_kernel(const uint64_t *__restrict__ rec, uint32_t rw, uint32_t n,
+                                  const uint32_t *__restrict__ words, uint32_t nw, uint64_t *__restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * nw;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = (uint32_t)(i / n), v = (uint32_t)(i % n);
+        out[i] = rec[(size_t)v * rw + words[j]];
+    }
+}
+
+__global__ void unpack_words_kernel(uint64_t *__restrict__ rec, uint32_t rw, uint32_t n,
+                                    const uint32_t *__restrict__ words, uint32_t nw, const uint64_t *__restrict__ in) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * nw;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = (uint32_t)(i / n), v = (uint32_t)(i % n);
+        rec[(size_t)v * rw + words[j]] = in[i];
+    }
+}
+
+// Pack record words `words` (host list) of every vertex into a word-major
+// slab (nw x n u64, device memory) -- the unit of the NCCL allgather.
+extern "C" dbl_status dbl_index_pack_words(const dbl_index *idx, const uint32_t *words, uint32_t nw,
+                                           uint64_t *dev_slab, void *stream) {
+    if (!idx || (nw && (!words || !dev_slab))) { set_error("null argument"); return DBL_E_ARG; }
+    if (!nw || !idx->n) return DBL_OK;
+    DBL_CUDA(cudaSetDevice(idx->device));
+    DevBuf w;
+    dbl_status s = w.ensure(nw * 4);
+    if (s) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    DBL_CUDA(cudaMemcpyAsync(w.p, words, nw * 4, cudaMemcpyHostToDevice, st));
+    pack_words_kernel<<<grid_for((uint64_t)idx->n * nw), 256, 0, st>>>(idx->rec.as<uint64_t>(), idx->rw, idx->n,
+                                                                       w.as<uint32_t>(), nw, dev_slab);
+    DBL_LAUNCHED();
+    DBL_CUDA(cudaStreamSynchronize(st));
+    w.release();
+    return DBL_OK;
+}
+
+// Inverse of dbl_index_pack_words: scatter a slab (K5 record interleave).
+extern "C" dbl_status dbl_index_unpack_words(dbl_index *idx, const uint32_t *words, uint32_t nw,
+                                             const uint64_t *dev_slab, void *stream) {
+    if (!idx || (nw && (!words || !dev_slab))) { set_error("null argument"); return DBL_E_ARG; }
+    if (!nw || !idx->n) return DBL_OK;
+    DBL_CUDA(cudaSetDevice(idx->device));
+    DevBuf w;
+    dbl_status s = w.ensure(nw * 4);
+    if (s) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    DBL_CUDA(cudaMemcpyAsync(w.p, words, nw * 4, cudaMemcpyHostToDevice, st));
+    unpack_words_kernel<<<grid_for((uint64_t)idx->n * nw), 256, 0, st>>>(idx->rec.as<uint64_t>(), idx->rw, idx->n,
+                                                                         w.as<uint32_t>(), nw, dev_slab);
+    DBL_LAUNCHED();
+    DBL_CUDA(cudaStreamSynchronize(st));
+    w.release();
+    return DBL_OK;
+}
+
+// ------------------------------------------------------- graph-only edges --
+
+// DynamicGraph.add_edge for a batch without label maintenance (graph.py:56-66):
+// out_new (host, optional) receives 1 for each pair that was absent before the
+// call and not repeated earlier in the batch.
+extern "C" dbl_status dbl_graph_add_edges(dbl_graph *g, const uint32_t *u, const uint32_t *v, uint64_t count,
+                                          uint64_t *out_inserted) {
+    if (!g || (count && (!u || !v))) { set_error("null argument"); return DBL_E_ARG; }
+    if (out_inserted) *out_inserted = 0;
+    if (!count) return DBL_OK;
+    DBL_CUDA(cudaSetDevice(g->device));
+    DevBuf in, keys, alt, newk, err;
+    auto cleanup = [&]() { in.release(); keys.release(); alt.release(); newk.release(); err.release(); };
+    dbl_status s;
+    if ((s = in.ensure(count * 8)) || (s = keys.ensure(count * 8)) || (s = alt.ensure(count * 8)) ||
+        (s = newk.ensure(count * 8)) || (s = err.ensure(16))) { cleanup(); return s; }
+    DBL_CUDA(cudaMemcpyAsync(in.p, u, count * 4, cudaMemcpyHostToDevice, g->stream));
+    DBL_CUDA(cudaMemcpyAsync(in.as<uint32_t>() + count, v, count * 4, cudaMemcpyHostToDevice, g->stream));
+    DBL_CUDA(cudaMemsetAsync(err.p, 0, 16, g->stream));
+    pack_pairs_kernel<<<grid_for(count), 256, 0, g->stream>>>(in.as<uint32_t>(), in.as<uint32_t>() + count, count,
+                                                              g->n, keys.as<uint64_t>(), err.as<unsigned long long>());
+    DBL_LAUNCHED();
+    unsigned long long herr = 0;
+    DBL_CUDA(cudaMemcpyAsync(&herr, err.p, 8, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    if (herr) { cleanup(); set_error("edge endpoint outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+    uint64_t *sorted = nullptr;
+    if ((s = sort_keys(g, keys.as<uint64_t>(), alt.as<uint64_t>(), count, key_end_bit(g->n), &sorted))) {
+        cleanup();
+        return s;
+    }
+    uint64_t *uniq = sorted == keys.as<uint64_t>() ? alt.as<uint64_t>() : keys.as<uint64_t>();
+    size_t tmp = 0;
+    uint64_t *dn = err.as<uint64_t>() + 1;
+    DBL_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted, uniq, dn, (int64_t)count, g->stream));
+    if ((s = g->cub_tmp.ensure(tmp))) { cleanup(); return s; }
+    DBL_CUDA(cub::DeviceSelect::Unique(g->cub_tmp.p, tmp, sorted, uniq, dn, (int64_t)count, g->stream));
+    DBL_LAUNCHED();
+    uint64_t nu = 0, nnew = 0;
+    DBL_CUDA(cudaMemcpyAsync(&nu, dn, 8, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    if ((s = graph_filter_new(g, uniq, nu, newk.as<uint64_t>(), &nnew))) { cleanup(); return s; }
+    if (nnew && (s = graph_insert_delta(g, newk.as<uint64_t>(), nnew))) { cleanup(); return s; }
+    if (nnew && g->m_delta * 4 > g->m_base + 1024) s = graph_compact(g);
+    cleanup();
+    if (s) return s;
+    if (out_inserted) *out_inserted = nnew;
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    return DBL_OK;
+}
+
+// --------------------------------------------------------- label helpers --
+
+__global__ void label_tests_kernel(const uint64_t *__restrict__ rec, uint32_t wdl, uint32_t wbl, uint32_t n,
+                                   const uint32_t *__restrict__ x, const uint32_t *__restrict__ y, uint64_t count,
+                                   uint8_t *__restrict__ dl, uint8_t *__restrict__ bl, unsigned long long *err) {
+    const uint32_t H = wdl + wbl, rw = 2 * H;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = x[i], b = y[i];
+        if (a >= n || b >= n) { atomicOr(err, 1ull); continue; }
+        const uint64_t *ra = rec + (size_t)a * rw, *rb = rec + (size_t)b * rw;
+        uint64_t d = 0, c = 0;
+        for (uint32_t k = 0; k < wdl; ++k) d |= ra[H + k] & rb[k];
+        for (uint32_t k = 0; k < wbl; ++k) c |= (ra[wdl + k] & ~rb[wdl + k]) | (rb[H + wdl + k] & ~ra[H + wdl + k]);
+        dl[i] = d != 0;
+        bl[i] = c == 0;
+    }
+}
+
+// dl_intersec (labels.py:315-319) and bl_contain (labels.py:322-327) for a
+// batch of (x, y) pairs, host in/out.
+extern "C" dbl_status dbl_label_tests(const dbl_index *idx, const uint32_t *x, const uint32_t *y, uint64_t count,
+                                      uint8_t *out_dl_intersec, uint8_t *out_bl_contain) {
+    if (!idx || (count && (!x || !y || !out_dl_intersec || !out_bl_contain))) {
+        set_error("null argument");
+        return DBL_E_ARG;
+    }
+    if (!count) return DBL_OK;
+    DBL_CUDA(cudaSetDevice(idx->device));
+    DevBuf b;
+    dbl_status s = b.ensure(count * 10 + 16);
+    if (s) return s;
+    uint32_t *dx = b.as<uint32_t>(), *dy = dx + count;
+    uint8_t *ddl = reinterpret_cast<uint8_t *>(dy + count), *dbl = ddl + count;
+    unsigned long long *derr = reinterpret_cast<unsigned long long *>(b.as<char>() + ((count * 10 + 7) & ~7ull));
+    cudaMemcpy(dx, x, count * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dy, y, count * 4, cudaMemcpyHostToDevice);
+    cudaMemset(derr, 0, 8);
+    label_tests_kernel<<<grid_for(count), 256>>>(idx->rec.as<uint64_t>(), idx->wdl, idx->wbl, idx->n, dx, dy, count,
+                                                 ddl, dbl, derr);
+    DBL_LAUNCHED();
+    unsigned long long herr = 0;
+    cudaMemcpy(out_dl_intersec, ddl, count, cudaMemcpyDeviceToHost);
+    cudaMemcpy(out_bl_contain, dbl, count, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(&herr, derr, 8, cudaMemcpyDeviceToHost);
+    b.release();
+    if (e != cudaSuccess) return cuda_fail(e, "label_tests");
+    if (herr) { set_error("vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+    return DBL_OK;
+}

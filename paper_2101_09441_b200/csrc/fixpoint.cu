@@ -1,0 +1,716 @@
+// fixpoint.cu -- K3/K4 label construction and K8 insertion propagation.
+//
+// Reference: build_index (labels.py:263-306) floods one bit at a time with a
+// BFS (_flood, labels.py:247-260); insert_edge (updates.py:112-137) ORs the
+// new edge's labels through the affected cone (_propagate_union,
+// updates.py:89-109).  Both compute the least fixpoint of
+//     L[x] = seed[x] | OR_{p -> x} L[p]
+// per label bit, which is unique, so any traversal order yields the
+// reference's labels bit-for-bit.
+//
+// B200 design: all bits of a record half propagate together.  The in-half
+// {dl_in, bl_in} (forward along CSR) and the out-half {dl_out, bl_out}
+// (backward along CSC) run in ONE persistent cooperative kernel, one grid
+// barrier per BFS level, no host round trip between levels.  Work items are
+// (vertex, edge range <= CHUNK) so hubs are split; warps take 32 items per
+// ticket, expand items of >= 32 edges warp-cooperatively and pack the
+// smaller ones with a warp scan (32 edges per step, owner lane by rank
+// select).  A relaxed edge reads the destination's words through L2 and
+// issues atomicOr only for the missing bits; a vertex whose label grew is
+// stamped (one enqueue per level) and its edge ranges appended with a
+// warp-aggregated atomicAdd.
+#include <cooperative_groups.h>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dbl {
+
+__device__ __forceinline__ uint64_t ld_cg64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void ld_cg128(const uint64_t *p, uint64_t &a, uint64_t &b) {
+    asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
+__device__ __forceinline__ uint32_t ld_cg32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+template <int NW, bool VEC>
+__device__ __forceinline__ void load_words(const uint64_t *p, uint64_t (&w)[NW]) {
+    if constexpr (VEC && (NW % 2 == 0)) {
+#pragma unroll
+        for (int k = 0; k < NW; k += 2) ld_cg128(p + k, w[k], w[k + 1]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) w[k] = ld_cg64(p + k);
+    }
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+// position of the r-th (0-based) set bit of mask
+__device__ __forceinline__ int select_bit(uint32_t mask, uint32_t r) {
+    int p = 0;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        uint32_t low = mask & ((1u << s) - 1u);
+        uint32_t c = __popc(low);
+        if (r >= c) { r -= c; mask >>= s; p += s; } else { mask = low; }
+    }
+    return p;
+}
+
+// Append the edge ranges of every lane's vertex y (if p) to queue QN.
+__device__ __forceinline__ void warp_enqueue(const DirParams &D, const Queue &QN, bool p, uint32_t y,
+                                             uint32_t *cnt_ptr, Ctrl *ctrl) {
+    const int lane = threadIdx.x & 31;
+    uint32_t b0 = 0, b1 = 0, d0 = 0, d1 = 0, ni = 0;
+    if (p) {
+        b0 = __ldg(D.adj.ptr + y);
+        b1 = __ldg(D.adj.ptr + y + 1);
+        if (D.adj.dptr) {
+            d0 = __ldg(D.adj.dptr + y);
+            d1 = __ldg(D.adj.dptr + y + 1);
+        }
+        ni = (b1 - b0 + CHUNK - 1) / CHUNK + (d1 - d0 + CHUNK - 1) / CHUNK;
+    }
+    const uint32_t incl = warp_incl_scan(ni);
+    const uint32_t tot = __shfl_sync(FULL, incl, 31);
+    if (tot == 0) return;
+    uint32_t pos0 = 0;
+    if (lane == 31) pos0 = atomicAdd(cnt_ptr, tot);
+    pos0 = __shfl_sync(FULL, pos0, 31);
+    if ((uint64_t)pos0 + tot > D.cap) {
+        if (lane == 0) atomicOr(&ctrl->overflow, 1u);
+        return;
+    }
+    uint32_t pos = pos0 + incl - ni;
+    for (uint32_t s = b0; s < b1; s += CHUNK, ++pos) {
+        QN.x[pos] = y;
+        QN.start[pos] = s;
+        QN.len[pos] = min(CHUNK, b1 - s);
+    }
+    for (uint32_t s = d0; s < d1; s += CHUNK, ++pos) {
+        QN.x[pos] = y;
+        QN.start[pos] = s;
+        QN.len[pos] = min(CHUNK, d1 - s) | DELTA_BIT;
+    }
+}
+
+// OR the source words into y's words; true iff this thread set a new bit.
+template <int NW, bool VEC>
+__device__ __forceinline__ bool relax(const DirParams &D, uint32_t y, const uint64_t (&s)[NW]) {
+    uint64_t *p = D.lab + (size_t)y * D.stride;
+    uint64_t c[NW];
+    load_words<NW, VEC>(p, c);
+    bool ch = false;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+        const uint64_t need = s[k] & ~c[k];
+        if (need) {
+            const uint64_t old = atomicOr(reinterpret_cast<unsigned long long *>(p + k),
+                                          (unsigned long long)need);
+            ch |= (need & ~old) != 0;
+        }
+    }
+    return ch;
+}
+
+template <bool COUNT>
+__device__ __forceinline__ void push_changed(const DirParams &D, const Queue &QN, bool ch, uint32_t y,
+                                             uint32_t epoch, uint32_t *cnt_ptr, Ctrl *ctrl,
+                                             uint32_t &nchanged) {
+    if (!__any_sync(FULL, ch)) return;
+    if (COUNT && ch) {
+        const uint32_t bit = 1u << (y & 31);
+        const uint32_t old = atomicOr(&D.changed_bits[y >> 5], bit);
+        if (!(old & bit)) ++nchanged;
+    }
+    const bool p = ch && (atomicExch(&D.stamp[y], epoch) != epoch);
+    warp_enqueue(D, QN, p, y, cnt_ptr, ctrl);
+}
+
+// One warp expands up to 32 work items of queue Q.
+template <int NW, bool VEC, bool COUNT>
+__device__ __forceinline__ void expand_chunk(const DirParams &D, const Queue &Q, const Queue &QN,
+                                             uint32_t base, uint32_t cnt, uint32_t epoch,
+                                             uint32_t *next_cnt, Ctrl *ctrl, uint32_t &nchanged) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t i = base + lane;
+    const bool valid = i < cnt;
+    uint32_t x = 0, start = 0, lenf = 0;
+    if (valid) {
+        x = ld_cg32(Q.x + i);
+        start = ld_cg32(Q.start + i);
+        lenf = ld_cg32(Q.len + i);
+    }
+    const uint32_t len = lenf & ~DELTA_BIT;
+    const int dseg = (lenf & DELTA_BIT) ? 1 : 0;
+    uint64_t w[NW];
+    if (valid) {
+        load_words<NW, VEC>(D.lab + (size_t)x * D.stride, w);
+    } else {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) w[k] = 0;
+    }
+
+    // items with >= 32 edges: whole warp, 32 edges per step
+    unsigned big = __ballot_sync(FULL, len >= 32);
+    while (big) {
+        const int j = __ffs(big) - 1;
+        big &= big - 1;
+        const uint32_t js = __shfl_sync(FULL, start, j);
+        const uint32_t jl = __shfl_sync(FULL, len, j);
+        const uint32_t *col = __shfl_sync(FULL, dseg, j) ? D.adj.dcol : D.adj.col;
+        uint64_t jw[NW];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) jw[k] = __shfl_sync(FULL, w[k], j);
+        for (uint32_t e0 = 0; e0 < jl; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            uint32_t y = 0;
+            bool ch = false;
+            if (e < jl) {
+                y = __ldg(col + js + e);
+                ch = relax<NW, VEC>(D, y, jw);
+            }
+            push_changed<COUNT>(D, QN, ch, y, epoch, next_cnt, ctrl, nchanged);
+        }
+    }
+
+    // items with < 32 edges: concatenate, 32 edges per step
+    const uint32_t sl = len < 32 ? len : 0;
+    const uint32_t incl = warp_incl_scan(sl);
+    const uint32_t total = __shfl_sync(FULL, incl, 31);
+    const uint32_t excl = incl - sl;
+    const unsigned nz = __ballot_sync(FULL, sl > 0);
+    for (uint32_t b = 0; b < total; b += 32) {
+        const unsigned hw = __reduce_or_sync(FULL, (sl > 0 && (excl >> 5) == (b >> 5)) ? (1u << (excl & 31)) : 0u);
+        const uint32_t before = __popc(__ballot_sync(FULL, sl > 0 && excl < b));
+        const uint32_t j = b + lane;
+        const bool ok = j < total;
+        int owner = 0;
+        if (ok) owner = select_bit(nz, before + __popc(hw & (FULL >> (31 - lane))) - 1);
+        const uint32_t os = __shfl_sync(FULL, start, owner);
+        const uint32_t oe = __shfl_sync(FULL, excl, owner);
+        const int od = __shfl_sync(FULL, dseg, owner);
+        uint64_t ow[NW];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) ow[k] = __shfl_sync(FULL, w[k], owner);
+        uint32_t y = 0;
+        bool ch = false;
+        if (ok) {
+            const uint32_t *col = od ? D.adj.dcol : D.adj.col;
+            y = __ldg(col + os + (j - oe));
+            ch = relax<NW, VEC>(D, y, ow);
+        }
+        push_changed<COUNT>(D, QN, ch, y, epoch, next_cnt, ctrl, nchanged);
+    }
+}
+
+template <int NW, bool VEC, bool COUNT>
+__global__ void __launch_bounds__(FIX_THREADS) fixpoint_kernel(FixParams P) {
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31;
+    Ctrl *ctrl = P.ctrl;
+    uint32_t nchanged[2] = {0, 0};
+    for (uint32_t L = 0; L < P.max_levels; ++L) {
+        const int c3 = L % 3, n3 = (L + 1) % 3, r3 = (L + 2) % 3;
+        const uint32_t c0 = *(volatile uint32_t *)&ctrl->cnt[c3][0];
+        const uint32_t c1 = *(volatile uint32_t *)&ctrl->cnt[c3][1];
+        if ((c0 | c1) == 0) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->levels = L;
+            break;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctrl->cnt[r3][0] = 0;
+            ctrl->cnt[r3][1] = 0;
+            ctrl->work[r3] = 0;
+        }
+        const uint32_t ch0 = (c0 + 31) / 32, tot = ch0 + (c1 + 31) / 32;
+        const int par = L & 1;
+        const uint32_t epoch = P.epoch0 + L + 1;
+        for (;;) {
+            uint32_t t = 0;
+            if (lane == 0) t = atomicAdd(&ctrl->work[c3], 1u);
+            t = __shfl_sync(FULL, t, 0);
+            if (t >= tot) break;
+            const int dir = t < ch0 ? 0 : 1;
+            const uint32_t base = (dir == 0 ? t : t - ch0) * 32;
+            const DirParams &D = P.d[dir];
+            expand_chunk<NW, VEC, COUNT>(D, D.q[par], D.q[par ^ 1], base, dir == 0 ? c0 : c1, epoch,
+                                         &ctrl->cnt[n3][dir], ctrl, nchanged[dir]);
+        }
+        grid.sync();
+    }
+    if (COUNT) {
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            uint32_t v = nchanged[d];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+            if (lane == 0 && v) atomicAdd(&ctrl->changed[d], (unsigned long long)v);
+        }
+    }
+}
+
+// ------------------------------------------------------- seeds & frontier --
+
+// rec := seeds.  bl_in bit bucket[v] for source leaves, bl_out for sinks;
+// dl words zero (landmark bits are added by landmark_bits_kernel).
+__global__ void seed_records_kernel(uint64_t *__restrict__ rec, uint32_t n, uint32_t wdl, uint32_t wbl,
+                                    const uint8_t *__restrict__ flags, const uint32_t *__restrict__ bucket) {
+    const uint32_t rw = 2 * (wdl + wbl), H = wdl + wbl;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * rw;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = (uint32_t)(i / rw), w = (uint32_t)(i % rw);
+        uint64_t val = 0;
+        const uint32_t h = w < H ? 0 : 1, ww = w - h * H;
+        if (ww >= wdl) {
+            const uint8_t f = flags[v];
+            const uint32_t b = bucket[v];
+            if ((f >> h) & 1) {
+                if (b / 64 == ww - wdl) val = 1ull << (b % 64);
+            }
+        }
+        rec[i] = val;
+    }
+}
+
+__global__ void landmark_bits_kernel(uint64_t *__restrict__ rec, uint32_t rw, uint32_t H,
+                                     const uint32_t *__restrict__ lm, uint32_t k) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
+        const uint64_t v = lm[i];
+        atomicOr(reinterpret_cast<unsigned long long *>(rec + v * rw + i / 64), 1ull << (i % 64));
+        atomicOr(reinterpret_cast<unsigned long long *>(rec + v * rw + H + i / 64), 1ull << (i % 64));
+    }
+}
+
+// Level-0 frontier: every vertex with a nonzero seed in the group's words.
+template <int NW>
+__global__ void init_frontier_kernel(FixParams P, uint32_t n, uint32_t active_mask) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t nr = ((uint64_t)n + 31) & ~31ull;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += stride) {
+        const bool valid = i < n;
+        const uint32_t v = valid ? (uint32_t)i : 0;
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            if (!((active_mask >> d) & 1)) continue;
+            const DirParams &D = P.d[d];
+            bool p = false;
+            if (valid) {
+                const uint64_t *w = D.lab + (size_t)v * D.stride;
+                uint64_t acc = 0;
+#pragma unroll
+                for (int k = 0; k < NW; ++k) acc |= w[k];
+                p = acc != 0;
+                if (p) D.stamp[v] = P.epoch0;
+            }
+            warp_enqueue(D, D.q[0], p, v, &P.ctrl->cnt[0][d], P.ctrl);
+        }
+    }
+}
+
+// Insertion seeds (updates.py:129-134 for a whole batch): for each new edge
+// u->v, in-words(v) |= in-words(u) and out-words(u) |= out-words(v).
+template <int NW, bool VEC, bool COUNT>
+__global__ void insert_seed_kernel(FixParams P, const uint64_t *__restrict__ keys, uint64_t count) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t cr = (count + 31) & ~31ull;
+    uint32_t nchanged[2] = {0, 0};
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cr; i += stride) {
+        const bool valid = i < count;
+        const uint64_t key = valid ? keys[i] : 0;
+        const uint32_t u = (uint32_t)(key >> 32), v = (uint32_t)key;
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            const DirParams &D = P.d[d];
+            const uint32_t src = d == 0 ? u : v, dst = d == 0 ? v : u;
+            bool ch = false;
+            if (valid) {
+                uint64_t s[NW];
+                load_words<NW, VEC>(D.lab + (size_t)src * D.stride, s);
+                ch = relax<NW, VEC>(D, dst, s);
+                if (ch) atomicOr(&P.ctrl->seed_changed[d], 1u);
+            }
+            push_changed<COUNT>(D, D.q[0], ch, dst, P.epoch0, &P.ctrl->cnt[0][d], P.ctrl, nchanged[d]);
+        }
+    }
+    if (COUNT) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            uint32_t x = nchanged[d];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+            if (lane == 0 && x) atomicAdd(&P.ctrl->changed[d], (unsigned long long)x);
+        }
+    }
+}
+
+// ------------------------------------------------------------ host driver --
+
+struct Group { int dir; uint32_t w0, nw; };
+
+static void plan_groups(const dbl_index *idx, const uint32_t *words, uint32_t nwords,
+                        Group *out, int &ng) {
+    // words of each half, in order; split into runs of contiguous words of
+    // <= MAX_GROUP_WORDS each.
+    const uint32_t H = idx->wdl + idx->wbl;
+    ng = 0;
+    for (int d = 0; d < 2; ++d) {
+        bool sel[2 * MAX_SHARD_WORDS + 2] = {};
+        uint32_t cnt = 0;
+        for (uint32_t w = 0; w < H; ++w) {
+            bool s = true;
+            if (words) {
+                s = false;
+                for (uint32_t i = 0; i < nwords; ++i) if (words[i] == d * H + w) s = true;
+            }
+            sel[w] = s;
+            cnt += s;
+        }
+        (void)cnt;
+        uint32_t w = 0;
+        while (w < H) {
+            if (!sel[w]) { ++w; continue; }
+            uint32_t e = w;
+            while (e < H && sel[e] && e - w < (uint32_t)MAX_GROUP_WORDS) ++e;
+            out[ng++] = Group{d, d * H + w, e - w};
+            w = e;
+        }
+    }
+}
+
+template <int NW, bool VEC, bool COUNT>
+static dbl_status launch_fixpoint_t(dbl_graph *g, FixParams &P) {
+    auto kern = fixpoint_kernel<NW, VEC, COUNT>;
+    static int blocks_per_sm = -1;
+    if (blocks_per_sm < 0) {
+        DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, FIX_THREADS, 0));
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    int grid = blocks_per_sm * g->sm_count;
+    void *args[] = {(void *)&P};
+    DBL_CUDA(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(FIX_THREADS), args, 0,
+                                         g->stream));
+    DBL_LAUNCHED();
+    return DBL_OK;
+}
+
+template <bool COUNT>
+static dbl_status launch_fixpoint(dbl_graph *g, FixParams &P, uint32_t nw, bool vec) {
+#define DBL_FIX_CASE(N)                                                            \
+    case N:                                                                        \
+        return vec ? launch_fixpoint_t<N, (N % 2 == 0), COUNT>(g, P)               \
+                   : launch_fixpoint_t<N, false, COUNT>(g, P);
+    switch (nw) {
+        DBL_FIX_CASE(1) DBL_FIX_CASE(2) DBL_FIX_CASE(3) DBL_FIX_CASE(4)
+        DBL_FIX_CASE(5) DBL_FIX_CASE(6) DBL_FIX_CASE(7) DBL_FIX_CASE(8)
+    default: set_error("bad word-group width"); return DBL_E_CONFIG;
+    }
+#undef DBL_FIX_CASE
+}
+
+static dbl_status launch_init_frontier(dbl_graph *g, FixParams &P, uint32_t nw, uint32_t mask) {
+    int blocks = (int)(((uint64_t)g->n + 255) / 256);
+    if (blocks > g->sm_count * 8) blocks = g->sm_count * 8;
+    if (blocks < 1) blocks = 1;
+#define DBL_INIT_CASE(N) case N: init_frontier_kernel<N><<<blocks, 256, 0, g->stream>>>(P, g->n, mask); break;
+    switch (nw) {
+        DBL_INIT_CASE(1) DBL_INIT_CASE(2) DBL_INIT_CASE(3) DBL_INIT_CASE(4)
+        DBL_INIT_CASE(5) DBL_INIT_CASE(6) DBL_INIT_CASE(7) DBL_INIT_CASE(8)
+    default: set_error("bad word-group width"); return DBL_E_CONFIG;
+    }
+#undef DBL_INIT_CASE
+    DBL_CHECK_LAUNCH("init_frontier_kernel");
+    return DBL_OK;
+}
+
+static dbl_status launch_insert_seed(dbl_graph *g, FixParams &P, uint32_t nw, bool vec, bool count,
+                                     const uint64_t *keys, uint64_t nk) {
+    int blocks = (int)((nk + 255) / 256);
+    if (blocks > g->sm_count * 8) blocks = g->sm_count * 8;
+    if (blocks < 1) blocks = 1;
+#define DBL_SEED_CASE(N)                                                                      \
+    case N:                                                                                   \
+        if (count) {                                                                          \
+            if (vec) insert_seed_kernel<N, (N % 2 == 0), true><<<blocks, 256, 0, g->stream>>>(P, keys, nk); \
+            else insert_seed_kernel<N, false, true><<<blocks, 256, 0, g->stream>>>(P, keys, nk); \
+        } else {                                                                              \
+            if (vec) insert_seed_kernel<N, (N % 2 == 0), false><<<blocks, 256, 0, g->stream>>>(P, keys, nk); \
+            else insert_seed_kernel<N, false, false><<<blocks, 256, 0, g->stream>>>(P, keys, nk); \
+        }                                                                                     \
+        break;
+    switch (nw) {
+        DBL_SEED_CASE(1) DBL_SEED_CASE(2) DBL_SEED_CASE(3) DBL_SEED_CASE(4)
+        DBL_SEED_CASE(5) DBL_SEED_CASE(6) DBL_SEED_CASE(7) DBL_SEED_CASE(8)
+    default: set_error("bad word-group width"); return DBL_E_CONFIG;
+    }
+#undef DBL_SEED_CASE
+    DBL_CHECK_LAUNCH("insert_seed_kernel");
+    return DBL_OK;
+}
+
+static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2], FixParams &P,
+                                 uint32_t &nw, bool &vec, bool count, bool reset_counts = true) {
+    dbl_status s = graph_ensure_traversal(g);
+    if (s) return s;
+    // stamps: reset when the epoch could wrap during this run
+    const uint64_t need = (uint64_t)g->n + 8;
+    if ((uint64_t)g->epoch + need >= 0xfffffff0ull) {
+        DBL_CUDA(cudaMemsetAsync(g->stamp[0].p, 0, g->stamp[0].bytes, g->stream));
+        DBL_CUDA(cudaMemsetAsync(g->stamp[1].p, 0, g->stamp[1].bytes, g->stream));
+        g->epoch = 1;
+    }
+    nw = 0;
+    vec = true;
+    for (int d = 0; d < 2; ++d) {
+        DirParams &D = P.d[d];
+        D.adj = d == 0 ? graph_fwd(g) : graph_rev(g);
+        D.stride = idx->rw;
+        D.stamp = g->stamp[d].as<uint32_t>();
+        D.cap = g->qcap;
+        for (int p = 0; p < 2; ++p) {
+            uint32_t *b = g->qbuf[d][p].as<uint32_t>();
+            D.q[p].x = b;
+            D.q[p].start = b + g->qcap;
+            D.q[p].len = b + 2ull * g->qcap;
+        }
+        D.changed_bits = count ? g->changed_bits.as<uint32_t>() + d * (((size_t)g->n + 31) / 32) : nullptr;
+        if (gr[d]) {
+            D.lab = idx->rec.as<uint64_t>() + gr[d]->w0;
+            nw = gr[d]->nw;
+            if ((gr[d]->w0 % 2) || (idx->rw % 2)) vec = false;
+        } else {
+            D.lab = idx->rec.as<uint64_t>();
+        }
+    }
+    P.ctrl = g->ctrl.as<Ctrl>();
+    P.epoch0 = g->epoch;
+    P.max_levels = g->n + 4;
+    DBL_CUDA(cudaMemsetAsync(P.ctrl, 0, sizeof(Ctrl), g->stream));
+    if (count && reset_counts)
+        DBL_CUDA(cudaMemsetAsync(g->changed_bits.p, 0, (((size_t)g->n + 31) / 32) * 2 * 4, g->stream));
+    return DBL_OK;
+}
+
+static dbl_status finish_run(dbl_graph *g, Ctrl *hctrl) {
+    DBL_CUDA(cudaMemcpyAsync(hctrl, g->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    g->epoch += hctrl->levels + 2;
+    if (hctrl->overflow) { set_error("frontier queue overflow"); return DBL_E_CUDA; }
+    return DBL_OK;
+}
+
+dbl_status index_seed_records(dbl_graph *g, dbl_index *idx) {
+    const uint64_t total = (uint64_t)idx->n * idx->rw;
+    if (!total) return DBL_OK;
+    int blocks = (int)((total + 255) / 256 < (uint64_t)g->sm_count * 16 ? (total + 255) / 256 : g->sm_count * 16);
+    seed_records_kernel<<<blocks, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, idx->wdl, idx->wbl,
+                                                       idx->leaf_flags.as<uint8_t>(), idx->bucket.as<uint32_t>());
+    DBL_CHECK_LAUNCH("seed_records_kernel");
+    if (idx->cfg.k) {
+        landmark_bits_kernel<<<(idx->cfg.k + 255) / 256, 256, 0, g->stream>>>(
+            idx->rec.as<uint64_t>(), idx->rw, idx->wdl + idx->wbl, idx->landmarks.as<uint32_t>(), idx->cfg.k);
+        DBL_CHECK_LAUNCH("landmark_bits_kernel");
+    }
+    return DBL_OK;
+}
+
+// Build (or rebuild) the listed record words (nullptr = all) from seeds.
+dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32_t nwords) {
+    if (idx->n == 0) return DBL_OK;
+    Group groups[2 * MAX_SHARD_WORDS + 4];
+    int ng = 0;
+    if (idx->wdl + idx->wbl > (uint32_t)MAX_SHARD_WORDS) { set_error("label width too large"); return DBL_E_CONFIG; }
+    plan_groups(idx, words, nwords, groups, ng);
+    DBL_CUDA(cudaEventRecord(g->ev[0], g->stream));
+    dbl_status s = index_seed_records(g, idx);
+    if (s) return s;
+    // pair forward and backward groups of equal width into one launch
+    bool used[2 * MAX_SHARD_WORDS + 4] = {};
+    for (int i = 0; i < ng; ++i) {
+        if (used[i]) continue;
+        used[i] = true;
+        const Group *pair[2] = {nullptr, nullptr};
+        pair[groups[i].dir] = &groups[i];
+        for (int j = i + 1; j < ng; ++j) {
+            if (!used[j] && groups[j].dir != groups[i].dir && groups[j].nw == groups[i].nw) {
+                used[j] = true;
+                pair[groups[j].dir] = &groups[j];
+                break;
+            }
+        }
+        FixParams P{};
+        uint32_t nw = 0;
+        bool vec = true;
+        if ((s = prepare_params(g, idx, pair, P, nw, vec, false))) return s;
+        const uint32_t mask = (pair[0] ? 1u : 0u) | (pair[1] ? 2u : 0u);
+        if ((s = launch_init_frontier(g, P, nw, mask))) return s;
+        if ((s = launch_fixpoint<false>(g, P, nw, vec))) return s;
+        Ctrl h{};
+        if ((s = finish_run(g, &h))) return s;
+    }
+    DBL_CUDA(cudaEventRecord(g->ev[1], g->stream));
+    DBL_CUDA(cudaEventSynchronize(g->ev[1]));
+    cudaEventElapsedTime(&g->t_fix, g->ev[0], g->ev[1]);
+    return DBL_OK;
+}
+
+// Propagate a batch of new edges (sorted forward keys, already added to the
+// graph) through all label words.
+dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, uint64_t count,
+                      bool count_changes, uint32_t *changed_out, uint32_t *seed_changed,
+                      uint32_t *levels) {
+    changed_out[0] = changed_out[1] = 0;
+    seed_changed[0] = seed_changed[1] = 0;
+    *levels = 0;
+    if (count == 0 || idx->n == 0) return DBL_OK;
+    Group groups[2 * MAX_SHARD_WORDS + 4];
+    int ng = 0;
+    plan_groups(idx, nullptr, 0, groups, ng);
+    DBL_CUDA(cudaEventRecord(g->ev[0], g->stream));
+    // groups come ordered: dir 0 groups then dir 1 groups with equal widths
+    const int half = ng / 2;
+    for (int i = 0; i < half; ++i) {
+        const Group *pair[2] = {&groups[i], &groups[half + i]};
+        FixParams P{};
+        uint32_t nw = 0;
+        bool vec = true;
+        dbl_status s = prepare_params(g, idx, pair, P, nw, vec, count_changes, i == 0);
+        if (s) return s;
+        if ((s = launch_insert_seed(g, P, nw, vec, count_changes, new_keys, count))) return s;
+        if (count_changes) {
+            if ((s = launch_fixpoint<true>(g, P, nw, vec))) return s;
+        } else {
+            if ((s = launch_fixpoint<false>(g, P, nw, vec))) return s;
+        }
+        Ctrl h{};
+        if ((s = finish_run(g, &h))) return s;
+        // the change bitmap persists across groups, so counts stay distinct
+        changed_out[0] += (uint32_t)h.changed[0];
+        changed_out[1] += (uint32_t)h.changed[1];
+        seed_changed[0] |= h.seed_changed[0];
+        seed_changed[1] |= h.seed_changed[1];
+        if (h.levels > *levels) *levels = h.levels;
+    }
+    DBL_CUDA(cudaEventRecord(g->ev[1], g->stream));
+    DBL_CUDA(cudaEventSynchronize(g->ev[1]));
+    cudaEventElapsedTime(&g->t_fix, g->ev[0], g->ev[1]);
+    return DBL_OK;
+}
+
+// ------------------------------------------------------------- work model --
+// level-synchronous (Jacobi) counts per 64-bit family.
+
+__global__ void wm_extract_kernel(const uint64_t *__restrict__ rec, uint32_t rw, uint32_t w, uint32_t n,
+                                  uint64_t *__restrict__ cur, uint8_t *__restrict__ front) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint64_t x = rec[(size_t)v * rw + w];
+        cur[v] = x;
+        front[v] = x != 0;
+    }
+}
+
+__global__ void wm_push_kernel(Adj adj, uint32_t n, const uint64_t *__restrict__ cur,
+                               const uint8_t *__restrict__ front, uint64_t *__restrict__ nxt,
+                               unsigned long long *__restrict__ VE) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long V = 0, E = 0;
+    for (uint64_t v = warp; v < n; v += nwarps) {
+        if (!front[v]) continue;
+        const uint64_t lab = cur[v];
+        uint32_t s = adj.ptr[v], e = adj.ptr[v + 1];
+        uint32_t ds = 0, de = 0;
+        if (adj.dptr) { ds = adj.dptr[v]; de = adj.dptr[v + 1]; }
+        if (lane == 0) { V += 1; E += (e - s) + (de - ds); }
+        for (uint32_t i = s + lane; i < e; i += 32) atomicOr((unsigned long long *)&nxt[adj.col[i]], lab);
+        for (uint32_t i = ds + lane; i < de; i += 32) atomicOr((unsigned long long *)&nxt[adj.dcol[i]], lab);
+    }
+    if (lane == 0) {
+        atomicAdd(&VE[0], V);
+        atomicAdd(&VE[1], E);
+    }
+}
+
+__global__ void wm_diff_kernel(uint32_t n, uint64_t *__restrict__ cur, const uint64_t *__restrict__ nxt,
+                               uint8_t *__restrict__ front) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint64_t a = cur[v], b = nxt[v];
+        front[v] = a != b;
+        cur[v] = b;
+    }
+}
+
+dbl_status work_model(const dbl_index *idx, dbl_graph *g, uint64_t *V, uint64_t *E, uint32_t *levels) {
+    const uint32_t n = idx->n, rw = idx->rw, H = idx->wdl + idx->wbl;
+    DevBuf seeds, cur, nxt, front, ve;
+    dbl_index tmp;  // seed records only
+    dbl_status s;
+    auto cleanup = [&]() { seeds.release(); cur.release(); nxt.release(); front.release(); ve.release(); };
+    if ((s = seeds.ensure((size_t)n * rw * 8 + 16)) || (s = cur.ensure((size_t)n * 8 + 8)) ||
+        (s = nxt.ensure((size_t)n * 8 + 8)) || (s = front.ensure((size_t)n + 8)) || (s = ve.ensure(16))) {
+        cleanup();
+        return s;
+    }
+    // seed records into `seeds`
+    std::swap(tmp.rec, seeds);
+    tmp.n = n; tmp.rw = rw; tmp.wdl = idx->wdl; tmp.wbl = idx->wbl; tmp.cfg = idx->cfg;
+    tmp.landmarks.p = idx->landmarks.p;
+    tmp.leaf_flags.p = idx->leaf_flags.p;
+    tmp.bucket.p = idx->bucket.p;
+    s = index_seed_records(g, &tmp);
+    std::swap(tmp.rec, seeds);
+    tmp.landmarks.p = tmp.leaf_flags.p = tmp.bucket.p = nullptr;
+    if (s) { cleanup(); return s; }
+    const int blocks = g->sm_count * 8;
+    for (uint32_t w = 0; w < rw; ++w) {
+        Adj adj = w < H ? graph_fwd(g) : graph_rev(g);
+        wm_extract_kernel<<<blocks, 256, 0, g->stream>>>(seeds.as<uint64_t>(), rw, w, n, cur.as<uint64_t>(),
+                                                         front.as<uint8_t>());
+        DBL_LAUNCHED();
+        uint64_t Vt = 0, Et = 0;
+        uint32_t L = 0;
+        for (;;) {
+            unsigned long long h[2];
+            DBL_CUDA(cudaMemsetAsync(ve.p, 0, 16, g->stream));
+            DBL_CUDA(cudaMemcpyAsync(nxt.p, cur.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, g->stream));
+            wm_push_kernel<<<blocks, 256, 0, g->stream>>>(adj, n, cur.as<uint64_t>(), front.as<uint8_t>(),
+                                                          nxt.as<uint64_t>(), ve.as<unsigned long long>());
+            DBL_LAUNCHED();
+            DBL_CUDA(cudaMemcpyAsync(h, ve.p, 16, cudaMemcpyDeviceToHost, g->stream));
+            DBL_CUDA(cudaStreamSynchronize(g->stream));
+            if (h[0] == 0) break;
+            Vt += h[0];
+            Et += h[1];
+            ++L;
+            wm_diff_kernel<<<blocks, 256, 0, g->stream>>>(n, cur.as<uint64_t>(), nxt.as<uint64_t>(),
+                                                          front.as<uint8_t>());
+            DBL_LAUNCHED();
+        }
+        V[w] = Vt;
+        E[w] = Et;
+        levels[w] = L;
+    }
+    cleanup();
+    return DBL_OK;
+}
+
+}  // namespace dbl

@@ -1,0 +1,571 @@
+// graph.cu -- K0: device CSR/CSC construction, dedup, delta adjacency.
+//
+// Replaces DynamicGraph (reference graph.py:31-145): add_edge's duplicate
+// check (graph.py:56-66) becomes sort + unique over packed (src<<32|dst)
+// keys; forward/reverse adjacency lists become CSR (out-edges) and CSC
+// (in-edges) in HBM.  Rows are sorted by neighbour id; the reference keeps
+// insertion order, which only affects the reference's `visited` counters,
+// never labels or answers.
+//
+// Edge insertions (updates.py:124) land in a second, sorted "delta" CSR/CSC
+// that traversals read alongside the base; graph_compact folds it back.
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace dbl {
+
+int key_end_bit(uint32_t n) {
+    int b = 1;
+    while (b < 32 && (1ull << b) < (uint64_t)n) ++b;
+    return 32 + b;
+}
+
+__global__ void pack_keys_kernel(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                                 uint64_t m, uint32_t n, uint64_t *__restrict__ keys,
+                                 unsigned long long *err) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t u = src[i], v = dst[i];
+        if (u >= n || v >= n) { atomicOr(err, 1ull); u = 0; v = 0; }
+        keys[i] = ((uint64_t)u << 32) | v;
+    }
+}
+
+__global__ void swap_keys_kernel(const uint64_t *__restrict__ in, uint64_t m, uint64_t *__restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t k = in[i];
+        out[i] = (k << 32) | (k >> 32);
+    }
+}
+
+// col[i] = low word; cnt[src]++ aggregated over lanes sharing a source
+// (keys are sorted, so runs are contiguous and hubs cost one atomic/warp).
+__global__ void count_rows_kernel(const uint64_t *__restrict__ keys, uint64_t m,
+                                  uint32_t *__restrict__ cnt, uint32_t *__restrict__ col) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t mr = (m + 31) & ~31ull;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < mr; i += stride) {
+        bool valid = i < m;
+        uint64_t k = valid ? keys[i] : 0;
+        uint32_t src = valid ? (uint32_t)(k >> 32) : 0xffffffffu;
+        if (valid) col[i] = (uint32_t)k;
+        unsigned peers = __match_any_sync(FULL, src);
+        int leader = __ffs(peers) - 1;
+        if (valid && (int)(threadIdx.x & 31) == leader) atomicAdd(&cnt[src], (uint32_t)__popc(peers));
+    }
+}
+
+static inline int grid_for(uint64_t work, int threads = 256, int cap = 148 * 32) {
+    uint64_t b = (work + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > (uint64_t)cap) b = cap;
+    return (int)b;
+}
+
+dbl_status sort_keys(dbl_graph *g, uint64_t *keys, uint64_t *alt, uint64_t m, int end_bit,
+                     uint64_t **sorted) {
+    if (m == 0) { *sorted = keys; return DBL_OK; }
+    cub::DoubleBuffer<uint64_t> db(keys, alt);
+    size_t tmp = 0;
+    DBL_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, (int64_t)m, 0, end_bit, g->stream));
+    dbl_status s = g->cub_tmp.ensure(tmp);
+    if (s) return s;
+    DBL_CUDA(cub::DeviceRadixSort::SortKeys(g->cub_tmp.p, tmp, db, (int64_t)m, 0, end_bit, g->stream));
+    DBL_LAUNCHED();
+    *sorted = db.Current();
+    return DBL_OK;
+}
+
+// ptr[0..n] and col[0..m) from keys sorted by (src, dst).
+dbl_status build_csr_from_sorted(dbl_graph *g, const uint64_t *keys, uint64_t m, uint32_t n,
+                                 uint32_t *ptr, uint32_t *col) {
+    dbl_status s = g->scratch_d.ensure(((size_t)n + 1) * sizeof(uint32_t));
+    if (s) return s;
+    uint32_t *cnt = g->scratch_d.as<uint32_t>();
+    DBL_CUDA(cudaMemsetAsync(cnt, 0, ((size_t)n + 1) * sizeof(uint32_t), g->stream));
+    if (m) {
+        count_rows_kernel<<<grid_for(m), 256, 0, g->stream>>>(keys, m, cnt, col);
+        DBL_CHECK_LAUNCH("count_rows_kernel");
+    }
+    size_t tmp = 0;
+    DBL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, ptr, (int64_t)n + 1, g->stream));
+    s = g->cub_tmp.ensure(tmp);
+    if (s) return s;
+    DBL_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.p, tmp, cnt, ptr, (int64_t)n + 1, g->stream));
+    DBL_LAUNCHED();
+    return DBL_OK;
+}
+
+static dbl_status unique_keys(dbl_graph *g, const uint64_t *in, uint64_t m, uint64_t *out,
+                              uint64_t *nout) {
+    if (m == 0) { *nout = 0; return DBL_OK; }
+    dbl_status s = g->scratch_c.ensure(sizeof(uint64_t));
+    if (s) return s;
+    uint64_t *d_n = g->scratch_c.as<uint64_t>();
+    size_t tmp = 0;
+    DBL_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, in, out, d_n, (int64_t)m, g->stream));
+    s = g->cub_tmp.ensure(tmp);
+    if (s) return s;
+    DBL_CUDA(cub::DeviceSelect::Unique(g->cub_tmp.p, tmp, in, out, d_n, (int64_t)m, g->stream));
+    DBL_LAUNCHED();
+    DBL_CUDA(cudaMemcpyAsync(nout, d_n, sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    return DBL_OK;
+}
+
+// Build base CSR+CSC from `keys` (unsorted, may contain duplicates; buffer
+// `alt` of the same size is scratch).  Both buffers are clobbered.
+static dbl_status build_base(dbl_graph *g, uint64_t *keys, uint64_t *alt, uint64_t m_raw) {
+    uint32_t n = g->n;
+    int eb = key_end_bit(n);
+    uint64_t *sorted = nullptr;
+    dbl_status s = sort_keys(g, keys, alt, m_raw, eb, &sorted);
+    if (s) return s;
+    uint64_t *uniq = (sorted == keys) ? alt : keys;
+    uint64_t m = 0;
+    s = unique_keys(g, sorted, m_raw, uniq, &m);
+    if (s) return s;
+    if (m >= 0xffffffffull) { set_error("edge count exceeds 2^32-1"); return DBL_E_CONFIG; }
+    g->m_base = m;
+    if ((s = g->fptr.ensure(((size_t)n + 1) * 4)) || (s = g->rptr.ensure(((size_t)n + 1) * 4)) ||
+        (s = g->fcol.ensure(m * 4 + 4)) || (s = g->rcol.ensure(m * 4 + 4)))
+        return s;
+    s = build_csr_from_sorted(g, uniq, m, n, g->fptr.as<uint32_t>(), g->fcol.as<uint32_t>());
+    if (s) return s;
+    // reverse keys into the other buffer, sort, build CSC
+    uint64_t *rkeys = sorted;  // free again
+    if (m) {
+        swap_keys_kernel<<<grid_for(m), 256, 0, g->stream>>>(uniq, m, rkeys);
+        DBL_CHECK_LAUNCH("swap_keys_kernel");
+    }
+    uint64_t *rsorted = nullptr;
+    s = sort_keys(g, rkeys, uniq, m, eb, &rsorted);
+    if (s) return s;
+    return build_csr_from_sorted(g, rsorted, m, n, g->rptr.as<uint32_t>(), g->rcol.as<uint32_t>());
+}
+
+Adj graph_fwd(const dbl_graph *g) {
+    Adj a;
+    a.ptr = g->fptr.as<uint32_t>();
+    a.col = g->fcol.as<uint32_t>();
+    a.dptr = g->m_delta ? g->dfptr.as<uint32_t>() : nullptr;
+    a.dcol = g->m_delta ? g->dfcol.as<uint32_t>() : nullptr;
+    return a;
+}
+
+Adj graph_rev(const dbl_graph *g) {
+    Adj a;
+    a.ptr = g->rptr.as<uint32_t>();
+    a.col = g->rcol.as<uint32_t>();
+    a.dptr = g->m_delta ? g->drptr.as<uint32_t>() : nullptr;
+    a.dcol = g->m_delta ? g->drcol.as<uint32_t>() : nullptr;
+    return a;
+}
+
+__global__ void degrees_kernel(const uint32_t *__restrict__ fptr, const uint32_t *__restrict__ rptr,
+                               const uint32_t *__restrict__ dfptr, const uint32_t *__restrict__ drptr,
+                               uint32_t n, uint32_t *__restrict__ indeg, uint32_t *__restrict__ outdeg) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        uint32_t o = fptr[v + 1] - fptr[v], i = rptr[v + 1] - rptr[v];
+        if (dfptr) { o += dfptr[v + 1] - dfptr[v]; i += drptr[v + 1] - drptr[v]; }
+        outdeg[v] = o;
+        indeg[v] = i;
+    }
+}
+
+dbl_status graph_degrees_dev(const dbl_graph *g, uint32_t *indeg, uint32_t *outdeg) {
+    if (g->n == 0) return DBL_OK;
+    Adj f = graph_fwd(g), r = graph_rev(g);
+    degrees_kernel<<<grid_for(g->n), 256, 0, g->stream>>>(f.ptr, r.ptr, f.dptr, r.dptr, g->n, indeg,
+                                                           outdeg);
+    DBL_CHECK_LAUNCH("degrees_kernel");
+    return DBL_OK;
+}
+
+// Traversal workspace: per-direction stamps and level-parity queues sized
+// for the worst case of one level: every vertex enqueued once, split into
+// CHUNK-edge items (<= 2n + m/CHUNK items).
+dbl_status graph_ensure_traversal(dbl_graph *g) {
+    uint64_t m = g->m_base + g->m_delta;
+    uint64_t cap = 2ull * g->n + m / CHUNK + 64;
+    if (cap > 0xffffffffull) { set_error("frontier capacity overflow"); return DBL_E_CONFIG; }
+    dbl_status s;
+    for (int d = 0; d < 2; ++d) {
+        size_t sb = ((size_t)g->n + 1) * 4;
+        bool fresh = g->stamp[d].bytes < sb;
+        if ((s = g->stamp[d].ensure(sb))) return s;
+        if (fresh) {
+            DBL_CUDA(cudaMemsetAsync(g->stamp[d].p, 0, g->stamp[d].bytes, g->stream));
+            g->epoch = 1;
+            int other = d ^ 1;
+            if (g->stamp[other].p) DBL_CUDA(cudaMemsetAsync(g->stamp[other].p, 0, g->stamp[other].bytes, g->stream));
+        }
+        for (int p = 0; p < 2; ++p)
+            if ((s = g->qbuf[d][p].ensure(cap * 12))) return s;
+    }
+    g->qcap = (uint32_t)cap;
+    if ((s = g->ctrl.ensure(sizeof(Ctrl)))) return s;
+    if ((s = g->changed_bits.ensure((((size_t)g->n + 31) / 32) * 2 * 4 + 8))) return s;
+    return DBL_OK;
+}
+
+// ------------------------------------------------------------- insertion --
+
+__device__ __forceinline__ bool bsearch_u32(const uint32_t *a, uint32_t lo, uint32_t hi, uint32_t x) {
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        uint32_t y = a[mid];
+        if (y == x) return true;
+        if (y < x) lo = mid + 1; else hi = mid;
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool bsearch_u64(const uint64_t *a, uint64_t n, uint64_t x) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        uint64_t y = a[mid];
+        if (y == x) return true;
+        if (y < x) lo = mid + 1; else hi = mid;
+    }
+    return false;
+}
+
+__global__ void flag_new_kernel(const uint64_t *__restrict__ keys, uint64_t count,
+                                const uint32_t *__restrict__ fptr, const uint32_t *__restrict__ fcol,
+                                const uint64_t *__restrict__ dkeys, uint64_t nd,
+                                uint8_t *__restrict__ flag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        uint32_t u = (uint32_t)(k >> 32), v = (uint32_t)k;
+        bool present = bsearch_u32(fcol, fptr[u], fptr[u + 1], v);
+        if (!present && nd) present = bsearch_u64(dkeys, nd, k);
+        flag[i] = present ? 0 : 1;
+    }
+}
+
+// out = keys not yet in the graph (keys sorted + unique on input).
+dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, uint64_t *out,
+                            uint64_t *nout) {
+    if (count == 0) { *nout = 0; return DBL_OK; }
+    dbl_status s = g->scratch_c.ensure(count + 16);
+    if (s) return s;
+    uint8_t *flag = g->scratch_c.as<uint8_t>() + 16;
+    uint64_t *d_n = g->scratch_c.as<uint64_t>();
+    flag_new_kernel<<<grid_for(count), 256, 0, g->stream>>>(keys, count, g->fptr.as<uint32_t>(),
+                                                             g->fcol.as<uint32_t>(),
+                                                             g->dkeys_f.as<uint64_t>(), g->m_delta, flag);
+    DBL_CHECK_LAUNCH("flag_new_kernel");
+    size_t tmp = 0;
+    DBL_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, keys, flag, out, d_n, (int64_t)count, g->stream));
+    if ((s = g->cub_tmp.ensure(tmp))) return s;
+    DBL_CUDA(cub::DeviceSelect::Flagged(g->cub_tmp.p, tmp, keys, flag, out, d_n, (int64_t)count, g->stream));
+    DBL_LAUNCHED();
+    DBL_CUDA(cudaMemcpyAsync(nout, d_n, sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    return DBL_OK;
+}
+
+static dbl_status merge_into(dbl_graph *g, DevBuf &dst, uint64_t nd, const uint64_t *add,
+                             uint64_t na, DevBuf &tmpbuf) {
+    if (nd + na >= (1ull << 31)) { set_error("delta adjacency too large to merge"); return DBL_E_CONFIG; }
+    dbl_status s = tmpbuf.ensure((nd + na) * 8 + 8);
+    if (s) return s;
+    size_t tmp = 0;
+    DBL_CUDA(cub::DeviceMerge::MergeKeys(nullptr, tmp, dst.as<uint64_t>(), (int)nd, add, (int)na,
+                                         tmpbuf.as<uint64_t>(), cuda::std::less<uint64_t>{}, g->stream));
+    if ((s = g->cub_tmp.ensure(tmp))) return s;
+    DBL_CUDA(cub::DeviceMerge::MergeKeys(g->cub_tmp.p, tmp, dst.as<uint64_t>(), (int)nd, add, (int)na,
+                                         tmpbuf.as<uint64_t>(), cuda::std::less<uint64_t>{}, g->stream));
+    DBL_LAUNCHED();
+    std::swap(dst, tmpbuf);
+    return DBL_OK;
+}
+
+// Add sorted, unique, not-present forward keys to the delta adjacency.
+dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t count) {
+    if (count == 0) return DBL_OK;
+    dbl_status s;
+    uint32_t n = g->n;
+    uint64_t nd = g->m_delta;
+    // reverse keys of the new edges, sorted
+    if ((s = g->scratch_a.ensure(count * 8 + 8)) || (s = g->scratch_b.ensure(count * 8 + 8))) return s;
+    uint64_t *ra = g->scratch_a.as<uint64_t>(), *rb = g->scratch_b.as<uint64_t>();
+    swap_keys_kernel<<<grid_for(count), 256, 0, g->stream>>>(new_keys_f, count, ra);
+    DBL_CHECK_LAUNCH("swap_keys_kernel");
+    uint64_t *rsorted = nullptr;
+    if ((s = sort_keys(g, ra, rb, count, key_end_bit(n), &rsorted))) return s;
+    if (nd == 0) {
+        if ((s = g->dkeys_f.ensure(count * 8 + 8)) || (s = g->dkeys_r.ensure(count * 8 + 8))) return s;
+        DBL_CUDA(cudaMemcpyAsync(g->dkeys_f.p, new_keys_f, count * 8, cudaMemcpyDeviceToDevice, g->stream));
+        DBL_CUDA(cudaMemcpyAsync(g->dkeys_r.p, rsorted, count * 8, cudaMemcpyDeviceToDevice, g->stream));
+    } else {
+        DevBuf t1;
+        if ((s = merge_into(g, g->dkeys_f, nd, new_keys_f, count, t1))) { t1.release(); return s; }
+        t1.release();
+        DevBuf t2;
+        if ((s = merge_into(g, g->dkeys_r, nd, rsorted, count, t2))) { t2.release(); return s; }
+        t2.release();
+    }
+    uint64_t m = nd + count;
+    if ((s = g->dfptr.ensure(((size_t)n + 1) * 4)) || (s = g->drptr.ensure(((size_t)n + 1) * 4)) ||
+        (s = g->dfcol.ensure(m * 4 + 4)) || (s = g->drcol.ensure(m * 4 + 4)))
+        return s;
+    if ((s = build_csr_from_sorted(g, g->dkeys_f.as<uint64_t>(), m, n, g->dfptr.as<uint32_t>(),
+                                   g->dfcol.as<uint32_t>())))
+        return s;
+    if ((s = build_csr_from_sorted(g, g->dkeys_r.as<uint64_t>(), m, n, g->drptr.as<uint32_t>(),
+                                   g->drcol.as<uint32_t>())))
+        return s;
+    g->m_delta = m;
+    return graph_ensure_traversal(g);
+}
+
+// all base edges as sorted forward keys (warp per row)
+__global__ void expand_rows_kernel(const uint32_t *__restrict__ ptr, const uint32_t *__restrict__ col,
+                                   uint32_t n, uint64_t *__restrict__ keys) {
+    uint32_t lane = threadIdx.x & 31;
+    uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t u = warp; u < n; u += nw) {
+        uint32_t s = ptr[u], e = ptr[u + 1];
+        for (uint32_t i = s + lane; i < e; i += 32) keys[i] = (u << 32) | col[i];
+    }
+}
+
+// Fold the delta adjacency into the base CSR/CSC.
+dbl_status graph_compact(dbl_graph *g) {
+    if (g->m_delta == 0) return DBL_OK;
+    uint64_t mb = g->m_base, md = g->m_delta, m = mb + md;
+    dbl_status s;
+    DevBuf a, b;
+    if ((s = a.ensure(mb * 8 + 8))) return s;
+    if (mb) {
+        expand_rows_kernel<<<148 * 16, 256, 0, g->stream>>>(g->fptr.as<uint32_t>(), g->fcol.as<uint32_t>(),
+                                                            g->n, a.as<uint64_t>());
+        DBL_CHECK_LAUNCH("expand_rows_kernel");
+    }
+    if ((s = merge_into(g, a, mb, g->dkeys_f.as<uint64_t>(), md, b))) { a.release(); b.release(); return s; }
+    b.release();
+    // `a` now holds all m forward keys, sorted and unique
+    if ((s = b.ensure(m * 8 + 8))) { a.release(); return s; }
+    g->m_delta = 0;
+    // build_base sorts again (already sorted: cheap enough, keeps one path)
+    s = build_base(g, a.as<uint64_t>(), b.as<uint64_t>(), m);
+    a.release();
+    b.release();
+    if (s) return s;
+    return graph_ensure_traversal(g);
+}
+
+}  // namespace dbl
+
+// ------------------------------------------------------------------ ABI --
+using namespace dbl;
+
+extern "C" dbl_status dbl_graph_create(uint32_t n, const uint32_t *src, const uint32_t *dst,
+                                       uint64_t m, dbl_mem mem, int device, dbl_graph **out) {
+    if (!out || (m && (!src || !dst))) { set_error("null argument"); return DBL_E_ARG; }
+    *out = nullptr;
+    DBL_CUDA(cudaSetDevice(device));
+    dbl_graph *g = new dbl_graph();
+    g->device = device;
+    g->n = n;
+    auto fail = [&](dbl_status s) { dbl_graph_free(g); return s; };
+    cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate"));
+    for (auto &ev : g->ev) {
+        e = cudaEventCreate(&ev);
+        if (e != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
+    }
+    cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device);
+    dbl_status s;
+    DevBuf keys, alt, ds, dd, err;
+    auto cleanup = [&]() { keys.release(); alt.release(); ds.release(); dd.release(); err.release(); };
+    if ((s = keys.ensure(m * 8 + 8)) || (s = alt.ensure(m * 8 + 8)) || (s = err.ensure(8))) {
+        cleanup();
+        return fail(s);
+    }
+    const uint32_t *psrc = src, *pdst = dst;
+    if (m && mem == DBL_MEM_HOST) {
+        if ((s = ds.ensure(m * 4)) || (s = dd.ensure(m * 4))) { cleanup(); return fail(s); }
+        e = cudaMemcpyAsync(ds.p, src, m * 4, cudaMemcpyHostToDevice, g->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dd.p, dst, m * 4, cudaMemcpyHostToDevice, g->stream);
+        if (e != cudaSuccess) { cleanup(); return fail(cuda_fail(e, "H2D edges")); }
+        psrc = ds.as<uint32_t>();
+        pdst = dd.as<uint32_t>();
+    }
+    cudaMemsetAsync(err.p, 0, 8, g->stream);
+    if (m) {
+        pack_keys_kernel<<<grid_for(m), 256, 0, g->stream>>>(psrc, pdst, m, n, keys.as<uint64_t>(),
+                                                             err.as<unsigned long long>());
+        DBL_LAUNCHED();
+    }
+    unsigned long long herr = 0;
+    cudaMemcpyAsync(&herr, err.p, 8, cudaMemcpyDeviceToHost, g->stream);
+    e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) { cleanup(); return fail(cuda_fail(e, "pack_keys_kernel")); }
+    if (herr) {
+        cleanup();
+        set_error("edge endpoint outside [0, n)");
+        return fail(DBL_E_VERTEX_RANGE);
+    }
+    ds.release();
+    dd.release();
+    s = build_base(g, keys.as<uint64_t>(), alt.as<uint64_t>(), m);
+    cleanup();
+    if (s) return fail(s);
+    if ((s = graph_ensure_traversal(g))) return fail(s);
+    e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "graph build"));
+    *out = g;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
+    if (!g) return DBL_OK;
+    cudaSetDevice(g->device);
+    if (g->stream) cudaStreamSynchronize(g->stream);
+    DevBuf *bufs[] = {&g->fptr, &g->fcol, &g->rptr, &g->rcol, &g->dfptr, &g->dfcol, &g->drptr,
+                      &g->drcol, &g->dkeys_f, &g->dkeys_r, &g->stamp[0], &g->stamp[1],
+                      &g->qbuf[0][0], &g->qbuf[0][1], &g->qbuf[1][0], &g->qbuf[1][1], &g->ctrl,
+                      &g->changed_bits, &g->cub_tmp, &g->scratch_a, &g->scratch_b, &g->scratch_c,
+                      &g->scratch_d, &g->q_in, &g->q_codes, &g->q_vis, &g->q_pending,
+                      &g->q_counters, &g->q_dense};
+    for (auto *b : bufs) b->release();
+    g->host_stage.release();
+    for (auto &ev : g->ev) if (ev) cudaEventDestroy(ev);
+    if (g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_graph_info(const dbl_graph *g, uint32_t *n, uint64_t *m) {
+    if (!g) { set_error("null graph"); return DBL_E_ARG; }
+    if (n) *n = g->n;
+    if (m) *m = g->m_base + g->m_delta;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_graph_degrees(const dbl_graph *g, uint32_t *indeg, uint32_t *outdeg) {
+    if (!g || !indeg || !outdeg) { set_error("null argument"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(g->device));
+    dbl_graph *gm = const_cast<dbl_graph *>(g);
+    dbl_status s = gm->scratch_a.ensure(((size_t)g->n + 1) * 8);
+    if (s) return s;
+    uint32_t *di = gm->scratch_a.as<uint32_t>(), *dout = di + g->n;
+    if ((s = graph_degrees_dev(g, di, dout))) return s;
+    DBL_CUDA(cudaMemcpyAsync(indeg, di, (size_t)g->n * 4, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaMemcpyAsync(outdeg, dout, (size_t)g->n * 4, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    return DBL_OK;
+}
+
+__global__ void has_edges_kernel(const uint32_t *__restrict__ u, const uint32_t *__restrict__ v,
+                                 uint64_t count, uint32_t n, const uint32_t *__restrict__ fptr,
+                                 const uint32_t *__restrict__ fcol, const uint64_t *__restrict__ dkeys,
+                                 uint64_t nd, uint8_t *__restrict__ out, unsigned long long *err) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t a = u[i], b = v[i];
+        if (a >= n || b >= n) { atomicOr(err, 1ull); out[i] = 0; continue; }
+        bool p = bsearch_u32(fcol, fptr[a], fptr[a + 1], b);
+        if (!p && nd) p = bsearch_u64(dkeys, nd, ((uint64_t)a << 32) | b);
+        out[i] = p;
+    }
+}
+
+extern "C" dbl_status dbl_graph_has_edges(const dbl_graph *g, const uint32_t *u, const uint32_t *v,
+                                          uint64_t count, uint8_t *out) {
+    if (!g || (count && (!u || !v || !out))) { set_error("null argument"); return DBL_E_ARG; }
+    if (!count) return DBL_OK;
+    DBL_CUDA(cudaSetDevice(g->device));
+    DevBuf b;
+    dbl_status s = b.ensure(count * 9 + 16);
+    if (s) return s;
+    uint32_t *du = b.as<uint32_t>(), *dv = du + count;
+    uint8_t *dout = reinterpret_cast<uint8_t *>(dv + count);
+    unsigned long long *derr = reinterpret_cast<unsigned long long *>(b.as<char>() + ((count * 9 + 7) & ~7ull));
+    cudaMemcpyAsync(du, u, count * 4, cudaMemcpyHostToDevice, g->stream);
+    cudaMemcpyAsync(dv, v, count * 4, cudaMemcpyHostToDevice, g->stream);
+    cudaMemsetAsync(derr, 0, 8, g->stream);
+    has_edges_kernel<<<grid_for(count), 256, 0, g->stream>>>(du, dv, count, g->n, g->fptr.as<uint32_t>(),
+                                                              g->fcol.as<uint32_t>(),
+                                                              g->dkeys_f.as<uint64_t>(), g->m_delta,
+                                                              dout, derr);
+    DBL_LAUNCHED();
+    unsigned long long herr = 0;
+    cudaMemcpyAsync(out, dout, count, cudaMemcpyDeviceToHost, g->stream);
+    cudaMemcpyAsync(&herr, derr, 8, cudaMemcpyDeviceToHost, g->stream);
+    cudaError_t e = cudaStreamSynchronize(g->stream);
+    b.release();
+    if (e != cudaSuccess) return cuda_fail(e, "has_edges_kernel");
+    if (herr) { set_error("vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+    return DBL_OK;
+}
+
+__global__ void split_keys_kernel(const uint64_t *__restrict__ keys, uint64_t m, uint32_t *__restrict__ s,
+                                  uint32_t *__restrict__ d) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        s[i] = (uint32_t)(k >> 32);
+        d[i] = (uint32_t)k;
+    }
+}
+
+extern "C" dbl_status dbl_graph_edges(const dbl_graph *g, uint32_t *src, uint32_t *dst) {
+    if (!g) { set_error("null graph"); return DBL_E_ARG; }
+    uint64_t mb = g->m_base, md = g->m_delta, m = mb + md;
+    if (!m) return DBL_OK;
+    if (!src || !dst) { set_error("null argument"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(g->device));
+    dbl_graph *gm = const_cast<dbl_graph *>(g);
+    DevBuf a, b;
+    dbl_status s;
+    if ((s = a.ensure(m * 8 + 8))) return s;
+    if (mb) {
+        expand_rows_kernel<<<148 * 16, 256, 0, g->stream>>>(g->fptr.as<uint32_t>(), g->fcol.as<uint32_t>(),
+                                                            g->n, a.as<uint64_t>());
+        DBL_LAUNCHED();
+    }
+    if (md) {
+        if ((s = merge_into(gm, a, mb, g->dkeys_f.as<uint64_t>(), md, b))) { a.release(); b.release(); return s; }
+    }
+    b.release();
+    if ((s = b.ensure(m * 8 + 8))) { a.release(); return s; }
+    uint32_t *ds = b.as<uint32_t>(), *dd = ds + m;
+    split_keys_kernel<<<grid_for(m), 256, 0, g->stream>>>(a.as<uint64_t>(), m, ds, dd);
+    DBL_LAUNCHED();
+    cudaMemcpyAsync(src, ds, m * 4, cudaMemcpyDeviceToHost, g->stream);
+    cudaMemcpyAsync(dst, dd, m * 4, cudaMemcpyDeviceToHost, g->stream);
+    cudaError_t e = cudaStreamSynchronize(g->stream);
+    a.release();
+    b.release();
+    if (e != cudaSuccess) return cuda_fail(e, "dbl_graph_edges");
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_sync(const dbl_graph *g) {
+    if (!g) { set_error("null graph"); return DBL_E_ARG; }
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_stream(const dbl_graph *g, void **s) {
+    if (!g || !s) { set_error("null argument"); return DBL_E_ARG; }
+    *s = (void *)g->stream;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_last_timings(const dbl_graph *g, float *fix, float *label, float *bfs) {
+    if (!g) { set_error("null graph"); return DBL_E_ARG; }
+    if (fix) *fix = g->t_fix;
+    if (label) *label = g->t_label;
+    if (bfs) *bfs = g->t_bfs;
+    return DBL_OK;
+}

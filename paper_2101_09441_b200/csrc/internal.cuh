@@ -1,0 +1,192 @@
+// internal.cuh -- shared device structures of the DBL engine (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstddef>
+#include <string>
+
+#include "dbl_b200.h"
+
+namespace dbl {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint32_t CHUNK = 1024;          // max edges per frontier work item
+constexpr uint32_t DELTA_BIT = 0x80000000u;
+constexpr int FIX_THREADS = 256;
+constexpr int MAX_GROUP_WORDS = 8;        // words propagated together by one fixpoint
+constexpr int MAX_SHARD_WORDS = 64;
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string &msg);
+dbl_status cuda_fail(cudaError_t e, const char *what);
+uint64_t &launch_counter();
+
+#define DBL_CUDA(call)                                                         \
+    do {                                                                       \
+        cudaError_t _e = (call);                                               \
+        if (_e != cudaSuccess) return ::dbl::cuda_fail(_e, #call);             \
+    } while (0)
+#define DBL_LAUNCHED() (++::dbl::launch_counter())
+#define DBL_CHECK_LAUNCH(what)                                                 \
+    do {                                                                       \
+        DBL_LAUNCHED();                                                        \
+        cudaError_t _e = cudaGetLastError();                                   \
+        if (_e != cudaSuccess) return ::dbl::cuda_fail(_e, what);              \
+    } while (0)
+
+// grow-only device buffer
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    dbl_status ensure(size_t need) {
+        if (need <= bytes) return DBL_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t nb = need < 256 ? 256 : need;
+        cudaError_t e = cudaMalloc(&p, nb);
+        if (e != cudaSuccess) { cudaGetLastError(); return cuda_fail(e, "cudaMalloc(workspace)"); }
+        bytes = nb;
+        return DBL_OK;
+    }
+    template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+    void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+};
+
+// Pinned host staging buffer (grow-only).
+struct HostBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    dbl_status ensure(size_t need) {
+        if (need <= bytes) return DBL_OK;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMallocHost(&p, need);
+        if (e != cudaSuccess) { cudaGetLastError(); return cuda_fail(e, "cudaMallocHost"); }
+        bytes = need;
+        return DBL_OK;
+    }
+    void release() { if (p) cudaFreeHost(p); p = nullptr; bytes = 0; }
+};
+
+// One traversal direction's adjacency: base CSR + delta CSR (insertions).
+struct Adj {
+    const uint32_t *ptr;    // n+1
+    const uint32_t *col;
+    const uint32_t *dptr;   // n+1 or nullptr
+    const uint32_t *dcol;
+};
+
+// Frontier work items: (vertex, first edge, length | DELTA_BIT).
+struct Queue {
+    uint32_t *x;
+    uint32_t *start;
+    uint32_t *len;
+};
+
+// Device control block of one fixpoint run.
+struct Ctrl {
+    uint32_t cnt[3][2];      // items per [level % 3][direction]
+    uint32_t work[3];        // warp-chunk tickets per level % 3
+    uint32_t levels;
+    uint32_t overflow;
+    uint32_t seed_changed[2];
+    uint32_t pad;
+    unsigned long long changed[2];   // distinct vertices whose label grew
+    unsigned long long error;        // range errors etc.
+};
+
+// One direction of a fixpoint: label words [lab + v*stride, +nw) propagate
+// along `adj` (forward CSR for in-labels, reverse CSC for out-labels).
+struct DirParams {
+    Adj adj;
+    uint64_t *lab;
+    uint32_t stride;
+    uint32_t *stamp;
+    Queue q[2];
+    uint32_t cap;
+    uint32_t *changed_bits;   // nullptr unless counting distinct changes
+};
+
+struct FixParams {
+    DirParams d[2];
+    Ctrl *ctrl;
+    uint32_t epoch0;
+    uint32_t max_levels;
+};
+
+}  // namespace dbl
+
+// ------------------------------------------------------------- handles --
+struct dbl_graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint32_t n = 0;
+    uint64_t m_base = 0, m_delta = 0;
+    // base adjacency
+    dbl::DevBuf fptr, fcol, rptr, rcol;
+    // delta adjacency (insertions since the last compaction)
+    dbl::DevBuf dfptr, dfcol, drptr, drcol, dkeys_f, dkeys_r;
+    // traversal workspace shared by builds/inserts on this graph
+    dbl::DevBuf stamp[2];
+    uint32_t epoch = 1;
+    dbl::DevBuf qbuf[2][2];   // [direction][parity] queue storage
+    uint32_t qcap = 0;
+    dbl::DevBuf ctrl;
+    dbl::DevBuf changed_bits;
+    // generic scratch
+    dbl::DevBuf cub_tmp, scratch_a, scratch_b, scratch_c, scratch_d;
+    dbl::HostBuf host_stage;
+    // query workspace
+    dbl::DevBuf q_in, q_codes, q_vis, q_pending, q_counters, q_dense;
+    int sm_count = 148;
+    int coop_blocks = 0;      // co-resident blocks for the fixpoint kernel
+    cudaEvent_t ev[6] = {};
+    float t_fix = 0, t_label = 0, t_bfs = 0;
+};
+
+struct dbl_index {
+    int device = 0;
+    uint32_t n = 0;
+    dbl_config cfg{};
+    uint32_t wdl = 0, wbl = 0, rw = 0;  // words: dl, bl, per record
+    dbl::DevBuf rec;                     // n * rw u64
+    dbl::DevBuf landmarks;               // k u32
+    dbl::DevBuf leaf_flags;              // n u8
+    dbl::DevBuf bucket;                  // n u32
+};
+
+namespace dbl {
+// graph.cu
+dbl_status graph_ensure_traversal(dbl_graph *g);
+dbl_status graph_degrees_dev(const dbl_graph *g, uint32_t *indeg, uint32_t *outdeg);
+Adj graph_fwd(const dbl_graph *g);
+Adj graph_rev(const dbl_graph *g);
+dbl_status build_csr_from_sorted(dbl_graph *g, const uint64_t *keys, uint64_t m, uint32_t n,
+                                 uint32_t *ptr, uint32_t *col);
+dbl_status sort_keys(dbl_graph *g, uint64_t *keys, uint64_t *alt, uint64_t m, int end_bit,
+                     uint64_t **sorted);
+int key_end_bit(uint32_t n);
+dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t count);
+dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, uint64_t *out,
+                            uint64_t *nout);
+dbl_status graph_compact(dbl_graph *g);
+// select.cu
+dbl_status select_landmarks_dev(dbl_graph *g, uint32_t k, int strategy, uint32_t *dev_out);
+dbl_status select_leaves_dev(dbl_graph *g, uint64_t threshold, uint32_t k_prime, uint64_t seed,
+                             const uint32_t *dev_ovr, uint8_t *dev_flags, uint32_t *dev_bucket);
+dbl_status leaf_hash_dev(const uint64_t *ids, uint64_t count, uint32_t k_prime, uint64_t seed,
+                         uint32_t *out, cudaStream_t s);
+// fixpoint.cu
+dbl_status index_seed_records(dbl_graph *g, dbl_index *idx);
+dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32_t nwords);
+dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, uint64_t count,
+                      bool count_changes, uint32_t *changed_out, uint32_t *seed_changed,
+                      uint32_t *levels);
+dbl_status work_model(const dbl_index *idx, dbl_graph *g, uint64_t *V, uint64_t *E,
+                      uint32_t *levels);
+// query.cu
+dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
+                     uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited);
+}  // namespace dbl

@@ -1,0 +1,252 @@
+// select.cu -- K1 landmark ranking and K2 leaf selection / leaf hashing.
+//
+// select_landmarks (reference labels.py:140-147) orders vertices by
+// (-score, id) and keeps the top k; the score is LandmarkStrategy.score
+// (labels.py:39-46) of (in-degree, out-degree), computed here as u64, which
+// is exact for n < 2^32.  A stable descending radix sort over the scores of
+// vertices listed in id order reproduces the (-score, id) tie-break exactly.
+//
+// select_leaves (labels.py:150-181) + leaf_hash (labels.py:119-137): one
+// thread per vertex, splitmix64 mix mod k' in u64 wrap-around arithmetic.
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace dbl {
+
+__host__ __device__ __forceinline__ uint32_t leaf_hash_u64(uint64_t v, uint32_t k_prime, uint64_t seed) {
+    uint64_t x = v * 0x9E3779B97F4A7C15ull + seed * 0xD1B54A32D192ED03ull;
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return (uint32_t)(x % (uint64_t)k_prime);
+}
+
+__global__ void leaf_hash_kernel(const uint64_t *__restrict__ ids, uint64_t count, uint32_t k_prime,
+                                 uint64_t seed, uint32_t *__restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = leaf_hash_u64(ids[i], k_prime, seed);
+}
+
+dbl_status leaf_hash_dev(const uint64_t *ids, uint64_t count, uint32_t k_prime, uint64_t seed,
+                         uint32_t *out, cudaStream_t s) {
+    if (!count) return DBL_OK;
+    int blocks = (int)((count + 255) / 256 < 4096 ? (count + 255) / 256 : 4096);
+    leaf_hash_kernel<<<blocks, 256, 0, s>>>(ids, count, k_prime, seed, out);
+    DBL_CHECK_LAUNCH("leaf_hash_kernel");
+    return DBL_OK;
+}
+
+__global__ void score_kernel(const uint32_t *__restrict__ fptr, const uint32_t *__restrict__ rptr,
+                             const uint32_t *__restrict__ dfptr, const uint32_t *__restrict__ drptr,
+                             uint32_t n, int strategy, uint64_t *__restrict__ score,
+                             uint32_t *__restrict__ ids) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        uint64_t out = fptr[v + 1] - fptr[v], in = rptr[v + 1] - rptr[v];
+        if (dfptr) { out += dfptr[v + 1] - dfptr[v]; in += drptr[v + 1] - drptr[v]; }
+        uint64_t s;
+        switch (strategy) {
+        case DBL_STRAT_MAX: s = in > out ? in : out; break;
+        case DBL_STRAT_MIN: s = in < out ? in : out; break;
+        case DBL_STRAT_SUM: s = in + out; break;
+        default: s = in * out; break;
+        }
+        score[v] = s;
+        ids[v] = v;
+    }
+}
+
+dbl_status select_landmarks_dev(dbl_graph *g, uint32_t k, int strategy, uint32_t *dev_out) {
+    uint32_t n = g->n;
+    if (k > n) { set_error("k exceeds vertex count"); return DBL_E_CONFIG; }
+    if (k == 0) return DBL_OK;
+    dbl_status s;
+    size_t nb = (size_t)n * 8;
+    if ((s = g->scratch_a.ensure(nb * 2)) || (s = g->scratch_b.ensure(nb * 2))) return s;
+    uint64_t *sc = g->scratch_a.as<uint64_t>(), *sc2 = sc + n;
+    uint32_t *id = g->scratch_b.as<uint32_t>(), *id2 = id + n;
+    Adj f = graph_fwd(g), r = graph_rev(g);
+    int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+    score_kernel<<<blocks, 256, 0, g->stream>>>(f.ptr, r.ptr, f.dptr, r.dptr, n, strategy, sc, id);
+    DBL_CHECK_LAUNCH("score_kernel");
+    cub::DoubleBuffer<uint64_t> dk(sc, sc2);
+    cub::DoubleBuffer<uint32_t> dv(id, id2);
+    size_t tmp = 0;
+    DBL_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, dk, dv, (int64_t)n, 0, 64, g->stream));
+    if ((s = g->cub_tmp.ensure(tmp))) return s;
+    DBL_CUDA(cub::DeviceRadixSort::SortPairsDescending(g->cub_tmp.p, tmp, dk, dv, (int64_t)n, 0, 64,
+                                                       g->stream));
+    DBL_LAUNCHED();
+    DBL_CUDA(cudaMemcpyAsync(dev_out, dv.Current(), (size_t)k * 4, cudaMemcpyDeviceToDevice, g->stream));
+    return DBL_OK;
+}
+
+__global__ void leaves_kernel(const uint32_t *__restrict__ fptr, const uint32_t *__restrict__ rptr,
+                              const uint32_t *__restrict__ dfptr, const uint32_t *__restrict__ drptr,
+                              uint32_t n, uint64_t threshold, uint32_t k_prime, uint64_t seed,
+                              const uint32_t *__restrict__ ovr, uint8_t *__restrict__ flags,
+                              uint32_t *__restrict__ bucket, unsigned long long *err) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        uint64_t out = fptr[v + 1] - fptr[v], in = rptr[v + 1] - rptr[v];
+        if (dfptr) { out += dfptr[v + 1] - dfptr[v]; in += drptr[v + 1] - drptr[v]; }
+        uint8_t f = 0;
+        if (in == 0) f |= 1;
+        if (out == 0) f |= 2;
+        if (threshold > 0 && in * out <= threshold) f |= 3;
+        uint32_t b = 0;
+        if (f) {
+            uint32_t o = ovr ? ovr[v] : 0xffffffffu;
+            if (o != 0xffffffffu) {
+                if (o >= k_prime) atomicOr(err, 1ull);
+                b = o;
+            } else {
+                b = leaf_hash_u64(v, k_prime, seed);
+            }
+        }
+        flags[v] = f;
+        bucket[v] = b;
+    }
+}
+
+dbl_status select_leaves_dev(dbl_graph *g, uint64_t threshold, uint32_t k_prime, uint64_t seed,
+                             const uint32_t *dev_ovr, uint8_t *dev_flags, uint32_t *dev_bucket) {
+    if (k_prime < 1) { set_error("k_prime must be >= 1"); return DBL_E_CONFIG; }
+    uint32_t n = g->n;
+    if (n == 0) return DBL_OK;
+    dbl_status s = g->scratch_c.ensure(16);
+    if (s) return s;
+    unsigned long long *err = g->scratch_c.as<unsigned long long>();
+    DBL_CUDA(cudaMemsetAsync(err, 0, 8, g->stream));
+    Adj f = graph_fwd(g), r = graph_rev(g);
+    int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+    leaves_kernel<<<blocks, 256, 0, g->stream>>>(f.ptr, r.ptr, f.dptr, r.dptr, n, threshold, k_prime,
+                                                 seed, dev_ovr, dev_flags, dev_bucket, err);
+    DBL_CHECK_LAUNCH("leaves_kernel");
+    unsigned long long herr = 0;
+    DBL_CUDA(cudaMemcpyAsync(&herr, err, 8, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    if (herr) { set_error("bucket override outside [0, k_prime)"); return DBL_E_CONFIG; }
+    return DBL_OK;
+}
+
+}  // namespace dbl
+
+using namespace dbl;
+
+extern "C" dbl_status dbl_leaf_hash(const uint64_t *ids, uint64_t count, uint32_t k_prime,
+                                    uint64_t seed, uint32_t *out, int device) {
+    if (k_prime < 1) { set_error("k_prime must be >= 1"); return DBL_E_CONFIG; }
+    if (!count) return DBL_OK;
+    if (!ids || !out) { set_error("null argument"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(device));
+    DevBuf b;
+    dbl_status s = b.ensure(count * 12);
+    if (s) return s;
+    uint64_t *di = b.as<uint64_t>();
+    uint32_t *dout = reinterpret_cast<uint32_t *>(di + count);
+    DBL_CUDA(cudaMemcpy(di, ids, count * 8, cudaMemcpyHostToDevice));
+    s = leaf_hash_dev(di, count, k_prime, seed, dout, 0);
+    if (!s) {
+        cudaError_t e = cudaMemcpy(out, dout, count * 4, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) s = cuda_fail(e, "leaf_hash D2H");
+    }
+    b.release();
+    return s;
+}
+
+extern "C" dbl_status dbl_select_landmarks(const dbl_graph *g, uint32_t k, int32_t strategy,
+                                           uint32_t *out_ids) {
+    if (!g || (k && !out_ids)) { set_error("null argument"); return DBL_E_ARG; }
+    if (k > g->n) { set_error("k exceeds vertex count"); return DBL_E_CONFIG; }
+    if (!k) return DBL_OK;
+    DBL_CUDA(cudaSetDevice(g->device));
+    dbl_graph *gm = const_cast<dbl_graph *>(g);
+    DevBuf b;
+    dbl_status s = b.ensure((size_t)k * 4);
+    if (s) return s;
+    s = select_landmarks_dev(gm, k, strategy, b.as<uint32_t>());
+    if (!s) {
+        cudaMemcpyAsync(out_ids, b.p, (size_t)k * 4, cudaMemcpyDeviceToHost, g->stream);
+        cudaError_t e = cudaStreamSynchronize(g->stream);
+        if (e != cudaSuccess) s = cuda_fail(e, "select_landmarks");
+    }
+    b.release();
+    return s;
+}
+
+__global__ void scatter_ovr_kernel(const uint32_t *__restrict__ ids, const uint32_t *__restrict__ b,
+                                   uint32_t cnt, uint32_t n, uint32_t *__restrict__ ovr,
+                                   unsigned long long *err) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        if (ids[i] >= n) continue;  // labels.py:167-171 only consults leaves
+        ovr[ids[i]] = b[i];
+    }
+}
+
+namespace dbl {
+// Device override table (n entries, 0xffffffff = none) from host pairs.
+dbl_status make_override(dbl_graph *g, const uint32_t *ids, const uint32_t *buckets, uint32_t cnt,
+                         DevBuf &ovr) {
+    uint32_t n = g->n;
+    dbl_status s = ovr.ensure((size_t)n * 4 + (size_t)cnt * 8 + 16);
+    if (s) return s;
+    uint32_t *o = ovr.as<uint32_t>();
+    uint32_t *di = o + n, *db = di + cnt;
+    unsigned long long *err = reinterpret_cast<unsigned long long *>(g->scratch_c.p);
+    if ((s = g->scratch_c.ensure(16))) return s;
+    err = g->scratch_c.as<unsigned long long>();
+    DBL_CUDA(cudaMemsetAsync(o, 0xff, (size_t)n * 4, g->stream));
+    DBL_CUDA(cudaMemsetAsync(err, 0, 8, g->stream));
+    if (cnt) {
+        DBL_CUDA(cudaMemcpyAsync(di, ids, (size_t)cnt * 4, cudaMemcpyHostToDevice, g->stream));
+        DBL_CUDA(cudaMemcpyAsync(db, buckets, (size_t)cnt * 4, cudaMemcpyHostToDevice, g->stream));
+        scatter_ovr_kernel<<<(cnt + 255) / 256, 256, 0, g->stream>>>(di, db, cnt, n, o, err);
+        DBL_CHECK_LAUNCH("scatter_ovr_kernel");
+    }
+    unsigned long long herr = 0;
+    DBL_CUDA(cudaMemcpyAsync(&herr, err, 8, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    (void)herr;
+    return DBL_OK;
+}
+}  // namespace dbl
+
+extern "C" dbl_status dbl_select_leaves(const dbl_graph *g, uint64_t threshold, uint32_t k_prime,
+                                        uint64_t hash_seed, const uint32_t *ovr_ids,
+                                        const uint32_t *ovr_buckets, uint32_t n_ovr,
+                                        uint8_t *out_flags, uint32_t *out_bucket) {
+    if (!g || (g->n && (!out_flags || !out_bucket)) || (n_ovr && (!ovr_ids || !ovr_buckets))) {
+        set_error("null argument");
+        return DBL_E_ARG;
+    }
+    if (k_prime < 1) { set_error("k_prime must be >= 1"); return DBL_E_CONFIG; }
+    uint32_t n = g->n;
+    if (!n) return DBL_OK;
+    DBL_CUDA(cudaSetDevice(g->device));
+    dbl_graph *gm = const_cast<dbl_graph *>(g);
+    DevBuf ovr, outb;
+    dbl_status s = DBL_OK;
+    const uint32_t *dovr = nullptr;
+    if (ovr_ids && n_ovr) {
+        s = make_override(gm, ovr_ids, ovr_buckets, n_ovr, ovr);
+        dovr = ovr.as<uint32_t>();
+    }
+    if (!s) s = outb.ensure((size_t)n * 5 + 16);
+    if (!s) {
+        uint32_t *db = outb.as<uint32_t>();
+        uint8_t *df = reinterpret_cast<uint8_t *>(db + n);
+        s = select_leaves_dev(gm, threshold, k_prime, hash_seed, dovr, df, db);
+        if (!s) {
+            cudaMemcpyAsync(out_flags, df, n, cudaMemcpyDeviceToHost, g->stream);
+            cudaMemcpyAsync(out_bucket, db, (size_t)n * 4, cudaMemcpyDeviceToHost, g->stream);
+            cudaError_t e = cudaStreamSynchronize(g->stream);
+            if (e != cudaSuccess) s = cuda_fail(e, "select_leaves D2H");
+        }
+    }
+    ovr.release();
+    outb.release();
+    return s;
+}

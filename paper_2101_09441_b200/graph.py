@@ -1,0 +1,229 @@
+"""Device-resident directed graph with the reference DynamicGraph's surface.
+
+Reference: graph.py:31-145 (DynamicGraph).  The adjacency lives in HBM as a
+CSR (out-edges) plus a CSC (in-edges), built and deduplicated on the GPU by
+dbl_graph_create (K0, csrc/graph.cu); later insertions go to a sorted delta
+CSR/CSC that every traversal reads alongside the base.
+
+Edges added before the graph is first used on the device are buffered on
+the host (with the reference's duplicate check, graph.py:60-61) and
+uploaded in one batch; afterwards every add_edge goes straight to the device.
+"""
+from __future__ import annotations
+
+import ctypes
+import weakref
+from typing import Iterator
+
+import numpy as np
+
+from . import _native as N
+from .errors import VertexRangeError
+
+
+class DynamicGraph:
+    """Directed graph on one GPU; ids are dense ints 0..n-1 (graph.py:31-46)."""
+
+    def __init__(self, vertex_count: int = 0, *, device: int = 0):
+        if vertex_count < 0:
+            raise VertexRangeError("vertex_count must be >= 0")
+        self._n = int(vertex_count)
+        self.device = int(device)
+        self._h = None
+        self._pending: dict[tuple[int, int], None] = {}
+        self._m_dev = 0
+        self.version = 0
+        self.original_ids: list[int] | None = None
+        self._dense_of: dict[int, int] | None = None
+
+    # -- construction -----------------------------------------------------
+    @classmethod
+    def from_edges(cls, n: int, src, dst, *, device: int = 0) -> "DynamicGraph":
+        """Bulk constructor: upload an edge list and build CSR/CSC on device."""
+        g = cls(n, device=device)
+        s = N.u32_array(src)
+        d = N.u32_array(dst)
+        if len(s) != len(d):
+            raise ValueError("src and dst differ in length")
+        g._create(s, d)
+        return g
+
+    def _create(self, s: np.ndarray, d: np.ndarray) -> None:
+        h = ctypes.c_void_p()
+        N.call("dbl_graph_create", self._n, N.ptr(s), N.ptr(d), len(s), N.MEM_HOST, self.device,
+               ctypes.byref(h))
+        self._h = h
+        self._refresh_count()
+        weakref.finalize(self, N.lib().dbl_graph_free, h)
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        """The device graph (materialises buffered edges on first use)."""
+        if self._h is None:
+            if self._pending:
+                e = np.array(list(self._pending), dtype=np.uint32).reshape(-1, 2)
+                s, d = np.ascontiguousarray(e[:, 0]), np.ascontiguousarray(e[:, 1])
+            else:
+                s = d = np.zeros(0, np.uint32)
+            self._pending = {}
+            self._create(s, d)
+        return self._h
+
+    def _refresh_count(self) -> None:
+        n = ctypes.c_uint32()
+        m = ctypes.c_uint64()
+        N.call("dbl_graph_info", self._h, ctypes.byref(n), ctypes.byref(m))
+        self._m_dev = int(m.value)
+
+    # -- reference surface ------------------------------------------------
+    @property
+    def vertex_count(self) -> int:
+        return self._n
+
+    @property
+    def edge_count(self) -> int:
+        return self._m_dev if self._h is not None else len(self._pending)
+
+    def _check_vertex(self, v: int) -> None:
+        if not 0 <= v < self._n:
+            raise VertexRangeError(f"vertex {v} outside [0, {self._n})")
+
+    def add_vertex(self) -> int:
+        if self._h is not None:
+            N.call("dbl_graph_add_vertices", self._h, 1)
+        self._n += 1
+        self.version += 1
+        return self._n - 1
+
+    def add_vertices(self, count: int) -> range:
+        if count and self._h is not None:
+            N.call("dbl_graph_add_vertices", self._h, count)
+        first = self._n
+        self._n += count
+        self.version += 1
+        return range(first, self._n)
+
+    def add_edge(self, u: int, v: int) -> bool:
+        """Insert edge (u, v); False if it was already present (graph.py:56-66)."""
+        self._check_vertex(u)
+        self._check_vertex(v)
+        if self._h is None:
+            if (u, v) in self._pending:
+                return False
+            self._pending[(u, v)] = None
+            self.version += 1
+            return True
+        return self.add_edges([u], [v]) == 1
+
+    def add_edges(self, src, dst) -> int:
+        """Batch add_edge; returns how many distinct new edges were added."""
+        s = N.u32_array(src)
+        d = N.u32_array(dst)
+        if len(s) != len(d):
+            raise ValueError("src and dst differ in length")
+        if not len(s):
+            return 0
+        if s.max() >= self._n or d.max() >= self._n:
+            bad = int(s.max() if s.max() >= self._n else d.max())
+            raise VertexRangeError(f"vertex {bad} outside [0, {self._n})")
+        if self._h is None:
+            before = len(self._pending)
+            for a, b in zip(s.tolist(), d.tolist()):
+                self._pending[(a, b)] = None
+            self.version += 1
+            return len(self._pending) - before
+        out = ctypes.c_uint64()
+        N.call("dbl_graph_add_edges", self.handle, N.ptr(s), N.ptr(d), len(s), ctypes.byref(out))
+        self._refresh_count()
+        self.version += 1
+        return int(out.value)
+
+    def has_edge(self, u: int, v: int) -> bool:
+        if self._h is None:
+            return (u, v) in self._pending
+        return bool(self.has_edges([u], [v])[0])
+
+    def has_edges(self, u, v) -> np.ndarray:
+        a, b = N.u32_array(u), N.u32_array(v)
+        out = np.zeros(len(a), np.uint8)
+        N.call("dbl_graph_has_edges", self.handle, N.ptr(a), N.ptr(b), len(a), N.ptr(out))
+        return out.astype(bool)
+
+    def degrees(self) -> tuple[np.ndarray, np.ndarray]:
+        """(in_degree[n], out_degree[n]) computed on the device."""
+        ind = np.zeros(self._n, np.uint32)
+        outd = np.zeros(self._n, np.uint32)
+        N.call("dbl_graph_degrees", self.handle, N.ptr(ind), N.ptr(outd))
+        return ind, outd
+
+    def out_degree(self, u: int) -> int:
+        self._check_vertex(u)
+        return int(self.degrees()[1][u])
+
+    def in_degree(self, v: int) -> int:
+        self._check_vertex(v)
+        return int(self.degrees()[0][v])
+
+    def edge_arrays(self) -> tuple[np.ndarray, np.ndarray]:
+        """All edges as (src, dst) arrays sorted by (src, dst)."""
+        h = self.handle
+        m = self.edge_count
+        s = np.zeros(m, np.uint32)
+        d = np.zeros(m, np.uint32)
+        if m:
+            N.call("dbl_graph_edges", h, N.ptr(s), N.ptr(d))
+        return s, d
+
+    def edges(self) -> Iterator[tuple[int, int]]:
+        s, d = self.edge_arrays()
+        return iter(zip(s.tolist(), d.tolist()))
+
+    def successors(self, u: int) -> list[int]:
+        self._check_vertex(u)
+        s, d = self.edge_arrays()
+        return d[s == u].tolist()
+
+    def predecessors(self, v: int) -> list[int]:
+        self._check_vertex(v)
+        s, d = self.edge_arrays()
+        return s[d == v].tolist()
+
+    def vertices(self) -> range:
+        return range(self._n)
+
+    def to_original(self, dense: int) -> int:
+        self._check_vertex(dense)
+        return self.original_ids[dense] if self.original_ids else dense
+
+    def __repr__(self) -> str:
+        return f"DynamicGraph(n={self._n}, m={self.edge_count}, device={self.device})"
+
+
+_converted: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def as_device_graph(g, device: int = 0) -> DynamicGraph:
+    """Accept this package's graph or any reference-style graph object.
+
+    A reference dblreach.DynamicGraph (forward adjacency lists, graph.py:36)
+    is uploaded once and cached until its vertex or edge count changes.
+    """
+    if isinstance(g, DynamicGraph):
+        return g
+    if hasattr(g, "forward") and hasattr(g, "vertex_count"):
+        key = (g.vertex_count, getattr(g, "edge_count", None))
+        try:
+            cached = _converted.get(g)
+        except TypeError:
+            cached = None
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        src = np.fromiter((u for u, succ in enumerate(g.forward) for _ in succ), np.uint32)
+        dst = np.fromiter((v for succ in g.forward for v in succ), np.uint32)
+        dg = DynamicGraph.from_edges(g.vertex_count, src, dst, device=device)
+        try:
+            _converted[g] = (key, dg)
+        except TypeError:
+            pass
+        return dg
+    raise TypeError(f"expected a DynamicGraph, got {type(g)!r}")

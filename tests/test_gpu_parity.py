@@ -1,0 +1,381 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the golden vectors
+and the CPU oracle.  Bit-exact for labels, metadata and answer codes.
+
+Golden fixtures come from the reference itself (oracle/gen_golden.py); larger
+cases compare with the oracle restatement (oracle/dbl_oracle.c), which
+tests/test_oracle.py pins to the same fixtures.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2101_09441_b200 as E
+from paper_2101_09441_b200 import workload as W
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FAMS = ("dl_in", "dl_out", "bl_in", "bl_out")
+FLAGSETS = {
+    "default": E.QueryFlags(),
+    "dl_only": E.QueryFlags(use_bl=False),
+    "bl_only": E.QueryFlags(use_dl=False),
+    "no_early": E.QueryFlags(use_thm1=False, use_thm2=False),
+    "no_prune": E.QueryFlags(prune_dl=False, prune_bl=False),
+    "bare": E.QueryFlags(use_thm1=False, use_thm2=False, prune_dl=False, prune_bl=False),
+}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def graph_of(d, p=""):
+    return E.DynamicGraph.from_edges(int(d[p + "n"]), d[p + "src"], d[p + "dst"])
+
+
+def assert_labels(idx, d, p=""):
+    w = idx.export_words()
+    for f in FAMS:
+        np.testing.assert_array_equal(w[f], d[p + f], err_msg=f)
+
+
+def assert_labels_equal_oracle(idx, oidx):
+    w = idx.export_words()
+    for f in FAMS:
+        np.testing.assert_array_equal(w[f], getattr(oidx, f), err_msg=f)
+
+
+def assert_meta(idx, d, p=""):
+    assert idx.landmark_set.landmarks == tuple(d[p + "landmarks"].tolist())
+    np.testing.assert_array_equal(idx.leaf_sets.flags, d[p + "leaf_flags"])
+    m = d[p + "leaf_flags"] != 0
+    np.testing.assert_array_equal(idx.leaf_sets.bucket_array[m], d[p + "bucket"][m])
+
+
+def toy_index(d):
+    g = graph_of(d)
+    ovr = {0: 0, 9: 0, 1: 1, 2: 1, 10: 1}   # EXAMPLE_BUCKETS, pkg/tests/conftest.py:23
+    leaves = E.select_leaves(g, 0, k_prime=2, bucket_override=ovr)
+    idx = E.build_index(g, E.IndexConfig(k=2, k_prime=2), landmarks=[4, 7], leaf_sets=leaves)
+    return g, idx
+
+
+# ------------------------------------------------------------------ toy --
+
+def test_toy_tables(toy_golden):
+    d = toy_golden
+    g, idx = toy_index(d)
+    assert_labels(idx, d)
+    for f in FAMS:
+        np.testing.assert_array_equal(idx.export_words()[f][:, 0], d["exp_" + f])
+    auto = E.build_index(g, E.IndexConfig(k=3, k_prime=4))
+    assert_meta(auto, d, "auto_")
+    assert_labels(auto, d, "auto_")
+
+
+def test_toy_queries_all_flagsets(toy_golden):
+    d = toy_golden
+    g, idx = toy_index(d)
+    for name, fl in FLAGSETS.items():
+        out, stats = E.query_batch(g, idx, (d["qu"], d["qv"]), flags=fl)
+        np.testing.assert_array_equal(out.codes, d[f"codes_{name}"], err_msg=name)
+        bfs = np.isin(out.codes, (5, 6))
+        np.testing.assert_array_equal(out.visited == 0, ~bfs)
+        assert stats.label_answered == int((~bfs).sum())
+
+
+def test_toy_single_queries(toy_golden):
+    d = toy_golden
+    g, idx = toy_index(d)
+    # tests/test_queries.py:12-47 outcomes
+    assert E.query(g, idx, 0, 9) == E.QueryOutcome(True, E.AnsweredBy.DL_POSITIVE, 0)
+    assert E.query(g, idx, 3, 5).answered_by is E.AnsweredBy.BL_NEGATIVE
+    o = E.query(g, idx, 2, 10)
+    assert o.reachable and o.answered_by is E.AnsweredBy.BFS_POSITIVE and o.visited >= 1
+    assert E.query(g, idx, 6, 6) == E.QueryOutcome(True, E.AnsweredBy.REFLEXIVE, 0)
+    assert E.query(g, idx, 9, 7).answered_by is E.AnsweredBy.THM1_NEGATIVE
+    assert E.query(g, idx, 4, 3, E.QueryFlags(use_bl=False)).answered_by is E.AnsweredBy.THM2_NEGATIVE
+    out, st = E.query_batch(g, idx, [(0, 9), (3, 5), (2, 10)])
+    assert [o.answered_by for o in out] == [E.AnsweredBy.DL_POSITIVE, E.AnsweredBy.BL_NEGATIVE,
+                                            E.AnsweredBy.BFS_POSITIVE]
+    assert st.rho == pytest.approx(2 / 3)
+
+
+def test_toy_insertion_example(toy_golden):
+    d = toy_golden
+    g, idx = toy_index(d)
+    st = E.insert_edge(g, idx, *map(int, d["ins_uv"]))
+    exp = d["ins_stats"]
+    assert (st.visited, st.labels_changed, st.early_terminated) == (int(exp[0]), int(exp[1]), bool(exp[2]))
+    assert_labels(idx, d, "ins_")
+    assert idx.labels_equal(E.rebuild_index(g, idx))
+    g2, idx2 = toy_index(d)
+    st2 = E.insert_edge(g2, idx2, *map(int, d["ins2_uv"]))
+    assert st2.early_terminated and st2.visited == 0 and st2.labels_changed == 0
+    assert g2.has_edge(*map(int, d["ins2_uv"]))
+    # re-inserting a present edge changes nothing (tests/test_updates.py:58-65)
+    m = g2.edge_count
+    E.insert_edge(g2, idx2, 2, 6)
+    assert g2.edge_count == m
+
+
+def test_toy_errors(toy_golden):
+    d = toy_golden
+    g, idx = toy_index(d)
+    with pytest.raises(E.VertexRangeError):
+        E.query(g, idx, 0, 11)
+    with pytest.raises(E.VertexRangeError):
+        E.query_batch(g, idx, [(0, 1), (12, 3)])
+    with pytest.raises(E.ConfigError):
+        E.query_batch(g, idx, [(0, 1)], workers=0)
+    with pytest.raises(E.ConfigError):
+        E.build_index(g, E.IndexConfig(k=12))
+    with pytest.raises(E.ConfigError):
+        E.build_index(g, E.IndexConfig(k=3, k_prime=2), landmarks=[4, 5])
+    with pytest.raises(E.ConfigError):
+        E.select_leaves(g, 0, k_prime=2, bucket_override={0: 5})
+    with pytest.raises(E.VertexRangeError):
+        E.insert_edge(g, idx, 0, 99)
+    g.add_vertex()
+    with pytest.raises(E.IndexGraphMismatchError):
+        E.query(g, idx, 0, 1)
+
+
+def test_leaf_hash_kats():
+    d = np.load(__import__("conftest").GOLDEN + "/leaf_hash.npz")
+    for j, kp in enumerate(d["kprimes"]):
+        for s, sd in enumerate(d["seeds"]):
+            got = E.leaf_hash_batch(d["ids"], int(kp), int(sd))
+            np.testing.assert_array_equal(got, d["buckets"][:, j, s])
+    assert E.leaf_hash(1, 64, 0) == 47 and E.leaf_hash(12345, 64, 7) == 5
+
+
+def test_landmark_and_leaf_kats():
+    d = np.load(__import__("conftest").GOLDEN + "/landmarks.npz")
+    for ci in range(4):
+        g = E.DynamicGraph.from_edges(int(d[f"c{ci}_n"]), d[f"c{ci}_src"], d[f"c{ci}_dst"])
+        for s in E.LandmarkStrategy:
+            exp = d[f"c{ci}_{s.value}"]
+            assert E.select_landmarks(g, len(exp), s).landmarks == tuple(exp.tolist())
+        for thr in (0, 2, 6):
+            ls = E.select_leaves(g, thr, k_prime=13, hash_seed=5)
+            np.testing.assert_array_equal(ls.flags, d[f"c{ci}_leaf_flags_t{thr}"])
+            m = ls.flags != 0
+            np.testing.assert_array_equal(ls.bucket_array[m], d[f"c{ci}_bucket_t{thr}"][m])
+
+
+# --------------------------------------------------------------- family --
+
+def test_family_build_and_all_pairs(family_golden):
+    d = family_golden
+    bits = {"default": FLAGSETS["default"], "bl_only": FLAGSETS["bl_only"], "bare": FLAGSETS["bare"]}
+    for i in range(int(d["count"])):
+        p = f"f{i}_"
+        g = graph_of(d, p)
+        k = int(d[p + "k"])
+        idx = E.build_index(g, E.IndexConfig(k=k, k_prime=k))
+        assert_meta(idx, d, p)
+        assert_labels(idx, d, p)
+        n = int(d[p + "n"])
+        qu = np.repeat(np.arange(n, dtype=np.uint32), n)
+        qv = np.tile(np.arange(n, dtype=np.uint32), n)
+        for name, fl in bits.items():
+            out, _ = E.query_batch(g, idx, (qu, qv), flags=fl)
+            np.testing.assert_array_equal(out.codes, d[p + f"codes_{name}"], err_msg=f"{i} {name}")
+            np.testing.assert_array_equal(out.visited == 0, d[p + f"visited_{name}"] == 0)
+
+
+def test_family_insert_sequence_exact_stats(family_golden):
+    d = family_golden
+    for i in range(int(d["count"])):
+        p = f"f{i}_"
+        g = graph_of(d, p)
+        k = int(d[p + "k"])
+        idx = E.build_index(g, E.IndexConfig(k=k, k_prime=k))
+        for j, (u, v) in enumerate(zip(d[p + "ins_u"], d[p + "ins_v"])):
+            st = E.insert_edge(g, idx, int(u), int(v))
+            e = d[p + "ins_stats"][j]
+            assert (st.visited, st.labels_changed, st.early_terminated) == \
+                (int(e[0]), int(e[1]), bool(e[2])), (i, j)
+        assert_labels(idx, d, p + "after_")
+        assert idx.labels_equal(E.rebuild_index(g, idx))
+
+
+def test_family_insert_batched(family_golden):
+    d = family_golden
+    for i in range(int(d["count"])):
+        p = f"f{i}_"
+        g = graph_of(d, p)
+        k = int(d[p + "k"])
+        idx = E.build_index(g, E.IndexConfig(k=k, k_prime=k))
+        st = E.insert_edges(g, idx, d[p + "ins_u"], d[p + "ins_v"])
+        assert st.inserted == len(d[p + "ins_u"])
+        assert_labels(idx, d, p + "after_")
+
+
+# ----------------------------------------------------------------- cfg1 --
+
+def test_cfg1_build_query_insert(cfg1_golden):
+    d = cfg1_golden
+    src, dst = W.gen_random_graph(10_000, 5, seed=1)
+    g = E.DynamicGraph.from_edges(10_000, src, dst)
+    assert g.edge_count == 50_000
+    idx = E.build_index(g)
+    assert_meta(idx, d)
+    assert_labels(idx, d)
+    out, st = E.query_batch(g, idx, (d["qu"], d["qv"]))
+    np.testing.assert_array_equal(out.codes, d["codes"])
+    assert st.rho == pytest.approx(float(np.mean(d["visited"] == 0)))
+    # batched insertion of the same 1000 edges == sequential reference result
+    g2 = E.DynamicGraph.from_edges(10_000, src, dst)
+    idx2 = E.build_index(g2)
+    E.insert_edges(g2, idx2, d["ins_u"], d["ins_v"])
+    assert_labels(idx2, d, "after_")
+    # sequential exact stats on the first 200
+    for j in range(200):
+        s1 = E.insert_edge(g, idx, int(d["ins_u"][j]), int(d["ins_v"][j]))
+        e = d["ins_stats"][j]
+        assert (s1.visited, s1.labels_changed, s1.early_terminated) == (int(e[0]), int(e[1]), bool(e[2])), j
+
+
+# ---------------------------------------------------- R-MAT vs the oracle --
+
+def rmat_case(scale, ef, seed):
+    src, dst = W.rmat_edges(scale, ef, seed)
+    n = 1 << scale
+    return n, src, dst
+
+
+@pytest.mark.parametrize("scale,ef", [(12, 8), (16, 8), (16, 2)])
+def test_rmat_build_and_queries_vs_oracle(scale, ef):
+    n, src, dst = rmat_case(scale, ef, 7)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    og = O.OracleGraph(n, src, dst)
+    assert g.edge_count == og.edge_count
+    idx = E.build_index(g)
+    oidx = og.build(64, 64, threads=8)
+    np.testing.assert_array_equal(np.array(idx.landmark_set.landmarks), oidx.landmarks)
+    np.testing.assert_array_equal(idx.leaf_sets.flags, oidx.leaf_flags)
+    assert_labels_equal_oracle(idx, oidx)
+    qu, qv = W.uniform_queries(n, 100_000, 3)
+    pu, pv = W.positive_queries(n, src, dst, 50_000, 4)
+    qu, qv = np.concatenate([qu, pu]), np.concatenate([qv, pv])
+    for fl in (E.QueryFlags(), E.QueryFlags(use_dl=False), E.QueryFlags(prune_dl=False, prune_bl=False)):
+        out, _ = E.query_batch(g, idx, (qu, qv), flags=fl)
+        oc, ov = og.query_batch(oidx, qu, qv, fl.bits(), threads=8)
+        np.testing.assert_array_equal(out.codes, oc)
+        np.testing.assert_array_equal(out.visited == 0, ov == 0)
+
+
+def test_rmat_insert_batches_vs_rebuild():
+    n, src, dst = rmat_case(16, 8, 11)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    og = O.OracleGraph(n, src, dst)
+    idx = E.build_index(g)
+    oidx = og.build(64, 64, threads=8)
+    prev = None
+    for b in range(3):
+        iu, iv = W.gen_insert_workload(src, dst, n, 2000, 100 + b, exclude=prev)
+        prev = (iu, iv) if prev is None else (np.concatenate([prev[0], iu]), np.concatenate([prev[1], iv]))
+        st = E.insert_edges(g, idx, iu, iv)
+        assert st.inserted == 2000
+        for u, v in zip(iu.tolist(), iv.tolist()):
+            og.insert_edge(oidx, u, v)
+        assert g.edge_count == og.edge_count
+        assert_labels_equal_oracle(idx, oidx)
+        assert idx.labels_equal(E.rebuild_index(g, idx))
+    qu, qv = W.uniform_queries(n, 100_000, 9)
+    out, _ = E.query_batch(g, idx, (qu, qv))
+    oc, _ = og.query_batch(oidx, qu, qv, threads=8)
+    np.testing.assert_array_equal(out.codes, oc)
+
+
+def test_dense_bfs_fallback_path():
+    # k = 0 and a single bucket: many BFS queries explore cones larger than the
+    # shared-memory table, exercising the dense re-run path.
+    src, dst = W.gen_random_graph(6000, 1.3, seed=5, acyclic=True)
+    g = E.DynamicGraph.from_edges(6000, src, dst)
+    og = O.OracleGraph(6000, src, dst)
+    idx = E.build_index(g, E.IndexConfig(k=0, k_prime=1))
+    oidx = og.build(0, 1)
+    assert_labels_equal_oracle(idx, oidx)
+    qu, qv = W.uniform_queries(6000, 20_000, 1)
+    for fl in (E.QueryFlags(), E.QueryFlags(use_bl=False), E.QueryFlags(prune_dl=False, prune_bl=False)):
+        out, _ = E.query_batch(g, idx, (qu, qv), flags=fl)
+        oc, _ = og.query_batch(oidx, qu, qv, fl.bits(), threads=8)
+        np.testing.assert_array_equal(out.codes, oc)
+
+
+def test_wide_labels_k256():
+    n, src, dst = rmat_case(14, 8, 21)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    og = O.OracleGraph(n, src, dst)
+    idx = E.build_index(g, E.IndexConfig(k=256, k_prime=64))
+    oidx = og.build(256, 64, threads=8)
+    assert_labels_equal_oracle(idx, oidx)
+    qu, qv = W.uniform_queries(n, 50_000, 2)
+    out, _ = E.query_batch(g, idx, (qu, qv))
+    oc, _ = og.query_batch(oidx, qu, qv, threads=8)
+    np.testing.assert_array_equal(out.codes, oc)
+    iu, iv = W.gen_insert_workload(src, dst, n, 500, 3)
+    E.insert_edges(g, idx, iu, iv)
+    for u, v in zip(iu.tolist(), iv.tolist()):
+        og.insert_edge(oidx, u, v)
+    assert_labels_equal_oracle(idx, oidx)
+
+
+def test_odd_widths_and_strategies():
+    src, dst = W.gen_random_graph(700, 3, seed=8)
+    g = E.DynamicGraph.from_edges(700, src, dst)
+    og = O.OracleGraph(700, src, dst)
+    for k, kp, strat, thr, seed in ((100, 96, "max", 0, 3), (0, 13, "sum", 2, 1), (640, 200, "min", 4, 9)):
+        cfg = E.IndexConfig(k=k, k_prime=kp, landmark_strategy=E.LandmarkStrategy(strat),
+                            leaf_threshold=thr, hash_seed=seed)
+        idx = E.build_index(g, cfg)
+        oidx = og.build(k, kp, strat, thr, seed, threads=4)
+        np.testing.assert_array_equal(np.array(idx.landmark_set.landmarks, np.uint32), oidx.landmarks)
+        assert_labels_equal_oracle(idx, oidx)
+        qu, qv = W.uniform_queries(700, 20_000, k)
+        out, _ = E.query_batch(g, idx, (qu, qv))
+        oc, _ = og.query_batch(oidx, qu, qv, threads=4)
+        np.testing.assert_array_equal(out.codes, oc)
+
+
+def test_empty_and_edge_cases():
+    g = E.DynamicGraph.from_edges(5, [], [])
+    idx = E.build_index(g, E.IndexConfig(k=5, k_prime=3))
+    out, st = E.query_batch(g, idx, [])
+    assert len(out) == 0 and st.query_count == 0
+    out, _ = E.query_batch(g, idx, [(0, 0), (1, 2)])
+    assert [o.answered_by for o in out] == [E.AnsweredBy.REFLEXIVE, E.AnsweredBy.BL_NEGATIVE]
+    # self-loops count toward degrees like the reference
+    g2 = E.DynamicGraph.from_edges(3, [0, 0, 1, 1], [0, 1, 2, 2])
+    assert g2.edge_count == 3
+    ind, outd = g2.degrees()
+    assert ind.tolist() == [1, 1, 1] and outd.tolist() == [2, 1, 0]
+    # insert_vertex grows graph and index together
+    g3 = E.DynamicGraph.from_edges(4, [0, 1, 2], [1, 2, 3])
+    idx3 = E.build_index(g3, E.IndexConfig(k=2, k_prime=2))
+    E.insert_vertex(g3, idx3, out_edges=[0], in_edges=[3])
+    assert g3.vertex_count == 5
+    assert E.query(g3, idx3, 3, 0).reachable
+    assert idx3.labels_equal(E.rebuild_index(g3, idx3))
+
+
+def test_graph_buffered_then_device_edges():
+    g = E.DynamicGraph(6)
+    assert g.add_edge(0, 1) and not g.add_edge(0, 1)
+    g.add_edge(1, 2)
+    idx = E.build_index(g, E.IndexConfig(k=2, k_prime=2))
+    assert g.edge_count == 2
+    assert g.add_edge(2, 3) and not g.add_edge(2, 3)
+    assert g.edge_count == 3 and g.has_edge(2, 3)
+    assert sorted(g.edges()) == [(0, 1), (1, 2), (2, 3)]
+    with pytest.raises(E.VertexRangeError):
+        g.add_edge(0, 6)
+    del idx
