@@ -150,6 +150,14 @@ dbl_status dbl_index_build(const dbl_graph *g, const dbl_config *cfg,
                            const uint32_t *bucket, const uint32_t *ovr_ids,
                            const uint32_t *ovr_buckets, uint32_t n_ovr,
                            dbl_index **out);
+/* Metadata selection (or pinning, as dbl_index_build) and label seeding
+ * only -- no propagation; pair with dbl_index_build_words for sharded
+ * builds. */
+dbl_status dbl_index_create(const dbl_graph *g, const dbl_config *cfg,
+                            const uint32_t *landmarks, const uint8_t *leaf_flags,
+                            const uint32_t *bucket, const uint32_t *ovr_ids,
+                            const uint32_t *ovr_buckets, uint32_t n_ovr,
+                            dbl_index **out);
 /* rebuild_index, labels.py:309-312: fresh build into `idx` reusing its
  * frozen metadata on the current graph. */
 dbl_status dbl_index_rebuild(const dbl_graph *g, dbl_index *idx);

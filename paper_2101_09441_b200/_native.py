@@ -51,6 +51,7 @@ _SIGS = {
     "dbl_select_landmarks": [P, u32, i32, P],
     "dbl_select_leaves": [P, u64, u32, u64, P, P, u32, P, P],
     "dbl_index_build": [P, ctypes.POINTER(Config), P, P, P, P, P, u32, ctypes.POINTER(P)],
+    "dbl_index_create": [P, ctypes.POINTER(Config), P, P, P, P, P, u32, ctypes.POINTER(P)],
     "dbl_index_rebuild": [P, P],
     "dbl_index_build_words": [P, P, P, u32],
     "dbl_index_free": [P],

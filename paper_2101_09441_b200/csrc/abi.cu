@@ -133,7 +133,7 @@ static dbl_status alloc_index(const dbl_graph *g, const dbl_config *cfg, dbl_ind
     idx->wdl = (cfg->k + 63) / 64;
     idx->wbl = (cfg->k_prime + 63) / 64;
     idx->rw = 2 * (idx->wdl + idx->wbl);
-    if (idx->wdl > 16 || idx->wbl > 16) {
+    if (idx->wdl > 16 || idx->wbl > 16 || idx->rw > 64) {
         delete idx;
         set_error("label widths above 1024 bits are not supported");
         return DBL_E_CONFIG;
@@ -148,7 +148,7 @@ static dbl_status alloc_index(const dbl_graph *g, const dbl_config *cfg, dbl_ind
     return DBL_OK;
 }
 
-extern "C" dbl_status dbl_index_build(const dbl_graph *gc, const dbl_config *cfg, const uint32_t *landmarks,
+static dbl_status index_create(const dbl_graph *gc, const dbl_config *cfg, const uint32_t *landmarks,
                                       const uint8_t *leaf_flags, const uint32_t *bucket,
                                       const uint32_t *ovr_ids, const uint32_t *ovr_buckets, uint32_t n_ovr,
                                       dbl_index **out) {
@@ -197,7 +197,29 @@ extern "C" dbl_status dbl_index_build(const dbl_graph *gc, const dbl_config *cfg
             if (s) return fail(s);
         }
     }
-    if ((s = run_build(g, idx, nullptr, 0))) return fail(s);
+    if ((s = index_seed_records(g, idx, ~0ull))) return fail(s);
+    *out = idx;
+    return DBL_OK;
+}
+
+extern "C" dbl_status dbl_index_create(const dbl_graph *gc, const dbl_config *cfg, const uint32_t *landmarks,
+                                       const uint8_t *leaf_flags, const uint32_t *bucket, const uint32_t *ovr_ids,
+                                       const uint32_t *ovr_buckets, uint32_t n_ovr, dbl_index **out) {
+    return index_create(gc, cfg, landmarks, leaf_flags, bucket, ovr_ids, ovr_buckets, n_ovr, out);
+}
+
+extern "C" dbl_status dbl_index_build(const dbl_graph *gc, const dbl_config *cfg, const uint32_t *landmarks,
+                                      const uint8_t *leaf_flags, const uint32_t *bucket,
+                                      const uint32_t *ovr_ids, const uint32_t *ovr_buckets, uint32_t n_ovr,
+                                      dbl_index **out) {
+    if (out) *out = nullptr;
+    dbl_index *idx = nullptr;
+    dbl_status s = index_create(gc, cfg, landmarks, leaf_flags, bucket, ovr_ids, ovr_buckets, n_ovr, &idx);
+    if (s) return s;
+    if ((s = run_build(const_cast<dbl_graph *>(gc), idx, nullptr, 0))) {
+        dbl_index_free(idx);
+        return s;
+    }
     *out = idx;
     return DBL_OK;
 }

@@ -272,11 +272,13 @@ __global__ void __launch_bounds__(FIX_THREADS) fixpoint_kernel(FixParams P) {
 // rec := seeds.  bl_in bit bucket[v] for source leaves, bl_out for sinks;
 // dl words zero (landmark bits are added by landmark_bits_kernel).
 __global__ void seed_records_kernel(uint64_t *__restrict__ rec, uint32_t n, uint32_t wdl, uint32_t wbl,
-                                    const uint8_t *__restrict__ flags, const uint32_t *__restrict__ bucket) {
+                                    const uint8_t *__restrict__ flags, const uint32_t *__restrict__ bucket,
+                                    uint64_t wmask) {
     const uint32_t rw = 2 * (wdl + wbl), H = wdl + wbl;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * rw;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = (uint32_t)(i / rw), w = (uint32_t)(i % rw);
+        if (!((wmask >> w) & 1)) continue;
         uint64_t val = 0;
         const uint32_t h = w < H ? 0 : 1, ww = w - h * H;
         if (ww >= wdl) {
@@ -291,11 +293,13 @@ __global__ void seed_records_kernel(uint64_t *__restrict__ rec, uint32_t n, uint
 }
 
 __global__ void landmark_bits_kernel(uint64_t *__restrict__ rec, uint32_t rw, uint32_t H,
-                                     const uint32_t *__restrict__ lm, uint32_t k) {
+                                     const uint32_t *__restrict__ lm, uint32_t k, uint64_t wmask) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
         const uint64_t v = lm[i];
-        atomicOr(reinterpret_cast<unsigned long long *>(rec + v * rw + i / 64), 1ull << (i % 64));
-        atomicOr(reinterpret_cast<unsigned long long *>(rec + v * rw + H + i / 64), 1ull << (i % 64));
+        if ((wmask >> (i / 64)) & 1)
+            atomicOr(reinterpret_cast<unsigned long long *>(rec + v * rw + i / 64), 1ull << (i % 64));
+        if ((wmask >> (H + i / 64)) & 1)
+            atomicOr(reinterpret_cast<unsigned long long *>(rec + v * rw + H + i / 64), 1ull << (i % 64));
     }
 }
 
@@ -517,16 +521,18 @@ static dbl_status finish_run(dbl_graph *g, Ctrl *hctrl) {
     return DBL_OK;
 }
 
-dbl_status index_seed_records(dbl_graph *g, dbl_index *idx) {
+dbl_status index_seed_records(dbl_graph *g, dbl_index *idx, uint64_t wmask) {
     const uint64_t total = (uint64_t)idx->n * idx->rw;
     if (!total) return DBL_OK;
     int blocks = (int)((total + 255) / 256 < (uint64_t)g->sm_count * 16 ? (total + 255) / 256 : g->sm_count * 16);
     seed_records_kernel<<<blocks, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, idx->wdl, idx->wbl,
-                                                       idx->leaf_flags.as<uint8_t>(), idx->bucket.as<uint32_t>());
+                                                       idx->leaf_flags.as<uint8_t>(), idx->bucket.as<uint32_t>(),
+                                                       wmask);
     DBL_CHECK_LAUNCH("seed_records_kernel");
     if (idx->cfg.k) {
         landmark_bits_kernel<<<(idx->cfg.k + 255) / 256, 256, 0, g->stream>>>(
-            idx->rec.as<uint64_t>(), idx->rw, idx->wdl + idx->wbl, idx->landmarks.as<uint32_t>(), idx->cfg.k);
+            idx->rec.as<uint64_t>(), idx->rw, idx->wdl + idx->wbl, idx->landmarks.as<uint32_t>(), idx->cfg.k,
+            wmask);
         DBL_CHECK_LAUNCH("landmark_bits_kernel");
     }
     return DBL_OK;
@@ -540,7 +546,12 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
     if (idx->wdl + idx->wbl > (uint32_t)MAX_SHARD_WORDS) { set_error("label width too large"); return DBL_E_CONFIG; }
     plan_groups(idx, words, nwords, groups, ng);
     DBL_CUDA(cudaEventRecord(g->ev[0], g->stream));
-    dbl_status s = index_seed_records(g, idx);
+    uint64_t wmask = ~0ull;
+    if (words) {
+        wmask = 0;
+        for (uint32_t i = 0; i < nwords; ++i) wmask |= 1ull << words[i];
+    }
+    dbl_status s = index_seed_records(g, idx, wmask);
     if (s) return s;
     // pair forward and backward groups of equal width into one launch
     bool used[2 * MAX_SHARD_WORDS + 4] = {};
@@ -676,7 +687,7 @@ dbl_status work_model(const dbl_index *idx, dbl_graph *g, uint64_t *V, uint64_t 
     tmp.landmarks.p = idx->landmarks.p;
     tmp.leaf_flags.p = idx->leaf_flags.p;
     tmp.bucket.p = idx->bucket.p;
-    s = index_seed_records(g, &tmp);
+    s = index_seed_records(g, &tmp, ~0ull);
     std::swap(tmp.rec, seeds);
     tmp.landmarks.p = tmp.leaf_flags.p = tmp.bucket.p = nullptr;
     if (s) { cleanup(); return s; }

@@ -564,6 +564,14 @@ extern "C" dbl_status dbl_stream(const dbl_graph *g, void **s) {
 
 extern "C" dbl_status dbl_last_timings(const dbl_graph *g, float *fix, float *label, float *bfs) {
     if (!g) { set_error("null graph"); return DBL_E_ARG; }
+    dbl_graph *gm = const_cast<dbl_graph *>(g);
+    // query kernels: events ev[2] -> ev[3] (K6) -> ev[4] (K7), read on demand
+    if (cudaEventQuery(g->ev[4]) == cudaSuccess || cudaEventSynchronize(g->ev[4]) == cudaSuccess) {
+        float a = 0, b = 0;
+        if (cudaEventElapsedTime(&a, g->ev[2], g->ev[3]) == cudaSuccess) gm->t_label = a;
+        if (cudaEventElapsedTime(&b, g->ev[3], g->ev[4]) == cudaSuccess) gm->t_bfs = b;
+    }
+    cudaGetLastError();
     if (fix) *fix = g->t_fix;
     if (label) *label = g->t_label;
     if (bfs) *bfs = g->t_bfs;

@@ -14,7 +14,7 @@ constexpr uint32_t CHUNK = 1024;          // max edges per frontier work item
 constexpr uint32_t DELTA_BIT = 0x80000000u;
 constexpr int FIX_THREADS = 256;
 constexpr int MAX_GROUP_WORDS = 8;        // words propagated together by one fixpoint
-constexpr int MAX_SHARD_WORDS = 64;
+constexpr int MAX_SHARD_WORDS = 32;  // words per record half (2 halves <= 64-bit word mask)
 
 // ---------------------------------------------------------------- errors --
 void set_error(const std::string &msg);
@@ -179,7 +179,7 @@ dbl_status select_leaves_dev(dbl_graph *g, uint64_t threshold, uint32_t k_prime,
 dbl_status leaf_hash_dev(const uint64_t *ids, uint64_t count, uint32_t k_prime, uint64_t seed,
                          uint32_t *out, cudaStream_t s);
 // fixpoint.cu
-dbl_status index_seed_records(dbl_graph *g, dbl_index *idx);
+dbl_status index_seed_records(dbl_graph *g, dbl_index *idx, uint64_t wmask);
 dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32_t nwords);
 dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, uint64_t count,
                       bool count_changes, uint32_t *changed_out, uint32_t *seed_changed,

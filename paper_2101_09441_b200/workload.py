@@ -98,8 +98,8 @@ def host_csr(n: int, src: np.ndarray, dst: np.ndarray) -> tuple[np.ndarray, np.n
     s = (key >> np.uint64(32)).astype(np.int64)
     col = (key & np.uint64(0xFFFFFFFF)).astype(np.uint32)
     ptr = np.zeros(n + 1, np.int64)
-    np.add.at(ptr, s + 1, 1)
-    return np.cumsum(ptr), col
+    ptr[1:] = np.cumsum(np.bincount(s, minlength=n))
+    return ptr, col
 
 
 def positive_queries(n: int, src: np.ndarray, dst: np.ndarray, count: int, seed: int,

@@ -379,3 +379,35 @@ def test_graph_buffered_then_device_edges():
     with pytest.raises(E.VertexRangeError):
         g.add_edge(0, 6)
     del idx
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_word_sharded_build_single_process(world):
+    """The sharded build's device pieces (dbl_index_create / build_words /
+    pack / unpack), with the allgather done in-process: every emulated rank
+    builds only its words into its own index; the exchanged tables must equal
+    a full build."""
+    import torch
+    from paper_2101_09441_b200.parallel import DeviceWordEngine, create_index, sharded_exchange
+    n, src, dst = rmat_case(13, 8, 5)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    full = E.build_index(g, E.IndexConfig(k=128, k_prime=64))
+    engines = [DeviceWordEngine(g, create_index(g, E.IndexConfig(k=128, k_prime=64))) for _ in range(world)]
+    from paper_2101_09441_b200.parallel import plan_words
+    plan = plan_words(engines[0].rw, world)
+    maxw = max(len(p) for p in plan)
+    slabs = []
+    for r, eng in enumerate(engines):
+        if plan[r]:
+            eng.build_words(plan[r])
+        s = eng.empty_slab(maxw)
+        if plan[r]:
+            eng.pack(plan[r], s)
+        slabs.append(s)
+    gathered = torch.cat(slabs)
+    per = maxw * n
+    for r, eng in enumerate(engines):
+        for p in range(world):
+            if p != r and plan[p]:
+                eng.unpack(plan[p], gathered[p * per:(p + 1) * per])
+        assert eng.idx.labels_equal(full), r
