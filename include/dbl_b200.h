@@ -99,6 +99,8 @@ const char *dbl_last_error(void);
 int dbl_version(void);
 /* number of kernels this process launched through the library */
 uint64_t dbl_kernel_launches(void);
+/* Return the library's cached device blocks to the driver (cudaFree). */
+dbl_status dbl_release_cached_memory(void);
 /* leaf_hash, labels.py:119-137, evaluated on the device for a batch */
 dbl_status dbl_leaf_hash(const uint64_t *ids, uint64_t count, uint32_t k_prime,
                          uint64_t seed, uint32_t *out_buckets, int device);
@@ -202,6 +204,9 @@ dbl_status dbl_query_async(const dbl_index *idx, const dbl_graph *g, const uint3
                            const uint32_t *v, uint64_t count, uint32_t flags,
                            uint8_t *codes, uint32_t *visited);
 dbl_status dbl_sync(const dbl_graph *g);
+/* Counters of the last query batch (8 x u32): [0] queries finished by the
+ * 64-query group kernel, [1] range-error flag, [3] groups re-run densely. */
+dbl_status dbl_query_counters(const dbl_graph *g, uint32_t *out8);
 /* The CUDA stream all work of `g` (and indexes built on it) runs on. */
 dbl_status dbl_stream(const dbl_graph *g, void **cuda_stream);
 

@@ -68,6 +68,8 @@ _SIGS = {
     "dbl_query": [P, P, P, P, u64, u32, P, P, i32],
     "dbl_query_async": [P, P, P, P, u64, u32, P, P],
     "dbl_sync": [P],
+    "dbl_query_counters": [P, P],
+    "dbl_release_cached_memory": [],
     "dbl_stream": [P, ctypes.POINTER(P)],
     "dbl_insert_edge": [P, P, u32, u32, ctypes.POINTER(UpdateStatsC)],
     "dbl_insert_edges": [P, P, P, P, u64, i32, ctypes.POINTER(BatchStatsC)],

@@ -4,7 +4,12 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -18,6 +23,105 @@ static uint64_t g_launches = 0;
 void set_error(const std::string &msg) { g_last_error = msg; }
 uint64_t &launch_counter() { return g_launches; }
 
+// ------------------------------------------------------ caching allocator --
+// Each cached block remembers the stream that last used it (the calling
+// thread's current engine stream, see set_stream); handing it to work on a
+// different stream first waits for that stream, so recycled memory is never
+// written while an earlier kernel may still read it.
+struct PoolBlock { void *p; cudaStream_t s; };
+static std::mutex g_pool_mu;
+static std::map<std::pair<int, size_t>, std::vector<PoolBlock>> g_pool;
+static thread_local cudaStream_t g_cur_stream = nullptr;
+
+void set_stream(cudaStream_t s) { g_cur_stream = s; }
+
+static size_t size_class(size_t n) {
+    if (n <= 4096) {
+        size_t c = 256;
+        while (c < n) c <<= 1;
+        return c;
+    }
+    size_t oct = 1;
+    while ((oct << 1) <= n) oct <<= 1;           // oct <= n < 2 oct
+    const size_t step = oct / 8;
+    return (n + step - 1) / step * step;
+}
+
+cudaError_t pool_alloc(void **p, size_t *bytes, int *device) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t c = size_class(*bytes);
+    PoolBlock blk{nullptr, nullptr};
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        auto it = g_pool.find({dev, c});
+        if (it != g_pool.end() && !it->second.empty()) {
+            auto &v = it->second;
+            size_t pick = v.size() - 1;
+            for (size_t i = 0; i < v.size(); ++i)
+                if (v[i].s == g_cur_stream && g_cur_stream) { pick = i; break; }
+            blk = v[pick];
+            v.erase(v.begin() + pick);
+        }
+    }
+    if (blk.p) {
+        if (blk.s != g_cur_stream || !blk.s) {
+            if (blk.s) cudaStreamSynchronize(blk.s); else cudaDeviceSynchronize();
+        }
+        *p = blk.p;
+        *bytes = c;
+        *device = dev;
+        return cudaSuccess;
+    }
+    cudaError_t e = cudaMalloc(p, c);
+    if (e == cudaErrorMemoryAllocation) {  // give cached blocks back and retry once
+        cudaGetLastError();
+        pool_trim();
+        e = cudaMalloc(p, c);
+    }
+    if (e != cudaSuccess) return e;
+    *bytes = c;
+    *device = dev;
+    return cudaSuccess;
+}
+
+void pool_forget_stream(cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (auto &kv : g_pool)
+        for (auto &b : kv.second)
+            if (b.s == st) b.s = nullptr;
+}
+
+void pool_free(void *p, size_t bytes, int device) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool[{device, bytes}].push_back(PoolBlock{p, g_cur_stream});
+}
+
+void pool_trim() {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto &kv : g_pool) {
+        cudaSetDevice(kv.first.first);
+        cudaDeviceSynchronize();
+        for (auto &b : kv.second) cudaFree(b.p);
+        kv.second.clear();
+    }
+    cudaSetDevice(cur);
+}
+
+static bool g_trace = std::getenv("DBL_TRACE") != nullptr;
+static auto g_trace_t0 = std::chrono::steady_clock::now();
+
+void trace(const char *what, cudaStream_t s) {
+    if (!g_trace) return;
+    cudaStreamSynchronize(s);
+    auto now = std::chrono::steady_clock::now();
+    double us = std::chrono::duration<double, std::micro>(now - g_trace_t0).count();
+    std::fprintf(stderr, "[dbl] %-28s +%9.1f us\n", what, us);
+    g_trace_t0 = std::chrono::steady_clock::now();
+}
+
 dbl_status cuda_fail(cudaError_t e, const char *what) {
     g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
     return e == cudaErrorMemoryAllocation ? DBL_E_OOM : DBL_E_CUDA;
@@ -26,6 +130,7 @@ dbl_status cuda_fail(cudaError_t e, const char *what) {
 dbl_status make_override(dbl_graph *g, const uint32_t *ids, const uint32_t *buckets, uint32_t cnt,
                          DevBuf &ovr);
 dbl_status query_finish(dbl_graph *g, uint32_t *err_out);
+dbl_status query_err_to(dbl_graph *g, uint32_t *dst);
 
 static int grid_for(uint64_t work, int threads = 256, int cap = 148 * 16) {
     uint64_t b = (work + threads - 1) / threads;
@@ -109,6 +214,10 @@ using namespace dbl;
 extern "C" const char *dbl_last_error(void) { return g_last_error.c_str(); }
 extern "C" int dbl_version(void) { return 1; }
 extern "C" uint64_t dbl_kernel_launches(void) { return g_launches; }
+extern "C" dbl_status dbl_release_cached_memory(void) {
+    pool_trim();
+    return DBL_OK;
+}
 
 static dbl_status check_pair(const dbl_index *idx, const dbl_graph *g) {
     if (!idx || !g) { set_error("null handle"); return DBL_E_ARG; }
@@ -151,11 +260,12 @@ static dbl_status alloc_index(const dbl_graph *g, const dbl_config *cfg, dbl_ind
 static dbl_status index_create(const dbl_graph *gc, const dbl_config *cfg, const uint32_t *landmarks,
                                       const uint8_t *leaf_flags, const uint32_t *bucket,
                                       const uint32_t *ovr_ids, const uint32_t *ovr_buckets, uint32_t n_ovr,
-                                      dbl_index **out) {
+                                      dbl_index **out, bool seed = true) {
     if (!gc || !cfg || !out) { set_error("null argument"); return DBL_E_ARG; }
     *out = nullptr;
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     if (landmarks && cfg->k) {  // LandmarkSet.of + _check_vertex (labels.py:59-63, 279-283)
         std::vector<uint32_t> seen(landmarks, landmarks + cfg->k);
         for (uint32_t i = 0; i < cfg->k; ++i)
@@ -170,8 +280,10 @@ static dbl_status index_create(const dbl_graph *gc, const dbl_config *cfg, const
         }
     }
     dbl_index *idx = nullptr;
+    trace("build: enter", g->stream);
     dbl_status s = alloc_index(g, cfg, &idx);
     if (s) return s;
+    trace("build: alloc", g->stream);
     auto fail = [&](dbl_status st) { dbl_index_free(idx); return st; };
     if (cfg->k) {
         if (landmarks) {
@@ -180,6 +292,7 @@ static dbl_status index_create(const dbl_graph *gc, const dbl_config *cfg, const
             return fail(s);
         }
     }
+    trace("build: landmarks", g->stream);
     if (g->n) {
         if (leaf_flags && bucket) {
             DBL_CUDA(cudaMemcpyAsync(idx->leaf_flags.p, leaf_flags, g->n, cudaMemcpyHostToDevice, g->stream));
@@ -197,7 +310,8 @@ static dbl_status index_create(const dbl_graph *gc, const dbl_config *cfg, const
             if (s) return fail(s);
         }
     }
-    if ((s = index_seed_records(g, idx, ~0ull))) return fail(s);
+    trace("build: leaves", g->stream);
+    if (seed && (s = index_seed_records(g, idx, ~0ull))) return fail(s);
     *out = idx;
     return DBL_OK;
 }
@@ -214,7 +328,7 @@ extern "C" dbl_status dbl_index_build(const dbl_graph *gc, const dbl_config *cfg
                                       dbl_index **out) {
     if (out) *out = nullptr;
     dbl_index *idx = nullptr;
-    dbl_status s = index_create(gc, cfg, landmarks, leaf_flags, bucket, ovr_ids, ovr_buckets, n_ovr, &idx);
+    dbl_status s = index_create(gc, cfg, landmarks, leaf_flags, bucket, ovr_ids, ovr_buckets, n_ovr, &idx, false);
     if (s) return s;
     if ((s = run_build(const_cast<dbl_graph *>(gc), idx, nullptr, 0))) {
         dbl_index_free(idx);
@@ -229,6 +343,7 @@ extern "C" dbl_status dbl_index_rebuild(const dbl_graph *gc, dbl_index *idx) {
     if (s) return s;
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     return run_build(g, idx, nullptr, 0);
 }
 
@@ -240,12 +355,14 @@ extern "C" dbl_status dbl_index_build_words(const dbl_graph *gc, dbl_index *idx,
         if (words[i] >= idx->rw) { set_error("record word out of range"); return DBL_E_ARG; }
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     return run_build(g, idx, words, nwords);
 }
 
 extern "C" dbl_status dbl_index_free(dbl_index *idx) {
     if (!idx) return DBL_OK;
     cudaSetDevice(idx->device);
+    set_stream(nullptr);
     cudaDeviceSynchronize();
     idx->rec.release();
     idx->landmarks.release();
@@ -266,6 +383,7 @@ extern "C" dbl_status dbl_index_metadata(const dbl_index *idx, uint32_t *landmar
                                          uint32_t *bucket) {
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(idx->device));
+    set_stream(nullptr);
     if (landmarks && idx->cfg.k) DBL_CUDA(cudaMemcpy(landmarks, idx->landmarks.p, (size_t)idx->cfg.k * 4, cudaMemcpyDeviceToHost));
     if (leaf_flags && idx->n) DBL_CUDA(cudaMemcpy(leaf_flags, idx->leaf_flags.p, idx->n, cudaMemcpyDeviceToHost));
     if (bucket && idx->n) DBL_CUDA(cudaMemcpy(bucket, idx->bucket.p, (size_t)idx->n * 4, cudaMemcpyDeviceToHost));
@@ -276,6 +394,7 @@ extern "C" dbl_status dbl_index_export(const dbl_index *idx, uint64_t *dl_in, ui
                                        uint64_t *bl_out) {
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(idx->device));
+    set_stream(nullptr);
     uint64_t *outs[4] = {dl_in, dl_out, bl_in, bl_out};
     DevBuf tmp;
     for (int f = 0; f < 4; ++f) {
@@ -299,6 +418,7 @@ extern "C" dbl_status dbl_index_import(dbl_index *idx, const uint64_t *dl_in, co
                                        const uint64_t *bl_in, const uint64_t *bl_out) {
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(idx->device));
+    set_stream(nullptr);
     const uint64_t *ins[4] = {dl_in, dl_out, bl_in, bl_out};
     DevBuf tmp;
     for (int f = 0; f < 4; ++f) {
@@ -326,6 +446,7 @@ extern "C" dbl_status dbl_index_equal(const dbl_index *a, const dbl_index *b, in
     if (a->n != b->n || a->cfg.k != b->cfg.k || a->cfg.k_prime != b->cfg.k_prime) return DBL_OK;
     if (a->device != b->device) { set_error("indexes live on different devices"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(a->device));
+    set_stream(nullptr);
     DevBuf flag;
     dbl_status s = flag.ensure(8);
     if (s) return s;
@@ -360,6 +481,7 @@ extern "C" dbl_status dbl_index_grow(dbl_index *idx, uint32_t n) {
     if (n < idx->n) { set_error("index cannot shrink"); return DBL_E_CONFIG; }
     if (n == idx->n) return DBL_OK;
     DBL_CUDA(cudaSetDevice(idx->device));
+    set_stream(nullptr);
     dbl_status s;
     if ((s = grow_buf(idx->rec, (size_t)idx->n * idx->rw * 8, (size_t)n * idx->rw * 8 + 16, 0)) ||
         (s = grow_buf(idx->leaf_flags, idx->n, (size_t)n + 16, 0)) ||
@@ -374,6 +496,7 @@ extern "C" dbl_status dbl_graph_add_vertices(dbl_graph *g, uint32_t count) {
     if (!count) return DBL_OK;
     if ((uint64_t)g->n + count >= 0xffffffffull) { set_error("vertex count overflow"); return DBL_E_CONFIG; }
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     DBL_CUDA(cudaStreamSynchronize(g->stream));
     const uint32_t n0 = g->n, n1 = n0 + count;
     DevBuf *ptrs[4] = {&g->fptr, &g->rptr, &g->dfptr, &g->drptr};
@@ -386,6 +509,7 @@ extern "C" dbl_status dbl_graph_add_vertices(dbl_graph *g, uint32_t count) {
     }
     DBL_CUDA(cudaDeviceSynchronize());
     g->n = n1;
+    ++g->topo_version;
     for (int d = 0; d < 2; ++d) g->stamp[d].release();
     g->changed_bits.release();
     return graph_ensure_traversal(g);
@@ -400,6 +524,58 @@ extern "C" dbl_status dbl_index_records(const dbl_index *idx, uint64_t **dev_rec
 
 // ---------------------------------------------------------------- queries --
 
+// Host-memory batches are pipelined in chunks: the H2D copy of chunk i+1
+// (copy stream), the query kernels of chunk i (engine stream) and the D2H copy
+// of chunk i-1 (second copy stream) overlap, so PCIe traffic in both
+// directions hides the device work.
+static dbl_status query_host_pipelined(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
+                                       uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited) {
+    dbl_status s;
+    const uint64_t cpad = (count + 63) & ~63ull;
+    if ((s = g->q_in.ensure(cpad * 8 + 64)) || (s = g->q_codes.ensure(count + 64)) ||
+        (visited && (s = g->q_vis.ensure(count * 4 + 64))) || (s = g->q_errs.ensure(64 * 4)))
+        return s;
+    if (!g->cstream[0]) {
+        DBL_CUDA(cudaStreamCreateWithFlags(&g->cstream[0], cudaStreamNonBlocking));
+        DBL_CUDA(cudaStreamCreateWithFlags(&g->cstream[1], cudaStreamNonBlocking));
+        for (auto &e : g->cev) DBL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const uint64_t target = 1ull << 18;
+    uint64_t nch = (count + target - 1) / target;
+    if (nch < 1) nch = 1;
+    if (nch > 16) nch = 16;
+    uint64_t csz = (count + nch - 1) / nch;
+    csz = (csz + 127) & ~127ull;
+    nch = (count + csz - 1) / csz;
+    uint32_t *bu = g->q_in.as<uint32_t>(), *bv = bu + cpad;
+    uint8_t *dc = g->q_codes.as<uint8_t>();
+    uint32_t *dvis = visited ? g->q_vis.as<uint32_t>() : nullptr;
+    uint32_t *errs = g->q_errs.as<uint32_t>();
+    DBL_CUDA(cudaMemsetAsync(errs, 0, 64 * 4, g->stream));
+    DBL_CUDA(cudaEventRecord(g->cev[32], g->stream));            // errs cleared
+    DBL_CUDA(cudaStreamWaitEvent(g->cstream[1], g->cev[32], 0));
+    for (uint64_t i = 0; i < nch; ++i) {
+        const uint64_t lo = i * csz, hi = lo + csz < count ? lo + csz : count, c = hi - lo;
+        DBL_CUDA(cudaMemcpyAsync(bu + lo, u + lo, c * 4, cudaMemcpyHostToDevice, g->cstream[0]));
+        DBL_CUDA(cudaMemcpyAsync(bv + lo, v + lo, c * 4, cudaMemcpyHostToDevice, g->cstream[0]));
+        DBL_CUDA(cudaEventRecord(g->cev[i], g->cstream[0]));
+        DBL_CUDA(cudaStreamWaitEvent(g->stream, g->cev[i], 0));
+        if ((s = run_query(idx, g, bu + lo, bv + lo, c, flags, dc + lo, dvis ? dvis + lo : nullptr))) return s;
+        if ((s = query_err_to(g, errs + i))) return s;
+        DBL_CUDA(cudaEventRecord(g->cev[16 + i], g->stream));
+        DBL_CUDA(cudaStreamWaitEvent(g->cstream[1], g->cev[16 + i], 0));
+        DBL_CUDA(cudaMemcpyAsync(codes + lo, dc + lo, c, cudaMemcpyDeviceToHost, g->cstream[1]));
+        if (visited) DBL_CUDA(cudaMemcpyAsync(visited + lo, dvis + lo, c * 4, cudaMemcpyDeviceToHost, g->cstream[1]));
+    }
+    uint32_t herr[64];
+    DBL_CUDA(cudaMemcpyAsync(herr, errs, 64 * 4, cudaMemcpyDeviceToHost, g->cstream[1]));
+    DBL_CUDA(cudaStreamSynchronize(g->cstream[1]));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    for (uint64_t i = 0; i < nch; ++i)
+        if (herr[i]) { set_error("query vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+    return DBL_OK;
+}
+
 static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const uint32_t *u, const uint32_t *v,
                              uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, dbl_mem mem,
                              bool sync) {
@@ -408,26 +584,9 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
     if (count && (!u || !v || !codes)) { set_error("null argument"); return DBL_E_ARG; }
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
-    const uint32_t *du = u, *dv = v;
-    uint8_t *dc = codes;
-    uint32_t *dvis = visited;
-    if (mem == DBL_MEM_HOST && count) {
-        if ((s = g->q_in.ensure(count * 8)) || (s = g->q_codes.ensure(count + 16)) ||
-            (visited && (s = g->q_vis.ensure(count * 4))))
-            return s;
-        uint32_t *bu = g->q_in.as<uint32_t>();
-        DBL_CUDA(cudaMemcpyAsync(bu, u, count * 4, cudaMemcpyHostToDevice, g->stream));
-        DBL_CUDA(cudaMemcpyAsync(bu + count, v, count * 4, cudaMemcpyHostToDevice, g->stream));
-        du = bu;
-        dv = bu + count;
-        dc = g->q_codes.as<uint8_t>();
-        dvis = visited ? g->q_vis.as<uint32_t>() : nullptr;
-    }
-    if ((s = run_query(idx, g, du, dv, count, flags, dc, dvis))) return s;
-    if (mem == DBL_MEM_HOST && count) {
-        DBL_CUDA(cudaMemcpyAsync(codes, dc, count, cudaMemcpyDeviceToHost, g->stream));
-        if (visited) DBL_CUDA(cudaMemcpyAsync(visited, dvis, count * 4, cudaMemcpyDeviceToHost, g->stream));
-    }
+    set_stream(g->stream);
+    if (mem == DBL_MEM_HOST && count) return query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
+    if ((s = run_query(idx, g, u, v, count, flags, codes, visited))) return s;
     if (!sync) return DBL_OK;
     uint32_t err = 0;
     if ((s = query_finish(g, &err))) return s;
@@ -476,6 +635,7 @@ extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, 
         return DBL_E_VERTEX_RANGE;
     }
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     dbl_update_stats st{};
     const uint64_t key = ((uint64_t)u << 32) | v;
     if ((s = g->scratch_b.ensure(64))) return s;
@@ -523,6 +683,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     if (!count) { if (stats) *stats = st; return DBL_OK; }
     if (!u || !v) { set_error("null argument"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     DevBuf in, keys, alt, newk, err;
     auto cleanup = [&]() { in.release(); keys.release(); alt.release(); newk.release(); err.release(); };
     if ((s = keys.ensure(count * 8)) || (s = alt.ensure(count * 8)) || (s = newk.ensure(count * 8)) ||
@@ -596,6 +757,7 @@ extern "C" dbl_status dbl_work_model(const dbl_index *idx, const dbl_graph *gc, 
     if (!V || !E || !levels) { set_error("null argument"); return DBL_E_ARG; }
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     return work_model(idx, g, V, E, levels);
 }
 
@@ -626,10 +788,12 @@ extern "C" dbl_status dbl_index_pack_words(const dbl_index *idx, const uint32_t 
     if (!idx || (nw && (!words || !dev_slab))) { set_error("null argument"); return DBL_E_ARG; }
     if (!nw || !idx->n) return DBL_OK;
     DBL_CUDA(cudaSetDevice(idx->device));
+    set_stream(nullptr);
     DevBuf w;
     dbl_status s = w.ensure(nw * 4);
     if (s) return s;
     cudaStream_t st = (cudaStream_t)stream;
+    set_stream(st);
     DBL_CUDA(cudaMemcpyAsync(w.p, words, nw * 4, cudaMemcpyHostToDevice, st));
     pack_words_kernel<<<grid_for((uint64_t)idx->n * nw), 256, 0, st>>>(idx->rec.as<uint64_t>(), idx->rw, idx->n,
                                                                        w.as<uint32_t>(), nw, dev_slab);
@@ -645,10 +809,12 @@ extern "C" dbl_status dbl_index_unpack_words(dbl_index *idx, const uint32_t *wor
     if (!idx || (nw && (!words || !dev_slab))) { set_error("null argument"); return DBL_E_ARG; }
     if (!nw || !idx->n) return DBL_OK;
     DBL_CUDA(cudaSetDevice(idx->device));
+    set_stream(nullptr);
     DevBuf w;
     dbl_status s = w.ensure(nw * 4);
     if (s) return s;
     cudaStream_t st = (cudaStream_t)stream;
+    set_stream(st);
     DBL_CUDA(cudaMemcpyAsync(w.p, words, nw * 4, cudaMemcpyHostToDevice, st));
     unpack_words_kernel<<<grid_for((uint64_t)idx->n * nw), 256, 0, st>>>(idx->rec.as<uint64_t>(), idx->rw, idx->n,
                                                                          w.as<uint32_t>(), nw, dev_slab);
@@ -669,6 +835,7 @@ extern "C" dbl_status dbl_graph_add_edges(dbl_graph *g, const uint32_t *u, const
     if (out_inserted) *out_inserted = 0;
     if (!count) return DBL_OK;
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     DevBuf in, keys, alt, newk, err;
     auto cleanup = [&]() { in.release(); keys.release(); alt.release(); newk.release(); err.release(); };
     dbl_status s;
@@ -738,6 +905,7 @@ extern "C" dbl_status dbl_label_tests(const dbl_index *idx, const uint32_t *x, c
     }
     if (!count) return DBL_OK;
     DBL_CUDA(cudaSetDevice(idx->device));
+    set_stream(nullptr);
     DevBuf b;
     dbl_status s = b.ensure(count * 10 + 16);
     if (s) return s;

@@ -11,15 +11,18 @@
 // B200 design: all bits of a record half propagate together.  The in-half
 // {dl_in, bl_in} (forward along CSR) and the out-half {dl_out, bl_out}
 // (backward along CSC) run in ONE persistent cooperative kernel, one grid
-// barrier per BFS level, no host round trip between levels.  Work items are
-// (vertex, edge range <= CHUNK) so hubs are split; warps take 32 items per
-// ticket, expand items of >= 32 edges warp-cooperatively and pack the
-// smaller ones with a warp scan (32 edges per step, owner lane by rank
-// select).  A relaxed edge reads the destination's words through L2 and
+// barrier per BFS level, no host round trip between levels.  Each level is
+// split into equal edge ranges, one per warp (work items carry their offset
+// in the level's edge space), so a hub's adjacency spreads over many warps
+// and every warp relaxes 32 consecutive edges per step regardless of the
+// degree mix.  A relaxed edge reads the destination's words through L2 and
 // issues atomicOr only for the missing bits; a vertex whose label grew is
 // stamped (one enqueue per level) and its edge ranges appended with a
 // warp-aggregated atomicAdd.
 #include <cooperative_groups.h>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -74,11 +77,13 @@ __device__ __forceinline__ int select_bit(uint32_t mask, uint32_t r) {
     return p;
 }
 
-// Append the edge ranges of every lane's vertex y (if p) to queue QN.
+// Append the adjacency segments of every lane's vertex y (if p) to queue QN:
+// one warp-aggregated 64-bit atomicAdd reserves both the item slots and the
+// edge-space offsets, so eoff stays monotone in the item index.
 __device__ __forceinline__ void warp_enqueue(const DirParams &D, const Queue &QN, bool p, uint32_t y,
-                                             uint32_t *cnt_ptr, Ctrl *ctrl) {
+                                             unsigned long long *cnt_ptr, Ctrl *ctrl) {
     const int lane = threadIdx.x & 31;
-    uint32_t b0 = 0, b1 = 0, d0 = 0, d1 = 0, ni = 0;
+    uint32_t b0 = 0, b1 = 0, d0 = 0, d1 = 0;
     if (p) {
         b0 = __ldg(D.adj.ptr + y);
         b1 = __ldg(D.adj.ptr + y + 1);
@@ -86,28 +91,28 @@ __device__ __forceinline__ void warp_enqueue(const DirParams &D, const Queue &QN
             d0 = __ldg(D.adj.dptr + y);
             d1 = __ldg(D.adj.dptr + y + 1);
         }
-        ni = (b1 - b0 + CHUNK - 1) / CHUNK + (d1 - d0 + CHUNK - 1) / CHUNK;
     }
-    const uint32_t incl = warp_incl_scan(ni);
-    const uint32_t tot = __shfl_sync(FULL, incl, 31);
-    if (tot == 0) return;
-    uint32_t pos0 = 0;
-    if (lane == 31) pos0 = atomicAdd(cnt_ptr, tot);
-    pos0 = __shfl_sync(FULL, pos0, 31);
-    if ((uint64_t)pos0 + tot > D.cap) {
+    const uint32_t ni = (b1 > b0) + (d1 > d0);
+    const uint32_t ne = (b1 - b0) + (d1 - d0);
+    const uint32_t ii = warp_incl_scan(ni), ei = warp_incl_scan(ne);
+    const uint32_t ti = __shfl_sync(FULL, ii, 31), te = __shfl_sync(FULL, ei, 31);
+    if (ti == 0) return;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(cnt_ptr, ((unsigned long long)ti << 32) | te);
+    base = __shfl_sync(FULL, base, 31);
+    const uint32_t ibase = (uint32_t)(base >> 32), ebase = (uint32_t)base;
+    if ((uint64_t)ibase + ti > D.cap) {
         if (lane == 0) atomicOr(&ctrl->overflow, 1u);
         return;
     }
-    uint32_t pos = pos0 + incl - ni;
-    for (uint32_t s = b0; s < b1; s += CHUNK, ++pos) {
-        QN.x[pos] = y;
-        QN.start[pos] = s;
-        QN.len[pos] = min(CHUNK, b1 - s);
+    uint32_t pos = ibase + ii - ni, eo = ebase + ei - ne;
+    if (b1 > b0) {
+        QN.x[pos] = y; QN.start[pos] = b0; QN.len[pos] = b1 - b0; QN.eoff[pos] = eo;
+        ++pos;
+        eo += b1 - b0;
     }
-    for (uint32_t s = d0; s < d1; s += CHUNK, ++pos) {
-        QN.x[pos] = y;
-        QN.start[pos] = s;
-        QN.len[pos] = min(CHUNK, d1 - s) | DELTA_BIT;
+    if (d1 > d0) {
+        QN.x[pos] = y; QN.start[pos] = d0; QN.len[pos] = (d1 - d0) | DELTA_BIT; QN.eoff[pos] = eo;
     }
 }
 
@@ -132,7 +137,7 @@ __device__ __forceinline__ bool relax(const DirParams &D, uint32_t y, const uint
 
 template <bool COUNT>
 __device__ __forceinline__ void push_changed(const DirParams &D, const Queue &QN, bool ch, uint32_t y,
-                                             uint32_t epoch, uint32_t *cnt_ptr, Ctrl *ctrl,
+                                             uint32_t epoch, unsigned long long *cnt_ptr, Ctrl *ctrl,
                                              uint32_t &nchanged) {
     if (!__any_sync(FULL, ch)) return;
     if (COUNT && ch) {
@@ -144,80 +149,185 @@ __device__ __forceinline__ void push_changed(const DirParams &D, const Queue &QN
     warp_enqueue(D, QN, p, y, cnt_ptr, ctrl);
 }
 
-// One warp expands up to 32 work items of queue Q.
-template <int NW, bool VEC, bool COUNT>
-__device__ __forceinline__ void expand_chunk(const DirParams &D, const Queue &Q, const Queue &QN,
-                                             uint32_t base, uint32_t cnt, uint32_t epoch,
-                                             uint32_t *next_cnt, Ctrl *ctrl, uint32_t &nchanged) {
+// Last item whose edge offset is <= e, searching [lo, nitems) 32-ary.
+__device__ __forceinline__ uint32_t find_item(const uint32_t *eoff, uint32_t lo, uint32_t nitems, uint32_t e) {
     const int lane = threadIdx.x & 31;
-    const uint32_t i = base + lane;
-    const bool valid = i < cnt;
-    uint32_t x = 0, start = 0, lenf = 0;
-    if (valid) {
-        x = ld_cg32(Q.x + i);
-        start = ld_cg32(Q.start + i);
-        lenf = ld_cg32(Q.len + i);
+    uint32_t hi = nitems;  // invariant: eoff[lo] <= e < eoff[hi] (eoff[nitems] = inf)
+    while (hi - lo > 1) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t idx = lo + lane * step;
+        const bool le = idx < hi && ld_cg32(eoff + idx) <= e;
+        const unsigned bal = __ballot_sync(FULL, le);
+        const uint32_t k = 31 - __clz(bal);
+        lo += k * step;
+        hi = min(hi, lo + step);
     }
-    const uint32_t len = lenf & ~DELTA_BIT;
-    const int dseg = (lenf & DELTA_BIT) ? 1 : 0;
-    uint64_t w[NW];
-    if (valid) {
-        load_words<NW, VEC>(D.lab + (size_t)x * D.stride, w);
-    } else {
-#pragma unroll
-        for (int k = 0; k < NW; ++k) w[k] = 0;
-    }
+    return lo;
+}
 
-    // items with >= 32 edges: whole warp, 32 edges per step
-    unsigned big = __ballot_sync(FULL, len >= 32);
-    while (big) {
-        const int j = __ffs(big) - 1;
-        big &= big - 1;
-        const uint32_t js = __shfl_sync(FULL, start, j);
-        const uint32_t jl = __shfl_sync(FULL, len, j);
-        const uint32_t *col = __shfl_sync(FULL, dseg, j) ? D.adj.dcol : D.adj.col;
-        uint64_t jw[NW];
+__device__ __forceinline__ void red_or(uint64_t *p, uint64_t v) {
+    asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Enqueue up to U vertices per lane (ys[r] where ps[r]) with one scan and one
+// 64-bit atomicAdd per warp.
+template <int U>
+__device__ __forceinline__ void warp_enqueue_multi(const DirParams &D, const Queue &QN, const bool (&ps)[U],
+                                                   const uint32_t (&ys)[U], unsigned long long *cnt_ptr,
+                                                   Ctrl *ctrl) {
+    const int lane = threadIdx.x & 31;
+    uint32_t b0[U], b1[U], d0[U], d1[U];
+    uint32_t ni = 0, ne = 0;
 #pragma unroll
-        for (int k = 0; k < NW; ++k) jw[k] = __shfl_sync(FULL, w[k], j);
-        for (uint32_t e0 = 0; e0 < jl; e0 += 32) {
-            const uint32_t e = e0 + lane;
-            uint32_t y = 0;
-            bool ch = false;
-            if (e < jl) {
-                y = __ldg(col + js + e);
-                ch = relax<NW, VEC>(D, y, jw);
+    for (int r = 0; r < U; ++r) {
+        b0[r] = b1[r] = d0[r] = d1[r] = 0;
+        if (ps[r]) {
+            b0[r] = __ldg(D.adj.ptr + ys[r]);
+            b1[r] = __ldg(D.adj.ptr + ys[r] + 1);
+            if (D.adj.dptr) {
+                d0[r] = __ldg(D.adj.dptr + ys[r]);
+                d1[r] = __ldg(D.adj.dptr + ys[r] + 1);
             }
-            push_changed<COUNT>(D, QN, ch, y, epoch, next_cnt, ctrl, nchanged);
+        }
+        ni += (b1[r] > b0[r]) + (d1[r] > d0[r]);
+        ne += (b1[r] - b0[r]) + (d1[r] - d0[r]);
+    }
+    const uint32_t ii = warp_incl_scan(ni), ei = warp_incl_scan(ne);
+    const uint32_t ti = __shfl_sync(FULL, ii, 31), te = __shfl_sync(FULL, ei, 31);
+    if (ti == 0) return;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(cnt_ptr, ((unsigned long long)ti << 32) | te);
+    base = __shfl_sync(FULL, base, 31);
+    const uint32_t ibase = (uint32_t)(base >> 32), ebase = (uint32_t)base;
+    if ((uint64_t)ibase + ti > D.cap) {
+        if (lane == 0) atomicOr(&ctrl->overflow, 1u);
+        return;
+    }
+    uint32_t pos = ibase + ii - ni, eo = ebase + ei - ne;
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+        if (b1[r] > b0[r]) {
+            QN.x[pos] = ys[r]; QN.start[pos] = b0[r]; QN.len[pos] = b1[r] - b0[r]; QN.eoff[pos] = eo;
+            ++pos;
+            eo += b1[r] - b0[r];
+        }
+        if (d1[r] > d0[r]) {
+            QN.x[pos] = ys[r]; QN.start[pos] = d0[r]; QN.len[pos] = (d1[r] - d0[r]) | DELTA_BIT;
+            QN.eoff[pos] = eo;
+            ++pos;
+            eo += d1[r] - d0[r];
         }
     }
+}
 
-    // items with < 32 edges: concatenate, 32 edges per step
-    const uint32_t sl = len < 32 ? len : 0;
-    const uint32_t incl = warp_incl_scan(sl);
-    const uint32_t total = __shfl_sync(FULL, incl, 31);
-    const uint32_t excl = incl - sl;
-    const unsigned nz = __ballot_sync(FULL, sl > 0);
-    for (uint32_t b = 0; b < total; b += 32) {
-        const unsigned hw = __reduce_or_sync(FULL, (sl > 0 && (excl >> 5) == (b >> 5)) ? (1u << (excl & 31)) : 0u);
-        const uint32_t before = __popc(__ballot_sync(FULL, sl > 0 && excl < b));
-        const uint32_t j = b + lane;
-        const bool ok = j < total;
-        int owner = 0;
-        if (ok) owner = select_bit(nz, before + __popc(hw & (FULL >> (31 - lane))) - 1);
-        const uint32_t os = __shfl_sync(FULL, start, owner);
-        const uint32_t oe = __shfl_sync(FULL, excl, owner);
-        const int od = __shfl_sync(FULL, dseg, owner);
-        uint64_t ow[NW];
+// One warp relaxes the edges [e0, e1) of a level's edge space, U rounds of
+// 32 consecutive edges at a time: each lane finds its item in a 32-item
+// window by a 5-step shuffle search (the window slides forward as edges are
+// consumed), then the U column loads, the U destination-label loads and the
+// fire-and-forget atomic ORs of the U rounds are issued back to back so their
+// latencies overlap.  A destination whose (L2-coherent) read lacked bits is
+// pushed: if another thread supplied the bits first the vertex is merely
+// re-expanded once with nothing new, which keeps the fixpoint exact.
+template <int NW, bool VEC, bool COUNT>
+__device__ __forceinline__ void expand_range(const DirParams &D, const Queue &Q, const Queue &QN,
+                                             uint32_t nitems, uint32_t e0, uint32_t e1, uint32_t epoch,
+                                             unsigned long long *next_cnt, Ctrl *ctrl, uint32_t &nchanged) {
+    constexpr int U = NW <= 2 ? 4 : (NW <= 4 ? 2 : 1);
+    const int lane = threadIdx.x & 31;
+    uint32_t i0 = find_item(Q.eoff, 0, nitems, e0);
+    uint32_t wE = 0xffffffffu, wS = 0, wEnd = 0, winEnd = 0;
+    int wD = 0;
+    uint64_t w[NW];
+    auto load_window = [&](uint32_t first) {
+        const uint32_t i = first + lane;
+        if (i < nitems) {
+            wE = ld_cg32(Q.eoff + i);
+            wS = ld_cg32(Q.start + i);
+            const uint32_t lf = ld_cg32(Q.len + i);
+            const uint32_t x = ld_cg32(Q.x + i);
+            wD = (lf & DELTA_BIT) ? 1 : 0;
+            wEnd = wE + (lf & ~DELTA_BIT);
+            load_words<NW, VEC>(D.lab + (size_t)x * D.stride, w);
+        } else {
+            wE = 0xffffffffu;
+            wEnd = 0;
 #pragma unroll
-        for (int k = 0; k < NW; ++k) ow[k] = __shfl_sync(FULL, w[k], owner);
-        uint32_t y = 0;
-        bool ch = false;
-        if (ok) {
-            const uint32_t *col = od ? D.adj.dcol : D.adj.col;
-            y = __ldg(col + os + (j - oe));
-            ch = relax<NW, VEC>(D, y, ow);
+            for (int k = 0; k < NW; ++k) w[k] = 0;
         }
-        push_changed<COUNT>(D, QN, ch, y, epoch, next_cnt, ctrl, nchanged);
+        const unsigned valid = __ballot_sync(FULL, i < nitems);
+        winEnd = __shfl_sync(FULL, wEnd, 31 - __clz(valid));
+    };
+    load_window(i0);
+    for (uint32_t e = e0; e < e1; e += 32 * U) {
+        uint32_t ys[U];
+        bool ok[U];
+        uint64_t src[U][NW];
+#pragma unroll
+        for (int r = 0; r < U; ++r) {
+            const uint32_t er = e + 32 * r;
+            ok[r] = false;
+            ys[r] = 0;
+#pragma unroll
+            for (int j = 0; j < NW; ++j) src[r][j] = 0;
+            if (er >= e1) continue;  // warp-uniform
+            const uint32_t last = min(er + 31, e1 - 1);
+            if (last >= winEnd) {
+                if (er < winEnd) {
+                    const unsigned bal = __ballot_sync(FULL, wE <= er);
+                    i0 += 31 - __clz(bal);
+                } else {
+                    i0 = find_item(Q.eoff, i0, nitems, er);
+                }
+                load_window(i0);
+            }
+            const uint32_t ei = er + lane;
+            int k = 0;
+#pragma unroll
+            for (int st = 16; st >= 1; st >>= 1) {
+                const uint32_t v = __shfl_sync(FULL, wE, (k + st) & 31);
+                if (k + st < 32 && v <= ei) k += st;
+            }
+            const uint32_t os = __shfl_sync(FULL, wS, k);
+            const uint32_t oe = __shfl_sync(FULL, wE, k);
+            const int od = __shfl_sync(FULL, wD, k);
+#pragma unroll
+            for (int j = 0; j < NW; ++j) src[r][j] = __shfl_sync(FULL, w[j], k);
+            if (ei < e1) {
+                ok[r] = true;
+                ys[r] = __ldg((od ? D.adj.dcol : D.adj.col) + os + (ei - oe));
+            }
+        }
+        uint64_t cur[U][NW];
+#pragma unroll
+        for (int r = 0; r < U; ++r)
+            if (ok[r]) load_words<NW, VEC>(D.lab + (size_t)ys[r] * D.stride, cur[r]);
+        bool ps[U];
+        bool any = false;
+#pragma unroll
+        for (int r = 0; r < U; ++r) {
+            bool ch = false;
+            if (ok[r]) {
+                uint64_t *p = D.lab + (size_t)ys[r] * D.stride;
+#pragma unroll
+                for (int j = 0; j < NW; ++j) {
+                    const uint64_t need = src[r][j] & ~cur[r][j];
+                    if (need) { red_or(p + j, need); ch = true; }
+                }
+            }
+            ps[r] = ch;
+            any |= ch;
+        }
+        if (!__any_sync(FULL, any)) continue;
+#pragma unroll
+        for (int r = 0; r < U; ++r) {
+            if (COUNT && ps[r]) {
+                const uint32_t bit = 1u << (ys[r] & 31);
+                const uint32_t old = atomicOr(&D.changed_bits[ys[r] >> 5], bit);
+                if (!(old & bit)) ++nchanged;
+            }
+            if (ps[r]) ps[r] = ld_cg32(D.stamp + ys[r]) != epoch && atomicExch(&D.stamp[ys[r]], epoch) != epoch;
+        }
+        warp_enqueue_multi<U>(D, QN, ps, ys, next_cnt, ctrl);
     }
 }
 
@@ -225,34 +335,44 @@ template <int NW, bool VEC, bool COUNT>
 __global__ void __launch_bounds__(FIX_THREADS) fixpoint_kernel(FixParams P) {
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     Ctrl *ctrl = P.ctrl;
     uint32_t nchanged[2] = {0, 0};
     for (uint32_t L = 0; L < P.max_levels; ++L) {
         const int c3 = L % 3, n3 = (L + 1) % 3, r3 = (L + 2) % 3;
-        const uint32_t c0 = *(volatile uint32_t *)&ctrl->cnt[c3][0];
-        const uint32_t c1 = *(volatile uint32_t *)&ctrl->cnt[c3][1];
-        if ((c0 | c1) == 0) {
+        const unsigned long long q0 = *(volatile unsigned long long *)&ctrl->cnt[c3][0];
+        const unsigned long long q1 = *(volatile unsigned long long *)&ctrl->cnt[c3][1];
+        if ((q0 | q1) == 0) {
             if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->levels = L;
             break;
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             ctrl->cnt[r3][0] = 0;
             ctrl->cnt[r3][1] = 0;
-            ctrl->work[r3] = 0;
         }
-        const uint32_t ch0 = (c0 + 31) / 32, tot = ch0 + (c1 + 31) / 32;
+        const uint32_t n0 = (uint32_t)(q0 >> 32), E0 = (uint32_t)q0;
+        const uint32_t n1 = (uint32_t)(q1 >> 32), E1 = (uint32_t)q1;
+        const uint64_t total = (uint64_t)E0 + E1;
+        // equal edge ranges per warp (multiple of 32)
+        uint64_t per = (total + nwarps - 1) / nwarps;
+        per = (per + 31) & ~31ull;
+        const uint64_t a = (uint64_t)warp * per, b = (a + per < total) ? a + per : total;
         const int par = L & 1;
         const uint32_t epoch = P.epoch0 + L + 1;
-        for (;;) {
-            uint32_t t = 0;
-            if (lane == 0) t = atomicAdd(&ctrl->work[c3], 1u);
-            t = __shfl_sync(FULL, t, 0);
-            if (t >= tot) break;
-            const int dir = t < ch0 ? 0 : 1;
-            const uint32_t base = (dir == 0 ? t : t - ch0) * 32;
-            const DirParams &D = P.d[dir];
-            expand_chunk<NW, VEC, COUNT>(D, D.q[par], D.q[par ^ 1], base, dir == 0 ? c0 : c1, epoch,
-                                         &ctrl->cnt[n3][dir], ctrl, nchanged[dir]);
+        if (a < b) {
+            if (a < E0) {
+                const DirParams &D = P.d[0];
+                expand_range<NW, VEC, COUNT>(D, D.q[par], D.q[par ^ 1], n0, (uint32_t)a,
+                                             (uint32_t)(b < E0 ? b : (uint64_t)E0), epoch, &ctrl->cnt[n3][0], ctrl,
+                                             nchanged[0]);
+            }
+            if (b > E0) {
+                const DirParams &D = P.d[1];
+                const uint32_t s = a > E0 ? (uint32_t)(a - E0) : 0u;
+                expand_range<NW, VEC, COUNT>(D, D.q[par], D.q[par ^ 1], n1, s, (uint32_t)(b - E0), epoch,
+                                             &ctrl->cnt[n3][1], ctrl, nchanged[1]);
+            }
         }
         grid.sync();
     }
@@ -494,6 +614,7 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
             D.q[p].x = b;
             D.q[p].start = b + g->qcap;
             D.q[p].len = b + 2ull * g->qcap;
+            D.q[p].eoff = b + 3ull * g->qcap;
         }
         D.changed_bits = count ? g->changed_bits.as<uint32_t>() + d * (((size_t)g->n + 31) / 32) : nullptr;
         if (gr[d]) {
@@ -553,6 +674,7 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
     }
     dbl_status s = index_seed_records(g, idx, wmask);
     if (s) return s;
+    trace("build: seed", g->stream);
     // pair forward and backward groups of equal width into one launch
     bool used[2 * MAX_SHARD_WORDS + 4] = {};
     for (int i = 0; i < ng; ++i) {
@@ -573,9 +695,12 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
         if ((s = prepare_params(g, idx, pair, P, nw, vec, false))) return s;
         const uint32_t mask = (pair[0] ? 1u : 0u) | (pair[1] ? 2u : 0u);
         if ((s = launch_init_frontier(g, P, nw, mask))) return s;
+        trace("build: init frontier", g->stream);
         if ((s = launch_fixpoint<false>(g, P, nw, vec))) return s;
         Ctrl h{};
         if ((s = finish_run(g, &h))) return s;
+        trace("build: fixpoint", g->stream);
+        if (std::getenv("DBL_TRACE")) std::fprintf(stderr, "[dbl] fixpoint levels=%u nw=%u\n", h.levels, nw);
     }
     DBL_CUDA(cudaEventRecord(g->ev[1], g->stream));
     DBL_CUDA(cudaEventSynchronize(g->ev[1]));

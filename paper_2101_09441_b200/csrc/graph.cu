@@ -185,11 +185,10 @@ dbl_status graph_degrees_dev(const dbl_graph *g, uint32_t *indeg, uint32_t *outd
 }
 
 // Traversal workspace: per-direction stamps and level-parity queues sized
-// for the worst case of one level: every vertex enqueued once, split into
-// CHUNK-edge items (<= 2n + m/CHUNK items).
+// for the worst case of one level: every vertex enqueued once, one item per
+// nonempty adjacency segment (<= 2n items).
 dbl_status graph_ensure_traversal(dbl_graph *g) {
-    uint64_t m = g->m_base + g->m_delta;
-    uint64_t cap = 2ull * g->n + m / CHUNK + 64;
+    uint64_t cap = 2ull * g->n + 64;
     if (cap > 0xffffffffull) { set_error("frontier capacity overflow"); return DBL_E_CONFIG; }
     dbl_status s;
     for (int d = 0; d < 2; ++d) {
@@ -203,7 +202,7 @@ dbl_status graph_ensure_traversal(dbl_graph *g) {
             if (g->stamp[other].p) DBL_CUDA(cudaMemsetAsync(g->stamp[other].p, 0, g->stamp[other].bytes, g->stream));
         }
         for (int p = 0; p < 2; ++p)
-            if ((s = g->qbuf[d][p].ensure(cap * 12))) return s;
+            if ((s = g->qbuf[d][p].ensure(cap * 16))) return s;
     }
     g->qcap = (uint32_t)cap;
     if ((s = g->ctrl.ensure(sizeof(Ctrl)))) return s;
@@ -322,6 +321,7 @@ dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t
                                    g->drcol.as<uint32_t>())))
         return s;
     g->m_delta = m;
+    ++g->topo_version;
     return graph_ensure_traversal(g);
 }
 
@@ -358,6 +358,7 @@ dbl_status graph_compact(dbl_graph *g) {
     s = build_base(g, a.as<uint64_t>(), b.as<uint64_t>(), m);
     a.release();
     b.release();
+    ++g->topo_version;
     if (s) return s;
     return graph_ensure_traversal(g);
 }
@@ -372,12 +373,14 @@ extern "C" dbl_status dbl_graph_create(uint32_t n, const uint32_t *src, const ui
     if (!out || (m && (!src || !dst))) { set_error("null argument"); return DBL_E_ARG; }
     *out = nullptr;
     DBL_CUDA(cudaSetDevice(device));
+    set_stream(nullptr);
     dbl_graph *g = new dbl_graph();
     g->device = device;
     g->n = n;
     auto fail = [&](dbl_status s) { dbl_graph_free(g); return s; };
     cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate"));
+    set_stream(g->stream);
     for (auto &ev : g->ev) {
         e = cudaEventCreate(&ev);
         if (e != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
@@ -429,6 +432,7 @@ extern "C" dbl_status dbl_graph_create(uint32_t n, const uint32_t *src, const ui
 extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
     if (!g) return DBL_OK;
     cudaSetDevice(g->device);
+    set_stream(g->stream);
     if (g->stream) cudaStreamSynchronize(g->stream);
     DevBuf *bufs[] = {&g->fptr, &g->fcol, &g->rptr, &g->rcol, &g->dfptr, &g->dfcol, &g->drptr,
                       &g->drcol, &g->dkeys_f, &g->dkeys_r, &g->stamp[0], &g->stamp[1],
@@ -436,7 +440,15 @@ extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
                       &g->changed_bits, &g->cub_tmp, &g->scratch_a, &g->scratch_b, &g->scratch_c,
                       &g->scratch_d, &g->q_in, &g->q_codes, &g->q_vis, &g->q_pending,
                       &g->q_counters, &g->q_dense};
+    if (g->q_exec) cudaGraphExecDestroy(g->q_exec);
+    if (g->q_graph) cudaGraphDestroy(g->q_graph);
+    set_stream(nullptr);
     for (auto *b : bufs) b->release();
+    g->q_desc.release();
+    g->q_errs.release();
+    for (auto &e : g->cev) if (e) cudaEventDestroy(e);
+    for (auto &cs : g->cstream) if (cs) { cudaStreamSynchronize(cs); pool_forget_stream(cs); cudaStreamDestroy(cs); }
+    pool_forget_stream(g->stream);
     g->host_stage.release();
     for (auto &ev : g->ev) if (ev) cudaEventDestroy(ev);
     if (g->stream) cudaStreamDestroy(g->stream);
@@ -454,6 +466,7 @@ extern "C" dbl_status dbl_graph_info(const dbl_graph *g, uint32_t *n, uint64_t *
 extern "C" dbl_status dbl_graph_degrees(const dbl_graph *g, uint32_t *indeg, uint32_t *outdeg) {
     if (!g || !indeg || !outdeg) { set_error("null argument"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     dbl_graph *gm = const_cast<dbl_graph *>(g);
     dbl_status s = gm->scratch_a.ensure(((size_t)g->n + 1) * 8);
     if (s) return s;
@@ -484,6 +497,7 @@ extern "C" dbl_status dbl_graph_has_edges(const dbl_graph *g, const uint32_t *u,
     if (!g || (count && (!u || !v || !out))) { set_error("null argument"); return DBL_E_ARG; }
     if (!count) return DBL_OK;
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     DevBuf b;
     dbl_status s = b.ensure(count * 9 + 16);
     if (s) return s;
@@ -524,6 +538,7 @@ extern "C" dbl_status dbl_graph_edges(const dbl_graph *g, uint32_t *src, uint32_
     if (!m) return DBL_OK;
     if (!src || !dst) { set_error("null argument"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     dbl_graph *gm = const_cast<dbl_graph *>(g);
     DevBuf a, b;
     dbl_status s;

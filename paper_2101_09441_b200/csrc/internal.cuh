@@ -10,7 +10,6 @@
 namespace dbl {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr uint32_t CHUNK = 1024;          // max edges per frontier work item
 constexpr uint32_t DELTA_BIT = 0x80000000u;
 constexpr int FIX_THREADS = 256;
 constexpr int MAX_GROUP_WORDS = 8;        // words propagated together by one fixpoint
@@ -34,23 +33,33 @@ uint64_t &launch_counter();
         if (_e != cudaSuccess) return ::dbl::cuda_fail(_e, what);              \
     } while (0)
 
-// grow-only device buffer
+// Caching device allocator (abi.cu): size classes of 1/8 octave, blocks are
+// recycled instead of cudaFree'd, so per-call workspaces cost no
+// cudaMalloc/cudaFree synchronisation after warm-up.
+cudaError_t pool_alloc(void **p, size_t *bytes, int *device);
+void pool_free(void *p, size_t bytes, int device);
+void pool_trim();
+void set_stream(cudaStream_t s);  // stream that subsequent pool traffic belongs to
+void pool_forget_stream(cudaStream_t s);  // before a stream is destroyed
+// Debug phase timer: DBL_TRACE=1 prints host-side phase times to stderr.
+void trace(const char *what, cudaStream_t s);
+
+// grow-only device buffer backed by the caching allocator
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
+    int dev = 0;
     dbl_status ensure(size_t need) {
         if (need <= bytes) return DBL_OK;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
+        release();
         size_t nb = need < 256 ? 256 : need;
-        cudaError_t e = cudaMalloc(&p, nb);
-        if (e != cudaSuccess) { cudaGetLastError(); return cuda_fail(e, "cudaMalloc(workspace)"); }
+        cudaError_t e = pool_alloc(&p, &nb, &dev);
+        if (e != cudaSuccess) { cudaGetLastError(); p = nullptr; return cuda_fail(e, "cudaMalloc(workspace)"); }
         bytes = nb;
         return DBL_OK;
     }
     template <class T> T *as() const { return reinterpret_cast<T *>(p); }
-    void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+    void release() { if (p) pool_free(p, bytes, dev); p = nullptr; bytes = 0; }
 };
 
 // Pinned host staging buffer (grow-only).
@@ -78,17 +87,20 @@ struct Adj {
     const uint32_t *dcol;
 };
 
-// Frontier work items: (vertex, first edge, length | DELTA_BIT).
+// Frontier work items: one per nonempty adjacency segment of a frontier
+// vertex: (vertex, first edge, length | DELTA_BIT, offset of its first edge
+// in the level's edge space).  eoff is monotone in the item index, so warps
+// can split a level into equal edge ranges and binary-search their items.
 struct Queue {
     uint32_t *x;
     uint32_t *start;
     uint32_t *len;
+    uint32_t *eoff;
 };
 
 // Device control block of one fixpoint run.
 struct Ctrl {
-    uint32_t cnt[3][2];      // items per [level % 3][direction]
-    uint32_t work[3];        // warp-chunk tickets per level % 3
+    unsigned long long cnt[3][2];   // (items << 32 | edges) per [level % 3][direction]
     uint32_t levels;
     uint32_t overflow;
     uint32_t seed_changed[2];
@@ -139,7 +151,15 @@ struct dbl_graph {
     dbl::DevBuf cub_tmp, scratch_a, scratch_b, scratch_c, scratch_d;
     dbl::HostBuf host_stage;
     // query workspace
-    dbl::DevBuf q_in, q_codes, q_vis, q_pending, q_counters, q_dense;
+    dbl::DevBuf q_in, q_codes, q_vis, q_pending, q_counters, q_dense, q_desc, q_errs;
+    cudaStream_t cstream[2] = {nullptr, nullptr};   // H2D / D2H copy streams
+    cudaEvent_t cev[33] = {};
+    uint64_t q_pending_cap = 0;
+    cudaGraph_t q_graph = nullptr;       // reusable query launch graph
+    cudaGraphExec_t q_exec = nullptr;
+    const void *q_key[6] = {};
+    uint64_t q_topo = 0;
+    uint64_t topo_version = 0;           // bumped whenever adjacency buffers change
     int sm_count = 148;
     int coop_blocks = 0;      // co-resident blocks for the fixpoint kernel
     cudaEvent_t ev[6] = {};

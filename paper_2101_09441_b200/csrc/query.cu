@@ -22,11 +22,14 @@
 // 64 queries' DL/BL words staged in shared memory.  A group whose BFS
 // outgrows the table is re-run by the dense variant (direct-mapped global
 // arrays), so no query is ever answered on the CPU.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace dbl {
 
 enum { CNT_PENDING = 0, CNT_ERR = 1, CNT_TICKET = 2, CNT_OVERFLOW = 3, CNT_DTICKET = 4, CNT_WORDS = 8 };
+// CNT_TILE (= 5, fused kernel tile ticket) is defined with the fused kernel below
 constexpr int GQ = 64;             // queries per BFS group
 constexpr int HCAP = 2048;         // shared hash capacity (power of two)
 constexpr int HBITS = 11;
@@ -34,6 +37,20 @@ constexpr int TCAP = 128;          // target table
 constexpr int BFS_THREADS = 256;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint8_t UNRESOLVED = 0xff;
+
+// Per-call query arguments, read by the kernels from device memory so that
+// the launch sequence can be a reusable CUDA graph (only this struct is
+// rewritten per batch).
+struct QueryDesc {
+    const uint32_t *u;
+    const uint32_t *v;
+    uint8_t *codes;
+    uint32_t *visited;
+    uint32_t count;
+    uint32_t flags;
+    int vec_ok;
+    int pad;
+};
 
 __device__ __forceinline__ void ld_nc128(const uint64_t *p, uint64_t &a, uint64_t &b) {
     asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
@@ -221,10 +238,13 @@ __device__ __forceinline__ unsigned long long tgt_lookup(const BfsShared &S, uin
 template <bool DENSE>
 __global__ void __launch_bounds__(BFS_THREADS)
 bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_t n, Adj adj,
-           const uint32_t *__restrict__ qu, const uint32_t *__restrict__ qv, uint32_t flags,
-           const uint32_t *__restrict__ pending, uint32_t *__restrict__ counters,
-           uint32_t *__restrict__ ovf, uint8_t *__restrict__ codes, uint32_t *__restrict__ visited,
-           char *__restrict__ ws) {
+           const QueryDesc *__restrict__ qd, const uint32_t *__restrict__ pending,
+           uint32_t *__restrict__ counters, uint32_t *__restrict__ ovf, char *__restrict__ ws) {
+    const uint32_t *__restrict__ qu = qd->u;
+    const uint32_t *__restrict__ qv = qd->v;
+    const uint32_t flags = qd->flags;
+    uint8_t *__restrict__ codes = qd->codes;
+    uint32_t *__restrict__ visited = qd->visited;
     const uint32_t H = WDL + WBL, rw = 2 * H;
     const uint32_t WD = WDL > 0 ? WDL : 1;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -427,6 +447,426 @@ static size_t bfs_smem(int wdl, int wbl, bool dense) {
     return s;
 }
 
+// --------------------------------------------------- fused K6 + warp BFS --
+//
+// The throughput path.  Persistent warps take 128-query tiles from a global
+// ticket; each lane owns 4 consecutive queries (one 128-bit load of u and of
+// v), gathers both endpoints' records with 256-bit read-only loads, and
+// applies rules 0-4.  The tile's unresolved queries (about 0.5% on R-MAT)
+// are answered right away by the same warp with a bit-parallel pruned BFS
+// over a per-warp shared-memory table (bit i of a 32-bit word = query i of
+// the batch): frontier expansion is flattened across lanes (32 edges per
+// step, owner entry found by a shuffle search over the degree prefix), so a
+// warp's BFS latency overlaps with every other warp's label checks instead
+// of running as a separate, latency-bound kernel.  A batch whose BFS outgrows
+// the table is appended to the global pending list and finished by the
+// 64-query group kernel (and, beyond that, the dense kernel).
+
+constexpr int QT = 128;            // queries per warp tile (4 per lane)
+constexpr int WH = 128;            // per-warp BFS hash slots (power of two)
+constexpr int WHBITS = 7;
+constexpr int WT = 64;             // per-warp target table slots
+constexpr int FUSED_THREADS = 256;
+// false: a warp answers its tile's unresolved queries right after the tile
+// (short BFS chains interleaved with other warps' label checks); true: it
+// accumulates 32 before running one BFS (fewer, longer chains at the end).
+// Measured on cfg2: immediate is faster (31 vs 39 us per 1M batch).
+constexpr bool DEFER_BFS = false;
+enum { CNT_TILE = 5 };
+
+template <int WDL, int WBL>
+struct WarpBfs {
+    static constexpr int WD = WDL > 0 ? WDL : 1;
+    uint32_t hkey[WH];
+    uint32_t hvis[WH];
+    uint32_t hfr[2][WH];
+    uint16_t hlist[2][WH];
+    uint32_t tkey[WT];
+    uint32_t tmask[WT];
+    uint32_t qidx[32];
+    uint32_t qu[32];
+    uint32_t qv[32];
+    uint32_t vcnt[32];
+    uint32_t nq;
+    uint64_t qdlo[32 * WD];
+    uint64_t qbli[32 * WBL];
+    uint64_t qblo[32 * WBL];
+    uint32_t nlist[2];
+    uint32_t done;
+    uint32_t overflow;
+};
+
+template <int RW>
+__device__ __forceinline__ void load_record(const uint64_t *p, uint64_t (&r)[RW]) {
+    if constexpr (RW % 4 == 0) {
+#pragma unroll
+        for (int k = 0; k < RW; k += 4)
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                         : "=l"(r[k]), "=l"(r[k + 1]), "=l"(r[k + 2]), "=l"(r[k + 3]) : "l"(p + k));
+    } else {
+#pragma unroll
+        for (int k = 0; k < RW; k += 2)
+            asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
+                         : "=l"(r[k]), "=l"(r[k + 1]) : "l"(p + k));
+    }
+}
+
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t &total) {
+    const int lane = threadIdx.x & 31;
+    uint32_t v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += y;
+    }
+    total = __shfl_sync(FULL, v, 31);
+    return v - x;
+}
+
+template <int WDL, int WBL>
+__device__ __forceinline__ int wb_slot(WarpBfs<WDL, WBL> &B, uint32_t x) {
+    uint32_t h = (x * 0x9E3779B1u) >> (32 - WHBITS);
+#pragma unroll 1
+    for (int probe = 0; probe < 32; ++probe) {
+        const uint32_t k = B.hkey[h];
+        if (k == x) return (int)h;
+        if (k == EMPTY) {
+            const uint32_t old = atomicCAS(&B.hkey[h], EMPTY, x);
+            if (old == EMPTY || old == x) return (int)h;
+        }
+        h = (h + 1) & (WH - 1);
+    }
+    return -1;
+}
+
+template <int WDL, int WBL>
+__device__ __forceinline__ uint32_t wb_target(const WarpBfs<WDL, WBL> &B, uint32_t x) {
+    uint32_t h = (x * 0x9E3779B1u) >> 26;  // 6 bits
+#pragma unroll 1
+    for (int probe = 0; probe < WT; ++probe) {
+        const uint32_t k = B.tkey[h];
+        if (k == x) return B.tmask[h];
+        if (k == EMPTY) return 0;
+        h = (h + 1) & (WT - 1);
+    }
+    return 0;
+}
+
+// Bit-parallel pruned BFS for the nb (<= 32) queries staged in B (qidx, qu,
+// qdlo, qbli, qblo, targets).  On return B.done holds the found bits and
+// B.vcnt the per-query expansion counts; B.overflow is set if the table
+// filled up (results then invalid).
+template <int WDL, int WBL>
+__device__ void warp_bfs(WarpBfs<WDL, WBL> &B, uint32_t nb, const uint64_t *__restrict__ rec,
+                         const Adj &adj, bool prune_dl, bool prune_bl) {
+    constexpr int H = WDL + WBL, RW = 2 * H, WD = WarpBfs<WDL, WBL>::WD;
+    const int lane = threadIdx.x & 31;
+    const uint32_t all = nb == 32 ? FULL : ((1u << nb) - 1u);
+    // sources
+    if (lane < (int)nb) {
+        const int sl = wb_slot(B, B.qu[lane]);
+        if (sl < 0) {
+            B.overflow = 1;
+        } else {
+            atomicOr(&B.hvis[sl], 1u << lane);
+            if (atomicOr(&B.hfr[0][sl], 1u << lane) == 0) {
+                const uint32_t p = atomicAdd(&B.nlist[0], 1u);
+                B.hlist[0][p] = (uint16_t)sl;
+            }
+        }
+    }
+    __syncwarp();
+    int cur = 0;
+    for (;;) {
+        const uint32_t ncur = *(volatile uint32_t *)&B.nlist[cur];
+        const uint32_t dn = *(volatile uint32_t *)&B.done;
+        if (ncur == 0 || (dn & all) == all || *(volatile uint32_t *)&B.overflow) break;
+        const int nxt = cur ^ 1;
+        for (uint32_t base = 0; base < ncur; base += 32) {
+            // lane j takes frontier entry base + j
+            const uint32_t ej = base + lane;
+            uint32_t fw = 0, w = 0, b0 = 0, bl = 0, d0 = 0, dl = 0;
+            if (ej < ncur) {
+                const uint32_t sl = B.hlist[cur][ej];
+                w = B.hkey[sl];
+                fw = B.hfr[cur][sl] & ~*(volatile uint32_t *)&B.done;
+                B.hfr[cur][sl] = 0;
+                if (fw) {
+                    b0 = __ldg(adj.ptr + w);
+                    bl = __ldg(adj.ptr + w + 1) - b0;
+                    if (adj.dptr) {
+                        d0 = __ldg(adj.dptr + w);
+                        dl = __ldg(adj.dptr + w + 1) - d0;
+                    }
+                }
+            }
+            // per-query expansion counts: lane q counts the entries holding bit q
+            {
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t fj = __shfl_sync(FULL, fw, j);
+                    if ((fj >> lane) & 1) B.vcnt[lane] += 1;
+                }
+            }
+            uint32_t total = 0;
+            const uint32_t excl = warp_excl_scan(bl + dl, total);
+            for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+                const uint32_t t = t0 + lane;
+                // owner: last lane with excl <= t (excl is non-decreasing)
+                int k = 0;
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1) {
+                    const uint32_t vv = __shfl_sync(FULL, excl, (k + st) & 31);
+                    if (k + st < 32 && vv <= t) k += st;
+                }
+                // skip empty owners: excl equal for several lanes -> take the last
+                const uint32_t ofw = __shfl_sync(FULL, fw, k);
+                const uint32_t ob0 = __shfl_sync(FULL, b0, k), obl = __shfl_sync(FULL, bl, k);
+                const uint32_t od0 = __shfl_sync(FULL, d0, k), oex = __shfl_sync(FULL, excl, k);
+                if (t >= total) continue;
+                const uint32_t r = t - oex;
+                const uint32_t x = r < obl ? __ldg(adj.col + ob0 + r) : __ldg(adj.dcol + od0 + (r - obl));
+                const uint32_t hit = ofw & wb_target(B, x);
+                if (hit) atomicOr(&B.done, hit);
+                const uint32_t cand = ofw & ~hit & ~*(volatile uint32_t *)&B.done;
+                if (!cand) continue;
+                const int sl = wb_slot(B, x);
+                if (sl < 0) { B.overflow = 1; continue; }
+                const uint32_t old = atomicOr(&B.hvis[sl], cand);
+                const uint32_t nw = cand & ~old;
+                if (!nw) continue;
+                uint32_t pruned = 0;
+                if (prune_dl || prune_bl) {   // queries.py:137-140
+                    uint64_t xr[RW];
+                    load_record<RW>(rec + (size_t)x * RW, xr);
+                    uint32_t m = nw;
+                    while (m) {
+                        const int bq = __ffs(m) - 1;
+                        m &= m - 1;
+                        bool p = false;
+                        if (prune_dl) {
+#pragma unroll
+                            for (int q = 0; q < WDL; ++q) p |= (B.qdlo[bq * WD + q] & xr[q]) != 0;
+                        }
+                        if (prune_bl && !p) {
+#pragma unroll
+                            for (int q = 0; q < WBL; ++q)
+                                p |= ((xr[WDL + q] & ~B.qbli[bq * WBL + q]) | (B.qblo[bq * WBL + q] & ~xr[H + WDL + q])) != 0;
+                        }
+                        if (p) pruned |= 1u << bq;
+                    }
+                }
+                const uint32_t nx = nw & ~pruned;
+                if (nx && atomicOr(&B.hfr[nxt][sl], nx) == 0) {
+                    const uint32_t p = atomicAdd(&B.nlist[nxt], 1u);
+                    B.hlist[nxt][p] = (uint16_t)sl;
+                }
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+        if (lane == 0) B.nlist[cur] = 0;
+        cur = nxt;
+        __syncwarp();
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void flush_tile_codes(uint8_t *__restrict__ codes, uint32_t *__restrict__ visited,
+                                                 uint32_t count, uint64_t qb, int vec_ok, const uint8_t (&code)[4],
+                                                 const uint32_t (&vcount)[4]) {
+    if (vec_ok && qb + 3 < count) {
+        const uint32_t packed = code[0] | (code[1] << 8) | (code[2] << 16) | ((uint32_t)code[3] << 24);
+        *reinterpret_cast<uint32_t *>(codes + qb) = packed;
+        if (visited) *reinterpret_cast<uint4 *>(visited + qb) = make_uint4(vcount[0], vcount[1], vcount[2], vcount[3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (qb + j >= count) break;
+            codes[qb + j] = code[j];
+            if (visited) visited[qb + j] = vcount[j];
+        }
+    }
+}
+
+// Run the warp's staged batch (B.nq queries) and write its answers.
+template <int WDL, int WBL>
+__device__ void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64_t *__restrict__ rec, const Adj &adj,
+                               bool prune_dl, bool prune_bl, uint8_t *__restrict__ codes,
+                               uint32_t *__restrict__ visited, uint32_t *__restrict__ pending,
+                               uint32_t *__restrict__ counters, cudaGraphConditionalHandle hard) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nb = B.nq;
+    for (int i = lane; i < WH; i += 32) {
+        B.hkey[i] = EMPTY; B.hvis[i] = 0; B.hfr[0][i] = 0; B.hfr[1][i] = 0;
+    }
+    for (int i = lane; i < WT; i += 32) { B.tkey[i] = EMPTY; B.tmask[i] = 0; }
+    B.vcnt[lane] = 0;
+    if (lane == 0) { B.nlist[0] = 0; B.nlist[1] = 0; B.done = 0; B.overflow = 0; }
+    __syncwarp();
+    if (lane < (int)nb) {  // target table: v -> bit lane
+        const uint32_t v = B.qv[lane];
+        uint32_t h = (v * 0x9E3779B1u) >> 26;
+        for (;;) {
+            const uint32_t old = atomicCAS(&B.tkey[h], EMPTY, v);
+            if (old == EMPTY || old == v) { atomicOr(&B.tmask[h], 1u << lane); break; }
+            h = (h + 1) & (WT - 1);
+        }
+    }
+    __syncwarp();
+    warp_bfs<WDL, WBL>(B, nb, rec, adj, prune_dl, prune_bl);
+    const bool ovf = B.overflow != 0;
+    const uint32_t dn = B.done;
+    if (lane < (int)nb) {
+        const uint32_t qi = B.qidx[lane];
+        if (ovf) {  // hand the batch to the group kernels via the pending list
+            const uint32_t p = atomicAdd(&counters[CNT_PENDING], 1u);
+            pending[p] = qi;
+        } else {
+            codes[qi] = ((dn >> lane) & 1) ? DBL_BFS_POSITIVE : DBL_BFS_NEGATIVE;
+            if (visited) visited[qi] = B.vcnt[lane];
+        }
+    }
+    if (ovf && lane == 0 && hard) cudaGraphSetConditional(hard, 1u);
+    __syncwarp();
+    if (lane == 0) B.nq = 0;
+    __syncwarp();
+}
+
+template <int WDL, int WBL>
+__global__ void __launch_bounds__(FUSED_THREADS)
+query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const QueryDesc *__restrict__ qd,
+                   uint32_t *__restrict__ pending, uint32_t *__restrict__ counters,
+                   cudaGraphConditionalHandle hard) {
+    const uint32_t *__restrict__ qu = qd->u;
+    const uint32_t *__restrict__ qv = qd->v;
+    const uint32_t count = qd->count, flags = qd->flags;
+    const int vec_ok = qd->vec_ok;
+    uint8_t *__restrict__ codes = qd->codes;
+    uint32_t *__restrict__ visited = qd->visited;
+    constexpr int H = WDL + WBL, RW = 2 * H, WD = WarpBfs<WDL, WBL>::WD;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WarpBfs<WDL, WBL> &B = reinterpret_cast<WarpBfs<WDL, WBL> *>(smem_raw)[wid];
+    const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
+    const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
+    const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
+    if (lane == 0) B.nq = 0;
+    __syncwarp();
+    for (;;) {
+        uint32_t tile = 0;
+        if (lane == 0) tile = atomicAdd(&counters[CNT_TILE], 1u);
+        tile = __shfl_sync(FULL, tile, 0);
+        const uint64_t q0 = (uint64_t)tile * QT;
+        if (q0 >= count) break;
+        const uint64_t qb = q0 + 4 * lane;
+        uint32_t us[4], vs[4];
+        if (vec_ok && qb + 3 < count) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4 *>(qu + qb));
+            const uint4 b = __ldg(reinterpret_cast<const uint4 *>(qv + qb));
+            us[0] = a.x; us[1] = a.y; us[2] = a.z; us[3] = a.w;
+            vs[0] = b.x; vs[1] = b.y; vs[2] = b.z; vs[3] = b.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                us[j] = qb + j < count ? __ldg(qu + qb + j) : 0;
+                vs[j] = qb + j < count ? __ldg(qv + qb + j) : 0;
+            }
+        }
+        uint8_t code[4];
+        uint32_t vcount[4] = {0, 0, 0, 0};
+        unsigned unres = 0;
+        uint64_t ra[4][RW], rb[4][RW];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool inb = qb + j < count;
+            const bool ok = inb && us[j] < n && vs[j] < n && us[j] != vs[j];
+            if (ok) {
+                load_record<RW>(rec + (size_t)us[j] * RW, ra[j]);
+                load_record<RW>(rec + (size_t)vs[j] * RW, rb[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool inb = qb + j < count;
+            code[j] = UNRESOLVED;
+            if (!inb) { code[j] = 0xfd; continue; }
+            const uint32_t u = us[j], v = vs[j];
+            if (u >= n || v >= n) {
+                atomicOr(&counters[CNT_ERR], 1u);
+                code[j] = 0xfe;
+                continue;
+            }
+            if (u == v) { code[j] = DBL_REFLEXIVE; continue; }
+            uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
+#pragma unroll
+            for (int k = 0; k < WDL; ++k) {
+                r1 |= ra[j][H + k] & rb[j][k];
+                r3 |= rb[j][H + k] & ra[j][k];
+                r4 |= (ra[j][H + k] & ra[j][k]) | (rb[j][H + k] & rb[j][k]);
+            }
+#pragma unroll
+            for (int k = 0; k < WBL; ++k)
+                r2 |= (ra[j][WDL + k] & ~rb[j][WDL + k]) | (rb[j][H + WDL + k] & ~ra[j][H + WDL + k]);
+            if (use_dl && r1) code[j] = DBL_DL_POSITIVE;
+            else if (use_bl && r2) code[j] = DBL_BL_NEGATIVE;
+            else if (thm1 && r3) code[j] = DBL_THM1_NEGATIVE;
+            else if (thm2 && r4) code[j] = DBL_THM2_NEGATIVE;
+            else unres |= 1u << j;
+        }
+        // Unresolved queries are appended to the warp's batch; the bit-parallel
+        // BFS runs when 32 have accumulated (and once more after the last
+        // tile), so a warp pays about one BFS latency chain per 32 queries.
+        // the tile's codes go out first (UNRESOLVED where a BFS will answer)
+        flush_tile_codes(codes, visited, count, qb, vec_ok, code, vcount);
+        __syncwarp();
+        uint32_t nun = __popc(unres), tot = 0;
+        uint32_t off = warp_excl_scan(nun, tot);
+        uint32_t done_upto = 0;   // tile entries [0, done_upto) already staged
+        while (done_upto < tot) {
+            const uint32_t nq = B.nq;
+            const uint32_t take = min(32u - nq, tot - done_upto);
+            uint32_t pos = off;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (!((unres >> j) & 1)) continue;
+                if (pos >= done_upto && pos < done_upto + take) {
+                    const uint32_t bi = nq + pos - done_upto;
+                    B.qidx[bi] = (uint32_t)(qb + j);
+                    B.qu[bi] = us[j];
+                    B.qv[bi] = vs[j];
+#pragma unroll
+                    for (int q = 0; q < WDL; ++q) B.qdlo[bi * WD + q] = ra[j][H + q];
+#pragma unroll
+                    for (int q = 0; q < WBL; ++q) {
+                        B.qbli[bi * WBL + q] = rb[j][WDL + q];
+                        B.qblo[bi * WBL + q] = rb[j][H + WDL + q];
+                    }
+                }
+                ++pos;
+            }
+            done_upto += take;
+            __syncwarp();
+            if (lane == 0) B.nq = nq + take;
+            __syncwarp();
+            if (nq + take == 32 || (!DEFER_BFS && done_upto == tot)) {
+                warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters, hard);
+            }
+        }
+    }
+    __syncwarp();
+    if (B.nq) warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters, hard);
+}
+
+typedef void (*fused_fn)(const uint64_t *, uint32_t, Adj, const QueryDesc *, uint32_t *, uint32_t *,
+                         cudaGraphConditionalHandle);
+
+static bool pick_fused(uint32_t wdl, uint32_t wbl, fused_fn &f, size_t &smem) {
+#define DBL_QF(A, B) if (wdl == A && wbl == B) { f = query_fused_kernel<A, B>; smem = sizeof(WarpBfs<A, B>) * (FUSED_THREADS / 32); return true; }
+    DBL_QF(0, 1) DBL_QF(1, 1) DBL_QF(2, 1) DBL_QF(4, 1) DBL_QF(0, 2) DBL_QF(1, 2) DBL_QF(2, 2)
+#undef DBL_QF
+    return false;
+}
+
 typedef void (*label_fn)(const uint64_t *, uint32_t, const uint32_t *, const uint32_t *, uint64_t,
                          uint32_t, uint8_t *, uint32_t *, uint32_t *, uint32_t *);
 
@@ -437,6 +877,102 @@ static label_fn pick_label(uint32_t wdl, uint32_t wbl) {
     return nullptr;
 }
 
+// Launch geometry of the hard path (64-query groups, then dense groups).
+struct HardPath {
+    int grid = 0, dctas = 0;
+    size_t smem = 0, dsmem = 0;
+};
+
+static dbl_status hard_path_config(const dbl_index *idx, dbl_graph *g, HardPath &hp) {
+    static int bps = -1;
+    static size_t last_smem = 0;
+    hp.smem = bfs_smem(idx->wdl, idx->wbl, false);
+    hp.dsmem = bfs_smem(idx->wdl, idx->wbl, true);
+    DBL_CUDA(cudaFuncSetAttribute((const void *)bfs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)hp.smem));
+    DBL_CUDA(cudaFuncSetAttribute((const void *)bfs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)hp.dsmem));
+    if (bps < 0 || last_smem != hp.smem) {
+        DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, bfs_kernel<false>, BFS_THREADS, hp.smem));
+        if (bps < 1) bps = 1;
+        last_smem = hp.smem;
+    }
+    hp.grid = g->sm_count * bps;
+    const size_t slab = (size_t)idx->n * 32;
+    hp.dctas = 8;
+    const size_t budget = (size_t)4 << 30;
+    while (hp.dctas > 1 && slab * hp.dctas > budget) --hp.dctas;
+    dbl_status s = g->q_dense.ensure(slab * hp.dctas + 16);
+    return s;
+}
+
+static void fill_kernel_node(cudaKernelNodeParams &kp, const void *fn, dim3 grid, dim3 block, size_t smem,
+                             void **args) {
+    kp = {};
+    kp.func = const_cast<void *>(fn);
+    kp.gridDim = grid;
+    kp.blockDim = block;
+    kp.sharedMemBytes = (unsigned)smem;
+    kp.kernelParams = args;
+}
+
+// Build the reusable query graph:
+//   memset(counters) -> ev2 -> fused -> ev3 -> IF(hard) { group -> dense } -> ev4
+static dbl_status build_query_graph(const dbl_index *idx, dbl_graph *g, fused_fn fused, size_t fsmem, int fgrid,
+                                    const HardPath &hp) {
+    if (g->q_exec) { cudaGraphExecDestroy(g->q_exec); g->q_exec = nullptr; }
+    if (g->q_graph) { cudaGraphDestroy(g->q_graph); g->q_graph = nullptr; }
+    cudaGraph_t gr;
+    DBL_CUDA(cudaGraphCreate(&gr, 0));
+    g->q_graph = gr;
+    cudaGraphConditionalHandle hard;
+    DBL_CUDA(cudaGraphConditionalHandleCreate(&hard, gr, 0, cudaGraphCondAssignDefault));
+    cudaGraphNode_t nmem, ne2, nfused, ne3, ncond, ne4;
+    cudaMemsetParams mp = {};
+    mp.dst = g->q_counters.p;
+    mp.value = 0;
+    mp.elementSize = 4;
+    mp.width = CNT_WORDS;
+    mp.height = 1;
+    DBL_CUDA(cudaGraphAddMemsetNode(&nmem, gr, nullptr, 0, &mp));
+    DBL_CUDA(cudaGraphAddEventRecordNode(&ne2, gr, &nmem, 1, g->ev[2]));
+    // kernel args must outlive cudaGraphAddKernelNode only (they are copied)
+    const uint64_t *rec = idx->rec.as<uint64_t>();
+    uint32_t n = idx->n, wdl = idx->wdl, wbl = idx->wbl;
+    Adj adj = graph_fwd(g);
+    const QueryDesc *qd = g->q_desc.as<QueryDesc>();
+    uint32_t *pending = g->q_pending.as<uint32_t>();
+    uint32_t *counters = g->q_counters.as<uint32_t>();
+    uint32_t *ovf = pending + g->q_pending_cap + 16;
+    char *ws = g->q_dense.as<char>();
+    char *nows = nullptr;
+    void *fargs[] = {(void *)&rec, (void *)&n, (void *)&adj, (void *)&qd, (void *)&pending, (void *)&counters,
+                     (void *)&hard};
+    cudaKernelNodeParams kp;
+    fill_kernel_node(kp, (const void *)fused, dim3(fgrid), dim3(FUSED_THREADS), fsmem, fargs);
+    DBL_CUDA(cudaGraphAddKernelNode(&nfused, gr, &ne2, 1, &kp));
+    DBL_CUDA(cudaGraphAddEventRecordNode(&ne3, gr, &nfused, 1, g->ev[3]));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hard;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    DBL_CUDA(cudaGraphAddNode(&ncond, gr, &ne3, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaGraphNode_t ngrp, nden;
+    void *gargs[] = {(void *)&rec, (void *)&wdl, (void *)&wbl, (void *)&n, (void *)&adj, (void *)&qd,
+                     (void *)&pending, (void *)&counters, (void *)&ovf, (void *)&nows};
+    fill_kernel_node(kp, (const void *)bfs_kernel<false>, dim3(hp.grid), dim3(BFS_THREADS), hp.smem, gargs);
+    DBL_CUDA(cudaGraphAddKernelNode(&ngrp, body, nullptr, 0, &kp));
+    void *dargs[] = {(void *)&rec, (void *)&wdl, (void *)&wbl, (void *)&n, (void *)&adj, (void *)&qd,
+                     (void *)&pending, (void *)&counters, (void *)&ovf, (void *)&ws};
+    fill_kernel_node(kp, (const void *)bfs_kernel<true>, dim3(hp.dctas), dim3(BFS_THREADS), hp.dsmem, dargs);
+    DBL_CUDA(cudaGraphAddKernelNode(&nden, body, &ngrp, 1, &kp));
+    DBL_CUDA(cudaGraphAddEventRecordNode(&ne4, gr, &ncond, 1, g->ev[4]));
+    DBL_CUDA(cudaGraphInstantiate(&g->q_exec, gr, 0));
+    return DBL_OK;
+}
+
 dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
                      uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited) {
     if (count >= 0xffffffffull) { set_error("query batch too large"); return DBL_E_ARG; }
@@ -444,20 +980,62 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
         set_error("label width too large for the query kernels");
         return DBL_E_CONFIG;
     }
-    const label_fn label = pick_label(idx->wdl, idx->wbl);
     dbl_status s;
-    if ((s = g->q_pending.ensure(count * 8 + 64)) || (s = g->q_counters.ensure(CNT_WORDS * 4))) return s;
+    // pending list capacity: grows with the largest batch seen (graph rebuilt on growth)
+    uint64_t cap = g->q_pending_cap;
+    if (count > cap) cap = count < 1024 ? 1024 : count;
+    if ((s = g->q_pending.ensure(cap * 8 + 64)) || (s = g->q_counters.ensure(CNT_WORDS * 4)) ||
+        (s = g->q_desc.ensure(sizeof(QueryDesc))))
+        return s;
+    const bool grown = cap != g->q_pending_cap;
+    g->q_pending_cap = cap;
+    QueryDesc hd{u, v, codes, visited, (uint32_t)count, flags, 0, 0};
+    hd.vec_ok = ((((uintptr_t)u) | ((uintptr_t)v)) & 15) == 0 && (((uintptr_t)codes) & 3) == 0 &&
+                (!visited || (((uintptr_t)visited) & 15) == 0);
+    DBL_CUDA(cudaMemcpyAsync(g->q_desc.p, &hd, sizeof(hd), cudaMemcpyHostToDevice, g->stream));
+    fused_fn fused = nullptr;
+    size_t fsmem = 0;
+    const bool use_fused = pick_fused(idx->wdl, idx->wbl, fused, fsmem) && !std::getenv("DBL_NO_FUSED");
+    HardPath hp;
+    if ((s = hard_path_config(idx, g, hp))) return s;
+    if (use_fused) {
+        static int fbps = -1;
+        static const void *last_fn = nullptr;
+        if (fbps < 0 || last_fn != (const void *)fused) {
+            DBL_CUDA(cudaFuncSetAttribute((const void *)fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
+            DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fbps, fused, FUSED_THREADS, fsmem));
+            if (fbps < 1) fbps = 1;
+            last_fn = (const void *)fused;
+        }
+        const int fgrid = g->sm_count * fbps;
+        // the graph bakes in device pointers: rebuild when any of them moved
+        const void *key[6] = {idx, idx->rec.p, g->fptr.p, g->m_delta ? g->dfptr.p : nullptr,
+                              g->q_pending.p, g->q_dense.p};
+        bool same = g->q_exec && !grown && g->q_topo == g->topo_version;
+        for (int i = 0; i < 6 && same; ++i) same = g->q_key[i] == key[i];
+        if (!same) {
+            if ((s = build_query_graph(idx, g, fused, fsmem, fgrid, hp))) return s;
+            for (int i = 0; i < 6; ++i) g->q_key[i] = key[i];
+            g->q_topo = g->topo_version;
+        }
+        DBL_CUDA(cudaGraphLaunch(g->q_exec, g->stream));
+        launch_counter() += 2;  // fused kernel (+ hard path when needed)
+        return DBL_OK;
+    }
+    // generic widths: label kernel, then the group and dense kernels
     uint32_t *pending = g->q_pending.as<uint32_t>();
-    uint32_t *ovf = pending + count + 16;
+    uint32_t *ovf = pending + g->q_pending_cap + 16;
     uint32_t *counters = g->q_counters.as<uint32_t>();
+    const QueryDesc *qd = g->q_desc.as<QueryDesc>();
     DBL_CUDA(cudaMemsetAsync(counters, 0, CNT_WORDS * 4, g->stream));
     DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
     if (count) {
         int blocks = (int)((count + 255) / 256);
         if (blocks > g->sm_count * 16) blocks = g->sm_count * 16;
+        const label_fn label = pick_label(idx->wdl, idx->wbl);
         if (label)
-            label<<<blocks, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, u, v, count, flags,
-                                                   codes, visited, pending, counters);
+            label<<<blocks, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, u, v, count, flags, codes,
+                                                 visited, pending, counters);
         else
             label_check_generic<<<blocks, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, idx->wdl,
                                                                idx->wbl, u, v, count, flags, codes, visited,
@@ -466,35 +1044,23 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     }
     DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
     if (count) {
-        // K7 over the compacted pending list (persistent CTAs, group tickets)
-        static int bps = -1;
-        static size_t last_smem = 0;
-        const size_t smem = bfs_smem(idx->wdl, idx->wbl, false);
-        DBL_CUDA(cudaFuncSetAttribute((const void *)bfs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        if (bps < 0 || last_smem != smem) {
-            DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, bfs_kernel<false>, BFS_THREADS, smem));
-            if (bps < 1) bps = 1;
-            last_smem = smem;
-        }
         Adj adj = graph_fwd(g);
-        bfs_kernel<false><<<g->sm_count * bps, BFS_THREADS, smem, g->stream>>>(idx->rec.as<uint64_t>(), idx->wdl, idx->wbl, idx->n, adj,
-                                                                  u, v, flags, pending, counters, ovf, codes,
-                                                                  visited, nullptr);
+        bfs_kernel<false><<<hp.grid, BFS_THREADS, hp.smem, g->stream>>>(idx->rec.as<uint64_t>(), idx->wdl, idx->wbl,
+                                                                        idx->n, adj, qd, pending, counters, ovf,
+                                                                        nullptr);
         DBL_CHECK_LAUNCH("bfs_kernel");
-        // dense re-run of overflowed groups: a few CTAs with n-sized slabs
-        const size_t slab = (size_t)idx->n * 32;
-        int dctas = 8;
-        const size_t budget = (size_t)4 << 30;
-        while (dctas > 1 && slab * dctas > budget) --dctas;
-        if ((s = g->q_dense.ensure(slab * dctas + 16))) return s;
-        const size_t dsmem = bfs_smem(idx->wdl, idx->wbl, true);
-        DBL_CUDA(cudaFuncSetAttribute((const void *)bfs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
-        bfs_kernel<true><<<dctas, BFS_THREADS, dsmem, g->stream>>>(idx->rec.as<uint64_t>(), idx->wdl, idx->wbl, idx->n, adj, u, v,
-                                                          flags, pending, counters, ovf, codes, visited,
-                                                          g->q_dense.as<char>());
+        bfs_kernel<true><<<hp.dctas, BFS_THREADS, hp.dsmem, g->stream>>>(idx->rec.as<uint64_t>(), idx->wdl,
+                                                                         idx->wbl, idx->n, adj, qd, pending,
+                                                                         counters, ovf, g->q_dense.as<char>());
         DBL_CHECK_LAUNCH("bfs_kernel_dense");
     }
     DBL_CUDA(cudaEventRecord(g->ev[4], g->stream));
+    return DBL_OK;
+}
+
+// Copy the range-error flag of the last batch to dst (device, stream-ordered).
+dbl_status query_err_to(dbl_graph *g, uint32_t *dst) {
+    DBL_CUDA(cudaMemcpyAsync(dst, g->q_counters.as<uint32_t>() + CNT_ERR, 4, cudaMemcpyDeviceToDevice, g->stream));
     return DBL_OK;
 }
 
@@ -509,3 +1075,17 @@ dbl_status query_finish(dbl_graph *g, uint32_t *err_out) {
 }
 
 }  // namespace dbl
+
+using namespace dbl;
+
+// Counters of the last query batch on g: [0] queries handed to the group
+// kernels (per-warp BFS table overflow or generic widths), [1] range-error
+// flag, [3] groups re-run densely.
+extern "C" dbl_status dbl_query_counters(const dbl_graph *g, uint32_t *out8) {
+    if (!g || !out8) { set_error("null argument"); return DBL_E_ARG; }
+    if (!g->q_counters.p) { for (int i = 0; i < 8; ++i) out8[i] = 0; return DBL_OK; }
+    DBL_CUDA(cudaSetDevice(g->device));
+    DBL_CUDA(cudaMemcpyAsync(out8, g->q_counters.p, 8 * 4, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    return DBL_OK;
+}

@@ -40,45 +40,106 @@ dbl_status leaf_hash_dev(const uint64_t *ids, uint64_t count, uint32_t k_prime, 
     return DBL_OK;
 }
 
-__global__ void score_kernel(const uint32_t *__restrict__ fptr, const uint32_t *__restrict__ rptr,
-                             const uint32_t *__restrict__ dfptr, const uint32_t *__restrict__ drptr,
-                             uint32_t n, int strategy, uint64_t *__restrict__ score,
-                             uint32_t *__restrict__ ids) {
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        uint64_t out = fptr[v + 1] - fptr[v], in = rptr[v + 1] - rptr[v];
-        if (dfptr) { out += dfptr[v + 1] - dfptr[v]; in += drptr[v + 1] - drptr[v]; }
-        uint64_t s;
-        switch (strategy) {
-        case DBL_STRAT_MAX: s = in > out ? in : out; break;
-        case DBL_STRAT_MIN: s = in < out ? in : out; break;
-        case DBL_STRAT_SUM: s = in + out; break;
-        default: s = in * out; break;
-        }
-        score[v] = s;
-        ids[v] = v;
+__device__ __forceinline__ uint64_t strategy_score(int strategy, uint64_t in, uint64_t out) {
+    switch (strategy) {
+    case DBL_STRAT_MAX: return in > out ? in : out;
+    case DBL_STRAT_MIN: return in < out ? in : out;
+    case DBL_STRAT_SUM: return in + out;
+    default: return in * out;
     }
 }
 
+// bin 0: score 0; bin i (1..64): floor(log2(score)) + 1
+__device__ __forceinline__ int score_bin(uint64_t s) { return s ? 64 - __clzll((long long)s) : 0; }
+
+// score[v] for every vertex + a 65-bin log2 histogram of the scores
+__global__ void score_hist_kernel(const uint32_t *__restrict__ fptr, const uint32_t *__restrict__ rptr,
+                                  const uint32_t *__restrict__ dfptr, const uint32_t *__restrict__ drptr,
+                                  uint32_t n, int strategy, uint64_t *__restrict__ score,
+                                  uint32_t *__restrict__ hist) {
+    __shared__ uint32_t h[65];
+    for (int i = threadIdx.x; i < 65; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        uint64_t out = fptr[v + 1] - fptr[v], in = rptr[v + 1] - rptr[v];
+        if (dfptr) { out += dfptr[v + 1] - dfptr[v]; in += drptr[v + 1] - drptr[v]; }
+        const uint64_t sc = strategy_score(strategy, in, out);
+        score[v] = sc;
+        atomicAdd(&h[score_bin(sc)], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 65; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+struct BinAtLeast {
+    const uint64_t *score;
+    int bin;
+    __device__ bool operator()(uint32_t v) const { return score_bin(score[v]) >= bin; }
+};
+
+__global__ void gather_scores_kernel(const uint64_t *__restrict__ score, const uint32_t *__restrict__ ids,
+                                     uint32_t c, uint64_t *__restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
+        out[i] = score[ids[i]];
+}
+
+// Top-k by (-score, id): a log2 histogram finds the lowest score bin that
+// still holds the k-th best vertex; only vertices in that bin or above can be
+// landmarks.  They are compacted in id order and stable-sorted by score
+// descending, which reproduces sorted(key=(-score, id)) (labels.py:145-146).
 dbl_status select_landmarks_dev(dbl_graph *g, uint32_t k, int strategy, uint32_t *dev_out) {
     uint32_t n = g->n;
     if (k > n) { set_error("k exceeds vertex count"); return DBL_E_CONFIG; }
     if (k == 0) return DBL_OK;
     dbl_status s;
-    size_t nb = (size_t)n * 8;
-    if ((s = g->scratch_a.ensure(nb * 2)) || (s = g->scratch_b.ensure(nb * 2))) return s;
-    uint64_t *sc = g->scratch_a.as<uint64_t>(), *sc2 = sc + n;
-    uint32_t *id = g->scratch_b.as<uint32_t>(), *id2 = id + n;
+    const size_t nb = (size_t)n * 8;
+    if ((s = g->scratch_a.ensure(nb * 2 + 65 * 4 + 64)) || (s = g->scratch_b.ensure((size_t)n * 8 + 64))) return s;
+    uint64_t *sc = g->scratch_a.as<uint64_t>(), *sc_sorted_a = sc + n;
+    uint32_t *hist = reinterpret_cast<uint32_t *>(sc + 2 * (size_t)n);
+    uint32_t *ids = g->scratch_b.as<uint32_t>(), *ids2 = ids + n;
     Adj f = graph_fwd(g), r = graph_rev(g);
-    int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-    score_kernel<<<blocks, 256, 0, g->stream>>>(f.ptr, r.ptr, f.dptr, r.dptr, n, strategy, sc, id);
-    DBL_CHECK_LAUNCH("score_kernel");
-    cub::DoubleBuffer<uint64_t> dk(sc, sc2);
-    cub::DoubleBuffer<uint32_t> dv(id, id2);
+    DBL_CUDA(cudaMemsetAsync(hist, 0, 65 * 4, g->stream));
+    int blocks = (int)((n + 255) / 256 < (uint32_t)g->sm_count * 8 ? (n + 255) / 256 : g->sm_count * 8);
+    score_hist_kernel<<<blocks, 256, 0, g->stream>>>(f.ptr, r.ptr, f.dptr, r.dptr, n, strategy, sc, hist);
+    DBL_CHECK_LAUNCH("score_hist_kernel");
+    uint32_t hh[65];
+    DBL_CUDA(cudaMemcpyAsync(hh, hist, sizeof(hh), cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    int bin = 64;
+    uint64_t acc = 0;
+    for (; bin >= 0; --bin) {
+        acc += hh[bin];
+        if (acc >= k) break;
+    }
+    if (bin < 0) bin = 0;
+    // candidates in id order
+    if ((s = g->scratch_c.ensure(16))) return s;
+    int *d_nsel = g->scratch_c.as<int>();
+    cub::CountingInputIterator<uint32_t> it(0);
     size_t tmp = 0;
-    DBL_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, dk, dv, (int64_t)n, 0, 64, g->stream));
+    BinAtLeast pred{sc, bin};
+    DBL_CUDA(cub::DeviceSelect::If(nullptr, tmp, it, ids, d_nsel, (int64_t)n, pred, g->stream));
     if ((s = g->cub_tmp.ensure(tmp))) return s;
-    DBL_CUDA(cub::DeviceRadixSort::SortPairsDescending(g->cub_tmp.p, tmp, dk, dv, (int64_t)n, 0, 64,
-                                                       g->stream));
+    DBL_CUDA(cub::DeviceSelect::If(g->cub_tmp.p, tmp, it, ids, d_nsel, (int64_t)n, pred, g->stream));
+    DBL_LAUNCHED();
+    int c = 0;
+    DBL_CUDA(cudaMemcpyAsync(&c, d_nsel, 4, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    uint64_t *csc = sc_sorted_a, *csc2 = csc + c;   // candidate scores (c <= n)
+    if ((size_t)c * 2 > (size_t)n) {                 // large candidate set: reuse score buffer layout
+        if ((s = g->scratch_d.ensure((size_t)c * 16 + 16))) return s;
+        csc = g->scratch_d.as<uint64_t>();
+        csc2 = csc + c;
+    }
+    gather_scores_kernel<<<(c + 255) / 256 < 4096 ? (c + 255) / 256 : 4096, 256, 0, g->stream>>>(sc, ids, c, csc);
+    DBL_CHECK_LAUNCH("gather_scores_kernel");
+    cub::DoubleBuffer<uint64_t> dk(csc, csc2);
+    cub::DoubleBuffer<uint32_t> dv(ids, ids2);
+    tmp = 0;
+    DBL_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, dk, dv, (int64_t)c, 0, 64, g->stream));
+    if ((s = g->cub_tmp.ensure(tmp))) return s;
+    DBL_CUDA(cub::DeviceRadixSort::SortPairsDescending(g->cub_tmp.p, tmp, dk, dv, (int64_t)c, 0, 64, g->stream));
     DBL_LAUNCHED();
     DBL_CUDA(cudaMemcpyAsync(dev_out, dv.Current(), (size_t)k * 4, cudaMemcpyDeviceToDevice, g->stream));
     return DBL_OK;
@@ -142,6 +203,7 @@ extern "C" dbl_status dbl_leaf_hash(const uint64_t *ids, uint64_t count, uint32_
     if (!count) return DBL_OK;
     if (!ids || !out) { set_error("null argument"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(device));
+    set_stream(nullptr);
     DevBuf b;
     dbl_status s = b.ensure(count * 12);
     if (s) return s;
@@ -163,6 +225,7 @@ extern "C" dbl_status dbl_select_landmarks(const dbl_graph *g, uint32_t k, int32
     if (k > g->n) { set_error("k exceeds vertex count"); return DBL_E_CONFIG; }
     if (!k) return DBL_OK;
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     dbl_graph *gm = const_cast<dbl_graph *>(g);
     DevBuf b;
     dbl_status s = b.ensure((size_t)k * 4);
@@ -226,6 +289,7 @@ extern "C" dbl_status dbl_select_leaves(const dbl_graph *g, uint64_t threshold, 
     uint32_t n = g->n;
     if (!n) return DBL_OK;
     DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     dbl_graph *gm = const_cast<dbl_graph *>(g);
     DevBuf ovr, outb;
     dbl_status s = DBL_OK;
