@@ -13,7 +13,8 @@ import numpy as np
 
 from .errors import STATUS_ERRORS, DeviceError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libdbl_b200.so")
+LIB_PATH = os.environ.get("DBL_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libdbl_b200.so")
 
 P = ctypes.c_void_p
 u8p = ctypes.POINTER(ctypes.c_uint8)

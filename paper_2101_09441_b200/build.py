@@ -48,6 +48,22 @@ def _compile(src: str) -> tuple[str, str]:
     return obj, r.stderr
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Experimental build with extra -D flags into _lib/variant_<name>.so."""
+    os.makedirs(OUTDIR, exist_ok=True)
+    out = os.path.join(OUTDIR, f"variant_{name}.so")
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(OUTDIR, f"{name}_{src.replace('.cu', '.o')}")
+        subprocess.check_call([NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c",
+                               os.path.join(CSRC, src), "-o", obj], stderr=subprocess.DEVNULL)
+        objs.append(obj)
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"])
+    for o in objs:
+        os.remove(o)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB

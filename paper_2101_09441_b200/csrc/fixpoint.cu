@@ -65,6 +65,12 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
     return x;
 }
 
+__device__ __forceinline__ uint32_t warp_excl_scan_u32(uint32_t x, uint32_t &total) {
+    const uint32_t incl = warp_incl_scan(x);
+    total = __shfl_sync(FULL, incl, 31);
+    return incl - x;
+}
+
 // position of the r-th (0-based) set bit of mask
 __device__ __forceinline__ int select_bit(uint32_t mask, uint32_t r) {
     int p = 0;
@@ -116,9 +122,17 @@ __device__ __forceinline__ void warp_enqueue(const DirParams &D, const Queue &QN
     }
 }
 
-// OR the source words into y's words; true iff this thread set a new bit.
+__device__ __forceinline__ void red_or(uint64_t *p, uint64_t v) {
+    asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_or32(uint32_t *p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// OR the source words into y's words, marking y in the next-level bitmap when
+// its (L2-coherent) read lacked bits; true iff anything was missing.
 template <int NW, bool VEC>
-__device__ __forceinline__ bool relax(const DirParams &D, uint32_t y, const uint64_t (&s)[NW]) {
+__device__ __forceinline__ bool relax_mark(const DirParams &D, uint32_t y, const uint64_t (&s)[NW]) {
     uint64_t *p = D.lab + (size_t)y * D.stride;
     uint64_t c[NW];
     load_words<NW, VEC>(p, c);
@@ -126,27 +140,10 @@ __device__ __forceinline__ bool relax(const DirParams &D, uint32_t y, const uint
 #pragma unroll
     for (int k = 0; k < NW; ++k) {
         const uint64_t need = s[k] & ~c[k];
-        if (need) {
-            const uint64_t old = atomicOr(reinterpret_cast<unsigned long long *>(p + k),
-                                          (unsigned long long)need);
-            ch |= (need & ~old) != 0;
-        }
+        if (need) { red_or(p + k, need); ch = true; }
     }
+    if (ch) red_or32(D.bits + (y >> 5), 1u << (y & 31));
     return ch;
-}
-
-template <bool COUNT>
-__device__ __forceinline__ void push_changed(const DirParams &D, const Queue &QN, bool ch, uint32_t y,
-                                             uint32_t epoch, unsigned long long *cnt_ptr, Ctrl *ctrl,
-                                             uint32_t &nchanged) {
-    if (!__any_sync(FULL, ch)) return;
-    if (COUNT && ch) {
-        const uint32_t bit = 1u << (y & 31);
-        const uint32_t old = atomicOr(&D.changed_bits[y >> 5], bit);
-        if (!(old & bit)) ++nchanged;
-    }
-    const bool p = ch && (atomicExch(&D.stamp[y], epoch) != epoch);
-    warp_enqueue(D, QN, p, y, cnt_ptr, ctrl);
 }
 
 // Last item whose edge offset is <= e, searching [lo, nitems) 32-ary.
@@ -165,74 +162,19 @@ __device__ __forceinline__ uint32_t find_item(const uint32_t *eoff, uint32_t lo,
     return lo;
 }
 
-__device__ __forceinline__ void red_or(uint64_t *p, uint64_t v) {
-    asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// Enqueue up to U vertices per lane (ys[r] where ps[r]) with one scan and one
-// 64-bit atomicAdd per warp.
-template <int U>
-__device__ __forceinline__ void warp_enqueue_multi(const DirParams &D, const Queue &QN, const bool (&ps)[U],
-                                                   const uint32_t (&ys)[U], unsigned long long *cnt_ptr,
-                                                   Ctrl *ctrl) {
-    const int lane = threadIdx.x & 31;
-    uint32_t b0[U], b1[U], d0[U], d1[U];
-    uint32_t ni = 0, ne = 0;
-#pragma unroll
-    for (int r = 0; r < U; ++r) {
-        b0[r] = b1[r] = d0[r] = d1[r] = 0;
-        if (ps[r]) {
-            b0[r] = __ldg(D.adj.ptr + ys[r]);
-            b1[r] = __ldg(D.adj.ptr + ys[r] + 1);
-            if (D.adj.dptr) {
-                d0[r] = __ldg(D.adj.dptr + ys[r]);
-                d1[r] = __ldg(D.adj.dptr + ys[r] + 1);
-            }
-        }
-        ni += (b1[r] > b0[r]) + (d1[r] > d0[r]);
-        ne += (b1[r] - b0[r]) + (d1[r] - d0[r]);
-    }
-    const uint32_t ii = warp_incl_scan(ni), ei = warp_incl_scan(ne);
-    const uint32_t ti = __shfl_sync(FULL, ii, 31), te = __shfl_sync(FULL, ei, 31);
-    if (ti == 0) return;
-    unsigned long long base = 0;
-    if (lane == 31) base = atomicAdd(cnt_ptr, ((unsigned long long)ti << 32) | te);
-    base = __shfl_sync(FULL, base, 31);
-    const uint32_t ibase = (uint32_t)(base >> 32), ebase = (uint32_t)base;
-    if ((uint64_t)ibase + ti > D.cap) {
-        if (lane == 0) atomicOr(&ctrl->overflow, 1u);
-        return;
-    }
-    uint32_t pos = ibase + ii - ni, eo = ebase + ei - ne;
-#pragma unroll
-    for (int r = 0; r < U; ++r) {
-        if (b1[r] > b0[r]) {
-            QN.x[pos] = ys[r]; QN.start[pos] = b0[r]; QN.len[pos] = b1[r] - b0[r]; QN.eoff[pos] = eo;
-            ++pos;
-            eo += b1[r] - b0[r];
-        }
-        if (d1[r] > d0[r]) {
-            QN.x[pos] = ys[r]; QN.start[pos] = d0[r]; QN.len[pos] = (d1[r] - d0[r]) | DELTA_BIT;
-            QN.eoff[pos] = eo;
-            ++pos;
-            eo += d1[r] - d0[r];
-        }
-    }
-}
-
-// One warp relaxes the edges [e0, e1) of a level's edge space, U rounds of
-// 32 consecutive edges at a time: each lane finds its item in a 32-item
-// window by a 5-step shuffle search (the window slides forward as edges are
-// consumed), then the U column loads, the U destination-label loads and the
-// fire-and-forget atomic ORs of the U rounds are issued back to back so their
-// latencies overlap.  A destination whose (L2-coherent) read lacked bits is
-// pushed: if another thread supplied the bits first the vertex is merely
-// re-expanded once with nothing new, which keeps the fixpoint exact.
-template <int NW, bool VEC, bool COUNT>
-__device__ __forceinline__ void expand_range(const DirParams &D, const Queue &Q, const Queue &QN,
-                                             uint32_t nitems, uint32_t e0, uint32_t e1, uint32_t epoch,
-                                             unsigned long long *next_cnt, Ctrl *ctrl, uint32_t &nchanged) {
-    constexpr int U = NW <= 2 ? 4 : (NW <= 4 ? 2 : 1);
+// Phase A: one warp relaxes the edges [e0, e1) of a level's edge space, U
+// rounds of 32 consecutive edges at a time.  Each lane finds its item in a
+// 32-item window by a 5-step shuffle search (the window slides forward as
+// edges are consumed); the U column loads, the U destination reads and the
+// fire-and-forget ORs (labels + next-frontier bitmap) are issued back to back
+// so their latencies overlap.  Nothing waits on an atomic result.
+template <int NW, bool VEC>
+__device__ __forceinline__ void expand_range(const DirParams &D, uint32_t nitems, uint32_t e0, uint32_t e1) {
+#ifndef DBL_FU
+#define DBL_FU 4
+#endif
+    constexpr int U = NW <= 2 ? DBL_FU : (NW <= 4 ? 2 : 1);
+    const Queue &Q = D.q;
     const int lane = threadIdx.x & 31;
     uint32_t i0 = find_item(Q.eoff, 0, nitems, e0);
     uint32_t wE = 0xffffffffu, wS = 0, wEnd = 0, winEnd = 0;
@@ -301,78 +243,285 @@ __device__ __forceinline__ void expand_range(const DirParams &D, const Queue &Q,
 #pragma unroll
         for (int r = 0; r < U; ++r)
             if (ok[r]) load_words<NW, VEC>(D.lab + (size_t)ys[r] * D.stride, cur[r]);
-        bool ps[U];
-        bool any = false;
 #pragma unroll
         for (int r = 0; r < U; ++r) {
+            if (!ok[r]) continue;
+            uint64_t *p = D.lab + (size_t)ys[r] * D.stride;
             bool ch = false;
-            if (ok[r]) {
-                uint64_t *p = D.lab + (size_t)ys[r] * D.stride;
 #pragma unroll
-                for (int j = 0; j < NW; ++j) {
-                    const uint64_t need = src[r][j] & ~cur[r][j];
-                    if (need) { red_or(p + j, need); ch = true; }
-                }
+            for (int j = 0; j < NW; ++j) {
+                const uint64_t need = src[r][j] & ~cur[r][j];
+                if (need) { red_or(p + j, need); ch = true; }
             }
-            ps[r] = ch;
-            any |= ch;
+            if (ch) red_or32(D.bits + (ys[r] >> 5), 1u << (ys[r] & 31));
         }
-        if (!__any_sync(FULL, any)) continue;
-#pragma unroll
-        for (int r = 0; r < U; ++r) {
-            if (COUNT && ps[r]) {
-                const uint32_t bit = 1u << (ys[r] & 31);
-                const uint32_t old = atomicOr(&D.changed_bits[ys[r] >> 5], bit);
-                if (!(old & bit)) ++nchanged;
-            }
-            if (ps[r]) ps[r] = ld_cg32(D.stamp + ys[r]) != epoch && atomicExch(&D.stamp[ys[r]], epoch) != epoch;
-        }
-        warp_enqueue_multi<U>(D, QN, ps, ys, next_cnt, ctrl);
     }
 }
 
+// Pull relaxation of the edges [e0, e1) of one adjacency segment (ptr/col):
+// row x collects the OR of its neighbours' words over the neighbours that are
+// in the current frontier (bitmap cur), with a segmented OR-scan across lanes;
+// only a row whose L2-coherent read lacks bits is written (red.or) and marked.
+// No per-edge atomics: used for the levels whose frontier covers a large part
+// of the graph (direction-optimising, as in push/pull BFS).
+template <int NW, bool VEC>
+__device__ __forceinline__ void pull_range(const DirParams &D, const uint32_t *__restrict__ ptr,
+                                           const uint32_t *__restrict__ col, uint32_t nrows, uint32_t e0,
+                                           uint32_t e1) {
+    const int lane = threadIdx.x & 31;
+    uint32_t x0 = find_item(ptr, 0, nrows, e0);   // ptr[nrows] = m bounds the search
+    uint32_t rS = 0xffffffffu, winEnd = 0;
+    auto load_window = [&](uint32_t first) {
+        const uint32_t i = first + lane;
+        rS = i < nrows ? __ldg(ptr + i) : 0xffffffffu;
+        const uint32_t last = first + 32 < nrows ? first + 32 : nrows;
+        winEnd = __ldg(ptr + last);
+    };
+    load_window(x0);
+    for (uint32_t e = e0; e < e1;) {
+        // a 32-row window may hold fewer than 32 edges (empty rows): a round
+        // covers the edges of the window only
+        if (e >= winEnd) {
+            x0 = find_item(ptr, x0, nrows, e);
+            load_window(x0);
+        } else if (min(e + 31, e1 - 1) >= winEnd) {
+            const unsigned bal = __ballot_sync(FULL, rS <= e);
+            x0 += 31 - __clz(bal);
+            load_window(x0);
+        }
+        const uint32_t rend = min(min(e + 32, e1), winEnd);
+        const uint32_t ei = e + lane;
+        const bool ok = ei < rend;
+        e = rend;
+        int k = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1) {
+            const uint32_t v = __shfl_sync(FULL, rS, (k + st) & 31);
+            if (k + st < 32 && v <= ei) k += st;
+        }
+        const uint32_t x = ok ? x0 + k : 0xffffffffu;
+        uint64_t acc[NW];
+#pragma unroll
+        for (int j = 0; j < NW; ++j) acc[j] = 0;
+        if (ok) {
+            const uint32_t p = __ldg(col + ei);
+            if ((D.cur[p >> 5] >> (p & 31)) & 1) load_words<NW, VEC>(D.lab + (size_t)p * D.stride, acc);
+        }
+        // segmented inclusive OR-scan over lanes holding the same row
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t xo = __shfl_up_sync(FULL, x, o);
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                const uint64_t y = __shfl_up_sync(FULL, acc[j], o);
+                if (lane >= o && xo == x) acc[j] |= y;
+            }
+        }
+        const uint32_t xn = __shfl_down_sync(FULL, x, 1);
+        const bool seg_last = ok && (lane == 31 || xn != x);
+        uint64_t any = 0;
+#pragma unroll
+        for (int j = 0; j < NW; ++j) any |= acc[j];
+        if (seg_last && any) {
+            uint64_t *q = D.lab + (size_t)x * D.stride;
+            uint64_t cur[NW];
+            load_words<NW, VEC>(q, cur);
+            bool ch = false;
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                const uint64_t need = acc[j] & ~cur[j];
+                if (need) { red_or(q + j, need); ch = true; }
+            }
+            if (ch) red_or32(D.bits + (x >> 5), 1u << (x & 31));
+        }
+    }
+}
+
+// Phase B: turn the direction's next-frontier bitmap into the current
+// frontier (copied to D.cur) and work items, clearing it.  Each warp owns an
+// equal slice of the bitmap; set bits are spread across lanes (32 vertices per
+// round) and four rounds are batched so their row-pointer loads are in flight
+// together and one 64-bit atomicAdd reserves the slots (and edge offsets) of
+// up to 128 vertices.
+template <bool COUNT>
+__device__ __forceinline__ void compact_bitmap(const DirParams &D, uint32_t nwords, uint32_t gwarp, uint32_t nwarps,
+                                               unsigned long long *cnt_ptr, Ctrl *ctrl, uint32_t &nchanged) {
+    constexpr int R = 4;
+    const int lane = threadIdx.x & 31;
+    const uint32_t per = (nwords + nwarps - 1) / nwarps;
+    const uint32_t w0 = gwarp * per, w1 = min(w0 + per, nwords);
+    for (uint32_t g0 = w0; g0 < w1; g0 += 32) {
+        const uint32_t wi = g0 + lane;
+        const uint32_t bits = wi < w1 ? ld_cg32(D.bits + wi) : 0u;
+        if (wi < w1) {
+            D.cur[wi] = bits;
+            if (bits) D.bits[wi] = 0;
+        }
+        uint32_t tot = 0;
+        const uint32_t excl = warp_excl_scan_u32(__popc(bits), tot);
+        for (uint32_t t0 = 0; t0 < tot; t0 += 32 * R) {
+            uint32_t ys[R], b0[R], b1[R], d0[R], d1[R];
+            bool val[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t t = t0 + 32 * r + lane;
+                int k = 0;
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1) {
+                    const uint32_t v = __shfl_sync(FULL, excl, (k + st) & 31);
+                    if (k + st < 32 && v <= t) k += st;
+                }
+                const uint32_t ob = __shfl_sync(FULL, bits, k);
+                const uint32_t oe = __shfl_sync(FULL, excl, k);
+                val[r] = t < tot;
+                ys[r] = val[r] ? (g0 + k) * 32 + select_bit(ob, t - oe) : 0u;
+            }
+            uint32_t ni = 0, ne = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                b0[r] = b1[r] = d0[r] = d1[r] = 0;
+                if (val[r]) {
+                    b0[r] = __ldg(D.adj.ptr + ys[r]);
+                    b1[r] = __ldg(D.adj.ptr + ys[r] + 1);
+                    if (D.adj.dptr) {
+                        d0[r] = __ldg(D.adj.dptr + ys[r]);
+                        d1[r] = __ldg(D.adj.dptr + ys[r] + 1);
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                ni += (b1[r] > b0[r]) + (d1[r] > d0[r]);
+                ne += (b1[r] - b0[r]) + (d1[r] - d0[r]);
+                if (COUNT && val[r]) {
+                    const uint32_t bit = 1u << (ys[r] & 31);
+                    const uint32_t old = atomicOr(&D.changed_bits[ys[r] >> 5], bit);
+                    if (!(old & bit)) ++nchanged;
+                }
+            }
+            const uint32_t ii = warp_incl_scan(ni), ei = warp_incl_scan(ne);
+            const uint32_t ti = __shfl_sync(FULL, ii, 31), te = __shfl_sync(FULL, ei, 31);
+            if (ti == 0) continue;
+            unsigned long long base = 0;
+            if (lane == 31) base = atomicAdd(cnt_ptr, ((unsigned long long)ti << 32) | te);
+            base = __shfl_sync(FULL, base, 31);
+            const uint32_t ibase = (uint32_t)(base >> 32), ebase = (uint32_t)base;
+            if ((uint64_t)ibase + ti > D.cap) {
+                if (lane == 0) atomicOr(&ctrl->overflow, 1u);
+                continue;
+            }
+            uint32_t pos = ibase + ii - ni, eo = ebase + ei - ne;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (b1[r] > b0[r]) {
+                    D.q.x[pos] = ys[r]; D.q.start[pos] = b0[r]; D.q.len[pos] = b1[r] - b0[r]; D.q.eoff[pos] = eo;
+                    ++pos;
+                    eo += b1[r] - b0[r];
+                }
+                if (d1[r] > d0[r]) {
+                    D.q.x[pos] = ys[r]; D.q.start[pos] = d0[r]; D.q.len[pos] = (d1[r] - d0[r]) | DELTA_BIT;
+                    D.q.eoff[pos] = eo;
+                    ++pos;
+                    eo += d1[r] - d0[r];
+                }
+            }
+        }
+    }
+}
+
+template <int NW, bool VEC>
+__device__ __forceinline__ void relax_part(const DirParams &D, bool pull, uint32_t nitems, uint32_t a, uint32_t b,
+                                           uint32_t n, uint32_t mbase) {
+    if (!pull) {
+        expand_range<NW, VEC>(D, nitems, a, b);
+        return;
+    }
+    // pull space: base segment [0, mbase), then the delta segment
+    if (a < mbase) pull_range<NW, VEC>(D, D.padj.ptr, D.padj.col, n, a, b < mbase ? b : mbase);
+    if (b > mbase && D.padj.dptr)
+        pull_range<NW, VEC>(D, D.padj.dptr, D.padj.dcol, n, a > mbase ? a - mbase : 0u, b - mbase);
+}
+
+#ifndef DBL_FMINB
+#define DBL_FMINB 1
+#endif
 template <int NW, bool VEC, bool COUNT>
-__global__ void __launch_bounds__(FIX_THREADS) fixpoint_kernel(FixParams P) {
+__global__ void __launch_bounds__(FIX_THREADS, DBL_FMINB) fixpoint_kernel(FixParams P) {
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nwords = (P.n + 31) / 32;
     Ctrl *ctrl = P.ctrl;
     uint32_t nchanged[2] = {0, 0};
+    auto stamp_time = [&](uint32_t slot) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && slot < 64) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            ctrl->level_t[slot] = t;
+        }
+    };
     for (uint32_t L = 0; L < P.max_levels; ++L) {
-        const int c3 = L % 3, n3 = (L + 1) % 3, r3 = (L + 2) % 3;
-        const unsigned long long q0 = *(volatile unsigned long long *)&ctrl->cnt[c3][0];
-        const unsigned long long q1 = *(volatile unsigned long long *)&ctrl->cnt[c3][1];
+        const int cb = L & 1;
+        stamp_time(2 * L);
+        // phase B: next-frontier bitmaps -> current frontier + work items
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+            if ((P.active >> d) & 1) compact_bitmap<COUNT>(P.d[d], nwords, warp, nwarps, &ctrl->cnt[cb][d], ctrl, nchanged[d]);
+        grid.sync();
+        const unsigned long long q0 = *(volatile unsigned long long *)&ctrl->cnt[cb][0];
+        const unsigned long long q1 = *(volatile unsigned long long *)&ctrl->cnt[cb][1];
         if ((q0 | q1) == 0) {
             if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->levels = L;
             break;
         }
+        // phase A: push (edge-balanced over the frontier's items) or pull
+        // (edge-balanced over the whole reverse adjacency) per direction
+        const uint32_t n0 = (uint32_t)(q0 >> 32), n1 = (uint32_t)(q1 >> 32);
+        const uint64_t mall = P.m_base + P.m_delta;
+        const bool pull0 = P.pull_div && (uint64_t)(uint32_t)q0 * P.pull_div > mall;
+        const bool pull1 = P.pull_div && (uint64_t)(uint32_t)q1 * P.pull_div > mall;
+        const uint32_t E0 = pull0 ? (uint32_t)mall : (uint32_t)q0;
+        const uint32_t E1 = (q1 == 0) ? 0u : (pull1 ? (uint32_t)mall : (uint32_t)q1);
+        const uint32_t E0a = (q0 == 0) ? 0u : E0;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
-            ctrl->cnt[r3][0] = 0;
-            ctrl->cnt[r3][1] = 0;
+            ctrl->cnt[cb ^ 1][0] = 0;
+            ctrl->cnt[cb ^ 1][1] = 0;
+            ctrl->ticket[cb ^ 1] = 0;
+            if (L < 32) {
+                ctrl->level_edges[L] = (q0 & 0xffffffffull) + (q1 & 0xffffffffull);
+                ctrl->level_items[L] = (q0 >> 32) + (q1 >> 32) | ((unsigned long long)(pull0 | (pull1 << 1)) << 60);
+            }
         }
-        const uint32_t n0 = (uint32_t)(q0 >> 32), E0 = (uint32_t)q0;
-        const uint32_t n1 = (uint32_t)(q1 >> 32), E1 = (uint32_t)q1;
-        const uint64_t total = (uint64_t)E0 + E1;
-        // equal edge ranges per warp (multiple of 32)
+        stamp_time(2 * L + 1);
+        const uint64_t total = (uint64_t)E0a + E1;
+        // dynamic edge tickets: a warp grabs TICKET edges at a time, so slow
+        // ranges (hub destinations, L2 misses) do not hold the level back
+        // (small levels use a static equal split: the one failing ticket grab
+        // per warp would serialise on the counter)
+        constexpr uint32_t TICKET = 1024;
+        const bool dynamic = total > (uint64_t)nwarps * 512;
+        const uint64_t ntick = dynamic ? (total + TICKET - 1) / TICKET : nwarps;
         uint64_t per = (total + nwarps - 1) / nwarps;
         per = (per + 31) & ~31ull;
-        const uint64_t a = (uint64_t)warp * per, b = (a + per < total) ? a + per : total;
-        const int par = L & 1;
-        const uint32_t epoch = P.epoch0 + L + 1;
-        if (a < b) {
-            if (a < E0) {
-                const DirParams &D = P.d[0];
-                expand_range<NW, VEC, COUNT>(D, D.q[par], D.q[par ^ 1], n0, (uint32_t)a,
-                                             (uint32_t)(b < E0 ? b : (uint64_t)E0), epoch, &ctrl->cnt[n3][0], ctrl,
-                                             nchanged[0]);
+        for (uint32_t it = 0;; ++it) {
+            uint32_t t = 0;
+            if (dynamic) {
+                if (lane == 0) t = atomicAdd(&ctrl->ticket[cb], 1u);
+                t = __shfl_sync(FULL, t, 0);
+            } else {
+                t = it == 0 ? warp : 0xffffffffu;
             }
-            if (b > E0) {
-                const DirParams &D = P.d[1];
-                const uint32_t s = a > E0 ? (uint32_t)(a - E0) : 0u;
-                expand_range<NW, VEC, COUNT>(D, D.q[par], D.q[par ^ 1], n1, s, (uint32_t)(b - E0), epoch,
-                                             &ctrl->cnt[n3][1], ctrl, nchanged[1]);
-            }
+            if (t >= ntick) break;
+            const uint64_t sz = dynamic ? TICKET : per;
+            const uint64_t a = (uint64_t)t * sz, b = (a + sz < total) ? a + sz : total;
+            if (a >= b) break;
+            if (a < E0a)
+                relax_part<NW, VEC>(P.d[0], pull0, n0, (uint32_t)a, (uint32_t)(b < E0a ? b : (uint64_t)E0a), P.n,
+                                    (uint32_t)P.m_base);
+            if (b > E0a)
+                relax_part<NW, VEC>(P.d[1], pull1, n1, a > E0a ? (uint32_t)(a - E0a) : 0u, (uint32_t)(b - E0a), P.n,
+                                    (uint32_t)P.m_base);
         }
         grid.sync();
     }
@@ -423,65 +572,48 @@ __global__ void landmark_bits_kernel(uint64_t *__restrict__ rec, uint32_t rw, ui
     }
 }
 
-// Level-0 frontier: every vertex with a nonzero seed in the group's words.
+// Level-0 frontier bitmap: every vertex with a nonzero seed in the group's
+// words (one ballot per 32 consecutive vertices, no atomics).
 template <int NW>
 __global__ void init_frontier_kernel(FixParams P, uint32_t n, uint32_t active_mask) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t nr = ((uint64_t)n + 31) & ~31ull;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += stride) {
         const bool valid = i < n;
-        const uint32_t v = valid ? (uint32_t)i : 0;
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
             if (!((active_mask >> d) & 1)) continue;
             const DirParams &D = P.d[d];
             bool p = false;
             if (valid) {
-                const uint64_t *w = D.lab + (size_t)v * D.stride;
+                const uint64_t *w = D.lab + (size_t)i * D.stride;
                 uint64_t acc = 0;
 #pragma unroll
                 for (int k = 0; k < NW; ++k) acc |= w[k];
                 p = acc != 0;
-                if (p) D.stamp[v] = P.epoch0;
             }
-            warp_enqueue(D, D.q[0], p, v, &P.ctrl->cnt[0][d], P.ctrl);
+            const unsigned bal = __ballot_sync(FULL, p);
+            if ((threadIdx.x & 31) == 0) D.bits[i >> 5] = bal;
         }
     }
 }
 
 // Insertion seeds (updates.py:129-134 for a whole batch): for each new edge
-// u->v, in-words(v) |= in-words(u) and out-words(u) |= out-words(v).
-template <int NW, bool VEC, bool COUNT>
+// u->v, in-words(v) |= in-words(u) and out-words(u) |= out-words(v); changed
+// endpoints start the level-0 frontier.
+template <int NW, bool VEC>
 __global__ void insert_seed_kernel(FixParams P, const uint64_t *__restrict__ keys, uint64_t count) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t cr = (count + 31) & ~31ull;
-    uint32_t nchanged[2] = {0, 0};
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cr; i += stride) {
-        const bool valid = i < count;
-        const uint64_t key = valid ? keys[i] : 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = keys[i];
         const uint32_t u = (uint32_t)(key >> 32), v = (uint32_t)key;
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
             const DirParams &D = P.d[d];
             const uint32_t src = d == 0 ? u : v, dst = d == 0 ? v : u;
-            bool ch = false;
-            if (valid) {
-                uint64_t s[NW];
-                load_words<NW, VEC>(D.lab + (size_t)src * D.stride, s);
-                ch = relax<NW, VEC>(D, dst, s);
-                if (ch) atomicOr(&P.ctrl->seed_changed[d], 1u);
-            }
-            push_changed<COUNT>(D, D.q[0], ch, dst, P.epoch0, &P.ctrl->cnt[0][d], P.ctrl, nchanged[d]);
-        }
-    }
-    if (COUNT) {
-        const int lane = threadIdx.x & 31;
-#pragma unroll
-        for (int d = 0; d < 2; ++d) {
-            uint32_t x = nchanged[d];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
-            if (lane == 0 && x) atomicAdd(&P.ctrl->changed[d], (unsigned long long)x);
+            uint64_t s[NW];
+            load_words<NW, VEC>(D.lab + (size_t)src * D.stride, s);
+            if (relax_mark<NW, VEC>(D, dst, s)) atomicOr(&P.ctrl->seed_changed[d], 1u);
         }
     }
 }
@@ -565,20 +697,15 @@ static dbl_status launch_init_frontier(dbl_graph *g, FixParams &P, uint32_t nw, 
     return DBL_OK;
 }
 
-static dbl_status launch_insert_seed(dbl_graph *g, FixParams &P, uint32_t nw, bool vec, bool count,
+static dbl_status launch_insert_seed(dbl_graph *g, FixParams &P, uint32_t nw, bool vec, bool /*count*/,
                                      const uint64_t *keys, uint64_t nk) {
     int blocks = (int)((nk + 255) / 256);
     if (blocks > g->sm_count * 8) blocks = g->sm_count * 8;
     if (blocks < 1) blocks = 1;
 #define DBL_SEED_CASE(N)                                                                      \
     case N:                                                                                   \
-        if (count) {                                                                          \
-            if (vec) insert_seed_kernel<N, (N % 2 == 0), true><<<blocks, 256, 0, g->stream>>>(P, keys, nk); \
-            else insert_seed_kernel<N, false, true><<<blocks, 256, 0, g->stream>>>(P, keys, nk); \
-        } else {                                                                              \
-            if (vec) insert_seed_kernel<N, (N % 2 == 0), false><<<blocks, 256, 0, g->stream>>>(P, keys, nk); \
-            else insert_seed_kernel<N, false, false><<<blocks, 256, 0, g->stream>>>(P, keys, nk); \
-        }                                                                                     \
+        if (vec) insert_seed_kernel<N, (N % 2 == 0)><<<blocks, 256, 0, g->stream>>>(P, keys, nk); \
+        else insert_seed_kernel<N, false><<<blocks, 256, 0, g->stream>>>(P, keys, nk);       \
         break;
     switch (nw) {
         DBL_SEED_CASE(1) DBL_SEED_CASE(2) DBL_SEED_CASE(3) DBL_SEED_CASE(4)
@@ -594,27 +721,25 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
                                  uint32_t &nw, bool &vec, bool count, bool reset_counts = true) {
     dbl_status s = graph_ensure_traversal(g);
     if (s) return s;
-    // stamps: reset when the epoch could wrap during this run
-    const uint64_t need = (uint64_t)g->n + 8;
-    if ((uint64_t)g->epoch + need >= 0xfffffff0ull) {
-        DBL_CUDA(cudaMemsetAsync(g->stamp[0].p, 0, g->stamp[0].bytes, g->stream));
-        DBL_CUDA(cudaMemsetAsync(g->stamp[1].p, 0, g->stamp[1].bytes, g->stream));
-        g->epoch = 1;
-    }
+    const size_t bmw = ((size_t)g->n + 31) / 32;
+    DBL_CUDA(cudaMemsetAsync(g->stamp[0].p, 0, bmw * 4, g->stream));
+    DBL_CUDA(cudaMemsetAsync(g->stamp[1].p, 0, bmw * 4, g->stream));
     nw = 0;
     vec = true;
     for (int d = 0; d < 2; ++d) {
         DirParams &D = P.d[d];
         D.adj = d == 0 ? graph_fwd(g) : graph_rev(g);
+        D.padj = d == 0 ? graph_rev(g) : graph_fwd(g);
         D.stride = idx->rw;
-        D.stamp = g->stamp[d].as<uint32_t>();
+        D.bits = g->stamp[d].as<uint32_t>();
+        D.cur = D.bits + bmw + 1;
         D.cap = g->qcap;
-        for (int p = 0; p < 2; ++p) {
-            uint32_t *b = g->qbuf[d][p].as<uint32_t>();
-            D.q[p].x = b;
-            D.q[p].start = b + g->qcap;
-            D.q[p].len = b + 2ull * g->qcap;
-            D.q[p].eoff = b + 3ull * g->qcap;
+        {
+            uint32_t *b = g->qbuf[d][0].as<uint32_t>();
+            D.q.x = b;
+            D.q.start = b + g->qcap;
+            D.q.len = b + 2ull * g->qcap;
+            D.q.eoff = b + 3ull * g->qcap;
         }
         D.changed_bits = count ? g->changed_bits.as<uint32_t>() + d * (((size_t)g->n + 31) / 32) : nullptr;
         if (gr[d]) {
@@ -626,7 +751,15 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
         }
     }
     P.ctrl = g->ctrl.as<Ctrl>();
-    P.epoch0 = g->epoch;
+    P.m_base = g->m_base;
+    P.m_delta = g->m_delta;
+    {
+        static const char *pd = std::getenv("DBL_PULL_DIV");
+        // pull measured slower than push on cfg2 (r01): off unless asked for
+        P.pull_div = pd ? (uint32_t)std::atoi(pd) : 0u;   // 0 disables pull
+    }
+    P.n = g->n;
+    P.active = (gr[0] ? 1u : 0u) | (gr[1] ? 2u : 0u);
     P.max_levels = g->n + 4;
     DBL_CUDA(cudaMemsetAsync(P.ctrl, 0, sizeof(Ctrl), g->stream));
     if (count && reset_counts)
@@ -637,7 +770,6 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
 static dbl_status finish_run(dbl_graph *g, Ctrl *hctrl) {
     DBL_CUDA(cudaMemcpyAsync(hctrl, g->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, g->stream));
     DBL_CUDA(cudaStreamSynchronize(g->stream));
-    g->epoch += hctrl->levels + 2;
     if (hctrl->overflow) { set_error("frontier queue overflow"); return DBL_E_CUDA; }
     return DBL_OK;
 }
@@ -700,7 +832,14 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
         Ctrl h{};
         if ((s = finish_run(g, &h))) return s;
         trace("build: fixpoint", g->stream);
-        if (std::getenv("DBL_TRACE")) std::fprintf(stderr, "[dbl] fixpoint levels=%u nw=%u\n", h.levels, nw);
+        if (std::getenv("DBL_TRACE")) {
+            std::fprintf(stderr, "[dbl] fixpoint levels=%u nw=%u\n", h.levels, nw);
+            for (uint32_t l = 0; l < h.levels && l < 31; ++l)
+                std::fprintf(stderr, "[dbl]   level %2u items %9llu edges %10llu pull %llu compact %7.1f us  relax %7.1f us\n",
+                             l, h.level_items[l] & ((1ull << 60) - 1), h.level_edges[l], h.level_items[l] >> 60,
+                             (h.level_t[2 * l + 1] - h.level_t[2 * l]) / 1e3,
+                             (h.level_t[2 * l + 2] - h.level_t[2 * l + 1]) / 1e3);
+        }
     }
     DBL_CUDA(cudaEventRecord(g->ev[1], g->stream));
     DBL_CUDA(cudaEventSynchronize(g->ev[1]));

@@ -192,17 +192,8 @@ dbl_status graph_ensure_traversal(dbl_graph *g) {
     if (cap > 0xffffffffull) { set_error("frontier capacity overflow"); return DBL_E_CONFIG; }
     dbl_status s;
     for (int d = 0; d < 2; ++d) {
-        size_t sb = ((size_t)g->n + 1) * 4;
-        bool fresh = g->stamp[d].bytes < sb;
-        if ((s = g->stamp[d].ensure(sb))) return s;
-        if (fresh) {
-            DBL_CUDA(cudaMemsetAsync(g->stamp[d].p, 0, g->stamp[d].bytes, g->stream));
-            g->epoch = 1;
-            int other = d ^ 1;
-            if (g->stamp[other].p) DBL_CUDA(cudaMemsetAsync(g->stamp[other].p, 0, g->stamp[other].bytes, g->stream));
-        }
-        for (int p = 0; p < 2; ++p)
-            if ((s = g->qbuf[d][p].ensure(cap * 16))) return s;
+        if ((s = g->stamp[d].ensure((((size_t)g->n + 31) / 32 + 1) * 8))) return s;  // next + current bitmaps
+        if ((s = g->qbuf[d][0].ensure(cap * 16))) return s;
     }
     g->qcap = (uint32_t)cap;
     if ((s = g->ctrl.ensure(sizeof(Ctrl)))) return s;

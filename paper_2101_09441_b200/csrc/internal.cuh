@@ -100,23 +100,29 @@ struct Queue {
 
 // Device control block of one fixpoint run.
 struct Ctrl {
-    unsigned long long cnt[3][2];   // (items << 32 | edges) per [level % 3][direction]
+    unsigned long long cnt[2][2];   // (items << 32 | edges) per [level % 2][direction]
+    uint32_t ticket[2];              // relax-phase edge tickets per level % 2
     uint32_t levels;
     uint32_t overflow;
     uint32_t seed_changed[2];
     uint32_t pad;
     unsigned long long changed[2];   // distinct vertices whose label grew
     unsigned long long error;        // range errors etc.
+    unsigned long long level_edges[32];  // edges expanded per level (first 32 levels, both directions)
+    unsigned long long level_items[32];
+    unsigned long long level_t[64];       // globaltimer at each phase boundary (block 0)
 };
 
 // One direction of a fixpoint: label words [lab + v*stride, +nw) propagate
 // along `adj` (forward CSR for in-labels, reverse CSC for out-labels).
 struct DirParams {
-    Adj adj;
+    Adj adj;                  // push adjacency (forward for in-labels)
+    Adj padj;                 // pull adjacency (the opposite direction)
     uint64_t *lab;
     uint32_t stride;
-    uint32_t *stamp;
-    Queue q[2];
+    uint32_t *bits;           // next-frontier bitmap (n bits)
+    uint32_t *cur;            // current-frontier bitmap (pull levels)
+    Queue q;                  // current level's work items
     uint32_t cap;
     uint32_t *changed_bits;   // nullptr unless counting distinct changes
 };
@@ -124,7 +130,10 @@ struct DirParams {
 struct FixParams {
     DirParams d[2];
     Ctrl *ctrl;
-    uint32_t epoch0;
+    uint64_t m_base, m_delta;
+    uint32_t pull_div;        // a direction pulls when its frontier edges exceed m / pull_div
+    uint32_t n;
+    uint32_t active;          // bit d: direction d has words in this run
     uint32_t max_levels;
 };
 
@@ -141,9 +150,8 @@ struct dbl_graph {
     // delta adjacency (insertions since the last compaction)
     dbl::DevBuf dfptr, dfcol, drptr, drcol, dkeys_f, dkeys_r;
     // traversal workspace shared by builds/inserts on this graph
-    dbl::DevBuf stamp[2];
-    uint32_t epoch = 1;
-    dbl::DevBuf qbuf[2][2];   // [direction][parity] queue storage
+    dbl::DevBuf stamp[2];     // per-direction frontier bitmaps
+    dbl::DevBuf qbuf[2][2];   // [direction][0] work-item queue storage
     uint32_t qcap = 0;
     dbl::DevBuf ctrl;
     dbl::DevBuf changed_bits;

@@ -462,7 +462,14 @@ static size_t bfs_smem(int wdl, int wbl, bool dense) {
 // the table is appended to the global pending list and finished by the
 // 64-query group kernel (and, beyond that, the dense kernel).
 
-constexpr int QT = 128;            // queries per warp tile (4 per lane)
+#ifndef DBL_QPL
+#define DBL_QPL 2
+#endif
+#ifndef DBL_QMINB
+#define DBL_QMINB 3
+#endif
+constexpr int QPL = DBL_QPL;        // queries per lane
+constexpr int QT = 32 * QPL;       // queries per warp tile
 constexpr int WH = 128;            // per-warp BFS hash slots (power of two)
 constexpr int WHBITS = 7;
 constexpr int WT = 64;             // per-warp target table slots
@@ -672,15 +679,21 @@ __device__ void warp_bfs(WarpBfs<WDL, WBL> &B, uint32_t nb, const uint64_t *__re
 }
 
 __device__ __forceinline__ void flush_tile_codes(uint8_t *__restrict__ codes, uint32_t *__restrict__ visited,
-                                                 uint32_t count, uint64_t qb, int vec_ok, const uint8_t (&code)[4],
-                                                 const uint32_t (&vcount)[4]) {
-    if (vec_ok && qb + 3 < count) {
-        const uint32_t packed = code[0] | (code[1] << 8) | (code[2] << 16) | ((uint32_t)code[3] << 24);
-        *reinterpret_cast<uint32_t *>(codes + qb) = packed;
-        if (visited) *reinterpret_cast<uint4 *>(visited + qb) = make_uint4(vcount[0], vcount[1], vcount[2], vcount[3]);
+                                                 uint32_t count, uint64_t qb, int vec_ok, const uint8_t (&code)[QPL],
+                                                 const uint32_t (&vcount)[QPL]) {
+    if (vec_ok && qb + QPL - 1 < count) {
+        if constexpr (QPL == 4) {
+            const uint32_t packed = code[0] | (code[1] << 8) | (code[2] << 16) | ((uint32_t)code[3] << 24);
+            *reinterpret_cast<uint32_t *>(codes + qb) = packed;
+            if (visited) *reinterpret_cast<uint4 *>(visited + qb) = make_uint4(vcount[0], vcount[1], vcount[2], vcount[3]);
+        } else {
+            const uint16_t packed = (uint16_t)(code[0] | (code[1] << 8));
+            *reinterpret_cast<uint16_t *>(codes + qb) = packed;
+            if (visited) *reinterpret_cast<uint2 *>(visited + qb) = make_uint2(vcount[0], vcount[1]);
+        }
     } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < QPL; ++j) {
             if (qb + j >= count) break;
             codes[qb + j] = code[j];
             if (visited) visited[qb + j] = vcount[j];
@@ -689,8 +702,13 @@ __device__ __forceinline__ void flush_tile_codes(uint8_t *__restrict__ codes, ui
 }
 
 // Run the warp's staged batch (B.nq queries) and write its answers.
+#ifdef DBL_BFS_NOINLINE
+#define DBL_BFS_INLINE __noinline__
+#else
+#define DBL_BFS_INLINE
+#endif
 template <int WDL, int WBL>
-__device__ void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64_t *__restrict__ rec, const Adj &adj,
+__device__ DBL_BFS_INLINE void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64_t *__restrict__ rec, const Adj &adj,
                                bool prune_dl, bool prune_bl, uint8_t *__restrict__ codes,
                                uint32_t *__restrict__ visited, uint32_t *__restrict__ pending,
                                uint32_t *__restrict__ counters, cudaGraphConditionalHandle hard) {
@@ -733,7 +751,7 @@ __device__ void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64_t *__restrict_
 }
 
 template <int WDL, int WBL>
-__global__ void __launch_bounds__(FUSED_THREADS)
+__global__ void __launch_bounds__(FUSED_THREADS, DBL_QMINB)
 query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const QueryDesc *__restrict__ qd,
                    uint32_t *__restrict__ pending, uint32_t *__restrict__ counters,
                    cudaGraphConditionalHandle hard) {
@@ -758,26 +776,35 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
         tile = __shfl_sync(FULL, tile, 0);
         const uint64_t q0 = (uint64_t)tile * QT;
         if (q0 >= count) break;
-        const uint64_t qb = q0 + 4 * lane;
-        uint32_t us[4], vs[4];
-        if (vec_ok && qb + 3 < count) {
-            const uint4 a = __ldg(reinterpret_cast<const uint4 *>(qu + qb));
-            const uint4 b = __ldg(reinterpret_cast<const uint4 *>(qv + qb));
-            us[0] = a.x; us[1] = a.y; us[2] = a.z; us[3] = a.w;
-            vs[0] = b.x; vs[1] = b.y; vs[2] = b.z; vs[3] = b.w;
+        const uint64_t qb = q0 + QPL * lane;
+        uint32_t us[QPL], vs[QPL];
+        if (vec_ok && qb + QPL - 1 < count) {
+            if constexpr (QPL == 4) {
+                const uint4 a = __ldg(reinterpret_cast<const uint4 *>(qu + qb));
+                const uint4 b = __ldg(reinterpret_cast<const uint4 *>(qv + qb));
+                us[0] = a.x; us[1] = a.y; us[2] = a.z; us[3] = a.w;
+                vs[0] = b.x; vs[1] = b.y; vs[2] = b.z; vs[3] = b.w;
+            } else {
+                const uint2 a = __ldg(reinterpret_cast<const uint2 *>(qu + qb));
+                const uint2 b = __ldg(reinterpret_cast<const uint2 *>(qv + qb));
+                us[0] = a.x; us[1] = a.y;
+                vs[0] = b.x; vs[1] = b.y;
+            }
         } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < QPL; ++j) {
                 us[j] = qb + j < count ? __ldg(qu + qb + j) : 0;
                 vs[j] = qb + j < count ? __ldg(qv + qb + j) : 0;
             }
         }
-        uint8_t code[4];
-        uint32_t vcount[4] = {0, 0, 0, 0};
-        unsigned unres = 0;
-        uint64_t ra[4][RW], rb[4][RW];
+        uint8_t code[QPL];
+        uint32_t vcount[QPL];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < QPL; ++j) vcount[j] = 0;
+        unsigned unres = 0;
+        uint64_t ra[QPL][RW], rb[QPL][RW];
+#pragma unroll
+        for (int j = 0; j < QPL; ++j) {
             const bool inb = qb + j < count;
             const bool ok = inb && us[j] < n && vs[j] < n && us[j] != vs[j];
             if (ok) {
@@ -786,7 +813,7 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
             }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < QPL; ++j) {
             const bool inb = qb + j < count;
             code[j] = UNRESOLVED;
             if (!inb) { code[j] = 0xfd; continue; }
@@ -827,7 +854,7 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
             const uint32_t take = min(32u - nq, tot - done_upto);
             uint32_t pos = off;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < QPL; ++j) {
                 if (!((unres >> j) & 1)) continue;
                 if (pos >= done_upto && pos < done_upto + take) {
                     const uint32_t bi = nq + pos - done_upto;
@@ -990,8 +1017,8 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     const bool grown = cap != g->q_pending_cap;
     g->q_pending_cap = cap;
     QueryDesc hd{u, v, codes, visited, (uint32_t)count, flags, 0, 0};
-    hd.vec_ok = ((((uintptr_t)u) | ((uintptr_t)v)) & 15) == 0 && (((uintptr_t)codes) & 3) == 0 &&
-                (!visited || (((uintptr_t)visited) & 15) == 0);
+    hd.vec_ok = ((((uintptr_t)u) | ((uintptr_t)v)) & (4 * QPL - 1)) == 0 && (((uintptr_t)codes) & (QPL - 1)) == 0 &&
+                (!visited || (((uintptr_t)visited) & (4 * QPL - 1)) == 0);
     DBL_CUDA(cudaMemcpyAsync(g->q_desc.p, &hd, sizeof(hd), cudaMemcpyHostToDevice, g->stream));
     fused_fn fused = nullptr;
     size_t fsmem = 0;
@@ -1008,6 +1035,31 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
             last_fn = (const void *)fused;
         }
         const int fgrid = g->sm_count * fbps;
+        if (std::getenv("DBL_NO_GRAPH")) {
+            // plain launches (profilers that skip graph nodes): same kernels, the
+            // hard path always launched
+            uint32_t *pending = g->q_pending.as<uint32_t>();
+            uint32_t *counters = g->q_counters.as<uint32_t>();
+            uint32_t *ovf = pending + g->q_pending_cap + 16;
+            const QueryDesc *qd = g->q_desc.as<QueryDesc>();
+            DBL_CUDA(cudaMemsetAsync(counters, 0, CNT_WORDS * 4, g->stream));
+            DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
+            fused<<<fgrid, FUSED_THREADS, fsmem, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, graph_fwd(g), qd,
+                                                              pending, counters, (cudaGraphConditionalHandle)0);
+            DBL_CHECK_LAUNCH("query_fused_kernel");
+            DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
+            Adj adj = graph_fwd(g);
+            bfs_kernel<false><<<hp.grid, BFS_THREADS, hp.smem, g->stream>>>(idx->rec.as<uint64_t>(), idx->wdl,
+                                                                            idx->wbl, idx->n, adj, qd, pending,
+                                                                            counters, ovf, nullptr);
+            DBL_CHECK_LAUNCH("bfs_kernel");
+            bfs_kernel<true><<<hp.dctas, BFS_THREADS, hp.dsmem, g->stream>>>(idx->rec.as<uint64_t>(), idx->wdl,
+                                                                             idx->wbl, idx->n, adj, qd, pending,
+                                                                             counters, ovf, g->q_dense.as<char>());
+            DBL_CHECK_LAUNCH("bfs_kernel_dense");
+            DBL_CUDA(cudaEventRecord(g->ev[4], g->stream));
+            return DBL_OK;
+        }
         // the graph bakes in device pointers: rebuild when any of them moved
         const void *key[6] = {idx, idx->rec.p, g->fptr.p, g->m_delta ? g->dfptr.p : nullptr,
                               g->q_pending.p, g->q_dense.p};
