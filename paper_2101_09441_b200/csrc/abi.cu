@@ -684,6 +684,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     if (!u || !v) { set_error("null argument"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
     set_stream(g->stream);
+    trace("insert: enter", g->stream);
     DevBuf in, keys, alt, newk, err;
     auto cleanup = [&]() { in.release(); keys.release(); alt.release(); newk.release(); err.release(); };
     if ((s = keys.ensure(count * 8)) || (s = alt.ensure(count * 8)) || (s = newk.ensure(count * 8)) ||
@@ -726,12 +727,15 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
         nsel.release();
         count = nu;
     }
+    trace("insert: sort+unique", g->stream);
     if ((s = count_certified(g, idx, uniq, count, &st.certified))) { cleanup(); return s; }
     uint64_t nnew = 0;
     if ((s = graph_filter_new(g, uniq, count, newk.as<uint64_t>(), &nnew))) { cleanup(); return s; }
     st.inserted = nnew;
+    trace("insert: certified+filter", g->stream);
     if (nnew) {
         if ((s = graph_insert_delta(g, newk.as<uint64_t>(), nnew))) { cleanup(); return s; }
+        trace("insert: delta merge", g->stream);
         uint32_t changed[2], seedc[2], levels = 0;
         if ((s = run_insert(g, idx, newk.as<uint64_t>(), nnew, true, changed, seedc, &levels))) {
             cleanup();

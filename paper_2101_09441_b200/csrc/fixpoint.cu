@@ -171,7 +171,7 @@ __device__ __forceinline__ uint32_t find_item(const uint32_t *eoff, uint32_t lo,
 template <int NW, bool VEC>
 __device__ __forceinline__ void expand_range(const DirParams &D, uint32_t nitems, uint32_t e0, uint32_t e1) {
 #ifndef DBL_FU
-#define DBL_FU 4
+#define DBL_FU 2
 #endif
     constexpr int U = NW <= 2 ? DBL_FU : (NW <= 4 ? 2 : 1);
     const Queue &Q = D.q;
@@ -443,7 +443,7 @@ __device__ __forceinline__ void relax_part(const DirParams &D, bool pull, uint32
 }
 
 #ifndef DBL_FMINB
-#define DBL_FMINB 1
+#define DBL_FMINB 4
 #endif
 template <int NW, bool VEC, bool COUNT>
 __global__ void __launch_bounds__(FIX_THREADS, DBL_FMINB) fixpoint_kernel(FixParams P) {
@@ -538,26 +538,34 @@ __global__ void __launch_bounds__(FIX_THREADS, DBL_FMINB) fixpoint_kernel(FixPar
 
 // ------------------------------------------------------- seeds & frontier --
 
-// rec := seeds.  bl_in bit bucket[v] for source leaves, bl_out for sinks;
-// dl words zero (landmark bits are added by landmark_bits_kernel).
+// rec := seeds, one thread per vertex writing its whole record (16-byte
+// stores when every word is selected).  bl_in bit bucket[v] for source
+// leaves, bl_out for sinks; dl words zero (landmark bits are added by
+// landmark_bits_kernel).
 __global__ void seed_records_kernel(uint64_t *__restrict__ rec, uint32_t n, uint32_t wdl, uint32_t wbl,
                                     const uint8_t *__restrict__ flags, const uint32_t *__restrict__ bucket,
                                     uint64_t wmask) {
-    const uint32_t rw = 2 * (wdl + wbl), H = wdl + wbl;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * rw;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t v = (uint32_t)(i / rw), w = (uint32_t)(i % rw);
-        if (!((wmask >> w) & 1)) continue;
-        uint64_t val = 0;
-        const uint32_t h = w < H ? 0 : 1, ww = w - h * H;
-        if (ww >= wdl) {
-            const uint8_t f = flags[v];
-            const uint32_t b = bucket[v];
-            if ((f >> h) & 1) {
-                if (b / 64 == ww - wdl) val = 1ull << (b % 64);
+    const uint32_t H = wdl + wbl, rw = 2 * H;
+    const bool all = (rw >= 64) ? wmask == ~0ull : (wmask & ((1ull << rw) - 1)) == ((1ull << rw) - 1);
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint8_t f = flags[v];
+        const uint32_t b = bucket[v];
+        uint64_t *r = rec + (size_t)v * rw;
+        // word index of the bucket bit in each half (or none)
+        const uint32_t win = (f & 1) ? wdl + b / 64 : 0xffffffffu;
+        const uint32_t wout = (f & 2) ? H + wdl + b / 64 : 0xffffffffu;
+        const uint64_t bit = 1ull << (b % 64);
+        if (all) {
+            for (uint32_t w = 0; w < rw; w += 2) {
+                ulonglong2 val;
+                val.x = (w == win || w == wout) ? bit : 0ull;
+                val.y = (w + 1 == win || w + 1 == wout) ? bit : 0ull;
+                *reinterpret_cast<ulonglong2 *>(r + w) = val;
             }
+        } else {
+            for (uint32_t w = 0; w < rw; ++w)
+                if ((wmask >> w) & 1) r[w] = (w == win || w == wout) ? bit : 0ull;
         }
-        rec[i] = val;
     }
 }
 
@@ -572,29 +580,41 @@ __global__ void landmark_bits_kernel(uint64_t *__restrict__ rec, uint32_t rw, ui
     }
 }
 
-// Level-0 frontier bitmap: every vertex with a nonzero seed in the group's
-// words (one ballot per 32 consecutive vertices, no atomics).
-template <int NW>
-__global__ void init_frontier_kernel(FixParams P, uint32_t n, uint32_t active_mask) {
+// Level-0 frontier bitmaps straight from the metadata: vertex v starts
+// direction d's frontier iff it seeds one of the words [w0_d, w0_d + nw_d) of
+// that half -- a leaf of side d whose bucket word is in range, or a landmark
+// whose DL word is (landmark_frontier_kernel).  One ballot per 32 vertices.
+__global__ void leaf_frontier_kernel(uint32_t *__restrict__ bits0, uint32_t *__restrict__ bits1, uint32_t n,
+                                     uint32_t wdl, uint32_t H, const uint8_t *__restrict__ flags,
+                                     const uint32_t *__restrict__ bucket, uint32_t a0, uint32_t e0, uint32_t a1,
+                                     uint32_t e1) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t nr = ((uint64_t)n + 31) & ~31ull;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += stride) {
-        const bool valid = i < n;
-#pragma unroll
-        for (int d = 0; d < 2; ++d) {
-            if (!((active_mask >> d) & 1)) continue;
-            const DirParams &D = P.d[d];
-            bool p = false;
-            if (valid) {
-                const uint64_t *w = D.lab + (size_t)i * D.stride;
-                uint64_t acc = 0;
-#pragma unroll
-                for (int k = 0; k < NW; ++k) acc |= w[k];
-                p = acc != 0;
+        bool p0 = false, p1 = false;
+        if (i < n) {
+            const uint8_t f = flags[i];
+            if (f) {
+                const uint32_t bw = wdl + bucket[i] / 64;
+                p0 = (f & 1) && bw >= a0 && bw < e0;
+                p1 = (f & 2) && H + bw >= a1 && H + bw < e1;
             }
-            const unsigned bal = __ballot_sync(FULL, p);
-            if ((threadIdx.x & 31) == 0) D.bits[i >> 5] = bal;
         }
+        const unsigned b0 = __ballot_sync(FULL, p0), b1 = __ballot_sync(FULL, p1);
+        if ((threadIdx.x & 31) == 0) {
+            if (bits0) bits0[i >> 5] = b0;
+            if (bits1) bits1[i >> 5] = b1;
+        }
+    }
+}
+
+__global__ void landmark_frontier_kernel(uint32_t *__restrict__ bits0, uint32_t *__restrict__ bits1, uint32_t H,
+                                         const uint32_t *__restrict__ lm, uint32_t k, uint32_t a0, uint32_t e0,
+                                         uint32_t a1, uint32_t e1) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
+        const uint32_t v = lm[i], w = i / 64;
+        if (bits0 && w >= a0 && w < e0) atomicOr(&bits0[v >> 5], 1u << (v & 31));
+        if (bits1 && H + w >= a1 && H + w < e1) atomicOr(&bits1[v >> 5], 1u << (v & 31));
     }
 }
 
@@ -682,18 +702,23 @@ static dbl_status launch_fixpoint(dbl_graph *g, FixParams &P, uint32_t nw, bool 
 #undef DBL_FIX_CASE
 }
 
-static dbl_status launch_init_frontier(dbl_graph *g, FixParams &P, uint32_t nw, uint32_t mask) {
+static dbl_status launch_init_frontier(dbl_graph *g, dbl_index *idx, const Group *pair[2]) {
+    const uint32_t H = idx->wdl + idx->wbl;
+    uint32_t *b0 = pair[0] ? g->stamp[0].as<uint32_t>() : nullptr;
+    uint32_t *b1 = pair[1] ? g->stamp[1].as<uint32_t>() : nullptr;
+    const uint32_t a0 = pair[0] ? pair[0]->w0 : 0, e0 = pair[0] ? pair[0]->w0 + pair[0]->nw : 0;
+    const uint32_t a1 = pair[1] ? pair[1]->w0 : 0, e1 = pair[1] ? pair[1]->w0 + pair[1]->nw : 0;
     int blocks = (int)(((uint64_t)g->n + 255) / 256);
     if (blocks > g->sm_count * 8) blocks = g->sm_count * 8;
     if (blocks < 1) blocks = 1;
-#define DBL_INIT_CASE(N) case N: init_frontier_kernel<N><<<blocks, 256, 0, g->stream>>>(P, g->n, mask); break;
-    switch (nw) {
-        DBL_INIT_CASE(1) DBL_INIT_CASE(2) DBL_INIT_CASE(3) DBL_INIT_CASE(4)
-        DBL_INIT_CASE(5) DBL_INIT_CASE(6) DBL_INIT_CASE(7) DBL_INIT_CASE(8)
-    default: set_error("bad word-group width"); return DBL_E_CONFIG;
+    leaf_frontier_kernel<<<blocks, 256, 0, g->stream>>>(b0, b1, g->n, idx->wdl, H, idx->leaf_flags.as<uint8_t>(),
+                                                         idx->bucket.as<uint32_t>(), a0, e0, a1, e1);
+    DBL_CHECK_LAUNCH("leaf_frontier_kernel");
+    if (idx->cfg.k) {
+        landmark_frontier_kernel<<<(idx->cfg.k + 255) / 256, 256, 0, g->stream>>>(
+            b0, b1, H, idx->landmarks.as<uint32_t>(), idx->cfg.k, a0, e0, a1, e1);
+        DBL_CHECK_LAUNCH("landmark_frontier_kernel");
     }
-#undef DBL_INIT_CASE
-    DBL_CHECK_LAUNCH("init_frontier_kernel");
     return DBL_OK;
 }
 
@@ -777,7 +802,7 @@ static dbl_status finish_run(dbl_graph *g, Ctrl *hctrl) {
 dbl_status index_seed_records(dbl_graph *g, dbl_index *idx, uint64_t wmask) {
     const uint64_t total = (uint64_t)idx->n * idx->rw;
     if (!total) return DBL_OK;
-    int blocks = (int)((total + 255) / 256 < (uint64_t)g->sm_count * 16 ? (total + 255) / 256 : g->sm_count * 16);
+    int blocks = (int)((idx->n + 255) / 256 < (uint32_t)g->sm_count * 8 ? (idx->n + 255) / 256 : g->sm_count * 8);
     seed_records_kernel<<<blocks, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, idx->wdl, idx->wbl,
                                                        idx->leaf_flags.as<uint8_t>(), idx->bucket.as<uint32_t>(),
                                                        wmask);
@@ -825,8 +850,7 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
         uint32_t nw = 0;
         bool vec = true;
         if ((s = prepare_params(g, idx, pair, P, nw, vec, false))) return s;
-        const uint32_t mask = (pair[0] ? 1u : 0u) | (pair[1] ? 2u : 0u);
-        if ((s = launch_init_frontier(g, P, nw, mask))) return s;
+        if ((s = launch_init_frontier(g, idx, pair))) return s;
         trace("build: init frontier", g->stream);
         if ((s = launch_fixpoint<false>(g, P, nw, vec))) return s;
         Ctrl h{};
@@ -877,6 +901,15 @@ dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, ui
         }
         Ctrl h{};
         if ((s = finish_run(g, &h))) return s;
+        trace("insert: fixpoint", g->stream);
+        if (std::getenv("DBL_TRACE")) {
+            std::fprintf(stderr, "[dbl] insert fixpoint levels=%u nw=%u\n", h.levels, nw);
+            for (uint32_t l = 0; l < h.levels && l < 31; ++l)
+                std::fprintf(stderr, "[dbl]   level %2u items %9llu edges %10llu compact %7.1f us  relax %7.1f us\n",
+                             l, h.level_items[l] & ((1ull << 60) - 1), h.level_edges[l],
+                             (h.level_t[2 * l + 1] - h.level_t[2 * l]) / 1e3,
+                             (h.level_t[2 * l + 2] - h.level_t[2 * l + 1]) / 1e3);
+        }
         // the change bitmap persists across groups, so counts stay distinct
         changed_out[0] += (uint32_t)h.changed[0];
         changed_out[1] += (uint32_t)h.changed[1];

@@ -263,7 +263,7 @@ dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, 
 static dbl_status merge_into(dbl_graph *g, DevBuf &dst, uint64_t nd, const uint64_t *add,
                              uint64_t na, DevBuf &tmpbuf) {
     if (nd + na >= (1ull << 31)) { set_error("delta adjacency too large to merge"); return DBL_E_CONFIG; }
-    dbl_status s = tmpbuf.ensure((nd + na) * 8 + 8);
+    dbl_status s = tmpbuf.ensure_geometric((nd + na) * 8 + 8);
     if (s) return s;
     size_t tmp = 0;
     DBL_CUDA(cub::DeviceMerge::MergeKeys(nullptr, tmp, dst.as<uint64_t>(), (int)nd, add, (int)na,
@@ -282,6 +282,33 @@ dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t
     dbl_status s;
     uint32_t n = g->n;
     uint64_t nd = g->m_delta;
+    // Size every delta buffer for the largest delta before the next
+    // compaction (m_base / 4 + a batch), so steady-state inserts never hit
+    // cudaMalloc.
+    {
+        const uint64_t need = nd + count;
+        uint64_t cap = g->m_base / 4 + 2 * count + 1024;
+        if (cap < need) cap = need + need / 2;
+        DevBuf *kb[3] = {&g->dkeys_f, &g->dkeys_r, &g->dmerge};
+        for (DevBuf *b : kb) {
+            if (b->bytes < need * 8 + 8) {
+                if (b == &g->dkeys_f || b == &g->dkeys_r) {
+                    if (nd) {  // keep the contents
+                        DevBuf nb;
+                        if ((s = nb.ensure(cap * 8 + 8))) return s;
+                        DBL_CUDA(cudaMemcpyAsync(nb.p, b->p, nd * 8, cudaMemcpyDeviceToDevice, g->stream));
+                        b->release();
+                        *b = nb;
+                        continue;
+                    }
+                }
+                b->release();
+                if ((s = b->ensure(cap * 8 + 8))) return s;
+            }
+        }
+        if (g->dfcol.bytes < need * 4 + 4) { g->dfcol.release(); if ((s = g->dfcol.ensure(cap * 4 + 4))) return s; }
+        if (g->drcol.bytes < need * 4 + 4) { g->drcol.release(); if ((s = g->drcol.ensure(cap * 4 + 4))) return s; }
+    }
     // reverse keys of the new edges, sorted
     if ((s = g->scratch_a.ensure(count * 8 + 8)) || (s = g->scratch_b.ensure(count * 8 + 8))) return s;
     uint64_t *ra = g->scratch_a.as<uint64_t>(), *rb = g->scratch_b.as<uint64_t>();
@@ -289,21 +316,22 @@ dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t
     DBL_CHECK_LAUNCH("swap_keys_kernel");
     uint64_t *rsorted = nullptr;
     if ((s = sort_keys(g, ra, rb, count, key_end_bit(n), &rsorted))) return s;
+    trace("delta: reverse sort", g->stream);
     if (nd == 0) {
-        if ((s = g->dkeys_f.ensure(count * 8 + 8)) || (s = g->dkeys_r.ensure(count * 8 + 8))) return s;
+        if ((s = g->dkeys_f.ensure_geometric(count * 8 + 8)) || (s = g->dkeys_r.ensure_geometric(count * 8 + 8)))
+            return s;
         DBL_CUDA(cudaMemcpyAsync(g->dkeys_f.p, new_keys_f, count * 8, cudaMemcpyDeviceToDevice, g->stream));
         DBL_CUDA(cudaMemcpyAsync(g->dkeys_r.p, rsorted, count * 8, cudaMemcpyDeviceToDevice, g->stream));
     } else {
-        DevBuf t1;
-        if ((s = merge_into(g, g->dkeys_f, nd, new_keys_f, count, t1))) { t1.release(); return s; }
-        t1.release();
-        DevBuf t2;
-        if ((s = merge_into(g, g->dkeys_r, nd, rsorted, count, t2))) { t2.release(); return s; }
-        t2.release();
+        // merged keys go to the spare buffer, which then swaps with the old one
+        if ((s = merge_into(g, g->dkeys_f, nd, new_keys_f, count, g->dmerge))) return s;
+        trace("delta: merge fwd", g->stream);
+        if ((s = merge_into(g, g->dkeys_r, nd, rsorted, count, g->dmerge))) return s;
+        trace("delta: merge rev", g->stream);
     }
     uint64_t m = nd + count;
     if ((s = g->dfptr.ensure(((size_t)n + 1) * 4)) || (s = g->drptr.ensure(((size_t)n + 1) * 4)) ||
-        (s = g->dfcol.ensure(m * 4 + 4)) || (s = g->drcol.ensure(m * 4 + 4)))
+        (s = g->dfcol.ensure_geometric(m * 4 + 4)) || (s = g->drcol.ensure_geometric(m * 4 + 4)))
         return s;
     if ((s = build_csr_from_sorted(g, g->dkeys_f.as<uint64_t>(), m, n, g->dfptr.as<uint32_t>(),
                                    g->dfcol.as<uint32_t>())))
@@ -311,6 +339,7 @@ dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t
     if ((s = build_csr_from_sorted(g, g->dkeys_r.as<uint64_t>(), m, n, g->drptr.as<uint32_t>(),
                                    g->drcol.as<uint32_t>())))
         return s;
+    trace("delta: csr+csc", g->stream);
     g->m_delta = m;
     ++g->topo_version;
     return graph_ensure_traversal(g);
@@ -426,7 +455,7 @@ extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
     set_stream(g->stream);
     if (g->stream) cudaStreamSynchronize(g->stream);
     DevBuf *bufs[] = {&g->fptr, &g->fcol, &g->rptr, &g->rcol, &g->dfptr, &g->dfcol, &g->drptr,
-                      &g->drcol, &g->dkeys_f, &g->dkeys_r, &g->stamp[0], &g->stamp[1],
+                      &g->drcol, &g->dkeys_f, &g->dkeys_r, &g->dmerge, &g->stamp[0], &g->stamp[1],
                       &g->qbuf[0][0], &g->qbuf[0][1], &g->qbuf[1][0], &g->qbuf[1][1], &g->ctrl,
                       &g->changed_bits, &g->cub_tmp, &g->scratch_a, &g->scratch_b, &g->scratch_c,
                       &g->scratch_d, &g->q_in, &g->q_codes, &g->q_vis, &g->q_pending,

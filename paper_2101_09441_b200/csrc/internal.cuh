@@ -58,6 +58,13 @@ struct DevBuf {
         bytes = nb;
         return DBL_OK;
     }
+    // grow by at least 1.5x so arrays that creep upward (delta adjacency)
+    // are not reallocated on every call
+    dbl_status ensure_geometric(size_t need) {
+        if (need <= bytes) return DBL_OK;
+        const size_t grown = bytes + bytes / 2;
+        return ensure(need > grown ? need : grown);
+    }
     template <class T> T *as() const { return reinterpret_cast<T *>(p); }
     void release() { if (p) pool_free(p, bytes, dev); p = nullptr; bytes = 0; }
 };
@@ -148,7 +155,7 @@ struct dbl_graph {
     // base adjacency
     dbl::DevBuf fptr, fcol, rptr, rcol;
     // delta adjacency (insertions since the last compaction)
-    dbl::DevBuf dfptr, dfcol, drptr, drcol, dkeys_f, dkeys_r;
+    dbl::DevBuf dfptr, dfcol, drptr, drcol, dkeys_f, dkeys_r, dmerge;
     // traversal workspace shared by builds/inserts on this graph
     dbl::DevBuf stamp[2];     // per-direction frontier bitmaps
     dbl::DevBuf qbuf[2][2];   // [direction][0] work-item queue storage
