@@ -327,8 +327,8 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": traffic, "peak_source": peak_src,
                      "bytes_per_query": q_bytes, "kernel_ms": k6_ms},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": 8 * BATCH,
-                "d2h_bytes_per_step": BATCH, "api": "dbl_query(mem=DBL_MEM_HOST), pinned buffers, "
-                "answer codes returned; H2D/kernels/D2H pipelined in 256k-query chunks",
+                "d2h_bytes_per_step": BATCH, "api": "dbl_query(mem=DBL_MEM_HOST) on pinned buffers: the kernels "
+                "read the pairs and write the codes over PCIe (zero-copy); answer codes returned",
                 "with_visited_counts": {"value": e2e_vis_value, "d2h_bytes_per_step": 5 * BATCH}},
         "gpu_launches": int(launches),
         "clocks": clocks,
@@ -391,6 +391,7 @@ def run_reference(args):
     n, src, dst, qu, qv = make_workload(0)
     cores = os.cpu_count() or 1
     og = O.OracleGraph(n, src, dst)
+    m = og.edge_count
     t0 = time.perf_counter()
     oidx = og.build(64, 64, threads=cores)
     build_s = time.perf_counter() - t0
@@ -415,7 +416,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded R-MAT; no dataset)", "impl": "reference",
-            "config": {"workload": WORKLOAD, "n": n, "m": og.edge_count, "queries_per_step": BATCH,
+            "config": {"workload": WORKLOAD, "n": n, "m": m, "queries_per_step": BATCH,
                        "k": 64, "k_prime": 64},
             "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "port",
                              "sample": sample},

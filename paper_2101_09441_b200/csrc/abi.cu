@@ -585,8 +585,32 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
     set_stream(g->stream);
-    if (mem == DBL_MEM_HOST && count) return query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
-    if ((s = run_query(idx, g, u, v, count, flags, codes, visited))) return s;
+    if (mem == DBL_MEM_HOST && count) {
+        // Page-locked host buffers are read and written by the query kernels
+        // directly over PCIe (zero-copy): the transfer streams under the
+        // label checks instead of being staged.  Pageable memory goes
+        // through the chunked copy pipeline.
+        const void *ptrs[4] = {u, v, codes, visited};
+        void *dptr[4] = {nullptr, nullptr, nullptr, nullptr};
+        bool pinned = !std::getenv("DBL_NO_ZEROCOPY");
+        for (int i = 0; i < 4 && pinned; ++i) {
+            if (!ptrs[i]) continue;
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, ptrs[i]) != cudaSuccess || at.type != cudaMemoryTypeHost ||
+                !at.devicePointer) {
+                cudaGetLastError();
+                pinned = false;
+            } else {
+                dptr[i] = at.devicePointer;
+            }
+        }
+        if (!pinned) return query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
+        if ((s = run_query(idx, g, (const uint32_t *)dptr[0], (const uint32_t *)dptr[1], count, flags,
+                           (uint8_t *)dptr[2], (uint32_t *)dptr[3])))
+            return s;
+    } else if ((s = run_query(idx, g, u, v, count, flags, codes, visited))) {
+        return s;
+    }
     if (!sync) return DBL_OK;
     uint32_t err = 0;
     if ((s = query_finish(g, &err))) return s;
