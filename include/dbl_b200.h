@@ -234,6 +234,16 @@ dbl_status dbl_index_pack_words(const dbl_index *idx, const uint32_t *words, uin
 dbl_status dbl_index_unpack_words(dbl_index *idx, const uint32_t *words, uint32_t nw,
                                   const uint64_t *dev_slab, void *cuda_stream);
 
+/* ------------------------------------------------------------ verifier */
+/* verify_labels (updates.py:323-363) on the device: the union-fixpoint
+ * check over every (vertex, half) and, if `exhaustive`, a diff against a
+ * fresh rebuild from the frozen metadata.  Writes up to max_out violation
+ * rows (vertex, half 0 = in / 1 = out, expected and actual half words,
+ * ceil(k/64)+ceil(k'/64) each, dl words first); *out_count = total found. */
+dbl_status dbl_verify(const dbl_index *idx, const dbl_graph *g, int exhaustive, uint64_t max_out,
+                      uint64_t *out_count, uint32_t *out_vertex, uint8_t *out_half,
+                      uint64_t *out_expected, uint64_t *out_actual);
+
 /* ------------------------------------------------------ instrumentation */
 /* Level-synchronous (Jacobi) work model of SURVEY.md §8(d) for every
  * 64-bit word family of `idx`'s metadata on `g`: per family f (order:

@@ -233,10 +233,33 @@ def gen_cfg1():
     return d
 
 
+def gen_snapshots():
+    """Reference save_index bytes (snapshot.py:76-101) for several indexes."""
+    import io
+    d = {}
+    cases = {
+        "toy": (RC.example_graph(), None),
+        "rand_k13": (R.gen_random_graph(70, 3, seed=5), R.IndexConfig(k=13, k_prime=96, leaf_threshold=2,
+                                                                     landmark_strategy=R.LandmarkStrategy.SUM,
+                                                                     hash_seed=9)),
+        "rand_k64": (R.gen_random_graph(300, 4, seed=6), R.IndexConfig()),
+        "rand_k130": (R.gen_random_graph(200, 5, seed=7, acyclic=True), R.IndexConfig(k=130, k_prime=1)),
+    }
+    for name, (g, cfg) in cases.items():
+        idx = RC.example_index(g) if cfg is None else R.build_index(g, cfg)
+        buf = io.BytesIO()
+        R.save_index(idx, buf)
+        d[f"{name}_bytes"] = np.frombuffer(buf.getvalue(), np.uint8)
+        d[f"{name}_src"], d[f"{name}_dst"] = edges_of(g)
+        d[f"{name}_n"] = np.int64(g.vertex_count)
+    return d
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     for name, fn in (("toy", gen_toy), ("leaf_hash", gen_leaf_hash),
-                     ("landmarks", gen_landmarks), ("family", gen_family), ("cfg1", gen_cfg1)):
+                     ("landmarks", gen_landmarks), ("family", gen_family), ("cfg1", gen_cfg1),
+                     ("snapshots", gen_snapshots)):
         d = fn()
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **d)

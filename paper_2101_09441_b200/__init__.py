@@ -17,10 +17,15 @@ from .queries import (BL_ONLY, DEFAULT_FLAGS, DL_ONLY, AnsweredBy, BatchStats, O
                       QueryFlags, QueryOutcome, default_workers, explain, query, query_batch,
                       query_codes)
 from .updates import BatchUpdateStats, UpdateStats, insert_edge, insert_edges, insert_vertex
+from .snapshot import SnapshotFormatError, load_index, save_index, sniff_snapshot
+from .verify import LabelViolation, VerifyReport, verify_labels
+from .estimator import DblReachability
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "DblReachability", "LabelViolation", "SnapshotFormatError", "VerifyReport", "load_index",
+    "save_index", "sniff_snapshot", "verify_labels",
     "AnsweredBy", "BL_ONLY", "BatchStats", "BatchUpdateStats", "ConfigError", "DEFAULT_FLAGS",
     "DL_ONLY", "DblError", "DblIndex", "DeviceError", "DynamicGraph", "EdgeListFormatError",
     "IndexConfig", "IndexGraphMismatchError", "LandmarkSet", "LandmarkStrategy", "LeafSets",

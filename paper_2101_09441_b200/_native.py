@@ -75,6 +75,7 @@ _SIGS = {
     "dbl_insert_edge": [P, P, u32, u32, ctypes.POINTER(UpdateStatsC)],
     "dbl_insert_edges": [P, P, P, P, u64, i32, ctypes.POINTER(BatchStatsC)],
     "dbl_work_model": [P, P, P, P, P],
+    "dbl_verify": [P, P, i32, u64, ctypes.POINTER(u64), P, P, P, P],
     "dbl_last_timings": [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float),
                          ctypes.POINTER(ctypes.c_float)],
 }
