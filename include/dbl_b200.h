@@ -122,6 +122,9 @@ dbl_status dbl_graph_has_edges(const dbl_graph *g, const uint32_t *u, const uint
 /* edges() (graph.py:101-105): all edges sorted by (src, dst), host out;
  * arrays must hold dbl_graph_info's m entries. */
 dbl_status dbl_graph_edges(const dbl_graph *g, uint32_t *src, uint32_t *dst);
+/* One direction's adjacency (reverse = 0: out-edges, 1: in-edges) as plain
+ * CSR, host out: ptr[n+1] and col[m] (rows: base edges then inserted ones). */
+dbl_status dbl_graph_adjacency(const dbl_graph *g, int reverse, uint32_t *ptr, uint32_t *col);
 /* add_edge (graph.py:56-66) for a batch, graph only (no label upkeep):
  * duplicates collapse; *out_inserted = number of new distinct edges. */
 dbl_status dbl_graph_add_edges(dbl_graph *g, const uint32_t *u, const uint32_t *v,
@@ -243,6 +246,13 @@ dbl_status dbl_index_unpack_words(dbl_index *idx, const uint32_t *words, uint32_
 dbl_status dbl_verify(const dbl_index *idx, const dbl_graph *g, int exhaustive, uint64_t max_out,
                       uint64_t *out_count, uint32_t *out_vertex, uint8_t *out_half,
                       uint64_t *out_expected, uint64_t *out_actual);
+
+/* ----------------------------------------------------- synthetic inputs */
+/* Counter-based R-MAT generator (configs 3-5): m edges over 2^scale
+ * vertices with quadrant probabilities a, b, c (d = 1-a-b-c) into device
+ * buffers; self-loops are kept (callers drop them). Deterministic in seed. */
+dbl_status dbl_rmat_generate(uint32_t scale, uint64_t m, uint64_t seed, double a, double b, double c,
+                             uint32_t *dev_src, uint32_t *dev_dst, int device);
 
 /* ------------------------------------------------------ instrumentation */
 /* Level-synchronous (Jacobi) work model of SURVEY.md §8(d) for every

@@ -636,3 +636,116 @@ int orc_reach_batch(const orc_graph *g, const uint32_t *qu, const uint32_t *qv, 
     free(tid); free(sl);
     return ORC_OK;
 }
+
+/* ------------------------------------------------------ CSR variants -- */
+/* Same algorithms over plain CSR arrays (no per-vertex vectors or edge
+ * hash), for the large configs where the list form does not fit in host
+ * memory.  Row order does not matter for any checked value. */
+
+/* reached[v] = 1 iff some seed reaches v along (ptr, col) (a _flood,
+ * labels.py:247-260, with a byte array as the visited mark). */
+int orc_csr_flood(uint32_t n, const uint64_t *ptr, const uint32_t *col, const uint32_t *seeds,
+                  uint64_t nseeds, uint8_t *reached) {
+    uint32_t *queue = (uint32_t *)malloc((size_t)(n ? n : 1) * 4);
+    if (!queue) return ORC_E_OOM;
+    memset(reached, 0, n);
+    uint64_t head = 0, tail = 0;
+    for (uint64_t i = 0; i < nseeds; ++i)
+        if (!reached[seeds[i]]) { reached[seeds[i]] = 1; queue[tail++] = seeds[i]; }
+    while (head < tail) {
+        uint32_t p = queue[head++];
+        for (uint64_t e = ptr[p]; e < ptr[p + 1]; ++e) {
+            uint32_t x = col[e];
+            if (!reached[x]) { reached[x] = 1; queue[tail++] = x; }
+        }
+    }
+    free(queue);
+    return ORC_OK;
+}
+
+typedef struct {
+    uint32_t n, wdl, wbl;
+    const uint64_t *ptr;
+    const uint32_t *col;
+    const uint64_t *dl_in, *dl_out, *bl_in, *bl_out;
+    const uint32_t *qu, *qv;
+    uint8_t *codes;
+    uint32_t flags;
+    uint64_t lo, hi;
+    int err;
+} cslice;
+
+/* query (queries.py:94-142) over a CSR forward adjacency */
+static void *csr_query_slice(void *arg) {
+    cslice *s = (cslice *)arg;
+    uint32_t n = s->n, wdl = s->wdl, wbl = s->wbl, fl = s->flags;
+    uint32_t *stamp = (uint32_t *)calloc(n ? n : 1, 4);
+    uint32_t *queue = (uint32_t *)malloc((size_t)(n ? n : 1) * 4);
+    uint32_t epoch = 0;
+    int use_dl = !!(fl & F_USE_DL), use_bl = !!(fl & F_USE_BL);
+    int prune_dl = use_dl && (fl & F_PRUNE_DL), prune_bl = use_bl && (fl & F_PRUNE_BL);
+    for (uint64_t q = s->lo; q < s->hi; ++q) {
+        uint32_t u = s->qu[q], v = s->qv[q];
+        uint8_t code;
+        if (u >= n || v >= n) { s->err = ORC_E_RANGE; break; }
+        const uint64_t *dlo_u = s->dl_out + (uint64_t)u * wdl, *dli_u = s->dl_in + (uint64_t)u * wdl;
+        const uint64_t *dlo_v = s->dl_out + (uint64_t)v * wdl, *dli_v = s->dl_in + (uint64_t)v * wdl;
+        const uint64_t *bli_u = s->bl_in + (uint64_t)u * wbl, *blo_u = s->bl_out + (uint64_t)u * wbl;
+        const uint64_t *bli_v = s->bl_in + (uint64_t)v * wbl, *blo_v = s->bl_out + (uint64_t)v * wbl;
+        if (u == v) code = A_REFLEXIVE;
+        else if (use_dl && and_nz(dlo_u, dli_v, wdl)) code = A_DL_POS;
+        else if (use_bl && (andnot_nz(bli_u, bli_v, wbl) || andnot_nz(blo_v, blo_u, wbl))) code = A_BL_NEG;
+        else if (use_dl && (fl & F_THM1) && and_nz(dlo_v, dli_u, wdl)) code = A_THM1;
+        else if (use_dl && (fl & F_THM2) && (and_nz(dlo_u, dli_u, wdl) || and_nz(dlo_v, dli_v, wdl))) code = A_THM2;
+        else {
+            if (++epoch == 0) { memset(stamp, 0, (size_t)n * 4); epoch = 1; }
+            stamp[u] = epoch;
+            uint32_t head = 0, tail = 0;
+            queue[tail++] = u;
+            code = A_BFS_NEG;
+            while (head < tail && code == A_BFS_NEG) {
+                uint32_t w = queue[head++];
+                for (uint64_t e = s->ptr[w]; e < s->ptr[w + 1]; ++e) {
+                    uint32_t x = s->col[e];
+                    if (x == v) { code = A_BFS_POS; break; }
+                    if (stamp[x] == epoch) continue;
+                    stamp[x] = epoch;
+                    if (prune_dl && and_nz(dlo_u, s->dl_in + (uint64_t)x * wdl, wdl)) continue;
+                    if (prune_bl && (andnot_nz(s->bl_in + (uint64_t)x * wbl, bli_v, wbl) ||
+                                     andnot_nz(blo_v, s->bl_out + (uint64_t)x * wbl, wbl)))
+                        continue;
+                    queue[tail++] = x;
+                }
+            }
+        }
+        s->codes[q] = code;
+    }
+    free(stamp);
+    free(queue);
+    return NULL;
+}
+
+int orc_csr_query_batch(uint32_t n, const uint64_t *ptr, const uint32_t *col, uint32_t k, uint32_t k_prime,
+                        const uint64_t *dl_in, const uint64_t *dl_out, const uint64_t *bl_in,
+                        const uint64_t *bl_out, const uint32_t *qu, const uint32_t *qv, uint64_t q,
+                        uint32_t flags, uint8_t *codes, int threads) {
+    uint32_t wdl = (k + 63) / 64, wbl = (k_prime + 63) / 64;
+    if (threads < 1) threads = 1;
+    if ((uint64_t)threads * 2 > q) threads = 1;
+    cslice *sl = (cslice *)calloc(threads, sizeof(cslice));
+    uint64_t chunk = (q + threads - 1) / threads;
+    pthread_t *tid = (pthread_t *)malloc(sizeof(pthread_t) * threads);
+    for (int i = 0; i < threads; ++i) {
+        uint64_t lo = (uint64_t)i * chunk, hi = lo + chunk;
+        if (lo > q) lo = q;
+        if (hi > q) hi = q;
+        cslice t = {n, wdl, wbl, ptr, col, dl_in, dl_out, bl_in, bl_out, qu, qv, codes, flags, lo, hi, 0};
+        sl[i] = t;
+        pthread_create(&tid[i], NULL, csr_query_slice, &sl[i]);
+    }
+    int err = 0;
+    for (int i = 0; i < threads; ++i) { pthread_join(tid[i], NULL); if (sl[i].err) err = sl[i].err; }
+    free(tid);
+    free(sl);
+    return err;
+}

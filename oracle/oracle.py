@@ -79,6 +79,10 @@ def lib():
         L.orc_insert_edge.argtypes = [P, u32, u32, P, P, P, P, u32, u32, P]
         L.orc_reach_batch.restype = i32
         L.orc_reach_batch.argtypes = [P, P, P, u64, P, i32]
+        L.orc_csr_flood.restype = i32
+        L.orc_csr_flood.argtypes = [u32, P, P, P, u64, P]
+        L.orc_csr_query_batch.restype = i32
+        L.orc_csr_query_batch.argtypes = [u32, P, P, u32, u32, P, P, P, P, P, P, u64, u32, P, i32]
         _lib = L
     return _lib
 
@@ -218,3 +222,37 @@ class OracleGraph:
         if rc:
             raise IndexError("vertex out of range")
         return out.astype(bool)
+
+
+def csr_from_edges(n: int, src, dst):
+    """Deduplicated CSR (u64 row pointers) of an edge list, for the CSR oracles."""
+    key = np.unique(np.asarray(src, np.uint64) << np.uint64(32) | np.asarray(dst, np.uint64))
+    s = (key >> np.uint64(32)).astype(np.int64)
+    col = np.ascontiguousarray((key & np.uint64(0xFFFFFFFF)).astype(np.uint32))
+    ptr = np.zeros(n + 1, np.uint64)
+    ptr[1:] = np.cumsum(np.bincount(s, minlength=n))
+    return ptr, col
+
+
+def csr_flood(n: int, ptr, col, seeds) -> np.ndarray:
+    """Vertices reachable from `seeds` along (ptr, col) (labels.py:247-260)."""
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint32)
+    out = np.zeros(n, np.uint8)
+    rc = lib().orc_csr_flood(n, _p(ptr), _p(col), _p(seeds), len(seeds), _p(out))
+    if rc:
+        raise MemoryError("oracle flood failed")
+    return out.astype(bool)
+
+
+def csr_query_batch(n: int, ptr, col, k: int, k_prime: int, labels: dict, qu, qv, flags: int = DEFAULT_FLAGS,
+                    threads: int = 1) -> np.ndarray:
+    """query (queries.py:94-142) over CSR arrays with given labels."""
+    qu = np.ascontiguousarray(qu, dtype=np.uint32)
+    qv = np.ascontiguousarray(qv, dtype=np.uint32)
+    codes = np.zeros(len(qu), np.uint8)
+    lab = [np.ascontiguousarray(labels[f], dtype=np.uint64) for f in ("dl_in", "dl_out", "bl_in", "bl_out")]
+    rc = lib().orc_csr_query_batch(n, _p(ptr), _p(col), k, k_prime, *[_p(a) for a in lab], _p(qu), _p(qv),
+                                   len(qu), flags, _p(codes), threads)
+    if rc:
+        raise IndexError("oracle query failed")
+    return codes

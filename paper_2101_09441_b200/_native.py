@@ -46,6 +46,7 @@ _SIGS = {
     "dbl_graph_degrees": [P, P, P],
     "dbl_graph_has_edges": [P, P, P, u64, P],
     "dbl_graph_edges": [P, P, P],
+    "dbl_graph_adjacency": [P, i32, P, P],
     "dbl_graph_add_edges": [P, P, P, u64, ctypes.POINTER(u64)],
     "dbl_graph_add_vertices": [P, u32],
     "dbl_leaf_hash": [P, u64, u32, u64, P, i32],
@@ -76,6 +77,7 @@ _SIGS = {
     "dbl_insert_edges": [P, P, P, P, u64, i32, ctypes.POINTER(BatchStatsC)],
     "dbl_work_model": [P, P, P, P, P],
     "dbl_verify": [P, P, i32, u64, ctypes.POINTER(u64), P, P, P, P],
+    "dbl_rmat_generate": [u32, u64, u64, ctypes.c_double, ctypes.c_double, ctypes.c_double, P, P, i32],
     "dbl_last_timings": [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float),
                          ctypes.POINTER(ctypes.c_float)],
 }

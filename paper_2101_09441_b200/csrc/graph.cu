@@ -612,3 +612,50 @@ extern "C" dbl_status dbl_last_timings(const dbl_graph *g, float *fix, float *la
     if (bfs) *bfs = g->t_bfs;
     return DBL_OK;
 }
+
+// One direction's adjacency as plain CSR (base + delta merged per row order
+// of the base followed by the delta), host out: ptr[n+1], col[m].
+__global__ void merge_rows_kernel(const uint32_t *__restrict__ bp, const uint32_t *__restrict__ bc,
+                                  const uint32_t *__restrict__ dp, const uint32_t *__restrict__ dc, uint32_t n,
+                                  const uint32_t *__restrict__ optr, uint32_t *__restrict__ ocol) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = warp; v < n; v += nw) {
+        const uint32_t o = optr[v], s = bp[v], e = bp[v + 1];
+        for (uint32_t i = s + lane; i < e; i += 32) ocol[o + i - s] = bc[i];
+        if (dp) {
+            const uint32_t ds = dp[v], de = dp[v + 1];
+            for (uint32_t i = ds + lane; i < de; i += 32) ocol[o + (e - s) + i - ds] = dc[i];
+        }
+    }
+}
+
+__global__ void add_ptr_kernel(const uint32_t *__restrict__ a, const uint32_t *__restrict__ b, uint32_t n,
+                               uint32_t *__restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
+        out[i] = a[i] + (b ? b[i] : 0u);
+}
+
+extern "C" dbl_status dbl_graph_adjacency(const dbl_graph *g, int reverse, uint32_t *ptr, uint32_t *col) {
+    if (!g || !ptr) { set_error("null argument"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
+    const uint64_t m = g->m_base + g->m_delta;
+    Adj a = reverse ? graph_rev(g) : graph_fwd(g);
+    DevBuf p, c;
+    dbl_status s;
+    if ((s = p.ensure(((size_t)g->n + 1) * 4)) || (s = c.ensure(m * 4 + 4))) { p.release(); c.release(); return s; }
+    add_ptr_kernel<<<grid_for(g->n + 1), 256, 0, g->stream>>>(a.ptr, a.dptr, g->n, p.as<uint32_t>());
+    DBL_LAUNCHED();
+    merge_rows_kernel<<<148 * 16, 256, 0, g->stream>>>(a.ptr, a.col, a.dptr, a.dcol, g->n, p.as<uint32_t>(),
+                                                       c.as<uint32_t>());
+    DBL_LAUNCHED();
+    cudaMemcpyAsync(ptr, p.p, ((size_t)g->n + 1) * 4, cudaMemcpyDeviceToHost, g->stream);
+    if (col && m) cudaMemcpyAsync(col, c.p, m * 4, cudaMemcpyDeviceToHost, g->stream);
+    cudaError_t e = cudaStreamSynchronize(g->stream);
+    p.release();
+    c.release();
+    if (e != cudaSuccess) return cuda_fail(e, "dbl_graph_adjacency");
+    return DBL_OK;
+}

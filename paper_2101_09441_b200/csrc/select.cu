@@ -314,3 +314,48 @@ extern "C" dbl_status dbl_select_leaves(const dbl_graph *g, uint64_t threshold, 
     outb.release();
     return s;
 }
+
+// ------------------------------------------------------- R-MAT generator --
+// Counter-based R-MAT edge generator for the large synthetic configs: edge i
+// at level l draws splitmix64(seed, i, l) (no RNG state), so any slice of the
+// edge list can be regenerated independently and the result is deterministic.
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__global__ void rmat_kernel(uint32_t scale, uint64_t m, uint64_t seed, uint32_t ta, uint32_t tab, uint32_t tabc,
+                            uint32_t *__restrict__ src, uint32_t *__restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t s = 0, d = 0;
+        const uint64_t base = splitmix64(seed ^ (i * 0xD1B54A32D192ED03ull));
+        for (uint32_t l = 0; l < scale; l += 2) {
+            const uint64_t r = splitmix64(base + l);
+            // two 32-bit uniforms per draw
+            for (int h = 0; h < 2 && l + h < scale; ++h) {
+                const uint32_t u = (uint32_t)(r >> (32 * h));
+                const uint32_t sb = u >= tab;                              // quadrants c, d
+                const uint32_t db = (u >= ta && u < tab) || u >= tabc;      // quadrants b, d
+                s |= sb << (l + h);
+                d |= db << (l + h);
+            }
+        }
+        src[i] = s;
+        dst[i] = d;
+    }
+}
+
+extern "C" dbl_status dbl_rmat_generate(uint32_t scale, uint64_t m, uint64_t seed, double a, double b, double c,
+                                        uint32_t *dev_src, uint32_t *dev_dst, int device) {
+    if (scale < 1 || scale > 31 || (m && (!dev_src || !dev_dst))) { set_error("bad R-MAT arguments"); return DBL_E_ARG; }
+    if (!m) return DBL_OK;
+    DBL_CUDA(cudaSetDevice(device));
+    auto th = [](double p) { double x = p * 4294967296.0; return (uint32_t)(x >= 4294967295.0 ? 4294967295.0 : x); };
+    rmat_kernel<<<148 * 16, 256>>>(scale, m, seed, th(a), th(a + b), th(a + b + c), dev_src, dev_dst);
+    DBL_CHECK_LAUNCH("rmat_kernel");
+    DBL_CUDA(cudaDeviceSynchronize());
+    return DBL_OK;
+}

@@ -39,8 +39,22 @@ class DynamicGraph:
     # -- construction -----------------------------------------------------
     @classmethod
     def from_edges(cls, n: int, src, dst, *, device: int = 0) -> "DynamicGraph":
-        """Bulk constructor: upload an edge list and build CSR/CSC on device."""
+        """Bulk constructor: upload an edge list and build CSR/CSC on device.
+
+        src/dst may be host arrays or CUDA tensors (uint32 ids, any 32-bit dtype).
+        """
         g = cls(n, device=device)
+        if hasattr(src, "is_cuda") and src.is_cuda:
+            if src.numel() != dst.numel():
+                raise ValueError("src and dst differ in length")
+            h = ctypes.c_void_p()
+            N.call("dbl_graph_create", n, N.ptr(src), N.ptr(dst), src.numel(), N.MEM_DEVICE, src.device.index,
+                   ctypes.byref(h))
+            g._h = h
+            g.device = src.device.index
+            g._refresh_count()
+            weakref.finalize(g, N.lib().dbl_graph_free, h)
+            return g
         s = N.u32_array(src)
         d = N.u32_array(dst)
         if len(s) != len(d):
@@ -173,6 +187,14 @@ class DynamicGraph:
         if m:
             N.call("dbl_graph_edges", h, N.ptr(s), N.ptr(d))
         return s, d
+
+    def adjacency(self, reverse: bool = False) -> tuple[np.ndarray, np.ndarray]:
+        """(ptr u32[n+1], col u32[m]) of the out-edges (or in-edges if reverse)."""
+        h = self.handle
+        ptr = np.zeros(self._n + 1, np.uint32)
+        col = np.zeros(max(self.edge_count, 1), np.uint32)
+        N.call("dbl_graph_adjacency", h, int(reverse), N.ptr(ptr), N.ptr(col))
+        return ptr, col[:self.edge_count]
 
     def edges(self) -> Iterator[tuple[int, int]]:
         s, d = self.edge_arrays()

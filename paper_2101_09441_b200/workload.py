@@ -164,3 +164,22 @@ def gen_insert_workload(src: np.ndarray, dst: np.ndarray, n: int, count: int, se
         chosen = allk[first]
     chosen = chosen[:count]
     return ((chosen >> np.uint64(32)).astype(np.uint32), (chosen & np.uint64(0xFFFFFFFF)).astype(np.uint32))
+
+
+def rmat_edges_device(scale: int, edge_factor: int, seed: int, device: int = 0, a: float = 0.57,
+                      b: float = 0.19, c: float = 0.19):
+    """R-MAT edges generated on the GPU (dbl_rmat_generate), self-loops dropped.
+
+    Returns (src, dst) int32 CUDA tensors holding uint32 ids.  Used for the
+    large configs (2^22..2^26) where host generation would dominate.
+    """
+    import torch
+
+    from . import _native as N
+    m = edge_factor << scale
+    dev = torch.device("cuda", device)
+    src = torch.empty(m, dtype=torch.int32, device=dev)
+    dst = torch.empty(m, dtype=torch.int32, device=dev)
+    N.call("dbl_rmat_generate", scale, m, seed, a, b, c, N.ptr(src), N.ptr(dst), device)
+    keep = src != dst
+    return src[keep].contiguous(), dst[keep].contiguous()
