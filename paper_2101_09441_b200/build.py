@@ -24,6 +24,14 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "-I" + os.path.join(ROOT, "include")]
+# query.cu tail-launches the BFS hard path from the device (CUDA dynamic
+# parallelism): relocatable device code, device-linked against cudadevrt.
+RDC = {"query.cu"}
+LINK = ["-rdc=true", "-lcudadevrt", "-lcudart"]
+
+
+def _flags(src: str) -> list:
+    return FLAGS + (["-rdc=true"] if src in RDC else [])
 
 
 def _inputs():
@@ -41,7 +49,7 @@ def _stale() -> bool:
 
 def _compile(src: str) -> tuple[str, str]:
     obj = os.path.join(OUTDIR, os.path.basename(src).replace(".cu", ".o"))
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *ARCH, *_flags(src), "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -55,10 +63,10 @@ def build_variant(name: str, defines: list[str]) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(OUTDIR, f"{name}_{src.replace('.cu', '.o')}")
-        subprocess.check_call([NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c",
+        subprocess.check_call([NVCC, *ARCH, *_flags(src), *[f"-D{d}" for d in defines], "-c",
                                os.path.join(CSRC, src), "-o", obj], stderr=subprocess.DEVNULL)
         objs.append(obj)
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs, *LINK])
     for o in objs:
         os.remove(o)
     return out
@@ -75,7 +83,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for (_, log), src in zip(results, SOURCES):
             f.write(f"=== {src}\n{log}\n")
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, *LINK]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     for o in objs:

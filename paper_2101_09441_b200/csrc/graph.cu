@@ -460,11 +460,8 @@ extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
                       &g->changed_bits, &g->cub_tmp, &g->scratch_a, &g->scratch_b, &g->scratch_c,
                       &g->scratch_d, &g->q_in, &g->q_codes, &g->q_vis, &g->q_pending,
                       &g->q_counters, &g->q_dense};
-    if (g->q_exec) cudaGraphExecDestroy(g->q_exec);
-    if (g->q_graph) cudaGraphDestroy(g->q_graph);
     set_stream(nullptr);
     for (auto *b : bufs) b->release();
-    g->q_desc.release();
     g->q_errs.release();
     for (auto &e : g->cev) if (e) cudaEventDestroy(e);
     for (auto &cs : g->cstream) if (cs) { cudaStreamSynchronize(cs); pool_forget_stream(cs); cudaStreamDestroy(cs); }
@@ -600,12 +597,9 @@ extern "C" dbl_status dbl_stream(const dbl_graph *g, void **s) {
 extern "C" dbl_status dbl_last_timings(const dbl_graph *g, float *fix, float *label, float *bfs) {
     if (!g) { set_error("null graph"); return DBL_E_ARG; }
     dbl_graph *gm = const_cast<dbl_graph *>(g);
-    // query kernels: events ev[2] -> ev[3] (K6) -> ev[4] (K7), read on demand
-    if (cudaEventQuery(g->ev[4]) == cudaSuccess || cudaEventSynchronize(g->ev[4]) == cudaSuccess) {
-        float a = 0, b = 0;
-        if (cudaEventElapsedTime(&a, g->ev[2], g->ev[3]) == cudaSuccess) gm->t_label = a;
-        if (cudaEventElapsedTime(&b, g->ev[3], g->ev[4]) == cudaSuccess) gm->t_bfs = b;
-    }
+    // query kernels: events ev[2] -> ev[3] (fused K6+K7, or the label kernel)
+    // -> ev[4] (separate BFS kernels), read on demand
+    if (cudaEventSynchronize(g->q_timed_bfs ? g->ev[4] : g->ev[3]) == cudaSuccess) query_timings(gm);
     cudaGetLastError();
     if (fix) *fix = g->t_fix;
     if (label) *label = g->t_label;

@@ -166,14 +166,11 @@ struct dbl_graph {
     dbl::DevBuf cub_tmp, scratch_a, scratch_b, scratch_c, scratch_d;
     dbl::HostBuf host_stage;
     // query workspace
-    dbl::DevBuf q_in, q_codes, q_vis, q_pending, q_counters, q_dense, q_desc, q_errs;
+    dbl::DevBuf q_in, q_codes, q_vis, q_pending, q_counters, q_dense, q_errs;
     cudaStream_t cstream[2] = {nullptr, nullptr};   // H2D / D2H copy streams
     cudaEvent_t cev[33] = {};
     uint64_t q_pending_cap = 0;
-    cudaGraph_t q_graph = nullptr;       // reusable query launch graph
-    cudaGraphExec_t q_exec = nullptr;
-    const void *q_key[6] = {};
-    uint64_t q_topo = 0;
+    bool q_timed_bfs = false;            // last batch ran the separate BFS kernels (ev[3] -> ev[4])
     uint64_t topo_version = 0;           // bumped whenever adjacency buffers change
     int sm_count = 148;
     int coop_blocks = 0;      // co-resident blocks for the fixpoint kernel
@@ -222,6 +219,7 @@ dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, ui
 dbl_status work_model(const dbl_index *idx, dbl_graph *g, uint64_t *V, uint64_t *E,
                       uint32_t *levels);
 // query.cu
+void query_timings(dbl_graph *g);
 dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
                      uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited);
 }  // namespace dbl

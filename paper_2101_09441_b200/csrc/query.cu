@@ -28,8 +28,12 @@
 
 namespace dbl {
 
-enum { CNT_PENDING = 0, CNT_ERR = 1, CNT_TICKET = 2, CNT_OVERFLOW = 3, CNT_DTICKET = 4, CNT_WORDS = 8 };
-// CNT_TILE (= 5, fused kernel tile ticket) is defined with the fused kernel below
+// Per-batch device counters.  Words [0, 8) are live during a batch and are
+// left zeroed by the batch's last kernel, which first copies them to the
+// result words [8, 16) (read by the host after the batch): no memset launch
+// per batch.
+enum { CNT_PENDING = 0, CNT_ERR = 1, CNT_TICKET = 2, CNT_OVERFLOW = 3, CNT_DTICKET = 4, CNT_TILE = 5,
+       CNT_DONE = 6, CNT_WORDS = 8, CNT_RES = 8, CNT_ALL = 16 };
 constexpr int GQ = 64;             // queries per BFS group
 constexpr int HCAP = 2048;         // shared hash capacity (power of two)
 constexpr int HBITS = 11;
@@ -38,9 +42,7 @@ constexpr int BFS_THREADS = 256;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint8_t UNRESOLVED = 0xff;
 
-// Per-call query arguments, read by the kernels from device memory so that
-// the launch sequence can be a reusable CUDA graph (only this struct is
-// rewritten per batch).
+// Per-call query arguments, passed by value to every query kernel.
 struct QueryDesc {
     const uint32_t *u;
     const uint32_t *v;
@@ -238,13 +240,13 @@ __device__ __forceinline__ unsigned long long tgt_lookup(const BfsShared &S, uin
 template <bool DENSE>
 __global__ void __launch_bounds__(BFS_THREADS)
 bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_t n, Adj adj,
-           const QueryDesc *__restrict__ qd, const uint32_t *__restrict__ pending,
+           const QueryDesc qd, const uint32_t *__restrict__ pending,
            uint32_t *__restrict__ counters, uint32_t *__restrict__ ovf, char *__restrict__ ws) {
-    const uint32_t *__restrict__ qu = qd->u;
-    const uint32_t *__restrict__ qv = qd->v;
-    const uint32_t flags = qd->flags;
-    uint8_t *__restrict__ codes = qd->codes;
-    uint32_t *__restrict__ visited = qd->visited;
+    const uint32_t *__restrict__ qu = qd.u;
+    const uint32_t *__restrict__ qv = qd.v;
+    const uint32_t flags = qd.flags;
+    uint8_t *__restrict__ codes = qd.codes;
+    uint32_t *__restrict__ visited = qd.visited;
     const uint32_t H = WDL + WBL, rw = 2 * H;
     const uint32_t WD = WDL > 0 ? WDL : 1;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -479,7 +481,6 @@ constexpr int FUSED_THREADS = 256;
 // accumulates 32 before running one BFS (fewer, longer chains at the end).
 // Measured on cfg2: immediate is faster (31 vs 39 us per 1M batch).
 constexpr bool DEFER_BFS = false;
-enum { CNT_TILE = 5 };
 
 template <int WDL, int WBL>
 struct WarpBfs {
@@ -711,7 +712,7 @@ template <int WDL, int WBL>
 __device__ DBL_BFS_INLINE void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64_t *__restrict__ rec, const Adj &adj,
                                bool prune_dl, bool prune_bl, uint8_t *__restrict__ codes,
                                uint32_t *__restrict__ visited, uint32_t *__restrict__ pending,
-                               uint32_t *__restrict__ counters, cudaGraphConditionalHandle hard) {
+                               uint32_t *__restrict__ counters) {
     const int lane = threadIdx.x & 31;
     const uint32_t nb = B.nq;
     for (int i = lane; i < WH; i += 32) {
@@ -744,23 +745,46 @@ __device__ DBL_BFS_INLINE void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64
             if (visited) visited[qi] = B.vcnt[lane];
         }
     }
-    if (ovf && lane == 0 && hard) cudaGraphSetConditional(hard, 1u);
     __syncwarp();
     if (lane == 0) B.nq = 0;
     __syncwarp();
 }
 
+// Close a batch: publish the live counters to the result words and zero them
+// for the next batch (stream order makes this the batch's last access).
+__device__ __forceinline__ void close_batch(uint32_t *counters) {
+#pragma unroll
+    for (int i = 0; i < CNT_WORDS; ++i) {
+        counters[CNT_RES + i] = counters[i];
+        counters[i] = 0;
+    }
+}
+
+__global__ void finish_batch_kernel(uint32_t *__restrict__ counters) {
+    if (threadIdx.x == 0) close_batch(counters);
+}
+
+// Launch geometry of the hard path, handed to the fused kernel so that its
+// last CTA can tail-launch the group and dense kernels when (and only when)
+// a warp's BFS table overflowed.
+struct HardArgs {
+    int grid, dctas;
+    uint32_t smem, dsmem;
+    uint32_t wdl, wbl;
+    uint32_t *ovf;
+    char *ws;
+};
+
 template <int WDL, int WBL>
 __global__ void __launch_bounds__(FUSED_THREADS, DBL_QMINB)
-query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const QueryDesc *__restrict__ qd,
-                   uint32_t *__restrict__ pending, uint32_t *__restrict__ counters,
-                   cudaGraphConditionalHandle hard) {
-    const uint32_t *__restrict__ qu = qd->u;
-    const uint32_t *__restrict__ qv = qd->v;
-    const uint32_t count = qd->count, flags = qd->flags;
-    const int vec_ok = qd->vec_ok;
-    uint8_t *__restrict__ codes = qd->codes;
-    uint32_t *__restrict__ visited = qd->visited;
+query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const QueryDesc qd,
+                   uint32_t *__restrict__ pending, uint32_t *__restrict__ counters, const HardArgs ha) {
+    const uint32_t *__restrict__ qu = qd.u;
+    const uint32_t *__restrict__ qv = qd.v;
+    const uint32_t count = qd.count, flags = qd.flags;
+    const int vec_ok = qd.vec_ok;
+    uint8_t *__restrict__ codes = qd.codes;
+    uint32_t *__restrict__ visited = qd.visited;
     constexpr int H = WDL + WBL, RW = 2 * H, WD = WarpBfs<WDL, WBL>::WD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -848,6 +872,9 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
         __syncwarp();
         uint32_t nun = __popc(unres), tot = 0;
         uint32_t off = warp_excl_scan(nun, tot);
+#ifdef DBL_QNOBFS
+        tot = 0;   // experiment: label checks only (unresolved codes left as is)
+#endif
         uint32_t done_upto = 0;   // tile entries [0, done_upto) already staged
         while (done_upto < tot) {
             const uint32_t nq = B.nq;
@@ -876,16 +903,36 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
             if (lane == 0) B.nq = nq + take;
             __syncwarp();
             if (nq + take == 32 || (!DEFER_BFS && done_upto == tot)) {
-                warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters, hard);
+                warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters);
             }
         }
     }
     __syncwarp();
-    if (B.nq) warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters, hard);
+    if (B.nq) warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters);
+    // the last CTA out closes the batch, or hands the overflowed BFS batches
+    // to the group/dense kernels through the tail-launch stream (they run
+    // after this grid, before the stream's next operation)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(&counters[CNT_DONE], 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence();
+            const uint32_t npend = *(volatile uint32_t *)&counters[CNT_PENDING];
+            if (npend == 0) {
+                close_batch(counters);
+            } else {
+                bfs_kernel<false><<<ha.grid, BFS_THREADS, ha.smem, cudaStreamTailLaunch>>>(
+                    rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, nullptr);
+                bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
+                    rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
+                finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters);
+            }
+        }
+    }
 }
 
-typedef void (*fused_fn)(const uint64_t *, uint32_t, Adj, const QueryDesc *, uint32_t *, uint32_t *,
-                         cudaGraphConditionalHandle);
+typedef void (*fused_fn)(const uint64_t *, uint32_t, Adj, const QueryDesc, uint32_t *, uint32_t *, const HardArgs);
 
 static bool pick_fused(uint32_t wdl, uint32_t wbl, fused_fn &f, size_t &smem) {
 #define DBL_QF(A, B) if (wdl == A && wbl == B) { f = query_fused_kernel<A, B>; smem = sizeof(WarpBfs<A, B>) * (FUSED_THREADS / 32); return true; }
@@ -912,94 +959,32 @@ struct HardPath {
 
 static dbl_status hard_path_config(const dbl_index *idx, dbl_graph *g, HardPath &hp) {
     static int bps = -1;
-    static size_t last_smem = 0;
+    static size_t last_smem = 0, last_dsmem = 0;
     hp.smem = bfs_smem(idx->wdl, idx->wbl, false);
     hp.dsmem = bfs_smem(idx->wdl, idx->wbl, true);
-    DBL_CUDA(cudaFuncSetAttribute((const void *)bfs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)hp.smem));
-    DBL_CUDA(cudaFuncSetAttribute((const void *)bfs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)hp.dsmem));
-    if (bps < 0 || last_smem != hp.smem) {
+    if (bps < 0 || last_smem != hp.smem || last_dsmem != hp.dsmem) {
+        DBL_CUDA(cudaFuncSetAttribute((const void *)bfs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)hp.smem));
+        DBL_CUDA(cudaFuncSetAttribute((const void *)bfs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)hp.dsmem));
         DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, bfs_kernel<false>, BFS_THREADS, hp.smem));
         if (bps < 1) bps = 1;
         last_smem = hp.smem;
+        last_dsmem = hp.dsmem;
     }
     hp.grid = g->sm_count * bps;
     const size_t slab = (size_t)idx->n * 32;
     hp.dctas = 8;
     const size_t budget = (size_t)4 << 30;
     while (hp.dctas > 1 && slab * hp.dctas > budget) --hp.dctas;
-    dbl_status s = g->q_dense.ensure(slab * hp.dctas + 16);
-    return s;
+    return g->q_dense.ensure(slab * hp.dctas + 16);
 }
 
-static void fill_kernel_node(cudaKernelNodeParams &kp, const void *fn, dim3 grid, dim3 block, size_t smem,
-                             void **args) {
-    kp = {};
-    kp.func = const_cast<void *>(fn);
-    kp.gridDim = grid;
-    kp.blockDim = block;
-    kp.sharedMemBytes = (unsigned)smem;
-    kp.kernelParams = args;
-}
-
-// Build the reusable query graph:
-//   memset(counters) -> ev2 -> fused -> ev3 -> IF(hard) { group -> dense } -> ev4
-static dbl_status build_query_graph(const dbl_index *idx, dbl_graph *g, fused_fn fused, size_t fsmem, int fgrid,
-                                    const HardPath &hp) {
-    if (g->q_exec) { cudaGraphExecDestroy(g->q_exec); g->q_exec = nullptr; }
-    if (g->q_graph) { cudaGraphDestroy(g->q_graph); g->q_graph = nullptr; }
-    cudaGraph_t gr;
-    DBL_CUDA(cudaGraphCreate(&gr, 0));
-    g->q_graph = gr;
-    cudaGraphConditionalHandle hard;
-    DBL_CUDA(cudaGraphConditionalHandleCreate(&hard, gr, 0, cudaGraphCondAssignDefault));
-    cudaGraphNode_t nmem, ne2, nfused, ne3, ncond, ne4;
-    cudaMemsetParams mp = {};
-    mp.dst = g->q_counters.p;
-    mp.value = 0;
-    mp.elementSize = 4;
-    mp.width = CNT_WORDS;
-    mp.height = 1;
-    DBL_CUDA(cudaGraphAddMemsetNode(&nmem, gr, nullptr, 0, &mp));
-    DBL_CUDA(cudaGraphAddEventRecordNode(&ne2, gr, &nmem, 1, g->ev[2]));
-    // kernel args must outlive cudaGraphAddKernelNode only (they are copied)
-    const uint64_t *rec = idx->rec.as<uint64_t>();
-    uint32_t n = idx->n, wdl = idx->wdl, wbl = idx->wbl;
-    Adj adj = graph_fwd(g);
-    const QueryDesc *qd = g->q_desc.as<QueryDesc>();
-    uint32_t *pending = g->q_pending.as<uint32_t>();
-    uint32_t *counters = g->q_counters.as<uint32_t>();
-    uint32_t *ovf = pending + g->q_pending_cap + 16;
-    char *ws = g->q_dense.as<char>();
-    char *nows = nullptr;
-    void *fargs[] = {(void *)&rec, (void *)&n, (void *)&adj, (void *)&qd, (void *)&pending, (void *)&counters,
-                     (void *)&hard};
-    cudaKernelNodeParams kp;
-    fill_kernel_node(kp, (const void *)fused, dim3(fgrid), dim3(FUSED_THREADS), fsmem, fargs);
-    DBL_CUDA(cudaGraphAddKernelNode(&nfused, gr, &ne2, 1, &kp));
-    DBL_CUDA(cudaGraphAddEventRecordNode(&ne3, gr, &nfused, 1, g->ev[3]));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = hard;
-    cp.conditional.type = cudaGraphCondTypeIf;
-    cp.conditional.size = 1;
-    DBL_CUDA(cudaGraphAddNode(&ncond, gr, &ne3, 1, &cp));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    cudaGraphNode_t ngrp, nden;
-    void *gargs[] = {(void *)&rec, (void *)&wdl, (void *)&wbl, (void *)&n, (void *)&adj, (void *)&qd,
-                     (void *)&pending, (void *)&counters, (void *)&ovf, (void *)&nows};
-    fill_kernel_node(kp, (const void *)bfs_kernel<false>, dim3(hp.grid), dim3(BFS_THREADS), hp.smem, gargs);
-    DBL_CUDA(cudaGraphAddKernelNode(&ngrp, body, nullptr, 0, &kp));
-    void *dargs[] = {(void *)&rec, (void *)&wdl, (void *)&wbl, (void *)&n, (void *)&adj, (void *)&qd,
-                     (void *)&pending, (void *)&counters, (void *)&ovf, (void *)&ws};
-    fill_kernel_node(kp, (const void *)bfs_kernel<true>, dim3(hp.dctas), dim3(BFS_THREADS), hp.dsmem, dargs);
-    DBL_CUDA(cudaGraphAddKernelNode(&nden, body, &ngrp, 1, &kp));
-    DBL_CUDA(cudaGraphAddEventRecordNode(&ne4, gr, &ncond, 1, g->ev[4]));
-    DBL_CUDA(cudaGraphInstantiate(&g->q_exec, gr, 0));
-    return DBL_OK;
-}
-
+// One batch = one launch on the fast path: the fused kernel (K6 + per-warp
+// K7) takes its arguments by value and leaves the counters zeroed; the
+// 64-query group kernel and the dense kernel are tail-launched from the
+// device only when some warp's BFS table overflowed (never on cfg2), so the
+// host submits one kernel and no memset, copy or graph per batch.
 dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
                      uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited) {
     if (count >= 0xffffffffull) { set_error("query batch too large"); return DBL_E_ARG; }
@@ -1008,24 +993,29 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
         return DBL_E_CONFIG;
     }
     dbl_status s;
-    // pending list capacity: grows with the largest batch seen (graph rebuilt on growth)
+    // pending list capacity: grows with the largest batch seen
     uint64_t cap = g->q_pending_cap;
     if (count > cap) cap = count < 1024 ? 1024 : count;
-    if ((s = g->q_pending.ensure(cap * 8 + 64)) || (s = g->q_counters.ensure(CNT_WORDS * 4)) ||
-        (s = g->q_desc.ensure(sizeof(QueryDesc))))
-        return s;
-    const bool grown = cap != g->q_pending_cap;
+    if ((s = g->q_pending.ensure(cap * 8 + 64))) return s;
     g->q_pending_cap = cap;
-    QueryDesc hd{u, v, codes, visited, (uint32_t)count, flags, 0, 0};
-    hd.vec_ok = ((((uintptr_t)u) | ((uintptr_t)v)) & (4 * QPL - 1)) == 0 && (((uintptr_t)codes) & (QPL - 1)) == 0 &&
+    if (!g->q_counters.p) {
+        if ((s = g->q_counters.ensure(CNT_ALL * 4))) return s;
+        DBL_CUDA(cudaMemsetAsync(g->q_counters.p, 0, CNT_ALL * 4, g->stream));
+    }
+    QueryDesc qd{u, v, codes, visited, (uint32_t)count, flags, 0, 0};
+    qd.vec_ok = ((((uintptr_t)u) | ((uintptr_t)v)) & (4 * QPL - 1)) == 0 && (((uintptr_t)codes) & (QPL - 1)) == 0 &&
                 (!visited || (((uintptr_t)visited) & (4 * QPL - 1)) == 0);
-    DBL_CUDA(cudaMemcpyAsync(g->q_desc.p, &hd, sizeof(hd), cudaMemcpyHostToDevice, g->stream));
-    fused_fn fused = nullptr;
-    size_t fsmem = 0;
-    const bool use_fused = pick_fused(idx->wdl, idx->wbl, fused, fsmem) && !std::getenv("DBL_NO_FUSED");
+    uint32_t *pending = g->q_pending.as<uint32_t>();
+    uint32_t *counters = g->q_counters.as<uint32_t>();
+    uint32_t *ovf = pending + g->q_pending_cap + 16;
+    const uint64_t *rec = idx->rec.as<uint64_t>();
+    const Adj adj = graph_fwd(g);
     HardPath hp;
     if ((s = hard_path_config(idx, g, hp))) return s;
-    if (use_fused) {
+    static const bool no_fused = std::getenv("DBL_NO_FUSED") != nullptr;
+    fused_fn fused = nullptr;
+    size_t fsmem = 0;
+    if (count && !no_fused && pick_fused(idx->wdl, idx->wbl, fused, fsmem)) {
         static int fbps = -1;
         static const void *last_fn = nullptr;
         if (fbps < 0 || last_fn != (const void *)fused) {
@@ -1034,94 +1024,67 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
             if (fbps < 1) fbps = 1;
             last_fn = (const void *)fused;
         }
-        const int fgrid = g->sm_count * fbps;
-        if (std::getenv("DBL_NO_GRAPH")) {
-            // plain launches (profilers that skip graph nodes): same kernels, the
-            // hard path always launched
-            uint32_t *pending = g->q_pending.as<uint32_t>();
-            uint32_t *counters = g->q_counters.as<uint32_t>();
-            uint32_t *ovf = pending + g->q_pending_cap + 16;
-            const QueryDesc *qd = g->q_desc.as<QueryDesc>();
-            DBL_CUDA(cudaMemsetAsync(counters, 0, CNT_WORDS * 4, g->stream));
-            DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
-            fused<<<fgrid, FUSED_THREADS, fsmem, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, graph_fwd(g), qd,
-                                                              pending, counters, (cudaGraphConditionalHandle)0);
-            DBL_CHECK_LAUNCH("query_fused_kernel");
-            DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
-            Adj adj = graph_fwd(g);
-            bfs_kernel<false><<<hp.grid, BFS_THREADS, hp.smem, g->stream>>>(idx->rec.as<uint64_t>(), idx->wdl,
-                                                                            idx->wbl, idx->n, adj, qd, pending,
-                                                                            counters, ovf, nullptr);
-            DBL_CHECK_LAUNCH("bfs_kernel");
-            bfs_kernel<true><<<hp.dctas, BFS_THREADS, hp.dsmem, g->stream>>>(idx->rec.as<uint64_t>(), idx->wdl,
-                                                                             idx->wbl, idx->n, adj, qd, pending,
-                                                                             counters, ovf, g->q_dense.as<char>());
-            DBL_CHECK_LAUNCH("bfs_kernel_dense");
-            DBL_CUDA(cudaEventRecord(g->ev[4], g->stream));
-            return DBL_OK;
-        }
-        // the graph bakes in device pointers: rebuild when any of them moved
-        const void *key[6] = {idx, idx->rec.p, g->fptr.p, g->m_delta ? g->dfptr.p : nullptr,
-                              g->q_pending.p, g->q_dense.p};
-        bool same = g->q_exec && !grown && g->q_topo == g->topo_version;
-        for (int i = 0; i < 6 && same; ++i) same = g->q_key[i] == key[i];
-        if (!same) {
-            if ((s = build_query_graph(idx, g, fused, fsmem, fgrid, hp))) return s;
-            for (int i = 0; i < 6; ++i) g->q_key[i] = key[i];
-            g->q_topo = g->topo_version;
-        }
-        DBL_CUDA(cudaGraphLaunch(g->q_exec, g->stream));
-        launch_counter() += 2;  // fused kernel (+ hard path when needed)
+        const HardArgs ha{hp.grid, hp.dctas, (uint32_t)hp.smem, (uint32_t)hp.dsmem, idx->wdl, idx->wbl, ovf,
+                          g->q_dense.as<char>()};
+        DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
+        fused<<<g->sm_count * fbps, FUSED_THREADS, fsmem, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);
+        DBL_CHECK_LAUNCH("query_fused_kernel");
+        DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
+        g->q_timed_bfs = false;
         return DBL_OK;
     }
-    // generic widths: label kernel, then the group and dense kernels
-    uint32_t *pending = g->q_pending.as<uint32_t>();
-    uint32_t *ovf = pending + g->q_pending_cap + 16;
-    uint32_t *counters = g->q_counters.as<uint32_t>();
-    const QueryDesc *qd = g->q_desc.as<QueryDesc>();
-    DBL_CUDA(cudaMemsetAsync(counters, 0, CNT_WORDS * 4, g->stream));
+    // generic widths (or DBL_NO_FUSED): label kernel, then the group and
+    // dense kernels, then the counter close
     DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
     if (count) {
         int blocks = (int)((count + 255) / 256);
         if (blocks > g->sm_count * 16) blocks = g->sm_count * 16;
         const label_fn label = pick_label(idx->wdl, idx->wbl);
         if (label)
-            label<<<blocks, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, u, v, count, flags, codes,
-                                                 visited, pending, counters);
+            label<<<blocks, 256, 0, g->stream>>>(rec, idx->n, u, v, count, flags, codes, visited, pending, counters);
         else
-            label_check_generic<<<blocks, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, idx->wdl,
-                                                               idx->wbl, u, v, count, flags, codes, visited,
-                                                               pending, counters);
+            label_check_generic<<<blocks, 256, 0, g->stream>>>(rec, idx->n, idx->wdl, idx->wbl, u, v, count, flags,
+                                                               codes, visited, pending, counters);
         DBL_CHECK_LAUNCH("label_check_kernel");
     }
     DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
     if (count) {
-        Adj adj = graph_fwd(g);
-        bfs_kernel<false><<<hp.grid, BFS_THREADS, hp.smem, g->stream>>>(idx->rec.as<uint64_t>(), idx->wdl, idx->wbl,
-                                                                        idx->n, adj, qd, pending, counters, ovf,
-                                                                        nullptr);
+        bfs_kernel<false><<<hp.grid, BFS_THREADS, hp.smem, g->stream>>>(rec, idx->wdl, idx->wbl, idx->n, adj, qd,
+                                                                        pending, counters, ovf, nullptr);
         DBL_CHECK_LAUNCH("bfs_kernel");
-        bfs_kernel<true><<<hp.dctas, BFS_THREADS, hp.dsmem, g->stream>>>(idx->rec.as<uint64_t>(), idx->wdl,
-                                                                         idx->wbl, idx->n, adj, qd, pending,
-                                                                         counters, ovf, g->q_dense.as<char>());
+        bfs_kernel<true><<<hp.dctas, BFS_THREADS, hp.dsmem, g->stream>>>(rec, idx->wdl, idx->wbl, idx->n, adj, qd,
+                                                                         pending, counters, ovf,
+                                                                         g->q_dense.as<char>());
         DBL_CHECK_LAUNCH("bfs_kernel_dense");
     }
+    finish_batch_kernel<<<1, 32, 0, g->stream>>>(counters);
+    DBL_CHECK_LAUNCH("finish_batch_kernel");
     DBL_CUDA(cudaEventRecord(g->ev[4], g->stream));
+    g->q_timed_bfs = true;
     return DBL_OK;
 }
 
 // Copy the range-error flag of the last batch to dst (device, stream-ordered).
 dbl_status query_err_to(dbl_graph *g, uint32_t *dst) {
-    DBL_CUDA(cudaMemcpyAsync(dst, g->q_counters.as<uint32_t>() + CNT_ERR, 4, cudaMemcpyDeviceToDevice, g->stream));
+    DBL_CUDA(cudaMemcpyAsync(dst, g->q_counters.as<uint32_t>() + CNT_RES + CNT_ERR, 4, cudaMemcpyDeviceToDevice,
+                             g->stream));
     return DBL_OK;
+}
+
+// Event times of the last batch: the fused kernel's span (incl. any
+// tail-launched hard path) as "label", the separate BFS kernels as "bfs".
+void query_timings(dbl_graph *g) {
+    cudaEventElapsedTime(&g->t_label, g->ev[2], g->ev[3]);
+    g->t_bfs = 0;
+    if (g->q_timed_bfs) cudaEventElapsedTime(&g->t_bfs, g->ev[3], g->ev[4]);
 }
 
 dbl_status query_finish(dbl_graph *g, uint32_t *err_out) {
     uint32_t h[CNT_WORDS];
-    DBL_CUDA(cudaMemcpyAsync(h, g->q_counters.p, CNT_WORDS * 4, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaMemcpyAsync(h, g->q_counters.as<uint32_t>() + CNT_RES, CNT_WORDS * 4, cudaMemcpyDeviceToHost,
+                             g->stream));
     DBL_CUDA(cudaStreamSynchronize(g->stream));
-    cudaEventElapsedTime(&g->t_label, g->ev[2], g->ev[3]);
-    cudaEventElapsedTime(&g->t_bfs, g->ev[3], g->ev[4]);
+    query_timings(g);
     *err_out = h[CNT_ERR];
     return DBL_OK;
 }
@@ -1137,7 +1100,7 @@ extern "C" dbl_status dbl_query_counters(const dbl_graph *g, uint32_t *out8) {
     if (!g || !out8) { set_error("null argument"); return DBL_E_ARG; }
     if (!g->q_counters.p) { for (int i = 0; i < 8; ++i) out8[i] = 0; return DBL_OK; }
     DBL_CUDA(cudaSetDevice(g->device));
-    DBL_CUDA(cudaMemcpyAsync(out8, g->q_counters.p, 8 * 4, cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaMemcpyAsync(out8, g->q_counters.as<uint32_t>() + CNT_RES, 8 * 4, cudaMemcpyDeviceToHost, g->stream));
     DBL_CUDA(cudaStreamSynchronize(g->stream));
     return DBL_OK;
 }
