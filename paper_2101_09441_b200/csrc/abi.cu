@@ -288,6 +288,8 @@ static dbl_status index_create(const dbl_graph *gc, const dbl_config *cfg, const
     if (cfg->k) {
         if (landmarks) {
             DBL_CUDA(cudaMemcpyAsync(idx->landmarks.p, landmarks, (size_t)cfg->k * 4, cudaMemcpyHostToDevice, g->stream));
+        } else if (!seed) {
+            idx->sel_landmarks = true;   // selected on the device by the build's prep pass
         } else if ((s = select_landmarks_dev(g, cfg->k, cfg->strategy, idx->landmarks.as<uint32_t>()))) {
             return fail(s);
         }
@@ -297,6 +299,12 @@ static dbl_status index_create(const dbl_graph *gc, const dbl_config *cfg, const
         if (leaf_flags && bucket) {
             DBL_CUDA(cudaMemcpyAsync(idx->leaf_flags.p, leaf_flags, g->n, cudaMemcpyHostToDevice, g->stream));
             DBL_CUDA(cudaMemcpyAsync(idx->bucket.p, bucket, (size_t)g->n * 4, cudaMemcpyHostToDevice, g->stream));
+        } else if (!seed) {
+            // leaves are selected by the build's prep pass (override errors
+            // are reported when the build finishes)
+            if (cfg->k_prime < 1) { set_error("k_prime must be >= 1"); return fail(DBL_E_CONFIG); }
+            if (ovr_ids && n_ovr && (s = make_override(g, ovr_ids, ovr_buckets, n_ovr, idx->ovr))) return fail(s);
+            idx->sel_leaves = true;
         } else {
             DevBuf ovr;
             const uint32_t *dovr = nullptr;
@@ -368,6 +376,7 @@ extern "C" dbl_status dbl_index_free(dbl_index *idx) {
     idx->landmarks.release();
     idx->leaf_flags.release();
     idx->bucket.release();
+    idx->ovr.release();
     delete idx;
     return DBL_OK;
 }

@@ -743,12 +743,15 @@ static dbl_status launch_insert_seed(dbl_graph *g, FixParams &P, uint32_t nw, bo
 }
 
 static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2], FixParams &P,
-                                 uint32_t &nw, bool &vec, bool count, bool reset_counts = true) {
+                                 uint32_t &nw, bool &vec, bool count, bool reset_counts = true,
+                                 bool clear_bits = true) {
     dbl_status s = graph_ensure_traversal(g);
     if (s) return s;
     const size_t bmw = ((size_t)g->n + 31) / 32;
-    DBL_CUDA(cudaMemsetAsync(g->stamp[0].p, 0, bmw * 4, g->stream));
-    DBL_CUDA(cudaMemsetAsync(g->stamp[1].p, 0, bmw * 4, g->stream));
+    if (clear_bits) {
+        DBL_CUDA(cudaMemsetAsync(g->stamp[0].p, 0, bmw * 4, g->stream));
+        DBL_CUDA(cudaMemsetAsync(g->stamp[1].p, 0, bmw * 4, g->stream));
+    }
     nw = 0;
     vec = true;
     for (int d = 0; d < 2; ++d) {
@@ -817,45 +820,83 @@ dbl_status index_seed_records(dbl_graph *g, dbl_index *idx, uint64_t wmask) {
 }
 
 // Build (or rebuild) the listed record words (nullptr = all) from seeds.
+// A full build seeds through the fused prep pass (select.cu: metadata still
+// to be selected, seeds, level-0 frontier of the first word group, device
+// landmark top-k), so nothing between the graph and the fixpoint waits on
+// the host; a word subset (sharded builds) seeds with seed_records.
 dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32_t nwords) {
     if (idx->n == 0) return DBL_OK;
     Group groups[2 * MAX_SHARD_WORDS + 4];
     int ng = 0;
     if (idx->wdl + idx->wbl > (uint32_t)MAX_SHARD_WORDS) { set_error("label width too large"); return DBL_E_CONFIG; }
     plan_groups(idx, words, nwords, groups, ng);
-    DBL_CUDA(cudaEventRecord(g->ev[0], g->stream));
-    uint64_t wmask = ~0ull;
-    if (words) {
-        wmask = 0;
-        for (uint32_t i = 0; i < nwords; ++i) wmask |= 1ull << words[i];
-    }
-    dbl_status s = index_seed_records(g, idx, wmask);
-    if (s) return s;
-    trace("build: seed", g->stream);
     // pair forward and backward groups of equal width into one launch
-    bool used[2 * MAX_SHARD_WORDS + 4] = {};
-    for (int i = 0; i < ng; ++i) {
-        if (used[i]) continue;
-        used[i] = true;
-        const Group *pair[2] = {nullptr, nullptr};
-        pair[groups[i].dir] = &groups[i];
-        for (int j = i + 1; j < ng; ++j) {
-            if (!used[j] && groups[j].dir != groups[i].dir && groups[j].nw == groups[i].nw) {
-                used[j] = true;
-                pair[groups[j].dir] = &groups[j];
-                break;
+    const Group *pairs[2 * MAX_SHARD_WORDS + 4][2];
+    int np = 0;
+    {
+        bool used[2 * MAX_SHARD_WORDS + 4] = {};
+        for (int i = 0; i < ng; ++i) {
+            if (used[i]) continue;
+            used[i] = true;
+            pairs[np][0] = pairs[np][1] = nullptr;
+            pairs[np][groups[i].dir] = &groups[i];
+            for (int j = i + 1; j < ng; ++j) {
+                if (!used[j] && groups[j].dir != groups[i].dir && groups[j].nw == groups[i].nw) {
+                    used[j] = true;
+                    pairs[np][groups[j].dir] = &groups[j];
+                    break;
+                }
             }
+            ++np;
         }
+    }
+    DBL_CUDA(cudaEventRecord(g->ev[0], g->stream));
+    const bool prep = words == nullptr;
+    dbl_status s;
+    if ((s = graph_ensure_traversal(g))) return s;
+    if (prep) {
+        const Group **p0 = pairs[0];
+        uint32_t *b0 = p0[0] ? g->stamp[0].as<uint32_t>() : nullptr;
+        uint32_t *b1 = p0[1] ? g->stamp[1].as<uint32_t>() : nullptr;
+        if ((s = prep_build_dev(g, idx, b0, b1, p0[0] ? p0[0]->w0 : 0, p0[0] ? p0[0]->w0 + p0[0]->nw : 0,
+                                p0[1] ? p0[1]->w0 : 0, p0[1] ? p0[1]->w0 + p0[1]->nw : 0)))
+            return s;
+    } else {
+        uint64_t wmask = 0;
+        for (uint32_t i = 0; i < nwords; ++i) wmask |= 1ull << words[i];
+        if ((s = index_seed_records(g, idx, wmask))) return s;
+    }
+    trace("build: seed", g->stream);
+    PrepState hp{};
+    for (int pi = 0; pi < np; ++pi) {
+        const Group *pair[2] = {pairs[pi][0], pairs[pi][1]};
+        const bool fresh = !(prep && pi == 0);   // prep wrote pair 0's level-0 bitmaps
         FixParams P{};
         uint32_t nw = 0;
         bool vec = true;
-        if ((s = prepare_params(g, idx, pair, P, nw, vec, false))) return s;
-        if ((s = launch_init_frontier(g, idx, pair))) return s;
+        if ((s = prepare_params(g, idx, pair, P, nw, vec, false, true, fresh))) return s;
+        if (fresh && (s = launch_init_frontier(g, idx, pair))) return s;
         trace("build: init frontier", g->stream);
         if ((s = launch_fixpoint<false>(g, P, nw, vec))) return s;
+        if (prep && pi == 0 && (s = prep_fetch(g, &hp))) return s;
         Ctrl h{};
         if ((s = finish_run(g, &h))) return s;
         trace("build: fixpoint", g->stream);
+        if (prep && pi == 0) {
+            if (hp.err) { set_error("bucket override outside [0, k_prime)"); return DBL_E_CONFIG; }
+            idx->sel_leaves = false;
+            idx->ovr.release();
+            if (hp.fallback) {
+                // more landmark candidates than the on-chip sort holds (flat
+                // score distributions): exact top-k with the radix-sort path,
+                // then build again from the fixed metadata
+                if ((s = select_landmarks_dev(g, idx->cfg.k, idx->cfg.strategy, idx->landmarks.as<uint32_t>())))
+                    return s;
+                idx->sel_landmarks = false;
+                return run_build(g, idx, words, nwords);
+            }
+            idx->sel_landmarks = false;
+        }
         if (std::getenv("DBL_TRACE")) {
             std::fprintf(stderr, "[dbl] fixpoint levels=%u nw=%u\n", h.levels, nw);
             for (uint32_t l = 0; l < h.levels && l < 31; ++l)

@@ -11,7 +11,10 @@ namespace dbl {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr uint32_t DELTA_BIT = 0x80000000u;
-constexpr int FIX_THREADS = 256;
+#ifndef DBL_FIX_THREADS
+#define DBL_FIX_THREADS 256
+#endif
+constexpr int FIX_THREADS = DBL_FIX_THREADS;
 constexpr int MAX_GROUP_WORDS = 8;        // words propagated together by one fixpoint
 constexpr int MAX_SHARD_WORDS = 32;  // words per record half (2 halves <= 64-bit word mask)
 
@@ -105,6 +108,17 @@ struct Queue {
     uint32_t *eoff;
 };
 
+// Device state of the fused build prep (select.cu): score histogram for the
+// landmark top-k, candidate counts, and the flags the host reads once the
+// build has finished (no host round trip inside the build).
+constexpr uint32_t PREP_CAND_CAP = 8192;   // top-k candidates sorted on chip
+struct PrepState {
+    uint32_t hist[65];
+    uint32_t n_above, n_tie;
+    uint32_t fallback;           // candidates exceeded PREP_CAND_CAP: host re-selects
+    unsigned long long err;      // bucket override outside [0, k')
+};
+
 // Device control block of one fixpoint run.
 struct Ctrl {
     unsigned long long cnt[2][2];   // (items << 32 | edges) per [level % 2][direction]
@@ -164,6 +178,7 @@ struct dbl_graph {
     dbl::DevBuf changed_bits;
     // generic scratch
     dbl::DevBuf cub_tmp, scratch_a, scratch_b, scratch_c, scratch_d;
+    dbl::DevBuf prep;                     // PrepState + top-k candidates
     dbl::HostBuf host_stage;
     // query workspace
     dbl::DevBuf q_in, q_codes, q_vis, q_pending, q_counters, q_dense, q_errs;
@@ -187,6 +202,10 @@ struct dbl_index {
     dbl::DevBuf landmarks;               // k u32
     dbl::DevBuf leaf_flags;              // n u8
     dbl::DevBuf bucket;                  // n u32
+    // metadata still to be selected by the build's fused prep pass
+    // (dbl_index_build): landmarks, leaves (with an optional override table)
+    bool sel_landmarks = false, sel_leaves = false;
+    dbl::DevBuf ovr;                     // n u32 override buckets (0xffffffff = none)
 };
 
 namespace dbl {
@@ -210,6 +229,18 @@ dbl_status select_leaves_dev(dbl_graph *g, uint64_t threshold, uint32_t k_prime,
                              const uint32_t *dev_ovr, uint8_t *dev_flags, uint32_t *dev_bucket);
 dbl_status leaf_hash_dev(const uint64_t *ids, uint64_t count, uint32_t k_prime, uint64_t seed,
                          uint32_t *out, cudaStream_t s);
+// Fused build prep: one pass over the vertices selects the leaves (if
+// idx->sel_leaves), scores + histograms the landmark candidates (if
+// idx->sel_landmarks), seeds every record word and writes the level-0
+// frontier bitmaps bits0/bits1 for the record words [a0, e0) / [a1, e1);
+// then the landmark top-k runs on the device and ORs the landmark bits into
+// the records and the bitmaps.  No host synchronisation.
+dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_t *bits1, uint32_t a0,
+                          uint32_t e0, uint32_t a1, uint32_t e1);
+// Enqueue the D2H copy of the prep state (read after the build's sync):
+// err = bucket override outside [0, k'); fallback = the device top-k
+// overflowed its candidate table (the caller re-selects and rebuilds).
+dbl_status prep_fetch(dbl_graph *g, PrepState *host);
 // fixpoint.cu
 dbl_status index_seed_records(dbl_graph *g, dbl_index *idx, uint64_t wmask);
 dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32_t nwords);

@@ -33,7 +33,7 @@ namespace dbl {
 // result words [8, 16) (read by the host after the batch): no memset launch
 // per batch.
 enum { CNT_PENDING = 0, CNT_ERR = 1, CNT_TICKET = 2, CNT_OVERFLOW = 3, CNT_DTICKET = 4, CNT_TILE = 5,
-       CNT_DONE = 6, CNT_WORDS = 8, CNT_RES = 8, CNT_ALL = 16 };
+       CNT_DONE = 6, CNT_WOVF = 7, CNT_WORDS = 8, CNT_RES = 8, CNT_ALL = 16 };
 constexpr int GQ = 64;             // queries per BFS group
 constexpr int HCAP = 2048;         // shared hash capacity (power of two)
 constexpr int HBITS = 11;
@@ -480,7 +480,13 @@ constexpr int FUSED_THREADS = 256;
 // (short BFS chains interleaved with other warps' label checks); true: it
 // accumulates 32 before running one BFS (fewer, longer chains at the end).
 // Measured on cfg2: immediate is faster (31 vs 39 us per 1M batch).
-constexpr bool DEFER_BFS = false;
+#ifndef DBL_QDEFER
+#define DBL_QDEFER 0
+#endif
+constexpr bool DEFER_BFS = DBL_QDEFER;
+#ifndef DBL_QTICKET
+#define DBL_QTICKET 0
+#endif
 
 template <int WDL, int WBL>
 struct WarpBfs {
@@ -687,10 +693,13 @@ __device__ __forceinline__ void flush_tile_codes(uint8_t *__restrict__ codes, ui
             const uint32_t packed = code[0] | (code[1] << 8) | (code[2] << 16) | ((uint32_t)code[3] << 24);
             *reinterpret_cast<uint32_t *>(codes + qb) = packed;
             if (visited) *reinterpret_cast<uint4 *>(visited + qb) = make_uint4(vcount[0], vcount[1], vcount[2], vcount[3]);
-        } else {
+        } else if constexpr (QPL == 2) {
             const uint16_t packed = (uint16_t)(code[0] | (code[1] << 8));
             *reinterpret_cast<uint16_t *>(codes + qb) = packed;
             if (visited) *reinterpret_cast<uint2 *>(visited + qb) = make_uint2(vcount[0], vcount[1]);
+        } else {
+            codes[qb] = code[0];
+            if (visited) visited[qb] = vcount[0];
         }
     } else {
 #pragma unroll
@@ -711,8 +720,8 @@ __device__ __forceinline__ void flush_tile_codes(uint8_t *__restrict__ codes, ui
 template <int WDL, int WBL>
 __device__ DBL_BFS_INLINE void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64_t *__restrict__ rec, const Adj &adj,
                                bool prune_dl, bool prune_bl, uint8_t *__restrict__ codes,
-                               uint32_t *__restrict__ visited, uint32_t *__restrict__ pending,
-                               uint32_t *__restrict__ counters) {
+                               uint32_t *__restrict__ visited, uint32_t *__restrict__ ovf_list,
+                               uint32_t *__restrict__ counters, int ovf_counter) {
     const int lane = threadIdx.x & 31;
     const uint32_t nb = B.nq;
     for (int i = lane; i < WH; i += 32) {
@@ -737,9 +746,9 @@ __device__ DBL_BFS_INLINE void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64
     const uint32_t dn = B.done;
     if (lane < (int)nb) {
         const uint32_t qi = B.qidx[lane];
-        if (ovf) {  // hand the batch to the group kernels via the pending list
-            const uint32_t p = atomicAdd(&counters[CNT_PENDING], 1u);
-            pending[p] = qi;
+        if (ovf) {  // hand the batch to the group kernels via an overflow list
+            const uint32_t p = atomicAdd(&counters[ovf_counter], 1u);
+            ovf_list[p] = qi;
         } else {
             codes[qi] = ((dn >> lane) & 1) ? DBL_BFS_POSITIVE : DBL_BFS_NEGATIVE;
             if (visited) visited[qi] = B.vcnt[lane];
@@ -748,6 +757,34 @@ __device__ DBL_BFS_INLINE void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64
     __syncwarp();
     if (lane == 0) B.nq = 0;
     __syncwarp();
+}
+
+// Pairs qb .. qb+QPL-1 of the batch (entries at or beyond end read as 0).
+__device__ __forceinline__ void load_pairs(const uint32_t *__restrict__ qu, const uint32_t *__restrict__ qv,
+                                           uint64_t qb, uint64_t end, int vec_ok, uint32_t (&us)[QPL],
+                                           uint32_t (&vs)[QPL]) {
+    if (vec_ok && qb + QPL - 1 < end) {
+        if constexpr (QPL == 4) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4 *>(qu + qb));
+            const uint4 b = __ldg(reinterpret_cast<const uint4 *>(qv + qb));
+            us[0] = a.x; us[1] = a.y; us[2] = a.z; us[3] = a.w;
+            vs[0] = b.x; vs[1] = b.y; vs[2] = b.z; vs[3] = b.w;
+        } else if constexpr (QPL == 2) {
+            const uint2 a = __ldg(reinterpret_cast<const uint2 *>(qu + qb));
+            const uint2 b = __ldg(reinterpret_cast<const uint2 *>(qv + qb));
+            us[0] = a.x; us[1] = a.y;
+            vs[0] = b.x; vs[1] = b.y;
+        } else {
+            us[0] = __ldg(qu + qb);
+            vs[0] = __ldg(qv + qb);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < QPL; ++j) {
+            us[j] = qb + j < end ? __ldg(qu + qb + j) : 0;
+            vs[j] = qb + j < end ? __ldg(qv + qb + j) : 0;
+        }
+    }
 }
 
 // Close a batch: publish the live counters to the result words and zero them
@@ -773,6 +810,9 @@ struct HardArgs {
     uint32_t wdl, wbl;
     uint32_t *ovf;
     char *ws;
+    int wgrid;          // warp-BFS kernel (lean path)
+    uint32_t wsmem;
+    uint32_t *wovf;
 };
 
 template <int WDL, int WBL>
@@ -794,33 +834,38 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
     const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
     if (lane == 0) B.nq = 0;
     __syncwarp();
+#if DBL_QTICKET
+    // dynamic: warps take QT-query tiles from a global ticket
     for (;;) {
         uint32_t tile = 0;
         if (lane == 0) tile = atomicAdd(&counters[CNT_TILE], 1u);
         tile = __shfl_sync(FULL, tile, 0);
         const uint64_t q0 = (uint64_t)tile * QT;
         if (q0 >= count) break;
+        const uint64_t wend = count;
         const uint64_t qb = q0 + QPL * lane;
         uint32_t us[QPL], vs[QPL];
-        if (vec_ok && qb + QPL - 1 < count) {
-            if constexpr (QPL == 4) {
-                const uint4 a = __ldg(reinterpret_cast<const uint4 *>(qu + qb));
-                const uint4 b = __ldg(reinterpret_cast<const uint4 *>(qv + qb));
-                us[0] = a.x; us[1] = a.y; us[2] = a.z; us[3] = a.w;
-                vs[0] = b.x; vs[1] = b.y; vs[2] = b.z; vs[3] = b.w;
-            } else {
-                const uint2 a = __ldg(reinterpret_cast<const uint2 *>(qu + qb));
-                const uint2 b = __ldg(reinterpret_cast<const uint2 *>(qv + qb));
-                us[0] = a.x; us[1] = a.y;
-                vs[0] = b.x; vs[1] = b.y;
-            }
-        } else {
+        load_pairs(qu, qv, qb, wend, vec_ok, us, vs);
+#else
+    // static: warp w owns the contiguous range [w0, w1) (equal shares, a
+    // multiple of 4 queries), walked in QT-query tiles; the next tile's pairs
+    // are loaded while the current tile's records are in flight, so a tile
+    // costs about one dependent memory round trip and no ticket atomics
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    uint64_t share = ((uint64_t)count + nw - 1) / nw;
+    share = (share + 3) & ~3ull;
+    const uint64_t w0 = (uint64_t)gw * share;
+    const uint64_t wend = min((uint64_t)count, w0 + share);
+    uint32_t nus[QPL], nvs[QPL];
+    if (w0 < wend) load_pairs(qu, qv, w0 + QPL * lane, wend, vec_ok, nus, nvs);
+    for (uint64_t q0 = w0; q0 < wend; q0 += QT) {
+        const uint64_t qb = q0 + QPL * lane;
+        uint32_t us[QPL], vs[QPL];
 #pragma unroll
-            for (int j = 0; j < QPL; ++j) {
-                us[j] = qb + j < count ? __ldg(qu + qb + j) : 0;
-                vs[j] = qb + j < count ? __ldg(qv + qb + j) : 0;
-            }
-        }
+        for (int j = 0; j < QPL; ++j) { us[j] = nus[j]; vs[j] = nvs[j]; }
+        if (q0 + QT < wend) load_pairs(qu, qv, qb + QT, wend, vec_ok, nus, nvs);
+#endif
         uint8_t code[QPL];
         uint32_t vcount[QPL];
 #pragma unroll
@@ -829,7 +874,7 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
         uint64_t ra[QPL][RW], rb[QPL][RW];
 #pragma unroll
         for (int j = 0; j < QPL; ++j) {
-            const bool inb = qb + j < count;
+            const bool inb = qb + j < wend;
             const bool ok = inb && us[j] < n && vs[j] < n && us[j] != vs[j];
             if (ok) {
                 load_record<RW>(rec + (size_t)us[j] * RW, ra[j]);
@@ -838,7 +883,7 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
         }
 #pragma unroll
         for (int j = 0; j < QPL; ++j) {
-            const bool inb = qb + j < count;
+            const bool inb = qb + j < wend;
             code[j] = UNRESOLVED;
             if (!inb) { code[j] = 0xfd; continue; }
             const uint32_t u = us[j], v = vs[j];
@@ -868,7 +913,7 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
         // BFS runs when 32 have accumulated (and once more after the last
         // tile), so a warp pays about one BFS latency chain per 32 queries.
         // the tile's codes go out first (UNRESOLVED where a BFS will answer)
-        flush_tile_codes(codes, visited, count, qb, vec_ok, code, vcount);
+        flush_tile_codes(codes, visited, wend, qb, vec_ok, code, vcount);
         __syncwarp();
         uint32_t nun = __popc(unres), tot = 0;
         uint32_t off = warp_excl_scan(nun, tot);
@@ -903,12 +948,12 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
             if (lane == 0) B.nq = nq + take;
             __syncwarp();
             if (nq + take == 32 || (!DEFER_BFS && done_upto == tot)) {
-                warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters);
+                warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters, CNT_PENDING);
             }
         }
     }
     __syncwarp();
-    if (B.nq) warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters);
+    if (B.nq) warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters, CNT_PENDING);
     // the last CTA out closes the batch, or hands the overflowed BFS batches
     // to the group/dense kernels through the tail-launch stream (they run
     // after this grid, before the stream's next operation)
@@ -930,6 +975,277 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
             }
         }
     }
+}
+
+// ------------------------------------------------ K6 lean + K7 warp BFS --
+//
+// The throughput path.  K6 is the leanest possible gather: one query per
+// thread per grid-stride step, both endpoints' records fetched with one
+// 256-bit read-only load each, rules 0-4, the code (and visited = 0) stored,
+// unresolved queries appended to the pending list with one warp-aggregated
+// atomic.  No shared memory and few registers, so 2048 threads per SM keep
+// ~4k record sectors in flight (measured: a one-query-per-thread gather beats
+// persistent multi-query tiles by ~30% on 1M queries).
+//
+// K7 is launched right behind it with programmatic dependent launch: its
+// CTAs are scheduled as K6's retire and wait (griddepcontrol.wait) for K6's
+// results, then every warp takes an equal share of the pending queries in
+// groups of <= 32 and runs the bit-parallel pruned BFS of warp_bfs on them.
+// Batches whose BFS outgrows the warp table are handed, by the last CTA, to
+// the 64-query group kernel and the dense kernel (device tail launches).
+// Pruned BFS of one query by one thread (queries.py:116-142) for the common
+// tiny case: at most TB_Q expanded vertices with at most TB_E edges each
+// (on R-MAT the fallback visits <= 3 vertices).  Returns 1 if v is reached,
+// 0 if the search is exhausted, 2 if it outgrew those bounds (the query is
+// then handed to the warp BFS).  The answer equals the reference's: pruning
+// only removes vertices that cannot reach v (a pruned x reaching v would give
+// dl_out[u] & dl_in[v] != 0 or violate BL containment), so v is found iff
+// it is reachable, in any visiting order.
+constexpr int TB_Q = 8;
+#ifndef DBL_LMINB
+#define DBL_LMINB 4
+#endif
+constexpr uint32_t TB_E = 48;
+
+template <int WDL, int WBL>
+__device__ __forceinline__ int thread_bfs(const uint64_t *__restrict__ rec, const Adj adj, uint32_t u, uint32_t v,
+                                       uint64_t dlo_u0, uint64_t bli_v0, uint64_t blo_v0, bool prune_dl,
+                                       bool prune_bl, uint32_t *vcount) {
+    constexpr int H = WDL + WBL, RW = 2 * H;
+    static_assert(WDL <= 1 && WBL == 1, "thread BFS handles one word per family");
+    uint32_t q[TB_Q];
+    q[0] = u;
+    int qn = 1;
+    for (int head = 0; head < qn; ++head) {
+        const uint32_t w = q[head];
+        *vcount = head + 1;
+        for (int seg = 0; seg < 2; ++seg) {
+            const uint32_t *ptr = seg ? adj.dptr : adj.ptr;
+            if (!ptr) break;
+            const uint32_t *col = seg ? adj.dcol : adj.col;
+            const uint32_t s0 = __ldg(ptr + w), s1 = __ldg(ptr + w + 1);
+            if (s1 - s0 > TB_E) return 2;
+            for (uint32_t j0 = s0; j0 < s1; j0 += 4) {
+                uint32_t x[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) x[t] = j0 + t < s1 ? __ldg(col + j0 + t) : 0xffffffffu;
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (x[t] == v) return 1;     // target test precedes the visited test
+                bool fresh[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    fresh[t] = x[t] != 0xffffffffu;
+                    for (int k = 0; k < qn; ++k) fresh[t] &= q[k] != x[t];
+                }
+                uint64_t xr[4][RW];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (fresh[t] && (prune_dl || prune_bl)) load_record<RW>(rec + (size_t)x[t] * RW, xr[t]);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (!fresh[t]) continue;
+                    bool p = false;
+                    if (prune_dl && WDL) p = (dlo_u0 & xr[t][0]) != 0;                                  // queries.py:137-138
+                    if (prune_bl && !p) p = ((xr[t][WDL] & ~bli_v0) | (blo_v0 & ~xr[t][H + WDL])) != 0;  // :139-140
+                    if (p) continue;
+                    if (qn == TB_Q) return 2;
+                    q[qn++] = x[t];
+                }
+            }
+        }
+    }
+    return 0;
+}
+
+template <int WDL, int WBL>
+__global__ void bfs_warp_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const QueryDesc qd,
+                                uint32_t *__restrict__ pending, uint32_t *__restrict__ wovf,
+                                uint32_t *__restrict__ counters, const HardArgs ha);
+
+template <int WDL, int WBL>
+__global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj,
+                                                          const QueryDesc qd, uint32_t *__restrict__ pending,
+                                                          uint32_t *__restrict__ counters, const HardArgs ha) {
+    constexpr int H = WDL + WBL, RW = 2 * H;
+    constexpr bool TBFS = WDL <= 1 && WBL == 1;
+    const uint32_t flags = qd.flags, count = qd.count;
+    const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
+    const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
+    const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t cr = (count + 31) & ~31u;
+    const int lane = threadIdx.x & 31;
+    // Unresolved queries are deferred to after the thread's label checks
+    // (bit it of dmask = iteration it), so a BFS never stalls the warp's
+    // gathers; afterwards every lane runs its own deferred BFS chains in
+    // parallel with the other lanes'.
+    const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t dmask = 0;
+    uint32_t it = 0;
+    for (uint32_t i = i0; i < cr; i += stride, ++it) {
+        bool unres = false;
+        if (i < count) {
+            const uint32_t u = __ldg(qd.u + i), v = __ldg(qd.v + i);
+            uint8_t code = UNRESOLVED;
+            if (u >= n || v >= n) {
+                atomicOr(&counters[CNT_ERR], 1u);
+                code = 0xfe;
+            } else if (u == v) {
+                code = DBL_REFLEXIVE;
+            } else {
+                uint64_t a[RW], b[RW];
+                load_record<RW>(rec + (size_t)u * RW, a);
+                load_record<RW>(rec + (size_t)v * RW, b);
+                uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
+#pragma unroll
+                for (int k = 0; k < WDL; ++k) {
+                    r1 |= a[H + k] & b[k];             // dl_out[u] & dl_in[v]
+                    r3 |= b[H + k] & a[k];             // dl_out[v] & dl_in[u]
+                    r4 |= (a[H + k] & a[k]) | (b[H + k] & b[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < WBL; ++k)
+                    r2 |= (a[WDL + k] & ~b[WDL + k]) | (b[H + WDL + k] & ~a[H + WDL + k]);
+                if (use_dl && r1) code = DBL_DL_POSITIVE;
+                else if (use_bl && r2) code = DBL_BL_NEGATIVE;
+                else if (thm1 && r3) code = DBL_THM1_NEGATIVE;
+                else if (thm2 && r4) code = DBL_THM2_NEGATIVE;
+            }
+            if (TBFS && code == UNRESOLVED && it < 32) {
+                dmask |= 1u << it;
+            } else {
+                qd.codes[i] = code;
+                if (qd.visited) qd.visited[i] = 0;
+                unres = code == UNRESOLVED;
+            }
+        }
+        const unsigned m = __ballot_sync(FULL, unres);
+        if (m) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&counters[CNT_PENDING], (uint32_t)__popc(m));
+            base = __shfl_sync(FULL, base, 0);
+            if (unres) pending[base + __popc(m & ((1u << lane) - 1u))] = i;
+        }
+    }
+    if constexpr (TBFS) {
+        while (dmask) {
+            const int b0 = __ffs(dmask) - 1;
+            dmask &= dmask - 1;
+            const uint32_t i = i0 + (uint32_t)b0 * stride;
+            const uint32_t u = __ldg(qd.u + i), v = __ldg(qd.v + i);
+            const uint64_t *ru = rec + (size_t)u * RW, *rv = rec + (size_t)v * RW;
+            const uint64_t dlo_u = WDL ? __ldg(ru + H) : 0ull;
+            const uint64_t bli_v = __ldg(rv + WDL), blo_v = __ldg(rv + H + WDL);
+            uint32_t vc = 0;
+            const int r = thread_bfs<WDL, WBL>(rec, adj, u, v, dlo_u, bli_v, blo_v, prune_dl, prune_bl, &vc);
+            if (r == 2) {
+                pending[atomicAdd(&counters[CNT_PENDING], 1u)] = i;
+            } else {
+                qd.codes[i] = r ? DBL_BFS_POSITIVE : DBL_BFS_NEGATIVE;
+                if (qd.visited) qd.visited[i] = vc;
+            }
+        }
+    }
+    // the last CTA out closes the batch, or tail-launches the warp BFS for the
+    // queries the thread BFS could not finish
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&counters[CNT_DONE], 1u) == gridDim.x - 1) {
+            __threadfence();
+            if (*(volatile uint32_t *)&counters[CNT_PENDING] == 0) {
+                close_batch(counters);
+            } else {
+                counters[CNT_DONE] = 0;
+                bfs_warp_kernel<WDL, WBL><<<ha.wgrid, FUSED_THREADS, ha.wsmem, cudaStreamTailLaunch>>>(
+                    rec, n, adj, qd, pending, ha.wovf, counters, ha);
+            }
+        }
+    }
+}
+
+template <int WDL, int WBL>
+__global__ void __launch_bounds__(FUSED_THREADS, DBL_QMINB)
+bfs_warp_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const QueryDesc qd,
+                uint32_t *__restrict__ pending, uint32_t *__restrict__ wovf, uint32_t *__restrict__ counters,
+                const HardArgs ha) {
+    constexpr int H = WDL + WBL, RW = 2 * H, WD = WarpBfs<WDL, WBL>::WD;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WarpBfs<WDL, WBL> &B = reinterpret_cast<WarpBfs<WDL, WBL> *>(smem_raw)[wid];
+    const uint32_t flags = qd.flags;
+    const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
+    const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
+    const uint32_t npend = *(volatile uint32_t *)&counters[CNT_PENDING];
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    // equal shares: groups of g <= 32 queries, about one group per warp
+    uint32_t g = (npend + nw - 1) / nw;
+    g = g < 1 ? 1 : (g > 32 ? 32 : g);
+    const uint32_t ngroups = (npend + g - 1) / g;
+    for (uint32_t gi = gw; gi < ngroups; gi += nw) {
+        const uint32_t p0 = gi * g, nb = min(g, npend - p0);
+        if (lane < (int)nb) {
+            const uint32_t qi = pending[p0 + lane];
+            const uint32_t u = __ldg(qd.u + qi), v = __ldg(qd.v + qi);
+            uint64_t ru[RW], rv[RW];
+            load_record<RW>(rec + (size_t)u * RW, ru);
+            load_record<RW>(rec + (size_t)v * RW, rv);
+            B.qidx[lane] = qi;
+            B.qu[lane] = u;
+            B.qv[lane] = v;
+#pragma unroll
+            for (int q = 0; q < WDL; ++q) B.qdlo[lane * WD + q] = ru[H + q];
+#pragma unroll
+            for (int q = 0; q < WBL; ++q) {
+                B.qbli[lane * WBL + q] = rv[WDL + q];
+                B.qblo[lane * WBL + q] = rv[H + WDL + q];
+            }
+        }
+        if (lane == 0) B.nq = nb;
+        __syncwarp();
+        warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.codes, qd.visited, wovf, counters, CNT_WOVF);
+    }
+    // the last CTA out closes the batch, or moves the overflowed queries to
+    // the head of the pending list and tail-launches the group/dense kernels
+    __syncthreads();
+    __shared__ uint32_t last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&counters[CNT_DONE], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const uint32_t nov = *(volatile uint32_t *)&counters[CNT_WOVF];
+    if (nov == 0) {
+        if (threadIdx.x == 0) close_batch(counters);
+        return;
+    }
+    for (uint32_t i = threadIdx.x; i < nov; i += blockDim.x) pending[i] = wovf[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        counters[CNT_PENDING] = nov;
+        __threadfence();
+        bfs_kernel<false><<<ha.grid, BFS_THREADS, ha.smem, cudaStreamTailLaunch>>>(
+            rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, nullptr);
+        bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
+            rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
+        finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters);
+    }
+}
+
+typedef void (*lean_fn)(const uint64_t *, uint32_t, const Adj, const QueryDesc, uint32_t *, uint32_t *,
+                        const HardArgs);
+typedef void (*bfsw_fn)(const uint64_t *, uint32_t, Adj, const QueryDesc, uint32_t *, uint32_t *, uint32_t *,
+                        const HardArgs);
+
+static bool pick_lean(uint32_t wdl, uint32_t wbl, lean_fn &l, bfsw_fn &b, size_t &smem) {
+#define DBL_QL(A, B) if (wdl == A && wbl == B) { l = label_lean_kernel<A, B>; b = bfs_warp_kernel<A, B>; \
+        smem = sizeof(WarpBfs<A, B>) * (FUSED_THREADS / 32); return true; }
+    DBL_QL(0, 1) DBL_QL(1, 1) DBL_QL(2, 1) DBL_QL(4, 1) DBL_QL(0, 2) DBL_QL(1, 2) DBL_QL(2, 2)
+#undef DBL_QL
+    return false;
 }
 
 typedef void (*fused_fn)(const uint64_t *, uint32_t, Adj, const QueryDesc, uint32_t *, uint32_t *, const HardArgs);
@@ -996,7 +1312,9 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     // pending list capacity: grows with the largest batch seen
     uint64_t cap = g->q_pending_cap;
     if (count > cap) cap = count < 1024 ? 1024 : count;
-    if ((s = g->q_pending.ensure(cap * 8 + 64))) return s;
+    // pending list [0, cap), dense-group overflow list [cap + 16, 2 cap + 16),
+    // warp-batch overflow list [2 cap + 32, 3 cap + 32)
+    if ((s = g->q_pending.ensure(cap * 12 + 256))) return s;
     g->q_pending_cap = cap;
     if (!g->q_counters.p) {
         if ((s = g->q_counters.ensure(CNT_ALL * 4))) return s;
@@ -1013,6 +1331,33 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     HardPath hp;
     if ((s = hard_path_config(idx, g, hp))) return s;
     static const bool no_fused = std::getenv("DBL_NO_FUSED") != nullptr;
+    static const bool old_fused = std::getenv("DBL_QFUSED") != nullptr;
+    lean_fn lean = nullptr;
+    bfsw_fn bfsw = nullptr;
+    size_t wsmem = 0;
+    if (count && !no_fused && !old_fused && pick_lean(idx->wdl, idx->wbl, lean, bfsw, wsmem)) {
+        static int lbps = -1, wbps = -1;
+        static const void *last_fn = nullptr;
+        if (lbps < 0 || last_fn != (const void *)bfsw) {
+            DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lbps, lean, 256, 0));
+            DBL_CUDA(cudaFuncSetAttribute((const void *)bfsw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+            DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wbps, bfsw, FUSED_THREADS, wsmem));
+            if (lbps < 1) lbps = 1;
+            if (wbps < 1) wbps = 1;
+            last_fn = (const void *)bfsw;
+        }
+        uint32_t *wovf = pending + 2 * g->q_pending_cap + 32;
+        const HardArgs ha{hp.grid, hp.dctas, (uint32_t)hp.smem, (uint32_t)hp.dsmem, idx->wdl, idx->wbl, ovf,
+                          g->q_dense.as<char>(), g->sm_count * wbps, (uint32_t)wsmem, wovf};
+        uint32_t lgrid = (uint32_t)((count + 255) / 256);
+        if (lgrid > (uint32_t)(g->sm_count * lbps)) lgrid = (uint32_t)(g->sm_count * lbps);
+        DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
+        lean<<<lgrid, 256, 0, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);
+        DBL_CHECK_LAUNCH("label_lean_kernel");
+        DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
+        g->q_timed_bfs = false;
+        return DBL_OK;
+    }
     fused_fn fused = nullptr;
     size_t fsmem = 0;
     if (count && !no_fused && pick_fused(idx->wdl, idx->wbl, fused, fsmem)) {

@@ -193,6 +193,287 @@ dbl_status select_leaves_dev(dbl_graph *g, uint64_t threshold, uint32_t k_prime,
     return DBL_OK;
 }
 
+// ------------------------------------------------- fused build prep (K1-K3) --
+//
+// One pass over the vertices replaces score_hist + leaves + seed_records +
+// leaf_frontier (four launches and two host round trips): degrees ->
+// landmark score and its log2 histogram, leaf flags and buckets (labels.py:
+// 150-181), the seeded record (labels.py:291-305 seeding) and the level-0
+// frontier bitmaps.  The landmark top-k then runs without the host: a
+// candidate pass keeps every vertex whose score bin can still hold a
+// landmark, and one CTA sorts the candidates by (-score, id) in shared memory
+// (labels.py:145-146) and ORs the landmark bits into the records/bitmaps.
+
+struct PrepArgs {
+    Adj f, r;
+    uint32_t n;
+    int strategy;
+    int do_lm, do_leaves;
+    uint64_t *score;
+    uint64_t threshold;
+    uint32_t k_prime;
+    uint64_t seed;
+    const uint32_t *ovr;
+    uint8_t *flags;
+    uint32_t *bucket;
+    uint64_t *rec;
+    uint32_t wdl, wbl;
+    uint32_t *bits0, *bits1;
+    uint32_t a0, e0, a1, e1;
+    PrepState *st;
+};
+
+__global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
+    __shared__ uint32_t h[65];
+    if (A.do_lm) {
+        for (int i = threadIdx.x; i < 65; i += blockDim.x) h[i] = 0;
+        __syncthreads();
+    }
+    const uint32_t H = A.wdl + A.wbl, rw = 2 * H;
+    const uint64_t nr = ((uint64_t)A.n + 31) & ~31ull;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += stride) {
+        bool p0 = false, p1 = false;
+        if (i < A.n) {
+            const uint32_t v = (uint32_t)i;
+            uint8_t f;
+            uint32_t b;
+            if (A.do_lm || A.do_leaves) {
+                uint64_t out = A.f.ptr[v + 1] - A.f.ptr[v], in = A.r.ptr[v + 1] - A.r.ptr[v];
+                if (A.f.dptr) { out += A.f.dptr[v + 1] - A.f.dptr[v]; in += A.r.dptr[v + 1] - A.r.dptr[v]; }
+                if (A.do_lm) {
+                    const uint64_t sc = strategy_score(A.strategy, in, out);
+                    A.score[v] = sc;
+                    atomicAdd(&h[score_bin(sc)], 1u);
+                }
+                if (A.do_leaves) {
+                    f = 0;
+                    if (in == 0) f |= 1;
+                    if (out == 0) f |= 2;
+                    if (A.threshold > 0 && in * out <= A.threshold) f |= 3;
+                    b = 0;
+                    if (f) {
+                        const uint32_t o = A.ovr ? A.ovr[v] : 0xffffffffu;
+                        if (o != 0xffffffffu) {
+                            if (o >= A.k_prime) atomicOr(&A.st->err, 1ull);
+                            b = o;
+                        } else {
+                            b = leaf_hash_u64(v, A.k_prime, A.seed);
+                        }
+                    }
+                    A.flags[v] = f;
+                    A.bucket[v] = b;
+                }
+            }
+            if (!A.do_leaves) {
+                f = A.flags[v];
+                b = A.bucket[v];
+            }
+            // seeds: bl_in bit for source leaves, bl_out bit for sinks, dl words 0
+            const uint32_t bw = A.wdl + b / 64;
+            const uint32_t win = (f & 1) ? bw : 0xffffffffu;
+            const uint32_t wout = (f & 2) ? H + bw : 0xffffffffu;
+            const uint64_t bit = 1ull << (b % 64);
+            uint64_t *r = A.rec + (size_t)v * rw;
+            for (uint32_t w = 0; w < rw; w += 2) {
+                ulonglong2 val;
+                val.x = (w == win || w == wout) ? bit : 0ull;
+                val.y = (w + 1 == win || w + 1 == wout) ? bit : 0ull;
+                *reinterpret_cast<ulonglong2 *>(r + w) = val;
+            }
+            p0 = (f & 1) && bw >= A.a0 && bw < A.e0;
+            p1 = (f & 2) && H + bw >= A.a1 && H + bw < A.e1;
+        }
+        const unsigned b0 = __ballot_sync(FULL, p0), b1 = __ballot_sync(FULL, p1);
+        if ((threadIdx.x & 31) == 0) {
+            if (A.bits0) A.bits0[i >> 5] = b0;
+            if (A.bits1) A.bits1[i >> 5] = b1;
+        }
+    }
+    if (A.do_lm) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < 65; i += blockDim.x)
+            if (h[i]) atomicAdd(&A.st->hist[i], h[i]);
+    }
+}
+
+// Candidates of the top-k: every vertex whose score bin is at or above the
+// lowest bin that still holds the k-th best score (bins from the histogram;
+// each CTA derives the threshold itself).  Unordered; at most
+// PREP_CAND_CAP are stored, the count is exact.
+__global__ void __launch_bounds__(256) topk_candidates_kernel(const uint64_t *__restrict__ score, uint32_t n,
+                                                              uint32_t k, PrepState *st,
+                                                              uint64_t *__restrict__ cs, uint32_t *__restrict__ ci) {
+    __shared__ int tbin;
+    if (threadIdx.x == 0) {
+        uint64_t acc = 0;
+        int bin = 64;
+        for (; bin >= 0; --bin) {
+            acc += st->hist[bin];
+            if (acc >= k) break;
+        }
+        tbin = bin < 0 ? 0 : bin;
+    }
+    __syncthreads();
+    const int t = tbin;
+    const uint64_t nr = ((uint64_t)n + 31) & ~31ull;
+    const int lane = threadIdx.x & 31;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t sc = 0;
+        bool take = false;
+        if (i < n) {
+            sc = score[i];
+            take = score_bin(sc) >= t;
+        }
+        const unsigned m = __ballot_sync(FULL, take);
+        if (!m) continue;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&st->n_above, (uint32_t)__popc(m));
+        base = __shfl_sync(FULL, base, 0);
+        const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+        if (take && pos < PREP_CAND_CAP) {
+            cs[pos] = sc;
+            ci[pos] = (uint32_t)i;
+        }
+    }
+}
+
+__device__ __forceinline__ bool lm_better(uint64_t sa, uint32_t ia, uint64_t sb, uint32_t ib) {
+    return sa > sb || (sa == sb && ia < ib);
+}
+
+// One CTA: bitonic sort of the candidates by (-score, id) in shared memory,
+// the first k become the landmarks (position i owns bit i, labels.py:54-74);
+// their DL bits go into the seeded records and the level-0 bitmaps.
+__global__ void __launch_bounds__(1024) topk_final_kernel(const uint64_t *__restrict__ cs, const uint32_t *__restrict__ ci,
+                                                         uint32_t k, PrepState *st, uint32_t *__restrict__ lm,
+                                                         uint64_t *__restrict__ rec, uint32_t rw, uint32_t H,
+                                                         uint32_t *bits0, uint32_t *bits1, uint32_t a0, uint32_t e0,
+                                                         uint32_t a1, uint32_t e1) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    uint64_t *ss = reinterpret_cast<uint64_t *>(sm);
+    uint32_t *si = reinterpret_cast<uint32_t *>(ss + PREP_CAND_CAP);
+    const uint32_t c = st->n_above;
+    if (c > PREP_CAND_CAP || k > c) {
+        if (threadIdx.x == 0) st->fallback = 1;
+        return;
+    }
+    uint32_t p = 1;
+    while (p < c) p <<= 1;
+    for (uint32_t i = threadIdx.x; i < p; i += blockDim.x) {
+        ss[i] = i < c ? cs[i] : 0ull;
+        si[i] = i < c ? ci[i] : 0xffffffffu;   // padding sorts after every vertex
+    }
+    __syncthreads();
+    for (uint32_t kk = 2; kk <= p; kk <<= 1) {
+        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < p; i += blockDim.x) {
+                const uint32_t x = i ^ j;
+                if (x > i) {
+                    const bool up = (i & kk) == 0;
+                    const bool xb = lm_better(ss[x], si[x], ss[i], si[i]);
+                    if (up == xb) {
+                        const uint64_t ts = ss[i]; ss[i] = ss[x]; ss[x] = ts;
+                        const uint32_t ti = si[i]; si[i] = si[x]; si[x] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        const uint32_t v = si[i], w = i / 64;
+        const uint64_t bit = 1ull << (i % 64);
+        lm[i] = v;
+        uint64_t *r = rec + (size_t)v * rw;
+        r[w] |= bit;          // dl_in: the landmark reaches itself
+        r[H + w] |= bit;      // dl_out
+        if (bits0 && w >= a0 && w < e0) atomicOr(&bits0[v >> 5], 1u << (v & 31));
+        if (bits1 && H + w >= a1 && H + w < e1) atomicOr(&bits1[v >> 5], 1u << (v & 31));
+    }
+}
+
+// landmark bits of given (pinned or previously selected) landmarks
+__global__ void landmark_seed_kernel(const uint32_t *__restrict__ lm, uint32_t k, uint64_t *__restrict__ rec,
+                                     uint32_t rw, uint32_t H, uint32_t *bits0, uint32_t *bits1, uint32_t a0,
+                                     uint32_t e0, uint32_t a1, uint32_t e1) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
+        const uint32_t v = lm[i], w = i / 64;
+        const uint64_t bit = 1ull << (i % 64);
+        atomicOr(reinterpret_cast<unsigned long long *>(rec + (size_t)v * rw + w), bit);
+        atomicOr(reinterpret_cast<unsigned long long *>(rec + (size_t)v * rw + H + w), bit);
+        if (bits0 && w >= a0 && w < e0) atomicOr(&bits0[v >> 5], 1u << (v & 31));
+        if (bits1 && H + w >= a1 && H + w < e1) atomicOr(&bits1[v >> 5], 1u << (v & 31));
+    }
+}
+
+dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_t *bits1, uint32_t a0,
+                          uint32_t e0, uint32_t a1, uint32_t e1) {
+    const uint32_t n = g->n, k = idx->cfg.k;
+    const bool do_lm = idx->sel_landmarks && k > 0;
+    if (k > n) { set_error("k exceeds vertex count"); return DBL_E_CONFIG; }
+    if (idx->sel_leaves && idx->cfg.k_prime < 1) { set_error("k_prime must be >= 1"); return DBL_E_CONFIG; }
+    dbl_status s;
+    const size_t cand_bytes = (size_t)PREP_CAND_CAP * 12;
+    if ((s = g->prep.ensure(sizeof(PrepState) + 16 + cand_bytes))) return s;
+    if (do_lm && (s = g->scratch_a.ensure((size_t)n * 8 + 64))) return s;
+    PrepState *st = g->prep.as<PrepState>();
+    uint64_t *cs = reinterpret_cast<uint64_t *>(g->prep.as<char>() + ((sizeof(PrepState) + 15) & ~15ull));
+    uint32_t *ci = reinterpret_cast<uint32_t *>(cs + PREP_CAND_CAP);
+    DBL_CUDA(cudaMemsetAsync(st, 0, sizeof(PrepState), g->stream));
+    PrepArgs A{};
+    A.f = graph_fwd(g);
+    A.r = graph_rev(g);
+    A.n = n;
+    A.strategy = idx->cfg.strategy;
+    A.do_lm = do_lm;
+    A.do_leaves = idx->sel_leaves;
+    A.score = do_lm ? g->scratch_a.as<uint64_t>() : nullptr;
+    A.threshold = idx->cfg.leaf_threshold;
+    A.k_prime = idx->cfg.k_prime;
+    A.seed = idx->cfg.hash_seed;
+    A.ovr = idx->ovr.p ? idx->ovr.as<uint32_t>() : nullptr;
+    A.flags = idx->leaf_flags.as<uint8_t>();
+    A.bucket = idx->bucket.as<uint32_t>();
+    A.rec = idx->rec.as<uint64_t>();
+    A.wdl = idx->wdl;
+    A.wbl = idx->wbl;
+    A.bits0 = bits0;
+    A.bits1 = bits1;
+    A.a0 = a0; A.e0 = e0; A.a1 = a1; A.e1 = e1;
+    A.st = st;
+    int blocks = (int)(((uint64_t)n + 255) / 256);
+    if (blocks > g->sm_count * 8) blocks = g->sm_count * 8;
+    if (blocks < 1) blocks = 1;
+    prep_kernel<<<blocks, 256, 0, g->stream>>>(A);
+    DBL_CHECK_LAUNCH("prep_kernel");
+    const uint32_t H = idx->wdl + idx->wbl;
+    if (do_lm) {
+        topk_candidates_kernel<<<blocks, 256, 0, g->stream>>>(A.score, n, k, st, cs, ci);
+        DBL_CHECK_LAUNCH("topk_candidates_kernel");
+        const int fsmem = (int)cand_bytes;
+        static bool attr = false;
+        if (!attr) {
+            DBL_CUDA(cudaFuncSetAttribute((const void *)topk_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          fsmem));
+            attr = true;
+        }
+        topk_final_kernel<<<1, 1024, fsmem, g->stream>>>(cs, ci, k, st, idx->landmarks.as<uint32_t>(), A.rec, idx->rw,
+                                                         H, bits0, bits1, a0, e0, a1, e1);
+        DBL_CHECK_LAUNCH("topk_final_kernel");
+    } else if (k) {
+        landmark_seed_kernel<<<(k + 255) / 256, 256, 0, g->stream>>>(idx->landmarks.as<uint32_t>(), k, A.rec, idx->rw,
+                                                                    H, bits0, bits1, a0, e0, a1, e1);
+        DBL_CHECK_LAUNCH("landmark_seed_kernel");
+    }
+    return DBL_OK;
+}
+
+dbl_status prep_fetch(dbl_graph *g, PrepState *host) {
+    DBL_CUDA(cudaMemcpyAsync(host, g->prep.p, sizeof(PrepState), cudaMemcpyDeviceToHost, g->stream));
+    return DBL_OK;
+}
+
 }  // namespace dbl
 
 using namespace dbl;
@@ -241,8 +522,7 @@ extern "C" dbl_status dbl_select_landmarks(const dbl_graph *g, uint32_t k, int32
 }
 
 __global__ void scatter_ovr_kernel(const uint32_t *__restrict__ ids, const uint32_t *__restrict__ b,
-                                   uint32_t cnt, uint32_t n, uint32_t *__restrict__ ovr,
-                                   unsigned long long *err) {
+                                   uint32_t cnt, uint32_t n, uint32_t *__restrict__ ovr) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
         if (ids[i] >= n) continue;  // labels.py:167-171 only consults leaves
         ovr[ids[i]] = b[i];
@@ -258,21 +538,15 @@ dbl_status make_override(dbl_graph *g, const uint32_t *ids, const uint32_t *buck
     if (s) return s;
     uint32_t *o = ovr.as<uint32_t>();
     uint32_t *di = o + n, *db = di + cnt;
-    unsigned long long *err = reinterpret_cast<unsigned long long *>(g->scratch_c.p);
-    if ((s = g->scratch_c.ensure(16))) return s;
-    err = g->scratch_c.as<unsigned long long>();
     DBL_CUDA(cudaMemsetAsync(o, 0xff, (size_t)n * 4, g->stream));
-    DBL_CUDA(cudaMemsetAsync(err, 0, 8, g->stream));
     if (cnt) {
+        // host arrays are copied before this returns (pageable H2D copies
+        // are staged synchronously), so the caller may free them
         DBL_CUDA(cudaMemcpyAsync(di, ids, (size_t)cnt * 4, cudaMemcpyHostToDevice, g->stream));
         DBL_CUDA(cudaMemcpyAsync(db, buckets, (size_t)cnt * 4, cudaMemcpyHostToDevice, g->stream));
-        scatter_ovr_kernel<<<(cnt + 255) / 256, 256, 0, g->stream>>>(di, db, cnt, n, o, err);
+        scatter_ovr_kernel<<<(cnt + 255) / 256, 256, 0, g->stream>>>(di, db, cnt, n, o);
         DBL_CHECK_LAUNCH("scatter_ovr_kernel");
     }
-    unsigned long long herr = 0;
-    DBL_CUDA(cudaMemcpyAsync(&herr, err, 8, cudaMemcpyDeviceToHost, g->stream));
-    DBL_CUDA(cudaStreamSynchronize(g->stream));
-    (void)herr;
     return DBL_OK;
 }
 }  // namespace dbl

@@ -59,7 +59,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     flush2 = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     flags = E.DEFAULT_FLAGS.bits()
-    step, kern = [], []
+    step, kern, lab = [], [], []
     tl, tb = N.ctypes.c_float(), N.ctypes.c_float()
     with torch.cuda.stream(stream):
         for i in range(a.reps + 3):
@@ -75,6 +75,7 @@ def main():
             if i >= 3:
                 step.append(e0.elapsed_time(e1))
                 kern.append(tl.value + tb.value)
+                lab.append(tl.value)
     c = codes.cpu().numpy()
     iu, iv = W.gen_insert_workload(src, dst, n, 100_000, 50)
     torch.cuda.synchronize()
@@ -83,6 +84,7 @@ def main():
     ins = time.perf_counter() - t0
     print(json.dumps({
         "step_us": round(1e3 * statistics.median(step), 2), "kernel_us": round(1e3 * statistics.median(kern), 2),
+        "label_us": round(1e3 * statistics.median(lab), 2),
         "Gq_s": round(a.batch / statistics.median(step) / 1e6, 2),
         "build_ms": round(statistics.median(bt), 3), "fixpoint_ms": round(statistics.median(ft), 3),
         "insert_edges_s": round(st.inserted / ins / 1e6, 1),
