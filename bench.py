@@ -310,7 +310,7 @@ def run_ours(args, rank, world, local_rank):
     q_bytes = 8 + 1 + 4 + 2 * rec_bytes
     k6_ms = statistics.median(label_ms)
     achieved = BATCH * q_bytes / (k6_ms / 1e3) / 1e9
-    traffic = ncu_traffic("query_fused_kernel")
+    traffic = ncu_traffic("label_lean_kernel")
     build_achieved = build_bytes / (build_ms_max / 1e3) / 1e9
     result = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
@@ -322,7 +322,7 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "flushed before every timed step (256 MB write, then 256 MB read so no dirty lines remain)",
                    "parallelism": f"replicated graph+labels, word-sharded build + NCCL allgather, "
                                   f"one 1M batch per GPU x{world}"},
-        "roofline": {"bound": "hbm", "kernel": "query_fused_kernel<1,1> (K6 label check + K7 warp BFS, one launch)",
+        "roofline": {"bound": "hbm", "kernel": "label_lean_kernel<1,1> (K6 label check + deferred per-lane K7 BFS, one launch)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "bytes_per_query": q_bytes, "kernel_ms": k6_ms},

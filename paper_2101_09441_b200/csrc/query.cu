@@ -1002,6 +1002,12 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
 // dl_out[u] & dl_in[v] != 0 or violate BL containment), so v is found iff
 // it is reachable, in any visiting order.
 constexpr int TB_Q = 8;
+constexpr uint32_t DQ_CAP = 128;   // deferred queries per CTA (more go to the warp BFS)
+struct DeferQ {
+    uint64_t dlo[DQ_CAP], bli[DQ_CAP], blo[DQ_CAP];
+    uint32_t i[DQ_CAP], u[DQ_CAP], v[DQ_CAP];
+    uint32_t n;
+};
 #ifndef DBL_LMINB
 #define DBL_LMINB 4
 #endif
@@ -1076,14 +1082,16 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t cr = (count + 31) & ~31u;
     const int lane = threadIdx.x & 31;
-    // Unresolved queries are deferred to after the thread's label checks
-    // (bit it of dmask = iteration it), so a BFS never stalls the warp's
-    // gathers; afterwards every lane runs its own deferred BFS chains in
-    // parallel with the other lanes'.
+    // Unresolved queries are deferred to a per-CTA queue (their BFS inputs
+    // staged in shared memory, the source's row pointer prefetched into L2),
+    // so a BFS never stalls the gathers; after the label checks each thread
+    // of the CTA takes one queued query, so the CTA pays about one BFS chain
+    // however its unresolved queries fell on its warps.
+    __shared__ DeferQ dq;
+    if (threadIdx.x == 0) dq.n = 0;
+    __syncthreads();
     const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t dmask = 0;
-    uint32_t it = 0;
-    for (uint32_t i = i0; i < cr; i += stride, ++it) {
+    for (uint32_t i = i0; i < cr; i += stride) {
         bool unres = false;
         if (i < count) {
             const uint32_t u = __ldg(qd.u + i), v = __ldg(qd.v + i);
@@ -1112,9 +1120,22 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
                 else if (thm1 && r3) code = DBL_THM1_NEGATIVE;
                 else if (thm2 && r4) code = DBL_THM2_NEGATIVE;
             }
-            if (TBFS && code == UNRESOLVED && it < 32) {
-                dmask |= 1u << it;
-            } else {
+            bool queued = false;
+            if (TBFS && code == UNRESOLVED) {
+                const uint32_t slot = atomicAdd(&dq.n, 1u);
+                if (slot < DQ_CAP) {
+                    const uint64_t *ru = rec + (size_t)u * RW, *rv = rec + (size_t)v * RW;
+                    dq.i[slot] = i;
+                    dq.u[slot] = u;
+                    dq.v[slot] = v;
+                    dq.dlo[slot] = WDL ? __ldg(ru + H) : 0ull;   // L1/L2 hits: just gathered
+                    dq.bli[slot] = __ldg(rv + WDL);
+                    dq.blo[slot] = __ldg(rv + H + WDL);
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(adj.ptr + u));
+                    queued = true;
+                }
+            }
+            if (!queued) {
                 qd.codes[i] = code;
                 if (qd.visited) qd.visited[i] = 0;
                 unres = code == UNRESOLVED;
@@ -1129,16 +1150,13 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
         }
     }
     if constexpr (TBFS) {
-        while (dmask) {
-            const int b0 = __ffs(dmask) - 1;
-            dmask &= dmask - 1;
-            const uint32_t i = i0 + (uint32_t)b0 * stride;
-            const uint32_t u = __ldg(qd.u + i), v = __ldg(qd.v + i);
-            const uint64_t *ru = rec + (size_t)u * RW, *rv = rec + (size_t)v * RW;
-            const uint64_t dlo_u = WDL ? __ldg(ru + H) : 0ull;
-            const uint64_t bli_v = __ldg(rv + WDL), blo_v = __ldg(rv + H + WDL);
+        __syncthreads();
+        const uint32_t nq = min(dq.n, DQ_CAP);
+        for (uint32_t t = threadIdx.x; t < nq; t += blockDim.x) {
+            const uint32_t i = dq.i[t];
             uint32_t vc = 0;
-            const int r = thread_bfs<WDL, WBL>(rec, adj, u, v, dlo_u, bli_v, blo_v, prune_dl, prune_bl, &vc);
+            const int r = thread_bfs<WDL, WBL>(rec, adj, dq.u[t], dq.v[t], dq.dlo[t], dq.bli[t], dq.blo[t], prune_dl,
+                                               prune_bl, &vc);
             if (r == 2) {
                 pending[atomicAdd(&counters[CNT_PENDING], 1u)] = i;
             } else {

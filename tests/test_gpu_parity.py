@@ -411,3 +411,53 @@ def test_word_sharded_build_single_process(world):
             if p != r and plan[p]:
                 eng.unpack(plan[p], gathered[p * per:(p + 1) * per])
         assert eng.idx.labels_equal(full), r
+
+
+# ------------------------------------------- device landmark top-k (prep) --
+
+@pytest.mark.parametrize("strategy", ["product", "sum", "max", "min"])
+def test_topk_flat_scores_fallback(strategy):
+    """Every vertex of a directed cycle has score 1 (or 2): more candidates in
+    the threshold bin than the on-chip sort holds, so the build re-selects
+    with the radix-sort path.  Landmarks must be ids 0..k-1 (ties by id,
+    labels.py:145-146) and the labels equal the oracle's."""
+    n = 20_000
+    src = np.arange(n, dtype=np.uint32)
+    dst = ((src + 1) % n).astype(np.uint32)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    cfg = E.IndexConfig(k=64, landmark_strategy=E.LandmarkStrategy(strategy))
+    idx = E.build_index(g, cfg)
+    og = O.OracleGraph(n, src, dst)
+    oidx = og.build(64, 64, strategy=strategy, threads=8)
+    assert idx.landmark_set.landmarks == tuple(range(64))
+    np.testing.assert_array_equal(np.array(idx.landmark_set.landmarks), oidx.landmarks)
+    assert_labels_equal_oracle(idx, oidx)
+
+
+@pytest.mark.parametrize("n_hot", [8000, 8300])
+def test_topk_candidate_table_boundary(n_hot):
+    """n_hot vertices share the top score bin (just under / just over the
+    8192-entry on-chip candidate table): both paths give the oracle's
+    landmarks and labels."""
+    rng = np.random.default_rng(n_hot)
+    n = 30_000
+    # hot vertices: in = out = 3 (score 9, bin 4); the rest: degree <= 1
+    hot = np.arange(n_hot, dtype=np.uint32)
+    src, dst = [], []
+    for j in range(3):
+        src.append(hot)
+        dst.append(((hot + 1 + j * 977) % n_hot).astype(np.uint32))
+    cold = np.arange(n_hot, n, dtype=np.uint32)
+    src.append(cold[:-1])
+    dst.append(cold[1:])
+    src = np.concatenate(src).astype(np.uint32)
+    dst = np.concatenate(dst).astype(np.uint32)
+    perm = rng.permutation(n).astype(np.uint32)   # scatter the hot ids
+    src, dst = perm[src], perm[dst]
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    og = O.OracleGraph(n, src, dst)
+    for k in (64, 256):
+        idx = E.build_index(g, E.IndexConfig(k=k))
+        oidx = og.build(k, 64, threads=8)
+        np.testing.assert_array_equal(np.array(idx.landmark_set.landmarks), oidx.landmarks)
+        assert_labels_equal_oracle(idx, oidx)

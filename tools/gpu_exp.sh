@@ -4,4 +4,4 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 for so in paper_2101_09441_b200/_lib/libdbl_b200.so paper_2101_09441_b200/_lib/variant_*.so; do
   echo "== $so"; DBL_LIB_PATH=$PWD/$so timeout 300 python tools/qbench.py 2>&1 | tail -1
 done
-DBL_LIB_PATH=$PWD/paper_2101_09441_b200/_lib/variant_fix1024.so DBL_TRACE=1 timeout 300 python tools/qbench.py --reps 3 2>&1 | grep "level" | tail -7
+DBL_TRACE=1 timeout 300 python tools/qbench.py --reps 3 2>&1 | grep "level" | tail -14
