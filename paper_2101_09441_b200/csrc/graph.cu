@@ -98,6 +98,47 @@ dbl_status build_csr_from_sorted(dbl_graph *g, const uint64_t *keys, uint64_t m,
     return DBL_OK;
 }
 
+// in-degree per destination of forward keys (u << 32 | v)
+__global__ void count_dst_kernel(const uint64_t *__restrict__ keys, uint64_t m, uint32_t *__restrict__ cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(&cnt[(uint32_t)keys[i]], 1u);
+}
+
+// col[cursor[v]++] = u for every forward key (u, v): the reverse adjacency
+// by counting scatter (rows in arbitrary order; every consumer of the delta
+// CSC -- fixpoint, verifier, floods -- is order-independent)
+__global__ void scatter_src_kernel(const uint64_t *__restrict__ keys, uint64_t m, uint32_t *__restrict__ cursor,
+                                   uint32_t *__restrict__ col) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        col[atomicAdd(&cursor[(uint32_t)k], 1u)] = (uint32_t)(k >> 32);
+    }
+}
+
+// Reverse CSR (ptr[0..n], col) of the forward keys by counting sort.
+static dbl_status build_csc_by_scatter(dbl_graph *g, const uint64_t *fkeys, uint64_t m, uint32_t n, uint32_t *ptr,
+                                       uint32_t *col) {
+    dbl_status s = g->scratch_d.ensure(((size_t)n + 1) * 2 * sizeof(uint32_t));
+    if (s) return s;
+    uint32_t *cnt = g->scratch_d.as<uint32_t>(), *cursor = cnt + n + 1;
+    DBL_CUDA(cudaMemsetAsync(cnt, 0, ((size_t)n + 1) * sizeof(uint32_t), g->stream));
+    if (m) {
+        count_dst_kernel<<<grid_for(m), 256, 0, g->stream>>>(fkeys, m, cnt);
+        DBL_CHECK_LAUNCH("count_dst_kernel");
+    }
+    size_t tmp = 0;
+    DBL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, ptr, (int64_t)n + 1, g->stream));
+    if ((s = g->cub_tmp.ensure(tmp))) return s;
+    DBL_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.p, tmp, cnt, ptr, (int64_t)n + 1, g->stream));
+    DBL_LAUNCHED();
+    if (m) {
+        DBL_CUDA(cudaMemcpyAsync(cursor, ptr, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, g->stream));
+        scatter_src_kernel<<<grid_for(m), 256, 0, g->stream>>>(fkeys, m, cursor, col);
+        DBL_CHECK_LAUNCH("scatter_src_kernel");
+    }
+    return DBL_OK;
+}
+
 static dbl_status unique_keys(dbl_graph *g, const uint64_t *in, uint64_t m, uint64_t *out,
                               uint64_t *nout) {
     if (m == 0) { *nout = 0; return DBL_OK; }
@@ -289,10 +330,10 @@ dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t
         const uint64_t need = nd + count;
         uint64_t cap = g->m_base / 4 + 2 * count + 1024;
         if (cap < need) cap = need + need / 2;
-        DevBuf *kb[3] = {&g->dkeys_f, &g->dkeys_r, &g->dmerge};
+        DevBuf *kb[2] = {&g->dkeys_f, &g->dmerge};
         for (DevBuf *b : kb) {
             if (b->bytes < need * 8 + 8) {
-                if (b == &g->dkeys_f || b == &g->dkeys_r) {
+                if (b == &g->dkeys_f) {
                     if (nd) {  // keep the contents
                         DevBuf nb;
                         if ((s = nb.ensure(cap * 8 + 8))) return s;
@@ -309,25 +350,13 @@ dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t
         if (g->dfcol.bytes < need * 4 + 4) { g->dfcol.release(); if ((s = g->dfcol.ensure(cap * 4 + 4))) return s; }
         if (g->drcol.bytes < need * 4 + 4) { g->drcol.release(); if ((s = g->drcol.ensure(cap * 4 + 4))) return s; }
     }
-    // reverse keys of the new edges, sorted
-    if ((s = g->scratch_a.ensure(count * 8 + 8)) || (s = g->scratch_b.ensure(count * 8 + 8))) return s;
-    uint64_t *ra = g->scratch_a.as<uint64_t>(), *rb = g->scratch_b.as<uint64_t>();
-    swap_keys_kernel<<<grid_for(count), 256, 0, g->stream>>>(new_keys_f, count, ra);
-    DBL_CHECK_LAUNCH("swap_keys_kernel");
-    uint64_t *rsorted = nullptr;
-    if ((s = sort_keys(g, ra, rb, count, key_end_bit(n), &rsorted))) return s;
-    trace("delta: reverse sort", g->stream);
     if (nd == 0) {
-        if ((s = g->dkeys_f.ensure_geometric(count * 8 + 8)) || (s = g->dkeys_r.ensure_geometric(count * 8 + 8)))
-            return s;
+        if ((s = g->dkeys_f.ensure_geometric(count * 8 + 8))) return s;
         DBL_CUDA(cudaMemcpyAsync(g->dkeys_f.p, new_keys_f, count * 8, cudaMemcpyDeviceToDevice, g->stream));
-        DBL_CUDA(cudaMemcpyAsync(g->dkeys_r.p, rsorted, count * 8, cudaMemcpyDeviceToDevice, g->stream));
     } else {
         // merged keys go to the spare buffer, which then swaps with the old one
         if ((s = merge_into(g, g->dkeys_f, nd, new_keys_f, count, g->dmerge))) return s;
         trace("delta: merge fwd", g->stream);
-        if ((s = merge_into(g, g->dkeys_r, nd, rsorted, count, g->dmerge))) return s;
-        trace("delta: merge rev", g->stream);
     }
     uint64_t m = nd + count;
     if ((s = g->dfptr.ensure(((size_t)n + 1) * 4)) || (s = g->drptr.ensure(((size_t)n + 1) * 4)) ||
@@ -336,8 +365,8 @@ dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t
     if ((s = build_csr_from_sorted(g, g->dkeys_f.as<uint64_t>(), m, n, g->dfptr.as<uint32_t>(),
                                    g->dfcol.as<uint32_t>())))
         return s;
-    if ((s = build_csr_from_sorted(g, g->dkeys_r.as<uint64_t>(), m, n, g->drptr.as<uint32_t>(),
-                                   g->drcol.as<uint32_t>())))
+    if ((s = build_csc_by_scatter(g, g->dkeys_f.as<uint64_t>(), m, n, g->drptr.as<uint32_t>(),
+                                  g->drcol.as<uint32_t>())))
         return s;
     trace("delta: csr+csc", g->stream);
     g->m_delta = m;

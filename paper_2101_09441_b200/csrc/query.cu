@@ -1003,8 +1003,12 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
 // it is reachable, in any visiting order.
 constexpr int TB_Q = 8;
 constexpr uint32_t DQ_CAP = 128;   // deferred queries per CTA (more go to the warp BFS)
+// A deferred query: its index, endpoints and the words its pruning needs
+// (dl_out[u], bl_in[v], bl_out[v]; queries.py:137-140).
+template <int WDL, int WBL>
 struct DeferQ {
-    uint64_t dlo[DQ_CAP], bli[DQ_CAP], blo[DQ_CAP];
+    static constexpr int WD = WDL > 0 ? WDL : 1;
+    uint64_t dlo[DQ_CAP][WD], bli[DQ_CAP][WBL], blo[DQ_CAP][WBL];
     uint32_t i[DQ_CAP], u[DQ_CAP], v[DQ_CAP];
     uint32_t n;
 };
@@ -1015,10 +1019,12 @@ constexpr uint32_t TB_E = 48;
 
 template <int WDL, int WBL>
 __device__ __forceinline__ int thread_bfs(const uint64_t *__restrict__ rec, const Adj adj, uint32_t u, uint32_t v,
-                                       uint64_t dlo_u0, uint64_t bli_v0, uint64_t blo_v0, bool prune_dl,
-                                       bool prune_bl, uint32_t *vcount) {
+                                       const uint64_t *dlo_u, const uint64_t *bli_v, const uint64_t *blo_v,
+                                       bool prune_dl, bool prune_bl, uint32_t *vcount) {
     constexpr int H = WDL + WBL, RW = 2 * H;
-    static_assert(WDL <= 1 && WBL == 1, "thread BFS handles one word per family");
+    // neighbours in flight per step: their pruning words (dl_in, bl_in,
+    // bl_out of x) are loaded word by word, fewer at a time for wide labels
+    constexpr int NB = (WDL + 2 * WBL) <= 3 ? 4 : 2;
     uint32_t q[TB_Q];
     q[0] = u;
     int qn = 1;
@@ -1031,29 +1037,48 @@ __device__ __forceinline__ int thread_bfs(const uint64_t *__restrict__ rec, cons
             const uint32_t *col = seg ? adj.dcol : adj.col;
             const uint32_t s0 = __ldg(ptr + w), s1 = __ldg(ptr + w + 1);
             if (s1 - s0 > TB_E) return 2;
-            for (uint32_t j0 = s0; j0 < s1; j0 += 4) {
-                uint32_t x[4];
+            for (uint32_t j0 = s0; j0 < s1; j0 += NB) {
+                uint32_t x[NB];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) x[t] = j0 + t < s1 ? __ldg(col + j0 + t) : 0xffffffffu;
+                for (int t = 0; t < NB; ++t) x[t] = j0 + t < s1 ? __ldg(col + j0 + t) : 0xffffffffu;
 #pragma unroll
-                for (int t = 0; t < 4; ++t)
+                for (int t = 0; t < NB; ++t)
                     if (x[t] == v) return 1;     // target test precedes the visited test
-                bool fresh[4];
+                bool fresh[NB];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
+                for (int t = 0; t < NB; ++t) {
                     fresh[t] = x[t] != 0xffffffffu;
                     for (int k = 0; k < qn; ++k) fresh[t] &= q[k] != x[t];
                 }
-                uint64_t xr[4][RW];
+                uint64_t xi[NB][WDL > 0 ? WDL : 1], xbi[NB][WBL], xbo[NB][WBL];
 #pragma unroll
-                for (int t = 0; t < 4; ++t)
-                    if (fresh[t] && (prune_dl || prune_bl)) load_record<RW>(rec + (size_t)x[t] * RW, xr[t]);
+                for (int t = 0; t < NB; ++t) {
+                    if (!fresh[t]) continue;
+                    const uint64_t *rx = rec + (size_t)x[t] * RW;
+                    if (prune_dl) {
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
+                        for (int k = 0; k < WDL; ++k) xi[t][k] = __ldg(rx + k);
+                    }
+                    if (prune_bl) {
+#pragma unroll
+                        for (int k = 0; k < WBL; ++k) {
+                            xbi[t][k] = __ldg(rx + WDL + k);
+                            xbo[t][k] = __ldg(rx + H + WDL + k);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < NB; ++t) {
                     if (!fresh[t]) continue;
                     bool p = false;
-                    if (prune_dl && WDL) p = (dlo_u0 & xr[t][0]) != 0;                                  // queries.py:137-138
-                    if (prune_bl && !p) p = ((xr[t][WDL] & ~bli_v0) | (blo_v0 & ~xr[t][H + WDL])) != 0;  // :139-140
+                    if (prune_dl) {   // queries.py:137-138
+#pragma unroll
+                        for (int k = 0; k < WDL; ++k) p |= (dlo_u[k] & xi[t][k]) != 0;
+                    }
+                    if (prune_bl && !p) {   // queries.py:139-140
+#pragma unroll
+                        for (int k = 0; k < WBL; ++k) p |= ((xbi[t][k] & ~bli_v[k]) | (blo_v[k] & ~xbo[t][k])) != 0;
+                    }
                     if (p) continue;
                     if (qn == TB_Q) return 2;
                     q[qn++] = x[t];
@@ -1074,7 +1099,10 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
                                                           const QueryDesc qd, uint32_t *__restrict__ pending,
                                                           uint32_t *__restrict__ counters, const HardArgs ha) {
     constexpr int H = WDL + WBL, RW = 2 * H;
-    constexpr bool TBFS = WDL <= 1 && WBL == 1;
+    // the per-thread BFS pays off for k <= 64; with wider labels (cfg5:
+    // k = 256, d = 16) most fallbacks outgrow its bounds (measured: 79% of
+    // cfg5's unresolved queries), so they go straight to the warp BFS
+    constexpr bool TBFS = WDL <= 1;
     const uint32_t flags = qd.flags, count = qd.count;
     const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
     const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
@@ -1087,7 +1115,7 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
     // so a BFS never stalls the gathers; after the label checks each thread
     // of the CTA takes one queued query, so the CTA pays about one BFS chain
     // however its unresolved queries fell on its warps.
-    __shared__ DeferQ dq;
+    __shared__ DeferQ<WDL, WBL> dq;
     if (threadIdx.x == 0) dq.n = 0;
     __syncthreads();
     const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1095,6 +1123,7 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
         bool unres = false;
         if (i < count) {
             const uint32_t u = __ldg(qd.u + i), v = __ldg(qd.v + i);
+            constexpr uint8_t QUEUED = 0xfc;   // in the CTA's BFS queue (code written later)
             uint8_t code = UNRESOLVED;
             if (u >= n || v >= n) {
                 atomicOr(&counters[CNT_ERR], 1u);
@@ -1119,23 +1148,25 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
                 else if (use_bl && r2) code = DBL_BL_NEGATIVE;
                 else if (thm1 && r3) code = DBL_THM1_NEGATIVE;
                 else if (thm2 && r4) code = DBL_THM2_NEGATIVE;
-            }
-            bool queued = false;
-            if (TBFS && code == UNRESOLVED) {
-                const uint32_t slot = atomicAdd(&dq.n, 1u);
-                if (slot < DQ_CAP) {
-                    const uint64_t *ru = rec + (size_t)u * RW, *rv = rec + (size_t)v * RW;
-                    dq.i[slot] = i;
-                    dq.u[slot] = u;
-                    dq.v[slot] = v;
-                    dq.dlo[slot] = WDL ? __ldg(ru + H) : 0ull;   // L1/L2 hits: just gathered
-                    dq.bli[slot] = __ldg(rv + WDL);
-                    dq.blo[slot] = __ldg(rv + H + WDL);
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(adj.ptr + u));
-                    queued = true;
+                if (TBFS && code == UNRESOLVED) {
+                    const uint32_t slot = atomicAdd(&dq.n, 1u);
+                    if (slot < DQ_CAP) {
+                        dq.i[slot] = i;
+                        dq.u[slot] = u;
+                        dq.v[slot] = v;
+#pragma unroll
+                        for (int k = 0; k < WDL; ++k) dq.dlo[slot][k] = a[H + k];   // still in registers
+#pragma unroll
+                        for (int k = 0; k < WBL; ++k) {
+                            dq.bli[slot][k] = b[WDL + k];
+                            dq.blo[slot][k] = b[H + WDL + k];
+                        }
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(adj.ptr + u));
+                        code = QUEUED;
+                    }
                 }
             }
-            if (!queued) {
+            if (code != QUEUED) {
                 qd.codes[i] = code;
                 if (qd.visited) qd.visited[i] = 0;
                 unres = code == UNRESOLVED;
