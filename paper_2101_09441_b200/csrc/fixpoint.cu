@@ -819,6 +819,214 @@ dbl_status index_seed_records(dbl_graph *g, dbl_index *idx, uint64_t wmask) {
     return DBL_OK;
 }
 
+// ------------------------------------------------------ pivot head start --
+//
+// Labels are least fixpoints, so any vertex may start from any subset of its
+// final label without changing the result.  Pick a pivot h (landmark 0, the
+// top-ranked hub) and compute D(h) = vertices reachable from h and A(h) =
+// vertices reaching h with a one-bit fixpoint per direction.  Every x in
+// D(h) ends with L_in(x) >= L_in(h) = OR of the in-seeds over A(h), every
+// x in A(h) with L_out(x) >= L_out(h) = OR of the out-seeds over D(h), so
+// those unions are ORed in before the label fixpoint.  D(h) is closed under
+// successors and A(h) under predecessors, so the head-start bits need no
+// propagation of their own: the label fixpoint then only moves the seed bits
+// the pivot's unions do not already hold.  On R-MAT the pivot's SCC holds
+// every seed bit, so this replaces the two label levels that relax almost
+// every edge (with multi-bit labels) by one single-bit reachability sweep
+// per direction.
+
+// Reachability of the pivot by bottom-up sweeps (direction-optimised BFS
+// without the top-down levels after the first): vis[0] = reached from h,
+// vis[1] = reaches h.  Each sweep, every unmarked vertex scans its
+// predecessors in that direction (in-edges for vis[0], out-edges for vis[1])
+// and stops at the first marked one -- on R-MAT almost every vertex of the
+// giant SCC finds a marked hub among its first neighbours, so a sweep costs
+// about one neighbour check per vertex instead of a push along every edge.
+// Marks made during a sweep may be seen by later vertices of the same sweep
+// (fewer sweeps); a stale L1 copy only defers a mark to the next sweep.
+struct ReachParams {
+    Adj adj[2];          // [0] in-edges (reverse adjacency), [1] out-edges (forward adjacency)
+    Adj top[2];          // first level from h: [0] out-edges, [1] in-edges
+    uint32_t *vis[2];
+    unsigned int *changed;   // [sweep % 3]: written in sweep s, read after its barrier, cleared in s + 2;
+                             // [3]: set when the sweep cap stopped the search (no head start then)
+    uint32_t max_sweeps;
+    const uint32_t *lm;
+    uint32_t n, nwords;
+};
+
+__device__ __forceinline__ bool vis_test_ca(const uint32_t *vis, uint32_t x) {
+    uint32_t w;
+    asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(w) : "l"(vis + (x >> 5)));
+    return (w >> (x & 31)) & 1u;
+}
+
+__device__ __forceinline__ bool any_marked(const Adj &a, const uint32_t *vis, uint32_t x) {
+    uint32_t s0 = __ldg(a.ptr + x), s1 = __ldg(a.ptr + x + 1);
+    for (uint32_t j = s0; j < s1; ++j)
+        if (vis_test_ca(vis, __ldg(a.col + j))) return true;
+    if (a.dptr) {
+        s0 = __ldg(a.dptr + x);
+        s1 = __ldg(a.dptr + x + 1);
+        for (uint32_t j = s0; j < s1; ++j)
+            if (vis_test_ca(vis, __ldg(a.dcol + j))) return true;
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
+    cg::grid_group grid = cg::this_grid();
+    const uint32_t h = P.lm[0];
+    if (h >= P.n) return;   // grid-uniform: no pivot, no head start
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    // h and its direct successors / predecessors (top-down first level)
+    if (tid == 0) {
+        atomicOr(&P.vis[0][h >> 5], 1u << (h & 31));
+        atomicOr(&P.vis[1][h >> 5], 1u << (h & 31));
+    }
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+        const Adj &a = P.top[d];
+        const uint32_t s0 = a.ptr[h], s1 = a.ptr[h + 1];
+        for (uint64_t j = s0 + tid; j < s1; j += nth) {
+            const uint32_t y = a.col[j];
+            atomicOr(&P.vis[d][y >> 5], 1u << (y & 31));
+        }
+        if (a.dptr) {
+            const uint32_t t0 = a.dptr[h], t1 = a.dptr[h + 1];
+            for (uint64_t j = t0 + tid; j < t1; j += nth) {
+                const uint32_t y = a.dcol[j];
+                atomicOr(&P.vis[d][y >> 5], 1u << (y & 31));
+            }
+        }
+    }
+    grid.sync();
+    for (uint32_t sweep = 0;; ++sweep) {
+        if (sweep == P.max_sweeps) {
+            // deep graph: D/A incomplete, hence not closed under successors /
+            // predecessors -- the head start is dropped (labels stay exact)
+            if (tid == 0) P.changed[3] = 1;
+            break;
+        }
+        const int cb = sweep % 3;
+        bool any = false;
+        for (uint64_t x = tid; x < P.n; x += nth) {
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+                const uint32_t w = *(volatile uint32_t *)&P.vis[d][x >> 5];
+                if ((w >> (x & 31)) & 1u) continue;
+                if (any_marked(P.adj[d], P.vis[d], (uint32_t)x)) {
+                    atomicOr(&P.vis[d][x >> 5], 1u << (x & 31));
+                    any = true;
+                }
+            }
+        }
+        if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(&P.changed[cb], 1u);
+        if (tid == 0) P.changed[(sweep + 1) % 3] = 0;
+        grid.sync();
+        if (!*(volatile unsigned int *)&P.changed[cb]) {
+            if (tid == 0) P.changed[4] = sweep + 1;   // sweeps run (trace)
+            break;
+        }
+    }
+}
+
+// L[0..H) = OR of the in-halves over A(h); L[H..2H) = OR of the out-halves over D(h)
+__global__ void reach_union_kernel(const uint32_t *__restrict__ vf, const uint32_t *__restrict__ vb,
+                                   const uint64_t *__restrict__ rec, uint32_t n, uint32_t H,
+                                   unsigned long long *__restrict__ L, const unsigned int *incomplete) {
+    if (*incomplete) return;
+    __shared__ unsigned long long acc[2 * MAX_SHARD_WORDS];
+    for (uint32_t i = threadIdx.x; i < 2 * H; i += blockDim.x) acc[i] = 0;
+    __syncthreads();
+    const uint32_t rw = 2 * H;
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+        const bool fwd = (vf[x >> 5] >> (x & 31)) & 1u, bwd = (vb[x >> 5] >> (x & 31)) & 1u;
+        const uint64_t *r = rec + (size_t)x * rw;
+        if (bwd)
+            for (uint32_t w = 0; w < H; ++w) {
+                const uint64_t v = r[w];
+                if (v) atomicOr(&acc[w], (unsigned long long)v);
+            }
+        if (fwd)
+            for (uint32_t w = H; w < rw; ++w) {
+                const uint64_t v = r[w];
+                if (v) atomicOr(&acc[w], (unsigned long long)v);
+            }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 2 * H; i += blockDim.x)
+        if (acc[i]) atomicOr(&L[i], acc[i]);
+}
+
+__global__ void reach_init_kernel(const uint32_t *__restrict__ vf, const uint32_t *__restrict__ vb,
+                                  uint64_t *__restrict__ rec, uint32_t n, uint32_t H,
+                                  const unsigned long long *__restrict__ L, const unsigned int *incomplete) {
+    if (*incomplete) return;
+    const uint32_t rw = 2 * H;
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+        uint64_t *r = rec + (size_t)x * rw;
+        if ((vf[x >> 5] >> (x & 31)) & 1u)
+            for (uint32_t w = 0; w < H; ++w) r[w] |= L[w];
+        if ((vb[x >> 5] >> (x & 31)) & 1u)
+            for (uint32_t w = H; w < rw; ++w) r[w] |= L[w];
+    }
+}
+
+static bool pivot_on() {
+    static const bool off = std::getenv("DBL_NO_PIVOT") != nullptr;
+    return !off;
+}
+
+// Head start from the pivot's reachability (all record words; after prep).
+static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx) {
+    const uint32_t n = g->n, H = idx->wdl + idx->wbl;
+    const size_t bmw = ((size_t)n + 31) / 32;
+    const size_t bbytes = ((bmw * 4 + 255) / 256) * 256;
+    dbl_status s;
+    if ((s = g->reach.ensure(2 * bbytes + 2 * MAX_SHARD_WORDS * 8 + 64))) return s;
+    uint32_t *vf = g->reach.as<uint32_t>();
+    uint32_t *vb = reinterpret_cast<uint32_t *>(g->reach.as<char>() + bbytes);
+    unsigned long long *L = reinterpret_cast<unsigned long long *>(g->reach.as<char>() + 2 * bbytes);
+    unsigned int *chg = reinterpret_cast<unsigned int *>(L + 2 * MAX_SHARD_WORDS);
+    DBL_CUDA(cudaMemsetAsync(g->reach.p, 0, 2 * bbytes + 2 * MAX_SHARD_WORDS * 8 + 64, g->stream));
+    ReachParams R{};
+    R.adj[0] = graph_rev(g);
+    R.adj[1] = graph_fwd(g);
+    R.top[0] = graph_fwd(g);
+    R.top[1] = graph_rev(g);
+    R.vis[0] = vf;
+    R.vis[1] = vb;
+    R.changed = chg;
+    R.lm = idx->landmarks.as<uint32_t>();
+    R.n = n;
+    R.nwords = (uint32_t)bmw;
+    R.max_sweeps = 64;
+    static int bps = -1;
+    if (bps < 0) {
+        DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, reach_kernel, 256, 0));
+        if (bps < 1) bps = 1;
+    }
+    void *args[] = {(void *)&R};
+    DBL_CUDA(cudaLaunchCooperativeKernel((const void *)reach_kernel, dim3(g->sm_count * bps), dim3(256), args, 0,
+                                         g->stream));
+    DBL_LAUNCHED();
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > g->sm_count * 8) blocks = g->sm_count * 8;
+    reach_union_kernel<<<blocks, 256, 0, g->stream>>>(vf, vb, idx->rec.as<uint64_t>(), n, H, L, chg + 3);
+    DBL_CHECK_LAUNCH("reach_union_kernel");
+    reach_init_kernel<<<blocks, 256, 0, g->stream>>>(vf, vb, idx->rec.as<uint64_t>(), n, H, L, chg + 3);
+    DBL_CHECK_LAUNCH("reach_init_kernel");
+    if (std::getenv("DBL_TRACE")) {
+        unsigned int hc[5];
+        DBL_CUDA(cudaMemcpyAsync(hc, chg, sizeof(hc), cudaMemcpyDeviceToHost, g->stream));
+        DBL_CUDA(cudaStreamSynchronize(g->stream));
+        std::fprintf(stderr, "[dbl] pivot reach: %u sweeps%s\n", hc[4], hc[3] ? " (cap hit: no head start)" : "");
+    }
+    return DBL_OK;
+}
+
 // Build (or rebuild) the listed record words (nullptr = all) from seeds.
 // A full build seeds through the fused prep pass (select.cu: metadata still
 // to be selected, seeds, level-0 frontier of the first word group, device
@@ -867,6 +1075,10 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
         if ((s = index_seed_records(g, idx, wmask))) return s;
     }
     trace("build: seed", g->stream);
+    if (prep && idx->cfg.k && pivot_on()) {
+        if ((s = pivot_head_start(g, idx))) return s;
+        trace("build: pivot head start", g->stream);
+    }
     PrepState hp{};
     for (int pi = 0; pi < np; ++pi) {
         const Group *pair[2] = {pairs[pi][0], pairs[pi][1]};

@@ -175,6 +175,7 @@ struct dbl_graph {
     dbl::DevBuf qbuf[2][2];   // [direction][0] work-item queue storage
     uint32_t qcap = 0;
     dbl::DevBuf ctrl;
+    dbl::DevBuf reach;        // pivot reachability: n x {from pivot, to pivot} u64 + 2 bitmaps + unions
     dbl::DevBuf changed_bits;
     // generic scratch
     dbl::DevBuf cub_tmp, scratch_a, scratch_b, scratch_c, scratch_d;

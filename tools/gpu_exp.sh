@@ -1,5 +1,5 @@
 set -x
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-DBL_BATCHES=5 timeout 300 python tools/insert_case.py 2>&1 | grep batch
-DBL_SCALE=22 DBL_BATCHES=5 timeout 300 python tools/insert_case.py 2>&1 | grep batch
 timeout 300 python tools/qbench.py 2>&1 | tail -1
+DBL_NO_PIVOT=1 timeout 300 python tools/qbench.py 2>&1 | tail -1
+DBL_TRACE=1 timeout 300 python tools/qbench.py --reps 3 2>&1 | grep "level\|build:" | tail -24
