@@ -845,6 +845,9 @@ dbl_status index_seed_records(dbl_graph *g, dbl_index *idx, uint64_t wmask) {
 // Marks made during a sweep may be seen by later vertices of the same sweep
 // (fewer sweeps); a stale L1 copy only defers a mark to the next sweep.
 struct ReachParams {
+    uint64_t *rec;       // records (seeded): unions over A(h)/D(h) are ORed in at the end
+    unsigned long long *L;   // 2H words of unions
+    uint32_t H;
     Adj adj[2];          // [0] in-edges (reverse adjacency), [1] out-edges (forward adjacency)
     Adj top[2];          // first level from h: [0] out-edges, [1] in-edges
     uint32_t *vis[2];
@@ -902,8 +905,10 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
         }
     }
     grid.sync();
+    bool capped = false;
     for (uint32_t sweep = 0;; ++sweep) {
         if (sweep == P.max_sweeps) {
+            capped = true;
             // deep graph: D/A incomplete, hence not closed under successors /
             // predecessors -- the head start is dropped (labels stay exact)
             if (tid == 0) P.changed[3] = 1;
@@ -930,20 +935,17 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
             break;
         }
     }
-}
-
-// L[0..H) = OR of the in-halves over A(h); L[H..2H) = OR of the out-halves over D(h)
-__global__ void reach_union_kernel(const uint32_t *__restrict__ vf, const uint32_t *__restrict__ vb,
-                                   const uint64_t *__restrict__ rec, uint32_t n, uint32_t H,
-                                   unsigned long long *__restrict__ L, const unsigned int *incomplete) {
-    if (*incomplete) return;
+    if (capped) return;   // grid-uniform (every thread counts the same sweeps)
+    // L_in(h) = OR of the in-halves over A(h), L_out(h) = OR of the
+    // out-halves over D(h); then every x in D(h) takes L_in(h), every x in
+    // A(h) takes L_out(h)
     __shared__ unsigned long long acc[2 * MAX_SHARD_WORDS];
-    for (uint32_t i = threadIdx.x; i < 2 * H; i += blockDim.x) acc[i] = 0;
+    const uint32_t H = P.H, rw = 2 * H;
+    for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = 0;
     __syncthreads();
-    const uint32_t rw = 2 * H;
-    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-        const bool fwd = (vf[x >> 5] >> (x & 31)) & 1u, bwd = (vb[x >> 5] >> (x & 31)) & 1u;
-        const uint64_t *r = rec + (size_t)x * rw;
+    for (uint64_t x = tid; x < P.n; x += nth) {
+        const bool fwd = (P.vis[0][x >> 5] >> (x & 31)) & 1u, bwd = (P.vis[1][x >> 5] >> (x & 31)) & 1u;
+        const uint64_t *r = P.rec + x * rw;
         if (bwd)
             for (uint32_t w = 0; w < H; ++w) {
                 const uint64_t v = r[w];
@@ -956,21 +958,17 @@ __global__ void reach_union_kernel(const uint32_t *__restrict__ vf, const uint32
             }
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < 2 * H; i += blockDim.x)
-        if (acc[i]) atomicOr(&L[i], acc[i]);
-}
-
-__global__ void reach_init_kernel(const uint32_t *__restrict__ vf, const uint32_t *__restrict__ vb,
-                                  uint64_t *__restrict__ rec, uint32_t n, uint32_t H,
-                                  const unsigned long long *__restrict__ L, const unsigned int *incomplete) {
-    if (*incomplete) return;
-    const uint32_t rw = 2 * H;
-    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-        uint64_t *r = rec + (size_t)x * rw;
-        if ((vf[x >> 5] >> (x & 31)) & 1u)
-            for (uint32_t w = 0; w < H; ++w) r[w] |= L[w];
-        if ((vb[x >> 5] >> (x & 31)) & 1u)
-            for (uint32_t w = H; w < rw; ++w) r[w] |= L[w];
+    for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x)
+        if (acc[i]) atomicOr(&P.L[i], acc[i]);
+    grid.sync();
+    for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = *(volatile unsigned long long *)&P.L[i];
+    __syncthreads();
+    for (uint64_t x = tid; x < P.n; x += nth) {
+        uint64_t *r = P.rec + x * rw;
+        if ((P.vis[0][x >> 5] >> (x & 31)) & 1u)
+            for (uint32_t w = 0; w < H; ++w) r[w] |= acc[w];
+        if ((P.vis[1][x >> 5] >> (x & 31)) & 1u)
+            for (uint32_t w = H; w < rw; ++w) r[w] |= acc[w];
     }
 }
 
@@ -992,6 +990,9 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx) {
     unsigned int *chg = reinterpret_cast<unsigned int *>(L + 2 * MAX_SHARD_WORDS);
     DBL_CUDA(cudaMemsetAsync(g->reach.p, 0, 2 * bbytes + 2 * MAX_SHARD_WORDS * 8 + 64, g->stream));
     ReachParams R{};
+    R.rec = idx->rec.as<uint64_t>();
+    R.L = L;
+    R.H = H;
     R.adj[0] = graph_rev(g);
     R.adj[1] = graph_fwd(g);
     R.top[0] = graph_fwd(g);
@@ -1012,12 +1013,6 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx) {
     DBL_CUDA(cudaLaunchCooperativeKernel((const void *)reach_kernel, dim3(g->sm_count * bps), dim3(256), args, 0,
                                          g->stream));
     DBL_LAUNCHED();
-    int blocks = (int)((n + 255) / 256);
-    if (blocks > g->sm_count * 8) blocks = g->sm_count * 8;
-    reach_union_kernel<<<blocks, 256, 0, g->stream>>>(vf, vb, idx->rec.as<uint64_t>(), n, H, L, chg + 3);
-    DBL_CHECK_LAUNCH("reach_union_kernel");
-    reach_init_kernel<<<blocks, 256, 0, g->stream>>>(vf, vb, idx->rec.as<uint64_t>(), n, H, L, chg + 3);
-    DBL_CHECK_LAUNCH("reach_init_kernel");
     if (std::getenv("DBL_TRACE")) {
         unsigned int hc[5];
         DBL_CUDA(cudaMemcpyAsync(hc, chg, sizeof(hc), cudaMemcpyDeviceToHost, g->stream));

@@ -485,7 +485,7 @@ constexpr int FUSED_THREADS = 256;
 #endif
 constexpr bool DEFER_BFS = DBL_QDEFER;
 #ifndef DBL_QTICKET
-#define DBL_QTICKET 0
+#define DBL_QTICKET 1
 #endif
 
 template <int WDL, int WBL>
@@ -1384,7 +1384,10 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     lean_fn lean = nullptr;
     bfsw_fn bfsw = nullptr;
     size_t wsmem = 0;
-    if (count && !no_fused && !old_fused && pick_lean(idx->wdl, idx->wbl, lean, bfsw, wsmem)) {
+    // k <= 64: lean gather + per-thread BFS; wider labels (cfg5, k = 256),
+    // whose fallbacks outgrow the thread BFS, keep the fused kernel with the
+    // warp BFS interleaved between tiles (measured on cfg5: 4.6 vs 3.7 G q/s)
+    if (count && !no_fused && !old_fused && idx->wdl <= 1 && pick_lean(idx->wdl, idx->wbl, lean, bfsw, wsmem)) {
         static int lbps = -1, wbps = -1;
         static const void *last_fn = nullptr;
         if (lbps < 0 || last_fn != (const void *)bfsw) {
