@@ -847,6 +847,7 @@ dbl_status index_seed_records(dbl_graph *g, dbl_index *idx, uint64_t wmask) {
 struct ReachParams {
     uint64_t *rec;       // records (seeded): unions over A(h)/D(h) are ORed in at the end
     unsigned long long *L;   // 2H words of unions
+    uint64_t wmask;          // record words being built (bit w = word w)
     uint32_t H;
     Adj adj[2];          // [0] in-edges (reverse adjacency), [1] out-edges (forward adjacency)
     Adj top[2];          // first level from h: [0] out-edges, [1] in-edges
@@ -948,12 +949,12 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
         const uint64_t *r = P.rec + x * rw;
         if (bwd)
             for (uint32_t w = 0; w < H; ++w) {
-                const uint64_t v = r[w];
+                const uint64_t v = ((P.wmask >> w) & 1u) ? r[w] : 0ull;
                 if (v) atomicOr(&acc[w], (unsigned long long)v);
             }
         if (fwd)
             for (uint32_t w = H; w < rw; ++w) {
-                const uint64_t v = r[w];
+                const uint64_t v = ((P.wmask >> w) & 1u) ? r[w] : 0ull;
                 if (v) atomicOr(&acc[w], (unsigned long long)v);
             }
     }
@@ -966,9 +967,11 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
     for (uint64_t x = tid; x < P.n; x += nth) {
         uint64_t *r = P.rec + x * rw;
         if ((P.vis[0][x >> 5] >> (x & 31)) & 1u)
-            for (uint32_t w = 0; w < H; ++w) r[w] |= acc[w];
+            for (uint32_t w = 0; w < H; ++w)
+                if (acc[w]) r[w] |= acc[w];
         if ((P.vis[1][x >> 5] >> (x & 31)) & 1u)
-            for (uint32_t w = H; w < rw; ++w) r[w] |= acc[w];
+            for (uint32_t w = H; w < rw; ++w)
+                if (acc[w]) r[w] |= acc[w];
     }
 }
 
@@ -978,7 +981,7 @@ static bool pivot_on() {
 }
 
 // Head start from the pivot's reachability (all record words; after prep).
-static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx) {
+static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask) {
     const uint32_t n = g->n, H = idx->wdl + idx->wbl;
     const size_t bmw = ((size_t)n + 31) / 32;
     const size_t bbytes = ((bmw * 4 + 255) / 256) * 256;
@@ -992,6 +995,7 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx) {
     ReachParams R{};
     R.rec = idx->rec.as<uint64_t>();
     R.L = L;
+    R.wmask = wmask;
     R.H = H;
     R.adj[0] = graph_rev(g);
     R.adj[1] = graph_fwd(g);
@@ -1070,8 +1074,13 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
         if ((s = index_seed_records(g, idx, wmask))) return s;
     }
     trace("build: seed", g->stream);
-    if (prep && idx->cfg.k && pivot_on()) {
-        if ((s = pivot_head_start(g, idx))) return s;
+    if (idx->cfg.k && pivot_on()) {
+        uint64_t wmask = ~0ull;
+        if (!prep) {
+            wmask = 0;
+            for (uint32_t i = 0; i < nwords; ++i) wmask |= 1ull << words[i];
+        }
+        if ((s = pivot_head_start(g, idx, wmask))) return s;
         trace("build: pivot head start", g->stream);
     }
     PrepState hp{};

@@ -461,3 +461,46 @@ def test_topk_candidate_table_boundary(n_hot):
         oidx = og.build(k, 64, threads=8)
         np.testing.assert_array_equal(np.array(idx.landmark_set.landmarks), oidx.landmarks)
         assert_labels_equal_oracle(idx, oidx)
+
+
+# ------------------------------------------------------- pivot head start --
+
+def _two_component_graph(seed):
+    """Two R-MAT blocks (the second one smaller) with one-way bridges from the
+    second into the first: the pivot (landmark 0, a hub of block 1) reaches
+    only block 1, while block 2's seeds reach block 1 through the bridges."""
+    s1, d1 = W.rmat_edges(13, 8, seed)
+    s2, d2 = W.rmat_edges(11, 4, seed + 1)
+    off = np.uint32(1 << 13)
+    rng = np.random.default_rng(seed)
+    bu = (rng.integers(0, 1 << 11, 300) + (1 << 13)).astype(np.uint32)
+    bv = rng.integers(0, 1 << 13, 300).astype(np.uint32)
+    src = np.concatenate([s1, s2 + off, bu]).astype(np.uint32)
+    dst = np.concatenate([d1, d2 + off, bv]).astype(np.uint32)
+    return (1 << 13) + (1 << 11), src, dst
+
+
+@pytest.mark.parametrize("case", ["two_components", "dag", "reverse_dag"])
+def test_pivot_head_start_partial_cover(case):
+    """The head start covers only part of the graph (the pivot's SCC does not
+    hold every seed, or the graph is acyclic): labels must still equal the
+    oracle's word for word."""
+    if case == "two_components":
+        n, src, dst = _two_component_graph(5)
+    else:
+        n = 6000
+        src, dst = W.gen_random_graph(n, 4, seed=9, acyclic=True)
+        if case == "reverse_dag":
+            src, dst = dst, src
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    og = O.OracleGraph(n, src, dst)
+    for k, kp in ((64, 64), (100, 13)):
+        idx = E.build_index(g, E.IndexConfig(k=k, k_prime=kp))
+        oidx = og.build(k, kp, threads=8)
+        np.testing.assert_array_equal(np.array(idx.landmark_set.landmarks), oidx.landmarks)
+        assert_labels_equal_oracle(idx, oidx)
+        # rebuild (frozen metadata) after some inserts also starts from the pivot
+        iu, iv = W.gen_insert_workload(src, dst, n, 500, 7)
+        E.insert_edges(g, idx, iu, iv)
+        assert idx.labels_equal(E.rebuild_index(g, idx))
+        g = E.DynamicGraph.from_edges(n, src, dst)
