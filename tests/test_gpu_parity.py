@@ -504,3 +504,27 @@ def test_pivot_head_start_partial_cover(case):
         E.insert_edges(g, idx, iu, iv)
         assert idx.labels_equal(E.rebuild_index(g, idx))
         g = E.DynamicGraph.from_edges(n, src, dst)
+
+
+@pytest.mark.parametrize("count", [1, 255, 256, 1000, 100_003])
+def test_zero_copy_host_queries_match_device(count):
+    """Pinned host buffers take the zero-copy path (pairs staged per CTA with
+    16-byte loads over PCIe); codes and visited counts must equal the
+    device-resident batch for ragged sizes."""
+    import torch
+    from paper_2101_09441_b200 import _native as N
+    n, src, dst = rmat_case(14, 8, 21)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    idx = E.build_index(g)
+    qu, qv = W.uniform_queries(n, count, 5)
+    du = torch.from_numpy(qu.view(np.int32)).cuda()
+    dv = torch.from_numpy(qv.view(np.int32)).cuda()
+    dc, dvis = E.query_codes(g, idx, du, dv)
+    hu = torch.from_numpy(qu.view(np.int32)).pin_memory()
+    hv = torch.from_numpy(qv.view(np.int32)).pin_memory()
+    hc = torch.empty(count, dtype=torch.uint8).pin_memory()
+    hvis = torch.empty(count, dtype=torch.int32).pin_memory()
+    N.call("dbl_query", idx.handle, g.handle, N.ptr(hu), N.ptr(hv), count, E.DEFAULT_FLAGS.bits(), N.ptr(hc),
+           N.ptr(hvis), N.MEM_HOST)
+    np.testing.assert_array_equal(hc.numpy(), dc.cpu().numpy())
+    np.testing.assert_array_equal(hvis.numpy(), dvis.cpu().numpy())
