@@ -795,9 +795,21 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
     return DBL_OK;
 }
 
-static dbl_status finish_run(dbl_graph *g, Ctrl *hctrl) {
-    DBL_CUDA(cudaMemcpyAsync(hctrl, g->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, g->stream));
+// Read the run's control block (and, for the first run of a build, the prep
+// state) through pinned staging with ONE stream synchronisation; the ev[1]
+// timestamp of the run is recorded before it.
+static dbl_status finish_run(dbl_graph *g, Ctrl *hctrl, PrepState *hprep = nullptr) {
+    dbl_status s = g->host_stage.ensure(sizeof(Ctrl) + sizeof(PrepState) + 64);
+    if (s) return s;
+    Ctrl *pc = reinterpret_cast<Ctrl *>(g->host_stage.p);
+    PrepState *pp = reinterpret_cast<PrepState *>(reinterpret_cast<char *>(g->host_stage.p) +
+                                                  ((sizeof(Ctrl) + 15) & ~size_t(15)));
+    DBL_CUDA(cudaMemcpyAsync(pc, g->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, g->stream));
+    if (hprep) DBL_CUDA(cudaMemcpyAsync(pp, g->prep.p, sizeof(PrepState), cudaMemcpyDeviceToHost, g->stream));
+    DBL_CUDA(cudaEventRecord(g->ev[1], g->stream));
     DBL_CUDA(cudaStreamSynchronize(g->stream));
+    *hctrl = *pc;
+    if (hprep) *hprep = *pp;
     if (hctrl->overflow) { set_error("frontier queue overflow"); return DBL_E_CUDA; }
     return DBL_OK;
 }
@@ -848,6 +860,7 @@ struct ReachParams {
     uint64_t *rec;       // records (seeded): unions over A(h)/D(h) are ORed in at the end
     unsigned long long *L;   // 2H words of unions
     uint64_t wmask;          // record words being built (bit w = word w)
+    uint32_t *front[2];      // level-0 frontier bitmaps of the label fixpoint (or nullptr)
     uint32_t H;
     Adj adj[2];          // [0] in-edges (reverse adjacency), [1] out-edges (forward adjacency)
     Adj top[2];          // first level from h: [0] out-edges, [1] in-edges
@@ -964,6 +977,16 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
     grid.sync();
     for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = *(volatile unsigned long long *)&P.L[i];
     __syncthreads();
+    // a vertex of h's SCC (in D(h) and A(h)) now holds L_in(h) / L_out(h),
+    // which every successor / predecessor also holds: it leaves the level-0
+    // frontier (on R-MAT that drops the landmarks, the hubs of that frontier)
+    for (uint64_t w = tid; w < P.nwords; w += nth) {
+        const uint32_t scc = P.vis[0][w] & P.vis[1][w];
+        if (scc) {
+            if (P.front[0]) P.front[0][w] &= ~scc;
+            if (P.front[1]) P.front[1][w] &= ~scc;
+        }
+    }
     for (uint64_t x = tid; x < P.n; x += nth) {
         uint64_t *r = P.rec + x * rw;
         if ((P.vis[0][x >> 5] >> (x & 31)) & 1u)
@@ -981,7 +1004,8 @@ static bool pivot_on() {
 }
 
 // Head start from the pivot's reachability (all record words; after prep).
-static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask) {
+static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask, uint32_t *front0,
+                                   uint32_t *front1) {
     const uint32_t n = g->n, H = idx->wdl + idx->wbl;
     const size_t bmw = ((size_t)n + 31) / 32;
     const size_t bbytes = ((bmw * 4 + 255) / 256) * 256;
@@ -996,6 +1020,8 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask)
     R.rec = idx->rec.as<uint64_t>();
     R.L = L;
     R.wmask = wmask;
+    R.front[0] = front0;
+    R.front[1] = front1;
     R.H = H;
     R.adj[0] = graph_rev(g);
     R.adj[1] = graph_fwd(g);
@@ -1080,7 +1106,14 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
             wmask = 0;
             for (uint32_t i = 0; i < nwords; ++i) wmask |= 1ull << words[i];
         }
-        if ((s = pivot_head_start(g, idx, wmask))) return s;
+        // prep wrote the first word group's level-0 bitmaps (all words are
+        // covered by the head start then): prune h's SCC from them
+        uint32_t *f0 = nullptr, *f1 = nullptr;
+        if (prep) {
+            f0 = pairs[0][0] ? g->stamp[0].as<uint32_t>() : nullptr;
+            f1 = pairs[0][1] ? g->stamp[1].as<uint32_t>() : nullptr;
+        }
+        if ((s = pivot_head_start(g, idx, wmask, f0, f1))) return s;
         trace("build: pivot head start", g->stream);
     }
     PrepState hp{};
@@ -1094,9 +1127,8 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
         if (fresh && (s = launch_init_frontier(g, idx, pair))) return s;
         trace("build: init frontier", g->stream);
         if ((s = launch_fixpoint<false>(g, P, nw, vec))) return s;
-        if (prep && pi == 0 && (s = prep_fetch(g, &hp))) return s;
         Ctrl h{};
-        if ((s = finish_run(g, &h))) return s;
+        if ((s = finish_run(g, &h, prep && pi == 0 ? &hp : nullptr))) return s;
         trace("build: fixpoint", g->stream);
         if (prep && pi == 0) {
             if (hp.err) { set_error("bucket override outside [0, k_prime)"); return DBL_E_CONFIG; }
@@ -1122,8 +1154,7 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
                              (h.level_t[2 * l + 2] - h.level_t[2 * l + 1]) / 1e3);
         }
     }
-    DBL_CUDA(cudaEventRecord(g->ev[1], g->stream));
-    DBL_CUDA(cudaEventSynchronize(g->ev[1]));
+    // ev[1] was recorded (and reached) by the last finish_run
     cudaEventElapsedTime(&g->t_fix, g->ev[0], g->ev[1]);
     return DBL_OK;
 }
