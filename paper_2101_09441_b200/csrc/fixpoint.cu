@@ -860,6 +860,7 @@ struct ReachParams {
     uint64_t *rec;       // records (seeded): unions over A(h)/D(h) are ORed in at the end
     unsigned long long *L;   // 2H words of unions
     uint64_t wmask;          // record words being built (bit w = word w)
+    uint64_t cap_wmask;      // words whose level-0 frontier is `front` (used when the sweeps are capped)
     uint32_t *front[2];      // level-0 frontier bitmaps of the label fixpoint (or nullptr)
     uint32_t H;
     Adj adj[2];          // [0] in-edges (reverse adjacency), [1] out-edges (forward adjacency)
@@ -922,9 +923,12 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
     bool capped = false;
     for (uint32_t sweep = 0;; ++sweep) {
         if (sweep == P.max_sweeps) {
+            // deep graph: the marked sets are only parts of D(h) / A(h), not
+            // closed under successors / predecessors.  The head start is
+            // still a subset of every marked vertex's final label, so it is
+            // kept when the marked vertices can join the level-0 frontier
+            // (they then propagate it), and dropped otherwise.
             capped = true;
-            // deep graph: D/A incomplete, hence not closed under successors /
-            // predecessors -- the head start is dropped (labels stay exact)
             if (tid == 0) P.changed[3] = 1;
             break;
         }
@@ -949,12 +953,13 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
             break;
         }
     }
-    if (capped) return;   // grid-uniform (every thread counts the same sweeps)
+    if (capped && !(P.front[0] && P.front[1])) return;   // grid-uniform
     // L_in(h) = OR of the in-halves over A(h), L_out(h) = OR of the
     // out-halves over D(h); then every x in D(h) takes L_in(h), every x in
     // A(h) takes L_out(h)
     __shared__ unsigned long long acc[2 * MAX_SHARD_WORDS];
     const uint32_t H = P.H, rw = 2 * H;
+    const uint64_t wm = capped ? P.cap_wmask : P.wmask;
     for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = 0;
     __syncthreads();
     for (uint64_t x = tid; x < P.n; x += nth) {
@@ -962,12 +967,12 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
         const uint64_t *r = P.rec + x * rw;
         if (bwd)
             for (uint32_t w = 0; w < H; ++w) {
-                const uint64_t v = ((P.wmask >> w) & 1u) ? r[w] : 0ull;
+                const uint64_t v = ((wm >> w) & 1u) ? r[w] : 0ull;
                 if (v) atomicOr(&acc[w], (unsigned long long)v);
             }
         if (fwd)
             for (uint32_t w = H; w < rw; ++w) {
-                const uint64_t v = ((P.wmask >> w) & 1u) ? r[w] : 0ull;
+                const uint64_t v = ((wm >> w) & 1u) ? r[w] : 0ull;
                 if (v) atomicOr(&acc[w], (unsigned long long)v);
             }
     }
@@ -981,6 +986,11 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
     // which every successor / predecessor also holds: it leaves the level-0
     // frontier (on R-MAT that drops the landmarks, the hubs of that frontier)
     for (uint64_t w = tid; w < P.nwords; w += nth) {
+        if (capped) {   // partial sets: every marked vertex propagates its head start
+            P.front[0][w] |= P.vis[0][w];
+            P.front[1][w] |= P.vis[1][w];
+            continue;
+        }
         const uint32_t scc = P.vis[0][w] & P.vis[1][w];
         if (scc) {
             if (P.front[0]) P.front[0][w] &= ~scc;
@@ -1005,7 +1015,7 @@ static bool pivot_on() {
 
 // Head start from the pivot's reachability (all record words; after prep).
 static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask, uint32_t *front0,
-                                   uint32_t *front1) {
+                                   uint32_t *front1, uint64_t cap_wmask) {
     const uint32_t n = g->n, H = idx->wdl + idx->wbl;
     const size_t bmw = ((size_t)n + 31) / 32;
     const size_t bbytes = ((bmw * 4 + 255) / 256) * 256;
@@ -1020,6 +1030,7 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     R.rec = idx->rec.as<uint64_t>();
     R.L = L;
     R.wmask = wmask;
+    R.cap_wmask = cap_wmask;
     R.front[0] = front0;
     R.front[1] = front1;
     R.H = H;
@@ -1033,7 +1044,10 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     R.lm = idx->landmarks.as<uint32_t>();
     R.n = n;
     R.nwords = (uint32_t)bmw;
-    R.max_sweeps = 64;
+    // bottom-up sweeps cost O(n) each: shallow graphs (R-MAT, d >= 4) finish
+    // in ~5; deep sparse ones stop here and hand the partial sets to the
+    // label fixpoint's frontier
+    R.max_sweeps = 12;
     static int bps = -1;
     if (bps < 0) {
         DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, reach_kernel, 256, 0));
@@ -1109,11 +1123,17 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
         // prep wrote the first word group's level-0 bitmaps (all words are
         // covered by the head start then): prune h's SCC from them
         uint32_t *f0 = nullptr, *f1 = nullptr;
+        uint64_t cap_wmask = 0;
         if (prep) {
             f0 = pairs[0][0] ? g->stamp[0].as<uint32_t>() : nullptr;
             f1 = pairs[0][1] ? g->stamp[1].as<uint32_t>() : nullptr;
+            for (int d = 0; d < 2; ++d)
+                if (pairs[0][d])
+                    for (uint32_t w = pairs[0][d]->w0; w < pairs[0][d]->w0 + pairs[0][d]->nw; ++w) cap_wmask |= 1ull << w;
         }
-        if ((s = pivot_head_start(g, idx, wmask, f0, f1))) return s;
+        if ((s = pivot_head_start(g, idx, wmask, f0, f1, cap_wmask))) return s;
+        // (the capped case needs both bitmaps; with a one-direction first
+        // group the kernel drops the head start instead)
         trace("build: pivot head start", g->stream);
     }
     PrepState hp{};

@@ -1002,6 +1002,9 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
 // dl_out[u] & dl_in[v] != 0 or violate BL containment), so v is found iff
 // it is reachable, in any visiting order.
 constexpr int TB_Q = 8;
+#ifndef DBL_WBFS
+#define DBL_WBFS 1
+#endif
 constexpr uint32_t DQ_CAP = 128;   // deferred queries per CTA (more go to the warp BFS)
 // A deferred query: its index, endpoints and the words its pruning needs
 // (dl_out[u], bl_in[v], bl_out[v]; queries.py:137-140).
@@ -1083,6 +1086,66 @@ __device__ __forceinline__ int thread_bfs(const uint64_t *__restrict__ rec, cons
                     if (qn == TB_Q) return 2;
                     q[qn++] = x[t];
                 }
+            }
+        }
+    }
+    return 0;
+}
+
+// The same bounded pruned BFS with the 32 lanes of a warp on one query: a
+// frontier vertex's adjacency is read 32 neighbours at a time and their
+// pruning words are gathered in parallel, so a level costs about two memory
+// round trips instead of one per 4 neighbours.  The expanded/visited list
+// (<= TB_Q) lives in the warp's slot of `wq`.  Warp-uniform result as in
+// thread_bfs; TB_EW bounds the neighbours of one expanded vertex.
+constexpr uint32_t TB_EW = 256;
+
+template <int WDL, int WBL>
+__device__ __forceinline__ int warp_query_bfs(const uint64_t *__restrict__ rec, const Adj &adj, uint32_t u, uint32_t v,
+                                              const uint64_t *dlo_u, const uint64_t *bli_v, const uint64_t *blo_v,
+                                              bool prune_dl, bool prune_bl, uint32_t *wq, uint32_t *vcount) {
+    constexpr int H = WDL + WBL, RW = 2 * H;
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) wq[0] = u;
+    __syncwarp();
+    uint32_t qn = 1;
+    for (uint32_t head = 0; head < qn; ++head) {
+        const uint32_t w = wq[head];
+        *vcount = head + 1;
+        for (int seg = 0; seg < 2; ++seg) {
+            const uint32_t *ptr = seg ? adj.dptr : adj.ptr;
+            if (!ptr) break;
+            const uint32_t *col = seg ? adj.dcol : adj.col;
+            const uint32_t s0 = __ldg(ptr + w), s1 = __ldg(ptr + w + 1);
+            if (s1 - s0 > TB_EW) return 2;
+            for (uint32_t j0 = s0; j0 < s1; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const bool ok = j < s1;
+                const uint32_t x = ok ? __ldg(col + j) : 0xffffffffu;
+                if (__any_sync(FULL, ok && x == v)) return 1;   // target test precedes the visited test
+                bool keep = ok;
+                for (uint32_t k = 0; k < qn; ++k) keep &= wq[k] != x;
+                if (keep && (prune_dl || prune_bl)) {
+                    const uint64_t *rx = rec + (size_t)x * RW;
+                    bool p = false;
+                    if (prune_dl) {   // queries.py:137-138
+#pragma unroll
+                        for (int k = 0; k < WDL; ++k) p |= (dlo_u[k] & __ldg(rx + k)) != 0;
+                    }
+                    if (prune_bl && !p) {   // queries.py:139-140
+#pragma unroll
+                        for (int k = 0; k < WBL; ++k)
+                            p |= ((__ldg(rx + WDL + k) & ~bli_v[k]) | (blo_v[k] & ~__ldg(rx + H + WDL + k))) != 0;
+                    }
+                    keep = !p;
+                }
+                const unsigned m = __ballot_sync(FULL, keep);
+                if (!m) continue;
+                if (qn + __popc(m) > TB_Q) return 2;
+                __syncwarp();
+                if (keep) wq[qn + __popc(m & ((1u << lane) - 1u))] = x;
+                __syncwarp();
+                qn += __popc(m);
             }
         }
     }
@@ -1183,6 +1246,26 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
     if constexpr (TBFS) {
         __syncthreads();
         const uint32_t nq = min(dq.n, DQ_CAP);
+#if DBL_WBFS
+        // one warp per queued query, neighbours in parallel
+        __shared__ uint32_t wq[256 / 32][TB_Q];
+        const int wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+        for (uint32_t t = wid; t < nq; t += nwb) {
+            const uint32_t i = dq.i[t];
+            uint32_t vc = 0;
+            const int r = warp_query_bfs<WDL, WBL>(rec, adj, dq.u[t], dq.v[t], dq.dlo[t], dq.bli[t], dq.blo[t],
+                                                   prune_dl, prune_bl, wq[wid], &vc);
+            if (lane == 0) {
+                if (r == 2) {
+                    pending[atomicAdd(&counters[CNT_PENDING], 1u)] = i;
+                } else {
+                    qd.codes[i] = r ? DBL_BFS_POSITIVE : DBL_BFS_NEGATIVE;
+                    if (qd.visited) qd.visited[i] = vc;
+                }
+            }
+            __syncwarp();
+        }
+#else
         for (uint32_t t = threadIdx.x; t < nq; t += blockDim.x) {
             const uint32_t i = dq.i[t];
             uint32_t vc = 0;
@@ -1195,6 +1278,7 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
                 if (qd.visited) qd.visited[i] = vc;
             }
         }
+#endif
     }
     // the last CTA out closes the batch, or tail-launches the warp BFS for the
     // queries the thread BFS could not finish

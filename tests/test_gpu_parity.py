@@ -528,3 +528,28 @@ def test_zero_copy_host_queries_match_device(count):
            N.ptr(hvis), N.MEM_HOST)
     np.testing.assert_array_equal(hc.numpy(), dc.cpu().numpy())
     np.testing.assert_array_equal(hvis.numpy(), dvis.cpu().numpy())
+
+
+@pytest.mark.parametrize("k,kp", [(64, 64), (640, 96)])
+def test_pivot_capped_sweeps_deep_graph(k, kp):
+    """A long cycle with sparse chords: the pivot's reachability needs far
+    more bottom-up sweeps than the cap, so the partial sets are handed to the
+    label fixpoint's frontier (with k = 640 the record has several word
+    groups and only the first group's words get the head start)."""
+    n = 12_000
+    rng = np.random.default_rng(3)
+    cyc_s = np.arange(n, dtype=np.uint32)
+    cyc_d = ((cyc_s + 1) % n).astype(np.uint32)
+    ch_s = rng.integers(0, n, 400).astype(np.uint32)
+    ch_d = ((ch_s.astype(np.int64) + rng.integers(2, 50, 400)) % n).astype(np.uint32)
+    tail_s = np.arange(n, n + 2000, dtype=np.uint32)          # a tail of leaves hanging off
+    tail_d = rng.integers(0, n, 2000).astype(np.uint32)
+    src = np.concatenate([cyc_s, ch_s, tail_s, tail_d]).astype(np.uint32)
+    dst = np.concatenate([cyc_d, ch_d, tail_d, tail_s + 2000]).astype(np.uint32)
+    nn = n + 4000
+    g = E.DynamicGraph.from_edges(nn, src, dst)
+    og = O.OracleGraph(nn, src, dst)
+    idx = E.build_index(g, E.IndexConfig(k=k, k_prime=kp))
+    oidx = og.build(k, kp, threads=8)
+    np.testing.assert_array_equal(np.array(idx.landmark_set.landmarks), oidx.landmarks)
+    assert_labels_equal_oracle(idx, oidx)
