@@ -1016,7 +1016,7 @@ struct DeferQ {
     uint32_t n;
 };
 #ifndef DBL_LMINB
-#define DBL_LMINB 4
+#define DBL_LMINB 8
 #endif
 constexpr uint32_t TB_E = 48;
 
