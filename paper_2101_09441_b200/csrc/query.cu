@@ -1165,7 +1165,10 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
     // the per-thread BFS pays off for k <= 64; with wider labels (cfg5:
     // k = 256, d = 16) most fallbacks outgrow its bounds (measured: 79% of
     // cfg5's unresolved queries), so they go straight to the warp BFS
-    constexpr bool TBFS = WDL <= 1;
+#ifndef DBL_TBFS_ALL
+#define DBL_TBFS_ALL 0
+#endif
+    constexpr bool TBFS = DBL_TBFS_ALL || WDL <= 1;
     const uint32_t flags = qd.flags, count = qd.count;
     const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
     const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
@@ -1471,7 +1474,8 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     // k <= 64: lean gather + per-thread BFS; wider labels (cfg5, k = 256),
     // whose fallbacks outgrow the thread BFS, keep the fused kernel with the
     // warp BFS interleaved between tiles (measured on cfg5: 4.6 vs 3.7 G q/s)
-    if (count && !no_fused && !old_fused && idx->wdl <= 1 && pick_lean(idx->wdl, idx->wbl, lean, bfsw, wsmem)) {
+    if (count && !no_fused && !old_fused && (DBL_TBFS_ALL || idx->wdl <= 1) &&
+        pick_lean(idx->wdl, idx->wbl, lean, bfsw, wsmem)) {
         static int lbps = -1, wbps = -1;
         static const void *last_fn = nullptr;
         if (lbps < 0 || last_fn != (const void *)bfsw) {
