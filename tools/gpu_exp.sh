@@ -1,3 +1,5 @@
 set -x
-timeout 900 python tools/run_configs.py --cfg 5 --out gpurun_out/cfg5a.json 2>&1 | grep query_qps | cut -c1-300
-DBL_LIB_PATH=$PWD/paper_2101_09441_b200/_lib/variant_tall.so timeout 900 python tools/run_configs.py --cfg 5 --out gpurun_out/cfg5b.json 2>&1 | grep query_qps | cut -c1-300
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+for so in paper_2101_09441_b200/_lib/libdbl_b200.so paper_2101_09441_b200/_lib/variant_*.so; do
+  echo "== $so"; DBL_LIB_PATH=$PWD/$so timeout 300 python tools/qbench.py 2>&1 | tail -1
+done
