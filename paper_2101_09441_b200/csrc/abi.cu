@@ -745,7 +745,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     DevBuf in, keys, alt, newk, err;
     auto cleanup = [&]() { in.release(); keys.release(); alt.release(); newk.release(); err.release(); };
     if ((s = keys.ensure(count * 8)) || (s = alt.ensure(count * 8)) || (s = newk.ensure(count * 8)) ||
-        (s = err.ensure(8))) { cleanup(); return s; }
+        (s = err.ensure(16))) { cleanup(); return s; }
     const uint32_t *du = u, *dv = v;
     if (mem == DBL_MEM_HOST) {
         if ((s = in.ensure(count * 8))) { cleanup(); return s; }
@@ -794,18 +794,32 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     }
     trace("insert: sort+unique", g->stream);
     if ((s = count_certified_async(g, idx, uniq, count, err.as<unsigned long long>()))) { cleanup(); return s; }
+    // from here to the fixpoint's readback nothing waits on the host: the
+    // number of new edges stays on the device (`count` bounds it) and is read
+    // together with the fixpoint's control block
     uint64_t nnew = 0;
-    if ((s = graph_filter_new(g, uniq, count, newk.as<uint64_t>(), &nnew))) { cleanup(); return s; }
-    st.inserted = nnew;
+    bool cert_read = false;
+    const uint64_t *dnew = nullptr;
+    if ((s = graph_filter_new(g, uniq, count, newk.as<uint64_t>(), &nnew, &dnew))) { cleanup(); return s; }
     trace("insert: certified+filter", g->stream);
-    if (nnew) {
-        if ((s = graph_insert_delta(g, newk.as<uint64_t>(), nnew))) { cleanup(); return s; }
+    if (count) {
+        const uint64_t nd = g->m_delta;
+        // err[1] = number of new edges (read with err[0] = certified)
+        DBL_CUDA(cudaMemcpyAsync(err.as<unsigned long long>() + 1, dnew, 8, cudaMemcpyDeviceToDevice, g->stream));
+        if ((s = graph_insert_delta(g, newk.as<uint64_t>(), count, dnew))) { cleanup(); return s; }
         trace("insert: delta merge", g->stream);
         uint32_t changed[2], seedc[2], levels = 0;
-        if ((s = run_insert(g, idx, newk.as<uint64_t>(), nnew, true, changed, seedc, &levels))) {
+        unsigned long long hx[2] = {0, 0};
+        if ((s = run_insert(g, idx, newk.as<uint64_t>(), count, true, changed, seedc, &levels,
+                            err.as<unsigned long long>(), hx, dnew))) {
             cleanup();
             return s;
         }
+        st.certified = hx[0];
+        nnew = hx[1];
+        cert_read = true;
+        g->m_delta = nd + nnew;   // settle the upper bound used while enqueueing
+        st.inserted = nnew;
         st.labels_changed = (uint64_t)changed[0] + changed[1];
         st.levels = levels;
         if (g->m_delta * 4 > g->m_base + 1024) {
@@ -813,10 +827,12 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
             st.delta_merged = 1;
         }
     }
-    unsigned long long hcert = 0;
-    DBL_CUDA(cudaMemcpyAsync(&hcert, err.p, 8, cudaMemcpyDeviceToHost, g->stream));
-    DBL_CUDA(cudaStreamSynchronize(g->stream));
-    st.certified = hcert;
+    if (!cert_read) {
+        unsigned long long hcert = 0;
+        DBL_CUDA(cudaMemcpyAsync(&hcert, err.p, 8, cudaMemcpyDeviceToHost, g->stream));
+        DBL_CUDA(cudaStreamSynchronize(g->stream));
+        st.certified = hcert;
+    }
     cleanup();
     if (stats) *stats = st;
     return DBL_OK;

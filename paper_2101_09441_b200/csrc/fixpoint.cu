@@ -622,7 +622,9 @@ __global__ void landmark_frontier_kernel(uint32_t *__restrict__ bits0, uint32_t 
 // u->v, in-words(v) |= in-words(u) and out-words(u) |= out-words(v); changed
 // endpoints start the level-0 frontier.
 template <int NW, bool VEC>
-__global__ void insert_seed_kernel(FixParams P, const uint64_t *__restrict__ keys, uint64_t count) {
+__global__ void insert_seed_kernel(FixParams P, const uint64_t *__restrict__ keys, uint64_t count,
+                                   const uint64_t *__restrict__ count_dev) {
+    if (count_dev) count = *count_dev;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t key = keys[i];
@@ -723,14 +725,14 @@ static dbl_status launch_init_frontier(dbl_graph *g, dbl_index *idx, const Group
 }
 
 static dbl_status launch_insert_seed(dbl_graph *g, FixParams &P, uint32_t nw, bool vec, bool /*count*/,
-                                     const uint64_t *keys, uint64_t nk) {
+                                     const uint64_t *keys, uint64_t nk, const uint64_t *nk_dev) {
     int blocks = (int)((nk + 255) / 256);
     if (blocks > g->sm_count * 8) blocks = g->sm_count * 8;
     if (blocks < 1) blocks = 1;
 #define DBL_SEED_CASE(N)                                                                      \
     case N:                                                                                   \
-        if (vec) insert_seed_kernel<N, (N % 2 == 0)><<<blocks, 256, 0, g->stream>>>(P, keys, nk); \
-        else insert_seed_kernel<N, false><<<blocks, 256, 0, g->stream>>>(P, keys, nk);       \
+        if (vec) insert_seed_kernel<N, (N % 2 == 0)><<<blocks, 256, 0, g->stream>>>(P, keys, nk, nk_dev); \
+        else insert_seed_kernel<N, false><<<blocks, 256, 0, g->stream>>>(P, keys, nk, nk_dev);       \
         break;
     switch (nw) {
         DBL_SEED_CASE(1) DBL_SEED_CASE(2) DBL_SEED_CASE(3) DBL_SEED_CASE(4)
@@ -798,18 +800,23 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
 // Read the run's control block (and, for the first run of a build, the prep
 // state) through pinned staging with ONE stream synchronisation; the ev[1]
 // timestamp of the run is recorded before it.
-static dbl_status finish_run(dbl_graph *g, Ctrl *hctrl, PrepState *hprep = nullptr) {
-    dbl_status s = g->host_stage.ensure(sizeof(Ctrl) + sizeof(PrepState) + 64);
+static dbl_status finish_run(dbl_graph *g, Ctrl *hctrl, PrepState *hprep = nullptr,
+                             const unsigned long long *extra_dev = nullptr, unsigned long long *extra_host = nullptr) {
+    dbl_status s = g->host_stage.ensure(sizeof(Ctrl) + sizeof(PrepState) + 96);
     if (s) return s;
     Ctrl *pc = reinterpret_cast<Ctrl *>(g->host_stage.p);
     PrepState *pp = reinterpret_cast<PrepState *>(reinterpret_cast<char *>(g->host_stage.p) +
                                                   ((sizeof(Ctrl) + 15) & ~size_t(15)));
     DBL_CUDA(cudaMemcpyAsync(pc, g->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, g->stream));
     if (hprep) DBL_CUDA(cudaMemcpyAsync(pp, g->prep.p, sizeof(PrepState), cudaMemcpyDeviceToHost, g->stream));
+    unsigned long long *pe = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(pp) +
+                                                                    ((sizeof(PrepState) + 15) & ~size_t(15)));
+    if (extra_dev) DBL_CUDA(cudaMemcpyAsync(pe, extra_dev, 16, cudaMemcpyDeviceToHost, g->stream));
     DBL_CUDA(cudaEventRecord(g->ev[1], g->stream));
     DBL_CUDA(cudaStreamSynchronize(g->stream));
     *hctrl = *pc;
     if (hprep) *hprep = *pp;
+    if (extra_dev) { extra_host[0] = pe[0]; extra_host[1] = pe[1]; }
     if (hctrl->overflow) { set_error("frontier queue overflow"); return DBL_E_CUDA; }
     return DBL_OK;
 }
@@ -1183,7 +1190,8 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
 // graph) through all label words.
 dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, uint64_t count,
                       bool count_changes, uint32_t *changed_out, uint32_t *seed_changed,
-                      uint32_t *levels) {
+                      uint32_t *levels, const unsigned long long *extra_dev, unsigned long long *extra_host,
+                      const uint64_t *dcount) {
     changed_out[0] = changed_out[1] = 0;
     seed_changed[0] = seed_changed[1] = 0;
     *levels = 0;
@@ -1201,14 +1209,16 @@ dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, ui
         bool vec = true;
         dbl_status s = prepare_params(g, idx, pair, P, nw, vec, count_changes, i == 0);
         if (s) return s;
-        if ((s = launch_insert_seed(g, P, nw, vec, count_changes, new_keys, count))) return s;
+        if ((s = launch_insert_seed(g, P, nw, vec, count_changes, new_keys, count, dcount))) return s;
         if (count_changes) {
             if ((s = launch_fixpoint<true>(g, P, nw, vec))) return s;
         } else {
             if ((s = launch_fixpoint<false>(g, P, nw, vec))) return s;
         }
         Ctrl h{};
-        if ((s = finish_run(g, &h))) return s;
+        // the caller's extra device word (batch stats) rides on the last sync
+        const bool last = i == half - 1;
+        if ((s = finish_run(g, &h, nullptr, last ? extra_dev : nullptr, last ? extra_host : nullptr))) return s;
         trace("insert: fixpoint", g->stream);
         if (std::getenv("DBL_TRACE")) {
             std::fprintf(stderr, "[dbl] insert fixpoint levels=%u nw=%u\n", h.levels, nw);
@@ -1225,8 +1235,7 @@ dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, ui
         seed_changed[1] |= h.seed_changed[1];
         if (h.levels > *levels) *levels = h.levels;
     }
-    DBL_CUDA(cudaEventRecord(g->ev[1], g->stream));
-    DBL_CUDA(cudaEventSynchronize(g->ev[1]));
+    // ev[1] was recorded (and reached) by the last finish_run
     cudaEventElapsedTime(&g->t_fix, g->ev[0], g->ev[1]);
     return DBL_OK;
 }

@@ -43,7 +43,9 @@ __global__ void swap_keys_kernel(const uint64_t *__restrict__ in, uint64_t m, ui
 // col[i] = low word; cnt[src]++ aggregated over lanes sharing a source
 // (keys are sorted, so runs are contiguous and hubs cost one atomic/warp).
 __global__ void count_rows_kernel(const uint64_t *__restrict__ keys, uint64_t m,
-                                  uint32_t *__restrict__ cnt, uint32_t *__restrict__ col) {
+                                  uint32_t *__restrict__ cnt, uint32_t *__restrict__ col,
+                                  const uint64_t *__restrict__ madd = nullptr) {
+    if (madd) m += *madd;   // device-side count (insert batches: m = delta + new keys)
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t mr = (m + 31) & ~31ull;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < mr; i += stride) {
@@ -80,13 +82,13 @@ dbl_status sort_keys(dbl_graph *g, uint64_t *keys, uint64_t *alt, uint64_t m, in
 
 // ptr[0..n] and col[0..m) from keys sorted by (src, dst).
 dbl_status build_csr_from_sorted(dbl_graph *g, const uint64_t *keys, uint64_t m, uint32_t n,
-                                 uint32_t *ptr, uint32_t *col) {
+                                 uint32_t *ptr, uint32_t *col, const uint64_t *madd, uint64_t madd_ub) {
     dbl_status s = g->scratch_d.ensure(((size_t)n + 1) * sizeof(uint32_t));
     if (s) return s;
     uint32_t *cnt = g->scratch_d.as<uint32_t>();
     DBL_CUDA(cudaMemsetAsync(cnt, 0, ((size_t)n + 1) * sizeof(uint32_t), g->stream));
-    if (m) {
-        count_rows_kernel<<<grid_for(m), 256, 0, g->stream>>>(keys, m, cnt, col);
+    if (m + madd_ub) {
+        count_rows_kernel<<<grid_for(m + madd_ub), 256, 0, g->stream>>>(keys, m, cnt, col, madd);
         DBL_CHECK_LAUNCH("count_rows_kernel");
     }
     size_t tmp = 0;
@@ -99,7 +101,9 @@ dbl_status build_csr_from_sorted(dbl_graph *g, const uint64_t *keys, uint64_t m,
 }
 
 // in-degree per destination of forward keys (u << 32 | v)
-__global__ void count_dst_kernel(const uint64_t *__restrict__ keys, uint64_t m, uint32_t *__restrict__ cnt) {
+__global__ void count_dst_kernel(const uint64_t *__restrict__ keys, uint64_t m, uint32_t *__restrict__ cnt,
+                                 const uint64_t *__restrict__ madd) {
+    if (madd) m += *madd;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
         atomicAdd(&cnt[(uint32_t)keys[i]], 1u);
 }
@@ -108,7 +112,8 @@ __global__ void count_dst_kernel(const uint64_t *__restrict__ keys, uint64_t m, 
 // by counting scatter (rows in arbitrary order; every consumer of the delta
 // CSC -- fixpoint, verifier, floods -- is order-independent)
 __global__ void scatter_src_kernel(const uint64_t *__restrict__ keys, uint64_t m, uint32_t *__restrict__ cursor,
-                                   uint32_t *__restrict__ col) {
+                                   uint32_t *__restrict__ col, const uint64_t *__restrict__ madd) {
+    if (madd) m += *madd;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = keys[i];
         col[atomicAdd(&cursor[(uint32_t)k], 1u)] = (uint32_t)(k >> 32);
@@ -117,13 +122,13 @@ __global__ void scatter_src_kernel(const uint64_t *__restrict__ keys, uint64_t m
 
 // Reverse CSR (ptr[0..n], col) of the forward keys by counting sort.
 static dbl_status build_csc_by_scatter(dbl_graph *g, const uint64_t *fkeys, uint64_t m, uint32_t n, uint32_t *ptr,
-                                       uint32_t *col) {
+                                       uint32_t *col, const uint64_t *madd = nullptr, uint64_t madd_ub = 0) {
     dbl_status s = g->scratch_d.ensure(((size_t)n + 1) * 2 * sizeof(uint32_t));
     if (s) return s;
     uint32_t *cnt = g->scratch_d.as<uint32_t>(), *cursor = cnt + n + 1;
     DBL_CUDA(cudaMemsetAsync(cnt, 0, ((size_t)n + 1) * sizeof(uint32_t), g->stream));
-    if (m) {
-        count_dst_kernel<<<grid_for(m), 256, 0, g->stream>>>(fkeys, m, cnt);
+    if (m + madd_ub) {
+        count_dst_kernel<<<grid_for(m + madd_ub), 256, 0, g->stream>>>(fkeys, m, cnt, madd);
         DBL_CHECK_LAUNCH("count_dst_kernel");
     }
     size_t tmp = 0;
@@ -131,9 +136,9 @@ static dbl_status build_csc_by_scatter(dbl_graph *g, const uint64_t *fkeys, uint
     if ((s = g->cub_tmp.ensure(tmp))) return s;
     DBL_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.p, tmp, cnt, ptr, (int64_t)n + 1, g->stream));
     DBL_LAUNCHED();
-    if (m) {
+    if (m + madd_ub) {
         DBL_CUDA(cudaMemcpyAsync(cursor, ptr, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, g->stream));
-        scatter_src_kernel<<<grid_for(m), 256, 0, g->stream>>>(fkeys, m, cursor, col);
+        scatter_src_kernel<<<grid_for(m + madd_ub), 256, 0, g->stream>>>(fkeys, m, cursor, col, madd);
         DBL_CHECK_LAUNCH("scatter_src_kernel");
     }
     return DBL_OK;
@@ -281,7 +286,7 @@ __global__ void flag_new_kernel(const uint64_t *__restrict__ keys, uint64_t coun
 
 // out = keys not yet in the graph (keys sorted + unique on input).
 dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, uint64_t *out,
-                            uint64_t *nout) {
+                            uint64_t *nout, const uint64_t **dcount) {
     if (count == 0) { *nout = 0; return DBL_OK; }
     dbl_status s = g->scratch_c.ensure(count + 16);
     if (s) return s;
@@ -296,9 +301,35 @@ dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, 
     if ((s = g->cub_tmp.ensure(tmp))) return s;
     DBL_CUDA(cub::DeviceSelect::Flagged(g->cub_tmp.p, tmp, keys, flag, out, d_n, (int64_t)count, g->stream));
     DBL_LAUNCHED();
+    if (dcount) {   // caller keeps the count on the device (read back with its final sync)
+        *dcount = d_n;
+        *nout = count;   // upper bound
+        return DBL_OK;
+    }
     DBL_CUDA(cudaMemcpyAsync(nout, d_n, sizeof(uint64_t), cudaMemcpyDeviceToHost, g->stream));
     DBL_CUDA(cudaStreamSynchronize(g->stream));
     return DBL_OK;
+}
+
+// Merge of two sorted key arrays with disjoint keys, B's length on the
+// device: every element finds its output slot by one binary search in the
+// other array (co-rank), so no host-side size is needed.
+__global__ void merge_scatter_kernel(const uint64_t *__restrict__ A, uint64_t na, const uint64_t *__restrict__ B,
+                                     const uint64_t *__restrict__ nb_dev, uint64_t nb_ub, uint64_t *__restrict__ C) {
+    const uint64_t nb = *nb_dev;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < na + nb_ub;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const bool fromA = t < na;
+        if (!fromA && t - na >= nb) continue;
+        const uint64_t x = fromA ? A[t] : B[t - na];
+        const uint64_t *o = fromA ? B : A;
+        uint64_t lo = 0, hi = fromA ? nb : na;
+        while (lo < hi) {   // number of elements of the other array below x
+            const uint64_t mid = (lo + hi) >> 1;
+            if (o[mid] < x) lo = mid + 1; else hi = mid;
+        }
+        C[(fromA ? t : t - na) + lo] = x;
+    }
 }
 
 static dbl_status merge_into(dbl_graph *g, DevBuf &dst, uint64_t nd, const uint64_t *add,
@@ -318,7 +349,7 @@ static dbl_status merge_into(dbl_graph *g, DevBuf &dst, uint64_t nd, const uint6
 }
 
 // Add sorted, unique, not-present forward keys to the delta adjacency.
-dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t count) {
+dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t count, const uint64_t *dcount) {
     if (count == 0) return DBL_OK;
     dbl_status s;
     uint32_t n = g->n;
@@ -353,20 +384,30 @@ dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t
     if (nd == 0) {
         if ((s = g->dkeys_f.ensure_geometric(count * 8 + 8))) return s;
         DBL_CUDA(cudaMemcpyAsync(g->dkeys_f.p, new_keys_f, count * 8, cudaMemcpyDeviceToDevice, g->stream));
+    } else if (dcount) {
+        if (nd + count >= (1ull << 31)) { set_error("delta adjacency too large to merge"); return DBL_E_CONFIG; }
+        if ((s = g->dmerge.ensure_geometric((nd + count) * 8 + 8))) return s;
+        merge_scatter_kernel<<<grid_for(nd + count), 256, 0, g->stream>>>(g->dkeys_f.as<uint64_t>(), nd, new_keys_f,
+                                                                           dcount, count, g->dmerge.as<uint64_t>());
+        DBL_CHECK_LAUNCH("merge_scatter_kernel");
+        std::swap(g->dkeys_f, g->dmerge);
+        trace("delta: merge fwd", g->stream);
     } else {
         // merged keys go to the spare buffer, which then swaps with the old one
         if ((s = merge_into(g, g->dkeys_f, nd, new_keys_f, count, g->dmerge))) return s;
         trace("delta: merge fwd", g->stream);
     }
+    // with a device-side count, m is an upper bound until the caller reads it
     uint64_t m = nd + count;
+    const uint64_t mb = dcount ? nd : m, mub = dcount ? count : 0;
     if ((s = g->dfptr.ensure(((size_t)n + 1) * 4)) || (s = g->drptr.ensure(((size_t)n + 1) * 4)) ||
         (s = g->dfcol.ensure_geometric(m * 4 + 4)) || (s = g->drcol.ensure_geometric(m * 4 + 4)))
         return s;
-    if ((s = build_csr_from_sorted(g, g->dkeys_f.as<uint64_t>(), m, n, g->dfptr.as<uint32_t>(),
-                                   g->dfcol.as<uint32_t>())))
+    if ((s = build_csr_from_sorted(g, g->dkeys_f.as<uint64_t>(), mb, n, g->dfptr.as<uint32_t>(),
+                                   g->dfcol.as<uint32_t>(), dcount, mub)))
         return s;
-    if ((s = build_csc_by_scatter(g, g->dkeys_f.as<uint64_t>(), m, n, g->drptr.as<uint32_t>(),
-                                  g->drcol.as<uint32_t>())))
+    if ((s = build_csc_by_scatter(g, g->dkeys_f.as<uint64_t>(), mb, n, g->drptr.as<uint32_t>(),
+                                  g->drcol.as<uint32_t>(), dcount, mub)))
         return s;
     trace("delta: csr+csc", g->stream);
     g->m_delta = m;

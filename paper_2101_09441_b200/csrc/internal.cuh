@@ -216,13 +216,17 @@ dbl_status graph_degrees_dev(const dbl_graph *g, uint32_t *indeg, uint32_t *outd
 Adj graph_fwd(const dbl_graph *g);
 Adj graph_rev(const dbl_graph *g);
 dbl_status build_csr_from_sorted(dbl_graph *g, const uint64_t *keys, uint64_t m, uint32_t n,
-                                 uint32_t *ptr, uint32_t *col);
+                                 uint32_t *ptr, uint32_t *col, const uint64_t *madd = nullptr,
+                                 uint64_t madd_ub = 0);
 dbl_status sort_keys(dbl_graph *g, uint64_t *keys, uint64_t *alt, uint64_t m, int end_bit,
                      uint64_t **sorted);
 int key_end_bit(uint32_t n);
-dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t count);
+// dcount (optional): the number of new keys lives on the device and `count`
+// is an upper bound; the caller settles g->m_delta after its final sync
+dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t count,
+                              const uint64_t *dcount = nullptr);
 dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, uint64_t *out,
-                            uint64_t *nout);
+                            uint64_t *nout, const uint64_t **dcount = nullptr);
 dbl_status graph_compact(dbl_graph *g);
 // select.cu
 dbl_status select_landmarks_dev(dbl_graph *g, uint32_t k, int strategy, uint32_t *dev_out);
@@ -247,7 +251,8 @@ dbl_status index_seed_records(dbl_graph *g, dbl_index *idx, uint64_t wmask);
 dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32_t nwords);
 dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, uint64_t count,
                       bool count_changes, uint32_t *changed_out, uint32_t *seed_changed,
-                      uint32_t *levels);
+                      uint32_t *levels, const unsigned long long *extra_dev = nullptr,
+                      unsigned long long *extra_host = nullptr, const uint64_t *dcount = nullptr);
 dbl_status work_model(const dbl_index *idx, dbl_graph *g, uint64_t *V, uint64_t *E,
                       uint32_t *levels);
 // query.cu
