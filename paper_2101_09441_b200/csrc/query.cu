@@ -1185,10 +1185,22 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
     if (threadIdx.x == 0) dq.n = 0;
     __syncthreads();
     const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
+#ifndef DBL_QPF
+#define DBL_QPF 1
+#endif
+    // the next iteration's pair is loaded while this one's records are in
+    // flight (one dependent round trip per iteration instead of two)
+    uint32_t nu = 0, nv = 0;
+    if (DBL_QPF && i0 < count) { nu = __ldg(qd.u + i0); nv = __ldg(qd.v + i0); }
     for (uint32_t i = i0; i < cr; i += stride) {
         bool unres = false;
+        uint32_t cu = nu, cv = nv;
+        if (DBL_QPF) {
+            const uint32_t inext = i + stride;
+            if (inext < count) { nu = __ldg(qd.u + inext); nv = __ldg(qd.v + inext); }
+        }
         if (i < count) {
-            const uint32_t u = __ldg(qd.u + i), v = __ldg(qd.v + i);
+            const uint32_t u = DBL_QPF ? cu : __ldg(qd.u + i), v = DBL_QPF ? cv : __ldg(qd.v + i);
             constexpr uint8_t QUEUED = 0xfc;   // in the CTA's BFS queue (code written later)
             uint8_t code = UNRESOLVED;
             if (u >= n || v >= n) {

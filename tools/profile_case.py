@@ -21,8 +21,12 @@ g = E.DynamicGraph.from_edges(n, src, dst)
 idx = E.build_index(g)
 idx = E.build_index(g)
 qu, qv = W.uniform_queries(n, 1_000_000, 2)
+import torch  # noqa: E402
+du = torch.from_numpy(qu.view(np.int32)).cuda()   # device-resident 1M batch, as bench.py times it
+dv = torch.from_numpy(qv.view(np.int32)).cuda()
 for _ in range(3):
-    codes, _ = E.query_codes(g, idx, qu, qv)
+    codes, _ = E.query_codes(g, idx, du, dv)
+codes = codes.cpu().numpy()
 iu, iv = W.gen_insert_workload(src, dst, n, 100_000, 50)
 st = E.insert_edges(g, idx, iu, iv)
 print("ok", g.edge_count, int(np.count_nonzero(codes >= 5)), st)
