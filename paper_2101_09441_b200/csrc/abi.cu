@@ -141,7 +141,9 @@ static int grid_for(uint64_t work, int threads = 256, int cap = 148 * 16) {
 
 __global__ void certified_kernel(const uint64_t *__restrict__ rec, uint32_t rw, uint32_t wdl,
                                  const uint64_t *__restrict__ keys, uint64_t count,
-                                 unsigned long long *out) {
+                                 unsigned long long *out, const uint64_t *__restrict__ valid_dev = nullptr,
+                                 const unsigned long long *__restrict__ abort_dev = nullptr) {
+    if (valid_dev) count = (abort_dev && *abort_dev) ? 0ull : min(count, *valid_dev);
     const uint32_t H = rw / 2;
     unsigned long long c = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
@@ -170,7 +172,9 @@ __global__ void pack_pairs_kernel(const uint32_t *__restrict__ u, const uint32_t
 }
 
 // (u << shift | v) -> (u << 32 | v), in place
-__global__ void widen_keys_kernel(uint64_t *__restrict__ keys, uint64_t count, uint32_t shift) {
+__global__ void widen_keys_kernel(uint64_t *__restrict__ keys, uint64_t count, uint32_t shift,
+                                  const uint64_t *__restrict__ valid_dev = nullptr) {
+    if (valid_dev) count = min(count, *valid_dev);
     const uint64_t mask = (1ull << shift) - 1;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -674,11 +678,11 @@ static dbl_status count_certified(dbl_graph *g, const dbl_index *idx, const uint
 // Same count into a device word (read by the caller after its final sync);
 // stream order puts it before the batch's label updates.
 static dbl_status count_certified_async(dbl_graph *g, const dbl_index *idx, const uint64_t *keys, uint64_t count,
-                                        unsigned long long *dcount) {
-    DBL_CUDA(cudaMemsetAsync(dcount, 0, 8, g->stream));
+                                        unsigned long long *dcount, const uint64_t *valid_dev,
+                                        const unsigned long long *abort_dev) {
     if (!count || !idx->wdl) return DBL_OK;
     certified_kernel<<<grid_for(count), 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->rw, idx->wdl, keys,
-                                                              count, dcount);
+                                                              count, dcount, valid_dev, abort_dev);
     DBL_LAUNCHED();
     return DBL_OK;
 }
@@ -745,7 +749,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     DevBuf in, keys, alt, newk, err;
     auto cleanup = [&]() { in.release(); keys.release(); alt.release(); newk.release(); err.release(); };
     if ((s = keys.ensure(count * 8)) || (s = alt.ensure(count * 8)) || (s = newk.ensure(count * 8)) ||
-        (s = err.ensure(16))) { cleanup(); return s; }
+        (s = err.ensure(32))) { cleanup(); return s; }
     const uint32_t *du = u, *dv = v;
     if (mem == DBL_MEM_HOST) {
         if ((s = in.ensure(count * 8))) { cleanup(); return s; }
@@ -754,79 +758,70 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
         du = in.as<uint32_t>();
         dv = du + count;
     }
-    DBL_CUDA(cudaMemsetAsync(err.p, 0, 8, g->stream));
+    // st4: [0] vertex-range flag, [1] certified count, [2] new-edge count,
+    // [3] unique count.  The whole batch is enqueued without a host round
+    // trip: counts stay on the device (the batch size bounds every launch)
+    // and a range error turns the batch into a no-op (no new edges), reported
+    // after the single readback -- the graph and labels are left as they were.
+    unsigned long long *st4 = err.as<unsigned long long>();
+    DBL_CUDA(cudaMemsetAsync(st4, 0, 32, g->stream));
     // the batch is sorted on (u << b | v), b = vertex-id bits: 2b radix bits
     // instead of 32 + b (5 onesweep passes instead of 7 at n = 2^20)
     const uint32_t shift = (uint32_t)key_end_bit(g->n) - 32;
-    pack_pairs_kernel<<<grid_for(count), 256, 0, g->stream>>>(du, dv, count, g->n, keys.as<uint64_t>(),
-                                                              err.as<unsigned long long>(), shift);
+    pack_pairs_kernel<<<grid_for(count), 256, 0, g->stream>>>(du, dv, count, g->n, keys.as<uint64_t>(), st4, shift);
     DBL_LAUNCHED();
-    // the range flag is read together with the unique count below (sorting
-    // and deduplicating the batch mutate nothing)
     uint64_t *sorted = nullptr;
     if ((s = sort_keys(g, keys.as<uint64_t>(), alt.as<uint64_t>(), count, (int)(2 * shift), &sorted))) {
         cleanup();
         return s;
     }
-    // unique (in place into the other buffer)
+    // unique (into the other buffer); its count goes to st4[3]
     uint64_t *uniq = sorted == keys.as<uint64_t>() ? alt.as<uint64_t>() : keys.as<uint64_t>();
+    const uint64_t *dnu = reinterpret_cast<const uint64_t *>(st4 + 3);
     {
-        DevBuf nsel;
-        if ((s = nsel.ensure(8))) { cleanup(); return s; }
         size_t tmp = 0;
-        DBL_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted, uniq, nsel.as<uint64_t>(), (int64_t)count, g->stream));
-        if ((s = g->cub_tmp.ensure(tmp))) { nsel.release(); cleanup(); return s; }
-        DBL_CUDA(cub::DeviceSelect::Unique(g->cub_tmp.p, tmp, sorted, uniq, nsel.as<uint64_t>(), (int64_t)count,
+        DBL_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted, uniq, (uint64_t *)(st4 + 3), (int64_t)count,
+                                           g->stream));
+        if ((s = g->cub_tmp.ensure(tmp))) { cleanup(); return s; }
+        DBL_CUDA(cub::DeviceSelect::Unique(g->cub_tmp.p, tmp, sorted, uniq, (uint64_t *)(st4 + 3), (int64_t)count,
                                            g->stream));
         DBL_LAUNCHED();
-        uint64_t nu = 0;
-        unsigned long long herr = 0;
-        DBL_CUDA(cudaMemcpyAsync(&nu, nsel.p, 8, cudaMemcpyDeviceToHost, g->stream));
-        DBL_CUDA(cudaMemcpyAsync(&herr, err.p, 8, cudaMemcpyDeviceToHost, g->stream));
-        DBL_CUDA(cudaStreamSynchronize(g->stream));
-        nsel.release();
-        if (herr) { cleanup(); set_error("insert vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
-        count = nu;
-        if (count) {
-            widen_keys_kernel<<<grid_for(count), 256, 0, g->stream>>>(uniq, count, shift);
-            DBL_LAUNCHED();
-        }
+        widen_keys_kernel<<<grid_for(count), 256, 0, g->stream>>>(uniq, count, shift, dnu);
+        DBL_LAUNCHED();
     }
     trace("insert: sort+unique", g->stream);
-    if ((s = count_certified_async(g, idx, uniq, count, err.as<unsigned long long>()))) { cleanup(); return s; }
-    // from here to the fixpoint's readback nothing waits on the host: the
-    // number of new edges stays on the device (`count` bounds it) and is read
-    // together with the fixpoint's control block
+    if ((s = count_certified_async(g, idx, uniq, count, st4 + 1, dnu, st4))) { cleanup(); return s; }
     uint64_t nnew = 0;
     bool cert_read = false;
     const uint64_t *dnew = nullptr;
-    if ((s = graph_filter_new(g, uniq, count, newk.as<uint64_t>(), &nnew, &dnew))) { cleanup(); return s; }
+    if ((s = graph_filter_new(g, uniq, count, newk.as<uint64_t>(), &nnew, &dnew, dnu, st4))) { cleanup(); return s; }
     trace("insert: certified+filter", g->stream);
-    if (count) {
+    bool range_error = false;
+    {
         const uint64_t nd = g->m_delta;
-        // err[1] = number of new edges (read with err[0] = certified)
-        DBL_CUDA(cudaMemcpyAsync(err.as<unsigned long long>() + 1, dnew, 8, cudaMemcpyDeviceToDevice, g->stream));
+        DBL_CUDA(cudaMemcpyAsync(st4 + 2, dnew, 8, cudaMemcpyDeviceToDevice, g->stream));
         if ((s = graph_insert_delta(g, newk.as<uint64_t>(), count, dnew))) { cleanup(); return s; }
         trace("insert: delta merge", g->stream);
         uint32_t changed[2], seedc[2], levels = 0;
-        unsigned long long hx[2] = {0, 0};
-        if ((s = run_insert(g, idx, newk.as<uint64_t>(), count, true, changed, seedc, &levels,
-                            err.as<unsigned long long>(), hx, dnew))) {
+        unsigned long long hx[4] = {0, 0, 0, 0};
+        if ((s = run_insert(g, idx, newk.as<uint64_t>(), count, true, changed, seedc, &levels, st4, hx, dnew))) {
             cleanup();
             return s;
         }
-        st.certified = hx[0];
-        nnew = hx[1];
+        range_error = hx[0] != 0;
+        st.certified = hx[1];
+        nnew = hx[2];
         cert_read = true;
         g->m_delta = nd + nnew;   // settle the upper bound used while enqueueing
         st.inserted = nnew;
         st.labels_changed = (uint64_t)changed[0] + changed[1];
         st.levels = levels;
-        if (g->m_delta * 4 > g->m_base + 1024) {
+        if (!range_error && g->m_delta * 4 > g->m_base + 1024) {
             if ((s = graph_compact(g))) { cleanup(); return s; }
             st.delta_merged = 1;
         }
     }
+    if (range_error) { cleanup(); set_error("insert vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
     if (!cert_read) {
         unsigned long long hcert = 0;
         DBL_CUDA(cudaMemcpyAsync(&hcert, err.p, 8, cudaMemcpyDeviceToHost, g->stream));

@@ -802,7 +802,7 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
 // timestamp of the run is recorded before it.
 static dbl_status finish_run(dbl_graph *g, Ctrl *hctrl, PrepState *hprep = nullptr,
                              const unsigned long long *extra_dev = nullptr, unsigned long long *extra_host = nullptr) {
-    dbl_status s = g->host_stage.ensure(sizeof(Ctrl) + sizeof(PrepState) + 96);
+    dbl_status s = g->host_stage.ensure(sizeof(Ctrl) + sizeof(PrepState) + 128);
     if (s) return s;
     Ctrl *pc = reinterpret_cast<Ctrl *>(g->host_stage.p);
     PrepState *pp = reinterpret_cast<PrepState *>(reinterpret_cast<char *>(g->host_stage.p) +
@@ -811,12 +811,13 @@ static dbl_status finish_run(dbl_graph *g, Ctrl *hctrl, PrepState *hprep = nullp
     if (hprep) DBL_CUDA(cudaMemcpyAsync(pp, g->prep.p, sizeof(PrepState), cudaMemcpyDeviceToHost, g->stream));
     unsigned long long *pe = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(pp) +
                                                                     ((sizeof(PrepState) + 15) & ~size_t(15)));
-    if (extra_dev) DBL_CUDA(cudaMemcpyAsync(pe, extra_dev, 16, cudaMemcpyDeviceToHost, g->stream));
+    if (extra_dev) DBL_CUDA(cudaMemcpyAsync(pe, extra_dev, 32, cudaMemcpyDeviceToHost, g->stream));
     DBL_CUDA(cudaEventRecord(g->ev[1], g->stream));
     DBL_CUDA(cudaStreamSynchronize(g->stream));
     *hctrl = *pc;
     if (hprep) *hprep = *pp;
-    if (extra_dev) { extra_host[0] = pe[0]; extra_host[1] = pe[1]; }
+    if (extra_dev)
+        for (int k = 0; k < 4; ++k) extra_host[k] = pe[k];
     if (hctrl->overflow) { set_error("frontier queue overflow"); return DBL_E_CUDA; }
     return DBL_OK;
 }

@@ -273,9 +273,14 @@ __device__ __forceinline__ bool bsearch_u64(const uint64_t *a, uint64_t n, uint6
 __global__ void flag_new_kernel(const uint64_t *__restrict__ keys, uint64_t count,
                                 const uint32_t *__restrict__ fptr, const uint32_t *__restrict__ fcol,
                                 const uint64_t *__restrict__ dkeys, uint64_t nd,
-                                uint8_t *__restrict__ flag) {
+                                uint8_t *__restrict__ flag, const uint64_t *__restrict__ valid_dev,
+                                const unsigned long long *__restrict__ abort_dev) {
+    // device-side batch size / abort flag (insert batches): entries beyond the
+    // unique count, or every entry of an aborted batch, are never new
+    const uint64_t valid = valid_dev ? (abort_dev && *abort_dev ? 0ull : *valid_dev) : count;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
          i += (uint64_t)gridDim.x * blockDim.x) {
+        if (i >= valid) { flag[i] = 0; continue; }
         uint64_t k = keys[i];
         uint32_t u = (uint32_t)(k >> 32), v = (uint32_t)k;
         bool present = bsearch_u32(fcol, fptr[u], fptr[u + 1], v);
@@ -286,7 +291,8 @@ __global__ void flag_new_kernel(const uint64_t *__restrict__ keys, uint64_t coun
 
 // out = keys not yet in the graph (keys sorted + unique on input).
 dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, uint64_t *out,
-                            uint64_t *nout, const uint64_t **dcount) {
+                            uint64_t *nout, const uint64_t **dcount, const uint64_t *valid_dev,
+                            const unsigned long long *abort_dev) {
     if (count == 0) { *nout = 0; return DBL_OK; }
     dbl_status s = g->scratch_c.ensure(count + 16);
     if (s) return s;
@@ -294,7 +300,8 @@ dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, 
     uint64_t *d_n = g->scratch_c.as<uint64_t>();
     flag_new_kernel<<<grid_for(count), 256, 0, g->stream>>>(keys, count, g->fptr.as<uint32_t>(),
                                                              g->fcol.as<uint32_t>(),
-                                                             g->dkeys_f.as<uint64_t>(), g->m_delta, flag);
+                                                             g->dkeys_f.as<uint64_t>(), g->m_delta, flag,
+                                                             valid_dev, abort_dev);
     DBL_CHECK_LAUNCH("flag_new_kernel");
     size_t tmp = 0;
     DBL_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, keys, flag, out, d_n, (int64_t)count, g->stream));

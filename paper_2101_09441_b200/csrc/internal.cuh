@@ -226,7 +226,8 @@ int key_end_bit(uint32_t n);
 dbl_status graph_insert_delta(dbl_graph *g, const uint64_t *new_keys_f, uint64_t count,
                               const uint64_t *dcount = nullptr);
 dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, uint64_t *out,
-                            uint64_t *nout, const uint64_t **dcount = nullptr);
+                            uint64_t *nout, const uint64_t **dcount = nullptr,
+                            const uint64_t *valid_dev = nullptr, const unsigned long long *abort_dev = nullptr);
 dbl_status graph_compact(dbl_graph *g);
 // select.cu
 dbl_status select_landmarks_dev(dbl_graph *g, uint32_t k, int strategy, uint32_t *dev_out);
