@@ -553,3 +553,29 @@ def test_pivot_capped_sweeps_deep_graph(k, kp):
     oidx = og.build(k, kp, threads=8)
     np.testing.assert_array_equal(np.array(idx.landmark_set.landmarks), oidx.landmarks)
     assert_labels_equal_oracle(idx, oidx)
+
+
+def test_insert_batch_range_error_leaves_index_untouched():
+    """A batch with one endpoint outside [0, n) raises VertexRangeError and
+    inserts nothing (updates.py checks before mutating): the batch is aborted
+    on the device, so edges, labels and the delta adjacency stay as they
+    were, before and after some delta already exists."""
+    n, src, dst = rmat_case(12, 8, 31)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    idx = E.build_index(g)
+    for round_ in range(2):
+        before_m = g.edge_count
+        before = idx.export_words()
+        iu, iv = W.gen_insert_workload(src, dst, n, 300, 40 + round_)
+        bad_v = iv.copy()
+        bad_v[137] = n + 5
+        with pytest.raises(E.VertexRangeError):
+            E.insert_edges(g, idx, iu, bad_v)
+        assert g.edge_count == before_m
+        after = idx.export_words()
+        for f in FAMS:
+            np.testing.assert_array_equal(after[f], before[f], err_msg=f)
+        # a valid batch afterwards still matches a frozen-metadata rebuild
+        st = E.insert_edges(g, idx, iu, iv)
+        assert st.inserted == len(iu)
+        assert idx.labels_equal(E.rebuild_index(g, idx))
