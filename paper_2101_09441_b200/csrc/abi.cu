@@ -28,12 +28,17 @@ uint64_t &launch_counter() { return g_launches; }
 // thread's current engine stream, see set_stream); handing it to work on a
 // different stream first waits for that stream, so recycled memory is never
 // written while an earlier kernel may still read it.
-struct PoolBlock { void *p; cudaStream_t s; };
+// A block freed right after a device-wide synchronisation (index / graph
+// teardown) is "clean": no work can still touch it, so reusing it needs no
+// wait at all (a device sync on reuse would sit inside the next build).
+struct PoolBlock { void *p; cudaStream_t s; bool clean; };
 static std::mutex g_pool_mu;
 static std::map<std::pair<int, size_t>, std::vector<PoolBlock>> g_pool;
 static thread_local cudaStream_t g_cur_stream = nullptr;
+static thread_local bool g_free_clean = false;
 
-void set_stream(cudaStream_t s) { g_cur_stream = s; }
+void set_stream(cudaStream_t s) { g_cur_stream = s; g_free_clean = false; }
+void set_stream_synced() { g_cur_stream = nullptr; g_free_clean = true; }
 
 static size_t size_class(size_t n) {
     if (n <= 4096) {
@@ -51,7 +56,7 @@ cudaError_t pool_alloc(void **p, size_t *bytes, int *device) {
     int dev = 0;
     cudaGetDevice(&dev);
     const size_t c = size_class(*bytes);
-    PoolBlock blk{nullptr, nullptr};
+    PoolBlock blk{nullptr, nullptr, false};
     {
         std::lock_guard<std::mutex> lk(g_pool_mu);
         auto it = g_pool.find({dev, c});
@@ -65,7 +70,7 @@ cudaError_t pool_alloc(void **p, size_t *bytes, int *device) {
         }
     }
     if (blk.p) {
-        if (blk.s != g_cur_stream || !blk.s) {
+        if (!blk.clean && (blk.s != g_cur_stream || !blk.s)) {
             if (blk.s) cudaStreamSynchronize(blk.s); else cudaDeviceSynchronize();
         }
         *p = blk.p;
@@ -94,7 +99,7 @@ void pool_forget_stream(cudaStream_t st) {
 
 void pool_free(void *p, size_t bytes, int device) {
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    g_pool[{device, bytes}].push_back(PoolBlock{p, g_cur_stream});
+    g_pool[{device, bytes}].push_back(PoolBlock{p, g_cur_stream, g_free_clean});
 }
 
 void pool_trim() {
@@ -386,8 +391,8 @@ extern "C" dbl_status dbl_index_build_words(const dbl_graph *gc, dbl_index *idx,
 extern "C" dbl_status dbl_index_free(dbl_index *idx) {
     if (!idx) return DBL_OK;
     cudaSetDevice(idx->device);
-    set_stream(nullptr);
     cudaDeviceSynchronize();
+    set_stream_synced();
     idx->rec.release();
     idx->landmarks.release();
     idx->leaf_flags.release();

@@ -43,6 +43,7 @@ cudaError_t pool_alloc(void **p, size_t *bytes, int *device);
 void pool_free(void *p, size_t bytes, int device);
 void pool_trim();
 void set_stream(cudaStream_t s);  // stream that subsequent pool traffic belongs to
+void set_stream_synced();         // the device was just synchronised: frees are reusable without waiting
 void pool_forget_stream(cudaStream_t s);  // before a stream is destroyed
 // Debug phase timer: DBL_TRACE=1 prints host-side phase times to stderr.
 void trace(const char *what, cudaStream_t s);
