@@ -144,17 +144,16 @@ static int grid_for(uint64_t work, int threads = 256, int cap = 148 * 16) {
     return (int)b;
 }
 
-__global__ void certified_kernel(const uint64_t *__restrict__ rec, uint32_t rw, uint32_t wdl,
+__global__ void certified_kernel(const uint64_t *__restrict__ rec, uint32_t rs, uint32_t H, uint32_t wdl,
                                  const uint64_t *__restrict__ keys, uint64_t count,
                                  unsigned long long *out, const uint64_t *__restrict__ valid_dev = nullptr,
                                  const unsigned long long *__restrict__ abort_dev = nullptr) {
     if (valid_dev) count = (abort_dev && *abort_dev) ? 0ull : min(count, *valid_dev);
-    const uint32_t H = rw / 2;
     unsigned long long c = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = keys[i];
-        const uint64_t *ru = rec + (k >> 32) * rw, *rv = rec + (uint32_t)k * (uint64_t)rw;
+        const uint64_t *ru = rec + (k >> 32) * rs, *rv = rec + (uint32_t)k * (uint64_t)rs;
         uint64_t acc = 0;
         for (uint32_t w = 0; w < wdl; ++w) acc |= ru[H + w] & rv[w];  // dl_out[u] & dl_in[v]
         c += acc != 0;
@@ -199,18 +198,18 @@ static void family_span(const dbl_index *idx, int f, uint32_t &off, uint32_t &w)
     }
 }
 
-__global__ void gather_family_kernel(const uint64_t *__restrict__ rec, uint32_t rw, uint32_t off, uint32_t w,
+__global__ void gather_family_kernel(const uint64_t *__restrict__ rec, uint32_t rs, uint32_t off, uint32_t w,
                                      uint32_t n, uint64_t *__restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * w;
          i += (uint64_t)gridDim.x * blockDim.x)
-        out[i] = rec[(i / w) * rw + off + i % w];
+        out[i] = rec[(i / w) * rs + off + i % w];
 }
 
-__global__ void scatter_family_kernel(uint64_t *__restrict__ rec, uint32_t rw, uint32_t off, uint32_t w,
+__global__ void scatter_family_kernel(uint64_t *__restrict__ rec, uint32_t rs, uint32_t off, uint32_t w,
                                       uint32_t n, const uint64_t *__restrict__ in) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * w;
          i += (uint64_t)gridDim.x * blockDim.x)
-        rec[(i / w) * rw + off + i % w] = in[i];
+        rec[(i / w) * rs + off + i % w] = in[i];
 }
 
 __global__ void diff_kernel(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b, uint64_t count,
@@ -263,16 +262,21 @@ static dbl_status alloc_index(const dbl_graph *g, const dbl_config *cfg, dbl_ind
     idx->wdl = (cfg->k + 63) / 64;
     idx->wbl = (cfg->k_prime + 63) / 64;
     idx->rw = 2 * (idx->wdl + idx->wbl);
+    idx->rs = rec_stride(idx->wdl + idx->wbl);
     if (idx->wdl > 16 || idx->wbl > 16 || idx->rw > 64) {
         delete idx;
         set_error("label widths above 1024 bits are not supported");
         return DBL_E_CONFIG;
     }
     dbl_status s;
-    if ((s = idx->rec.ensure((size_t)g->n * idx->rw * 8 + 16)) || (s = idx->landmarks.ensure((size_t)cfg->k * 4 + 4)) ||
+    if ((s = idx->rec.ensure((size_t)g->n * idx->rs * 8 + 16)) || (s = idx->landmarks.ensure((size_t)cfg->k * 4 + 4)) ||
         (s = idx->leaf_flags.ensure((size_t)g->n + 16)) || (s = idx->bucket.ensure((size_t)g->n * 4 + 16))) {
         dbl_index_free(idx);
         return s;
+    }
+    if (idx->rs != idx->rw && g->n) {   // pad words are never written: zero them once
+        const cudaError_t e = cudaMemsetAsync(idx->rec.p, 0, (size_t)g->n * idx->rs * 8, g->stream);
+        if (e != cudaSuccess) { dbl_index_free(idx); return cuda_fail(e, "clear records"); }
     }
     *out = idx;
     return DBL_OK;
@@ -398,6 +402,8 @@ extern "C" dbl_status dbl_index_free(dbl_index *idx) {
     idx->leaf_flags.release();
     idx->bucket.release();
     idx->ovr.release();
+    idx->dmask.release();
+    idx->sccmask.release();
     delete idx;
     return DBL_OK;
 }
@@ -434,7 +440,7 @@ extern "C" dbl_status dbl_index_export(const dbl_index *idx, uint64_t *dl_in, ui
         const uint64_t cnt = (uint64_t)idx->n * w;
         dbl_status s = tmp.ensure(cnt * 8);
         if (s) return s;
-        gather_family_kernel<<<grid_for(cnt), 256>>>(idx->rec.as<uint64_t>(), idx->rw, off, w, idx->n,
+        gather_family_kernel<<<grid_for(cnt), 256>>>(idx->rec.as<uint64_t>(), idx->rs, off, w, idx->n,
                                                      tmp.as<uint64_t>());
         DBL_LAUNCHED();
         cudaError_t e = cudaMemcpy(outs[f], tmp.p, cnt * 8, cudaMemcpyDeviceToHost);
@@ -460,7 +466,7 @@ extern "C" dbl_status dbl_index_import(dbl_index *idx, const uint64_t *dl_in, co
         if (s) return s;
         cudaError_t e = cudaMemcpy(tmp.p, ins[f], cnt * 8, cudaMemcpyHostToDevice);
         if (e != cudaSuccess) { tmp.release(); return cuda_fail(e, "import labels"); }
-        scatter_family_kernel<<<grid_for(cnt), 256>>>(idx->rec.as<uint64_t>(), idx->rw, off, w, idx->n,
+        scatter_family_kernel<<<grid_for(cnt), 256>>>(idx->rec.as<uint64_t>(), idx->rs, off, w, idx->n,
                                                       tmp.as<uint64_t>());
         DBL_LAUNCHED();
     }
@@ -481,7 +487,7 @@ extern "C" dbl_status dbl_index_equal(const dbl_index *a, const dbl_index *b, in
     dbl_status s = flag.ensure(8);
     if (s) return s;
     cudaMemset(flag.p, 0, 8);
-    const uint64_t cnt = (uint64_t)a->n * a->rw;
+    const uint64_t cnt = (uint64_t)a->n * a->rs;
     if (cnt) {
         diff_kernel<<<grid_for(cnt), 256>>>(a->rec.as<uint64_t>(), b->rec.as<uint64_t>(), cnt,
                                             flag.as<unsigned long long>());
@@ -513,7 +519,7 @@ extern "C" dbl_status dbl_index_grow(dbl_index *idx, uint32_t n) {
     DBL_CUDA(cudaSetDevice(idx->device));
     set_stream(nullptr);
     dbl_status s;
-    if ((s = grow_buf(idx->rec, (size_t)idx->n * idx->rw * 8, (size_t)n * idx->rw * 8 + 16, 0)) ||
+    if ((s = grow_buf(idx->rec, (size_t)idx->n * idx->rs * 8, (size_t)n * idx->rs * 8 + 16, 0)) ||
         (s = grow_buf(idx->leaf_flags, idx->n, (size_t)n + 16, 0)) ||
         (s = grow_buf(idx->bucket, (size_t)idx->n * 4, (size_t)n * 4 + 16, 0)))
         return s;
@@ -548,7 +554,7 @@ extern "C" dbl_status dbl_graph_add_vertices(dbl_graph *g, uint32_t count) {
 extern "C" dbl_status dbl_index_records(const dbl_index *idx, uint64_t **dev_records, uint32_t *wpr) {
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     if (dev_records) *dev_records = idx->rec.as<uint64_t>();
-    if (wpr) *wpr = idx->rw;
+    if (wpr) *wpr = idx->rs;
     return DBL_OK;
 }
 
@@ -669,7 +675,7 @@ static dbl_status count_certified(dbl_graph *g, const dbl_index *idx, const uint
     dbl_status s = c.ensure(8);
     if (s) return s;
     DBL_CUDA(cudaMemsetAsync(c.p, 0, 8, g->stream));
-    certified_kernel<<<grid_for(count), 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->rw, idx->wdl, keys,
+    certified_kernel<<<grid_for(count), 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->rs, idx->wdl + idx->wbl, idx->wdl, keys,
                                                               count, c.as<unsigned long long>());
     DBL_LAUNCHED();
     unsigned long long h = 0;
@@ -686,7 +692,7 @@ static dbl_status count_certified_async(dbl_graph *g, const dbl_index *idx, cons
                                         unsigned long long *dcount, const uint64_t *valid_dev,
                                         const unsigned long long *abort_dev) {
     if (!count || !idx->wdl) return DBL_OK;
-    certified_kernel<<<grid_for(count), 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->rw, idx->wdl, keys,
+    certified_kernel<<<grid_for(count), 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->rs, idx->wdl + idx->wbl, idx->wdl, keys,
                                                               count, dcount, valid_dev, abort_dev);
     DBL_LAUNCHED();
     return DBL_OK;
@@ -851,21 +857,21 @@ extern "C" dbl_status dbl_work_model(const dbl_index *idx, const dbl_graph *gc, 
 
 // -------------------------------------------------- multi-GPU word shards --
 
-__global__ void pack_words_kernel(const uint64_t *__restrict__ rec, uint32_t rw, uint32_t n,
+__global__ void pack_words_kernel(const uint64_t *__restrict__ rec, uint32_t rs, uint32_t n,
                                   const uint32_t *__restrict__ words, uint32_t nw, uint64_t *__restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * nw;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t j = (uint32_t)(i / n), v = (uint32_t)(i % n);
-        out[i] = rec[(size_t)v * rw + words[j]];
+        out[i] = rec[(size_t)v * rs + words[j]];
     }
 }
 
-__global__ void unpack_words_kernel(uint64_t *__restrict__ rec, uint32_t rw, uint32_t n,
+__global__ void unpack_words_kernel(uint64_t *__restrict__ rec, uint32_t rs, uint32_t n,
                                     const uint32_t *__restrict__ words, uint32_t nw, const uint64_t *__restrict__ in) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * nw;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t j = (uint32_t)(i / n), v = (uint32_t)(i % n);
-        rec[(size_t)v * rw + words[j]] = in[i];
+        rec[(size_t)v * rs + words[j]] = in[i];
     }
 }
 
@@ -883,7 +889,7 @@ extern "C" dbl_status dbl_index_pack_words(const dbl_index *idx, const uint32_t 
     cudaStream_t st = (cudaStream_t)stream;
     set_stream(st);
     DBL_CUDA(cudaMemcpyAsync(w.p, words, nw * 4, cudaMemcpyHostToDevice, st));
-    pack_words_kernel<<<grid_for((uint64_t)idx->n * nw), 256, 0, st>>>(idx->rec.as<uint64_t>(), idx->rw, idx->n,
+    pack_words_kernel<<<grid_for((uint64_t)idx->n * nw), 256, 0, st>>>(idx->rec.as<uint64_t>(), idx->rs, idx->n,
                                                                        w.as<uint32_t>(), nw, dev_slab);
     DBL_LAUNCHED();
     DBL_CUDA(cudaStreamSynchronize(st));
@@ -904,7 +910,7 @@ extern "C" dbl_status dbl_index_unpack_words(dbl_index *idx, const uint32_t *wor
     cudaStream_t st = (cudaStream_t)stream;
     set_stream(st);
     DBL_CUDA(cudaMemcpyAsync(w.p, words, nw * 4, cudaMemcpyHostToDevice, st));
-    unpack_words_kernel<<<grid_for((uint64_t)idx->n * nw), 256, 0, st>>>(idx->rec.as<uint64_t>(), idx->rw, idx->n,
+    unpack_words_kernel<<<grid_for((uint64_t)idx->n * nw), 256, 0, st>>>(idx->rec.as<uint64_t>(), idx->rs, idx->n,
                                                                          w.as<uint32_t>(), nw, dev_slab);
     DBL_LAUNCHED();
     DBL_CUDA(cudaStreamSynchronize(st));
@@ -969,12 +975,12 @@ extern "C" dbl_status dbl_graph_add_edges(dbl_graph *g, const uint32_t *u, const
 __global__ void label_tests_kernel(const uint64_t *__restrict__ rec, uint32_t wdl, uint32_t wbl, uint32_t n,
                                    const uint32_t *__restrict__ x, const uint32_t *__restrict__ y, uint64_t count,
                                    uint8_t *__restrict__ dl, uint8_t *__restrict__ bl, unsigned long long *err) {
-    const uint32_t H = wdl + wbl, rw = 2 * H;
+    const uint32_t H = wdl + wbl, rs = rec_stride(H);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t a = x[i], b = y[i];
         if (a >= n || b >= n) { atomicOr(err, 1ull); continue; }
-        const uint64_t *ra = rec + (size_t)a * rw, *rb = rec + (size_t)b * rw;
+        const uint64_t *ra = rec + (size_t)a * rs, *rb = rec + (size_t)b * rs;
         uint64_t d = 0, c = 0;
         for (uint32_t k = 0; k < wdl; ++k) d |= ra[H + k] & rb[k];
         for (uint32_t k = 0; k < wbl; ++k) c |= (ra[wdl + k] & ~rb[wdl + k]) | (rb[H + wdl + k] & ~ra[H + wdl + k]);

@@ -545,12 +545,12 @@ __global__ void __launch_bounds__(FIX_THREADS, DBL_FMINB) fixpoint_kernel(FixPar
 __global__ void seed_records_kernel(uint64_t *__restrict__ rec, uint32_t n, uint32_t wdl, uint32_t wbl,
                                     const uint8_t *__restrict__ flags, const uint32_t *__restrict__ bucket,
                                     uint64_t wmask) {
-    const uint32_t H = wdl + wbl, rw = 2 * H;
+    const uint32_t H = wdl + wbl, rw = 2 * H, rs = rec_stride(H);
     const bool all = (rw >= 64) ? wmask == ~0ull : (wmask & ((1ull << rw) - 1)) == ((1ull << rw) - 1);
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
         const uint8_t f = flags[v];
         const uint32_t b = bucket[v];
-        uint64_t *r = rec + (size_t)v * rw;
+        uint64_t *r = rec + (size_t)v * rs;
         // word index of the bucket bit in each half (or none)
         const uint32_t win = (f & 1) ? wdl + b / 64 : 0xffffffffu;
         const uint32_t wout = (f & 2) ? H + wdl + b / 64 : 0xffffffffu;
@@ -569,14 +569,14 @@ __global__ void seed_records_kernel(uint64_t *__restrict__ rec, uint32_t n, uint
     }
 }
 
-__global__ void landmark_bits_kernel(uint64_t *__restrict__ rec, uint32_t rw, uint32_t H,
+__global__ void landmark_bits_kernel(uint64_t *__restrict__ rec, uint32_t rs, uint32_t H,
                                      const uint32_t *__restrict__ lm, uint32_t k, uint64_t wmask) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
         const uint64_t v = lm[i];
         if ((wmask >> (i / 64)) & 1)
-            atomicOr(reinterpret_cast<unsigned long long *>(rec + v * rw + i / 64), 1ull << (i % 64));
+            atomicOr(reinterpret_cast<unsigned long long *>(rec + v * rs + i / 64), 1ull << (i % 64));
         if ((wmask >> (H + i / 64)) & 1)
-            atomicOr(reinterpret_cast<unsigned long long *>(rec + v * rw + H + i / 64), 1ull << (i % 64));
+            atomicOr(reinterpret_cast<unsigned long long *>(rec + v * rs + H + i / 64), 1ull << (i % 64));
     }
 }
 
@@ -760,7 +760,7 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
         DirParams &D = P.d[d];
         D.adj = d == 0 ? graph_fwd(g) : graph_rev(g);
         D.padj = d == 0 ? graph_rev(g) : graph_fwd(g);
-        D.stride = idx->rw;
+        D.stride = idx->rs;
         D.bits = g->stamp[d].as<uint32_t>();
         D.cur = D.bits + bmw + 1;
         D.cap = g->qcap;
@@ -775,7 +775,7 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
         if (gr[d]) {
             D.lab = idx->rec.as<uint64_t>() + gr[d]->w0;
             nw = gr[d]->nw;
-            if ((gr[d]->w0 % 2) || (idx->rw % 2)) vec = false;
+            if ((gr[d]->w0 % 2) || (idx->rs % 2)) vec = false;
         } else {
             D.lab = idx->rec.as<uint64_t>();
         }
@@ -832,7 +832,7 @@ dbl_status index_seed_records(dbl_graph *g, dbl_index *idx, uint64_t wmask) {
     DBL_CHECK_LAUNCH("seed_records_kernel");
     if (idx->cfg.k) {
         landmark_bits_kernel<<<(idx->cfg.k + 255) / 256, 256, 0, g->stream>>>(
-            idx->rec.as<uint64_t>(), idx->rw, idx->wdl + idx->wbl, idx->landmarks.as<uint32_t>(), idx->cfg.k,
+            idx->rec.as<uint64_t>(), idx->rs, idx->wdl + idx->wbl, idx->landmarks.as<uint32_t>(), idx->cfg.k,
             wmask);
         DBL_CHECK_LAUNCH("landmark_bits_kernel");
     }
@@ -870,6 +870,9 @@ struct ReachParams {
     uint64_t wmask;          // record words being built (bit w = word w)
     uint64_t cap_wmask;      // words whose level-0 frontier is `front` (used when the sweeps are capped)
     uint32_t *front[2];      // level-0 frontier bitmaps of the label fixpoint (or nullptr)
+    uint32_t *dmask_out;     // copy of vis[0] kept with the index (or nullptr)
+    unsigned long long *scc_out;   // DL bits of the landmarks in h's SCC (wdl words)
+    uint32_t k, wdl;
     uint32_t H;
     Adj adj[2];          // [0] in-edges (reverse adjacency), [1] out-edges (forward adjacency)
     Adj top[2];          // first level from h: [0] out-edges, [1] in-edges
@@ -961,18 +964,28 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
             break;
         }
     }
+    // keep D(h) and the SCC landmarks for query pruning (marks are exact
+    // members even when the sweeps were capped)
+    if (P.dmask_out)
+        for (uint64_t w = tid; w < P.nwords; w += nth) P.dmask_out[w] = P.vis[0][w];
+    if (P.scc_out)
+        for (uint64_t i = tid; i < P.k; i += nth) {
+            const uint32_t x = P.lm[i];
+            if (x < P.n && (((P.vis[0][x >> 5] & P.vis[1][x >> 5]) >> (x & 31)) & 1u))
+                atomicOr(&P.scc_out[i / 64], 1ull << (i % 64));
+        }
     if (capped && !(P.front[0] && P.front[1])) return;   // grid-uniform
     // L_in(h) = OR of the in-halves over A(h), L_out(h) = OR of the
     // out-halves over D(h); then every x in D(h) takes L_in(h), every x in
     // A(h) takes L_out(h)
     __shared__ unsigned long long acc[2 * MAX_SHARD_WORDS];
-    const uint32_t H = P.H, rw = 2 * H;
+    const uint32_t H = P.H, rw = 2 * H, rs = rec_stride(H);
     const uint64_t wm = capped ? P.cap_wmask : P.wmask;
     for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = 0;
     __syncthreads();
     for (uint64_t x = tid; x < P.n; x += nth) {
         const bool fwd = (P.vis[0][x >> 5] >> (x & 31)) & 1u, bwd = (P.vis[1][x >> 5] >> (x & 31)) & 1u;
-        const uint64_t *r = P.rec + x * rw;
+        const uint64_t *r = P.rec + x * rs;
         if (bwd)
             for (uint32_t w = 0; w < H; ++w) {
                 const uint64_t v = ((wm >> w) & 1u) ? r[w] : 0ull;
@@ -1006,7 +1019,7 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
         }
     }
     for (uint64_t x = tid; x < P.n; x += nth) {
-        uint64_t *r = P.rec + x * rw;
+        uint64_t *r = P.rec + x * rs;
         if ((P.vis[0][x >> 5] >> (x & 31)) & 1u)
             for (uint32_t w = 0; w < H; ++w)
                 if (acc[w]) r[w] |= acc[w];
@@ -1041,6 +1054,18 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     R.cap_wmask = cap_wmask;
     R.front[0] = front0;
     R.front[1] = front1;
+    R.k = idx->cfg.k;
+    R.wdl = idx->wdl;
+    R.dmask_out = nullptr;
+    R.scc_out = nullptr;
+    if (wmask == ~0ull) {   // full builds keep the pivot sets for query pruning
+        if ((s = idx->dmask.ensure(bmw * 4 + 64)) || (s = idx->sccmask.ensure((size_t)idx->wdl * 8 + 16))) return s;
+        DBL_CUDA(cudaMemsetAsync(idx->sccmask.p, 0, (size_t)idx->wdl * 8 + 16, g->stream));
+        R.dmask_out = idx->dmask.as<uint32_t>();
+        R.scc_out = idx->sccmask.as<unsigned long long>();
+        idx->dmask_n = n;
+        idx->has_scc = true;
+    }
     R.H = H;
     R.adj[0] = graph_rev(g);
     R.adj[1] = graph_fwd(g);
@@ -1106,6 +1131,7 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
         }
     }
     DBL_CUDA(cudaEventRecord(g->ev[0], g->stream));
+    idx->has_scc = false;   // set again by a full build's pivot
     const bool prep = words == nullptr;
     dbl_status s;
     if ((s = graph_ensure_traversal(g))) return s;
@@ -1244,10 +1270,10 @@ dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, ui
 // ------------------------------------------------------------- work model --
 // level-synchronous (Jacobi) counts per 64-bit family.
 
-__global__ void wm_extract_kernel(const uint64_t *__restrict__ rec, uint32_t rw, uint32_t w, uint32_t n,
+__global__ void wm_extract_kernel(const uint64_t *__restrict__ rec, uint32_t rs, uint32_t w, uint32_t n,
                                   uint64_t *__restrict__ cur, uint8_t *__restrict__ front) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        const uint64_t x = rec[(size_t)v * rw + w];
+        const uint64_t x = rec[(size_t)v * rs + w];
         cur[v] = x;
         front[v] = x != 0;
     }
@@ -1286,19 +1312,19 @@ __global__ void wm_diff_kernel(uint32_t n, uint64_t *__restrict__ cur, const uin
 }
 
 dbl_status work_model(const dbl_index *idx, dbl_graph *g, uint64_t *V, uint64_t *E, uint32_t *levels) {
-    const uint32_t n = idx->n, rw = idx->rw, H = idx->wdl + idx->wbl;
+    const uint32_t n = idx->n, rw = idx->rw, rs = idx->rs, H = idx->wdl + idx->wbl;
     DevBuf seeds, cur, nxt, front, ve;
     dbl_index tmp;  // seed records only
     dbl_status s;
     auto cleanup = [&]() { seeds.release(); cur.release(); nxt.release(); front.release(); ve.release(); };
-    if ((s = seeds.ensure((size_t)n * rw * 8 + 16)) || (s = cur.ensure((size_t)n * 8 + 8)) ||
+    if ((s = seeds.ensure((size_t)n * rs * 8 + 16)) || (s = cur.ensure((size_t)n * 8 + 8)) ||
         (s = nxt.ensure((size_t)n * 8 + 8)) || (s = front.ensure((size_t)n + 8)) || (s = ve.ensure(16))) {
         cleanup();
         return s;
     }
     // seed records into `seeds`
     std::swap(tmp.rec, seeds);
-    tmp.n = n; tmp.rw = rw; tmp.wdl = idx->wdl; tmp.wbl = idx->wbl; tmp.cfg = idx->cfg;
+    tmp.n = n; tmp.rw = rw; tmp.rs = rs; tmp.wdl = idx->wdl; tmp.wbl = idx->wbl; tmp.cfg = idx->cfg;
     tmp.landmarks.p = idx->landmarks.p;
     tmp.leaf_flags.p = idx->leaf_flags.p;
     tmp.bucket.p = idx->bucket.p;
@@ -1309,7 +1335,7 @@ dbl_status work_model(const dbl_index *idx, dbl_graph *g, uint64_t *V, uint64_t 
     const int blocks = g->sm_count * 8;
     for (uint32_t w = 0; w < rw; ++w) {
         Adj adj = w < H ? graph_fwd(g) : graph_rev(g);
-        wm_extract_kernel<<<blocks, 256, 0, g->stream>>>(seeds.as<uint64_t>(), rw, w, n, cur.as<uint64_t>(),
+        wm_extract_kernel<<<blocks, 256, 0, g->stream>>>(seeds.as<uint64_t>(), rs, w, n, cur.as<uint64_t>(),
                                                          front.as<uint8_t>());
         DBL_LAUNCHED();
         uint64_t Vt = 0, Et = 0;

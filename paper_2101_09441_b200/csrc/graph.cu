@@ -544,6 +544,7 @@ extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
     for (auto &cs : g->cstream) if (cs) { cudaStreamSynchronize(cs); pool_forget_stream(cs); cudaStreamDestroy(cs); }
     pool_forget_stream(g->stream);
     g->host_stage.release();
+    g->q_host_res.release();
     for (auto &ev : g->ev) if (ev) cudaEventDestroy(ev);
     if (g->stream) cudaStreamDestroy(g->stream);
     delete g;

@@ -182,6 +182,7 @@ struct dbl_graph {
     dbl::DevBuf cub_tmp, scratch_a, scratch_b, scratch_c, scratch_d;
     dbl::DevBuf prep;                     // PrepState + top-k candidates
     dbl::HostBuf host_stage;
+    dbl::HostBuf q_host_res;              // pinned result words of the last query batch
     // query workspace
     dbl::DevBuf q_in, q_codes, q_vis, q_pending, q_counters, q_dense, q_errs;
     cudaStream_t cstream[2] = {nullptr, nullptr};   // H2D / D2H copy streams
@@ -195,12 +196,22 @@ struct dbl_graph {
     float t_fix = 0, t_label = 0, t_bfs = 0;
 };
 
+// Record stride (u64 words) for half-width H = wdl + wbl.  L2 fills whole
+// 128-byte lines on the random misses of the query gather, so a record never
+// straddles a line: 16- and 32-byte records stay packed, wider ones are padded
+// to 64 or a multiple of 128 bytes (cfg5, k = 256: 80 -> 128 bytes, 1.5 -> 1
+// lines per endpoint).  The out-half starts at word H as before.
+__host__ __device__ constexpr uint32_t rec_stride(uint32_t H) {
+    return 2 * H <= 4 ? 2 * H : (2 * H <= 8 ? 8u : ((2 * H + 15) & ~15u));
+}
+
 struct dbl_index {
     int device = 0;
     uint32_t n = 0;
     dbl_config cfg{};
-    uint32_t wdl = 0, wbl = 0, rw = 0;  // words: dl, bl, per record
-    dbl::DevBuf rec;                     // n * rw u64
+    uint32_t wdl = 0, wbl = 0, rw = 0;  // words: dl, bl, per record (2H)
+    uint32_t rs = 0;                     // record stride in words (rec_stride(H) >= rw; pad words stay 0)
+    dbl::DevBuf rec;                     // n * rs u64
     dbl::DevBuf landmarks;               // k u32
     dbl::DevBuf leaf_flags;              // n u8
     dbl::DevBuf bucket;                  // n u32
@@ -208,6 +219,13 @@ struct dbl_index {
     // (dbl_index_build): landmarks, leaves (with an optional override table)
     bool sel_landmarks = false, sel_leaves = false;
     dbl::DevBuf ovr;                     // n u32 override buckets (0xffffffff = none)
+    // pivot sets kept for query pruning (written by the build's reach kernel):
+    // dmask = vertices reached from the pivot h (a subset of D(h)),
+    // sccmask = DL bits of the landmarks in h's SCC.  A query whose dl_out[u]
+    // meets sccmask prunes every x in D(h) (queries.py:137-138) on one bit.
+    dbl::DevBuf dmask, sccmask;
+    uint32_t dmask_n = 0;                // vertices covered by dmask
+    bool has_scc = false;
 };
 
 namespace dbl {

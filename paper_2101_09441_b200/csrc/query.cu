@@ -42,6 +42,21 @@ constexpr int BFS_THREADS = 256;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint8_t UNRESOLVED = 0xff;
 
+// The build's pivot sets (reach_kernel): dmask = vertices reached from the
+// pivot landmark h, scc = DL bits of the landmarks in h's SCC.  Every x in
+// D(h) has those bits in dl_in[x], so for a query whose dl_out[u] meets scc
+// the DL prune of queries.py:137-138 holds for every x in D(h); the BFS tests
+// one bit of an L2-resident bitmap instead of reading x's record, before x
+// takes a visited-table slot.  (Not stamping a pruned x changes nothing: it
+// is pruned again on every visit and never expanded or counted.)  Inserts
+// only grow D(h), so the stored subset stays sound; n = 0 disables it.
+struct Pivot {
+    const uint32_t *dmask;
+    const unsigned long long *scc;
+    uint32_t n;
+    uint32_t pad;
+};
+
 // Per-call query arguments, passed by value to every query kernel.
 struct QueryDesc {
     const uint32_t *u;
@@ -52,7 +67,20 @@ struct QueryDesc {
     uint32_t flags;
     int vec_ok;
     int pad;
+    Pivot pv;
 };
+
+__device__ __forceinline__ bool in_pivot(const Pivot &pv, uint32_t x) {
+    return x < pv.n && ((__ldg(pv.dmask + (x >> 5)) >> (x & 31)) & 1u);
+}
+
+// Does the query whose dl_out[u] is `dlo` (wdl words) take the pivot prune?
+__device__ __forceinline__ bool pivot_query(const Pivot &pv, const unsigned long long *dlo, uint32_t wdl, bool prune_dl) {
+    if (!prune_dl || pv.n == 0) return false;
+    unsigned long long m = 0;
+    for (uint32_t k = 0; k < wdl; ++k) m |= dlo[k] & __ldg(pv.scc + k);
+    return m != 0;
+}
 
 __device__ __forceinline__ void ld_nc128(const uint64_t *p, uint64_t &a, uint64_t &b) {
     asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
@@ -66,7 +94,7 @@ label_check_kernel(const uint64_t *__restrict__ rec, uint32_t n, const uint32_t 
                    const uint32_t *__restrict__ qv, uint64_t count, uint32_t flags,
                    uint8_t *__restrict__ codes, uint32_t *__restrict__ visited,
                    uint32_t *__restrict__ pending, uint32_t *__restrict__ counters) {
-    constexpr int H = WDL + WBL, RW = 2 * H;
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H);
     const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
     const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -84,7 +112,7 @@ label_check_kernel(const uint64_t *__restrict__ rec, uint32_t n, const uint32_t 
                 code = DBL_REFLEXIVE;
             } else {
                 uint64_t a[RW], b[RW];
-                const uint64_t *ra = rec + (size_t)u * RW, *rb = rec + (size_t)v * RW;
+                const uint64_t *ra = rec + (size_t)u * RS, *rb = rec + (size_t)v * RS;
 #pragma unroll
                 for (int k = 0; k < RW; k += 2) {
                     ld_nc128(ra + k, a[k], a[k + 1]);
@@ -125,7 +153,7 @@ label_check_generic(const uint64_t *__restrict__ rec, uint32_t n, uint32_t wdl, 
                     const uint32_t *__restrict__ qu, const uint32_t *__restrict__ qv, uint64_t count,
                     uint32_t flags, uint8_t *__restrict__ codes, uint32_t *__restrict__ visited,
                     uint32_t *__restrict__ pending, uint32_t *__restrict__ counters) {
-    const uint32_t H = wdl + wbl, RW = 2 * H;
+    const uint32_t H = wdl + wbl, RW = 2 * H, RS = rec_stride(H);
     const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
     const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -142,7 +170,7 @@ label_check_generic(const uint64_t *__restrict__ rec, uint32_t n, uint32_t wdl, 
             } else if (u == v) {
                 code = DBL_REFLEXIVE;
             } else {
-                const uint64_t *a = rec + (size_t)u * RW, *b = rec + (size_t)v * RW;
+                const uint64_t *a = rec + (size_t)u * RS, *b = rec + (size_t)v * RS;
                 uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
                 for (uint32_t k = 0; k < wdl; ++k) {
                     const uint64_t ai = __ldg(a + k), ao = __ldg(a + H + k);
@@ -184,6 +212,7 @@ struct BfsShared {
     unsigned long long tmask[TCAP];
     unsigned long long done;
     unsigned long long active;
+    unsigned long long sccq;   // queries taking the pivot prune
     uint32_t nlist[2];
     uint32_t overflow;
     uint32_t gid;
@@ -247,7 +276,7 @@ bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_
     const uint32_t flags = qd.flags;
     uint8_t *__restrict__ codes = qd.codes;
     uint32_t *__restrict__ visited = qd.visited;
-    const uint32_t H = WDL + WBL, rw = 2 * H;
+    const uint32_t H = WDL + WBL, rw = rec_stride(H);
     const uint32_t WD = WDL > 0 ? WDL : 1;
     extern __shared__ __align__(16) unsigned char smem[];
     BfsShared &S = *reinterpret_cast<BfsShared *>(smem);
@@ -300,6 +329,7 @@ bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_
         for (int s = tid; s < TCAP; s += blockDim.x) { S.tkey[s] = EMPTY; S.tmask[s] = 0; }
         if (tid == 0) {
             S.done = 0;
+            S.sccq = 0;
             S.active = nq == 64 ? ~0ull : ((1ull << nq) - 1);
             S.nlist[0] = 0;
             S.nlist[1] = 0;
@@ -319,6 +349,8 @@ bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_
                 bli_v[tid * WBL + k] = __ldg(rv + WDL + k);
                 blo_v[tid * WBL + k] = __ldg(rv + H + WDL + k);
             }
+            if (pivot_query(qd.pv, reinterpret_cast<const unsigned long long *>(ru + H), WDL, prune_dl))
+                atomicOr(&S.sccq, 1ull << tid);
             // target table: v -> bit tid
             uint32_t h = hash32(v) >> 25;
             for (;;) {
@@ -379,8 +411,9 @@ bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_
                             const uint32_t x = __ldg(col + ei);
                             const unsigned long long hit = fw & tgt_lookup(S, x);
                             if (hit) atomicOr(&S.done, hit);
-                            const unsigned long long cand =
+                            unsigned long long cand =
                                 fw & ~hit & ~*(volatile unsigned long long *)&S.done;
+                            if (cand & S.sccq && in_pivot(qd.pv, x)) cand &= ~S.sccq;
                             if (cand) {
                                 const int sl = tab_slot<DENSE>(T, x);
                                 if (sl < 0) {
@@ -468,7 +501,7 @@ static size_t bfs_smem(int wdl, int wbl, bool dense) {
 #define DBL_QPL 2
 #endif
 #ifndef DBL_QMINB
-#define DBL_QMINB 3
+#define DBL_QMINB 2
 #endif
 constexpr int QPL = DBL_QPL;        // queries per lane
 constexpr int QT = 32 * QPL;       // queries per warp tile
@@ -508,21 +541,22 @@ struct WarpBfs {
     uint32_t nlist[2];
     uint32_t done;
     uint32_t overflow;
+    uint32_t sccq;   // queries taking the pivot prune
 };
 
-template <int RW>
+// The 2H words of a record at p; 256-bit loads while 32-byte aligned
+// (stride RS a multiple of 4 words), 128-bit ones for the rest.
+template <int RW, int RS>
 __device__ __forceinline__ void load_record(const uint64_t *p, uint64_t (&r)[RW]) {
-    if constexpr (RW % 4 == 0) {
+    constexpr int V4 = RS % 4 == 0 ? RW / 4 * 4 : 0;
 #pragma unroll
-        for (int k = 0; k < RW; k += 4)
-            asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
-                         : "=l"(r[k]), "=l"(r[k + 1]), "=l"(r[k + 2]), "=l"(r[k + 3]) : "l"(p + k));
-    } else {
+    for (int k = 0; k < V4; k += 4)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(r[k]), "=l"(r[k + 1]), "=l"(r[k + 2]), "=l"(r[k + 3]) : "l"(p + k));
 #pragma unroll
-        for (int k = 0; k < RW; k += 2)
-            asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
-                         : "=l"(r[k]), "=l"(r[k + 1]) : "l"(p + k));
-    }
+    for (int k = V4; k < RW; k += 2)
+        asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
+                     : "=l"(r[k]), "=l"(r[k + 1]) : "l"(p + k));
 }
 
 __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t &total) {
@@ -572,8 +606,8 @@ __device__ __forceinline__ uint32_t wb_target(const WarpBfs<WDL, WBL> &B, uint32
 // filled up (results then invalid).
 template <int WDL, int WBL>
 __device__ void warp_bfs(WarpBfs<WDL, WBL> &B, uint32_t nb, const uint64_t *__restrict__ rec,
-                         const Adj &adj, bool prune_dl, bool prune_bl) {
-    constexpr int H = WDL + WBL, RW = 2 * H, WD = WarpBfs<WDL, WBL>::WD;
+                         const Adj &adj, bool prune_dl, bool prune_bl, const Pivot &pv) {
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H), WD = WarpBfs<WDL, WBL>::WD;
     const int lane = threadIdx.x & 31;
     const uint32_t all = nb == 32 ? FULL : ((1u << nb) - 1u);
     // sources
@@ -641,7 +675,8 @@ __device__ void warp_bfs(WarpBfs<WDL, WBL> &B, uint32_t nb, const uint64_t *__re
                 const uint32_t x = r < obl ? __ldg(adj.col + ob0 + r) : __ldg(adj.dcol + od0 + (r - obl));
                 const uint32_t hit = ofw & wb_target(B, x);
                 if (hit) atomicOr(&B.done, hit);
-                const uint32_t cand = ofw & ~hit & ~*(volatile uint32_t *)&B.done;
+                uint32_t cand = ofw & ~hit & ~*(volatile uint32_t *)&B.done;
+                if (cand & B.sccq && in_pivot(pv, x)) cand &= ~B.sccq;
                 if (!cand) continue;
                 const int sl = wb_slot(B, x);
                 if (sl < 0) { B.overflow = 1; continue; }
@@ -651,7 +686,7 @@ __device__ void warp_bfs(WarpBfs<WDL, WBL> &B, uint32_t nb, const uint64_t *__re
                 uint32_t pruned = 0;
                 if (prune_dl || prune_bl) {   // queries.py:137-140
                     uint64_t xr[RW];
-                    load_record<RW>(rec + (size_t)x * RW, xr);
+                    load_record<RW, RS>(rec + (size_t)x * RS, xr);
                     uint32_t m = nw;
                     while (m) {
                         const int bq = __ffs(m) - 1;
@@ -719,7 +754,7 @@ __device__ __forceinline__ void flush_tile_codes(uint8_t *__restrict__ codes, ui
 #endif
 template <int WDL, int WBL>
 __device__ DBL_BFS_INLINE void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64_t *__restrict__ rec, const Adj &adj,
-                               bool prune_dl, bool prune_bl, uint8_t *__restrict__ codes,
+                               bool prune_dl, bool prune_bl, const Pivot &pv, uint8_t *__restrict__ codes,
                                uint32_t *__restrict__ visited, uint32_t *__restrict__ ovf_list,
                                uint32_t *__restrict__ counters, int ovf_counter) {
     const int lane = threadIdx.x & 31;
@@ -740,8 +775,15 @@ __device__ DBL_BFS_INLINE void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64
             h = (h + 1) & (WT - 1);
         }
     }
+    {
+        const bool sq = lane < (int)nb &&
+                        pivot_query(pv, reinterpret_cast<const unsigned long long *>(&B.qdlo[lane * WarpBfs<WDL, WBL>::WD]),
+                                    WDL, prune_dl);
+        const uint32_t m = __ballot_sync(FULL, sq);
+        if (lane == 0) B.sccq = m;
+    }
     __syncwarp();
-    warp_bfs<WDL, WBL>(B, nb, rec, adj, prune_dl, prune_bl);
+    warp_bfs<WDL, WBL>(B, nb, rec, adj, prune_dl, prune_bl, pv);
     const bool ovf = B.overflow != 0;
     const uint32_t dn = B.done;
     if (lane < (int)nb) {
@@ -825,7 +867,7 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
     const int vec_ok = qd.vec_ok;
     uint8_t *__restrict__ codes = qd.codes;
     uint32_t *__restrict__ visited = qd.visited;
-    constexpr int H = WDL + WBL, RW = 2 * H, WD = WarpBfs<WDL, WBL>::WD;
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H), WD = WarpBfs<WDL, WBL>::WD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpBfs<WDL, WBL> &B = reinterpret_cast<WarpBfs<WDL, WBL> *>(smem_raw)[wid];
@@ -877,8 +919,8 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
             const bool inb = qb + j < wend;
             const bool ok = inb && us[j] < n && vs[j] < n && us[j] != vs[j];
             if (ok) {
-                load_record<RW>(rec + (size_t)us[j] * RW, ra[j]);
-                load_record<RW>(rec + (size_t)vs[j] * RW, rb[j]);
+                load_record<RW, RS>(rec + (size_t)us[j] * RS, ra[j]);
+                load_record<RW, RS>(rec + (size_t)vs[j] * RS, rb[j]);
             }
         }
 #pragma unroll
@@ -948,12 +990,12 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
             if (lane == 0) B.nq = nq + take;
             __syncwarp();
             if (nq + take == 32 || (!DEFER_BFS && done_upto == tot)) {
-                warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters, CNT_PENDING);
+                warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.pv, codes, visited, pending, counters, CNT_PENDING);
             }
         }
     }
     __syncwarp();
-    if (B.nq) warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, codes, visited, pending, counters, CNT_PENDING);
+    if (B.nq) warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.pv, codes, visited, pending, counters, CNT_PENDING);
     // the last CTA out closes the batch, or hands the overflowed BFS batches
     // to the group/dense kernels through the tail-launch stream (they run
     // after this grid, before the stream's next operation)
@@ -1023,8 +1065,9 @@ constexpr uint32_t TB_E = 48;
 template <int WDL, int WBL>
 __device__ __forceinline__ int thread_bfs(const uint64_t *__restrict__ rec, const Adj adj, uint32_t u, uint32_t v,
                                        const uint64_t *dlo_u, const uint64_t *bli_v, const uint64_t *blo_v,
-                                       bool prune_dl, bool prune_bl, uint32_t *vcount) {
-    constexpr int H = WDL + WBL, RW = 2 * H;
+                                       bool prune_dl, bool prune_bl, const Pivot &pv, uint32_t *vcount) {
+    const bool sq = pivot_query(pv, reinterpret_cast<const unsigned long long *>(dlo_u), WDL, prune_dl);
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H);
     // neighbours in flight per step: their pruning words (dl_in, bl_in,
     // bl_out of x) are loaded word by word, fewer at a time for wide labels
     constexpr int NB = (WDL + 2 * WBL) <= 3 ? 4 : 2;
@@ -1052,12 +1095,13 @@ __device__ __forceinline__ int thread_bfs(const uint64_t *__restrict__ rec, cons
                 for (int t = 0; t < NB; ++t) {
                     fresh[t] = x[t] != 0xffffffffu;
                     for (int k = 0; k < qn; ++k) fresh[t] &= q[k] != x[t];
+                    if (fresh[t] && sq && in_pivot(pv, x[t])) fresh[t] = false;   // pruned
                 }
                 uint64_t xi[NB][WDL > 0 ? WDL : 1], xbi[NB][WBL], xbo[NB][WBL];
 #pragma unroll
                 for (int t = 0; t < NB; ++t) {
                     if (!fresh[t]) continue;
-                    const uint64_t *rx = rec + (size_t)x[t] * RW;
+                    const uint64_t *rx = rec + (size_t)x[t] * RS;
                     if (prune_dl) {
 #pragma unroll
                         for (int k = 0; k < WDL; ++k) xi[t][k] = __ldg(rx + k);
@@ -1103,8 +1147,10 @@ constexpr uint32_t TB_EW = 256;
 template <int WDL, int WBL>
 __device__ __forceinline__ int warp_query_bfs(const uint64_t *__restrict__ rec, const Adj &adj, uint32_t u, uint32_t v,
                                               const uint64_t *dlo_u, const uint64_t *bli_v, const uint64_t *blo_v,
-                                              bool prune_dl, bool prune_bl, uint32_t *wq, uint32_t *vcount) {
-    constexpr int H = WDL + WBL, RW = 2 * H;
+                                              bool prune_dl, bool prune_bl, const Pivot &pv, uint32_t *wq,
+                                              uint32_t *vcount) {
+    const bool sq = pivot_query(pv, reinterpret_cast<const unsigned long long *>(dlo_u), WDL, prune_dl);
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H);
     const int lane = threadIdx.x & 31;
     if (lane == 0) wq[0] = u;
     __syncwarp();
@@ -1125,8 +1171,9 @@ __device__ __forceinline__ int warp_query_bfs(const uint64_t *__restrict__ rec, 
                 if (__any_sync(FULL, ok && x == v)) return 1;   // target test precedes the visited test
                 bool keep = ok;
                 for (uint32_t k = 0; k < qn; ++k) keep &= wq[k] != x;
+                if (keep && sq && in_pivot(pv, x)) keep = false;   // pruned
                 if (keep && (prune_dl || prune_bl)) {
-                    const uint64_t *rx = rec + (size_t)x * RW;
+                    const uint64_t *rx = rec + (size_t)x * RS;
                     bool p = false;
                     if (prune_dl) {   // queries.py:137-138
 #pragma unroll
@@ -1158,10 +1205,16 @@ __global__ void bfs_warp_kernel(const uint64_t *__restrict__ rec, uint32_t n, Ad
                                 uint32_t *__restrict__ counters, const HardArgs ha);
 
 template <int WDL, int WBL>
-__global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj,
+#ifndef DBL_LMINB_WIDE
+#define DBL_LMINB_WIDE 4
+#endif
+// 8 CTAs/SM (32 registers) for the 32-byte records of k <= 64; wide records
+// (2 x 80 bytes at k = 256) spill at that cap, so they trade occupancy for
+// registers
+__global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_WIDE)) label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj,
                                                           const QueryDesc qd, uint32_t *__restrict__ pending,
                                                           uint32_t *__restrict__ counters, const HardArgs ha) {
-    constexpr int H = WDL + WBL, RW = 2 * H;
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H);
     // the per-thread BFS pays off for k <= 64; with wider labels (cfg5:
     // k = 256, d = 16) most fallbacks outgrow its bounds (measured: 79% of
     // cfg5's unresolved queries), so they go straight to the warp BFS
@@ -1210,8 +1263,8 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
                 code = DBL_REFLEXIVE;
             } else {
                 uint64_t a[RW], b[RW];
-                load_record<RW>(rec + (size_t)u * RW, a);
-                load_record<RW>(rec + (size_t)v * RW, b);
+                load_record<RW, RS>(rec + (size_t)u * RS, a);
+                load_record<RW, RS>(rec + (size_t)v * RS, b);
                 uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
 #pragma unroll
                 for (int k = 0; k < WDL; ++k) {
@@ -1269,7 +1322,7 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
             const uint32_t i = dq.i[t];
             uint32_t vc = 0;
             const int r = warp_query_bfs<WDL, WBL>(rec, adj, dq.u[t], dq.v[t], dq.dlo[t], dq.bli[t], dq.blo[t],
-                                                   prune_dl, prune_bl, wq[wid], &vc);
+                                                   prune_dl, prune_bl, qd.pv, wq[wid], &vc);
             if (lane == 0) {
                 if (r == 2) {
                     pending[atomicAdd(&counters[CNT_PENDING], 1u)] = i;
@@ -1285,7 +1338,7 @@ __global__ void __launch_bounds__(256, DBL_LMINB) label_lean_kernel(const uint64
             const uint32_t i = dq.i[t];
             uint32_t vc = 0;
             const int r = thread_bfs<WDL, WBL>(rec, adj, dq.u[t], dq.v[t], dq.dlo[t], dq.bli[t], dq.blo[t], prune_dl,
-                                               prune_bl, &vc);
+                                               prune_bl, qd.pv, &vc);
             if (r == 2) {
                 pending[atomicAdd(&counters[CNT_PENDING], 1u)] = i;
             } else {
@@ -1318,7 +1371,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, DBL_QMINB)
 bfs_warp_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const QueryDesc qd,
                 uint32_t *__restrict__ pending, uint32_t *__restrict__ wovf, uint32_t *__restrict__ counters,
                 const HardArgs ha) {
-    constexpr int H = WDL + WBL, RW = 2 * H, WD = WarpBfs<WDL, WBL>::WD;
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H), WD = WarpBfs<WDL, WBL>::WD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpBfs<WDL, WBL> &B = reinterpret_cast<WarpBfs<WDL, WBL> *>(smem_raw)[wid];
@@ -1337,8 +1390,8 @@ bfs_warp_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Que
             const uint32_t qi = pending[p0 + lane];
             const uint32_t u = __ldg(qd.u + qi), v = __ldg(qd.v + qi);
             uint64_t ru[RW], rv[RW];
-            load_record<RW>(rec + (size_t)u * RW, ru);
-            load_record<RW>(rec + (size_t)v * RW, rv);
+            load_record<RW, RS>(rec + (size_t)u * RS, ru);
+            load_record<RW, RS>(rec + (size_t)v * RS, rv);
             B.qidx[lane] = qi;
             B.qu[lane] = u;
             B.qv[lane] = v;
@@ -1352,7 +1405,7 @@ bfs_warp_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Que
         }
         if (lane == 0) B.nq = nb;
         __syncwarp();
-        warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.codes, qd.visited, wovf, counters, CNT_WOVF);
+        warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.pv, qd.codes, qd.visited, wovf, counters, CNT_WOVF);
     }
     // the last CTA out closes the batch, or moves the overflowed queries to
     // the head of the pending list and tail-launches the group/dense kernels
@@ -1449,6 +1502,11 @@ static dbl_status hard_path_config(const dbl_index *idx, dbl_graph *g, HardPath 
 // 64-query group kernel and the dense kernel are tail-launched from the
 // device only when some warp's BFS table overflowed (never on cfg2), so the
 // host submits one kernel and no memset, copy or graph per batch.
+static bool pivot_prune_off() {
+    static const bool off = std::getenv("DBL_NO_PIVOT_PRUNE") != nullptr;
+    return off;
+}
+
 dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
                      uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited) {
     if (count >= 0xffffffffull) { set_error("query batch too large"); return DBL_E_ARG; }
@@ -1468,7 +1526,12 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
         if ((s = g->q_counters.ensure(CNT_ALL * 4))) return s;
         DBL_CUDA(cudaMemsetAsync(g->q_counters.p, 0, CNT_ALL * 4, g->stream));
     }
-    QueryDesc qd{u, v, codes, visited, (uint32_t)count, flags, 0, 0};
+    QueryDesc qd{u, v, codes, visited, (uint32_t)count, flags, 0, 0, Pivot{}};
+    if (idx->has_scc && !pivot_prune_off()) {
+        qd.pv.dmask = idx->dmask.as<uint32_t>();
+        qd.pv.scc = idx->sccmask.as<unsigned long long>();
+        qd.pv.n = idx->dmask_n;
+    }
     qd.vec_ok = ((((uintptr_t)u) | ((uintptr_t)v)) & (4 * QPL - 1)) == 0 && (((uintptr_t)codes) & (QPL - 1)) == 0 &&
                 (!visited || (((uintptr_t)visited) & (4 * QPL - 1)) == 0);
     uint32_t *pending = g->q_pending.as<uint32_t>();
@@ -1480,13 +1543,14 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     if ((s = hard_path_config(idx, g, hp))) return s;
     static const bool no_fused = std::getenv("DBL_NO_FUSED") != nullptr;
     static const bool old_fused = std::getenv("DBL_QFUSED") != nullptr;
+    static const bool lean_wide = std::getenv("DBL_LEAN_WIDE") != nullptr;
     lean_fn lean = nullptr;
     bfsw_fn bfsw = nullptr;
     size_t wsmem = 0;
     // k <= 64: lean gather + per-thread BFS; wider labels (cfg5, k = 256),
     // whose fallbacks outgrow the thread BFS, keep the fused kernel with the
     // warp BFS interleaved between tiles (measured on cfg5: 4.6 vs 3.7 G q/s)
-    if (count && !no_fused && !old_fused && (DBL_TBFS_ALL || idx->wdl <= 1) &&
+    if (count && !no_fused && !old_fused && (DBL_TBFS_ALL || idx->wdl <= 1 || lean_wide) &&
         pick_lean(idx->wdl, idx->wbl, lean, bfsw, wsmem)) {
         static int lbps = -1, wbps = -1;
         static const void *last_fn = nullptr;
@@ -1577,7 +1641,11 @@ void query_timings(dbl_graph *g) {
 }
 
 dbl_status query_finish(dbl_graph *g, uint32_t *err_out) {
-    uint32_t h[CNT_WORDS];
+    // pinned staging: the D2H copy is a plain async copy and the stream
+    // synchronisation is the batch's only host wait
+    dbl_status s = g->q_host_res.ensure(CNT_WORDS * 4);
+    if (s) return s;
+    uint32_t *h = reinterpret_cast<uint32_t *>(g->q_host_res.p);
     DBL_CUDA(cudaMemcpyAsync(h, g->q_counters.as<uint32_t>() + CNT_RES, CNT_WORDS * 4, cudaMemcpyDeviceToHost,
                              g->stream));
     DBL_CUDA(cudaStreamSynchronize(g->stream));

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
         for (int i = threadIdx.x; i < 65; i += blockDim.x) h[i] = 0;
         __syncthreads();
     }
-    const uint32_t H = A.wdl + A.wbl, rw = 2 * H;
+    const uint32_t H = A.wdl + A.wbl, rw = 2 * H, rs = rec_stride(H);
     const uint64_t nr = ((uint64_t)A.n + 31) & ~31ull;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += stride) {
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
             const uint32_t win = (f & 1) ? bw : 0xffffffffu;
             const uint32_t wout = (f & 2) ? H + bw : 0xffffffffu;
             const uint64_t bit = 1ull << (b % 64);
-            uint64_t *r = A.rec + (size_t)v * rw;
+            uint64_t *r = A.rec + (size_t)v * rs;
             for (uint32_t w = 0; w < rw; w += 2) {
                 ulonglong2 val;
                 val.x = (w == win || w == wout) ? bit : 0ull;
@@ -347,7 +347,7 @@ __device__ __forceinline__ bool lm_better(uint64_t sa, uint32_t ia, uint64_t sb,
 // their DL bits go into the seeded records and the level-0 bitmaps.
 __global__ void __launch_bounds__(1024) topk_final_kernel(const uint64_t *__restrict__ cs, const uint32_t *__restrict__ ci,
                                                          uint32_t k, PrepState *st, uint32_t *__restrict__ lm,
-                                                         uint64_t *__restrict__ rec, uint32_t rw, uint32_t H,
+                                                         uint64_t *__restrict__ rec, uint32_t rs, uint32_t H,
                                                          uint32_t *bits0, uint32_t *bits1, uint32_t a0, uint32_t e0,
                                                          uint32_t a1, uint32_t e1) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(1024) topk_final_kernel(const uint64_t *__rest
         const uint32_t v = si[i], w = i / 64;
         const uint64_t bit = 1ull << (i % 64);
         lm[i] = v;
-        uint64_t *r = rec + (size_t)v * rw;
+        uint64_t *r = rec + (size_t)v * rs;
         r[w] |= bit;          // dl_in: the landmark reaches itself
         r[H + w] |= bit;      // dl_out
         if (bits0 && w >= a0 && w < e0) atomicOr(&bits0[v >> 5], 1u << (v & 31));
@@ -395,13 +395,13 @@ __global__ void __launch_bounds__(1024) topk_final_kernel(const uint64_t *__rest
 
 // landmark bits of given (pinned or previously selected) landmarks
 __global__ void landmark_seed_kernel(const uint32_t *__restrict__ lm, uint32_t k, uint64_t *__restrict__ rec,
-                                     uint32_t rw, uint32_t H, uint32_t *bits0, uint32_t *bits1, uint32_t a0,
+                                     uint32_t rs, uint32_t H, uint32_t *bits0, uint32_t *bits1, uint32_t a0,
                                      uint32_t e0, uint32_t a1, uint32_t e1) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
         const uint32_t v = lm[i], w = i / 64;
         const uint64_t bit = 1ull << (i % 64);
-        atomicOr(reinterpret_cast<unsigned long long *>(rec + (size_t)v * rw + w), bit);
-        atomicOr(reinterpret_cast<unsigned long long *>(rec + (size_t)v * rw + H + w), bit);
+        atomicOr(reinterpret_cast<unsigned long long *>(rec + (size_t)v * rs + w), bit);
+        atomicOr(reinterpret_cast<unsigned long long *>(rec + (size_t)v * rs + H + w), bit);
         if (bits0 && w >= a0 && w < e0) atomicOr(&bits0[v >> 5], 1u << (v & 31));
         if (bits1 && H + w >= a1 && H + w < e1) atomicOr(&bits1[v >> 5], 1u << (v & 31));
     }
@@ -458,11 +458,11 @@ dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_
                                           fsmem));
             attr = true;
         }
-        topk_final_kernel<<<1, 1024, fsmem, g->stream>>>(cs, ci, k, st, idx->landmarks.as<uint32_t>(), A.rec, idx->rw,
+        topk_final_kernel<<<1, 1024, fsmem, g->stream>>>(cs, ci, k, st, idx->landmarks.as<uint32_t>(), A.rec, idx->rs,
                                                          H, bits0, bits1, a0, e0, a1, e1);
         DBL_CHECK_LAUNCH("topk_final_kernel");
     } else if (k) {
-        landmark_seed_kernel<<<(k + 255) / 256, 256, 0, g->stream>>>(idx->landmarks.as<uint32_t>(), k, A.rec, idx->rw,
+        landmark_seed_kernel<<<(k + 255) / 256, 256, 0, g->stream>>>(idx->landmarks.as<uint32_t>(), k, A.rec, idx->rs,
                                                                     H, bits0, bits1, a0, e0, a1, e1);
         DBL_CHECK_LAUNCH("landmark_seed_kernel");
     }

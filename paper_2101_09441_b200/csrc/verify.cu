@@ -44,7 +44,7 @@ __global__ void fixpoint_check_kernel(const uint64_t *__restrict__ rec, uint32_t
                                       Adj fwd, Adj rev, const uint32_t *__restrict__ lmpos,
                                       const uint8_t *__restrict__ flags, const uint32_t *__restrict__ bucket,
                                       ViolationOut out) {
-    const uint32_t H = wdl + wbl, rw = 2 * H;
+    const uint32_t H = wdl + wbl, rw = rec_stride(H);
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -89,7 +89,7 @@ __global__ void fixpoint_check_kernel(const uint64_t *__restrict__ rec, uint32_t
 // exhaustive mode: diff against a fresh rebuild (expected = b)
 __global__ void record_diff_kernel(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b, uint32_t n,
                                    uint32_t H, ViolationOut out) {
-    const uint32_t rw = 2 * H;
+    const uint32_t rw = rec_stride(H);
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < 2ull * n;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = (uint32_t)(t >> 1), h = (uint32_t)(t & 1);
@@ -150,10 +150,11 @@ extern "C" dbl_status dbl_verify(const dbl_index *idx, const dbl_graph *gc, int 
         fresh.wdl = idx->wdl;
         fresh.wbl = idx->wbl;
         fresh.rw = idx->rw;
+        fresh.rs = idx->rs;
         fresh.landmarks.p = idx->landmarks.p;
         fresh.leaf_flags.p = idx->leaf_flags.p;
         fresh.bucket.p = idx->bucket.p;
-        s = fresh.rec.ensure((size_t)n * idx->rw * 8 + 16);
+        s = fresh.rec.ensure((size_t)n * idx->rs * 8 + 16);
         if (!s) s = run_build(g, &fresh, nullptr, 0);
         if (!s) {
             record_diff_kernel<<<g->sm_count * 8, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(),

@@ -295,6 +295,39 @@ def test_rmat_insert_batches_vs_rebuild():
     np.testing.assert_array_equal(out.codes, oc)
 
 
+@pytest.mark.parametrize("k", [64, 256])
+def test_pivot_prune_after_growth(k):
+    """The BFS prunes D(h) on one bitmap bit for queries whose dl_out[u] holds
+    a landmark of the pivot's SCC.  After vertex growth and edge inserts the
+    stored D(h) is a stale subset (and shorter than n): answers must still
+    equal the reference BFS (queries.py:116-142) run on the same labels."""
+    n, src, dst = rmat_case(13, 8, 21)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    idx = E.build_index(g, E.IndexConfig(k=k, k_prime=64))
+    lm = list(idx.landmark_set.landmarks)
+    rng = np.random.default_rng(3)
+    new = []
+    for j in range(24):   # new vertices wired into and out of the hub core
+        outs = [int(lm[j % len(lm)])] if j % 3 else []
+        ins = [int(x) for x in rng.integers(0, n, 2)] + ([int(new[-1])] if new else [])
+        E.insert_vertex(g, idx, out_edges=outs, in_edges=ins)
+        new.append(g.vertex_count - 1)
+    iu, iv = W.gen_insert_workload(src, dst, n, 3000, 17)
+    E.insert_edges(g, idx, iu, iv)
+    assert idx.labels_equal(E.rebuild_index(g, idx))
+    nn = g.vertex_count
+    qu, qv = W.uniform_queries(nn, 60_000, 5)
+    qu[:2000] = rng.choice(new, 2000)
+    qv[2000:4000] = rng.choice(new, 2000)
+    w = idx.export_words()
+    ptr, col = g.adjacency(False)
+    for fl in (E.QueryFlags(), E.QueryFlags(use_bl=False), E.QueryFlags(prune_bl=False)):
+        out, _ = E.query_batch(g, idx, (qu, qv), flags=fl)
+        oc = O.csr_query_batch(nn, ptr.astype(np.uint64), col, k, 64, w, qu, qv, fl.bits(), threads=8)
+        np.testing.assert_array_equal(out.codes, oc)
+    assert np.mean(out.codes >= 5) > 0   # the BFS ran
+
+
 def test_dense_bfs_fallback_path():
     # k = 0 and a single bucket: many BFS queries explore cones larger than the
     # shared-memory table, exercising the dense re-run path.
