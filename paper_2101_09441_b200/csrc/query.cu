@@ -1019,6 +1019,166 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
     }
 }
 
+// ------------------------------------------------- K6 wide: quad gathers --
+//
+// Records wider than 32 bytes (k > 64) live at 64/128-byte strides.  Random
+// gathers that miss L2 are bound by L1->L2 requests, not bytes (measured with
+// tools/ubench_gather: ~37 G requests/s whether a request carries one sector
+// or a whole 128-byte line), and a thread reading its own 80-byte record
+// issues three requests (32 + 32 + 16 bytes).  Here a lane quad reads one
+// record: lane j of the quad loads 32-byte chunk j, so one warp instruction
+// fetches 8 records with one request per record.  A warp tile is 32 queries
+// gathered in 4 rounds of 8 (u and v chunks, all 8 loads in flight), the
+// rules are evaluated inside each quad (the dl_out words a lane needs come
+// from the quad lane holding them, by shuffle; the BL words of u and v sit in
+// the same lane), and the codes move to lane 8r + i.  Unresolved queries are
+// staged for the warp's bit-parallel BFS straight from the lanes holding the
+// words, as in query_fused_kernel.
+__device__ __forceinline__ uint64_t shfl64(uint64_t x, int src) {
+    const uint32_t lo = __shfl_sync(FULL, (uint32_t)x, src), hi = __shfl_sync(FULL, (uint32_t)(x >> 32), src);
+    return ((uint64_t)hi << 32) | lo;
+}
+
+template <int WDL, int WBL>
+__global__ void __launch_bounds__(FUSED_THREADS, DBL_QMINB)
+query_quad_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const QueryDesc qd,
+                  uint32_t *__restrict__ pending, uint32_t *__restrict__ counters, const HardArgs ha) {
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H), WD = WarpBfs<WDL, WBL>::WD;
+    constexpr int C = (RW + 3) / 4;   // 32-byte chunks per record
+    static_assert(RS % 4 == 0 && C <= 4, "quad gather: 32-byte aligned records of at most 128 bytes");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int qi = lane >> 2, qj = lane & 3, qbase = lane & ~3;
+    WarpBfs<WDL, WBL> &B = reinterpret_cast<WarpBfs<WDL, WBL> *>(smem_raw)[wid];
+    const uint32_t count = qd.count, flags = qd.flags;
+    const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
+    const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
+    const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
+    for (;;) {
+        uint32_t tile = 0;
+        if (lane == 0) tile = atomicAdd(&counters[CNT_TILE], 1u);
+        tile = __shfl_sync(FULL, tile, 0);
+        const uint64_t q0 = (uint64_t)tile * 32;
+        if (q0 >= count) break;
+        const uint64_t q = q0 + lane;
+        const bool inb = q < count;
+        uint32_t u = 0, v = 0;
+        if (inb) { u = __ldg(qd.u + q); v = __ldg(qd.v + q); }
+        const bool bad = inb && (u >= n || v >= n);
+        const bool live = inb && !bad && u != v;
+        // gather: round r, quad i -> query 8r + i, lane j -> chunk j
+        uint64_t cu[4][4], cv[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int src = 8 * r + qi;
+            const uint32_t su = __shfl_sync(FULL, u, src), sv = __shfl_sync(FULL, v, src);
+            const bool sl = __shfl_sync(FULL, (int)live, src) != 0;
+            if (sl && qj < C) {
+                const uint64_t *pu = rec + (size_t)su * RS + 4 * qj, *pv = rec + (size_t)sv * RS + 4 * qj;
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                             : "=l"(cu[r][0]), "=l"(cu[r][1]), "=l"(cu[r][2]), "=l"(cu[r][3]) : "l"(pu));
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                             : "=l"(cv[r][0]), "=l"(cv[r][1]), "=l"(cv[r][2]), "=l"(cv[r][3]) : "l"(pv));
+            } else {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) cu[r][t] = cv[r][t] = 0;
+            }
+        }
+        // rules 1-4 per quad (queries.py:96-114); lane j holds record words 4j..4j+3
+        uint32_t mycode = UNRESOLVED;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int w = 4 * qj + t;
+                if (WDL > 0) {
+                    // out-half DL word k = w is record word H + k: quad lane (H + w) / 4, slot (H + t) % 4
+                    const int srcl = (qbase + ((H + 4 * qj + t) >> 2)) & 31;
+                    const uint64_t ou = shfl64(cu[r][(H + t) & 3], srcl), ov = shfl64(cv[r][(H + t) & 3], srcl);
+                    if (w < WDL) {
+                        r1 |= ou & cv[r][t];                               // dl_out[u] & dl_in[v]
+                        r3 |= ov & cu[r][t];                               // dl_out[v] & dl_in[u]
+                        r4 |= (ou & cu[r][t]) | (ov & cv[r][t]);           // Theorem 2
+                    }
+                }
+                if (w >= WDL && w < H) r2 |= cu[r][t] & ~cv[r][t];         // bl_in[u] \ bl_in[v]
+                if (w >= H + WDL && w < RW) r2 |= cv[r][t] & ~cu[r][t];    // bl_out[v] \ bl_out[u]
+            }
+            uint32_t bits = (r1 != 0) | ((r2 != 0) << 1) | ((r3 != 0) << 2) | ((r4 != 0) << 3);
+            bits |= __shfl_xor_sync(FULL, bits, 1);
+            bits |= __shfl_xor_sync(FULL, bits, 2);
+            uint32_t c = UNRESOLVED;
+            if (use_dl && (bits & 1)) c = DBL_DL_POSITIVE;
+            else if (use_bl && (bits & 2)) c = DBL_BL_NEGATIVE;
+            else if (thm1 && (bits & 4)) c = DBL_THM1_NEGATIVE;
+            else if (thm2 && (bits & 8)) c = DBL_THM2_NEGATIVE;
+            const uint32_t cc = __shfl_sync(FULL, c, (lane & 7) << 2);
+            if ((lane >> 3) == r) mycode = cc;
+        }
+        uint32_t code = mycode;
+        if (bad) {
+            atomicOr(&counters[CNT_ERR], 1u);
+            code = 0xfe;
+        } else if (inb && u == v) {
+            code = DBL_REFLEXIVE;
+        }
+        const bool unres = live && code == UNRESOLVED;
+        if (inb && !unres) {
+            qd.codes[q] = (uint8_t)code;
+            if (qd.visited) qd.visited[q] = 0;
+        }
+        const uint32_t mask = __ballot_sync(FULL, unres);
+        if (mask) {
+            // stage the unresolved queries (<= 32) and answer them right away
+            if (unres) {
+                const uint32_t slot = __popc(mask & ((1u << lane) - 1u));
+                B.qidx[slot] = (uint32_t)q;
+                B.qu[slot] = u;
+                B.qv[slot] = v;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int lq = 8 * r + qi;
+                if (!((mask >> lq) & 1u)) continue;
+                const uint32_t slot = __popc(mask & ((1u << lq) - 1u));
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int w = 4 * qj + t;
+                    if (w >= H && w < H + WDL) B.qdlo[slot * WD + (w - H)] = cu[r][t];
+                    if (w >= WDL && w < H) B.qbli[slot * WBL + (w - WDL)] = cv[r][t];
+                    if (w >= H + WDL && w < RW) B.qblo[slot * WBL + (w - H - WDL)] = cv[r][t];
+                }
+            }
+            if (lane == 0) B.nq = __popc(mask);
+            __syncwarp();
+            warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.pv, qd.codes, qd.visited, pending, counters,
+                                     CNT_PENDING);
+            __syncwarp();
+        }
+    }
+    // the last CTA out closes the batch, or tail-launches the group/dense
+    // kernels for BFS batches that outgrew the warp tables
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(&counters[CNT_DONE], 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence();
+            const uint32_t npend = *(volatile uint32_t *)&counters[CNT_PENDING];
+            if (npend == 0) {
+                close_batch(counters);
+            } else {
+                bfs_kernel<false><<<ha.grid, BFS_THREADS, ha.smem, cudaStreamTailLaunch>>>(
+                    rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, nullptr);
+                bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
+                    rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
+                finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters);
+            }
+        }
+    }
+}
+
 // ------------------------------------------------ K6 lean + K7 warp BFS --
 //
 // The throughput path.  K6 is the leanest possible gather: one query per
@@ -1458,6 +1618,13 @@ static bool pick_fused(uint32_t wdl, uint32_t wbl, fused_fn &f, size_t &smem) {
     return false;
 }
 
+static bool pick_quad(uint32_t wdl, uint32_t wbl, fused_fn &f, size_t &smem) {
+#define DBL_QQ(A, B) if (wdl == A && wbl == B) { f = query_quad_kernel<A, B>; smem = sizeof(WarpBfs<A, B>) * (FUSED_THREADS / 32); return true; }
+    DBL_QQ(2, 1) DBL_QQ(4, 1) DBL_QQ(1, 2) DBL_QQ(2, 2)
+#undef DBL_QQ
+    return false;
+}
+
 typedef void (*label_fn)(const uint64_t *, uint32_t, const uint32_t *, const uint32_t *, uint64_t,
                          uint32_t, uint8_t *, uint32_t *, uint32_t *, uint32_t *);
 
@@ -1576,7 +1743,9 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     }
     fused_fn fused = nullptr;
     size_t fsmem = 0;
-    if (count && !no_fused && pick_fused(idx->wdl, idx->wbl, fused, fsmem)) {
+    static const bool no_quad = std::getenv("DBL_NO_QUAD") != nullptr;
+    const bool quad = count && !no_fused && !no_quad && pick_quad(idx->wdl, idx->wbl, fused, fsmem);
+    if (quad || (count && !no_fused && pick_fused(idx->wdl, idx->wbl, fused, fsmem))) {
         static int fbps = -1;
         static const void *last_fn = nullptr;
         if (fbps < 0 || last_fn != (const void *)fused) {
@@ -1589,7 +1758,7 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
                           g->q_dense.as<char>()};
         DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
         fused<<<g->sm_count * fbps, FUSED_THREADS, fsmem, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);
-        DBL_CHECK_LAUNCH("query_fused_kernel");
+        DBL_CHECK_LAUNCH(quad ? "query_quad_kernel" : "query_fused_kernel");
         DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
         g->q_timed_bfs = false;
         return DBL_OK;
