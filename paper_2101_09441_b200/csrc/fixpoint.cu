@@ -877,9 +877,14 @@ struct ReachParams {
     Adj adj[2];          // [0] in-edges (reverse adjacency), [1] out-edges (forward adjacency)
     Adj top[2];          // first level from h: [0] out-edges, [1] in-edges
     uint32_t *vis[2];
-    unsigned int *changed;   // [sweep % 3]: written in sweep s, read after its barrier, cleared in s + 2;
-                             // [3]: set when the sweep cap stopped the search (no head start then)
-    uint32_t max_sweeps;
+    uint32_t *nb[2][3];      // per direction: vertices newly marked in step s go to nb[d][s % 3]
+    unsigned int *changed;   // [step % 3]: marks made in step s (read after its barrier, cleared in s + 2);
+                             // [3]: set when the step cap stopped the search (no head start then);
+                             // [4]: steps run, [5]: bottom-up sweeps among them (trace)
+    uint32_t max_sweeps;     // cap on bottom-up sweeps (each O(n))
+    uint32_t max_steps;      // cap on all steps
+    uint32_t td_switch;      // switch to top-down once a step marks fewer vertices than this
+    unsigned long long *tr;  // trace (or nullptr): [2s] end time of step s (globaltimer), [2s+1] its marks
     const uint32_t *lm;
     uint32_t n, nwords;
 };
@@ -891,6 +896,9 @@ __device__ __forceinline__ bool vis_test_ca(const uint32_t *vis, uint32_t x) {
 }
 
 __device__ __forceinline__ bool any_marked(const Adj &a, const uint32_t *vis, uint32_t x) {
+    // one neighbour at a time: most vertices stop at their first or second
+    // neighbour, and batching 4 or 8 loads per step measured slower (cfg2
+    // first sweep 40 -> 60 us, cfg5 1.4 -> 3.3 ms)
     uint32_t s0 = __ldg(a.ptr + x), s1 = __ldg(a.ptr + x + 1);
     for (uint32_t j = s0; j < s1; ++j)
         if (vis_test_ca(vis, __ldg(a.col + j))) return true;
@@ -931,38 +939,94 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
         }
     }
     grid.sync();
-    bool capped = false;
-    for (uint32_t sweep = 0;; ++sweep) {
-        if (sweep == P.max_sweeps) {
+    if (P.tr && tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.tr[64] = t;
+    }
+    // Steps: bottom-up sweeps while they mark many vertices, then top-down
+    // levels from the vertices the previous step marked (a bottom-up sweep
+    // rescans every unmarked vertex's edges, which in the tail is mostly the
+    // vertices outside D(h)/A(h); a top-down level only touches the out-edges
+    // of the few new marks).  Every mark is also recorded in nb[d][s % 3].
+    bool capped = false, td = false;
+    uint32_t bu = 0;
+    for (uint32_t step = 0;; ++step) {
+        if (step == P.max_steps || (!td && bu == P.max_sweeps)) {
             // deep graph: the marked sets are only parts of D(h) / A(h), not
             // closed under successors / predecessors.  The head start is
             // still a subset of every marked vertex's final label, so it is
             // kept when the marked vertices can join the level-0 frontier
             // (they then propagate it), and dropped otherwise.
             capped = true;
-            if (tid == 0) P.changed[3] = 1;
+            if (tid == 0) { P.changed[3] = 1; P.changed[4] = step; P.changed[5] = bu; }
             break;
         }
-        const int cb = sweep % 3;
-        bool any = false;
-        for (uint64_t x = tid; x < P.n; x += nth) {
+        const int cb = step % 3;
+        unsigned marks = 0;
+        if (!td) {
+            for (uint64_t x = tid; x < P.n; x += nth) {
+#pragma unroll
+                for (int d = 0; d < 2; ++d) {
+                    const uint32_t w = *(volatile uint32_t *)&P.vis[d][x >> 5];
+                    if ((w >> (x & 31)) & 1u) continue;
+                    if (any_marked(P.adj[d], P.vis[d], (uint32_t)x)) {
+                        atomicOr(&P.vis[d][x >> 5], 1u << (x & 31));
+                        atomicOr(&P.nb[d][cb][x >> 5], 1u << (x & 31));
+                        ++marks;
+                    }
+                }
+            }
+            ++bu;
+        } else {
+            const int pb = (step + 2) % 3;   // the previous step's marks
 #pragma unroll
             for (int d = 0; d < 2; ++d) {
-                const uint32_t w = *(volatile uint32_t *)&P.vis[d][x >> 5];
-                if ((w >> (x & 31)) & 1u) continue;
-                if (any_marked(P.adj[d], P.vis[d], (uint32_t)x)) {
-                    atomicOr(&P.vis[d][x >> 5], 1u << (x & 31));
-                    any = true;
+                const Adj &a = P.top[d];
+                for (uint64_t wi = tid; wi < P.nwords; wi += nth) {
+                    uint32_t f = P.nb[d][pb][wi];
+                    while (f) {
+                        const uint32_t y = (uint32_t)(wi * 32 + __ffs(f) - 1);
+                        f &= f - 1;
+#pragma unroll 1
+                        for (int seg = 0; seg < 2; ++seg) {
+                            const uint32_t *ptr = seg ? a.dptr : a.ptr;
+                            if (!ptr) break;
+                            const uint32_t *col = seg ? a.dcol : a.col;
+                            const uint32_t s0 = __ldg(ptr + y), s1 = __ldg(ptr + y + 1);
+                            for (uint32_t j = s0; j < s1; ++j) {
+                                const uint32_t z = __ldg(col + j);
+                                const uint32_t bit = 1u << (z & 31);
+                                if (vis_test_ca(P.vis[d], z)) continue;
+                                if (!(atomicOr(&P.vis[d][z >> 5], bit) & bit)) {
+                                    atomicOr(&P.nb[d][cb][z >> 5], bit);
+                                    ++marks;
+                                }
+                            }
+                        }
+                    }
                 }
             }
         }
-        if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(&P.changed[cb], 1u);
-        if (tid == 0) P.changed[(sweep + 1) % 3] = 0;
+        // clear the bitmaps step s + 1 writes (written in s - 2, read in s - 1)
+        const int clr = (step + 1) % 3;
+        for (uint64_t wi = tid; wi < P.nwords; wi += nth) { P.nb[0][clr][wi] = 0; P.nb[1][clr][wi] = 0; }
+        for (int o = 16; o > 0; o >>= 1) marks += __shfl_xor_sync(FULL, marks, o);
+        if ((threadIdx.x & 31) == 0 && marks) atomicAdd(&P.changed[cb], marks);
+        if (tid == 0) P.changed[(step + 1) % 3] = 0;
         grid.sync();
-        if (!*(volatile unsigned int *)&P.changed[cb]) {
-            if (tid == 0) P.changed[4] = sweep + 1;   // sweeps run (trace)
+        const unsigned got = *(volatile unsigned int *)&P.changed[cb];
+        if (P.tr && tid == 0 && step < 32) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            P.tr[2 * step] = t;
+            P.tr[2 * step + 1] = got | ((unsigned long long)td << 32);
+        }
+        if (!got) {
+            if (tid == 0) { P.changed[4] = step + 1; P.changed[5] = bu; }
             break;
         }
+        if (!td && got < P.td_switch) td = true;
     }
     // keep D(h) and the SCC landmarks for query pruning (marks are exact
     // members even when the sweeps were capped)
@@ -1041,12 +1105,13 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     const size_t bmw = ((size_t)n + 31) / 32;
     const size_t bbytes = ((bmw * 4 + 255) / 256) * 256;
     dbl_status s;
-    if ((s = g->reach.ensure(2 * bbytes + 2 * MAX_SHARD_WORDS * 8 + 64))) return s;
+    const size_t rbytes = 8 * bbytes + 2 * MAX_SHARD_WORDS * 8 + 64 + 66 * 8;
+    if ((s = g->reach.ensure(rbytes))) return s;
     uint32_t *vf = g->reach.as<uint32_t>();
     uint32_t *vb = reinterpret_cast<uint32_t *>(g->reach.as<char>() + bbytes);
-    unsigned long long *L = reinterpret_cast<unsigned long long *>(g->reach.as<char>() + 2 * bbytes);
+    unsigned long long *L = reinterpret_cast<unsigned long long *>(g->reach.as<char>() + 8 * bbytes);
     unsigned int *chg = reinterpret_cast<unsigned int *>(L + 2 * MAX_SHARD_WORDS);
-    DBL_CUDA(cudaMemsetAsync(g->reach.p, 0, 2 * bbytes + 2 * MAX_SHARD_WORDS * 8 + 64, g->stream));
+    DBL_CUDA(cudaMemsetAsync(g->reach.p, 0, rbytes, g->stream));
     ReachParams R{};
     R.rec = idx->rec.as<uint64_t>();
     R.L = L;
@@ -1073,6 +1138,9 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     R.top[1] = graph_rev(g);
     R.vis[0] = vf;
     R.vis[1] = vb;
+    for (int d = 0; d < 2; ++d)
+        for (int j = 0; j < 3; ++j)
+            R.nb[d][j] = reinterpret_cast<uint32_t *>(g->reach.as<char>() + (2 + 3 * d + j) * bbytes);
     R.changed = chg;
     R.lm = idx->landmarks.as<uint32_t>();
     R.n = n;
@@ -1081,6 +1149,15 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     // in ~5; deep sparse ones stop here and hand the partial sets to the
     // label fixpoint's frontier
     R.max_sweeps = 12;
+    R.max_steps = 64;
+    static const uint32_t td_div = [] {
+        const char *e = std::getenv("DBL_TD_DIV");
+        return e ? (uint32_t)std::atoi(e) : 64u;
+    }();
+    R.td_switch = td_div ? (uint32_t)(n / td_div) : 0u;
+    static const bool tr = std::getenv("DBL_TRACE") != nullptr;
+    unsigned long long *trb = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(chg) + 64);
+    R.tr = tr ? trb : nullptr;
     static int bps = -1;
     if (bps < 0) {
         DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, reach_kernel, 256, 0));
@@ -1091,10 +1168,19 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
                                          g->stream));
     DBL_LAUNCHED();
     if (std::getenv("DBL_TRACE")) {
-        unsigned int hc[5];
+        unsigned int hc[6];
         DBL_CUDA(cudaMemcpyAsync(hc, chg, sizeof(hc), cudaMemcpyDeviceToHost, g->stream));
         DBL_CUDA(cudaStreamSynchronize(g->stream));
-        std::fprintf(stderr, "[dbl] pivot reach: %u sweeps%s\n", hc[4], hc[3] ? " (cap hit: no head start)" : "");
+        std::fprintf(stderr, "[dbl] pivot reach: %u steps, %u bottom-up%s\n", hc[4], hc[5],
+                     hc[3] ? " (cap hit: partial sets)" : "");
+        unsigned long long ht[66];
+        DBL_CUDA(cudaMemcpy(ht, trb, sizeof(ht), cudaMemcpyDeviceToHost));
+        unsigned long long prev = ht[64];
+        for (uint32_t st = 0; st < hc[4] && st < 32; ++st) {
+            std::fprintf(stderr, "[dbl]   step %2u %s marks %9u  %8.1f us\n", st, (ht[2 * st + 1] >> 32) ? "TD" : "BU",
+                         (unsigned)ht[2 * st + 1], (ht[2 * st] - prev) / 1000.0);
+            prev = ht[2 * st];
+        }
     }
     return DBL_OK;
 }

@@ -232,8 +232,11 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
     const uint32_t H = A.wdl + A.wbl, rw = 2 * H, rs = rec_stride(H);
     const uint64_t nr = ((uint64_t)A.n + 31) & ~31ull;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += stride) {
         bool p0 = false, p1 = false;
+        uint32_t win = 0xffffffffu, wout = 0xffffffffu;
+        uint64_t bit = 0;
         if (i < A.n) {
             const uint32_t v = (uint32_t)i;
             uint8_t f;
@@ -271,18 +274,31 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
             }
             // seeds: bl_in bit for source leaves, bl_out bit for sinks, dl words 0
             const uint32_t bw = A.wdl + b / 64;
-            const uint32_t win = (f & 1) ? bw : 0xffffffffu;
-            const uint32_t wout = (f & 2) ? H + bw : 0xffffffffu;
-            const uint64_t bit = 1ull << (b % 64);
-            uint64_t *r = A.rec + (size_t)v * rs;
-            for (uint32_t w = 0; w < rw; w += 2) {
-                ulonglong2 val;
-                val.x = (w == win || w == wout) ? bit : 0ull;
-                val.y = (w + 1 == win || w + 1 == wout) ? bit : 0ull;
-                *reinterpret_cast<ulonglong2 *>(r + w) = val;
-            }
+            win = (f & 1) ? bw : 0xffffffffu;
+            wout = (f & 2) ? H + bw : 0xffffffffu;
+            bit = 1ull << (b % 64);
             p0 = (f & 1) && bw >= A.a0 && bw < A.e0;
             p1 = (f & 2) && H + bw >= A.a1 && H + bw < A.e1;
+        }
+        // the warp's 32 records (pad words included) as one contiguous block:
+        // each store instruction covers 512 bytes, whole sectors and lines
+        // (per-record 16-byte stores at the record stride are partial-sector
+        // writes, which cost L2 read-fills)
+        {
+            const uint64_t v0 = i - lane;
+            uint64_t *blk = A.rec + v0 * rs;
+            for (uint32_t t = 0; t < rs * 32; t += 64) {
+                const uint32_t wi = t + 2 * lane, r = wi / rs, w = wi % rs;
+                const uint32_t swin = __shfl_sync(FULL, win, r), swout = __shfl_sync(FULL, wout, r);
+                const uint64_t sbit = ((uint64_t)__shfl_sync(FULL, (uint32_t)(bit >> 32), r) << 32) |
+                                      __shfl_sync(FULL, (uint32_t)bit, r);
+                if (v0 + r < A.n) {
+                    ulonglong2 val;
+                    val.x = (w == swin || w == swout) ? sbit : 0ull;
+                    val.y = (w + 1 == swin || w + 1 == swout) ? sbit : 0ull;
+                    *reinterpret_cast<ulonglong2 *>(blk + wi) = val;
+                }
+            }
         }
         const unsigned b0 = __ballot_sync(FULL, p0), b1 = __ballot_sync(FULL, p1);
         if ((threadIdx.x & 31) == 0) {
