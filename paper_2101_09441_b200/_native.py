@@ -119,6 +119,19 @@ def call(name: str, *args) -> None:
     check(getattr(lib(), name)(*args))
 
 
+def device_inputs_ready(*tensors) -> None:
+    """The engine orders its stream after the legacy default stream (where torch
+    produces tensors unless told otherwise); tensors made on another current
+    stream are waited for here."""
+    import torch
+    for t in tensors:
+        if t is not None and getattr(t, "is_cuda", False):
+            cur = torch.cuda.current_stream(t.device)
+            if cur != torch.cuda.default_stream(t.device):
+                cur.synchronize()
+            return
+
+
 def ptr(a) -> ctypes.c_void_p | None:
     """Address of a numpy array / torch tensor (host or device) or None."""
     if a is None:

@@ -40,6 +40,12 @@ static thread_local bool g_free_clean = false;
 void set_stream(cudaStream_t s) { g_cur_stream = s; g_free_clean = false; }
 void set_stream_synced() { g_cur_stream = nullptr; g_free_clean = true; }
 
+dbl_status order_after_caller(dbl_graph *g) {
+    DBL_CUDA(cudaEventRecord(g->ev_in, cudaStreamLegacy));
+    DBL_CUDA(cudaStreamWaitEvent(g->stream, g->ev_in, 0));
+    return DBL_OK;
+}
+
 static size_t size_class(size_t n) {
     if (n <= 4096) {
         size_t c = 256;
@@ -644,8 +650,9 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
         if ((s = run_query(idx, g, (const uint32_t *)dptr[0], (const uint32_t *)dptr[1], count, flags,
                            (uint8_t *)dptr[2], (uint32_t *)dptr[3])))
             return s;
-    } else if ((s = run_query(idx, g, u, v, count, flags, codes, visited))) {
-        return s;
+    } else {
+        if (count && (s = order_after_caller(g))) return s;
+        if ((s = run_query(idx, g, u, v, count, flags, codes, visited))) return s;
     }
     if (!sync) return DBL_OK;
     uint32_t err = 0;
@@ -768,6 +775,9 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
         DBL_CUDA(cudaMemcpyAsync(in.as<uint32_t>() + count, v, count * 4, cudaMemcpyHostToDevice, g->stream));
         du = in.as<uint32_t>();
         dv = du + count;
+    } else if ((s = order_after_caller(g))) {
+        cleanup();
+        return s;
     }
     // st4: [0] vertex-range flag, [1] certified count, [2] new-edge count,
     // [3] unique count.  The whole batch is enqueued without a host round

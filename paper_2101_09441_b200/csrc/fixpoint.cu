@@ -886,6 +886,8 @@ struct ReachParams {
     uint32_t td_switch;      // switch to top-down once a step marks fewer vertices than this
     unsigned long long *tr;  // trace (or nullptr): [2s] end time of step s (globaltimer), [2s+1] its marks
     const uint32_t *lm;
+    const uint8_t *flags;    // leaf flags and buckets: the seeds, read instead of the seeded records
+    const uint32_t *bucket;
     uint32_t n, nwords;
 };
 
@@ -911,7 +913,7 @@ __device__ __forceinline__ bool any_marked(const Adj &a, const uint32_t *vis, ui
     return false;
 }
 
-__global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
+__global__ void __launch_bounds__(256, 8) reach_kernel(ReachParams P) {
     cg::grid_group grid = cg::this_grid();
     const uint32_t h = P.lm[0];
     if (h >= P.n) return;   // grid-uniform: no pivot, no head start
@@ -1047,19 +1049,45 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
     const uint64_t wm = capped ? P.cap_wmask : P.wmask;
     for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = 0;
     __syncthreads();
-    for (uint64_t x = tid; x < P.n; x += nth) {
-        const bool fwd = (P.vis[0][x >> 5] >> (x & 31)) & 1u, bwd = (P.vis[1][x >> 5] >> (x & 31)) & 1u;
-        const uint64_t *r = P.rec + x * rs;
-        if (bwd)
-            for (uint32_t w = 0; w < H; ++w) {
-                const uint64_t v = ((wm >> w) & 1u) ? r[w] : 0ull;
-                if (v) atomicOr(&acc[w], (unsigned long long)v);
+    // The records hold exactly the seeds now, so the unions come from the
+    // metadata (5 coalesced bytes per vertex instead of the records): source
+    // leaves and landmarks in A(h) give L_in(h), sinks and landmarks in D(h)
+    // give L_out(h) (seeding as in prep_kernel / landmark_seed_kernel).
+    {
+        const uint32_t wdl = P.wdl, wbl = H - wdl;
+        const int lane = threadIdx.x & 31;
+        const uint64_t nr = ((uint64_t)P.n + 31) & ~31ull;   // warp-uniform trips
+        for (uint64_t x = tid; x < nr; x += nth) {
+            uint32_t qin = 0xffffffffu, qout = 0xffffffffu, bb = 0;
+            if (x < P.n) {
+                const uint8_t f = P.flags[x];
+                if (f) {
+                    const uint32_t b = P.bucket[x];
+                    bb = b % 64;
+                    if ((f & 1) && ((P.vis[1][x >> 5] >> (x & 31)) & 1u)) qin = b / 64;
+                    if ((f & 2) && ((P.vis[0][x >> 5] >> (x & 31)) & 1u)) qout = b / 64;
+                }
             }
-        if (fwd)
-            for (uint32_t w = H; w < rw; ++w) {
-                const uint64_t v = ((wm >> w) & 1u) ? r[w] : 0ull;
-                if (v) atomicOr(&acc[w], (unsigned long long)v);
+            if (!__any_sync(FULL, qin != 0xffffffffu || qout != 0xffffffffu)) continue;
+            for (uint32_t q = 0; q < wbl; ++q) {
+                const uint64_t vi = qin == q ? 1ull << bb : 0ull, vo = qout == q ? 1ull << bb : 0ull;
+                const uint64_t ri = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(vi >> 32)) << 32) |
+                                    __reduce_or_sync(FULL, (uint32_t)vi);
+                const uint64_t ro = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(vo >> 32)) << 32) |
+                                    __reduce_or_sync(FULL, (uint32_t)vo);
+                if (lane == 0) {
+                    if (ri && ((wm >> (wdl + q)) & 1u)) atomicOr(&acc[wdl + q], (unsigned long long)ri);
+                    if (ro && ((wm >> (H + wdl + q)) & 1u)) atomicOr(&acc[H + wdl + q], (unsigned long long)ro);
+                }
             }
+        }
+        for (uint64_t i = tid; i < P.k; i += nth) {
+            const uint32_t x = P.lm[i], w = (uint32_t)(i / 64);
+            if (x >= P.n) continue;
+            const unsigned long long bit = 1ull << (i % 64);
+            if (((P.vis[1][x >> 5] >> (x & 31)) & 1u) && ((wm >> w) & 1u)) atomicOr(&acc[w], bit);
+            if (((P.vis[0][x >> 5] >> (x & 31)) & 1u) && ((wm >> (H + w)) & 1u)) atomicOr(&acc[H + w], bit);
+        }
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x)
@@ -1082,14 +1110,31 @@ __global__ void __launch_bounds__(256) reach_kernel(ReachParams P) {
             if (P.front[1]) P.front[1][w] &= ~scc;
         }
     }
-    for (uint64_t x = tid; x < P.n; x += nth) {
-        uint64_t *r = P.rec + x * rs;
-        if ((P.vis[0][x >> 5] >> (x & 31)) & 1u)
-            for (uint32_t w = 0; w < H; ++w)
-                if (acc[w]) r[w] |= acc[w];
-        if ((P.vis[1][x >> 5] >> (x & 31)) & 1u)
-            for (uint32_t w = H; w < rw; ++w)
-                if (acc[w]) r[w] |= acc[w];
+    // apply: a warp takes 32 consecutive records (one bitmap word per
+    // direction) and ORs the unions in with 512-byte coalesced
+    // read-modify-writes, instead of 8-byte accesses at the record stride
+    {
+        const int lane = threadIdx.x & 31;
+        const uint64_t nblk = P.nwords, gw = tid >> 5, nw = nth >> 5;
+        for (uint64_t blk = gw; blk < nblk; blk += nw) {
+            const uint32_t fb = P.vis[0][blk], bb = P.vis[1][blk];
+            if (!(fb | bb)) continue;
+            uint64_t *base = P.rec + blk * 32 * rs;
+            for (uint32_t t = 0; t < rs * 32; t += 64) {
+                const uint32_t wi = t + 2 * lane, r = wi / rs, w = wi % rs;
+                if (blk * 32 + r >= P.n) continue;
+                const bool in_d = (fb >> r) & 1u, in_a = (bb >> r) & 1u;
+                const uint64_t a0 = (w < H ? in_d : (w < rw && in_a)) ? acc[w] : 0ull;
+                const uint64_t a1 = (w + 1 < H ? in_d : (w + 1 < rw && in_a)) ? acc[w + 1] : 0ull;
+                if (a0 | a1) {
+                    ulonglong2 *p = reinterpret_cast<ulonglong2 *>(base + wi);
+                    ulonglong2 val = *p;
+                    val.x |= a0;
+                    val.y |= a1;
+                    *p = val;
+                }
+            }
+        }
     }
 }
 
@@ -1143,6 +1188,8 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
             R.nb[d][j] = reinterpret_cast<uint32_t *>(g->reach.as<char>() + (2 + 3 * d + j) * bbytes);
     R.changed = chg;
     R.lm = idx->landmarks.as<uint32_t>();
+    R.flags = idx->leaf_flags.as<uint8_t>();
+    R.bucket = idx->bucket.as<uint32_t>();
     R.n = n;
     R.nwords = (uint32_t)bmw;
     // bottom-up sweeps cost O(n) each: shallow graphs (R-MAT, d >= 4) finish

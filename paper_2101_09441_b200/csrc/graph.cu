@@ -482,6 +482,8 @@ extern "C" dbl_status dbl_graph_create(uint32_t n, const uint32_t *src, const ui
         e = cudaEventCreate(&ev);
         if (e != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
     }
+    e = cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
     cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device);
     dbl_status s;
     DevBuf keys, alt, ds, dd, err;
@@ -500,6 +502,7 @@ extern "C" dbl_status dbl_graph_create(uint32_t n, const uint32_t *src, const ui
         pdst = dd.as<uint32_t>();
     }
     cudaMemsetAsync(err.p, 0, 8, g->stream);
+    if (m && mem != DBL_MEM_HOST && (s = order_after_caller(g))) { cleanup(); return fail(s); }
     if (m) {
         pack_keys_kernel<<<grid_for(m), 256, 0, g->stream>>>(psrc, pdst, m, n, keys.as<uint64_t>(),
                                                              err.as<unsigned long long>());
@@ -546,6 +549,7 @@ extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
     g->host_stage.release();
     g->q_host_res.release();
     for (auto &ev : g->ev) if (ev) cudaEventDestroy(ev);
+    if (g->ev_in) cudaEventDestroy(g->ev_in);
     if (g->stream) cudaStreamDestroy(g->stream);
     delete g;
     return DBL_OK;

@@ -44,6 +44,11 @@ void pool_free(void *p, size_t bytes, int device);
 void pool_trim();
 void set_stream(cudaStream_t s);  // stream that subsequent pool traffic belongs to
 void set_stream_synced();         // the device was just synchronised: frees are reusable without waiting
+// Device-memory inputs are produced by the caller on the legacy default
+// stream (torch's, unless the caller set another and synchronised it); the
+// engine's stream is non-blocking, so it waits for that stream's pending work
+// through an event (no host sync) before reading them.
+dbl_status order_after_caller(dbl_graph *g);
 void pool_forget_stream(cudaStream_t s);  // before a stream is destroyed
 // Debug phase timer: DBL_TRACE=1 prints host-side phase times to stderr.
 void trace(const char *what, cudaStream_t s);
@@ -193,6 +198,7 @@ struct dbl_graph {
     int sm_count = 148;
     int coop_blocks = 0;      // co-resident blocks for the fixpoint kernel
     cudaEvent_t ev[6] = {};
+    cudaEvent_t ev_in = nullptr;   // orders the engine stream after the caller's (order_after_caller)
     float t_fix = 0, t_label = 0, t_bfs = 0;
 };
 

@@ -48,6 +48,7 @@ class DynamicGraph:
             if src.numel() != dst.numel():
                 raise ValueError("src and dst differ in length")
             h = ctypes.c_void_p()
+            N.device_inputs_ready(src, dst)
             N.call("dbl_graph_create", n, N.ptr(src), N.ptr(dst), src.numel(), N.MEM_DEVICE, src.device.index,
                    ctypes.byref(h))
             g._h = h

@@ -184,6 +184,7 @@ def query_codes(g, idx: DblIndex, u, v, flags: QueryFlags = DEFAULT_FLAGS,
         import torch
         codes = torch.empty(u.numel(), dtype=torch.uint8, device=u.device)
         vis = torch.empty(u.numel(), dtype=torch.int32, device=u.device) if with_visited else None
+        N.device_inputs_ready(u, v)
         N.call("dbl_query", idx.handle, g.handle, N.ptr(u), N.ptr(v), u.numel(), flags.bits(),
                N.ptr(codes), N.ptr(vis), N.MEM_DEVICE)
         return codes, vis

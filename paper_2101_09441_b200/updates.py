@@ -86,6 +86,7 @@ def insert_edges(g, idx: DblIndex, u, v) -> BatchUpdateStats:
     _check_consistent(g, idx)
     st = N.BatchStatsC()
     if hasattr(u, "is_cuda") and u.is_cuda:
+        N.device_inputs_ready(u, v)
         N.call("dbl_insert_edges", idx.handle, g.handle, N.ptr(u), N.ptr(v), u.numel(), N.MEM_DEVICE,
                ctypes.byref(st))
     else:

@@ -612,3 +612,33 @@ def test_insert_batch_range_error_leaves_index_untouched():
         st = E.insert_edges(g, idx, iu, iv)
         assert st.inserted == len(iu)
         assert idx.labels_equal(E.rebuild_index(g, idx))
+
+
+def test_device_inputs_ordered_after_producer_stream():
+    """Device edge/query arrays produced by still-running torch kernels (legacy
+    default stream) must be read only after those kernels finish: the engine's
+    non-blocking stream waits on them.  Before the fix, a graph built right
+    after asynchronous torch work, with the engine's pool already warm (no
+    implicit cudaMalloc sync), lost edges (cfg5 after cfg4: 1.06 B -> 0.29 B)."""
+    import torch
+    n, src, dst = rmat_case(20, 8, 3)
+    keys = np.unique((src.astype(np.uint64) << np.uint64(32)) | dst.astype(np.uint64))
+    keys = keys[(keys >> np.uint64(32)) != (keys & np.uint64(0xFFFFFFFF))]
+    expected = len(keys)
+    E.DynamicGraph.from_edges(n, torch.from_numpy(src.view(np.int32)).cuda(),
+                              torch.from_numpy(dst.view(np.int32)).cuda())   # warms the pool
+    s0 = torch.from_numpy(src.view(np.int32)).cuda()
+    d0 = torch.from_numpy(dst.view(np.int32)).cuda()
+    for trial in range(3):
+        perm = torch.randperm(s0.numel(), device="cuda")
+        inv = torch.argsort(perm)
+        s2, d2 = s0[perm][inv], d0[perm][inv]   # same content, written by queued kernels
+        g = E.DynamicGraph.from_edges(n, s2, d2)
+        assert g.edge_count == expected, trial
+        idx = E.build_index(g)
+        qu = torch.randint(0, n, (1 << 20,), device="cuda", dtype=torch.int32)
+        qv = torch.randint(0, n, (1 << 20,), device="cuda", dtype=torch.int32)
+        qu2, qv2 = qu[perm[: 1 << 20] % (1 << 20)], qv[perm[: 1 << 20] % (1 << 20)]
+        codes, _ = E.query_codes(g, idx, qu2, qv2)
+        ref, _ = E.query_batch(g, idx, (qu2.cpu().numpy().view(np.uint32), qv2.cpu().numpy().view(np.uint32)))
+        np.testing.assert_array_equal(codes.cpu().numpy(), ref.codes)

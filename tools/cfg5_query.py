@@ -43,7 +43,7 @@ def main():
     v = vis.cpu().numpy() if vis is not None else np.zeros(0, np.uint32)
     qc = np.zeros(8, np.uint32)
     R.N.call("dbl_query_counters", g.handle, R.N.ptr(qc))
-    print(json.dumps({"label": args.label, "n": n, "build_s": tb, "query_s": t, "Gq_s": args.nq / t / 1e9,
+    print(json.dumps({"label": args.label, "n": n, "m": g.edge_count, "build_s": tb, "query_s": t, "Gq_s": args.nq / t / 1e9,
                       "bfs_fraction": float(np.mean(c >= 5)), "hard_path": int(qc[0]),
                       "visited_total": int(v.astype(np.uint64).sum()),
                       "codes_md5": hashlib.md5(c.tobytes()).hexdigest(),
