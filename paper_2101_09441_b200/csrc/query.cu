@@ -1472,6 +1472,9 @@ __global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_W
         }
     }
     if constexpr (TBFS) {
+        // (the pivot prune is left out here: these BFS expand <= 3 vertices
+        // on R-MAT, and its bitmap test adds a dependent load before each
+        // record read -- measured 24.2 vs 23.1 us per 1M batch on cfg2)
         __syncthreads();
         const uint32_t nq = min(dq.n, DQ_CAP);
 #if DBL_WBFS
@@ -1482,7 +1485,7 @@ __global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_W
             const uint32_t i = dq.i[t];
             uint32_t vc = 0;
             const int r = warp_query_bfs<WDL, WBL>(rec, adj, dq.u[t], dq.v[t], dq.dlo[t], dq.bli[t], dq.blo[t],
-                                                   prune_dl, prune_bl, qd.pv, wq[wid], &vc);
+                                                   prune_dl, prune_bl, Pivot{}, wq[wid], &vc);
             if (lane == 0) {
                 if (r == 2) {
                     pending[atomicAdd(&counters[CNT_PENDING], 1u)] = i;
@@ -1498,7 +1501,7 @@ __global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_W
             const uint32_t i = dq.i[t];
             uint32_t vc = 0;
             const int r = thread_bfs<WDL, WBL>(rec, adj, dq.u[t], dq.v[t], dq.dlo[t], dq.bli[t], dq.blo[t], prune_dl,
-                                               prune_bl, qd.pv, &vc);
+                                               prune_bl, Pivot{}, &vc);
             if (r == 2) {
                 pending[atomicAdd(&counters[CNT_PENDING], 1u)] = i;
             } else {
