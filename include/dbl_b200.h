@@ -15,7 +15,11 @@
  *  - Vertex ids are uint32; vertex count n < 2^32; edge count < 2^32.
  *  - Pointer arguments marked (host|device) honour `mem`: DBL_MEM_HOST means
  *    pageable/pinned host memory (the call stages copies itself),
- *    DBL_MEM_DEVICE means device memory on the handle's GPU.
+ *    DBL_MEM_DEVICE means device memory on the handle's GPU.  Device inputs
+ *    are read only after the work already queued on the legacy default
+ *    stream (the handle's own stream waits on it through an event, without
+ *    a host sync); a caller producing them on another stream synchronises
+ *    that stream first.
  *  - Handles own all device state.  Calls on one handle are serialised on
  *    the handle's stream; queries are read-only and may not overlap an
  *    insertion (reference contract: pkg/README.md:179-183).

@@ -28,10 +28,13 @@ def main():
     ap.add_argument("--nq", type=int, default=64_000_000)
     ap.add_argument("--label", default="")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--builds", type=int, default=1, help="builds before the timed one (warm allocations)")
     args = ap.parse_args()
     g = R.device_graph(args.scale, 16, 55)
     n = g.vertex_count
-    idx, tb = R.timed(lambda: E.build_index(g, E.IndexConfig(k=256, k_prime=64)))
+    for _ in range(args.builds - 1):
+        E.build_index(g, E.IndexConfig(k=256, k_prime=64))
+    idx, tb = R.build_time(g, E.IndexConfig(k=256, k_prime=64), reps=1)
     rng = np.random.default_rng(56)
     qu = rng.integers(0, n, args.nq, dtype=np.uint32)
     qv = rng.integers(0, n, args.nq, dtype=np.uint32)
