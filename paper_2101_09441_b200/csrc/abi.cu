@@ -280,10 +280,9 @@ static dbl_status alloc_index(const dbl_graph *g, const dbl_config *cfg, dbl_ind
         dbl_index_free(idx);
         return s;
     }
-    if (idx->rs != idx->rw && g->n) {   // pad words are never written: zero them once
-        const cudaError_t e = cudaMemsetAsync(idx->rec.p, 0, (size_t)g->n * idx->rs * 8, g->stream);
-        if (e != cudaSuccess) { dbl_index_free(idx); return cuda_fail(e, "clear records"); }
-    }
+    // pad words (rs > rw) are zeroed by whichever pass seeds the records
+    // (prep_kernel for a build, seed_records_kernel otherwise) and never
+    // written again; grown records are zero-filled
     *out = idx;
     return DBL_OK;
 }

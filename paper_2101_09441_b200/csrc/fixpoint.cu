@@ -555,6 +555,7 @@ __global__ void seed_records_kernel(uint64_t *__restrict__ rec, uint32_t n, uint
         const uint32_t win = (f & 1) ? wdl + b / 64 : 0xffffffffu;
         const uint32_t wout = (f & 2) ? H + wdl + b / 64 : 0xffffffffu;
         const uint64_t bit = 1ull << (b % 64);
+        for (uint32_t w = rw; w < rs; ++w) r[w] = 0ull;   // pad words
         if (all) {
             for (uint32_t w = 0; w < rw; w += 2) {
                 ulonglong2 val;
