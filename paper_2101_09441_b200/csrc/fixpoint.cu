@@ -889,6 +889,7 @@ struct ReachParams {
     const uint32_t *lm;
     const uint8_t *flags;    // leaf flags and buckets: the seeds, read instead of the seeded records
     const uint32_t *bucket;
+    bool write_rec;          // records not seeded yet (full build): write seeds | head start, whole lines
     uint32_t n, nwords;
 };
 
@@ -917,16 +918,17 @@ __device__ __forceinline__ bool any_marked(const Adj &a, const uint32_t *vis, ui
 __global__ void __launch_bounds__(256, 8) reach_kernel(ReachParams P) {
     cg::grid_group grid = cg::this_grid();
     const uint32_t h = P.lm[0];
-    if (h >= P.n) return;   // grid-uniform: no pivot, no head start
+    const bool have = h < P.n;   // grid-uniform (landmarks are validated, so always in practice)
+    if (!have && !P.write_rec) return;   // no pivot, no head start
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
     // h and its direct successors / predecessors (top-down first level)
-    if (tid == 0) {
+    if (have && tid == 0) {
         atomicOr(&P.vis[0][h >> 5], 1u << (h & 31));
         atomicOr(&P.vis[1][h >> 5], 1u << (h & 31));
     }
 #pragma unroll
-    for (int d = 0; d < 2; ++d) {
+    for (int d = 0; d < 2 && have; ++d) {
         const Adj &a = P.top[d];
         const uint32_t s0 = a.ptr[h], s1 = a.ptr[h + 1];
         for (uint64_t j = s0 + tid; j < s1; j += nth) {
@@ -954,7 +956,7 @@ __global__ void __launch_bounds__(256, 8) reach_kernel(ReachParams P) {
     // of the few new marks).  Every mark is also recorded in nb[d][s % 3].
     bool capped = false, td = false;
     uint32_t bu = 0;
-    for (uint32_t step = 0;; ++step) {
+    for (uint32_t step = 0; have; ++step) {
         if (step == P.max_steps || (!td && bu == P.max_sweeps)) {
             // deep graph: the marked sets are only parts of D(h) / A(h), not
             // closed under successors / predecessors.  The head start is
@@ -1041,7 +1043,10 @@ __global__ void __launch_bounds__(256, 8) reach_kernel(ReachParams P) {
             if (x < P.n && (((P.vis[0][x >> 5] & P.vis[1][x >> 5]) >> (x & 31)) & 1u))
                 atomicOr(&P.scc_out[i / 64], 1ull << (i % 64));
         }
-    if (capped && !(P.front[0] && P.front[1])) return;   // grid-uniform
+    // a capped search without both level-0 bitmaps drops the head start
+    // (grid-uniform); the records are still written when they are not yet
+    const bool drop = capped && !(P.front[0] && P.front[1]);
+    if (drop && !P.write_rec) return;
     // L_in(h) = OR of the in-halves over A(h), L_out(h) = OR of the
     // out-halves over D(h); then every x in D(h) takes L_in(h), every x in
     // A(h) takes L_out(h)
@@ -1050,11 +1055,11 @@ __global__ void __launch_bounds__(256, 8) reach_kernel(ReachParams P) {
     const uint64_t wm = capped ? P.cap_wmask : P.wmask;
     for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = 0;
     __syncthreads();
-    // The records hold exactly the seeds now, so the unions come from the
+    // The records hold exactly the seeds (or are about to), so the unions come from the
     // metadata (5 coalesced bytes per vertex instead of the records): source
     // leaves and landmarks in A(h) give L_in(h), sinks and landmarks in D(h)
     // give L_out(h) (seeding as in prep_kernel / landmark_seed_kernel).
-    {
+    if (!drop) {
         const uint32_t wdl = P.wdl, wbl = H - wdl;
         const int lane = threadIdx.x & 31;
         const uint64_t nr = ((uint64_t)P.n + 31) & ~31ull;   // warp-uniform trips
@@ -1099,7 +1104,7 @@ __global__ void __launch_bounds__(256, 8) reach_kernel(ReachParams P) {
     // a vertex of h's SCC (in D(h) and A(h)) now holds L_in(h) / L_out(h),
     // which every successor / predecessor also holds: it leaves the level-0
     // frontier (on R-MAT that drops the landmarks, the hubs of that frontier)
-    for (uint64_t w = tid; w < P.nwords; w += nth) {
+    for (uint64_t w = tid; w < P.nwords && !drop; w += nth) {
         if (capped) {   // partial sets: every marked vertex propagates its head start
             P.front[0][w] |= P.vis[0][w];
             P.front[1][w] |= P.vis[1][w];
@@ -1113,27 +1118,62 @@ __global__ void __launch_bounds__(256, 8) reach_kernel(ReachParams P) {
     }
     // apply: a warp takes 32 consecutive records (one bitmap word per
     // direction) and ORs the unions in with 512-byte coalesced
-    // read-modify-writes, instead of 8-byte accesses at the record stride
+    // read-modify-writes, instead of 8-byte accesses at the record stride.
+    // In write mode (full build, prep skipped the records) it writes every
+    // record whole instead -- seeds from the metadata | the unions, pad words
+    // zero -- with no read at all, and the landmark bits follow.
     {
         const int lane = threadIdx.x & 31;
+        const uint32_t wdl = P.wdl;
         const uint64_t nblk = P.nwords, gw = tid >> 5, nw = nth >> 5;
         for (uint64_t blk = gw; blk < nblk; blk += nw) {
-            const uint32_t fb = P.vis[0][blk], bb = P.vis[1][blk];
-            if (!(fb | bb)) continue;
+            const uint32_t fb = drop ? 0u : P.vis[0][blk], bb = drop ? 0u : P.vis[1][blk];
+            if (!(fb | bb) && !P.write_rec) continue;
             uint64_t *base = P.rec + blk * 32 * rs;
+            uint32_t win = 0xffffffffu, wout = 0xffffffffu, sb = 0;
+            if (P.write_rec) {
+                const uint64_t v = blk * 32 + lane;
+                if (v < P.n) {
+                    const uint8_t f = P.flags[v];
+                    if (f) {
+                        const uint32_t b = P.bucket[v];
+                        sb = b % 64;
+                        if (f & 1) win = wdl + b / 64;
+                        if (f & 2) wout = H + wdl + b / 64;
+                    }
+                }
+            }
             for (uint32_t t = 0; t < rs * 32; t += 64) {
                 const uint32_t wi = t + 2 * lane, r = wi / rs, w = wi % rs;
-                if (blk * 32 + r >= P.n) continue;
                 const bool in_d = (fb >> r) & 1u, in_a = (bb >> r) & 1u;
                 const uint64_t a0 = (w < H ? in_d : (w < rw && in_a)) ? acc[w] : 0ull;
                 const uint64_t a1 = (w + 1 < H ? in_d : (w + 1 < rw && in_a)) ? acc[w + 1] : 0ull;
-                if (a0 | a1) {
+                if (P.write_rec) {
+                    const uint32_t swin = __shfl_sync(FULL, win, r), swout = __shfl_sync(FULL, wout, r);
+                    const uint64_t sbit = 1ull << __shfl_sync(FULL, sb, r);
+                    if (blk * 32 + r >= P.n) continue;
+                    ulonglong2 val;
+                    val.x = a0 | ((w == swin || w == swout) ? sbit : 0ull);
+                    val.y = a1 | ((w + 1 == swin || w + 1 == swout) ? sbit : 0ull);
+                    *reinterpret_cast<ulonglong2 *>(base + wi) = val;
+                } else if (a0 | a1) {
+                    if (blk * 32 + r >= P.n) continue;
                     ulonglong2 *p = reinterpret_cast<ulonglong2 *>(base + wi);
                     ulonglong2 val = *p;
                     val.x |= a0;
                     val.y |= a1;
                     *p = val;
                 }
+            }
+        }
+        if (P.write_rec) {   // landmark i seeds bit i of both DL halves (labels.py:291-293)
+            grid.sync();
+            for (uint64_t i = tid; i < P.k; i += nth) {
+                const uint32_t x = P.lm[i];
+                if (x >= P.n) continue;
+                const unsigned long long bit = 1ull << (i % 64);
+                atomicOr(reinterpret_cast<unsigned long long *>(P.rec + (uint64_t)x * rs + i / 64), bit);
+                atomicOr(reinterpret_cast<unsigned long long *>(P.rec + (uint64_t)x * rs + H + i / 64), bit);
             }
         }
     }
@@ -1146,7 +1186,7 @@ static bool pivot_on() {
 
 // Head start from the pivot's reachability (all record words; after prep).
 static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask, uint32_t *front0,
-                                   uint32_t *front1, uint64_t cap_wmask) {
+                                   uint32_t *front1, uint64_t cap_wmask, bool write_rec) {
     const uint32_t n = g->n, H = idx->wdl + idx->wbl;
     const size_t bmw = ((size_t)n + 31) / 32;
     const size_t bbytes = ((bmw * 4 + 255) / 256) * 256;
@@ -1191,6 +1231,7 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     R.lm = idx->landmarks.as<uint32_t>();
     R.flags = idx->leaf_flags.as<uint8_t>();
     R.bucket = idx->bucket.as<uint32_t>();
+    R.write_rec = write_rec;
     R.n = n;
     R.nwords = (uint32_t)bmw;
     // bottom-up sweeps cost O(n) each: shallow graphs (R-MAT, d >= 4) finish
@@ -1269,12 +1310,17 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
     const bool prep = words == nullptr;
     dbl_status s;
     if ((s = graph_ensure_traversal(g))) return s;
+    // a full build with a pivot lets the pivot pass write the seeded records
+    // (one write of the table instead of seed + read-modify-write)
+    static const bool rec_in_prep = std::getenv("DBL_PREP_RECORDS") != nullptr;
+    const bool pivot = idx->cfg.k && pivot_on();
+    const bool pivot_writes = prep && pivot && !rec_in_prep;
     if (prep) {
         const Group **p0 = pairs[0];
         uint32_t *b0 = p0[0] ? g->stamp[0].as<uint32_t>() : nullptr;
         uint32_t *b1 = p0[1] ? g->stamp[1].as<uint32_t>() : nullptr;
         if ((s = prep_build_dev(g, idx, b0, b1, p0[0] ? p0[0]->w0 : 0, p0[0] ? p0[0]->w0 + p0[0]->nw : 0,
-                                p0[1] ? p0[1]->w0 : 0, p0[1] ? p0[1]->w0 + p0[1]->nw : 0)))
+                                p0[1] ? p0[1]->w0 : 0, p0[1] ? p0[1]->w0 + p0[1]->nw : 0, !pivot_writes)))
             return s;
     } else {
         uint64_t wmask = 0;
@@ -1282,7 +1328,7 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
         if ((s = index_seed_records(g, idx, wmask))) return s;
     }
     trace("build: seed", g->stream);
-    if (idx->cfg.k && pivot_on()) {
+    if (pivot) {
         uint64_t wmask = ~0ull;
         if (!prep) {
             wmask = 0;
@@ -1299,7 +1345,7 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
                 if (pairs[0][d])
                     for (uint32_t w = pairs[0][d]->w0; w < pairs[0][d]->w0 + pairs[0][d]->nw; ++w) cap_wmask |= 1ull << w;
         }
-        if ((s = pivot_head_start(g, idx, wmask, f0, f1, cap_wmask))) return s;
+        if ((s = pivot_head_start(g, idx, wmask, f0, f1, cap_wmask, pivot_writes))) return s;
         // (the capped case needs both bitmaps; with a one-direction first
         // group the kernel drops the head start instead)
         trace("build: pivot head start", g->stream);

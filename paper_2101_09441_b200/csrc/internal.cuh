@@ -267,7 +267,7 @@ dbl_status leaf_hash_dev(const uint64_t *ids, uint64_t count, uint32_t k_prime, 
 // then the landmark top-k runs on the device and ORs the landmark bits into
 // the records and the bitmaps.  No host synchronisation.
 dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_t *bits1, uint32_t a0,
-                          uint32_t e0, uint32_t a1, uint32_t e1);
+                          uint32_t e0, uint32_t a1, uint32_t e1, bool write_rec = true);
 // Enqueue the D2H copy of the prep state (read after the build's sync):
 // err = bucket override outside [0, k'); fallback = the device top-k
 // overflowed its candidate table (the caller re-selects and rebuilds).

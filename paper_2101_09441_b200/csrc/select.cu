@@ -280,11 +280,12 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
             p0 = (f & 1) && bw >= A.a0 && bw < A.e0;
             p1 = (f & 2) && H + bw >= A.a1 && H + bw < A.e1;
         }
-        // the warp's 32 records (pad words included) as one contiguous block:
+        // the warp's 32 records (pad words included) as one contiguous block
+        // (skipped when the pivot pass writes the records: A.rec == nullptr):
         // each store instruction covers 512 bytes, whole sectors and lines
         // (per-record 16-byte stores at the record stride are partial-sector
         // writes, which cost L2 read-fills)
-        {
+        if (A.rec) {
             const uint64_t v0 = i - lane;
             uint64_t *blk = A.rec + v0 * rs;
             for (uint32_t t = 0; t < rs * 32; t += 64) {
@@ -401,9 +402,11 @@ __global__ void __launch_bounds__(1024) topk_final_kernel(const uint64_t *__rest
         const uint32_t v = si[i], w = i / 64;
         const uint64_t bit = 1ull << (i % 64);
         lm[i] = v;
-        uint64_t *r = rec + (size_t)v * rs;
-        r[w] |= bit;          // dl_in: the landmark reaches itself
-        r[H + w] |= bit;      // dl_out
+        if (rec) {
+            uint64_t *r = rec + (size_t)v * rs;
+            r[w] |= bit;          // dl_in: the landmark reaches itself
+            r[H + w] |= bit;      // dl_out
+        }
         if (bits0 && w >= a0 && w < e0) atomicOr(&bits0[v >> 5], 1u << (v & 31));
         if (bits1 && H + w >= a1 && H + w < e1) atomicOr(&bits1[v >> 5], 1u << (v & 31));
     }
@@ -416,15 +419,17 @@ __global__ void landmark_seed_kernel(const uint32_t *__restrict__ lm, uint32_t k
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
         const uint32_t v = lm[i], w = i / 64;
         const uint64_t bit = 1ull << (i % 64);
-        atomicOr(reinterpret_cast<unsigned long long *>(rec + (size_t)v * rs + w), bit);
-        atomicOr(reinterpret_cast<unsigned long long *>(rec + (size_t)v * rs + H + w), bit);
+        if (rec) {
+            atomicOr(reinterpret_cast<unsigned long long *>(rec + (size_t)v * rs + w), bit);
+            atomicOr(reinterpret_cast<unsigned long long *>(rec + (size_t)v * rs + H + w), bit);
+        }
         if (bits0 && w >= a0 && w < e0) atomicOr(&bits0[v >> 5], 1u << (v & 31));
         if (bits1 && H + w >= a1 && H + w < e1) atomicOr(&bits1[v >> 5], 1u << (v & 31));
     }
 }
 
 dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_t *bits1, uint32_t a0,
-                          uint32_t e0, uint32_t a1, uint32_t e1) {
+                          uint32_t e0, uint32_t a1, uint32_t e1, bool write_rec) {
     const uint32_t n = g->n, k = idx->cfg.k;
     const bool do_lm = idx->sel_landmarks && k > 0;
     if (k > n) { set_error("k exceeds vertex count"); return DBL_E_CONFIG; }
@@ -451,7 +456,7 @@ dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_
     A.ovr = idx->ovr.p ? idx->ovr.as<uint32_t>() : nullptr;
     A.flags = idx->leaf_flags.as<uint8_t>();
     A.bucket = idx->bucket.as<uint32_t>();
-    A.rec = idx->rec.as<uint64_t>();
+    A.rec = write_rec ? idx->rec.as<uint64_t>() : nullptr;
     A.wdl = idx->wdl;
     A.wbl = idx->wbl;
     A.bits0 = bits0;

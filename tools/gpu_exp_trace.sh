@@ -1,6 +1,7 @@
 set -x
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -3 gpurun_out/pytest_gpu.log
-DBL_TRACE=1 timeout 600 python tools/cfg5_query.py --nq 100000 --reps 1 --builds 2 2>&1 | grep "build:" | tail -7
-timeout 600 python tools/cfg5_query.py --builds 3 2>&1 | tail -1
-timeout 300 python tools/qbench.py 2>&1 | tail -1
+for v in "" "DBL_PREP_RECORDS=1" ""; do
+  env $v timeout 300 python tools/qbench.py 2>&1 | tail -1
+  env $v timeout 600 python tools/cfg5_query.py --nq 1000000 --builds 3 2>&1 | tail -1
+done
