@@ -44,8 +44,43 @@ __device__ __forceinline__ uint32_t ld_cg32(const uint32_t *p) {
     return v;
 }
 
+__device__ __forceinline__ void ld_cg256(const uint64_t *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
+    asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+
+template <int NW, int AL>
+__device__ __forceinline__ void load_chunked(const uint64_t *p, uint64_t (&w)[NW]) {
+    const uint64_t *b = p - AL;
+    uint64_t c0, c1, c2, c3;
+    ld_cg256(b, c0, c1, c2, c3);
+    const uint64_t lo[4] = {c0, c1, c2, c3};
+#pragma unroll
+    for (int k = 0; k < NW && k + AL < 4; ++k) w[k] = lo[k + AL];
+    if constexpr (AL + NW > 4) {
+        ld_cg256(b + 4, c0, c1, c2, c3);
+        const uint64_t hi[4] = {c0, c1, c2, c3};
+#pragma unroll
+        for (int k = 4 - AL; k < NW; ++k) w[k] = hi[k + AL - 4];
+    }
+}
+
+// NW label words at p.  `al` (warp-uniform, from DirParams) is p's offset in
+// words inside a 32-byte chunk when the record stride keeps chunks aligned,
+// else -1.  5-word groups (the k = 256, k' = 64 halves) then load the covering
+// 32-byte chunks -- two requests instead of one per word: random label reads
+// are bound by L1->L2 requests, not bytes (tools/ubench_gather.cu).
 template <int NW, bool VEC>
-__device__ __forceinline__ void load_words(const uint64_t *p, uint64_t (&w)[NW]) {
+__device__ __forceinline__ void load_words(const uint64_t *p, uint64_t (&w)[NW], int al) {
+    if constexpr (NW == 5) {   // (3- and 4-word groups spill at 64 registers with the 4-way switch)
+        if (al >= 0) {
+            switch (al) {   // warp-uniform; compile-time register indices in each case
+            case 0: load_chunked<NW, 0>(p, w); return;
+            case 1: load_chunked<NW, 1>(p, w); return;
+            case 2: load_chunked<NW, 2>(p, w); return;
+            default: load_chunked<NW, 3>(p, w); return;
+            }
+        }
+    }
     if constexpr (VEC && (NW % 2 == 0)) {
 #pragma unroll
         for (int k = 0; k < NW; k += 2) ld_cg128(p + k, w[k], w[k + 1]);
@@ -135,7 +170,7 @@ template <int NW, bool VEC>
 __device__ __forceinline__ bool relax_mark(const DirParams &D, uint32_t y, const uint64_t (&s)[NW]) {
     uint64_t *p = D.lab + (size_t)y * D.stride;
     uint64_t c[NW];
-    load_words<NW, VEC>(p, c);
+    load_words<NW, VEC>(p, c, D.al);
     bool ch = false;
 #pragma unroll
     for (int k = 0; k < NW; ++k) {
@@ -189,7 +224,7 @@ __device__ __forceinline__ void expand_range(const DirParams &D, uint32_t nitems
             const uint32_t x = ld_cg32(Q.x + i);
             wD = (lf & DELTA_BIT) ? 1 : 0;
             wEnd = wE + (lf & ~DELTA_BIT);
-            load_words<NW, VEC>(D.lab + (size_t)x * D.stride, w);
+            load_words<NW, VEC>(D.lab + (size_t)x * D.stride, w, D.al);
         } else {
             wE = 0xffffffffu;
             wEnd = 0;
@@ -242,7 +277,7 @@ __device__ __forceinline__ void expand_range(const DirParams &D, uint32_t nitems
         uint64_t cur[U][NW];
 #pragma unroll
         for (int r = 0; r < U; ++r)
-            if (ok[r]) load_words<NW, VEC>(D.lab + (size_t)ys[r] * D.stride, cur[r]);
+            if (ok[r]) load_words<NW, VEC>(D.lab + (size_t)ys[r] * D.stride, cur[r], D.al);
 #pragma unroll
         for (int r = 0; r < U; ++r) {
             if (!ok[r]) continue;
@@ -305,7 +340,7 @@ __device__ __forceinline__ void pull_range(const DirParams &D, const uint32_t *_
         for (int j = 0; j < NW; ++j) acc[j] = 0;
         if (ok) {
             const uint32_t p = __ldg(col + ei);
-            if ((D.cur[p >> 5] >> (p & 31)) & 1) load_words<NW, VEC>(D.lab + (size_t)p * D.stride, acc);
+            if ((D.cur[p >> 5] >> (p & 31)) & 1) load_words<NW, VEC>(D.lab + (size_t)p * D.stride, acc, D.al);
         }
         // segmented inclusive OR-scan over lanes holding the same row
 #pragma unroll
@@ -325,7 +360,7 @@ __device__ __forceinline__ void pull_range(const DirParams &D, const uint32_t *_
         if (seg_last && any) {
             uint64_t *q = D.lab + (size_t)x * D.stride;
             uint64_t cur[NW];
-            load_words<NW, VEC>(q, cur);
+            load_words<NW, VEC>(q, cur, D.al);
             bool ch = false;
 #pragma unroll
             for (int j = 0; j < NW; ++j) {
@@ -635,7 +670,7 @@ __global__ void insert_seed_kernel(FixParams P, const uint64_t *__restrict__ key
             const DirParams &D = P.d[d];
             const uint32_t src = d == 0 ? u : v, dst = d == 0 ? v : u;
             uint64_t s[NW];
-            load_words<NW, VEC>(D.lab + (size_t)src * D.stride, s);
+            load_words<NW, VEC>(D.lab + (size_t)src * D.stride, s, D.al);
             if (relax_mark<NW, VEC>(D, dst, s)) atomicOr(&P.ctrl->seed_changed[d], 1u);
         }
     }
@@ -775,10 +810,12 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
         D.changed_bits = count ? g->changed_bits.as<uint32_t>() + d * (((size_t)g->n + 31) / 32) : nullptr;
         if (gr[d]) {
             D.lab = idx->rec.as<uint64_t>() + gr[d]->w0;
+            D.al = (idx->rs % 4 == 0 && !std::getenv("DBL_NO_CHUNK_LOADS")) ? (int)(gr[d]->w0 % 4) : -1;
             nw = gr[d]->nw;
             if ((gr[d]->w0 % 2) || (idx->rs % 2)) vec = false;
         } else {
             D.lab = idx->rec.as<uint64_t>();
+            D.al = -1;
         }
     }
     P.ctrl = g->ctrl.as<Ctrl>();

@@ -147,6 +147,7 @@ struct DirParams {
     Adj padj;                 // pull adjacency (the opposite direction)
     uint64_t *lab;
     uint32_t stride;
+    int al;                   // lab's word offset in a 32-byte chunk (stride % 4 == 0), else -1
     uint32_t *bits;           // next-frontier bitmap (n bits)
     uint32_t *cur;            // current-frontier bitmap (pull levels)
     Queue q;                  // current level's work items
