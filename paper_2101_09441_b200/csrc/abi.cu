@@ -647,11 +647,11 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
         }
         if (!pinned) return query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
         if ((s = run_query(idx, g, (const uint32_t *)dptr[0], (const uint32_t *)dptr[1], count, flags,
-                           (uint8_t *)dptr[2], (uint32_t *)dptr[3])))
+                           (uint8_t *)dptr[2], (uint32_t *)dptr[3], sync)))
             return s;
     } else {
         if (count && (s = order_after_caller(g))) return s;
-        if ((s = run_query(idx, g, u, v, count, flags, codes, visited))) return s;
+        if ((s = run_query(idx, g, u, v, count, flags, codes, visited, sync))) return s;
     }
     if (!sync) return DBL_OK;
     uint32_t err = 0;

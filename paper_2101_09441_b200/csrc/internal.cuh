@@ -284,6 +284,8 @@ dbl_status work_model(const dbl_index *idx, dbl_graph *g, uint64_t *V, uint64_t 
                       uint32_t *levels);
 // query.cu
 void query_timings(dbl_graph *g);
+// host_result: the closing CTA also writes the result words into the pinned
+// g->q_host_res (synchronous calls read them there after the stream sync)
 dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
-                     uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited);
+                     uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, bool host_result = false);
 }  // namespace dbl

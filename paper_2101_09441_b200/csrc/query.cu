@@ -68,6 +68,7 @@ struct QueryDesc {
     int vec_ok;
     int pad;
     Pivot pv;
+    uint32_t *hres;   // pinned host copy of the result words (written by the closing CTA), or nullptr
 };
 
 __device__ __forceinline__ bool in_pivot(const Pivot &pv, uint32_t x) {
@@ -831,16 +832,22 @@ __device__ __forceinline__ void load_pairs(const uint32_t *__restrict__ qu, cons
 
 // Close a batch: publish the live counters to the result words and zero them
 // for the next batch (stream order makes this the batch's last access).
-__device__ __forceinline__ void close_batch(uint32_t *counters) {
+// The batch's last CTA moves the live counters to the result words (and to
+// the caller-visible pinned copy, so the host reads them after its stream
+// sync without a device->host copy) and zeroes them for the next batch.
+__device__ __forceinline__ void close_batch(uint32_t *counters, uint32_t *hres) {
 #pragma unroll
     for (int i = 0; i < CNT_WORDS; ++i) {
-        counters[CNT_RES + i] = counters[i];
+        const uint32_t c = counters[i];
+        counters[CNT_RES + i] = c;
+        if (hres) hres[i] = c;
         counters[i] = 0;
     }
+    if (hres) __threadfence_system();
 }
 
-__global__ void finish_batch_kernel(uint32_t *__restrict__ counters) {
-    if (threadIdx.x == 0) close_batch(counters);
+__global__ void finish_batch_kernel(uint32_t *__restrict__ counters, uint32_t *hres) {
+    if (threadIdx.x == 0) close_batch(counters, hres);
 }
 
 // Launch geometry of the hard path, handed to the fused kernel so that its
@@ -1007,13 +1014,13 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
             __threadfence();
             const uint32_t npend = *(volatile uint32_t *)&counters[CNT_PENDING];
             if (npend == 0) {
-                close_batch(counters);
+                close_batch(counters, qd.hres);
             } else {
                 bfs_kernel<false><<<ha.grid, BFS_THREADS, ha.smem, cudaStreamTailLaunch>>>(
                     rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, nullptr);
                 bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
                     rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
-                finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters);
+                finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters, qd.hres);
             }
         }
     }
@@ -1167,13 +1174,13 @@ query_quad_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Q
             __threadfence();
             const uint32_t npend = *(volatile uint32_t *)&counters[CNT_PENDING];
             if (npend == 0) {
-                close_batch(counters);
+                close_batch(counters, qd.hres);
             } else {
                 bfs_kernel<false><<<ha.grid, BFS_THREADS, ha.smem, cudaStreamTailLaunch>>>(
                     rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, nullptr);
                 bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
                     rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
-                finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters);
+                finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters, qd.hres);
             }
         }
     }
@@ -1519,7 +1526,7 @@ __global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_W
         if (atomicAdd(&counters[CNT_DONE], 1u) == gridDim.x - 1) {
             __threadfence();
             if (*(volatile uint32_t *)&counters[CNT_PENDING] == 0) {
-                close_batch(counters);
+                close_batch(counters, qd.hres);
             } else {
                 counters[CNT_DONE] = 0;
                 bfs_warp_kernel<WDL, WBL><<<ha.wgrid, FUSED_THREADS, ha.wsmem, cudaStreamTailLaunch>>>(
@@ -1583,7 +1590,7 @@ bfs_warp_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Que
     __threadfence();
     const uint32_t nov = *(volatile uint32_t *)&counters[CNT_WOVF];
     if (nov == 0) {
-        if (threadIdx.x == 0) close_batch(counters);
+        if (threadIdx.x == 0) close_batch(counters, qd.hres);
         return;
     }
     for (uint32_t i = threadIdx.x; i < nov; i += blockDim.x) pending[i] = wovf[i];
@@ -1595,7 +1602,7 @@ bfs_warp_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Que
             rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, nullptr);
         bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
             rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
-        finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters);
+        finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters, qd.hres);
     }
 }
 
@@ -1678,7 +1685,7 @@ static bool pivot_prune_off() {
 }
 
 dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
-                     uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited) {
+                     uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, bool host_result) {
     if (count >= 0xffffffffull) { set_error("query batch too large"); return DBL_E_ARG; }
     if (idx->wdl > MAXW || idx->wbl > MAXW) {
         set_error("label width too large for the query kernels");
@@ -1696,7 +1703,9 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
         if ((s = g->q_counters.ensure(CNT_ALL * 4))) return s;
         DBL_CUDA(cudaMemsetAsync(g->q_counters.p, 0, CNT_ALL * 4, g->stream));
     }
-    QueryDesc qd{u, v, codes, visited, (uint32_t)count, flags, 0, 0, Pivot{}};
+    if ((s = g->q_host_res.ensure(CNT_WORDS * 4))) return s;
+    QueryDesc qd{u, v, codes, visited, (uint32_t)count, flags, 0, 0, Pivot{},
+                 host_result ? reinterpret_cast<uint32_t *>(g->q_host_res.p) : nullptr};
     if (idx->has_scc && !pivot_prune_off()) {
         qd.pv.dmask = idx->dmask.as<uint32_t>();
         qd.pv.scc = idx->sccmask.as<unsigned long long>();
@@ -1790,7 +1799,7 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
                                                                          g->q_dense.as<char>());
         DBL_CHECK_LAUNCH("bfs_kernel_dense");
     }
-    finish_batch_kernel<<<1, 32, 0, g->stream>>>(counters);
+    finish_batch_kernel<<<1, 32, 0, g->stream>>>(counters, qd.hres);
     DBL_CHECK_LAUNCH("finish_batch_kernel");
     DBL_CUDA(cudaEventRecord(g->ev[4], g->stream));
     g->q_timed_bfs = true;
@@ -1813,16 +1822,11 @@ void query_timings(dbl_graph *g) {
 }
 
 dbl_status query_finish(dbl_graph *g, uint32_t *err_out) {
-    // pinned staging: the D2H copy is a plain async copy and the stream
-    // synchronisation is the batch's only host wait
-    dbl_status s = g->q_host_res.ensure(CNT_WORDS * 4);
-    if (s) return s;
-    uint32_t *h = reinterpret_cast<uint32_t *>(g->q_host_res.p);
-    DBL_CUDA(cudaMemcpyAsync(h, g->q_counters.as<uint32_t>() + CNT_RES, CNT_WORDS * 4, cudaMemcpyDeviceToHost,
-                             g->stream));
+    // the closing CTA wrote the result words into the pinned q_host_res:
+    // the stream synchronisation is the batch's only host step (timings are
+    // read lazily by dbl_last_timings)
     DBL_CUDA(cudaStreamSynchronize(g->stream));
-    query_timings(g);
-    *err_out = h[CNT_ERR];
+    *err_out = reinterpret_cast<const volatile uint32_t *>(g->q_host_res.p)[CNT_ERR];
     return DBL_OK;
 }
 
