@@ -1046,6 +1046,9 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t x, int src) {
     return ((uint64_t)hi << 32) | lo;
 }
 
+#ifndef DBL_QUAD_DEFER
+#define DBL_QUAD_DEFER 1
+#endif
 template <int WDL, int WBL>
 __global__ void __launch_bounds__(FUSED_THREADS, DBL_QMINB)
 query_quad_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const QueryDesc qd,
@@ -1061,6 +1064,8 @@ query_quad_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Q
     const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
     const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
     const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
+    if (lane == 0) B.nq = 0;
+    __syncwarp();
     for (;;) {
         uint32_t tile = 0;
         if (lane == 0) tile = atomicAdd(&counters[CNT_TILE], 1u);
@@ -1137,9 +1142,18 @@ query_quad_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Q
         }
         const uint32_t mask = __ballot_sync(FULL, unres);
         if (mask) {
-            // stage the unresolved queries (<= 32) and answer them right away
+            // stage the unresolved queries; the bit-parallel BFS runs once 32
+            // have accumulated (and after the last tile): on cfg5 ~17% of
+            // tiles hold one, and a BFS of 1 query costs the warp the same
+            // latency chain as one of 32
+            uint32_t nq0 = B.nq;
+            if (nq0 + __popc(mask) > 32) {
+                warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.pv, qd.codes, qd.visited, pending,
+                                         counters, CNT_PENDING);
+                nq0 = 0;
+            }
             if (unres) {
-                const uint32_t slot = __popc(mask & ((1u << lane) - 1u));
+                const uint32_t slot = nq0 + __popc(mask & ((1u << lane) - 1u));
                 B.qidx[slot] = (uint32_t)q;
                 B.qu[slot] = u;
                 B.qv[slot] = v;
@@ -1148,7 +1162,7 @@ query_quad_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Q
             for (int r = 0; r < 4; ++r) {
                 const int lq = 8 * r + qi;
                 if (!((mask >> lq) & 1u)) continue;
-                const uint32_t slot = __popc(mask & ((1u << lq) - 1u));
+                const uint32_t slot = nq0 + __popc(mask & ((1u << lq) - 1u));
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                     const int w = 4 * qj + t;
@@ -1157,13 +1171,20 @@ query_quad_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Q
                     if (w >= H + WDL && w < RW) B.qblo[slot * WBL + (w - H - WDL)] = cv[r][t];
                 }
             }
-            if (lane == 0) B.nq = __popc(mask);
             __syncwarp();
+            if (lane == 0) B.nq = nq0 + __popc(mask);
+            __syncwarp();
+#if !DBL_QUAD_DEFER
             warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.pv, qd.codes, qd.visited, pending, counters,
                                      CNT_PENDING);
             __syncwarp();
+#endif
         }
     }
+    __syncwarp();
+    if (B.nq)
+        warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.pv, qd.codes, qd.visited, pending, counters,
+                                 CNT_PENDING);
     // the last CTA out closes the batch, or tail-launches the group/dense
     // kernels for BFS batches that outgrew the warp tables
     __syncthreads();
