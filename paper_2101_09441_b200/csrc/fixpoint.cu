@@ -952,7 +952,10 @@ __device__ __forceinline__ bool any_marked(const Adj &a, const uint32_t *vis, ui
     return false;
 }
 
-__global__ void __launch_bounds__(256, 8) reach_kernel(ReachParams P) {
+#ifndef DBL_REACH_MINB
+#define DBL_REACH_MINB 6   // 40 registers, no spills: measured best (8: 0.283, 6: 0.280, 4: 0.287 ms on cfg2)
+#endif
+__global__ void __launch_bounds__(256, DBL_REACH_MINB) reach_kernel(ReachParams P) {
     cg::grid_group grid = cg::this_grid();
     const uint32_t h = P.lm[0];
     const bool have = h < P.n;   // grid-uniform (landmarks are validated, so always in practice)
@@ -1351,7 +1354,9 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
     // (one write of the table instead of seed + read-modify-write)
     static const bool rec_in_prep = std::getenv("DBL_PREP_RECORDS") != nullptr;
     const bool pivot = idx->cfg.k && pivot_on();
-    const bool pivot_writes = prep && pivot && !rec_in_prep;
+    // (measured: wins on padded k = 256 records, cfg5 9.3 -> 8.4 ms; costs ~4 us
+    // on 32-byte records, cfg2, where prep's write is cheap)
+    const bool pivot_writes = prep && pivot && !rec_in_prep && idx->rs > 4;
     if (prep) {
         const Group **p0 = pairs[0];
         uint32_t *b0 = p0[0] ? g->stamp[0].as<uint32_t>() : nullptr;

@@ -289,7 +289,22 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
         // each store instruction covers 512 bytes, whole sectors and lines
         // (per-record 16-byte stores at the record stride are partial-sector
         // writes, which cost L2 read-fills)
-        if (A.rec) {
+#ifndef DBL_PREP_COALESCED_ALL
+#define DBL_PREP_COALESCED_ALL 0
+#endif
+        if (A.rec && !DBL_PREP_COALESCED_ALL && rs <= 4) {
+            // one-sector records: the thread's own two 16-byte stores complete
+            // its sector (no partial-sector fills)
+            if (i < A.n) {
+                uint64_t *r = A.rec + i * rs;
+                for (uint32_t w = 0; w < rw; w += 2) {
+                    ulonglong2 val;
+                    val.x = (w == win || w == wout) ? bit : 0ull;
+                    val.y = (w + 1 == win || w + 1 == wout) ? bit : 0ull;
+                    *reinterpret_cast<ulonglong2 *>(r + w) = val;
+                }
+            }
+        } else if (A.rec) {
             const uint64_t v0 = i - lane;
             uint64_t *blk = A.rec + v0 * rs;
             for (uint32_t t = 0; t < rs * 32; t += 64) {
