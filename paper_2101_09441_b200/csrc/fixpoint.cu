@@ -961,10 +961,12 @@ __device__ __forceinline__ bool any_marked(const Adj &a, const uint32_t *vis, ui
     return false;
 }
 
-#ifndef DBL_REACH_MINB
-#define DBL_REACH_MINB 6   // 40 registers, no spills: measured best (8: 0.283, 6: 0.280, 4: 0.287 ms on cfg2)
-#endif
-__global__ void __launch_bounds__(256, DBL_REACH_MINB) reach_kernel(ReachParams P) {
+// CTAs per SM as a template: 6 (40 registers, no spills) is best on cfg2
+// (8: 0.283, 6: 0.280, 4: 0.287 ms per build), 8 (32 registers, a few spills)
+// on cfg5's 2^26 vertices (reach 4.8 vs 5.1 ms): the latency-bound sweeps
+// want the occupancy once the graph is large
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
     cg::grid_group grid = cg::this_grid();
     const uint32_t h = P.lm[0];
     const bool have = h < P.n;   // grid-uniform (landmarks are validated, so always in practice)
@@ -1296,14 +1298,16 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     static const bool tr = std::getenv("DBL_TRACE") != nullptr;
     unsigned long long *trb = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(chg) + 64);
     R.tr = tr ? trb : nullptr;
-    static int bps = -1;
+    const bool big = n >= (1u << 24);
+    const void *kern = big ? (const void *)reach_kernel<8> : (const void *)reach_kernel<6>;
+    static int bps_s[2] = {-1, -1};
+    int &bps = bps_s[big ? 1 : 0];
     if (bps < 0) {
-        DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, reach_kernel, 256, 0));
+        DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0));
         if (bps < 1) bps = 1;
     }
     void *args[] = {(void *)&R};
-    DBL_CUDA(cudaLaunchCooperativeKernel((const void *)reach_kernel, dim3(g->sm_count * bps), dim3(256), args, 0,
-                                         g->stream));
+    DBL_CUDA(cudaLaunchCooperativeKernel(kern, dim3(g->sm_count * bps), dim3(256), args, 0, g->stream));
     DBL_LAUNCHED();
     if (std::getenv("DBL_TRACE")) {
         unsigned int hc[6];
