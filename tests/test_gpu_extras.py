@@ -153,3 +153,35 @@ def test_estimator_mutations_stay_truthful():
     og = O.OracleGraph(n, src, dst)
     truth = og.reach_batch([p[0] for p in pairs], [p[1] for p in pairs])
     assert est.predict(pairs) == truth.tolist()
+
+
+@pytest.mark.parametrize("k", [128, 256])
+def test_wide_records_roundtrip_and_verify(k):
+    """Padded record strides (k = 128: 48 -> 64 B, k = 256: 80 -> 128 B):
+    snapshot save/load (import into a fresh index), export/import, the
+    exhaustive verifier (a fresh rebuild compared record by record, pad words
+    included via labels_equal), and answers vs the oracle on the same labels."""
+    from paper_2101_09441_b200 import workload as W
+    s, d = W.rmat_edges(14, 8, 9)
+    n = 1 << 14
+    g = E.DynamicGraph.from_edges(n, s, d)
+    idx = E.build_index(g, E.IndexConfig(k=k, k_prime=64))
+    buf = io.BytesIO()
+    E.save_index(idx, buf)
+    loaded = E.load_index(io.BytesIO(buf.getvalue()), g)
+    assert loaded.labels_equal(idx)
+    assert E.verify_labels(g, idx, exhaustive=True).ok
+    assert E.verify_labels(g, loaded, exhaustive=True).ok
+    w = idx.export_words()
+    other = E.rebuild_index(g, idx)
+    other.import_words(w)
+    assert other.labels_equal(idx)
+    og = O.OracleGraph(n, s, d)
+    oidx = og.build(k, 64, threads=8)
+    for f in ("dl_in", "dl_out", "bl_in", "bl_out"):
+        np.testing.assert_array_equal(w[f], getattr(oidx, f), err_msg=f)
+    qu, qv = W.uniform_queries(n, 200_000, 11)
+    out, _ = E.query_batch(g, loaded, (qu, qv))
+    oc, ov = og.query_batch(oidx, qu, qv, threads=8)
+    np.testing.assert_array_equal(out.codes, oc)
+    np.testing.assert_array_equal(out.visited == 0, ov == 0)
