@@ -381,7 +381,10 @@ __device__ __forceinline__ void pull_range(const DirParams &D, const uint32_t *_
 template <bool COUNT>
 __device__ __forceinline__ void compact_bitmap(const DirParams &D, uint32_t nwords, uint32_t gwarp, uint32_t nwarps,
                                                unsigned long long *cnt_ptr, Ctrl *ctrl, uint32_t &nchanged) {
-    constexpr int R = 4;
+#ifndef DBL_COMPACT_R
+#define DBL_COMPACT_R 4
+#endif
+    constexpr int R = DBL_COMPACT_R;
     const int lane = threadIdx.x & 31;
     const uint32_t per = (nwords + nwarps - 1) / nwarps;
     const uint32_t w0 = gwarp * per, w1 = min(w0 + per, nwords);
