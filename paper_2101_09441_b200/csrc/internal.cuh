@@ -117,7 +117,10 @@ struct Queue {
 // Device state of the fused build prep (select.cu): score histogram for the
 // landmark top-k, candidate counts, and the flags the host reads once the
 // build has finished (no host round trip inside the build).
-constexpr uint32_t PREP_CAND_CAP = 8192;   // top-k candidates sorted on chip
+#ifndef DBL_PREP_CAND_CAP
+#define DBL_PREP_CAND_CAP 8192
+#endif
+constexpr uint32_t PREP_CAND_CAP = DBL_PREP_CAND_CAP;   // top-k candidates sorted on chip
 struct PrepState {
     uint32_t hist[65];
     uint32_t n_above, n_tie;
