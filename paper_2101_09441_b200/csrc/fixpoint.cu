@@ -968,6 +968,9 @@ __device__ __forceinline__ bool any_marked(const Adj &a, const uint32_t *vis, ui
 // (8: 0.283, 6: 0.280, 4: 0.287 ms per build), 8 (32 registers, a few spills)
 // on cfg5's 2^26 vertices (reach 4.8 vs 5.1 ms): the latency-bound sweeps
 // want the occupancy once the graph is large
+#ifndef DBL_BU_ILP
+#define DBL_BU_ILP 1
+#endif
 template <int MINB>
 __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
     cg::grid_group grid = cg::this_grid();
@@ -1024,6 +1027,62 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
         const int cb = step % 3;
         unsigned marks = 0;
         if (!td) {
+#if DBL_BU_ILP
+            // two vertices x both directions per iteration: the four
+            // dependent chains (bitmap word -> row pointers -> first
+            // neighbour -> its bitmap bit) run interleaved, so a sweep pays
+            // about half the serial round trips; most vertices stop at the
+            // first neighbour, the rest continue with the serial scan
+            for (uint64_t x0 = tid; x0 < P.n; x0 += 2 * nth) {
+                uint32_t xv[2], w[2][2], s0[2][2], s1[2][2], c0[2][2];
+                bool need[2][2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const uint64_t x = x0 + i * nth;
+                    xv[i] = (uint32_t)x;
+#pragma unroll
+                    for (int d = 0; d < 2; ++d)
+                        w[i][d] = x < P.n ? *(volatile uint32_t *)&P.vis[d][x >> 5] : ~0u;
+                }
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int d = 0; d < 2; ++d) {
+                        need[i][d] = !((w[i][d] >> (xv[i] & 31)) & 1u);
+                        s0[i][d] = s1[i][d] = 0;
+                        if (need[i][d]) {
+                            s0[i][d] = __ldg(P.adj[d].ptr + xv[i]);
+                            s1[i][d] = __ldg(P.adj[d].ptr + xv[i] + 1);
+                        }
+                    }
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int d = 0; d < 2; ++d)
+                        c0[i][d] = (need[i][d] && s1[i][d] > s0[i][d]) ? __ldg(P.adj[d].col + s0[i][d]) : 0xffffffffu;
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int d = 0; d < 2; ++d) {
+                        if (!need[i][d]) continue;
+                        bool hit = c0[i][d] != 0xffffffffu && vis_test_ca(P.vis[d], c0[i][d]);
+                        if (!hit) {
+                            const Adj &a = P.adj[d];
+                            for (uint32_t j = s0[i][d] + 1; j < s1[i][d] && !hit; ++j)
+                                hit = vis_test_ca(P.vis[d], __ldg(a.col + j));
+                            if (!hit && a.dptr) {
+                                const uint32_t t0 = __ldg(a.dptr + xv[i]), t1 = __ldg(a.dptr + xv[i] + 1);
+                                for (uint32_t j = t0; j < t1 && !hit; ++j) hit = vis_test_ca(P.vis[d], __ldg(a.dcol + j));
+                            }
+                        }
+                        if (hit) {
+                            atomicOr(&P.vis[d][xv[i] >> 5], 1u << (xv[i] & 31));
+                            atomicOr(&P.nb[d][cb][xv[i] >> 5], 1u << (xv[i] & 31));
+                            ++marks;
+                        }
+                    }
+            }
+#else
             for (uint64_t x = tid; x < P.n; x += nth) {
 #pragma unroll
                 for (int d = 0; d < 2; ++d) {
@@ -1036,6 +1095,7 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
                     }
                 }
             }
+#endif
             ++bu;
         } else {
             const int pb = (step + 2) % 3;   // the previous step's marks
