@@ -233,16 +233,30 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
     const uint64_t nr = ((uint64_t)A.n + 31) & ~31ull;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += stride) {
+    // the next vertex's row pointers are loaded while this one is processed
+    // (one dependent round trip per vertex instead of two)
+    const bool degs = A.do_lm || A.do_leaves;
+    const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    uint32_t nf0 = 0, nf1 = 0, nr0 = 0, nr1 = 0;
+    if (degs && i0 < A.n) {
+        nf0 = __ldg(A.f.ptr + i0); nf1 = __ldg(A.f.ptr + i0 + 1);
+        nr0 = __ldg(A.r.ptr + i0); nr1 = __ldg(A.r.ptr + i0 + 1);
+    }
+    for (uint64_t i = i0; i < nr; i += stride) {
         bool p0 = false, p1 = false;
         uint32_t win = 0xffffffffu, wout = 0xffffffffu;
         uint64_t bit = 0;
+        const uint32_t cf0 = nf0, cf1 = nf1, cr0 = nr0, cr1 = nr1;
+        if (degs && i + stride < A.n) {
+            nf0 = __ldg(A.f.ptr + i + stride); nf1 = __ldg(A.f.ptr + i + stride + 1);
+            nr0 = __ldg(A.r.ptr + i + stride); nr1 = __ldg(A.r.ptr + i + stride + 1);
+        }
         if (i < A.n) {
             const uint32_t v = (uint32_t)i;
             uint8_t f;
             uint32_t b;
-            if (A.do_lm || A.do_leaves) {
-                uint64_t out = A.f.ptr[v + 1] - A.f.ptr[v], in = A.r.ptr[v + 1] - A.r.ptr[v];
+            if (degs) {
+                uint64_t out = cf1 - cf0, in = cr1 - cr0;
                 if (A.f.dptr) { out += A.f.dptr[v + 1] - A.f.dptr[v]; in += A.r.dptr[v + 1] - A.r.dptr[v]; }
                 if (A.do_lm) {
                     const uint64_t sc = strategy_score(A.strategy, in, out);
