@@ -1013,6 +1013,7 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
     // of the few new marks).  Every mark is also recorded in nb[d][s % 3].
     bool capped = false, td = false;
     uint32_t bu = 0;
+    unsigned prev_got = 0xffffffffu;
     for (uint32_t step = 0; have; ++step) {
         if (step == P.max_steps || (!td && bu == P.max_sweeps)) {
             // deep graph: the marked sets are only parts of D(h) / A(h), not
@@ -1145,7 +1146,12 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
             if (tid == 0) { P.changed[4] = step + 1; P.changed[5] = bu; }
             break;
         }
-        if (!td && got < P.td_switch) td = true;
+        // switch on the shrinking tail only: a growing frontier (a pivot with
+        // few neighbours, uniform random graphs: cfg1) stays bottom-up --
+        // top-down levels take one thread per bitmap word and serialise on
+        // large frontiers (cfg1: 0.25 -> 1.06 ms when it switched at step 0)
+        if (!td && step >= 1 && got < P.td_switch && got < prev_got) td = true;
+        prev_got = got;
     }
     // keep D(h) and the SCC landmarks for query pruning (marks are exact
     // members even when the sweeps were capped)
