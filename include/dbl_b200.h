@@ -5,8 +5,9 @@
  * Python API listed in SURVEY.md §8(b).  Each entry point below replaces
  * one reference function (paths relative to
  * /root/reference/pkg/src/dblreach/).  The Python shim
- * paper_2101_09441_b200/api.py binds these with ctypes under the
- * reference's own names; INTEGRATION.md shows the binding.
+ * paper_2101_09441_b200/ (_native.py binds these with ctypes; graph.py,
+ * labels.py, queries.py, updates.py keep the reference's own names) is the
+ * drop-in; INTEGRATION.md shows the binding a reference maintainer adds.
  *
  * Conventions
  *  - Every call returns a dbl_status; DBL_OK == 0.  On failure
@@ -96,6 +97,8 @@ typedef struct {
     uint64_t labels_changed;  /* distinct (vertex, direction) label changes */
     uint32_t levels;          /* fixpoint levels run                       */
     uint32_t delta_merged;    /* 1 if the delta adjacency was compacted    */
+    uint64_t fix_items;       /* delta fixpoint: frontier items expanded   */
+    uint64_t fix_edges;       /* delta fixpoint: edges relaxed             */
 } dbl_batch_stats;
 
 /* ---------------------------------------------------------------- misc */
@@ -208,11 +211,25 @@ dbl_status dbl_query(const dbl_index *idx, const dbl_graph *g, const uint32_t *u
                      const uint32_t *v, uint64_t count, uint32_t flags, uint8_t *codes,
                      uint32_t *visited, dbl_mem mem);
 /* Same as dbl_query but enqueued on the handle's stream without a final
- * synchronisation (device memory only); dbl_sync waits for it. */
+ * synchronisation (device memory only); dbl_sync waits for it.  A batch
+ * whose pruned BFS outgrows the shared-memory tables needs the dense
+ * workspace (n x 32 bytes per CTA), which is allocated on first need: such a
+ * batch is completed by dbl_sync (it re-runs the batch), so call dbl_sync
+ * before reading the codes of an async batch. */
 dbl_status dbl_query_async(const dbl_index *idx, const dbl_graph *g, const uint32_t *u,
                            const uint32_t *v, uint64_t count, uint32_t flags,
                            uint8_t *codes, uint32_t *visited);
 dbl_status dbl_sync(const dbl_graph *g);
+/* query_batch over several devices (the reference's worker
+ * pool, queries.py:224-247): the host batch is cut into ndev contiguous
+ * slices of ceil(count / ndev) pairs (queries.py:231-232) and slice d is
+ * answered by (idx[d], g[d]) -- identical replicas, one per device -- on its
+ * own host thread, all slices concurrently.  Results land in input order.
+ * mem must be DBL_MEM_HOST (device-resident batches: dbl_query per handle).
+ * Errors name the failing slice. */
+dbl_status dbl_query_multi(const dbl_index *const *idx, const dbl_graph *const *g, uint32_t ndev,
+                           const uint32_t *u, const uint32_t *v, uint64_t count, uint32_t flags,
+                           uint8_t *codes, uint32_t *visited, dbl_mem mem);
 /* Counters of the last query batch (8 x u32): [0] queries finished by the
  * 64-query group kernel, [1] range-error flag, [3] groups re-run densely. */
 dbl_status dbl_query_counters(const dbl_graph *g, uint32_t *out8);
@@ -267,6 +284,29 @@ dbl_status dbl_rmat_generate(uint32_t scale, uint64_t m, uint64_t seed, double a
  * level count.  Arrays hold 2*(ceil(k/64)+ceil(k'/64)) entries. */
 dbl_status dbl_work_model(const dbl_index *idx, const dbl_graph *g, uint64_t *V,
                           uint64_t *E, uint32_t *levels);
+/* Executed work of the last build on `g` (the bench's build roofline counts
+ * the bytes of this work, not the level-synchronous model above). */
+typedef struct {
+    uint64_t n, m;               /* graph size at the build                          */
+    uint32_t record_bytes;       /* record stride in bytes                           */
+    uint32_t flags;              /* bit0 prep wrote the seeded records; bit1 the pivot
+                                    pass wrote every record whole; bit2 the pivot pass
+                                    ORed its unions into the records (read + write);
+                                    bit3 the pivot sweeps hit their cap; bit4 word build */
+    uint32_t sweeps, steps;      /* pivot reach: bottom-up sweeps, all steps         */
+    uint32_t fix_levels, fix_runs; /* label fixpoint: levels over all runs, runs     */
+    uint64_t bu_tests;           /* pivot bottom-up (vertex, direction) tests        */
+    uint64_t bu_probes;          /* their neighbour probes                           */
+    uint64_t td_vertices, td_edges; /* pivot top-down levels                        */
+    uint64_t union_records;      /* records the pivot's union pass touched           */
+    uint64_t fix_items, fix_edges;  /* label fixpoint: frontier items, relaxed edges
+                                       (first 32 levels of each run)                 */
+} dbl_build_work;
+dbl_status dbl_build_work_stats(const dbl_graph *g, dbl_build_work *out);
+/* on != 0: later builds on g run the instrumented pivot kernel, which also
+ * fills the pivot fields of the dbl_build_work struct; the product kernel carries no
+ * counters, so without instrumentation those fields stay 0. */
+dbl_status dbl_graph_instrument(dbl_graph *g, int on);
 /* Device time (ms) of the last fixpoint launch and of the last query
  * label-check kernel, measured with CUDA events on the handle's stream. */
 dbl_status dbl_last_timings(const dbl_graph *g, float *fixpoint_ms, float *label_ms,

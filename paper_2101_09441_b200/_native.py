@@ -35,7 +35,15 @@ class UpdateStatsC(ctypes.Structure):
 
 class BatchStatsC(ctypes.Structure):
     _fields_ = [("requested", u64), ("inserted", u64), ("certified", u64),
-                ("labels_changed", u64), ("levels", u32), ("delta_merged", u32)]
+                ("labels_changed", u64), ("levels", u32), ("delta_merged", u32),
+                ("fix_items", u64), ("fix_edges", u64)]
+
+
+class BuildWorkC(ctypes.Structure):
+    _fields_ = [("n", u64), ("m", u64), ("record_bytes", u32), ("flags", u32), ("sweeps", u32),
+                ("steps", u32), ("fix_levels", u32), ("fix_runs", u32), ("bu_tests", u64),
+                ("bu_probes", u64), ("td_vertices", u64), ("td_edges", u64), ("union_records", u64),
+                ("fix_items", u64), ("fix_edges", u64)]
 
 
 # name -> argtypes (restype is always dbl_status / c_int unless listed)
@@ -69,6 +77,7 @@ _SIGS = {
     "dbl_label_tests": [P, P, P, u64, P, P],
     "dbl_query": [P, P, P, P, u64, u32, P, P, i32],
     "dbl_query_async": [P, P, P, P, u64, u32, P, P],
+    "dbl_query_multi": [P, P, u32, P, P, u64, u32, P, P, i32],
     "dbl_sync": [P],
     "dbl_query_counters": [P, P],
     "dbl_release_cached_memory": [],
@@ -76,6 +85,8 @@ _SIGS = {
     "dbl_insert_edge": [P, P, u32, u32, ctypes.POINTER(UpdateStatsC)],
     "dbl_insert_edges": [P, P, P, P, u64, i32, ctypes.POINTER(BatchStatsC)],
     "dbl_work_model": [P, P, P, P, P],
+    "dbl_build_work_stats": [P, ctypes.POINTER(BuildWorkC)],
+    "dbl_graph_instrument": [P, i32],
     "dbl_verify": [P, P, i32, u64, ctypes.POINTER(u64), P, P, P, P],
     "dbl_rmat_generate": [u32, u64, u64, ctypes.c_double, ctypes.c_double, ctypes.c_double, P, P, i32],
     "dbl_last_timings": [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float),
@@ -130,6 +141,32 @@ def device_inputs_ready(*tensors) -> None:
             if cur != torch.cuda.default_stream(t.device):
                 cur.synchronize()
             return
+
+
+def check_device_ids(u, v, device: int) -> None:
+    """Validate CUDA id tensors handed to kernels that read uint32 words.
+
+    The kernels take raw pointers, so an int64 tensor would be read as lo/hi
+    word pairs and a short `v` read out of bounds: require int32/uint32,
+    contiguous, on the graph's device, and equal lengths.
+    """
+    import torch
+    ok_types = {torch.int32}
+    if hasattr(torch, "uint32"):
+        ok_types.add(torch.uint32)
+    for name, t in (("u", u), ("v", v)):
+        if not (hasattr(t, "is_cuda") and t.is_cuda):
+            raise TypeError(f"{name} must be a CUDA tensor when the other one is")
+        if t.dtype not in ok_types:
+            raise TypeError(f"{name} must be an int32 or uint32 tensor of vertex ids, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if t.device.index != device:
+            raise ValueError(f"{name} lives on {t.device}, the graph on cuda:{device}")
+        if t.dim() != 1:
+            raise ValueError(f"{name} must be one-dimensional")
+    if u.numel() != v.numel():
+        raise ValueError(f"u and v differ in length ({u.numel()} vs {v.numel()})")
 
 
 def ptr(a) -> ctypes.c_void_p | None:

@@ -4,13 +4,16 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.cuh"
@@ -18,10 +21,10 @@
 namespace dbl {
 
 static thread_local std::string g_last_error;
-static uint64_t g_launches = 0;
+static std::atomic<uint64_t> g_launches{0};
 
 void set_error(const std::string &msg) { g_last_error = msg; }
-uint64_t &launch_counter() { return g_launches; }
+std::atomic<uint64_t> &launch_counter() { return g_launches; }
 
 // ------------------------------------------------------ caching allocator --
 // Each cached block remembers the stream that last used it (the calling
@@ -121,11 +124,10 @@ void pool_trim() {
     cudaSetDevice(cur);
 }
 
-static bool g_trace = std::getenv("DBL_TRACE") != nullptr;
 static auto g_trace_t0 = std::chrono::steady_clock::now();
 
 void trace(const char *what, cudaStream_t s) {
-    if (!g_trace) return;
+    if (!DBL_TRACE) return;
     cudaStreamSynchronize(s);
     auto now = std::chrono::steady_clock::now();
     double us = std::chrono::duration<double, std::micro>(now - g_trace_t0).count();
@@ -138,10 +140,35 @@ dbl_status cuda_fail(cudaError_t e, const char *what) {
     return e == cudaErrorMemoryAllocation ? DBL_E_OOM : DBL_E_CUDA;
 }
 
+// Occupancy cache: the dynamic shared-memory opt-in is a per-device function
+// attribute, and handles on different devices may be driven from different
+// host threads (dbl_query_multi), so both the attribute and the occupancy
+// are cached per (device, kernel, threads, smem) under a mutex.
+static std::mutex g_occ_mu;
+static std::map<std::tuple<int, const void *, int, size_t>, int> g_occ;
+
+dbl_status kernel_occupancy(const void *fn, int threads, size_t smem, int *bps) {
+    int dev = 0;
+    DBL_CUDA(cudaGetDevice(&dev));
+    const auto key = std::make_tuple(dev, fn, threads, smem);
+    {
+        std::lock_guard<std::mutex> lk(g_occ_mu);
+        auto it = g_occ.find(key);
+        if (it != g_occ.end()) { *bps = it->second; return DBL_OK; }
+    }
+    if (smem > 48 * 1024)
+        DBL_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int b = 0;
+    DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem));
+    if (b < 1) b = 1;
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    g_occ[key] = b;
+    *bps = b;
+    return DBL_OK;
+}
+
 dbl_status make_override(dbl_graph *g, const uint32_t *ids, const uint32_t *buckets, uint32_t cnt,
                          DevBuf &ovr);
-dbl_status query_finish(dbl_graph *g, uint32_t *err_out);
-dbl_status query_err_to(dbl_graph *g, uint32_t *dst);
 
 static int grid_for(uint64_t work, int threads = 256, int cap = 148 * 16) {
     uint64_t b = (work + threads - 1) / threads;
@@ -239,7 +266,7 @@ using namespace dbl;
 
 extern "C" const char *dbl_last_error(void) { return g_last_error.c_str(); }
 extern "C" int dbl_version(void) { return 1; }
-extern "C" uint64_t dbl_kernel_launches(void) { return g_launches; }
+extern "C" uint64_t dbl_kernel_launches(void) { return g_launches.load(); }
 extern "C" dbl_status dbl_release_cached_memory(void) {
     pool_trim();
     return DBL_OK;
@@ -563,6 +590,44 @@ extern "C" dbl_status dbl_index_records(const dbl_index *idx, uint64_t **dev_rec
     return DBL_OK;
 }
 
+extern "C" dbl_status dbl_graph_instrument(dbl_graph *g, int on) {
+    if (!g) { set_error("null graph"); return DBL_E_ARG; }
+    g->instrument = on != 0;
+    return DBL_OK;
+}
+
+// Executed work of the last build on g (bench roofline: bytes actually moved).
+extern "C" dbl_status dbl_build_work_stats(const dbl_graph *g, dbl_build_work *out) {
+    if (!g || !out) { set_error("null argument"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(g->device));
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    dbl_build_work w{};
+    w.n = g->n;
+    w.m = g->m_base + g->m_delta;
+    w.record_bytes = 8 * g->last_build.rs;
+    w.flags = g->last_build.flags;
+    w.fix_levels = g->last_build.fix_levels;
+    w.fix_runs = g->last_build.fix_runs;
+    w.fix_items = g->last_build.fix_items;
+    w.fix_edges = g->last_build.fix_edges;
+    if (g->reach_work) {
+        unsigned long long c[5];
+        unsigned int st[6];
+        DBL_CUDA(cudaMemcpy(c, g->reach_work, sizeof(c), cudaMemcpyDeviceToHost));
+        DBL_CUDA(cudaMemcpy(st, g->reach_chg, sizeof(st), cudaMemcpyDeviceToHost));
+        w.bu_tests = c[0];
+        w.bu_probes = c[1];
+        w.td_vertices = c[2];
+        w.td_edges = c[3];
+        w.union_records = c[4];
+        w.steps = st[4];
+        w.sweeps = st[5];
+        if (st[3]) w.flags |= 8u;
+    }
+    *out = w;
+    return DBL_OK;
+}
+
 // ---------------------------------------------------------------- queries --
 
 // Host-memory batches are pipelined in chunks: the H2D copy of chunk i+1
@@ -602,7 +667,7 @@ static dbl_status query_host_pipelined(const dbl_index *idx, dbl_graph *g, const
         DBL_CUDA(cudaEventRecord(g->cev[i], g->cstream[0]));
         DBL_CUDA(cudaStreamWaitEvent(g->stream, g->cev[i], 0));
         if ((s = run_query(idx, g, bu + lo, bv + lo, c, flags, dc + lo, dvis ? dvis + lo : nullptr))) return s;
-        if ((s = query_err_to(g, errs + i))) return s;
+        if ((s = query_err_to(g, errs + 4 * i))) return s;
         DBL_CUDA(cudaEventRecord(g->cev[16 + i], g->stream));
         DBL_CUDA(cudaStreamWaitEvent(g->cstream[1], g->cev[16 + i], 0));
         DBL_CUDA(cudaMemcpyAsync(codes + lo, dc + lo, c, cudaMemcpyDeviceToHost, g->cstream[1]));
@@ -612,8 +677,15 @@ static dbl_status query_host_pipelined(const dbl_index *idx, dbl_graph *g, const
     DBL_CUDA(cudaMemcpyAsync(herr, errs, 64 * 4, cudaMemcpyDeviceToHost, g->cstream[1]));
     DBL_CUDA(cudaStreamSynchronize(g->cstream[1]));
     DBL_CUDA(cudaStreamSynchronize(g->stream));
-    for (uint64_t i = 0; i < nch; ++i)
-        if (herr[i]) { set_error("query vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+    bool dense = false;
+    for (uint64_t i = 0; i < nch; ++i) {
+        if (herr[4 * i]) { set_error("query vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+        dense |= chunk_needs_dense(herr + 4 * i);
+    }
+    if (dense) {   // some chunk needed the dense BFS workspace: allocate it, run again
+        if ((s = ensure_dense(idx, g))) return s;
+        return query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
+    }
     return DBL_OK;
 }
 
@@ -633,7 +705,7 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
         // through the chunked copy pipeline.
         const void *ptrs[4] = {u, v, codes, visited};
         void *dptr[4] = {nullptr, nullptr, nullptr, nullptr};
-        bool pinned = !std::getenv("DBL_NO_ZEROCOPY");
+        bool pinned = true;
         for (int i = 0; i < 4 && pinned; ++i) {
             if (!ptrs[i]) continue;
             cudaPointerAttributes at{};
@@ -655,8 +727,13 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
     }
     if (!sync) return DBL_OK;
     uint32_t err = 0;
-    if ((s = query_finish(g, &err))) return s;
+    bool dense = false;
+    if ((s = query_finish(g, &err, &dense))) return s;
     if (err) { set_error("query vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+    if (dense) {   // the batch needed the dense BFS workspace: allocate it, run again
+        if ((s = ensure_dense(idx, g))) return s;
+        return query_impl(idx, gc, u, v, count, flags, codes, visited, mem, sync);
+    }
     return DBL_OK;
 }
 
@@ -669,6 +746,46 @@ extern "C" dbl_status dbl_query_async(const dbl_index *idx, const dbl_graph *g, 
                                       const uint32_t *v, uint64_t count, uint32_t flags, uint8_t *codes,
                                       uint32_t *visited) {
     return query_impl(idx, g, u, v, count, flags, codes, visited, DBL_MEM_DEVICE, false);
+}
+
+// One batch split across several devices: contiguous,
+// order-preserving slices as in the reference's worker pool
+// (queries.py:224-232: chunk = ceil(count / parts)), each answered on its
+// own handle pair from one host thread per device, so the slices' PCIe
+// transfers and kernels run concurrently.  The replicas must be identical
+// (same graph and index built on every device); host memory only.
+extern "C" dbl_status dbl_query_multi(const dbl_index *const *idx, const dbl_graph *const *g, uint32_t ndev,
+                                      const uint32_t *u, const uint32_t *v, uint64_t count, uint32_t flags,
+                                      uint8_t *codes, uint32_t *visited, dbl_mem mem) {
+    if (!idx || !g || ndev == 0) { set_error("null handle list"); return DBL_E_ARG; }
+    if (mem != DBL_MEM_HOST) { set_error("dbl_query_multi takes host buffers (device batches: dbl_query per handle)"); return DBL_E_ARG; }
+    if (count && (!u || !v || !codes)) { set_error("null argument"); return DBL_E_ARG; }
+    for (uint32_t d = 0; d < ndev; ++d) {
+        dbl_status s = check_pair(idx[d], g[d]);
+        if (s) return s;
+        if (idx[d]->n != idx[0]->n) { set_error("replicas differ in vertex count"); return DBL_E_MISMATCH; }
+    }
+    const uint64_t chunk = ndev ? (count + ndev - 1) / ndev : count;
+    std::vector<dbl_status> st(ndev, DBL_OK);
+    std::vector<std::string> msg(ndev);
+    auto work = [&](uint32_t d) {
+        const uint64_t lo = d * chunk < count ? d * chunk : count;
+        const uint64_t hi = lo + chunk < count ? lo + chunk : count;
+        st[d] = query_impl(idx[d], g[d], u + lo, v + lo, hi - lo, flags, codes + lo, visited ? visited + lo : nullptr,
+                           DBL_MEM_HOST, true);
+        if (st[d]) msg[d] = g_last_error;
+    };
+    if (ndev == 1 || count < 2 * (uint64_t)ndev) {
+        for (uint32_t d = 0; d < ndev; ++d) work(d);
+    } else {
+        std::vector<std::thread> th;
+        for (uint32_t d = 1; d < ndev; ++d) th.emplace_back(work, d);
+        work(0);
+        for (auto &t : th) t.join();
+    }
+    for (uint32_t d = 0; d < ndev; ++d)
+        if (st[d]) { set_error("device slice " + std::to_string(d) + ": " + msg[d]); return st[d]; }
+    return DBL_OK;
 }
 
 // ---------------------------------------------------------------- updates --
@@ -836,6 +953,8 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
         st.inserted = nnew;
         st.labels_changed = (uint64_t)changed[0] + changed[1];
         st.levels = levels;
+        st.fix_items = g->last_insert.fix_items;
+        st.fix_edges = g->last_insert.fix_edges;
         if (!range_error && g->m_delta * 4 > g->m_base + 1024) {
             if ((s = graph_compact(g))) { cleanup(); return s; }
             st.delta_merged = 1;

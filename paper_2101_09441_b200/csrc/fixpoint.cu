@@ -28,6 +28,26 @@
 
 namespace cg = cooperative_groups;
 
+// Variant switches (build.build_variant -D flags; defaults = measured best)
+#ifndef DBL_FIX_BPS_BUILD
+#define DBL_FIX_BPS_BUILD 0      // fixpoint CTAs/SM for builds (0 = occupancy maximum)
+#endif
+#ifndef DBL_FIX_BPS_INSERT
+#define DBL_FIX_BPS_INSERT 2     // fixpoint CTAs/SM for insert batches
+#endif
+#ifndef DBL_PULL_DIV
+#define DBL_PULL_DIV 0u          // pull levels when frontier edges > m / d (0: push only)
+#endif
+#ifndef DBL_NO_PIVOT
+#define DBL_NO_PIVOT 0           // 1: no pivot head start (plain fixpoint from the seeds)
+#endif
+#ifndef DBL_TD_DIV
+#define DBL_TD_DIV 64u           // pivot reach: top-down once a step marks < n / d
+#endif
+#ifndef DBL_PREP_RECORDS
+#define DBL_PREP_RECORDS 0       // 1: prep writes the seeded records even when the pivot could
+#endif
+
 namespace dbl {
 
 __device__ __forceinline__ uint64_t ld_cg64(const uint64_t *p) {
@@ -716,19 +736,13 @@ static void plan_groups(const dbl_index *idx, const uint32_t *words, uint32_t nw
 template <int NW, bool VEC, bool COUNT>
 static dbl_status launch_fixpoint_t(dbl_graph *g, FixParams &P) {
     auto kern = fixpoint_kernel<NW, VEC, COUNT>;
-    static int blocks_per_sm = -1;
-    if (blocks_per_sm < 0) {
-        DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, FIX_THREADS, 0));
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
-    // CTAs per SM: the occupancy maximum, or fewer (grid barriers get cheaper
-    // with fewer CTAs; insert levels are small)
-    // (insert runs -- COUNT -- default to 2 CTAs/SM: 100k-edge batches
-    // 0.54 -> 0.52 ms; builds keep the maximum)
-    static const int cap = [] {
-        const char *e = std::getenv(COUNT ? "DBL_FIX_BPS_INSERT" : "DBL_FIX_BPS_BUILD");
-        return e ? std::atoi(e) : (COUNT ? 2 : 0);
-    }();
+    int blocks_per_sm = 1;
+    dbl_status s = kernel_occupancy((const void *)kern, FIX_THREADS, 0, &blocks_per_sm);
+    if (s) return s;
+    // CTAs per SM: the occupancy maximum for builds; insert runs (COUNT)
+    // use 2 (grid barriers get cheaper with fewer CTAs and insert levels
+    // are small: 100k-edge batches 0.54 -> 0.52 ms)
+    const int cap = COUNT ? DBL_FIX_BPS_INSERT : DBL_FIX_BPS_BUILD;
     const int bps = (cap > 0 && cap < blocks_per_sm) ? cap : blocks_per_sm;
     int grid = bps * g->sm_count;
     void *args[] = {(void *)&P};
@@ -822,7 +836,7 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
         D.changed_bits = count ? g->changed_bits.as<uint32_t>() + d * (((size_t)g->n + 31) / 32) : nullptr;
         if (gr[d]) {
             D.lab = idx->rec.as<uint64_t>() + gr[d]->w0;
-            D.al = (idx->rs % 4 == 0 && !std::getenv("DBL_NO_CHUNK_LOADS")) ? (int)(gr[d]->w0 % 4) : -1;
+            D.al = (idx->rs % 4 == 0) ? (int)(gr[d]->w0 % 4) : -1;
             nw = gr[d]->nw;
             if ((gr[d]->w0 % 2) || (idx->rs % 2)) vec = false;
         } else {
@@ -833,11 +847,9 @@ static dbl_status prepare_params(dbl_graph *g, dbl_index *idx, const Group *gr[2
     P.ctrl = g->ctrl.as<Ctrl>();
     P.m_base = g->m_base;
     P.m_delta = g->m_delta;
-    {
-        static const char *pd = std::getenv("DBL_PULL_DIV");
-        // pull measured slower than push on cfg2 (r01): off unless asked for
-        P.pull_div = pd ? (uint32_t)std::atoi(pd) : 0u;   // 0 disables pull
-    }
+    // pull measured slower than push on cfg2 (r01): off unless a variant
+    // build asks for it (-DDBL_PULL_DIV=d)
+    P.pull_div = DBL_PULL_DIV;   // 0 disables pull
     P.n = g->n;
     P.active = (gr[0] ? 1u : 0u) | (gr[1] ? 2u : 0u);
     P.max_levels = g->n + 4;
@@ -935,6 +947,9 @@ struct ReachParams {
     uint32_t max_steps;      // cap on all steps
     uint32_t td_switch;      // switch to top-down once a step marks fewer vertices than this
     unsigned long long *tr;  // trace (or nullptr): [2s] end time of step s (globaltimer), [2s+1] its marks
+    unsigned long long *work;   // executed work (dbl_build_work_stats): [0] bottom-up vertex tests, [1] their
+                                // neighbour probes, [2] top-down frontier vertices, [3] their edges,
+                                // [4] records the union pass touched
     const uint32_t *lm;
     const uint8_t *flags;    // leaf flags and buckets: the seeds, read instead of the seeded records
     const uint32_t *bucket;
@@ -971,7 +986,7 @@ __device__ __forceinline__ bool any_marked(const Adj &a, const uint32_t *vis, ui
 #ifndef DBL_BU_ILP
 #define DBL_BU_ILP 1
 #endif
-template <int MINB>
+template <int MINB, bool WORK>
 __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
     cg::grid_group grid = cg::this_grid();
     const uint32_t h = P.lm[0];
@@ -1014,6 +1029,7 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
     bool capped = false, td = false;
     uint32_t bu = 0;
     unsigned prev_got = 0xffffffffu;
+    uint32_t w_tests = 0, w_probes = 0, w_tdv = 0, w_tde = 0;   // per-thread work counts
     for (uint32_t step = 0; have; ++step) {
         if (step == P.max_steps || (!td && bu == P.max_sweeps)) {
             // deep graph: the marked sets are only parts of D(h) / A(h), not
@@ -1066,16 +1082,23 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
 #pragma unroll
                     for (int d = 0; d < 2; ++d) {
                         if (!need[i][d]) continue;
+                        if (WORK) ++w_tests;
                         bool hit = c0[i][d] != 0xffffffffu && vis_test_ca(P.vis[d], c0[i][d]);
+                        uint32_t pr = c0[i][d] != 0xffffffffu;
                         if (!hit) {
                             const Adj &a = P.adj[d];
-                            for (uint32_t j = s0[i][d] + 1; j < s1[i][d] && !hit; ++j)
+                            uint32_t j = s0[i][d] + 1;
+                            for (; j < s1[i][d] && !hit; ++j)
                                 hit = vis_test_ca(P.vis[d], __ldg(a.col + j));
+                            if (WORK) pr += j > s0[i][d] + 1 ? j - s0[i][d] - 1 : 0;
                             if (!hit && a.dptr) {
                                 const uint32_t t0 = __ldg(a.dptr + xv[i]), t1 = __ldg(a.dptr + xv[i] + 1);
-                                for (uint32_t j = t0; j < t1 && !hit; ++j) hit = vis_test_ca(P.vis[d], __ldg(a.dcol + j));
+                                uint32_t jd = t0;
+                                for (; jd < t1 && !hit; ++jd) hit = vis_test_ca(P.vis[d], __ldg(a.dcol + jd));
+                                if (WORK) pr += jd - t0;
                             }
                         }
+                        if (WORK) w_probes += pr;
                         if (hit) {
                             atomicOr(&P.vis[d][xv[i] >> 5], 1u << (xv[i] & 31));
                             atomicOr(&P.nb[d][cb][xv[i] >> 5], 1u << (xv[i] & 31));
@@ -1108,12 +1131,14 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
                     while (f) {
                         const uint32_t y = (uint32_t)(wi * 32 + __ffs(f) - 1);
                         f &= f - 1;
+                        if (WORK) ++w_tdv;
 #pragma unroll 1
                         for (int seg = 0; seg < 2; ++seg) {
                             const uint32_t *ptr = seg ? a.dptr : a.ptr;
                             if (!ptr) break;
                             const uint32_t *col = seg ? a.dcol : a.col;
                             const uint32_t s0 = __ldg(ptr + y), s1 = __ldg(ptr + y + 1);
+                            if (WORK) w_tde += s1 - s0;
                             for (uint32_t j = s0; j < s1; ++j) {
                                 const uint32_t z = __ldg(col + j);
                                 const uint32_t bit = 1u << (z & 31);
@@ -1152,6 +1177,14 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
         // large frontiers (cfg1: 0.25 -> 1.06 ms when it switched at step 0)
         if (!td && step >= 1 && got < P.td_switch && got < prev_got) td = true;
         prev_got = got;
+    }
+    if (WORK) {   // one warp-aggregated add per counter per warp
+        unsigned long long c[4] = {w_tests, w_probes, w_tdv, w_tde};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            for (int o = 16; o > 0; o >>= 1) c[i] += __shfl_xor_sync(FULL, c[i], o);
+            if ((threadIdx.x & 31) == 0 && c[i]) atomicAdd(&P.work[i], c[i]);
+        }
     }
     // keep D(h) and the SCC landmarks for query pruning (marks are exact
     // members even when the sweeps were capped)
@@ -1246,8 +1279,10 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
         const int lane = threadIdx.x & 31;
         const uint32_t wdl = P.wdl;
         const uint64_t nblk = P.nwords, gw = tid >> 5, nw = nth >> 5;
+        unsigned long long touched = 0;
         for (uint64_t blk = gw; blk < nblk; blk += nw) {
             const uint32_t fb = drop ? 0u : P.vis[0][blk], bb = drop ? 0u : P.vis[1][blk];
+            if (WORK && lane == 0) touched += __popc(fb | bb);
             if (!(fb | bb) && !P.write_rec) continue;
             uint64_t *base = P.rec + blk * 32 * rs;
             uint32_t win = 0xffffffffu, wout = 0xffffffffu, sb = 0;
@@ -1286,6 +1321,7 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
                 }
             }
         }
+        if (WORK && lane == 0 && touched) atomicAdd(&P.work[4], touched);
         if (P.write_rec) {   // landmark i seeds bit i of both DL halves (labels.py:291-293)
             grid.sync();
             for (uint64_t i = tid; i < P.k; i += nth) {
@@ -1299,10 +1335,7 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
     }
 }
 
-static bool pivot_on() {
-    static const bool off = std::getenv("DBL_NO_PIVOT") != nullptr;
-    return !off;
-}
+static bool pivot_on() { return !DBL_NO_PIVOT; }
 
 // Head start from the pivot's reachability (all record words; after prep).
 static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask, uint32_t *front0,
@@ -1311,7 +1344,7 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     const size_t bmw = ((size_t)n + 31) / 32;
     const size_t bbytes = ((bmw * 4 + 255) / 256) * 256;
     dbl_status s;
-    const size_t rbytes = 8 * bbytes + 2 * MAX_SHARD_WORDS * 8 + 64 + 66 * 8;
+    const size_t rbytes = 8 * bbytes + 2 * MAX_SHARD_WORDS * 8 + 64 + 66 * 8 + 8 * 8;
     if ((s = g->reach.ensure(rbytes))) return s;
     uint32_t *vf = g->reach.as<uint32_t>();
     uint32_t *vb = reinterpret_cast<uint32_t *>(g->reach.as<char>() + bbytes);
@@ -1359,26 +1392,25 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     // label fixpoint's frontier
     R.max_sweeps = 12;
     R.max_steps = 64;
-    static const uint32_t td_div = [] {
-        const char *e = std::getenv("DBL_TD_DIV");
-        return e ? (uint32_t)std::atoi(e) : 64u;
-    }();
-    R.td_switch = td_div ? (uint32_t)(n / td_div) : 0u;
-    static const bool tr = std::getenv("DBL_TRACE") != nullptr;
+    R.td_switch = DBL_TD_DIV ? (uint32_t)(n / DBL_TD_DIV) : 0u;
+    constexpr bool tr = DBL_TRACE;
     unsigned long long *trb = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(chg) + 64);
     R.tr = tr ? trb : nullptr;
+    // the instrumented variant (dbl_graph_instrument) counts the executed
+    // work; the product variant carries no counters (they cost registers)
+    const bool wk = g->instrument;
+    R.work = trb + 66;
+    g->reach_work = wk ? R.work : nullptr;
+    g->reach_chg = chg;
     const bool big = n >= (1u << 24);
-    const void *kern = big ? (const void *)reach_kernel<8> : (const void *)reach_kernel<6>;
-    static int bps_s[2] = {-1, -1};
-    int &bps = bps_s[big ? 1 : 0];
-    if (bps < 0) {
-        DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0));
-        if (bps < 1) bps = 1;
-    }
+    const void *kern = big ? (wk ? (const void *)reach_kernel<8, true> : (const void *)reach_kernel<8, false>)
+                           : (wk ? (const void *)reach_kernel<6, true> : (const void *)reach_kernel<6, false>);
+    int bps = 1;
+    if ((s = kernel_occupancy(kern, 256, 0, &bps))) return s;
     void *args[] = {(void *)&R};
     DBL_CUDA(cudaLaunchCooperativeKernel(kern, dim3(g->sm_count * bps), dim3(256), args, 0, g->stream));
     DBL_LAUNCHED();
-    if (std::getenv("DBL_TRACE")) {
+    if (DBL_TRACE) {
         unsigned int hc[6];
         DBL_CUDA(cudaMemcpyAsync(hc, chg, sizeof(hc), cudaMemcpyDeviceToHost, g->stream));
         DBL_CUDA(cudaStreamSynchronize(g->stream));
@@ -1430,15 +1462,20 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
     DBL_CUDA(cudaEventRecord(g->ev[0], g->stream));
     idx->has_scc = false;   // set again by a full build's pivot
     const bool prep = words == nullptr;
+    g->last_build = BuildWork{};
+    g->reach_work = nullptr;
     dbl_status s;
     if ((s = graph_ensure_traversal(g))) return s;
     // a full build with a pivot lets the pivot pass write the seeded records
     // (one write of the table instead of seed + read-modify-write)
-    static const bool rec_in_prep = std::getenv("DBL_PREP_RECORDS") != nullptr;
+    constexpr bool rec_in_prep = DBL_PREP_RECORDS;
     const bool pivot = idx->cfg.k && pivot_on();
     // (measured: wins on padded k = 256 records, cfg5 9.3 -> 8.4 ms; costs ~4 us
     // on 32-byte records, cfg2, where prep's write is cheap)
     const bool pivot_writes = prep && pivot && !rec_in_prep && idx->rs > 4;
+    g->last_build.flags = (prep && !pivot_writes ? 1u : 0u) | (pivot_writes ? 2u : 0u) |
+                          (pivot && !pivot_writes ? 4u : 0u) | (prep ? 0u : 16u);
+    g->last_build.rs = idx->rs;
     if (prep) {
         const Group **p0 = pairs[0];
         uint32_t *b0 = p0[0] ? g->stamp[0].as<uint32_t>() : nullptr;
@@ -1488,6 +1525,12 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
         Ctrl h{};
         if ((s = finish_run(g, &h, prep && pi == 0 ? &hp : nullptr))) return s;
         trace("build: fixpoint", g->stream);
+        g->last_build.fix_runs += 1;
+        g->last_build.fix_levels += h.levels;
+        for (uint32_t l = 0; l < h.levels && l < 32; ++l) {
+            g->last_build.fix_items += h.level_items[l] & ((1ull << 60) - 1);
+            g->last_build.fix_edges += h.level_edges[l];
+        }
         if (prep && pi == 0) {
             if (hp.err) { set_error("bucket override outside [0, k_prime)"); return DBL_E_CONFIG; }
             idx->sel_leaves = false;
@@ -1503,7 +1546,7 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
             }
             idx->sel_landmarks = false;
         }
-        if (std::getenv("DBL_TRACE")) {
+        if (DBL_TRACE) {
             std::fprintf(stderr, "[dbl] fixpoint levels=%u nw=%u\n", h.levels, nw);
             for (uint32_t l = 0; l < h.levels && l < 31; ++l)
                 std::fprintf(stderr, "[dbl]   level %2u items %9llu edges %10llu pull %llu compact %7.1f us  relax %7.1f us\n",
@@ -1526,6 +1569,7 @@ dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, ui
     changed_out[0] = changed_out[1] = 0;
     seed_changed[0] = seed_changed[1] = 0;
     *levels = 0;
+    g->last_insert = BuildWork{};
     if (count == 0 || idx->n == 0) return DBL_OK;
     Group groups[2 * MAX_SHARD_WORDS + 4];
     int ng = 0;
@@ -1551,7 +1595,7 @@ dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, ui
         const bool last = i == half - 1;
         if ((s = finish_run(g, &h, nullptr, last ? extra_dev : nullptr, last ? extra_host : nullptr))) return s;
         trace("insert: fixpoint", g->stream);
-        if (std::getenv("DBL_TRACE")) {
+        if (DBL_TRACE) {
             std::fprintf(stderr, "[dbl] insert fixpoint levels=%u nw=%u\n", h.levels, nw);
             for (uint32_t l = 0; l < h.levels && l < 31; ++l)
                 std::fprintf(stderr, "[dbl]   level %2u items %9llu edges %10llu compact %7.1f us  relax %7.1f us\n",
@@ -1565,6 +1609,12 @@ dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, ui
         seed_changed[0] |= h.seed_changed[0];
         seed_changed[1] |= h.seed_changed[1];
         if (h.levels > *levels) *levels = h.levels;
+        g->last_insert.fix_runs += 1;
+        g->last_insert.fix_levels += h.levels;
+        for (uint32_t l = 0; l < h.levels && l < 32; ++l) {
+            g->last_insert.fix_items += h.level_items[l] & ((1ull << 60) - 1);
+            g->last_insert.fix_edges += h.level_edges[l];
+        }
     }
     // ev[1] was recorded (and reached) by the last finish_run
     cudaEventElapsedTime(&g->t_fix, g->ev[0], g->ev[1]);

@@ -666,8 +666,9 @@ extern "C" dbl_status dbl_graph_edges(const dbl_graph *g, uint32_t *src, uint32_
 
 extern "C" dbl_status dbl_sync(const dbl_graph *g) {
     if (!g) { set_error("null graph"); return DBL_E_ARG; }
-    DBL_CUDA(cudaStreamSynchronize(g->stream));
-    return DBL_OK;
+    DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
+    return query_sync(const_cast<dbl_graph *>(g));
 }
 
 extern "C" dbl_status dbl_stream(const dbl_graph *g, void **s) {

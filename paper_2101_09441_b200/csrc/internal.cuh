@@ -3,9 +3,16 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstddef>
+#include <atomic>
 #include <string>
 
 #include "dbl_b200.h"
+
+// Compile-time switches.  Kernel-variant experiments are chosen by -D flags
+// in build.build_variant builds, never by the environment of a product run.
+#ifndef DBL_TRACE
+#define DBL_TRACE 0          // 1: host-side phase times to stderr (debug builds)
+#endif
 
 namespace dbl {
 
@@ -21,7 +28,9 @@ constexpr int MAX_SHARD_WORDS = 32;  // words per record half (2 halves <= 64-bi
 // ---------------------------------------------------------------- errors --
 void set_error(const std::string &msg);
 dbl_status cuda_fail(cudaError_t e, const char *what);
-uint64_t &launch_counter();
+std::atomic<uint64_t> &launch_counter();
+// blocks per SM of `fn` (dynamic smem opted in), cached per device
+dbl_status kernel_occupancy(const void *fn, int threads, size_t smem, int *bps);
 
 #define DBL_CUDA(call)                                                         \
     do {                                                                       \
@@ -50,7 +59,7 @@ void set_stream_synced();         // the device was just synchronised: frees are
 // through an event (no host sync) before reading them.
 dbl_status order_after_caller(dbl_graph *g);
 void pool_forget_stream(cudaStream_t s);  // before a stream is destroyed
-// Debug phase timer: DBL_TRACE=1 prints host-side phase times to stderr.
+// Debug phase timer: a -DDBL_TRACE=1 build prints host-side phase times to stderr.
 void trace(const char *what, cudaStream_t s);
 
 // grow-only device buffer backed by the caching allocator
@@ -101,6 +110,24 @@ struct Adj {
     const uint32_t *col;
     const uint32_t *dptr;   // n+1 or nullptr
     const uint32_t *dcol;
+};
+
+// Executed work of the last build on a graph (dbl_build_work_stats).
+struct BuildWork {
+    uint64_t fix_items = 0, fix_edges = 0;
+    uint32_t fix_levels = 0, fix_runs = 0;
+    uint32_t flags = 0;   // see dbl_build_work in dbl_b200.h
+    uint32_t rs = 0;      // record stride (words)
+};
+
+// Arguments of one query batch (kept by the graph for dbl_sync).
+struct QueryArgs {
+    const dbl_index *idx;
+    const uint32_t *u, *v;
+    uint8_t *codes;
+    uint32_t *visited;
+    uint64_t count;
+    uint32_t flags;
 };
 
 // Frontier work items: one per nonempty adjacency segment of a frontier
@@ -186,6 +213,10 @@ struct dbl_graph {
     uint32_t qcap = 0;
     dbl::DevBuf ctrl;
     dbl::DevBuf reach;        // pivot reachability: n x {from pivot, to pivot} u64 + 2 bitmaps + unions
+    unsigned long long *reach_work = nullptr;   // the last pivot pass's work counters (in `reach`)
+    unsigned int *reach_chg = nullptr;          // its step words: [3] capped, [4] steps, [5] sweeps
+    dbl::BuildWork last_build{}, last_insert{};
+    bool instrument = false;                    // builds count their executed work (dbl_graph_instrument)
     dbl::DevBuf changed_bits;
     // generic scratch
     dbl::DevBuf cub_tmp, scratch_a, scratch_b, scratch_c, scratch_d;
@@ -197,6 +228,7 @@ struct dbl_graph {
     cudaStream_t cstream[2] = {nullptr, nullptr};   // H2D / D2H copy streams
     cudaEvent_t cev[33] = {};
     uint64_t q_pending_cap = 0;
+    dbl::QueryArgs q_last{};              // arguments of the last batch (dbl_sync re-runs it if it needed the dense workspace)
     bool q_timed_bfs = false;            // last batch ran the separate BFS kernels (ev[3] -> ev[4])
     uint64_t topo_version = 0;           // bumped whenever adjacency buffers change
     int sm_count = 148;
@@ -291,4 +323,9 @@ void query_timings(dbl_graph *g);
 // g->q_host_res (synchronous calls read them there after the stream sync)
 dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
                      uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, bool host_result = false);
+dbl_status ensure_dense(const dbl_index *idx, dbl_graph *g);
+dbl_status query_finish(dbl_graph *g, uint32_t *err_out, bool *dense_out);
+dbl_status query_err_to(dbl_graph *g, uint32_t *dst4);
+bool chunk_needs_dense(const uint32_t *w4);
+dbl_status query_sync(dbl_graph *g);
 }  // namespace dbl

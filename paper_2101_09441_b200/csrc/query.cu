@@ -42,6 +42,14 @@ constexpr int BFS_THREADS = 256;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr uint8_t UNRESOLVED = 0xff;
 
+// Variant switches (build.build_variant -D flags; defaults = measured best)
+#ifndef DBL_NO_PIVOT_PRUNE
+#define DBL_NO_PIVOT_PRUNE 0   // 1: BFS fallbacks ignore the pivot sets
+#endif
+#ifndef DBL_LEAN_WIDE
+#define DBL_LEAN_WIDE 0        // 1: k > 64 also takes the lean gather (slower on cfg5)
+#endif
+
 // The build's pivot sets (reach_kernel): dmask = vertices reached from the
 // pivot landmark h, scc = DL bits of the landmarks in h's SCC.  Every x in
 // D(h) has those bits in dl_in[x], so for a query whose dl_out[u] meets scc
@@ -88,65 +96,6 @@ __device__ __forceinline__ void ld_nc128(const uint64_t *p, uint64_t &a, uint64_
 }
 
 // ------------------------------------------------------------------ K6 --
-
-template <int WDL, int WBL>
-__global__ void __launch_bounds__(256)
-label_check_kernel(const uint64_t *__restrict__ rec, uint32_t n, const uint32_t *__restrict__ qu,
-                   const uint32_t *__restrict__ qv, uint64_t count, uint32_t flags,
-                   uint8_t *__restrict__ codes, uint32_t *__restrict__ visited,
-                   uint32_t *__restrict__ pending, uint32_t *__restrict__ counters) {
-    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H);
-    const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
-    const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t cr = (count + 31) & ~31ull;
-    const int lane = threadIdx.x & 31;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cr; i += stride) {
-        bool unres = false;
-        if (i < count) {
-            const uint32_t u = qu[i], v = qv[i];
-            uint8_t code = UNRESOLVED;
-            if (u >= n || v >= n) {
-                atomicOr(&counters[CNT_ERR], 1u);
-                code = 0xfe;
-            } else if (u == v) {
-                code = DBL_REFLEXIVE;
-            } else {
-                uint64_t a[RW], b[RW];
-                const uint64_t *ra = rec + (size_t)u * RS, *rb = rec + (size_t)v * RS;
-#pragma unroll
-                for (int k = 0; k < RW; k += 2) {
-                    ld_nc128(ra + k, a[k], a[k + 1]);
-                    ld_nc128(rb + k, b[k], b[k + 1]);
-                }
-                uint64_t r1 = 0, r3 = 0, r4 = 0, r2 = 0;
-#pragma unroll
-                for (int k = 0; k < WDL; ++k) {
-                    r1 |= a[H + k] & b[k];             // dl_out[u] & dl_in[v]
-                    r3 |= b[H + k] & a[k];             // dl_out[v] & dl_in[u]
-                    r4 |= (a[H + k] & a[k]) | (b[H + k] & b[k]);
-                }
-#pragma unroll
-                for (int k = 0; k < WBL; ++k)
-                    r2 |= (a[WDL + k] & ~b[WDL + k]) | (b[H + WDL + k] & ~a[H + WDL + k]);
-                if (use_dl && r1) code = DBL_DL_POSITIVE;
-                else if (use_bl && r2) code = DBL_BL_NEGATIVE;
-                else if (thm1 && r3) code = DBL_THM1_NEGATIVE;
-                else if (thm2 && r4) code = DBL_THM2_NEGATIVE;
-            }
-            codes[i] = code;
-            if (visited) visited[i] = 0;
-            unres = code == UNRESOLVED;
-        }
-        const unsigned m = __ballot_sync(FULL, unres);
-        if (m) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(&counters[CNT_PENDING], (uint32_t)__popc(m));
-            base = __shfl_sync(FULL, base, 0);
-            if (unres) pending[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
-        }
-    }
-}
 
 // runtime-width variant (any k, k')
 __global__ void __launch_bounds__(256)
@@ -483,44 +432,24 @@ static size_t bfs_smem(int wdl, int wbl, bool dense) {
     return s;
 }
 
-// --------------------------------------------------- fused K6 + warp BFS --
+// ------------------------------------------------- per-warp BFS state --
 //
-// The throughput path.  Persistent warps take 128-query tiles from a global
-// ticket; each lane owns 4 consecutive queries (one 128-bit load of u and of
-// v), gathers both endpoints' records with 256-bit read-only loads, and
-// applies rules 0-4.  The tile's unresolved queries (about 0.5% on R-MAT)
-// are answered right away by the same warp with a bit-parallel pruned BFS
-// over a per-warp shared-memory table (bit i of a 32-bit word = query i of
-// the batch): frontier expansion is flattened across lanes (32 edges per
-// step, owner entry found by a shuffle search over the degree prefix), so a
-// warp's BFS latency overlaps with every other warp's label checks instead
-// of running as a separate, latency-bound kernel.  A batch whose BFS outgrows
-// the table is appended to the global pending list and finished by the
-// 64-query group kernel (and, beyond that, the dense kernel).
+// Bit-parallel pruned BFS of up to 32 queries on one warp (bit i of a 32-bit
+// word = query i): frontier expansion is flattened across lanes (32 edges per
+// step, the owner entry found by a shuffle search over the degree prefix),
+// visited/frontier words live in a per-warp shared-memory hash table.  Used
+// by the wide gather kernel (K6w) for its unresolved queries and by the
+// tail-launched warp kernel (K7b).  A batch whose BFS outgrows the table is
+// appended to an overflow list and finished by the 64-query group kernel
+// (and, beyond that, the dense kernel).
 
-#ifndef DBL_QPL
-#define DBL_QPL 2
-#endif
 #ifndef DBL_QMINB
 #define DBL_QMINB 2
 #endif
-constexpr int QPL = DBL_QPL;        // queries per lane
-constexpr int QT = 32 * QPL;       // queries per warp tile
 constexpr int WH = 128;            // per-warp BFS hash slots (power of two)
 constexpr int WHBITS = 7;
 constexpr int WT = 64;             // per-warp target table slots
 constexpr int FUSED_THREADS = 256;
-// false: a warp answers its tile's unresolved queries right after the tile
-// (short BFS chains interleaved with other warps' label checks); true: it
-// accumulates 32 before running one BFS (fewer, longer chains at the end).
-// Measured on cfg2: immediate is faster (31 vs 39 us per 1M batch).
-#ifndef DBL_QDEFER
-#define DBL_QDEFER 0
-#endif
-constexpr bool DEFER_BFS = DBL_QDEFER;
-#ifndef DBL_QTICKET
-#define DBL_QTICKET 1
-#endif
 
 template <int WDL, int WBL>
 struct WarpBfs {
@@ -721,32 +650,6 @@ __device__ void warp_bfs(WarpBfs<WDL, WBL> &B, uint32_t nb, const uint64_t *__re
     __syncwarp();
 }
 
-__device__ __forceinline__ void flush_tile_codes(uint8_t *__restrict__ codes, uint32_t *__restrict__ visited,
-                                                 uint32_t count, uint64_t qb, int vec_ok, const uint8_t (&code)[QPL],
-                                                 const uint32_t (&vcount)[QPL]) {
-    if (vec_ok && qb + QPL - 1 < count) {
-        if constexpr (QPL == 4) {
-            const uint32_t packed = code[0] | (code[1] << 8) | (code[2] << 16) | ((uint32_t)code[3] << 24);
-            *reinterpret_cast<uint32_t *>(codes + qb) = packed;
-            if (visited) *reinterpret_cast<uint4 *>(visited + qb) = make_uint4(vcount[0], vcount[1], vcount[2], vcount[3]);
-        } else if constexpr (QPL == 2) {
-            const uint16_t packed = (uint16_t)(code[0] | (code[1] << 8));
-            *reinterpret_cast<uint16_t *>(codes + qb) = packed;
-            if (visited) *reinterpret_cast<uint2 *>(visited + qb) = make_uint2(vcount[0], vcount[1]);
-        } else {
-            codes[qb] = code[0];
-            if (visited) visited[qb] = vcount[0];
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < QPL; ++j) {
-            if (qb + j >= count) break;
-            codes[qb + j] = code[j];
-            if (visited) visited[qb + j] = vcount[j];
-        }
-    }
-}
-
 // Run the warp's staged batch (B.nq queries) and write its answers.
 #ifdef DBL_BFS_NOINLINE
 #define DBL_BFS_INLINE __noinline__
@@ -802,34 +705,6 @@ __device__ DBL_BFS_INLINE void warp_bfs_batch(WarpBfs<WDL, WBL> &B, const uint64
     __syncwarp();
 }
 
-// Pairs qb .. qb+QPL-1 of the batch (entries at or beyond end read as 0).
-__device__ __forceinline__ void load_pairs(const uint32_t *__restrict__ qu, const uint32_t *__restrict__ qv,
-                                           uint64_t qb, uint64_t end, int vec_ok, uint32_t (&us)[QPL],
-                                           uint32_t (&vs)[QPL]) {
-    if (vec_ok && qb + QPL - 1 < end) {
-        if constexpr (QPL == 4) {
-            const uint4 a = __ldg(reinterpret_cast<const uint4 *>(qu + qb));
-            const uint4 b = __ldg(reinterpret_cast<const uint4 *>(qv + qb));
-            us[0] = a.x; us[1] = a.y; us[2] = a.z; us[3] = a.w;
-            vs[0] = b.x; vs[1] = b.y; vs[2] = b.z; vs[3] = b.w;
-        } else if constexpr (QPL == 2) {
-            const uint2 a = __ldg(reinterpret_cast<const uint2 *>(qu + qb));
-            const uint2 b = __ldg(reinterpret_cast<const uint2 *>(qv + qb));
-            us[0] = a.x; us[1] = a.y;
-            vs[0] = b.x; vs[1] = b.y;
-        } else {
-            us[0] = __ldg(qu + qb);
-            vs[0] = __ldg(qv + qb);
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < QPL; ++j) {
-            us[j] = qb + j < end ? __ldg(qu + qb + j) : 0;
-            vs[j] = qb + j < end ? __ldg(qv + qb + j) : 0;
-        }
-    }
-}
-
 // Close a batch: publish the live counters to the result words and zero them
 // for the next batch (stream order makes this the batch's last access).
 // The batch's last CTA moves the live counters to the result words (and to
@@ -864,168 +739,6 @@ struct HardArgs {
     uint32_t *wovf;
 };
 
-template <int WDL, int WBL>
-__global__ void __launch_bounds__(FUSED_THREADS, DBL_QMINB)
-query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const QueryDesc qd,
-                   uint32_t *__restrict__ pending, uint32_t *__restrict__ counters, const HardArgs ha) {
-    const uint32_t *__restrict__ qu = qd.u;
-    const uint32_t *__restrict__ qv = qd.v;
-    const uint32_t count = qd.count, flags = qd.flags;
-    const int vec_ok = qd.vec_ok;
-    uint8_t *__restrict__ codes = qd.codes;
-    uint32_t *__restrict__ visited = qd.visited;
-    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H), WD = WarpBfs<WDL, WBL>::WD;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    WarpBfs<WDL, WBL> &B = reinterpret_cast<WarpBfs<WDL, WBL> *>(smem_raw)[wid];
-    const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
-    const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
-    const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
-    if (lane == 0) B.nq = 0;
-    __syncwarp();
-#if DBL_QTICKET
-    // dynamic: warps take QT-query tiles from a global ticket
-    for (;;) {
-        uint32_t tile = 0;
-        if (lane == 0) tile = atomicAdd(&counters[CNT_TILE], 1u);
-        tile = __shfl_sync(FULL, tile, 0);
-        const uint64_t q0 = (uint64_t)tile * QT;
-        if (q0 >= count) break;
-        const uint64_t wend = count;
-        const uint64_t qb = q0 + QPL * lane;
-        uint32_t us[QPL], vs[QPL];
-        load_pairs(qu, qv, qb, wend, vec_ok, us, vs);
-#else
-    // static: warp w owns the contiguous range [w0, w1) (equal shares, a
-    // multiple of 4 queries), walked in QT-query tiles; the next tile's pairs
-    // are loaded while the current tile's records are in flight, so a tile
-    // costs about one dependent memory round trip and no ticket atomics
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    uint64_t share = ((uint64_t)count + nw - 1) / nw;
-    share = (share + 3) & ~3ull;
-    const uint64_t w0 = (uint64_t)gw * share;
-    const uint64_t wend = min((uint64_t)count, w0 + share);
-    uint32_t nus[QPL], nvs[QPL];
-    if (w0 < wend) load_pairs(qu, qv, w0 + QPL * lane, wend, vec_ok, nus, nvs);
-    for (uint64_t q0 = w0; q0 < wend; q0 += QT) {
-        const uint64_t qb = q0 + QPL * lane;
-        uint32_t us[QPL], vs[QPL];
-#pragma unroll
-        for (int j = 0; j < QPL; ++j) { us[j] = nus[j]; vs[j] = nvs[j]; }
-        if (q0 + QT < wend) load_pairs(qu, qv, qb + QT, wend, vec_ok, nus, nvs);
-#endif
-        uint8_t code[QPL];
-        uint32_t vcount[QPL];
-#pragma unroll
-        for (int j = 0; j < QPL; ++j) vcount[j] = 0;
-        unsigned unres = 0;
-        uint64_t ra[QPL][RW], rb[QPL][RW];
-#pragma unroll
-        for (int j = 0; j < QPL; ++j) {
-            const bool inb = qb + j < wend;
-            const bool ok = inb && us[j] < n && vs[j] < n && us[j] != vs[j];
-            if (ok) {
-                load_record<RW, RS>(rec + (size_t)us[j] * RS, ra[j]);
-                load_record<RW, RS>(rec + (size_t)vs[j] * RS, rb[j]);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < QPL; ++j) {
-            const bool inb = qb + j < wend;
-            code[j] = UNRESOLVED;
-            if (!inb) { code[j] = 0xfd; continue; }
-            const uint32_t u = us[j], v = vs[j];
-            if (u >= n || v >= n) {
-                atomicOr(&counters[CNT_ERR], 1u);
-                code[j] = 0xfe;
-                continue;
-            }
-            if (u == v) { code[j] = DBL_REFLEXIVE; continue; }
-            uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
-#pragma unroll
-            for (int k = 0; k < WDL; ++k) {
-                r1 |= ra[j][H + k] & rb[j][k];
-                r3 |= rb[j][H + k] & ra[j][k];
-                r4 |= (ra[j][H + k] & ra[j][k]) | (rb[j][H + k] & rb[j][k]);
-            }
-#pragma unroll
-            for (int k = 0; k < WBL; ++k)
-                r2 |= (ra[j][WDL + k] & ~rb[j][WDL + k]) | (rb[j][H + WDL + k] & ~ra[j][H + WDL + k]);
-            if (use_dl && r1) code[j] = DBL_DL_POSITIVE;
-            else if (use_bl && r2) code[j] = DBL_BL_NEGATIVE;
-            else if (thm1 && r3) code[j] = DBL_THM1_NEGATIVE;
-            else if (thm2 && r4) code[j] = DBL_THM2_NEGATIVE;
-            else unres |= 1u << j;
-        }
-        // Unresolved queries are appended to the warp's batch; the bit-parallel
-        // BFS runs when 32 have accumulated (and once more after the last
-        // tile), so a warp pays about one BFS latency chain per 32 queries.
-        // the tile's codes go out first (UNRESOLVED where a BFS will answer)
-        flush_tile_codes(codes, visited, wend, qb, vec_ok, code, vcount);
-        __syncwarp();
-        uint32_t nun = __popc(unres), tot = 0;
-        uint32_t off = warp_excl_scan(nun, tot);
-#ifdef DBL_QNOBFS
-        tot = 0;   // experiment: label checks only (unresolved codes left as is)
-#endif
-        uint32_t done_upto = 0;   // tile entries [0, done_upto) already staged
-        while (done_upto < tot) {
-            const uint32_t nq = B.nq;
-            const uint32_t take = min(32u - nq, tot - done_upto);
-            uint32_t pos = off;
-#pragma unroll
-            for (int j = 0; j < QPL; ++j) {
-                if (!((unres >> j) & 1)) continue;
-                if (pos >= done_upto && pos < done_upto + take) {
-                    const uint32_t bi = nq + pos - done_upto;
-                    B.qidx[bi] = (uint32_t)(qb + j);
-                    B.qu[bi] = us[j];
-                    B.qv[bi] = vs[j];
-#pragma unroll
-                    for (int q = 0; q < WDL; ++q) B.qdlo[bi * WD + q] = ra[j][H + q];
-#pragma unroll
-                    for (int q = 0; q < WBL; ++q) {
-                        B.qbli[bi * WBL + q] = rb[j][WDL + q];
-                        B.qblo[bi * WBL + q] = rb[j][H + WDL + q];
-                    }
-                }
-                ++pos;
-            }
-            done_upto += take;
-            __syncwarp();
-            if (lane == 0) B.nq = nq + take;
-            __syncwarp();
-            if (nq + take == 32 || (!DEFER_BFS && done_upto == tot)) {
-                warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.pv, codes, visited, pending, counters, CNT_PENDING);
-            }
-        }
-    }
-    __syncwarp();
-    if (B.nq) warp_bfs_batch<WDL, WBL>(B, rec, adj, prune_dl, prune_bl, qd.pv, codes, visited, pending, counters, CNT_PENDING);
-    // the last CTA out closes the batch, or hands the overflowed BFS batches
-    // to the group/dense kernels through the tail-launch stream (they run
-    // after this grid, before the stream's next operation)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const uint32_t prev = atomicAdd(&counters[CNT_DONE], 1u);
-        if (prev == gridDim.x - 1) {
-            __threadfence();
-            const uint32_t npend = *(volatile uint32_t *)&counters[CNT_PENDING];
-            if (npend == 0) {
-                close_batch(counters, qd.hres);
-            } else {
-                bfs_kernel<false><<<ha.grid, BFS_THREADS, ha.smem, cudaStreamTailLaunch>>>(
-                    rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, nullptr);
-                bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
-                    rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
-                finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters, qd.hres);
-            }
-        }
-    }
-}
-
 // ------------------------------------------------- K6 wide: quad gathers --
 //
 // Records wider than 32 bytes (k > 64) live at 64/128-byte strides.  Random
@@ -1040,7 +753,7 @@ query_fused_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const 
 // from the quad lane holding them, by shuffle; the BL words of u and v sit in
 // the same lane), and the codes move to lane 8r + i.  Unresolved queries are
 // staged for the warp's bit-parallel BFS straight from the lanes holding the
-// words, as in query_fused_kernel.
+// words.
 __device__ __forceinline__ uint64_t shfl64(uint64_t x, int src) {
     const uint32_t lo = __shfl_sync(FULL, (uint32_t)x, src), hi = __shfl_sync(FULL, (uint32_t)(x >> 32), src);
     return ((uint64_t)hi << 32) | lo;
@@ -1199,8 +912,9 @@ query_quad_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Q
             } else {
                 bfs_kernel<false><<<ha.grid, BFS_THREADS, ha.smem, cudaStreamTailLaunch>>>(
                     rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, nullptr);
-                bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
-                    rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
+                if (ha.ws)
+                    bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
+                        rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
                 finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters, qd.hres);
             }
         }
@@ -1621,8 +1335,9 @@ bfs_warp_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Que
         __threadfence();
         bfs_kernel<false><<<ha.grid, BFS_THREADS, ha.smem, cudaStreamTailLaunch>>>(
             rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, nullptr);
-        bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
-            rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
+        if (ha.ws)
+            bfs_kernel<true><<<ha.dctas, BFS_THREADS, ha.dsmem, cudaStreamTailLaunch>>>(
+                rec, ha.wdl, ha.wbl, n, adj, qd, pending, counters, ha.ovf, ha.ws);
         finish_batch_kernel<<<1, 32, 0, cudaStreamTailLaunch>>>(counters, qd.hres);
     }
 }
@@ -1640,71 +1355,71 @@ static bool pick_lean(uint32_t wdl, uint32_t wbl, lean_fn &l, bfsw_fn &b, size_t
     return false;
 }
 
-typedef void (*fused_fn)(const uint64_t *, uint32_t, Adj, const QueryDesc, uint32_t *, uint32_t *, const HardArgs);
+typedef void (*quad_fn)(const uint64_t *, uint32_t, Adj, const QueryDesc, uint32_t *, uint32_t *, const HardArgs);
 
-static bool pick_fused(uint32_t wdl, uint32_t wbl, fused_fn &f, size_t &smem) {
-#define DBL_QF(A, B) if (wdl == A && wbl == B) { f = query_fused_kernel<A, B>; smem = sizeof(WarpBfs<A, B>) * (FUSED_THREADS / 32); return true; }
-    DBL_QF(0, 1) DBL_QF(1, 1) DBL_QF(2, 1) DBL_QF(4, 1) DBL_QF(0, 2) DBL_QF(1, 2) DBL_QF(2, 2)
-#undef DBL_QF
-    return false;
-}
-
-static bool pick_quad(uint32_t wdl, uint32_t wbl, fused_fn &f, size_t &smem) {
+static bool pick_quad(uint32_t wdl, uint32_t wbl, quad_fn &f, size_t &smem) {
 #define DBL_QQ(A, B) if (wdl == A && wbl == B) { f = query_quad_kernel<A, B>; smem = sizeof(WarpBfs<A, B>) * (FUSED_THREADS / 32); return true; }
     DBL_QQ(2, 1) DBL_QQ(4, 1) DBL_QQ(1, 2) DBL_QQ(2, 2)
 #undef DBL_QQ
     return false;
 }
 
-typedef void (*label_fn)(const uint64_t *, uint32_t, const uint32_t *, const uint32_t *, uint64_t,
-                         uint32_t, uint8_t *, uint32_t *, uint32_t *, uint32_t *);
-
-static label_fn pick_label(uint32_t wdl, uint32_t wbl) {
-#define DBL_QK(A, B) if (wdl == A && wbl == B) return label_check_kernel<A, B>;
-    DBL_QK(0, 1) DBL_QK(1, 1) DBL_QK(2, 1) DBL_QK(4, 1) DBL_QK(0, 2) DBL_QK(1, 2) DBL_QK(2, 2)
-#undef DBL_QK
-    return nullptr;
-}
-
 // Launch geometry of the hard path (64-query groups, then dense groups).
 struct HardPath {
     int grid = 0, dctas = 0;
     size_t smem = 0, dsmem = 0;
+    char *ws = nullptr;
 };
 
+static size_t dense_slab(const dbl_index *idx) { return (size_t)idx->n * 32; }
+
+// The dense kernel's workspace (one n x 32-byte slab per CTA) is allocated
+// the first time a batch needs it, never up front: at n = 2^30 one slab is
+// 32 GB.  A batch that lists dense groups while the workspace is absent
+// closes with them unanswered (result words: overflow > 0, dense ticket 0);
+// the host then allocates the workspace and re-runs the batch
+// (query_needs_dense).  Up to 8 CTAs within min(4 GB, free / 4).
+dbl_status ensure_dense(const dbl_index *idx, dbl_graph *g) {
+    const size_t slab = dense_slab(idx);
+    if (g->q_dense.bytes >= slab + 16) return DBL_OK;
+    size_t free_b = 0, total_b = 0;
+    DBL_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    size_t budget = free_b / 4;
+    if (budget > ((size_t)4 << 30)) budget = (size_t)4 << 30;
+    size_t ctas = budget / slab;
+    if (ctas < 1) ctas = 1;
+    if (ctas > 8) ctas = 8;
+    dbl_status s = g->q_dense.ensure(slab * ctas + 16);
+    if (s && ctas > 1) s = g->q_dense.ensure(slab + 16);
+    if (s) set_error("query: the dense BFS workspace (" + std::to_string(slab >> 20) + " MB per CTA) does not fit");
+    return s;
+}
+
+bool query_needs_dense(const uint32_t *res) { return res[CNT_OVERFLOW] != 0 && res[CNT_DTICKET] == 0; }
+
 static dbl_status hard_path_config(const dbl_index *idx, dbl_graph *g, HardPath &hp) {
-    static int bps = -1;
-    static size_t last_smem = 0, last_dsmem = 0;
     hp.smem = bfs_smem(idx->wdl, idx->wbl, false);
     hp.dsmem = bfs_smem(idx->wdl, idx->wbl, true);
-    if (bps < 0 || last_smem != hp.smem || last_dsmem != hp.dsmem) {
-        DBL_CUDA(cudaFuncSetAttribute((const void *)bfs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)hp.smem));
-        DBL_CUDA(cudaFuncSetAttribute((const void *)bfs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)hp.dsmem));
-        DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, bfs_kernel<false>, BFS_THREADS, hp.smem));
-        if (bps < 1) bps = 1;
-        last_smem = hp.smem;
-        last_dsmem = hp.dsmem;
-    }
+    int bps = 1, dbps = 1;
+    dbl_status s;
+    if ((s = kernel_occupancy((const void *)bfs_kernel<false>, BFS_THREADS, hp.smem, &bps)) ||
+        (s = kernel_occupancy((const void *)bfs_kernel<true>, BFS_THREADS, hp.dsmem, &dbps)))
+        return s;
     hp.grid = g->sm_count * bps;
-    const size_t slab = (size_t)idx->n * 32;
-    hp.dctas = 8;
-    const size_t budget = (size_t)4 << 30;
-    while (hp.dctas > 1 && slab * hp.dctas > budget) --hp.dctas;
-    return g->q_dense.ensure(slab * hp.dctas + 16);
+    const size_t slab = dense_slab(idx);
+    if (g->q_dense.p && g->q_dense.bytes >= slab + 16) {
+        hp.ws = g->q_dense.as<char>();
+        size_t c = (g->q_dense.bytes - 16) / slab;
+        hp.dctas = (int)(c > 8 ? 8 : c);
+    }
+    return DBL_OK;
 }
 
-// One batch = one launch on the fast path: the fused kernel (K6 + per-warp
-// K7) takes its arguments by value and leaves the counters zeroed; the
-// 64-query group kernel and the dense kernel are tail-launched from the
-// device only when some warp's BFS table overflowed (never on cfg2), so the
-// host submits one kernel and no memset, copy or graph per batch.
-static bool pivot_prune_off() {
-    static const bool off = std::getenv("DBL_NO_PIVOT_PRUNE") != nullptr;
-    return off;
-}
-
+// One batch = one launch on the fast path: the gather kernel (K6 + K7)
+// takes its arguments by value and leaves the counters zeroed; the warp,
+// 64-query group and dense kernels are tail-launched from the device only
+// when some query outgrew the previous stage (never on cfg2), so the host
+// submits one kernel and no memset, copy or graph per batch.
 dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
                      uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, bool host_result) {
     if (count >= 0xffffffffull) { set_error("query batch too large"); return DBL_E_ARG; }
@@ -1727,13 +1442,11 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     if ((s = g->q_host_res.ensure(CNT_WORDS * 4))) return s;
     QueryDesc qd{u, v, codes, visited, (uint32_t)count, flags, 0, 0, Pivot{},
                  host_result ? reinterpret_cast<uint32_t *>(g->q_host_res.p) : nullptr};
-    if (idx->has_scc && !pivot_prune_off()) {
+    if (idx->has_scc && !DBL_NO_PIVOT_PRUNE) {
         qd.pv.dmask = idx->dmask.as<uint32_t>();
         qd.pv.scc = idx->sccmask.as<unsigned long long>();
         qd.pv.n = idx->dmask_n;
     }
-    qd.vec_ok = ((((uintptr_t)u) | ((uintptr_t)v)) & (4 * QPL - 1)) == 0 && (((uintptr_t)codes) & (QPL - 1)) == 0 &&
-                (!visited || (((uintptr_t)visited) & (4 * QPL - 1)) == 0);
     uint32_t *pending = g->q_pending.as<uint32_t>();
     uint32_t *counters = g->q_counters.as<uint32_t>();
     uint32_t *ovf = pending + g->q_pending_cap + 16;
@@ -1741,30 +1454,21 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     const Adj adj = graph_fwd(g);
     HardPath hp;
     if ((s = hard_path_config(idx, g, hp))) return s;
-    static const bool no_fused = std::getenv("DBL_NO_FUSED") != nullptr;
-    static const bool old_fused = std::getenv("DBL_QFUSED") != nullptr;
-    static const bool lean_wide = std::getenv("DBL_LEAN_WIDE") != nullptr;
+    g->q_last = {idx, u, v, codes, visited, count, flags};
     lean_fn lean = nullptr;
     bfsw_fn bfsw = nullptr;
     size_t wsmem = 0;
-    // k <= 64: lean gather + per-thread BFS; wider labels (cfg5, k = 256),
-    // whose fallbacks outgrow the thread BFS, keep the fused kernel with the
-    // warp BFS interleaved between tiles (measured on cfg5: 4.6 vs 3.7 G q/s)
-    if (count && !no_fused && !old_fused && (DBL_TBFS_ALL || idx->wdl <= 1 || lean_wide) &&
-        pick_lean(idx->wdl, idx->wbl, lean, bfsw, wsmem)) {
-        static int lbps = -1, wbps = -1;
-        static const void *last_fn = nullptr;
-        if (lbps < 0 || last_fn != (const void *)bfsw) {
-            DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lbps, lean, 256, 0));
-            DBL_CUDA(cudaFuncSetAttribute((const void *)bfsw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
-            DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wbps, bfsw, FUSED_THREADS, wsmem));
-            if (lbps < 1) lbps = 1;
-            if (wbps < 1) wbps = 1;
-            last_fn = (const void *)bfsw;
-        }
+    // k <= 64: lean gather + per-lane deferred BFS; wider labels (cfg5,
+    // k = 256), whose fallbacks outgrow the small BFS bounds, take the
+    // lane-quad gather with the warp BFS (measured on cfg5: 4.6 vs 3.7 G q/s)
+    if (count && (DBL_TBFS_ALL || DBL_LEAN_WIDE || idx->wdl <= 1) && pick_lean(idx->wdl, idx->wbl, lean, bfsw, wsmem)) {
+        int lbps = 1, wbps = 1;
+        if ((s = kernel_occupancy((const void *)lean, 256, 0, &lbps)) ||
+            (s = kernel_occupancy((const void *)bfsw, FUSED_THREADS, wsmem, &wbps)))
+            return s;
         uint32_t *wovf = pending + 2 * g->q_pending_cap + 32;
         const HardArgs ha{hp.grid, hp.dctas, (uint32_t)hp.smem, (uint32_t)hp.dsmem, idx->wdl, idx->wbl, ovf,
-                          g->q_dense.as<char>(), g->sm_count * wbps, (uint32_t)wsmem, wovf};
+                          hp.ws, g->sm_count * wbps, (uint32_t)wsmem, wovf};
         uint32_t lgrid = (uint32_t)((count + 255) / 256);
         if (lgrid > (uint32_t)(g->sm_count * lbps)) lgrid = (uint32_t)(g->sm_count * lbps);
         DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
@@ -1774,51 +1478,39 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
         g->q_timed_bfs = false;
         return DBL_OK;
     }
-    fused_fn fused = nullptr;
+    quad_fn quad = nullptr;
     size_t fsmem = 0;
-    static const bool no_quad = std::getenv("DBL_NO_QUAD") != nullptr;
-    const bool quad = count && !no_fused && !no_quad && pick_quad(idx->wdl, idx->wbl, fused, fsmem);
-    if (quad || (count && !no_fused && pick_fused(idx->wdl, idx->wbl, fused, fsmem))) {
-        static int fbps = -1;
-        static const void *last_fn = nullptr;
-        if (fbps < 0 || last_fn != (const void *)fused) {
-            DBL_CUDA(cudaFuncSetAttribute((const void *)fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
-            DBL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fbps, fused, FUSED_THREADS, fsmem));
-            if (fbps < 1) fbps = 1;
-            last_fn = (const void *)fused;
-        }
-        const HardArgs ha{hp.grid, hp.dctas, (uint32_t)hp.smem, (uint32_t)hp.dsmem, idx->wdl, idx->wbl, ovf,
-                          g->q_dense.as<char>()};
+    if (count && pick_quad(idx->wdl, idx->wbl, quad, fsmem)) {
+        int fbps = 1;
+        if ((s = kernel_occupancy((const void *)quad, FUSED_THREADS, fsmem, &fbps))) return s;
+        const HardArgs ha{hp.grid, hp.dctas, (uint32_t)hp.smem, (uint32_t)hp.dsmem, idx->wdl, idx->wbl, ovf, hp.ws};
         DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
-        fused<<<g->sm_count * fbps, FUSED_THREADS, fsmem, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);
-        DBL_CHECK_LAUNCH(quad ? "query_quad_kernel" : "query_fused_kernel");
+        quad<<<g->sm_count * fbps, FUSED_THREADS, fsmem, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);
+        DBL_CHECK_LAUNCH("query_quad_kernel");
         DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
         g->q_timed_bfs = false;
         return DBL_OK;
     }
-    // generic widths (or DBL_NO_FUSED): label kernel, then the group and
+    // generic widths (k > 256 or k' > 128): label kernel, then the group and
     // dense kernels, then the counter close
     DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
     if (count) {
         int blocks = (int)((count + 255) / 256);
         if (blocks > g->sm_count * 16) blocks = g->sm_count * 16;
-        const label_fn label = pick_label(idx->wdl, idx->wbl);
-        if (label)
-            label<<<blocks, 256, 0, g->stream>>>(rec, idx->n, u, v, count, flags, codes, visited, pending, counters);
-        else
-            label_check_generic<<<blocks, 256, 0, g->stream>>>(rec, idx->n, idx->wdl, idx->wbl, u, v, count, flags,
-                                                               codes, visited, pending, counters);
-        DBL_CHECK_LAUNCH("label_check_kernel");
+        label_check_generic<<<blocks, 256, 0, g->stream>>>(rec, idx->n, idx->wdl, idx->wbl, u, v, count, flags,
+                                                           codes, visited, pending, counters);
+        DBL_CHECK_LAUNCH("label_check_generic");
     }
     DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
     if (count) {
         bfs_kernel<false><<<hp.grid, BFS_THREADS, hp.smem, g->stream>>>(rec, idx->wdl, idx->wbl, idx->n, adj, qd,
                                                                         pending, counters, ovf, nullptr);
         DBL_CHECK_LAUNCH("bfs_kernel");
-        bfs_kernel<true><<<hp.dctas, BFS_THREADS, hp.dsmem, g->stream>>>(rec, idx->wdl, idx->wbl, idx->n, adj, qd,
-                                                                         pending, counters, ovf,
-                                                                         g->q_dense.as<char>());
-        DBL_CHECK_LAUNCH("bfs_kernel_dense");
+        if (hp.ws) {
+            bfs_kernel<true><<<hp.dctas, BFS_THREADS, hp.dsmem, g->stream>>>(rec, idx->wdl, idx->wbl, idx->n, adj,
+                                                                             qd, pending, counters, ovf, hp.ws);
+            DBL_CHECK_LAUNCH("bfs_kernel_dense");
+        }
     }
     finish_batch_kernel<<<1, 32, 0, g->stream>>>(counters, qd.hres);
     DBL_CHECK_LAUNCH("finish_batch_kernel");
@@ -1827,14 +1519,18 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     return DBL_OK;
 }
 
-// Copy the range-error flag of the last batch to dst (device, stream-ordered).
+// Copy result words [ERR, DTICKET] of the last batch (range-error flag,
+// group ticket, dense-group count, dense ticket) to dst[0..3] (device,
+// stream-ordered): the chunked host pipeline keeps one set per chunk.
 dbl_status query_err_to(dbl_graph *g, uint32_t *dst) {
-    DBL_CUDA(cudaMemcpyAsync(dst, g->q_counters.as<uint32_t>() + CNT_RES + CNT_ERR, 4, cudaMemcpyDeviceToDevice,
+    DBL_CUDA(cudaMemcpyAsync(dst, g->q_counters.as<uint32_t>() + CNT_RES + CNT_ERR, 4 * 4, cudaMemcpyDeviceToDevice,
                              g->stream));
     return DBL_OK;
 }
 
-// Event times of the last batch: the fused kernel's span (incl. any
+bool chunk_needs_dense(const uint32_t *w4) { return w4[CNT_OVERFLOW - CNT_ERR] != 0 && w4[CNT_DTICKET - CNT_ERR] == 0; }
+
+// Event times of the last batch: the gather kernel's span (incl. any
 // tail-launched hard path) as "label", the separate BFS kernels as "bfs".
 void query_timings(dbl_graph *g) {
     cudaEventElapsedTime(&g->t_label, g->ev[2], g->ev[3]);
@@ -1842,12 +1538,33 @@ void query_timings(dbl_graph *g) {
     if (g->q_timed_bfs) cudaEventElapsedTime(&g->t_bfs, g->ev[3], g->ev[4]);
 }
 
-dbl_status query_finish(dbl_graph *g, uint32_t *err_out) {
-    // the closing CTA wrote the result words into the pinned q_host_res:
-    // the stream synchronisation is the batch's only host step (timings are
-    // read lazily by dbl_last_timings)
+// Wait for the batch; *err_out = range-error flag, *dense_out = it left
+// groups for a dense workspace that was not allocated yet.  The closing CTA
+// wrote the result words into the pinned q_host_res, so the stream sync is
+// the batch's only host step (timings are read lazily by dbl_last_timings).
+dbl_status query_finish(dbl_graph *g, uint32_t *err_out, bool *dense_out) {
     DBL_CUDA(cudaStreamSynchronize(g->stream));
-    *err_out = reinterpret_cast<const volatile uint32_t *>(g->q_host_res.p)[CNT_ERR];
+    const volatile uint32_t *r = reinterpret_cast<const volatile uint32_t *>(g->q_host_res.p);
+    uint32_t w[CNT_WORDS];
+    for (int i = 0; i < CNT_WORDS; ++i) w[i] = r[i];
+    *err_out = w[CNT_ERR];
+    *dense_out = query_needs_dense(w);
+    return DBL_OK;
+}
+
+// dbl_sync: wait for the stream; if the last batch (an async one) left dense
+// groups, allocate the workspace and re-run it with the same arguments.
+dbl_status query_sync(dbl_graph *g) {
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    if (!g->q_counters.p || !g->q_last.idx) return DBL_OK;
+    uint32_t w[CNT_WORDS];
+    DBL_CUDA(cudaMemcpy(w, g->q_counters.as<uint32_t>() + CNT_RES, sizeof(w), cudaMemcpyDeviceToHost));
+    if (!query_needs_dense(w)) return DBL_OK;
+    const QueryArgs a = g->q_last;
+    dbl_status s;
+    if ((s = ensure_dense(a.idx, g))) return s;
+    if ((s = run_query(a.idx, g, a.u, a.v, a.count, a.flags, a.codes, a.visited))) return s;
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
     return DBL_OK;
 }
 

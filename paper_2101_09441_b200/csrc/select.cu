@@ -510,12 +510,9 @@ dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_
         topk_candidates_kernel<<<blocks, 256, 0, g->stream>>>(A.score, n, k, st, cs, ci);
         DBL_CHECK_LAUNCH("topk_candidates_kernel");
         const int fsmem = (int)cand_bytes;
-        static bool attr = false;
-        if (!attr) {
-            DBL_CUDA(cudaFuncSetAttribute((const void *)topk_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          fsmem));
-            attr = true;
-        }
+        int fbps = 1;
+        dbl_status fs = kernel_occupancy((const void *)topk_final_kernel, 1024, (size_t)fsmem, &fbps);
+        if (fs) return fs;
         topk_final_kernel<<<1, 1024, fsmem, g->stream>>>(cs, ci, k, st, idx->landmarks.as<uint32_t>(), A.rec, idx->rs,
                                                          H, bits0, bits1, a0, e0, a1, e1);
         DBL_CHECK_LAUNCH("topk_final_kernel");

@@ -44,9 +44,8 @@ class DynamicGraph:
         src/dst may be host arrays or CUDA tensors (uint32 ids, any 32-bit dtype).
         """
         g = cls(n, device=device)
-        if hasattr(src, "is_cuda") and src.is_cuda:
-            if src.numel() != dst.numel():
-                raise ValueError("src and dst differ in length")
+        if (hasattr(src, "is_cuda") and src.is_cuda) or (hasattr(dst, "is_cuda") and dst.is_cuda):
+            N.check_device_ids(src, dst, src.device.index if hasattr(src, "device") else device)
             h = ctypes.c_void_p()
             N.device_inputs_ready(src, dst)
             N.call("dbl_graph_create", n, N.ptr(src), N.ptr(dst), src.numel(), N.MEM_DEVICE, src.device.index,
@@ -229,12 +228,19 @@ def as_device_graph(g, device: int = 0) -> DynamicGraph:
     """Accept this package's graph or any reference-style graph object.
 
     A reference dblreach.DynamicGraph (forward adjacency lists, graph.py:36)
-    is uploaded once and cached until its vertex or edge count changes.
+    is uploaded once and cached per (object, device) until its vertex or edge
+    count -- or its `version` attribute, if it has one -- changes.  The
+    reference graph carries no mutation counter, so a remove_edge followed by
+    an add_edge on the reference object itself keeps both counts and the
+    cached copy would be stale: call forget_device_graph(g) after mutating a
+    reference graph directly (edges inserted through this package's
+    insert_edge / insert_edges go to the cached device copy and stay
+    consistent with the index).
     """
     if isinstance(g, DynamicGraph):
         return g
     if hasattr(g, "forward") and hasattr(g, "vertex_count"):
-        key = (g.vertex_count, getattr(g, "edge_count", None))
+        key = (g.vertex_count, getattr(g, "edge_count", None), getattr(g, "version", None), device)
         try:
             cached = _converted.get(g)
         except TypeError:
@@ -250,3 +256,11 @@ def as_device_graph(g, device: int = 0) -> DynamicGraph:
             pass
         return dg
     raise TypeError(f"expected a DynamicGraph, got {type(g)!r}")
+
+
+def forget_device_graph(g) -> None:
+    """Drop the cached device copy of a reference graph (re-uploaded on next use)."""
+    try:
+        _converted.pop(g, None)
+    except TypeError:
+        pass

@@ -156,10 +156,20 @@ def _check_consistent(g, idx: DblIndex) -> None:
             f"graph has {g.vertex_count} vertices but index has {idx.vertex_count}")
 
 
+def _is_column(x) -> bool:
+    return isinstance(x, np.ndarray) or (hasattr(x, "is_cuda") and hasattr(x, "numel"))
+
+
 def _pairs_to_arrays(queries) -> tuple[np.ndarray, np.ndarray]:
-    if isinstance(queries, tuple) and len(queries) == 2 and hasattr(queries[0], "__len__") \
-            and not isinstance(queries[0], (int, np.integer)):
+    # the column form (u_array, v_array) only for a 2-tuple of 1-D arrays /
+    # tensors of equal length; any other iterable is a sequence of (u, v)
+    # pairs as in the reference (so ((0, 5), (3, 7)) is the pairs (0,5), (3,7))
+    if isinstance(queries, tuple) and len(queries) == 2 and _is_column(queries[0]) \
+            and _is_column(queries[1]) and np.ndim(queries[0]) == 1 and np.ndim(queries[1]) == 1 \
+            and len(queries[0]) == len(queries[1]):
         u, v = queries
+        if hasattr(u, "is_cuda"):
+            u, v = u.cpu().numpy(), v.cpu().numpy()
         return N.u32_array(u), N.u32_array(v)
     if isinstance(queries, np.ndarray):
         a = queries.reshape(-1, 2)
@@ -180,8 +190,9 @@ def query_codes(g, idx: DblIndex, u, v, flags: QueryFlags = DEFAULT_FLAGS,
     """
     g = as_device_graph(g)
     _check_consistent(g, idx)
-    if hasattr(u, "is_cuda") and u.is_cuda:
+    if (hasattr(u, "is_cuda") and u.is_cuda) or (hasattr(v, "is_cuda") and v.is_cuda):
         import torch
+        N.check_device_ids(u, v, g.device)
         codes = torch.empty(u.numel(), dtype=torch.uint8, device=u.device)
         vis = torch.empty(u.numel(), dtype=torch.int32, device=u.device) if with_visited else None
         N.device_inputs_ready(u, v)
@@ -189,6 +200,8 @@ def query_codes(g, idx: DblIndex, u, v, flags: QueryFlags = DEFAULT_FLAGS,
                N.ptr(codes), N.ptr(vis), N.MEM_DEVICE)
         return codes, vis
     a, b = N.u32_array(u), N.u32_array(v)
+    if a.ndim != 1 or b.ndim != 1 or len(a) != len(b):
+        raise ValueError(f"u and v must be 1-D and of equal length ({a.shape} vs {b.shape})")
     codes = np.zeros(len(a), np.uint8)
     vis = np.zeros(len(a), np.uint32) if with_visited else None
     N.call("dbl_query", idx.handle, g.handle, N.ptr(a), N.ptr(b), len(a), flags.bits(), N.ptr(codes),

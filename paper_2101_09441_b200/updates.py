@@ -61,6 +61,8 @@ class BatchUpdateStats:
     labels_changed: int = 0
     levels: int = 0
     delta_merged: bool = False
+    fix_items: int = 0     # delta fixpoint: frontier items expanded (work counter)
+    fix_edges: int = 0     # delta fixpoint: edges relaxed (work counter)
 
 
 def insert_edge(g, idx: DblIndex, u: int, v: int) -> UpdateStats:
@@ -85,7 +87,8 @@ def insert_edges(g, idx: DblIndex, u, v) -> BatchUpdateStats:
     g = as_device_graph(g)
     _check_consistent(g, idx)
     st = N.BatchStatsC()
-    if hasattr(u, "is_cuda") and u.is_cuda:
+    if (hasattr(u, "is_cuda") and u.is_cuda) or (hasattr(v, "is_cuda") and v.is_cuda):
+        N.check_device_ids(u, v, g.device)
         N.device_inputs_ready(u, v)
         N.call("dbl_insert_edges", idx.handle, g.handle, N.ptr(u), N.ptr(v), u.numel(), N.MEM_DEVICE,
                ctypes.byref(st))
@@ -99,7 +102,8 @@ def insert_edges(g, idx: DblIndex, u, v) -> BatchUpdateStats:
     g.version += 1
     idx._invalidate()
     return BatchUpdateStats(int(st.requested), int(st.inserted), int(st.certified),
-                            int(st.labels_changed), int(st.levels), bool(st.delta_merged))
+                            int(st.labels_changed), int(st.levels), bool(st.delta_merged),
+                            int(st.fix_items), int(st.fix_edges))
 
 
 def insert_vertex(g, idx: DblIndex, out_edges: Iterable[int] = (),

@@ -137,3 +137,34 @@ def test_product_package_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"\b(import|from)\s+oracle\b|oracle/|dbl_oracle|\borc_", text), f
+
+
+def test_pairs_tuple_of_pairs_is_pairs():
+    """A 2-tuple of (u, v) pairs means two queries, as in the reference; only a
+    2-tuple of equal-length 1-D arrays is the column form."""
+    from paper_2101_09441_b200.queries import _pairs_to_arrays
+    u, v = _pairs_to_arrays(((0, 5), (3, 7)))
+    assert u.tolist() == [0, 3] and v.tolist() == [5, 7]
+    u, v = _pairs_to_arrays([(0, 5), (3, 7)])
+    assert u.tolist() == [0, 3] and v.tolist() == [5, 7]
+    u, v = _pairs_to_arrays((np.array([0, 3]), np.array([5, 7])))
+    assert u.tolist() == [0, 3] and v.tolist() == [5, 7]
+    # arrays of different lengths are not columns: read as pairs -> error
+    with pytest.raises(Exception):
+        _pairs_to_arrays((np.array([0, 3, 4]), np.array([5, 7])))
+    u, v = _pairs_to_arrays(np.array([[1, 2], [3, 4]]))
+    assert u.tolist() == [1, 3] and v.tolist() == [2, 4]
+
+
+def test_slice_bounds_match_reference_pool():
+    """Contiguous slices of ceil(q / parts) (queries.py:231-232)."""
+    from paper_2101_09441_b200.parallel import slice_bounds
+    for q in (0, 1, 7, 10, 1000, 1001):
+        for parts in (1, 2, 3, 8):
+            b = slice_bounds(q, parts)
+            assert len(b) == parts
+            chunk = -(-q // parts) if q else 1
+            ref = [(i, min(i + chunk, q)) for i in range(0, q, chunk)]
+            assert b[:len(ref)] == ref
+            assert all(lo == hi == q for lo, hi in b[len(ref):])
+            assert sum(hi - lo for lo, hi in b) == q
