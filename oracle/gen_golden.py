@@ -21,6 +21,12 @@ Fixtures:
   family.npz     C4-style family (tests/test_acceptance.py:30-37): graphs,
                  metadata, labels, all-pairs codes, insert-sequence results.
   cfg1.npz       BASELINE config 1 (ER 10k/50k, 100k queries, 1000 inserts).
+  label_tests.npz  dl_intersec / bl_contain (labels.py:315-327) for all pairs
+                 of the worked example (the KATs of tests/test_labels.py:166-191
+                 are rows of it) and of seeded random graphs with one- and
+                 multi-word labels, with those graphs' reference labels.
+
+    python oracle/gen_golden.py [fixture ...]     # default: all fixtures
 """
 from __future__ import annotations
 
@@ -255,11 +261,41 @@ def gen_snapshots():
     return d
 
 
+def gen_label_tests():
+    """dl_intersec / bl_contain of the reference on all pairs."""
+    d = {}
+    g = RC.example_graph()
+    idx = RC.example_index(g)
+    pairs = [(x, y) for x in range(11) for y in range(11)]
+    d["toy_x"] = np.array([p[0] for p in pairs], np.uint32)
+    d["toy_y"] = np.array([p[1] for p in pairs], np.uint32)
+    d["toy_dl"] = np.array([R.dl_intersec(idx, x, y) for x, y in pairs], np.uint8)
+    d["toy_bl"] = np.array([R.bl_contain(idx, x, y) for x, y in pairs], np.uint8)
+    cases = {"r64": (90, 4, 11, R.IndexConfig(k=64, k_prime=64)),
+             "r130": (150, 3, 12, R.IndexConfig(k=130, k_prime=96, leaf_threshold=2)),
+             "dag": (100, 5, 13, R.IndexConfig(k=20, k_prime=7))}
+    for name, (n, deg, seed, cfg) in cases.items():
+        g = R.gen_random_graph(n, deg, seed=seed, acyclic=name == "dag")
+        idx = R.build_index(g, cfg)
+        p = name + "_"
+        d[p + "n"], d[p + "k"], d[p + "k_prime"] = np.int64(n), np.int64(cfg.k), np.int64(cfg.k_prime)
+        d[p + "threshold"] = np.int64(cfg.leaf_threshold)
+        d[p + "src"], d[p + "dst"] = edges_of(g)
+        d.update(index_arrays(p, g, idx))
+        d[p + "dl"] = np.array([[R.dl_intersec(idx, x, y) for y in range(n)] for x in range(n)], np.uint8)
+        d[p + "bl"] = np.array([[R.bl_contain(idx, x, y) for y in range(n)] for x in range(n)], np.uint8)
+    return d
+
+
+FIXTURES = {"toy": gen_toy, "leaf_hash": gen_leaf_hash, "landmarks": gen_landmarks, "family": gen_family,
+            "cfg1": gen_cfg1, "snapshots": gen_snapshots, "label_tests": gen_label_tests}
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
-    for name, fn in (("toy", gen_toy), ("leaf_hash", gen_leaf_hash),
-                     ("landmarks", gen_landmarks), ("family", gen_family), ("cfg1", gen_cfg1),
-                     ("snapshots", gen_snapshots)):
+    names = sys.argv[1:] or list(FIXTURES)
+    for name in names:
+        fn = FIXTURES[name]
         d = fn()
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **d)

@@ -256,3 +256,16 @@ def csr_query_batch(n: int, ptr, col, k: int, k_prime: int, labels: dict, qu, qv
     if rc:
         raise IndexError("oracle query failed")
     return codes
+
+
+def label_tests(labels: dict, x, y) -> tuple[np.ndarray, np.ndarray]:
+    """dl_intersec (labels.py:315-319) and bl_contain (labels.py:322-327) over
+    u64 word arrays: dl_out[x] & dl_in[y] != 0; bl_in[x] subset of bl_in[y]
+    and bl_out[y] subset of bl_out[x]."""
+    x = np.asarray(x, np.int64)
+    y = np.asarray(y, np.int64)
+    dl = (labels["dl_out"][x] & labels["dl_in"][y]).any(axis=1) if labels["dl_in"].shape[1] else \
+        np.zeros(len(x), bool)
+    bl = ~((labels["bl_in"][x] & ~labels["bl_in"][y]).any(axis=1)
+           | (labels["bl_out"][y] & ~labels["bl_out"][x]).any(axis=1))
+    return dl, bl

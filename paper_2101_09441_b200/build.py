@@ -19,7 +19,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUTDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUTDIR, "libdbl_b200.so")
-SOURCES = ["graph.cu", "select.cu", "fixpoint.cu", "query.cu", "verify.cu", "abi.cu"]
+SOURCES = ["graph.cu", "select.cu", "fixpoint.cu", "query.cu", "verify.cu", "insert_one.cu", "abi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

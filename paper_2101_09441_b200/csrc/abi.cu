@@ -322,6 +322,7 @@ static dbl_status index_create(const dbl_graph *gc, const dbl_config *cfg, const
     *out = nullptr;
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     if (landmarks && cfg->k) {  // LandmarkSet.of + _check_vertex (labels.py:59-63, 279-283)
         std::vector<uint32_t> seen(landmarks, landmarks + cfg->k);
@@ -408,6 +409,7 @@ extern "C" dbl_status dbl_index_rebuild(const dbl_graph *gc, dbl_index *idx) {
     if (s) return s;
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     return run_build(g, idx, nullptr, 0);
 }
@@ -420,6 +422,7 @@ extern "C" dbl_status dbl_index_build_words(const dbl_graph *gc, dbl_index *idx,
         if (words[i] >= idx->rw) { set_error("record word out of range"); return DBL_E_ARG; }
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     return run_build(g, idx, words, nwords);
 }
@@ -564,6 +567,7 @@ extern "C" dbl_status dbl_graph_add_vertices(dbl_graph *g, uint32_t count) {
     if (!count) return DBL_OK;
     if ((uint64_t)g->n + count >= 0xffffffffull) { set_error("vertex count overflow"); return DBL_E_CONFIG; }
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     DBL_CUDA(cudaStreamSynchronize(g->stream));
     const uint32_t n0 = g->n, n1 = n0 + count;
@@ -689,6 +693,36 @@ static dbl_status query_host_pipelined(const dbl_index *idx, dbl_graph *g, const
     return DBL_OK;
 }
 
+// Small pageable host batches: the pairs are copied into a pinned staging
+// buffer of the graph and read by the query kernel over PCIe (zero-copy),
+// which also writes the codes there; one launch and one stream sync instead
+// of the copy pipeline's seven operations (a single query() call).
+constexpr uint64_t STAGE_MAX = 1ull << 16;
+
+static dbl_status query_host_staged(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
+                                    uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited) {
+    dbl_status s;
+    const uint64_t cpad = (count + 63) & ~63ull;
+    if ((s = g->q_stage.ensure(cpad * 13 + 256))) return s;
+    uint32_t *su = reinterpret_cast<uint32_t *>(g->q_stage.p), *sv = su + cpad;
+    uint32_t *svis = sv + cpad;
+    uint8_t *sc = reinterpret_cast<uint8_t *>(svis + cpad);
+    std::memcpy(su, u, count * 4);
+    std::memcpy(sv, v, count * 4);
+    if ((s = run_query(idx, g, su, sv, count, flags, sc, visited ? svis : nullptr, true))) return s;
+    uint32_t err = 0;
+    bool dense = false;
+    if ((s = query_finish(g, &err, &dense))) return s;
+    if (err) { set_error("query vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+    if (dense) {
+        if ((s = ensure_dense(idx, g))) return s;
+        return query_host_staged(idx, g, u, v, count, flags, codes, visited);
+    }
+    std::memcpy(codes, sc, count);
+    if (visited) std::memcpy(visited, svis, count * 4);
+    return DBL_OK;
+}
+
 static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const uint32_t *u, const uint32_t *v,
                              uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, dbl_mem mem,
                              bool sync) {
@@ -697,6 +731,7 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
     if (count && (!u || !v || !codes)) { set_error("null argument"); return DBL_E_ARG; }
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     if (mem == DBL_MEM_HOST && count) {
         // Page-locked host buffers are read and written by the query kernels
@@ -717,7 +752,9 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
                 dptr[i] = at.devicePointer;
             }
         }
-        if (!pinned) return query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
+        if (!pinned)
+            return count <= STAGE_MAX ? query_host_staged(idx, g, u, v, count, flags, codes, visited)
+                                      : query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
         if ((s = run_query(idx, g, (const uint32_t *)dptr[0], (const uint32_t *)dptr[1], count, flags,
                            (uint8_t *)dptr[2], (uint32_t *)dptr[3], sync)))
             return s;
@@ -832,39 +869,36 @@ extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, 
     DBL_CUDA(cudaSetDevice(g->device));
     set_stream(g->stream);
     dbl_update_stats st{};
+    // one launch + one sync: pre-check, add_edge into the pending log, both
+    // propagations (insert_one.cu)
+    bool done = false;
+    uint32_t dirs_done = 0;
+    if ((s = insert_edge_fast(idx, g, u, v, &st, &done, &dirs_done))) return s;
+    if (done) {
+        if (stats) *stats = st;
+        return DBL_OK;
+    }
+    // a cone outgrew the single-CTA tables (no label was written; the edge is
+    // in the graph): fold the log into the delta adjacency and run the batch
+    // fixpoint from this edge's seeds
+    if ((s = graph_flush_pending(g))) return s;
     const uint64_t key = ((uint64_t)u << 32) | v;
-    if ((s = g->scratch_b.ensure(64))) return s;
-    uint64_t *dkey = g->scratch_b.as<uint64_t>();
-    DBL_CUDA(cudaMemcpyAsync(dkey, &key, 8, cudaMemcpyHostToDevice, g->stream));
-    uint64_t cert = 0;  // pre-check on pre-insertion labels, updates.py:123
-    if ((s = count_certified(g, idx, dkey, 1, &cert))) return s;
-    // add_edge (updates.py:124); graph_filter_new/insert_delta use scratch_a..d
     DevBuf kb;
     if ((s = kb.ensure(16))) return s;
     DBL_CUDA(cudaMemcpyAsync(kb.p, &key, 8, cudaMemcpyHostToDevice, g->stream));
-    uint64_t nnew = 0;
-    DevBuf nb;
-    if ((s = nb.ensure(16))) { kb.release(); return s; }
-    s = graph_filter_new(g, kb.as<uint64_t>(), 1, nb.as<uint64_t>(), &nnew);
-    if (!s && nnew) s = graph_insert_delta(g, nb.as<uint64_t>(), nnew);
-    st.inserted = (uint32_t)nnew;
-    if (s || cert) {
-        kb.release();
-        nb.release();
-        if (!s) {
-            st.early_terminated = 1;
-            if (stats) *stats = st;
-        }
-        return s;
-    }
     uint32_t changed[2], seedc[2], levels = 0;
     s = run_insert(g, idx, kb.as<uint64_t>(), 1, true, changed, seedc, &levels);
     kb.release();
-    nb.release();
     if (s) return s;
-    // _propagate_union dequeues the seed plus every changed non-seed vertex
-    st.visited = (1 + changed[0] - seedc[0]) + (1 + changed[1] - seedc[1]);
-    st.labels_changed = changed[0] + changed[1];
+    // _propagate_union dequeues the seed plus every changed non-seed vertex;
+    // a direction the fast path already finished (its labels are final, so
+    // the fixpoint changes nothing there) keeps the fast path's counts
+    if (dirs_done == 0) {
+        st.visited = 1 + changed[0] - seedc[0];
+        st.labels_changed = changed[0];
+    }
+    st.visited += 1 + changed[1] - seedc[1];
+    st.labels_changed += changed[1];
     if (stats) *stats = st;
     return DBL_OK;
 }
@@ -878,6 +912,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     if (!count) { if (stats) *stats = st; return DBL_OK; }
     if (!u || !v) { set_error("null argument"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     trace("insert: enter", g->stream);
     DevBuf in, keys, alt, newk, err;
@@ -979,6 +1014,7 @@ extern "C" dbl_status dbl_work_model(const dbl_index *idx, const dbl_graph *gc, 
     if (!V || !E || !levels) { set_error("null argument"); return DBL_E_ARG; }
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     return work_model(idx, g, V, E, levels);
 }
@@ -1057,6 +1093,7 @@ extern "C" dbl_status dbl_graph_add_edges(dbl_graph *g, const uint32_t *u, const
     if (out_inserted) *out_inserted = 0;
     if (!count) return DBL_OK;
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     DevBuf in, keys, alt, newk, err;
     auto cleanup = [&]() { in.release(); keys.release(); alt.release(); newk.release(); err.release(); };

@@ -434,6 +434,24 @@ __global__ void expand_rows_kernel(const uint32_t *__restrict__ ptr, const uint3
     }
 }
 
+dbl_status graph_flush_pending(dbl_graph *g) {
+    if (!g->n_pend) return DBL_OK;
+    const uint64_t np = g->n_pend;
+    set_stream(g->stream);
+    dbl_status s;
+    if ((s = g->pend_sort.ensure(2 * PEND_CAP * 8 + 64))) return s;
+    uint64_t *a = g->pend_sort.as<uint64_t>(), *b = a + PEND_CAP;
+    DBL_CUDA(cudaMemcpyAsync(a, g->pend.p, np * 8, cudaMemcpyDeviceToDevice, g->stream));
+    uint64_t *sorted = nullptr;
+    if ((s = sort_keys(g, a, b, np, 64, &sorted))) return s;
+    // logged keys are unique and absent from base + delta (insert_one_kernel
+    // checked both and the log itself before appending)
+    if ((s = graph_insert_delta(g, sorted, np))) return s;
+    g->n_pend = 0;
+    if (g->m_delta * 4 > g->m_base + 1024) return graph_compact(g);
+    return DBL_OK;
+}
+
 // Fold the delta adjacency into the base CSR/CSC.
 dbl_status graph_compact(dbl_graph *g) {
     if (g->m_delta == 0) return DBL_OK;
@@ -548,6 +566,8 @@ extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
     pool_forget_stream(g->stream);
     g->host_stage.release();
     g->q_host_res.release();
+    g->q_stage.release();
+    g->one_out.release();
     for (auto &ev : g->ev) if (ev) cudaEventDestroy(ev);
     if (g->ev_in) cudaEventDestroy(g->ev_in);
     if (g->stream) cudaStreamDestroy(g->stream);
@@ -558,13 +578,14 @@ extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
 extern "C" dbl_status dbl_graph_info(const dbl_graph *g, uint32_t *n, uint64_t *m) {
     if (!g) { set_error("null graph"); return DBL_E_ARG; }
     if (n) *n = g->n;
-    if (m) *m = g->m_base + g->m_delta;
+    if (m) *m = g->m_base + g->m_delta + g->n_pend;   // logged single inserts count (no flush needed)
     return DBL_OK;
 }
 
 extern "C" dbl_status dbl_graph_degrees(const dbl_graph *g, uint32_t *indeg, uint32_t *outdeg) {
     if (!g || !indeg || !outdeg) { set_error("null argument"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     dbl_graph *gm = const_cast<dbl_graph *>(g);
     dbl_status s = gm->scratch_a.ensure(((size_t)g->n + 1) * 8);
@@ -596,6 +617,7 @@ extern "C" dbl_status dbl_graph_has_edges(const dbl_graph *g, const uint32_t *u,
     if (!g || (count && (!u || !v || !out))) { set_error("null argument"); return DBL_E_ARG; }
     if (!count) return DBL_OK;
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     DevBuf b;
     dbl_status s = b.ensure(count * 9 + 16);
@@ -633,10 +655,11 @@ __global__ void split_keys_kernel(const uint64_t *__restrict__ keys, uint64_t m,
 
 extern "C" dbl_status dbl_graph_edges(const dbl_graph *g, uint32_t *src, uint32_t *dst) {
     if (!g) { set_error("null graph"); return DBL_E_ARG; }
+    DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     uint64_t mb = g->m_base, md = g->m_delta, m = mb + md;
     if (!m) return DBL_OK;
     if (!src || !dst) { set_error("null argument"); return DBL_E_ARG; }
-    DBL_CUDA(cudaSetDevice(g->device));
     set_stream(g->stream);
     dbl_graph *gm = const_cast<dbl_graph *>(g);
     DevBuf a, b;
@@ -717,6 +740,7 @@ __global__ void add_ptr_kernel(const uint32_t *__restrict__ a, const uint32_t *_
 extern "C" dbl_status dbl_graph_adjacency(const dbl_graph *g, int reverse, uint32_t *ptr, uint32_t *col) {
     if (!g || !ptr) { set_error("null argument"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     const uint64_t m = g->m_base + g->m_delta;
     Adj a = reverse ? graph_rev(g) : graph_fwd(g);

@@ -217,12 +217,18 @@ struct dbl_graph {
     unsigned int *reach_chg = nullptr;          // its step words: [3] capped, [4] steps, [5] sweeps
     dbl::BuildWork last_build{}, last_insert{};
     bool instrument = false;                    // builds count their executed work (dbl_graph_instrument)
+    // single-edge inserts not yet folded into the delta adjacency
+    // (insert_one.cu; graph_flush_pending folds them before any other use)
+    dbl::DevBuf pend, pend_sort;
+    uint32_t n_pend = 0;
+    dbl::HostBuf one_out;
     dbl::DevBuf changed_bits;
     // generic scratch
     dbl::DevBuf cub_tmp, scratch_a, scratch_b, scratch_c, scratch_d;
     dbl::DevBuf prep;                     // PrepState + top-k candidates
     dbl::HostBuf host_stage;
     dbl::HostBuf q_host_res;              // pinned result words of the last query batch
+    dbl::HostBuf q_stage;                 // pinned staging of small pageable query batches
     // query workspace
     dbl::DevBuf q_in, q_codes, q_vis, q_pending, q_counters, q_dense, q_errs;
     cudaStream_t cstream[2] = {nullptr, nullptr};   // H2D / D2H copy streams
@@ -290,6 +296,14 @@ dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, 
                             uint64_t *nout, const uint64_t **dcount = nullptr,
                             const uint64_t *valid_dev = nullptr, const unsigned long long *abort_dev = nullptr);
 dbl_status graph_compact(dbl_graph *g);
+// Fold the single-edge pending log into the delta adjacency (every entry
+// point that reads the adjacency or changes the graph calls this first).
+constexpr uint32_t PEND_CAP = 1024;
+dbl_status graph_flush_pending(dbl_graph *g);
+// insert_one.cu: single-edge insert in one launch (done = false: the caller
+// finishes with the batch fixpoint; the edge is already in the pending log)
+dbl_status insert_edge_fast(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, dbl_update_stats *st,
+                            bool *done, uint32_t *dirs_done);
 // select.cu
 dbl_status select_landmarks_dev(dbl_graph *g, uint32_t k, int strategy, uint32_t *dev_out);
 dbl_status select_leaves_dev(dbl_graph *g, uint64_t threshold, uint32_t k_prime, uint64_t seed,

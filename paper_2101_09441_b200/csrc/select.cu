@@ -561,6 +561,7 @@ extern "C" dbl_status dbl_select_landmarks(const dbl_graph *g, uint32_t k, int32
     if (k > g->n) { set_error("k exceeds vertex count"); return DBL_E_CONFIG; }
     if (!k) return DBL_OK;
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     dbl_graph *gm = const_cast<dbl_graph *>(g);
     DevBuf b;
@@ -618,6 +619,7 @@ extern "C" dbl_status dbl_select_leaves(const dbl_graph *g, uint64_t threshold, 
     uint32_t n = g->n;
     if (!n) return DBL_OK;
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     dbl_graph *gm = const_cast<dbl_graph *>(g);
     DevBuf ovr, outb;

@@ -114,6 +114,7 @@ extern "C" dbl_status dbl_verify(const dbl_index *idx, const dbl_graph *gc, int 
     }
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));
+    if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
     const uint32_t n = idx->n, H = idx->wdl + idx->wbl;
     if (H > (uint32_t)VMAXH) { set_error("label width too large for the verifier"); return DBL_E_CONFIG; }

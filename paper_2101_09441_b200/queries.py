@@ -11,7 +11,9 @@ parity contract).
 """
 from __future__ import annotations
 
+import ctypes
 import os
+import threading
 import time
 from dataclasses import dataclass
 from enum import Enum
@@ -126,9 +128,14 @@ class BatchStats:
     def collect(cls, outcomes, elapsed_ms: float) -> "BatchStats":
         if isinstance(outcomes, Outcomes):
             q = len(outcomes)
-            la = int(np.count_nonzero(outcomes.visited == 0))
+            c = outcomes.codes
+            # visited == 0 exactly for the label-answered codes 0..4, and the
+            # reachable codes are 0, 1, 5 (queries.py:50-56): counted on the
+            # u8 codes instead of materialising boolean arrays
+            la = int(np.count_nonzero(c < 5))
+            reach = int(np.count_nonzero(c <= 1)) + int(np.count_nonzero(c == 5))
             return cls(q, la, la / q if q else 0.0, int(outcomes.visited.sum(dtype=np.uint64)),
-                       int(np.count_nonzero(outcomes.reachable)), elapsed_ms)
+                       reach, elapsed_ms)
         label_answered = sum(1 for o in outcomes if o.visited == 0)
         return cls(len(outcomes), label_answered,
                    label_answered / len(outcomes) if outcomes else 0.0,
@@ -209,14 +216,26 @@ def query_codes(g, idx: DblIndex, u, v, flags: QueryFlags = DEFAULT_FLAGS,
     return codes, vis
 
 
+_ONE = threading.local()
+
+
 def query(g, idx: DblIndex, u: int, v: int, flags: QueryFlags = DEFAULT_FLAGS) -> QueryOutcome:
-    """Answer q(u, v) (queries.py:94-142)."""
+    """Answer q(u, v) (queries.py:94-142): one staged launch and one sync."""
     g = as_device_graph(g)
     _check_consistent(g, idx)
     g._check_vertex(u)
     g._check_vertex(v)
-    codes, vis = query_codes(g, idx, [u], [v], flags)
-    return Outcomes(codes, vis)[0]
+    buf = getattr(_ONE, "buf", None)
+    if buf is None:   # per-thread 1-query buffers (u, v, visited | code) and their addresses
+        arr = np.zeros(4, np.uint32)
+        code = np.zeros(8, np.uint8)
+        buf = _ONE.buf = (arr, code, N.ptr(arr[0:1]), N.ptr(arr[1:2]), N.ptr(code),
+                          ctypes.c_void_p(arr.ctypes.data + 8))
+    arr, code, pu, pv, pc, pvis = buf
+    arr[0], arr[1] = u, v
+    N.check(N.lib().dbl_query(idx.handle, g.handle, pu, pv, 1, flags.bits(), pc, pvis, N.MEM_HOST))
+    c = int(code[0])
+    return QueryOutcome(c in REACHABLE_CODES, ANSWER_ORDER[c], int(arr[2]))
 
 
 def query_batch(g, idx: DblIndex, queries: Iterable[tuple[int, int]], workers: int = 1,

@@ -72,8 +72,8 @@ def insert_edge(g, idx: DblIndex, u: int, v: int) -> UpdateStats:
     g._check_vertex(u)
     g._check_vertex(v)
     st = N.UpdateStatsC()
-    N.call("dbl_insert_edge", idx.handle, g.handle, u, v, ctypes.byref(st))
-    g._refresh_count()
+    N.check(N.lib().dbl_insert_edge(idx.handle, g.handle, u, v, ctypes.byref(st)))
+    g._m_dev += int(st.inserted)   # add_edge's return (the C side counts it the same way)
     g.version += 1
     idx._invalidate()
     return UpdateStats(int(st.visited), int(st.labels_changed), bool(st.early_terminated))

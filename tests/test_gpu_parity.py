@@ -642,3 +642,54 @@ def test_device_inputs_ordered_after_producer_stream():
         codes, _ = E.query_codes(g, idx, qu2, qv2)
         ref, _ = E.query_batch(g, idx, (qu2.cpu().numpy().view(np.uint32), qv2.cpu().numpy().view(np.uint32)))
         np.testing.assert_array_equal(codes.cpu().numpy(), ref.codes)
+
+
+# ------------------------------------------------- dl_intersec / bl_contain --
+
+def test_label_tests_kats(toy_golden):
+    """dl_intersec / bl_contain (labels.py:315-327) on the device against the
+    reference's answers for all pairs (tests/golden/label_tests.npz; the
+    reference's KATs tests/test_labels.py:166-191 are rows of the toy set)."""
+    from conftest import golden
+    from paper_2101_09441_b200.labels import _label_tests
+    d = golden("label_tests")
+    g, idx = toy_index(toy_golden)
+    dl, bl = _label_tests(idx, d["toy_x"], d["toy_y"])
+    np.testing.assert_array_equal(dl, d["toy_dl"].astype(bool))
+    np.testing.assert_array_equal(bl, d["toy_bl"].astype(bool))
+    assert E.dl_intersec(idx, 0, 9) is True          # (V1, V10)
+    assert E.dl_intersec(idx, 2, 10) is False        # (V3, V11): a miss, not a refutation
+    assert E.dl_intersec(idx, 2, 2) is False
+    assert E.bl_contain(idx, 3, 5) is False          # (V4, V6)
+    assert E.bl_contain(idx, 4, 1) is True           # (V5, V2)
+    assert all(E.bl_contain(idx, v, v) for v in range(11))
+    with pytest.raises(E.VertexRangeError):
+        E.dl_intersec(idx, 0, 11)
+    for name in ("r64", "r130", "dag"):
+        n = int(d[name + "_n"])
+        gg = E.DynamicGraph.from_edges(n, d[name + "_src"], d[name + "_dst"])
+        cfg = E.IndexConfig(k=int(d[name + "_k"]), k_prime=int(d[name + "_k_prime"]),
+                            leaf_threshold=int(d[name + "_threshold"]))
+        ix = E.build_index(gg, cfg)
+        assert_labels(ix, d, name + "_")
+        x, y = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+        dl, bl = _label_tests(ix, x.ravel(), y.ravel())
+        np.testing.assert_array_equal(dl, d[name + "_dl"].ravel().astype(bool), err_msg=name)
+        np.testing.assert_array_equal(bl, d[name + "_bl"].ravel().astype(bool), err_msg=name)
+
+
+@pytest.mark.parametrize("k,kp", [(64, 64), (256, 64), (100, 13)])
+def test_label_tests_random_pairs_vs_oracle(k, kp):
+    """10k random pairs on R-MAT 2^12 against the oracle formula on the oracle's words."""
+    n = 1 << 12
+    src, dst = W.rmat_edges(12, 8, seed=21)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    idx = E.build_index(g, E.IndexConfig(k=k, k_prime=kp))
+    oidx = O.OracleGraph(n, src, dst).build(k, kp, threads=2)
+    assert_labels_equal_oracle(idx, oidx)
+    from paper_2101_09441_b200.labels import _label_tests
+    x, y = W.uniform_queries(n, 10_000, seed=22)
+    dl, bl = _label_tests(idx, x, y)
+    odl, obl = O.label_tests({f: getattr(oidx, f) for f in FAMS}, x, y)
+    np.testing.assert_array_equal(dl, odl)
+    np.testing.assert_array_equal(bl, obl)

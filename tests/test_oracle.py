@@ -138,3 +138,36 @@ def test_reach_batch_matches_codes(cfg1_golden):
     reach = g.reach_batch(d["qu"][:20000], d["qv"][:20000], threads=4)
     exp = np.isin(d["codes"][:20000], (0, 1, 5))
     np.testing.assert_array_equal(reach, exp)
+
+
+def test_label_tests_kats():
+    """dl_intersec / bl_contain: the restated formula against the reference's
+    answers on all pairs (tests/golden/label_tests.npz), incl. the KATs of
+    the reference's tests/test_labels.py:166-191 (worked example)."""
+    from conftest import golden
+    d = golden("label_tests")
+    t = golden("toy")
+    lab = {f: t[f] for f in ("dl_in", "dl_out", "bl_in", "bl_out")}
+    dl, bl = O.label_tests(lab, d["toy_x"], d["toy_y"])
+    np.testing.assert_array_equal(dl, d["toy_dl"].astype(bool))
+    np.testing.assert_array_equal(bl, d["toy_bl"].astype(bool))
+    pair = {(int(a), int(b)): i for i, (a, b) in enumerate(zip(d["toy_x"], d["toy_y"]))}
+    V1, V2, V3, V4, V5, V6, V10, V11 = 0, 1, 2, 3, 4, 5, 9, 10
+    assert d["toy_dl"][pair[V1, V10]] == 1
+    assert d["toy_dl"][pair[V3, V11]] == 0
+    assert d["toy_dl"][pair[V3, V3]] == 0
+    assert d["toy_bl"][pair[V4, V6]] == 0
+    assert d["toy_bl"][pair[V5, V2]] == 1
+    assert all(d["toy_bl"][pair[v, v]] == 1 for v in range(11))
+    for name in ("r64", "r130", "dag"):
+        n = int(d[name + "_n"])
+        lab = {f: d[f"{name}_{f}"] for f in ("dl_in", "dl_out", "bl_in", "bl_out")}
+        x, y = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+        dl, bl = O.label_tests(lab, x.ravel(), y.ravel())
+        np.testing.assert_array_equal(dl, d[name + "_dl"].ravel().astype(bool), err_msg=name)
+        np.testing.assert_array_equal(bl, d[name + "_bl"].ravel().astype(bool), err_msg=name)
+        # the oracle's own build reproduces the reference labels of these graphs
+        og = O.OracleGraph(n, d[name + "_src"], d[name + "_dst"])
+        oidx = og.build(int(d[name + "_k"]), int(d[name + "_k_prime"]), leaf_threshold=int(d[name + "_threshold"]))
+        for f in ("dl_in", "dl_out", "bl_in", "bl_out"):
+            np.testing.assert_array_equal(getattr(oidx, f), lab[f], err_msg=f"{name} {f}")

@@ -107,7 +107,12 @@ def query_rate(g, idx, qu, qv, reps=5):
 
 
 def label_columns_check(g, idx, n_lm=8, n_bk=8, seed=0):
-    """Sampled bit columns vs CPU floods (labels.py:247-260) over exported adjacency."""
+    """Sampled bit columns vs CPU floods (labels.py:247-260) over exported adjacency.
+
+    Each column is one reference-style single-bit flood (oracle csr_flood);
+    the floods run on a thread pool (the C oracle releases the GIL).
+    """
+    from concurrent.futures import ThreadPoolExecutor
     w = idx.export_words()
     fptr, fcol = g.adjacency(False)
     rptr, rcol = g.adjacency(True)
@@ -115,26 +120,32 @@ def label_columns_check(g, idx, n_lm=8, n_bk=8, seed=0):
     n = g.vertex_count
     rng = np.random.default_rng(seed)
     lms = np.array(idx.landmark_set.landmarks)
-    checked = 0
-    for i in rng.choice(len(lms), min(n_lm, len(lms)), replace=False) if len(lms) else []:
-        fwd = O.csr_flood(n, fptr, fcol, [lms[i]])
-        bwd = O.csr_flood(n, rptr, rcol, [lms[i]])
-        col_in = (w["dl_in"][:, i // 64] >> np.uint64(i % 64)) & np.uint64(1)
-        col_out = (w["dl_out"][:, i // 64] >> np.uint64(i % 64)) & np.uint64(1)
-        assert np.array_equal(col_in.astype(bool), fwd), f"dl_in column {i}"
-        assert np.array_equal(col_out.astype(bool), bwd), f"dl_out column {i}"
-        checked += 2
+    jobs = []   # (family, bit, ptr, col, seeds)
+    for i in (rng.choice(len(lms), min(n_lm, len(lms)), replace=False) if len(lms) else []):
+        jobs.append(("dl_in", int(i), fptr, fcol, [lms[i]]))
+        jobs.append(("dl_out", int(i), rptr, rcol, [lms[i]]))
     flags, bucket = idx.leaf_sets.flags, idx.leaf_sets.bucket_array
     kp = idx.config.k_prime
     for b in rng.choice(kp, min(n_bk, kp), replace=False):
         for side, fam, ptr, col in ((1, "bl_in", fptr, fcol), (2, "bl_out", rptr, rcol)):
             seeds = np.flatnonzero((flags & side) != 0)
             seeds = seeds[bucket[seeds] == b].astype(np.uint32)
-            reach = O.csr_flood(n, ptr, col, seeds)
-            colv = (w[fam][:, b // 64] >> np.uint64(b % 64)) & np.uint64(1)
-            assert np.array_equal(colv.astype(bool), reach), f"{fam} column {b}"
-            checked += 1
-    return checked
+            jobs.append((fam, int(b), ptr, col, seeds))
+
+    def run(job):
+        fam, bit, ptr, col, seeds = job
+        reach = O.csr_flood(n, ptr, col, seeds)
+        colv = (w[fam][:, bit // 64] >> np.uint64(bit % 64)) & np.uint64(1)
+        return fam, bit, bool(np.array_equal(colv.astype(bool), reach))
+
+    with ThreadPoolExecutor(max(1, min(CORES, 16))) as ex:
+        res = list(ex.map(run, jobs))
+    bad = [(f, b) for f, b, ok in res if not ok]
+    assert not bad, f"label columns differ from the CPU floods: {bad[:5]}"
+    per = {}
+    for f, _, _ in res:
+        per[f] = per.get(f, 0) + 1
+    return {"columns": len(res), "per_family": per}
 
 
 def csr_codes_check(g, idx, qu, qv, codes):
@@ -267,7 +278,7 @@ def cfg5(scale=26, ef=16, nq=64_000_000):
     codes, qps, st = query_rate(g, idx, qu, qv, reps=3)
     rep = E.verify_labels(g, idx, exhaustive=False)
     assert rep.ok, rep.violations[:3]
-    cols = label_columns_check(g, idx, n_lm=4, n_bk=2, seed=5)
+    cols = label_columns_check(g, idx, n_lm=32, n_bk=32, seed=5)
     sample = rng.choice(nq, 200_000, replace=False)
     nchk = csr_codes_check(g, idx, qu[sample], qv[sample], codes[sample])
     return {"n": n, "m": g.edge_count, "k": 256, "k_prime": 64, "build_s": tb, "query_batch": nq,
@@ -278,7 +289,7 @@ def cfg5(scale=26, ef=16, nq=64_000_000):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", default="1,3,4,5")
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_configs.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_configs.json"))
     ap.add_argument("--scale3", type=int, default=22)
     ap.add_argument("--scale5", type=int, default=26)
     args = ap.parse_args()
