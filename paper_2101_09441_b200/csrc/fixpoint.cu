@@ -292,6 +292,7 @@ __device__ __forceinline__ void expand_range(const DirParams &D, uint32_t nitems
             if (ei < e1) {
                 ok[r] = true;
                 ys[r] = __ldg((od ? D.adj.dcol : D.adj.col) + os + (ei - oe));
+                DBL_DCHECK(ys[r] < D.adj.n);
             }
         }
         uint64_t cur[U][NW];
@@ -360,6 +361,7 @@ __device__ __forceinline__ void pull_range(const DirParams &D, const uint32_t *_
         for (int j = 0; j < NW; ++j) acc[j] = 0;
         if (ok) {
             const uint32_t p = __ldg(col + ei);
+            DBL_DCHECK(p < D.padj.n);
             if ((D.cur[p >> 5] >> (p & 31)) & 1) load_words<NW, VEC>(D.lab + (size_t)p * D.stride, acc, D.al);
         }
         // segmented inclusive OR-scan over lanes holding the same row
@@ -1005,12 +1007,14 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
         const uint32_t s0 = a.ptr[h], s1 = a.ptr[h + 1];
         for (uint64_t j = s0 + tid; j < s1; j += nth) {
             const uint32_t y = a.col[j];
+            DBL_DCHECK(y < P.n);
             atomicOr(&P.vis[d][y >> 5], 1u << (y & 31));
         }
         if (a.dptr) {
             const uint32_t t0 = a.dptr[h], t1 = a.dptr[h + 1];
             for (uint64_t j = t0 + tid; j < t1; j += nth) {
                 const uint32_t y = a.dcol[j];
+                DBL_DCHECK(y < P.n);
                 atomicOr(&P.vis[d][y >> 5], 1u << (y & 31));
             }
         }
@@ -1075,8 +1079,10 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
-                    for (int d = 0; d < 2; ++d)
+                    for (int d = 0; d < 2; ++d) {
                         c0[i][d] = (need[i][d] && s1[i][d] > s0[i][d]) ? __ldg(P.adj[d].col + s0[i][d]) : 0xffffffffu;
+                        DBL_DCHECK(c0[i][d] == 0xffffffffu || c0[i][d] < P.n);
+                    }
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -1141,6 +1147,7 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
                             if (WORK) w_tde += s1 - s0;
                             for (uint32_t j = s0; j < s1; ++j) {
                                 const uint32_t z = __ldg(col + j);
+                                DBL_DCHECK(z < P.n);
                                 const uint32_t bit = 1u << (z & 31);
                                 if (vis_test_ca(P.vis[d], z)) continue;
                                 if (!(atomicOr(&P.vis[d][z >> 5], bit) & bit)) {

@@ -198,6 +198,8 @@ Adj graph_fwd(const dbl_graph *g) {
     a.col = g->fcol.as<uint32_t>();
     a.dptr = g->m_delta ? g->dfptr.as<uint32_t>() : nullptr;
     a.dcol = g->m_delta ? g->dfcol.as<uint32_t>() : nullptr;
+    a.n = g->n;
+    a.pad = 0;
     return a;
 }
 
@@ -207,6 +209,8 @@ Adj graph_rev(const dbl_graph *g) {
     a.col = g->rcol.as<uint32_t>();
     a.dptr = g->m_delta ? g->drptr.as<uint32_t>() : nullptr;
     a.dcol = g->m_delta ? g->drcol.as<uint32_t>() : nullptr;
+    a.n = g->n;
+    a.pad = 0;
     return a;
 }
 

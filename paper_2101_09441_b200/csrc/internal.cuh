@@ -13,6 +13,26 @@
 #ifndef DBL_TRACE
 #define DBL_TRACE 0          // 1: host-side phase times to stderr (debug builds)
 #endif
+// Checked build (build.build_variant("checked", ["DBL_CHECKED=1"])): device
+// bounds checks on every adjacency column id, queue slot and record index
+// the kernels derive from data; a failure prints the site and traps, so the
+// next CUDA call of the test fails.  The substitute for compute-sanitizer
+// memcheck, which this pool does not run.
+#ifndef DBL_CHECKED
+#define DBL_CHECKED 0
+#endif
+#if DBL_CHECKED
+#include <cstdio>
+#define DBL_DCHECK(c)                                                                     \
+    do {                                                                                  \
+        if (!(c)) {                                                                       \
+            printf("DBL_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);              \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define DBL_DCHECK(c) ((void)0)
+#endif
 
 namespace dbl {
 
@@ -110,6 +130,8 @@ struct Adj {
     const uint32_t *col;
     const uint32_t *dptr;   // n+1 or nullptr
     const uint32_t *dcol;
+    uint32_t n;             // vertex count (bounds of every column id; DBL_DCHECK)
+    uint32_t pad;
 };
 
 // Executed work of the last build on a graph (dbl_build_work_stats).

@@ -316,6 +316,7 @@ bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_
                 atomicOr(&T.vis[sl], 1ull << tid);
                 if (atomicOr(&T.fr[0][sl], 1ull << tid) == 0) {
                     const uint32_t p = atomicAdd(&S.nlist[0], 1u);
+                    DBL_DCHECK(p < T.cap);
                     T.list[0][p] = (uint32_t)sl;
                 }
             }
@@ -359,6 +360,7 @@ bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_
                         const uint32_t ei = e0 + lane;
                         if (ei < s1) {
                             const uint32_t x = __ldg(col + ei);
+                            DBL_DCHECK(x < adj.n);
                             const unsigned long long hit = fw & tgt_lookup(S, x);
                             if (hit) atomicOr(&S.done, hit);
                             unsigned long long cand =
@@ -394,6 +396,7 @@ bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_
                                         const unsigned long long nx = nw & ~pruned;
                                         if (nx && atomicOr(&T.fr[nxt][sl], nx) == 0) {
                                             const uint32_t p = atomicAdd(&S.nlist[nxt], 1u);
+                                            DBL_DCHECK(p < T.cap);
                                             T.list[nxt][p] = (uint32_t)sl;
                                         }
                                     }
@@ -603,6 +606,7 @@ __device__ void warp_bfs(WarpBfs<WDL, WBL> &B, uint32_t nb, const uint64_t *__re
                 if (t >= total) continue;
                 const uint32_t r = t - oex;
                 const uint32_t x = r < obl ? __ldg(adj.col + ob0 + r) : __ldg(adj.dcol + od0 + (r - obl));
+                DBL_DCHECK(x < adj.n);
                 const uint32_t hit = ofw & wb_target(B, x);
                 if (hit) atomicOr(&B.done, hit);
                 uint32_t cand = ofw & ~hit & ~*(volatile uint32_t *)&B.done;
@@ -637,6 +641,7 @@ __device__ void warp_bfs(WarpBfs<WDL, WBL> &B, uint32_t nb, const uint64_t *__re
                 const uint32_t nx = nw & ~pruned;
                 if (nx && atomicOr(&B.hfr[nxt][sl], nx) == 0) {
                     const uint32_t p = atomicAdd(&B.nlist[nxt], 1u);
+                    DBL_DCHECK(p < (uint32_t)WH);
                     B.hlist[nxt][p] = (uint16_t)sl;
                 }
             }
@@ -990,6 +995,8 @@ __device__ __forceinline__ int thread_bfs(const uint64_t *__restrict__ rec, cons
 #pragma unroll
                 for (int t = 0; t < NB; ++t) x[t] = j0 + t < s1 ? __ldg(col + j0 + t) : 0xffffffffu;
 #pragma unroll
+                for (int t = 0; t < NB; ++t) DBL_DCHECK(x[t] == 0xffffffffu || x[t] < adj.n);
+#pragma unroll
                 for (int t = 0; t < NB; ++t)
                     if (x[t] == v) return 1;     // target test precedes the visited test
                 bool fresh[NB];
@@ -1070,6 +1077,7 @@ __device__ __forceinline__ int warp_query_bfs(const uint64_t *__restrict__ rec, 
                 const uint32_t j = j0 + lane;
                 const bool ok = j < s1;
                 const uint32_t x = ok ? __ldg(col + j) : 0xffffffffu;
+                DBL_DCHECK(!ok || x < adj.n);
                 if (__any_sync(FULL, ok && x == v)) return 1;   // target test precedes the visited test
                 bool keep = ok;
                 for (uint32_t k = 0; k < qn; ++k) keep &= wq[k] != x;
@@ -1230,8 +1238,11 @@ __global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_W
                                                    prune_dl, prune_bl, Pivot{}, wq[wid], &vc);
             if (lane == 0) {
                 if (r == 2) {
-                    pending[atomicAdd(&counters[CNT_PENDING], 1u)] = i;
+                    const uint32_t pp = atomicAdd(&counters[CNT_PENDING], 1u);
+                    DBL_DCHECK(pp < count && i < count);
+                    pending[pp] = i;
                 } else {
+                    DBL_DCHECK(i < count);
                     qd.codes[i] = r ? DBL_BFS_POSITIVE : DBL_BFS_NEGATIVE;
                     if (qd.visited) qd.visited[i] = vc;
                 }
