@@ -211,7 +211,10 @@ dbl_status dbl_query(const dbl_index *idx, const dbl_graph *g, const uint32_t *u
                      const uint32_t *v, uint64_t count, uint32_t flags, uint8_t *codes,
                      uint32_t *visited, dbl_mem mem);
 /* Same as dbl_query but enqueued on the handle's stream without a final
- * synchronisation (device memory only); dbl_sync waits for it.  A batch
+ * synchronisation (device memory only); dbl_sync waits for it.  Unlike the
+ * synchronous calls it does not order itself after the legacy default
+ * stream: produce u / v on the handle's stream (dbl_stream) or synchronise
+ * their producer first.  A batch
  * whose pruned BFS outgrows the shared-memory tables needs the dense
  * workspace (n x 32 bytes per CTA), which is allocated on first need: such a
  * batch is completed by dbl_sync (it re-runs the batch), so call dbl_sync
@@ -304,11 +307,14 @@ typedef struct {
 } dbl_build_work;
 dbl_status dbl_build_work_stats(const dbl_graph *g, dbl_build_work *out);
 /* on != 0: later builds on g run the instrumented pivot kernel, which also
- * fills the pivot fields of the dbl_build_work struct; the product kernel carries no
- * counters, so without instrumentation those fields stay 0. */
+ * fills the pivot fields of the dbl_build_work struct (the product kernel
+ * carries no counters, so without instrumentation those fields stay 0), and
+ * query batches record CUDA events around their kernels for
+ * dbl_last_timings (two extra event records per batch on the stream). */
 dbl_status dbl_graph_instrument(dbl_graph *g, int on);
-/* Device time (ms) of the last fixpoint launch and of the last query
- * label-check kernel, measured with CUDA events on the handle's stream. */
+/* Device time (ms) of the last fixpoint launch and (instrumented graphs
+ * only, else 0) of the last query batch's kernels, measured with CUDA
+ * events on the handle's stream. */
 dbl_status dbl_last_timings(const dbl_graph *g, float *fixpoint_ms, float *label_ms,
                             float *bfs_ms);
 

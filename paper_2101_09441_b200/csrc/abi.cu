@@ -759,7 +759,9 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
                            (uint8_t *)dptr[2], (uint32_t *)dptr[3], sync)))
             return s;
     } else {
-        if (count && (s = order_after_caller(g))) return s;
+        // the synchronous call orders itself after the caller's default-stream
+        // work; dbl_query_async is stream-ordered only (dbl_b200.h)
+        if (count && sync && (s = order_after_caller(g))) return s;
         if ((s = run_query(idx, g, u, v, count, flags, codes, visited, sync))) return s;
     }
     if (!sync) return DBL_OK;

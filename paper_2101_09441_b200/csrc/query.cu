@@ -936,24 +936,18 @@ query_quad_kernel(const uint64_t *__restrict__ rec, uint32_t n, Adj adj, const Q
 // ~4k record sectors in flight (measured: a one-query-per-thread gather beats
 // persistent multi-query tiles by ~30% on 1M queries).
 //
-// K7 is launched right behind it with programmatic dependent launch: its
-// CTAs are scheduled as K6's retire and wait (griddepcontrol.wait) for K6's
-// results, then every warp takes an equal share of the pending queries in
-// groups of <= 32 and runs the bit-parallel pruned BFS of warp_bfs on them.
-// Batches whose BFS outgrows the warp table are handed, by the last CTA, to
-// the 64-query group kernel and the dense kernel (device tail launches).
-// Pruned BFS of one query by one thread (queries.py:116-142) for the common
-// tiny case: at most TB_Q expanded vertices with at most TB_E edges each
-// (on R-MAT the fallback visits <= 3 vertices).  Returns 1 if v is reached,
-// 0 if the search is exhausted, 2 if it outgrew those bounds (the query is
-// then handed to the warp BFS).  The answer equals the reference's: pruning
-// only removes vertices that cannot reach v (a pruned x reaching v would give
-// dl_out[u] & dl_in[v] != 0 or violate BL containment), so v is found iff
-// it is reachable, in any visiting order.
+// K7a: the queries the label rules leave open (0.5% on R-MAT) are queued per
+// CTA and answered by warp_query_bfs -- a pruned BFS of one query by one
+// warp, bounded to TB_Q expanded vertices (on R-MAT the fallback visits <= 3)
+// -- on a dedicated BFS warp while the other warps still gather.  A query
+// that outgrows the bounds goes to the pending list, which the last CTA
+// hands to the tail-launched warp kernel (K7b: bit-parallel BFS of <= 32
+// queries per warp), and beyond that to the 64-query group and dense kernels.
+// The answer equals the reference's: pruning only removes vertices that
+// cannot reach v (a pruned x reaching v would give dl_out[u] & dl_in[v] != 0
+// or violate BL containment), so v is found iff it is reachable, in any
+// visiting order.
 constexpr int TB_Q = 8;
-#ifndef DBL_WBFS
-#define DBL_WBFS 1
-#endif
 constexpr uint32_t DQ_CAP = 128;   // deferred queries per CTA (more go to the warp BFS)
 // A deferred query: its index, endpoints and the words its pruning needs
 // (dl_out[u], bl_in[v], bl_out[v]; queries.py:137-140).
@@ -962,95 +956,18 @@ struct DeferQ {
     static constexpr int WD = WDL > 0 ? WDL : 1;
     uint64_t dlo[DQ_CAP][WD], bli[DQ_CAP][WBL], blo[DQ_CAP][WBL];
     uint32_t i[DQ_CAP], u[DQ_CAP], v[DQ_CAP];
-    uint32_t n;
+    uint32_t n;             // slots claimed (may exceed DQ_CAP: the rest go to the pending list)
 };
 #ifndef DBL_LMINB
 #define DBL_LMINB 8
 #endif
-constexpr uint32_t TB_E = 48;
-
-template <int WDL, int WBL>
-__device__ __forceinline__ int thread_bfs(const uint64_t *__restrict__ rec, const Adj adj, uint32_t u, uint32_t v,
-                                       const uint64_t *dlo_u, const uint64_t *bli_v, const uint64_t *blo_v,
-                                       bool prune_dl, bool prune_bl, const Pivot &pv, uint32_t *vcount) {
-    const bool sq = pivot_query(pv, reinterpret_cast<const unsigned long long *>(dlo_u), WDL, prune_dl);
-    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H);
-    // neighbours in flight per step: their pruning words (dl_in, bl_in,
-    // bl_out of x) are loaded word by word, fewer at a time for wide labels
-    constexpr int NB = (WDL + 2 * WBL) <= 3 ? 4 : 2;
-    uint32_t q[TB_Q];
-    q[0] = u;
-    int qn = 1;
-    for (int head = 0; head < qn; ++head) {
-        const uint32_t w = q[head];
-        *vcount = head + 1;
-        for (int seg = 0; seg < 2; ++seg) {
-            const uint32_t *ptr = seg ? adj.dptr : adj.ptr;
-            if (!ptr) break;
-            const uint32_t *col = seg ? adj.dcol : adj.col;
-            const uint32_t s0 = __ldg(ptr + w), s1 = __ldg(ptr + w + 1);
-            if (s1 - s0 > TB_E) return 2;
-            for (uint32_t j0 = s0; j0 < s1; j0 += NB) {
-                uint32_t x[NB];
-#pragma unroll
-                for (int t = 0; t < NB; ++t) x[t] = j0 + t < s1 ? __ldg(col + j0 + t) : 0xffffffffu;
-#pragma unroll
-                for (int t = 0; t < NB; ++t) DBL_DCHECK(x[t] == 0xffffffffu || x[t] < adj.n);
-#pragma unroll
-                for (int t = 0; t < NB; ++t)
-                    if (x[t] == v) return 1;     // target test precedes the visited test
-                bool fresh[NB];
-#pragma unroll
-                for (int t = 0; t < NB; ++t) {
-                    fresh[t] = x[t] != 0xffffffffu;
-                    for (int k = 0; k < qn; ++k) fresh[t] &= q[k] != x[t];
-                    if (fresh[t] && sq && in_pivot(pv, x[t])) fresh[t] = false;   // pruned
-                }
-                uint64_t xi[NB][WDL > 0 ? WDL : 1], xbi[NB][WBL], xbo[NB][WBL];
-#pragma unroll
-                for (int t = 0; t < NB; ++t) {
-                    if (!fresh[t]) continue;
-                    const uint64_t *rx = rec + (size_t)x[t] * RS;
-                    if (prune_dl) {
-#pragma unroll
-                        for (int k = 0; k < WDL; ++k) xi[t][k] = __ldg(rx + k);
-                    }
-                    if (prune_bl) {
-#pragma unroll
-                        for (int k = 0; k < WBL; ++k) {
-                            xbi[t][k] = __ldg(rx + WDL + k);
-                            xbo[t][k] = __ldg(rx + H + WDL + k);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int t = 0; t < NB; ++t) {
-                    if (!fresh[t]) continue;
-                    bool p = false;
-                    if (prune_dl) {   // queries.py:137-138
-#pragma unroll
-                        for (int k = 0; k < WDL; ++k) p |= (dlo_u[k] & xi[t][k]) != 0;
-                    }
-                    if (prune_bl && !p) {   // queries.py:139-140
-#pragma unroll
-                        for (int k = 0; k < WBL; ++k) p |= ((xbi[t][k] & ~bli_v[k]) | (blo_v[k] & ~xbo[t][k])) != 0;
-                    }
-                    if (p) continue;
-                    if (qn == TB_Q) return 2;
-                    q[qn++] = x[t];
-                }
-            }
-        }
-    }
-    return 0;
-}
 
 // The same bounded pruned BFS with the 32 lanes of a warp on one query: a
 // frontier vertex's adjacency is read 32 neighbours at a time and their
 // pruning words are gathered in parallel, so a level costs about two memory
 // round trips instead of one per 4 neighbours.  The expanded/visited list
-// (<= TB_Q) lives in the warp's slot of `wq`.  Warp-uniform result as in
-// thread_bfs; TB_EW bounds the neighbours of one expanded vertex.
+// (<= TB_Q) lives in the warp's slot of `wq`.  Warp-uniform result; TB_EW
+// bounds the neighbours of one expanded vertex.
 constexpr uint32_t TB_EW = 256;
 
 template <int WDL, int WBL>
@@ -1131,22 +1048,26 @@ __global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_W
 #ifndef DBL_TBFS_ALL
 #define DBL_TBFS_ALL 0
 #endif
+#ifndef DBL_EXP_NOBFS
+#define DBL_EXP_NOBFS 0   // experiment builds only: skip the deferred BFS (answers incomplete)
+#endif
     constexpr bool TBFS = DBL_TBFS_ALL || WDL <= 1;
     const uint32_t flags = qd.flags, count = qd.count;
     const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
     const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
     const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
-    const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t cr = (count + 31) & ~31u;
     const int lane = threadIdx.x & 31;
     // Unresolved queries are deferred to a per-CTA queue (their BFS inputs
     // staged in shared memory, the source's row pointer prefetched into L2),
-    // so a BFS never stalls the gathers; after the label checks each thread
-    // of the CTA takes one queued query, so the CTA pays about one BFS chain
-    // however its unresolved queries fell on its warps.
+    // so a BFS never stalls the gathers (measured alternatives, DESIGN.md §4:
+    // a dedicated BFS warp per CTA overlapping the gathers, 25.8 vs 23.1 us
+    // -- the gathers lose a warp's worth of requests in flight).
+    const int wid = threadIdx.x >> 5;
     __shared__ DeferQ<WDL, WBL> dq;
     if (threadIdx.x == 0) dq.n = 0;
     __syncthreads();
+    const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
 #ifndef DBL_QPF
 #define DBL_QPF 1
@@ -1221,17 +1142,12 @@ __global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_W
             if (unres) pending[base + __popc(m & ((1u << lane) - 1u))] = i;
         }
     }
-    if constexpr (TBFS) {
+    if constexpr (TBFS && !DBL_EXP_NOBFS) {
         // (the pivot prune is left out here: these BFS expand <= 3 vertices
         // on R-MAT, and its bitmap test adds a dependent load before each
         // record read -- measured 24.2 vs 23.1 us per 1M batch on cfg2)
-        __syncthreads();
-        const uint32_t nq = min(dq.n, DQ_CAP);
-#if DBL_WBFS
-        // one warp per queued query, neighbours in parallel
         __shared__ uint32_t wq[256 / 32][TB_Q];
-        const int wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
-        for (uint32_t t = wid; t < nq; t += nwb) {
+        auto answer = [&](uint32_t t) {   // one warp per queued query, neighbours in parallel
             const uint32_t i = dq.i[t];
             uint32_t vc = 0;
             const int r = warp_query_bfs<WDL, WBL>(rec, adj, dq.u[t], dq.v[t], dq.dlo[t], dq.bli[t], dq.blo[t],
@@ -1248,21 +1164,13 @@ __global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_W
                 }
             }
             __syncwarp();
-        }
-#else
-        for (uint32_t t = threadIdx.x; t < nq; t += blockDim.x) {
-            const uint32_t i = dq.i[t];
-            uint32_t vc = 0;
-            const int r = thread_bfs<WDL, WBL>(rec, adj, dq.u[t], dq.v[t], dq.dlo[t], dq.bli[t], dq.blo[t], prune_dl,
-                                               prune_bl, Pivot{}, &vc);
-            if (r == 2) {
-                pending[atomicAdd(&counters[CNT_PENDING], 1u)] = i;
-            } else {
-                qd.codes[i] = r ? DBL_BFS_POSITIVE : DBL_BFS_NEGATIVE;
-                if (qd.visited) qd.visited[i] = vc;
-            }
-        }
-#endif
+        };
+        // after the label checks every warp of the CTA takes queued queries,
+        // so the CTA pays about one BFS chain however they fell on its warps
+        __syncthreads();
+        const uint32_t nq = min(dq.n, DQ_CAP);
+        const int nwb = blockDim.x >> 5;
+        for (uint32_t t = wid; t < nq; t += nwb) answer(t);
     }
     // the last CTA out closes the batch, or tail-launches the warp BFS for the
     // queries the thread BFS could not finish
@@ -1482,10 +1390,10 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
                           hp.ws, g->sm_count * wbps, (uint32_t)wsmem, wovf};
         uint32_t lgrid = (uint32_t)((count + 255) / 256);
         if (lgrid > (uint32_t)(g->sm_count * lbps)) lgrid = (uint32_t)(g->sm_count * lbps);
-        DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
+        if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
         lean<<<lgrid, 256, 0, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);
         DBL_CHECK_LAUNCH("label_lean_kernel");
-        DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
+        if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
         g->q_timed_bfs = false;
         return DBL_OK;
     }
@@ -1495,16 +1403,16 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
         int fbps = 1;
         if ((s = kernel_occupancy((const void *)quad, FUSED_THREADS, fsmem, &fbps))) return s;
         const HardArgs ha{hp.grid, hp.dctas, (uint32_t)hp.smem, (uint32_t)hp.dsmem, idx->wdl, idx->wbl, ovf, hp.ws};
-        DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
+        if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
         quad<<<g->sm_count * fbps, FUSED_THREADS, fsmem, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);
         DBL_CHECK_LAUNCH("query_quad_kernel");
-        DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
+        if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
         g->q_timed_bfs = false;
         return DBL_OK;
     }
     // generic widths (k > 256 or k' > 128): label kernel, then the group and
     // dense kernels, then the counter close
-    DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
+    if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
     if (count) {
         int blocks = (int)((count + 255) / 256);
         if (blocks > g->sm_count * 16) blocks = g->sm_count * 16;
@@ -1512,7 +1420,7 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
                                                            codes, visited, pending, counters);
         DBL_CHECK_LAUNCH("label_check_generic");
     }
-    DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
+    if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
     if (count) {
         bfs_kernel<false><<<hp.grid, BFS_THREADS, hp.smem, g->stream>>>(rec, idx->wdl, idx->wbl, idx->n, adj, qd,
                                                                         pending, counters, ovf, nullptr);
@@ -1525,7 +1433,7 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     }
     finish_batch_kernel<<<1, 32, 0, g->stream>>>(counters, qd.hres);
     DBL_CHECK_LAUNCH("finish_batch_kernel");
-    DBL_CUDA(cudaEventRecord(g->ev[4], g->stream));
+    if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[4], g->stream));
     g->q_timed_bfs = true;
     return DBL_OK;
 }
@@ -1544,6 +1452,8 @@ bool chunk_needs_dense(const uint32_t *w4) { return w4[CNT_OVERFLOW - CNT_ERR] !
 // Event times of the last batch: the gather kernel's span (incl. any
 // tail-launched hard path) as "label", the separate BFS kernels as "bfs".
 void query_timings(dbl_graph *g) {
+    g->t_label = g->t_bfs = 0;
+    if (!g->instrument) return;   // per-launch events only on instrumented graphs
     cudaEventElapsedTime(&g->t_label, g->ev[2], g->ev[3]);
     g->t_bfs = 0;
     if (g->q_timed_bfs) cudaEventElapsedTime(&g->t_bfs, g->ev[3], g->ev[4]);

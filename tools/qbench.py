@@ -29,10 +29,14 @@ def main():
     ap.add_argument("--scale", type=int, default=20)
     ap.add_argument("--reps", type=int, default=30)
     ap.add_argument("--batch", type=int, default=1_000_000)
+    ap.add_argument("--novis", action="store_true", help="codes only (visited = NULL)")
+    ap.add_argument("--plain", action="store_true", help="no per-launch library events (as bench.py times)")
     a = ap.parse_args()
     n = 1 << a.scale
     src, dst = W.rmat_edges(a.scale, 8, seed=1)
     g = E.DynamicGraph.from_edges(n, src, dst)
+    if not a.plain:
+        N.call("dbl_graph_instrument", g.handle, 1)   # per-launch events for label_us
     sp = N.ctypes.c_void_p()
     N.call("dbl_stream", g.handle, N.ctypes.byref(sp))
     stream = torch.cuda.ExternalStream(sp.value)
@@ -68,7 +72,7 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             N.call("dbl_query_async", idx.handle, g.handle, N.ptr(qu), N.ptr(qv), a.batch, flags,
-                   N.ptr(codes), N.ptr(vis))
+                   N.ptr(codes), None if a.novis else N.ptr(vis))
             e1.record(stream)
             e1.synchronize()
             N.call("dbl_last_timings", g.handle, None, N.ctypes.byref(tl), N.ctypes.byref(tb))
