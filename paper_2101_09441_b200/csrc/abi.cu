@@ -709,7 +709,7 @@ static dbl_status query_host_staged(const dbl_index *idx, dbl_graph *g, const ui
     uint8_t *sc = reinterpret_cast<uint8_t *>(svis + cpad);
     std::memcpy(su, u, count * 4);
     std::memcpy(sv, v, count * 4);
-    if ((s = run_query(idx, g, su, sv, count, flags, sc, visited ? svis : nullptr, true))) return s;
+    if ((s = run_query(idx, g, su, sv, count, flags, sc, visited ? svis : nullptr, true, true))) return s;
     uint32_t err = 0;
     bool dense = false;
     if ((s = query_finish(g, &err, &dense))) return s;
@@ -756,7 +756,7 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
             return count <= STAGE_MAX ? query_host_staged(idx, g, u, v, count, flags, codes, visited)
                                       : query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
         if ((s = run_query(idx, g, (const uint32_t *)dptr[0], (const uint32_t *)dptr[1], count, flags,
-                           (uint8_t *)dptr[2], (uint32_t *)dptr[3], sync)))
+                           (uint8_t *)dptr[2], (uint32_t *)dptr[3], sync, true)))
             return s;
     } else {
         // the synchronous call orders itself after the caller's default-stream

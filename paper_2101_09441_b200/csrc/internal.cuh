@@ -357,8 +357,10 @@ dbl_status work_model(const dbl_index *idx, dbl_graph *g, uint64_t *V, uint64_t 
 void query_timings(dbl_graph *g);
 // host_result: the closing CTA also writes the result words into the pinned
 // g->q_host_res (synchronous calls read them there after the stream sync)
+// host_inputs: u / v are pinned host memory read over PCIe (zero-copy)
 dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
-                     uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, bool host_result = false);
+                     uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, bool host_result = false,
+                     bool host_inputs = false);
 dbl_status ensure_dense(const dbl_index *idx, dbl_graph *g);
 dbl_status query_finish(dbl_graph *g, uint32_t *err_out, bool *dense_out);
 dbl_status query_err_to(dbl_graph *g, uint32_t *dst4);

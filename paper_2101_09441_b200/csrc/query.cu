@@ -723,7 +723,8 @@ __device__ __forceinline__ void close_batch(uint32_t *counters, uint32_t *hres) 
         if (hres) hres[i] = c;
         counters[i] = 0;
     }
-    if (hres) __threadfence_system();
+    // (no system fence: the host reads hres only after the stream sync, and
+    // kernel completion makes the pinned writes visible)
 }
 
 __global__ void finish_batch_kernel(uint32_t *__restrict__ counters, uint32_t *hres) {
@@ -1031,32 +1032,104 @@ __global__ void bfs_warp_kernel(const uint64_t *__restrict__ rec, uint32_t n, Ad
                                 uint32_t *__restrict__ pending, uint32_t *__restrict__ wovf,
                                 uint32_t *__restrict__ counters, const HardArgs ha);
 
-template <int WDL, int WBL>
 #ifndef DBL_LMINB_WIDE
 #define DBL_LMINB_WIDE 4
 #endif
-// 8 CTAs/SM (32 registers) for the 32-byte records of k <= 64; wide records
-// (2 x 80 bytes at k = 256) spill at that cap, so they trade occupancy for
-// registers
-__global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_WIDE)) label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj,
-                                                          const QueryDesc qd, uint32_t *__restrict__ pending,
-                                                          uint32_t *__restrict__ counters, const HardArgs ha) {
-    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H);
-    // the per-thread BFS pays off for k <= 64; with wider labels (cfg5:
-    // k = 256, d = 16) most fallbacks outgrow its bounds (measured: 79% of
-    // cfg5's unresolved queries), so they go straight to the warp BFS
 #ifndef DBL_TBFS_ALL
 #define DBL_TBFS_ALL 0
 #endif
 #ifndef DBL_EXP_NOBFS
 #define DBL_EXP_NOBFS 0   // experiment builds only: skip the deferred BFS (answers incomplete)
 #endif
+constexpr uint8_t QUEUED = 0xfc;   // in the CTA's BFS queue (code written later)
+#ifndef DBL_QPT_HOST
+#define DBL_QPT_HOST 4   // pairs per thread per step when they are read over PCIe (4 or 8)
+#endif
+
+// Rules 0-4 for pair i = (u, v) (queries.py:94-114).  Returns the code, or
+// QUEUED if the query went to the CTA's BFS queue, or UNRESOLVED if it is
+// open and the queue is full (the caller appends it to the pending list).
+template <int WDL, int WBL, bool TBFS>
+__device__ __forceinline__ uint8_t lean_eval(const uint64_t *__restrict__ rec, uint32_t n, const Adj &adj, uint32_t i,
+                                             uint32_t u, uint32_t v, bool use_dl, bool use_bl, bool thm1, bool thm2,
+                                             DeferQ<WDL, WBL> &dq, uint32_t *__restrict__ counters) {
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H);
+    if (u >= n || v >= n) {
+        atomicOr(&counters[CNT_ERR], 1u);
+        return 0xfe;
+    }
+    if (u == v) return DBL_REFLEXIVE;
+    uint64_t a[RW], b[RW];
+    load_record<RW, RS>(rec + (size_t)u * RS, a);
+    load_record<RW, RS>(rec + (size_t)v * RS, b);
+    uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
+#pragma unroll
+    for (int k = 0; k < WDL; ++k) {
+        r1 |= a[H + k] & b[k];             // dl_out[u] & dl_in[v]
+        r3 |= b[H + k] & a[k];             // dl_out[v] & dl_in[u]
+        r4 |= (a[H + k] & a[k]) | (b[H + k] & b[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < WBL; ++k)
+        r2 |= (a[WDL + k] & ~b[WDL + k]) | (b[H + WDL + k] & ~a[H + WDL + k]);
+    if (use_dl && r1) return DBL_DL_POSITIVE;
+    if (use_bl && r2) return DBL_BL_NEGATIVE;
+    if (thm1 && r3) return DBL_THM1_NEGATIVE;
+    if (thm2 && r4) return DBL_THM2_NEGATIVE;
+    if (TBFS) {
+        const uint32_t slot = atomicAdd(&dq.n, 1u);
+        if (slot < DQ_CAP) {
+            dq.i[slot] = i;
+            dq.u[slot] = u;
+            dq.v[slot] = v;
+#pragma unroll
+            for (int k = 0; k < WDL; ++k) dq.dlo[slot][k] = a[H + k];   // still in registers
+#pragma unroll
+            for (int k = 0; k < WBL; ++k) {
+                dq.bli[slot][k] = b[WDL + k];
+                dq.blo[slot][k] = b[H + WDL + k];
+            }
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(adj.ptr + u));
+            return QUEUED;
+        }
+    }
+    return UNRESOLVED;
+}
+
+// Open queries of one warp step (unres lanes) go to the global pending list
+// with one warp-aggregated atomic.
+__device__ __forceinline__ void lean_pend(bool unres, uint32_t i, uint32_t *__restrict__ pending,
+                                          uint32_t *__restrict__ counters) {
+    const int lane = threadIdx.x & 31;
+    const unsigned m = __ballot_sync(FULL, unres);
+    if (m) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&counters[CNT_PENDING], (uint32_t)__popc(m));
+        base = __shfl_sync(FULL, base, 0);
+        if (unres) pending[base + __popc(m & ((1u << lane) - 1u))] = i;
+    }
+}
+
+// QPT = 1: device-resident pairs, one query per thread per step.
+// QPT = 4: pairs read from pinned host memory over PCIe (zero-copy): a
+// thread takes 4 consecutive pairs with one 16-byte load of u and of v, so a
+// warp instruction asks PCIe for 512 contiguous bytes instead of 128, and
+// writes their 4 codes with one store; PCIe, not the gather, bounds it.
+// 8 CTAs/SM (32 registers) for the 32-byte records of k <= 64; wide records
+// (2 x 80 bytes at k = 256) spill at that cap, so they trade occupancy for
+// registers
+template <int WDL, int WBL, int QPT>
+__global__ void __launch_bounds__(256, (QPT > 1 ? 4 : (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_WIDE)))
+label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj, const QueryDesc qd,
+                  uint32_t *__restrict__ pending, uint32_t *__restrict__ counters, const HardArgs ha) {
+    // the per-thread BFS pays off for k <= 64; with wider labels (cfg5:
+    // k = 256, d = 16) most fallbacks outgrow its bounds (measured: 79% of
+    // cfg5's unresolved queries), so they go straight to the warp BFS
     constexpr bool TBFS = DBL_TBFS_ALL || WDL <= 1;
     const uint32_t flags = qd.flags, count = qd.count;
     const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
     const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
     const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
-    const uint32_t cr = (count + 31) & ~31u;
     const int lane = threadIdx.x & 31;
     // Unresolved queries are deferred to a per-CTA queue (their BFS inputs
     // staged in shared memory, the source's row pointer prefetched into L2),
@@ -1069,77 +1142,86 @@ __global__ void __launch_bounds__(256, (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_W
     __syncthreads();
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
-#ifndef DBL_QPF
-#define DBL_QPF 1
-#endif
-    // the next iteration's pair is loaded while this one's records are in
-    // flight (one dependent round trip per iteration instead of two)
-    uint32_t nu = 0, nv = 0;
-    if (DBL_QPF && i0 < count) { nu = __ldg(qd.u + i0); nv = __ldg(qd.v + i0); }
-    for (uint32_t i = i0; i < cr; i += stride) {
-        bool unres = false;
-        uint32_t cu = nu, cv = nv;
-        if (DBL_QPF) {
+    if constexpr (QPT == 1) {
+        const uint32_t cr = (count + 31) & ~31u;
+        // the next iteration's pair is loaded while this one's records are in
+        // flight (one dependent round trip per iteration instead of two)
+        uint32_t nu = 0, nv = 0;
+        if (i0 < count) { nu = __ldg(qd.u + i0); nv = __ldg(qd.v + i0); }
+        for (uint32_t i = i0; i < cr; i += stride) {
+            bool unres = false;
+            const uint32_t u = nu, v = nv;
             const uint32_t inext = i + stride;
             if (inext < count) { nu = __ldg(qd.u + inext); nv = __ldg(qd.v + inext); }
-        }
-        if (i < count) {
-            const uint32_t u = DBL_QPF ? cu : __ldg(qd.u + i), v = DBL_QPF ? cv : __ldg(qd.v + i);
-            constexpr uint8_t QUEUED = 0xfc;   // in the CTA's BFS queue (code written later)
-            uint8_t code = UNRESOLVED;
-            if (u >= n || v >= n) {
-                atomicOr(&counters[CNT_ERR], 1u);
-                code = 0xfe;
-            } else if (u == v) {
-                code = DBL_REFLEXIVE;
-            } else {
-                uint64_t a[RW], b[RW];
-                load_record<RW, RS>(rec + (size_t)u * RS, a);
-                load_record<RW, RS>(rec + (size_t)v * RS, b);
-                uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
-#pragma unroll
-                for (int k = 0; k < WDL; ++k) {
-                    r1 |= a[H + k] & b[k];             // dl_out[u] & dl_in[v]
-                    r3 |= b[H + k] & a[k];             // dl_out[v] & dl_in[u]
-                    r4 |= (a[H + k] & a[k]) | (b[H + k] & b[k]);
+            if (i < count) {
+                const uint8_t code = lean_eval<WDL, WBL, TBFS>(rec, n, adj, i, u, v, use_dl, use_bl, thm1, thm2, dq,
+                                                               counters);
+                if (code != QUEUED) {
+                    qd.codes[i] = code;
+                    if (qd.visited) qd.visited[i] = 0;
+                    unres = code == UNRESOLVED;
                 }
+            }
+            lean_pend(unres, i, pending, counters);
+        }
+    } else {
+        // (run_query takes this path only for 16-byte aligned u, v and
+        // 4-byte aligned codes / 16-byte aligned visited)
+        const uint32_t nblk = (count + QPT - 1) / QPT, cr = (nblk + 31) & ~31u;
+        for (uint32_t bi = i0; bi < cr; bi += stride) {
+            const uint32_t q0 = bi * QPT;
+            uint32_t us[QPT], vs[QPT];
+            const bool full = q0 + QPT <= count;
+            if (bi < nblk) {
+                if (full) {
 #pragma unroll
-                for (int k = 0; k < WBL; ++k)
-                    r2 |= (a[WDL + k] & ~b[WDL + k]) | (b[H + WDL + k] & ~a[H + WDL + k]);
-                if (use_dl && r1) code = DBL_DL_POSITIVE;
-                else if (use_bl && r2) code = DBL_BL_NEGATIVE;
-                else if (thm1 && r3) code = DBL_THM1_NEGATIVE;
-                else if (thm2 && r4) code = DBL_THM2_NEGATIVE;
-                if (TBFS && code == UNRESOLVED) {
-                    const uint32_t slot = atomicAdd(&dq.n, 1u);
-                    if (slot < DQ_CAP) {
-                        dq.i[slot] = i;
-                        dq.u[slot] = u;
-                        dq.v[slot] = v;
+                    for (int c = 0; c < QPT / 4; ++c) {
+                        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(qd.u + q0) + c);
+                        const uint4 b = __ldg(reinterpret_cast<const uint4 *>(qd.v + q0) + c);
+                        us[4 * c] = a.x; us[4 * c + 1] = a.y; us[4 * c + 2] = a.z; us[4 * c + 3] = a.w;
+                        vs[4 * c] = b.x; vs[4 * c + 1] = b.y; vs[4 * c + 2] = b.z; vs[4 * c + 3] = b.w;
+                    }
+                } else {
 #pragma unroll
-                        for (int k = 0; k < WDL; ++k) dq.dlo[slot][k] = a[H + k];   // still in registers
-#pragma unroll
-                        for (int k = 0; k < WBL; ++k) {
-                            dq.bli[slot][k] = b[WDL + k];
-                            dq.blo[slot][k] = b[H + WDL + k];
-                        }
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(adj.ptr + u));
-                        code = QUEUED;
+                    for (int j = 0; j < QPT; ++j) {
+                        us[j] = q0 + j < count ? __ldg(qd.u + q0 + j) : 0;
+                        vs[j] = q0 + j < count ? __ldg(qd.v + q0 + j) : 0;
                     }
                 }
             }
-            if (code != QUEUED) {
-                qd.codes[i] = code;
-                if (qd.visited) qd.visited[i] = 0;
-                unres = code == UNRESOLVED;
+            uint8_t cs[QPT];
+#pragma unroll
+            for (int j = 0; j < QPT; ++j) {
+                bool unres = false;
+                cs[j] = QUEUED;
+                if (bi < nblk && q0 + j < count) {
+                    cs[j] = lean_eval<WDL, WBL, TBFS>(rec, n, adj, q0 + j, us[j], vs[j], use_dl, use_bl, thm1, thm2,
+                                                      dq, counters);
+                    unres = cs[j] == UNRESOLVED;
+                }
+                lean_pend(unres, q0 + j, pending, counters);
             }
-        }
-        const unsigned m = __ballot_sync(FULL, unres);
-        if (m) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(&counters[CNT_PENDING], (uint32_t)__popc(m));
-            base = __shfl_sync(FULL, base, 0);
-            if (unres) pending[base + __popc(m & ((1u << lane) - 1u))] = i;
+            if (bi < nblk) {
+                // queued codes are written by the BFS later: store the others
+                bool anyq = false;
+#pragma unroll
+                for (int j = 0; j < QPT; ++j) anyq |= cs[j] == QUEUED;
+                if (full && !anyq) {
+#pragma unroll
+                    for (int c = 0; c < QPT / 4; ++c) {
+                        reinterpret_cast<uchar4 *>(qd.codes + q0)[c] =
+                            make_uchar4(cs[4 * c], cs[4 * c + 1], cs[4 * c + 2], cs[4 * c + 3]);
+                        if (qd.visited) reinterpret_cast<uint4 *>(qd.visited + q0)[c] = make_uint4(0, 0, 0, 0);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < QPT; ++j)
+                        if (q0 + j < count && cs[j] != QUEUED) {
+                            qd.codes[q0 + j] = cs[j];
+                            if (qd.visited) qd.visited[q0 + j] = 0;
+                        }
+                }
+            }
         }
     }
     if constexpr (TBFS && !DBL_EXP_NOBFS) {
@@ -1266,8 +1348,9 @@ typedef void (*lean_fn)(const uint64_t *, uint32_t, const Adj, const QueryDesc, 
 typedef void (*bfsw_fn)(const uint64_t *, uint32_t, Adj, const QueryDesc, uint32_t *, uint32_t *, uint32_t *,
                         const HardArgs);
 
-static bool pick_lean(uint32_t wdl, uint32_t wbl, lean_fn &l, bfsw_fn &b, size_t &smem) {
-#define DBL_QL(A, B) if (wdl == A && wbl == B) { l = label_lean_kernel<A, B>; b = bfs_warp_kernel<A, B>; \
+static bool pick_lean(uint32_t wdl, uint32_t wbl, bool qpt4, lean_fn &l, bfsw_fn &b, size_t &smem) {
+#define DBL_QL(A, B) if (wdl == A && wbl == B) { l = qpt4 ? label_lean_kernel<A, B, DBL_QPT_HOST> : label_lean_kernel<A, B, 1>; \
+        b = bfs_warp_kernel<A, B>; \
         smem = sizeof(WarpBfs<A, B>) * (FUSED_THREADS / 32); return true; }
     DBL_QL(0, 1) DBL_QL(1, 1) DBL_QL(2, 1) DBL_QL(4, 1) DBL_QL(0, 2) DBL_QL(1, 2) DBL_QL(2, 2)
 #undef DBL_QL
@@ -1340,7 +1423,8 @@ static dbl_status hard_path_config(const dbl_index *idx, dbl_graph *g, HardPath 
 // when some query outgrew the previous stage (never on cfg2), so the host
 // submits one kernel and no memset, copy or graph per batch.
 dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
-                     uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, bool host_result) {
+                     uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited, bool host_result,
+                     bool host_inputs) {
     if (count >= 0xffffffffull) { set_error("query batch too large"); return DBL_E_ARG; }
     if (idx->wdl > MAXW || idx->wbl > MAXW) {
         set_error("label width too large for the query kernels");
@@ -1380,7 +1464,12 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     // k <= 64: lean gather + per-lane deferred BFS; wider labels (cfg5,
     // k = 256), whose fallbacks outgrow the small BFS bounds, take the
     // lane-quad gather with the warp BFS (measured on cfg5: 4.6 vs 3.7 G q/s)
-    if (count && (DBL_TBFS_ALL || DBL_LEAN_WIDE || idx->wdl <= 1) && pick_lean(idx->wdl, idx->wbl, lean, bfsw, wsmem)) {
+    // pairs in pinned host memory (zero-copy): 4 pairs per thread per step
+    // when the buffers allow the vector loads and stores
+    const bool qpt4 = host_inputs && ((((uintptr_t)u) | ((uintptr_t)v)) & 15) == 0 && (((uintptr_t)codes) & 3) == 0 &&
+                      (!visited || (((uintptr_t)visited) & 15) == 0);
+    if (count && (DBL_TBFS_ALL || DBL_LEAN_WIDE || idx->wdl <= 1) &&
+        pick_lean(idx->wdl, idx->wbl, qpt4, lean, bfsw, wsmem)) {
         int lbps = 1, wbps = 1;
         if ((s = kernel_occupancy((const void *)lean, 256, 0, &lbps)) ||
             (s = kernel_occupancy((const void *)bfsw, FUSED_THREADS, wsmem, &wbps)))
@@ -1388,7 +1477,8 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
         uint32_t *wovf = pending + 2 * g->q_pending_cap + 32;
         const HardArgs ha{hp.grid, hp.dctas, (uint32_t)hp.smem, (uint32_t)hp.dsmem, idx->wdl, idx->wbl, ovf,
                           hp.ws, g->sm_count * wbps, (uint32_t)wsmem, wovf};
-        uint32_t lgrid = (uint32_t)((count + 255) / 256);
+        const uint64_t per = qpt4 ? DBL_QPT_HOST * 256 : 256;   // queries per CTA per step
+        uint32_t lgrid = (uint32_t)((count + per - 1) / per);
         if (lgrid > (uint32_t)(g->sm_count * lbps)) lgrid = (uint32_t)(g->sm_count * lbps);
         if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
         lean<<<lgrid, 256, 0, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);

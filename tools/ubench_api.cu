@@ -50,5 +50,14 @@ int main() {
     std::printf("dbl_query, device, 1 query:       %6.1f us\n", med_us([&] { dbl_query(idx, g, du, dv, 1, 0x3f, dc, nullptr, DBL_MEM_DEVICE); }));
     std::printf("dbl_query, host (pageable), 1 q:  %6.1f us\n", med_us([&] { dbl_query(idx, g, &hu, &hv, 1, 0x3f, &hc, nullptr, DBL_MEM_HOST); }));
     std::printf("dbl_query_async + dbl_sync, 1 q:  %6.1f us\n", med_us([&] { dbl_query_async(idx, g, du, dv, 1, 0x3f, dc, nullptr); dbl_sync(g); }));
+    uint32_t *pu, *pv;
+    uint8_t *pc;
+    const size_t Q = 1 << 20;
+    cudaHostAlloc(&pu, Q * 4, 0); cudaHostAlloc(&pv, Q * 4, 0); cudaHostAlloc(&pc, Q, 0);
+    for (size_t i = 0; i < Q; ++i) { pu[i] = (uint32_t)((i * 2654435761u) % n); pv[i] = (uint32_t)((i * 40503u + 7) % n); }
+    cudaPointerAttributes at{};
+    std::printf("cudaPointerGetAttributes (pinned):%6.2f us\n", med_us([&] { cudaPointerGetAttributes(&at, pu); }));
+    std::printf("dbl_query, host pinned, 1 query:  %6.1f us\n", med_us([&] { dbl_query(idx, g, pu, pv, 1, 0x3f, pc, nullptr, DBL_MEM_HOST); }));
+    std::printf("dbl_query, host pinned, 2^20 q:   %6.1f us\n", med_us([&] { dbl_query(idx, g, pu, pv, Q, 0x3f, pc, nullptr, DBL_MEM_HOST); }, 60));
     return 0;
 }
