@@ -21,6 +21,9 @@ Fixtures:
   family.npz     C4-style family (tests/test_acceptance.py:30-37): graphs,
                  metadata, labels, all-pairs codes, insert-sequence results.
   cfg1.npz       BASELINE config 1 (ER 10k/50k, 100k queries, 1000 inserts).
+  cli.npz        the reference CLI (cli.py) on small files: build summary and
+                 snapshot bytes, query output (csv, json, from a snapshot),
+                 an update stream with per-line stats and the saved snapshot.
   label_tests.npz  dl_intersec / bl_contain (labels.py:315-327) for all pairs
                  of the worked example (the KATs of tests/test_labels.py:166-191
                  are rows of it) and of seeded random graphs with one- and
@@ -287,8 +290,57 @@ def gen_label_tests():
     return d
 
 
+def gen_cli():
+    """The reference CLI (cli.py) on small files: build summary + snapshot
+    bytes, query output (csv and json), an update stream with line stats."""
+    import contextlib
+    import io
+    import tempfile
+    from dblreach import cli as RCLI
+    d = {}
+    rng = np.random.default_rng(5)
+    # original ids are sparse and unordered, so the dense remap is exercised
+    ids = rng.permutation(np.arange(1000, 1000 + 7 * 60, 7))[:60]
+    g = R.gen_random_graph(60, 2.5, seed=9)
+    edges = [(int(ids[u]), int(ids[v])) for u, v in g.edges()]
+    lines = ["# test graph"] + [f"{u} {v}" for u, v in edges] + [f"{edges[0][0]} {edges[0][1]}"]
+    qs = [(int(ids[a]), int(ids[b])) for a, b in rng.integers(0, 60, (300, 2))]
+    ups = []
+    for a, b in rng.integers(0, 60, (40, 2)):
+        ups.append(f"+ {int(ids[a])} {int(ids[b])}")
+        if a % 3 == 0:
+            ups.append(f"? {int(ids[b])} {int(ids[a])}")
+    ups.append("+ 5000 5001")          # unseen ids: new vertices
+    ups.append(f"+ {int(ids[0])} 5000")
+    ups.append(f"? {int(ids[1])} 5001")
+    with tempfile.TemporaryDirectory() as tmp:
+        gp, qp, up, sp = (os.path.join(tmp, x) for x in ("g.txt", "q.txt", "u.txt", "s.idx"))
+        open(gp, "w").write("\n".join(lines) + "\n")
+        open(qp, "w").write("\n".join(f"{a} {b}" for a, b in qs) + "\n")
+        open(up, "w").write("\n".join(ups) + "\n")
+
+        def run(argv):
+            out, err = io.StringIO(), io.StringIO()
+            with contextlib.redirect_stdout(out), contextlib.redirect_stderr(err):
+                rc = RCLI.main(argv)
+            return rc, out.getvalue(), err.getvalue()
+        rc, out, _ = run(["build", gp, "-o", sp, "--k", "16", "--kprime", "8"])
+        d["build_rc"], d["build_out"] = np.int64(rc), np.array(out)
+        d["build_snapshot"] = np.frombuffer(open(sp, "rb").read(), np.uint8)
+        for fmt in ("csv", "json"):
+            rc, out, _ = run(["query", gp, qp, "--k", "16", "--kprime", "8", "--format", fmt, "--workers", "1"])
+            d[f"query_{fmt}_rc"], d[f"query_{fmt}_out"] = np.int64(rc), np.array(out)
+        rc, out, _ = run(["query", sp, qp, "--graph", gp, "--workers", "1"])
+        d["query_snap_rc"], d["query_snap_out"] = np.int64(rc), np.array(out)
+        rc, out, err = run(["update", gp, up, "--k", "16", "--kprime", "8", "--line-stats", "--save-index", sp])
+        d["update_rc"], d["update_out"], d["update_err"] = np.int64(rc), np.array(out), np.array(err)
+        d["update_snapshot"] = np.frombuffer(open(sp, "rb").read(), np.uint8)
+        d["graph_txt"], d["queries_txt"], d["updates_txt"] = (np.array(open(p).read()) for p in (gp, qp, up))
+    return d
+
+
 FIXTURES = {"toy": gen_toy, "leaf_hash": gen_leaf_hash, "landmarks": gen_landmarks, "family": gen_family,
-            "cfg1": gen_cfg1, "snapshots": gen_snapshots, "label_tests": gen_label_tests}
+            "cfg1": gen_cfg1, "snapshots": gen_snapshots, "label_tests": gen_label_tests, "cli": gen_cli}
 
 
 def main():

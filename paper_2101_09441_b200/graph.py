@@ -217,8 +217,78 @@ class DynamicGraph:
         self._check_vertex(dense)
         return self.original_ids[dense] if self.original_ids else dense
 
+    def to_dense(self, original: int) -> int:
+        """Dense id of an original id (graph.py:126-133)."""
+        if self._dense_of is None:
+            self._check_vertex(original)
+            return original
+        try:
+            return self._dense_of[original]
+        except KeyError:
+            raise VertexRangeError(f"unknown original vertex id {original}") from None
+
+    def register_original(self, original: int) -> int:
+        """Map an original id to a dense id, creating a vertex if unseen (graph.py:135-145)."""
+        if self._dense_of is None:
+            self._dense_of = {self.to_original(v): v for v in self.vertices()}
+            self.original_ids = [self.to_original(v) for v in self.vertices()]
+        dense = self._dense_of.get(original)
+        if dense is None:
+            dense = self.add_vertex()
+            self._dense_of[original] = dense
+            self.original_ids.append(original)
+        return dense
+
     def __repr__(self) -> str:
         return f"DynamicGraph(n={self._n}, m={self.edge_count}, device={self.device})"
+
+
+def load_edge_list(source, gzipped: bool | None = None, *, device: int = 0) -> DynamicGraph:
+    """Parse "src dst" lines into a device graph with densely remapped ids
+    (graph.py:174-210): '#' lines are comments, duplicates collapse, dense
+    ids follow first appearance (src before dst on a line), original ids are
+    kept on the side table.  The edges go to the device in one upload.
+    """
+    import gzip
+    import io
+    from .errors import EdgeListFormatError
+    if isinstance(source, str):
+        if gzipped or (gzipped is None and source.endswith(".gz")):
+            stream = io.TextIOWrapper(gzip.open(source, "rb"), encoding="utf-8")
+        else:
+            stream = open(source, "r", encoding="utf-8")
+    elif isinstance(source, bytes):
+        raw = gzip.decompress(source) if (gzipped or (gzipped is None and source[:2] == b"\x1f\x8b")) else source
+        stream = io.StringIO(raw.decode("utf-8"))
+    else:
+        stream = source
+    flat: list[int] = []
+    with stream:
+        for line_no, line in enumerate(stream, start=1):
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            parts = line.split()
+            if len(parts) != 2:
+                raise EdgeListFormatError(line_no, f"expected 'src dst', got {line!r}")
+            try:
+                raw_u, raw_v = int(parts[0]), int(parts[1])
+            except ValueError:
+                raise EdgeListFormatError(line_no, f"non-integer vertex id in {line!r}") from None
+            if raw_u < 0 or raw_v < 0:
+                raise EdgeListFormatError(line_no, f"negative vertex id in {line!r}")
+            flat.append(raw_u)
+            flat.append(raw_v)
+    a = np.array(flat, dtype=np.int64)
+    uniq, first, inv = np.unique(a, return_index=True, return_inverse=True)
+    order = np.argsort(first, kind="stable")          # originals in first-appearance order
+    rank = np.empty(len(uniq), np.int64)
+    rank[order] = np.arange(len(uniq))
+    dense = rank[inv].astype(np.uint32)
+    g = DynamicGraph.from_edges(len(uniq), dense[0::2], dense[1::2], device=device)
+    g.original_ids = uniq[order].tolist()
+    g._dense_of = {o: i for i, o in enumerate(g.original_ids)}
+    return g
 
 
 _converted: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
