@@ -659,6 +659,7 @@ def run_reference(args):
     ins_rate = len(iu) / (time.perf_counter() - t0)
     sample = (f"1M-query batch per step, oracle/dbl_oracle.c (port of queries.py:94-142), "
               f"{cores} threads; build {build_s:.2f} s; inserts: sequential insert_edge x20000")
+    pyref = python_reference(n, src, dst, oidx, qu, qv, cores)
     return {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
@@ -668,7 +669,55 @@ def run_reference(args):
                              "sample": sample},
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "build": {"value_s": build_s, "threads": cores},
-            "inserts": {"value": ins_rate, "unit": "edges/s", "threads": 1}}
+            "inserts": {"value": ins_rate, "unit": "edges/s", "threads": 1},
+            "python_reference": pyref}
+
+
+def python_reference(n, src, dst, oidx, qu, qv, cores) -> dict:
+    """Context only: the unmodified Python reference (dblreach, pip-installed
+    into baseline/_ref) answering the same batch.  Its own build takes ~640 s
+    at this size, so it loads the labels from a DBLIDX01 snapshot of the
+    port's index (the format both engines read; snapshot.py:104-148), then
+    query_batch with workers = 1 on a 100k sample and workers = cpu_count on
+    the whole batch (queries.py:210-249).  Codes are checked against the port."""
+    import io
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(ref_dir):
+        return {"unavailable": "baseline/_ref not installed"}
+    sys.path.insert(0, ref_dir)
+    try:
+        import dblreach as R
+    except ImportError as e:
+        return {"unavailable": f"import dblreach failed: {e}"}
+    finally:
+        sys.path.remove(ref_dir)
+    from oracle import oracle as O
+    from paper_2101_09441_b200.labels import IndexConfig
+    from paper_2101_09441_b200.snapshot import encode_snapshot
+    t0 = time.perf_counter()
+    g = R.DynamicGraph(n)
+    for u, v in zip(src.tolist(), dst.tolist()):
+        g.add_edge(u, v)
+    load_s = time.perf_counter() - t0
+    blob = encode_snapshot(IndexConfig(), n, oidx.landmarks.astype(np.uint64), oidx.leaf_flags, oidx.bucket,
+                           oidx.dl_in, oidx.dl_out, oidx.bl_in, oidx.bl_out)
+    idx = R.load_index(io.BytesIO(blob))
+    pairs = list(zip(qu.tolist(), qv.tolist()))
+    k = 100_000
+    t0 = time.perf_counter()
+    outs1, _ = R.query_batch(g, idx, pairs[:k], workers=1)
+    one = k / (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    outs, _ = R.query_batch(g, idx, pairs, workers=cores)
+    many = len(pairs) / (time.perf_counter() - t0)
+    names = [a.value for a in R.AnsweredBy]
+    codes = np.array([names.index(o.answered_by.value) for o in outs], np.uint8)
+    oc, _ = O.OracleGraph(n, src, dst).query_batch(oidx, qu, qv, threads=cores)
+    return {"value_workers_1": one, "value_workers_all": many, "unit": "queries/s", "cores": cores,
+            "codes_equal_port": bool(np.array_equal(codes, oc)),
+            "sample": f"dblreach 0.1.0 (unmodified, baseline/_ref): query_batch workers=1 on {k} pairs, "
+                      f"workers={cores} on the 1M batch; labels via load_index of a DBLIDX01 snapshot of "
+                      f"the port's build (graph load {load_s:.1f} s not timed)"}
 
 
 def main():
