@@ -207,7 +207,7 @@ def cfg3(degrees=(2, 4, 8, 16, 32, 64), scale=22):
         assert rep.ok, rep.violations[:3]
         cols = label_columns_check(g, idx, seed=d)
         nq = csr_codes_check(g, idx, qu[:200_000], qv[:200_000], codes[:200_000])
-        full = False
+        full = "not run: the oracle build at d >= 16 is too slow for this run (sampled columns, CSR-oracle codes and the verifier stand in)"
         if d <= 8:
             s, dd = g.edge_arrays()
             og = O.OracleGraph(n, s, dd)
@@ -216,7 +216,7 @@ def cfg3(degrees=(2, 4, 8, 16, 32, 64), scale=22):
             for f in FAMS:
                 assert np.array_equal(w[f], getattr(oidx, f)), f
             del og, oidx
-            full = True
+            full = "all four families equal the oracle's"
         out.append({"degree": d, "n": n, "m": g.edge_count, "build_s": tb, "query_qps": qps, **st,
                     "parity": {"verify_fixpoint": True, "bit_columns": cols, "codes_vs_csr_oracle": nq,
                                "full_labels_vs_oracle": full}})
