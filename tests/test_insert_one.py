@@ -118,3 +118,55 @@ def test_pending_edges_visible_to_graph_ops():
         og.insert_edge(oidx, u, v)
     assert labels_match(idx, oidx)
     assert st.early_terminated is False
+
+
+# ------------------------------------------------------- batched insertion --
+
+def _batch_vs_oracle(n, src, dst, iu, iv, k=64, kp=64):
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    idx = E.build_index(g, E.IndexConfig(k=k, k_prime=kp))
+    og = O.OracleGraph(n, src, dst)
+    oidx = og.build(k, kp, threads=2)
+    st = E.insert_edges(g, idx, iu, iv)
+    for u, v in zip(iu.tolist(), iv.tolist()):
+        og.insert_edge(oidx, u, v)
+    assert g.edge_count == og.edge_count
+    assert labels_match(idx, oidx)
+    assert idx.labels_equal(E.rebuild_index(g, idx))
+    return g, idx, st
+
+
+def test_batch_prep_duplicates_and_skew():
+    """Batched insertion on batches with heavy duplication (6000 copies of one
+    edge), on a batch of edges all leaving one hub, tiny batches and batches
+    of already-present edges."""
+    n = 1 << 12
+    src, dst = W.rmat_edges(12, 4, seed=51)
+    rng = np.random.default_rng(52)
+    # 6000 copies of one edge + 2000 random ones
+    iu = np.concatenate([np.full(6000, 7, np.uint32), rng.integers(0, n, 2000, dtype=np.uint32)])
+    iv = np.concatenate([np.full(6000, 4000, np.uint32), rng.integers(0, n, 2000, dtype=np.uint32)])
+    _, _, st = _batch_vs_oracle(n, src, dst, iu, iv)
+    assert st.requested == 8000
+    # 3000 edges from one hub
+    hv = rng.permutation(n)[:3000].astype(np.uint32)
+    _batch_vs_oracle(n, src, dst, np.full(3000, 1, np.uint32), hv)
+    # tiny batches, and a batch that repeats already-present edges
+    _batch_vs_oracle(n, src, dst, np.array([5], np.uint32), np.array([9], np.uint32))
+    _batch_vs_oracle(n, src, dst, src[:500].copy(), dst[:500].copy())
+
+
+def test_batch_prep_range_error_is_a_noop():
+    n = 1 << 10
+    src, dst = W.rmat_edges(10, 4, seed=53)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    idx = E.build_index(g)
+    before = idx.export_words()
+    m0 = g.edge_count
+    iu = np.array([1, 2, 3, n], np.uint32)
+    iv = np.array([4, 5, 6, 7], np.uint32)
+    with pytest.raises(E.VertexRangeError):
+        E.insert_edges(g, idx, iu, iv)
+    assert g.edge_count == m0
+    after = idx.export_words()
+    assert all(np.array_equal(before[f], after[f]) for f in FAMS)
