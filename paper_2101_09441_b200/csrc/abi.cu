@@ -895,12 +895,11 @@ extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, 
     // _propagate_union dequeues the seed plus every changed non-seed vertex;
     // a direction the fast path already finished (its labels are final, so
     // the fixpoint changes nothing there) keeps the fast path's counts
-    if (dirs_done == 0) {
-        st.visited = 1 + changed[0] - seedc[0];
-        st.labels_changed = changed[0];
+    for (int d = 0; d < 2; ++d) {
+        if ((dirs_done >> d) & 1u) continue;
+        st.visited += 1 + changed[d] - seedc[d];
+        st.labels_changed += changed[d];
     }
-    st.visited += 1 + changed[1] - seedc[1];
-    st.labels_changed += changed[1];
     if (stats) *stats = st;
     return DBL_OK;
 }

@@ -16,6 +16,7 @@
 //      known to fit the CTA's tables.  A cone that outgrows them leaves that
 //      direction's labels untouched and the host runs the batch fixpoint
 //      (run_insert), counting only the directions the kernel did not finish.
+//      The two directions run concurrently, one per half of the CTA.
 // The counts are the reference's: visited = dequeues = 1 + changed
 // non-seed vertices per direction, labels_changed = changed vertices
 // (the seed when `add` was new to it).
@@ -31,6 +32,7 @@
 namespace dbl {
 
 constexpr int ONE_THREADS = 512;
+constexpr int ONE_HALF = ONE_THREADS / 2;   // threads per direction (the two run concurrently)
 constexpr int ONE_HCAP = 4096;        // discovered-vertex hash (power of two)
 constexpr int ONE_FCAP = 2048;        // frontier list capacity per level
 constexpr uint32_t ONE_EMAX = 1u << 16;   // adjacency entries scanned per direction before giving up
@@ -43,8 +45,8 @@ struct OneOut {
     uint32_t visited;
     uint32_t changed;
     uint32_t range;       // a discovered id was outside [0, n) (corrupt adjacency)
-    uint32_t dirs_done;   // directions propagated and written (0, 1 or 2)
-    uint32_t visited0, changed0;   // direction 0's counts (kept when direction 1 overflows)
+    uint32_t done[2];     // direction d propagated and written
+    uint32_t dvisited[2], dchanged[2];   // per-direction counts (kept when the other overflows)
 };
 
 struct OneShared {
@@ -59,16 +61,24 @@ struct OneShared {
     uint64_t add[2 * MAX_SHARD_WORDS];
 };
 
-__device__ __forceinline__ bool row_has(const uint32_t *ptr, const uint32_t *col, uint32_t u, uint32_t v) {
+// Warp-cooperative search of a sorted row: 32 probes per step narrow the
+// interval 32-fold (a hub's row of 10^5 ids takes 3 steps, not 17).
+__device__ __forceinline__ bool row_has_warp(const uint32_t *ptr, const uint32_t *col, uint32_t u, uint32_t v) {
     if (!ptr) return false;
-    uint32_t lo = ptr[u], hi = ptr[u + 1];
-    while (lo < hi) {   // rows are sorted (built from sorted keys)
-        const uint32_t mid = (lo + hi) >> 1;
-        const uint32_t c = col[mid];
-        if (c == v) return true;
-        if (c < v) lo = mid + 1; else hi = mid;
+    const int lane = threadIdx.x & 31;
+    uint32_t lo = ptr[u], hi = ptr[u + 1];   // candidates [lo, hi)
+    while (hi - lo > 32) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t p = lo + lane * step;
+        const bool le = p < hi && col[p] <= v;
+        const unsigned b = __ballot_sync(FULL, le);
+        const uint32_t k = b ? 31 - __clz(b) : 0;   // last probe <= v
+        if (!b) return false;
+        lo = lo + k * step;
+        hi = min(hi, lo + step);
     }
-    return false;
+    const bool hit = lo + lane < hi && col[lo + lane] == v;
+    return __any_sync(FULL, hit);
 }
 
 // Insert x into the discovered set at level `l`; returns 1 if this call
@@ -125,15 +135,20 @@ __device__ void one_consider(OneShared &S, const uint64_t *rec, uint32_t rs, uin
     }
 }
 
+// barrier of one direction's half of the CTA (named barriers 1 and 2)
+__device__ __forceinline__ void half_sync(int h) {
+    asm volatile("bar.sync %0, %1;" ::"r"(h + 1), "r"(ONE_HALF) : "memory");
+}
+
 // One direction: seed s, add = the other endpoint's half, labels at word
 // offset `off` of each record, neighbours along `a` plus the pending edges
 // (fwd: entries (s', t) with s' in the frontier give t; bwd: (t, s') give t).
 // Returns the number of discovered non-seed vertices (S.overflow on failure).
 __device__ uint32_t one_direction(OneShared &S, const uint64_t *rec, uint32_t rs, uint32_t off, uint32_t H,
                                   uint32_t n, const Adj &a, const uint64_t *pend, uint32_t npend, bool fwd,
-                                  uint32_t seed, uint32_t *range) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = ONE_THREADS / 32;
-    for (int i = tid; i < ONE_HCAP; i += ONE_THREADS) S.key[i] = ONE_EMPTY;
+                                  uint32_t seed, uint32_t *range, int h) {
+    const int tid = threadIdx.x - h * ONE_HALF, lane = tid & 31, warp = tid >> 5, nwarps = ONE_HALF / 32;
+    for (int i = tid; i < ONE_HCAP; i += ONE_HALF) S.key[i] = ONE_EMPTY;
     if (tid == 0) {
         S.nfront[0] = 1;
         S.nfront[1] = 0;
@@ -141,9 +156,9 @@ __device__ uint32_t one_direction(OneShared &S, const uint64_t *rec, uint32_t rs
         S.found = 0;
         S.edges = 0;
     }
-    __syncthreads();
+    half_sync(h);
     if (tid == 0) one_insert(S, seed, 0);   // the seed is expanded once and never re-enqueued
-    __syncthreads();
+    half_sync(h);
     for (uint16_t l = 0;; ++l) {
         const int cb = l & 1, nb = cb ^ 1;
         const uint32_t nf = min(S.nfront[cb], (uint32_t)ONE_FCAP);
@@ -168,89 +183,104 @@ __device__ uint32_t one_direction(OneShared &S, const uint64_t *rec, uint32_t rs
             }
         }
         // pending edges leaving (fwd) / entering (bwd) a vertex of this level
-        for (uint32_t e = tid; e < npend; e += ONE_THREADS) {
+        for (uint32_t e = tid; e < npend; e += ONE_HALF) {
             const uint64_t k = pend[e];
             const uint32_t from = fwd ? (uint32_t)(k >> 32) : (uint32_t)k;
             const uint32_t to = fwd ? (uint32_t)k : (uint32_t)(k >> 32);
             const int sl = one_find(S, from);
             if (sl >= 0 && S.lvl[sl] == l) one_consider(S, rec, rs, off, H, n, to, (uint16_t)(l + 1), range);
         }
-        __syncthreads();
+        half_sync(h);
         if (tid == 0) S.nfront[cb] = 0;
-        __syncthreads();
+        half_sync(h);
         (void)nb;
     }
-    __syncthreads();
+    half_sync(h);
     return S.found;
 }
 
 // OR S.add into the discovered vertices' halves (and the seed's).
-__device__ void one_apply(OneShared &S, uint64_t *rec, uint32_t rs, uint32_t off, uint32_t H) {
-    for (int i = threadIdx.x; i < ONE_HCAP; i += ONE_THREADS) {
+__device__ void one_apply(OneShared &S, uint64_t *rec, uint32_t rs, uint32_t off, uint32_t H, int h) {
+    for (int i = threadIdx.x - h * ONE_HALF; i < ONE_HCAP; i += ONE_HALF) {
         const uint32_t x = S.key[i];
         if (x == ONE_EMPTY) continue;
         uint64_t *p = rec + (uint64_t)x * rs + off;
         for (uint32_t j = 0; j < H; ++j) p[j] |= S.add[j];
     }
-    __syncthreads();
+    half_sync(h);
 }
 
 __global__ void __launch_bounds__(ONE_THREADS, 1)
 insert_one_kernel(uint64_t *rec, uint32_t rs, uint32_t H, uint32_t wdl, uint32_t n, uint32_t u, uint32_t v,
                   Adj fwd, Adj rev, uint64_t *pend, uint32_t npend, uint32_t pcap, OneOut *out) {
     extern __shared__ __align__(16) unsigned char smem[];
-    OneShared &S = *reinterpret_cast<OneShared *>(smem);
+    OneShared *S2 = reinterpret_cast<OneShared *>(smem);   // one table set per direction
     const int tid = threadIdx.x;
     const uint64_t key = ((uint64_t)u << 32) | v;
-    __shared__ uint32_t cert, range;
-    if (tid == 0) {
-        // pre-check on pre-insertion labels (updates.py:123)
-        uint64_t c = 0;
-        for (uint32_t j = 0; j < wdl; ++j) c |= rec[(uint64_t)u * rs + H + j] & rec[(uint64_t)v * rs + j];
-        cert = c != 0;
-        range = 0;
-        S.overflow = 0;
-        S.exists = row_has(fwd.ptr, fwd.col, u, v) || row_has(fwd.dptr, fwd.dcol, u, v);
-    }
+    __shared__ uint32_t cert, range, exists;
+    __shared__ uint32_t rok[2], rvis[2], rchg[2];
+    if (tid == 0) { range = 0; exists = 0; }
     __syncthreads();
-    for (uint32_t e = tid; e < npend; e += ONE_THREADS)
-        if (pend[e] == key) S.exists = 1;
-    __syncthreads();
-    const bool is_new = !S.exists;
-    if (tid == 0 && is_new && npend < pcap) pend[npend] = key;   // add_edge (updates.py:124)
-    OneOut o{};
-    o.certified = cert;
-    o.is_new = is_new;
-    if (!cert) {
-        // forward from v with L_in(u) (updates.py:128-130), then backward from u
-        // with L_out(v) (:131-133); the halves are {dl | bl} at offsets 0 and H
-        uint32_t changed = 0, visited = 0;
-        bool ok = true;
-        for (int d = 0; d < 2 && ok; ++d) {
-            const uint32_t seed = d == 0 ? v : u, other = d == 0 ? u : v, off = d == 0 ? 0 : H;
-            for (uint32_t j = tid; j < H; j += ONE_THREADS) S.add[j] = rec[(uint64_t)other * rs + off + j];
-            __syncthreads();
-            const bool seed_changes = lacks(rec, rs, off, H, seed, S.add);
-            const uint32_t found = one_direction(S, rec, rs, off, H, n, d == 0 ? fwd : rev, pend,
-                                                 npend + ((is_new && npend < pcap) ? 1 : 0), d == 0, seed, &range);
-            if (S.overflow) { ok = false; break; }
-            // the directions touch disjoint words (in- vs out-half), so each is
-            // written as soon as its cone is known; when direction 1 then
-            // overflows, the host finishes only that one (dirs_done = 1)
-            one_apply(S, rec, rs, off, H);
-            visited += 1 + found;
-            changed += found + (seed_changes ? 1 : 0);
-            o.dirs_done = d + 1;
-            if (d == 0) { o.visited0 = visited; o.changed0 = changed; }
+    // in parallel: warp 0 the base row, warp 1 the delta row, warp 2 the
+    // pre-check on pre-insertion labels (updates.py:123), the rest the log
+    const int w = tid >> 5;
+    if (w == 0) {
+        if (row_has_warp(fwd.ptr, fwd.col, u, v) && (tid & 31) == 0) exists = 1;
+    } else if (w == 1) {
+        if (row_has_warp(fwd.dptr, fwd.dcol, u, v) && (tid & 31) == 0) exists = 1;
+    } else if (w == 2) {
+        if ((tid & 31) == 0) {
+            uint64_t c = 0;
+            for (uint32_t j = 0; j < wdl; ++j) c |= rec[(uint64_t)u * rs + H + j] & rec[(uint64_t)v * rs + j];
+            cert = c != 0;
         }
-        o.overflow = !ok;
-        o.visited = visited;
-        o.changed = changed;
+    } else {
+        for (uint32_t e = tid - 96; e < npend; e += ONE_THREADS - 96)
+            if (pend[e] == key) exists = 1;
     }
+    __syncthreads();
+    const bool is_new = !exists;
+    if (tid == 0 && is_new && npend < pcap) pend[npend] = key;   // add_edge (updates.py:124)
+    if (!cert) {
+        // both propagations at once, one per half of the CTA: forward from v
+        // with L_in(u) (updates.py:128-130), backward from u with L_out(v)
+        // (:131-133).  They read and write disjoint words (the in-half at
+        // word 0, the out-half at word H of every record), so neither sees
+        // the other's writes.
+        const int h = tid / ONE_HALF, ltid = tid - h * ONE_HALF;
+        OneShared &S = S2[h];
+        const uint32_t seed = h == 0 ? v : u, other = h == 0 ? u : v, off = h == 0 ? 0 : H;
+        for (uint32_t j = ltid; j < H; j += ONE_HALF) S.add[j] = rec[(uint64_t)other * rs + off + j];
+        if (ltid == 0) S.overflow = 0;
+        half_sync(h);
+        const bool seed_changes = lacks(rec, rs, off, H, seed, S.add);
+        const uint32_t found = one_direction(S, rec, rs, off, H, n, h == 0 ? fwd : rev, pend,
+                                             npend + ((is_new && npend < pcap) ? 1 : 0), h == 0, seed, &range, h);
+        const bool ok = !S.overflow;
+        if (ok) one_apply(S, rec, rs, off, H, h);
+        if (ltid == 0) {
+            rok[h] = ok;
+            rvis[h] = 1 + found;
+            rchg[h] = found + (seed_changes ? 1 : 0);
+        }
+    }
+    __syncthreads();
     if (tid == 0) {
+        OneOut o{};
+        o.certified = cert;
+        o.is_new = is_new;
         o.range = range;
+        if (!cert) {
+            o.overflow = !(rok[0] && rok[1]);
+            for (int d = 0; d < 2; ++d) {
+                o.done[d] = rok[d];
+                o.dvisited[d] = rok[d] ? rvis[d] : 0;
+                o.dchanged[d] = rok[d] ? rchg[d] : 0;
+            }
+            o.visited = o.dvisited[0] + o.dvisited[1];
+            o.changed = o.dchanged[0] + o.dchanged[1];
+        }
         *out = o;
-        __threadfence_system();
     }
 }
 
@@ -262,8 +292,8 @@ namespace dbl {
 
 // Single-edge insert, fast path.  Returns DBL_OK with *done = false when the
 // caller must finish with the batch fixpoint: a cone outgrew the tables; the
-// edge is in the pending log, direction 0 is finished (labels written, counts
-// in *st) iff *dirs_done == 1, and direction 1 is untouched.
+// edge is in the pending log, direction d is finished (labels written, its
+// counts in *st) iff bit d of *dirs_done is set, the other is untouched.
 dbl_status insert_edge_fast(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, dbl_update_stats *st,
                             bool *done, uint32_t *dirs_done) {
     *done = false;
@@ -273,9 +303,9 @@ dbl_status insert_edge_fast(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v
     if ((s = g->pend.ensure(PEND_CAP * 8 + 64)) || (s = g->one_out.ensure(sizeof(OneOut) + 64))) return s;
     if (idx->wdl + idx->wbl > (uint32_t)MAX_SHARD_WORDS) { set_error("label width too large"); return DBL_E_CONFIG; }
     int bps = 1;
-    if ((s = kernel_occupancy((const void *)insert_one_kernel, ONE_THREADS, sizeof(OneShared), &bps))) return s;
+    if ((s = kernel_occupancy((const void *)insert_one_kernel, ONE_THREADS, 2 * sizeof(OneShared), &bps))) return s;
     OneOut *out = reinterpret_cast<OneOut *>(g->one_out.p);
-    insert_one_kernel<<<1, ONE_THREADS, sizeof(OneShared), g->stream>>>(
+    insert_one_kernel<<<1, ONE_THREADS, 2 * sizeof(OneShared), g->stream>>>(
         idx->rec.as<uint64_t>(), idx->rs, idx->wdl + idx->wbl, idx->wdl, g->n, u, v, graph_fwd(g), graph_rev(g),
         g->pend.as<uint64_t>(), g->n_pend, PEND_CAP, out);
     DBL_CHECK_LAUNCH("insert_one_kernel");
@@ -290,10 +320,10 @@ dbl_status insert_edge_fast(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v
         *done = true;
         return DBL_OK;
     }
-    if (o.overflow) {   // direction 0 may be done: its counts stand
-        st->visited = o.dirs_done ? o.visited0 : 0;
-        st->labels_changed = o.dirs_done ? o.changed0 : 0;
-        *dirs_done = o.dirs_done;
+    if (o.overflow) {   // a finished direction's counts stand
+        st->visited = o.dvisited[0] + o.dvisited[1];
+        st->labels_changed = o.dchanged[0] + o.dchanged[1];
+        *dirs_done = (o.done[0] ? 1u : 0u) | (o.done[1] ? 2u : 0u);
         return DBL_OK;
     }
     st->visited = o.visited;
