@@ -21,9 +21,11 @@
  *    stream (the handle's own stream waits on it through an event, without
  *    a host sync); a caller producing them on another stream synchronises
  *    that stream first.
- *  - Handles own all device state.  Calls on one handle are serialised on
- *    the handle's stream; queries are read-only and may not overlap an
- *    insertion (reference contract: pkg/README.md:179-183).
+ *  - Handles own all device state (including per-call workspaces), so a
+ *    graph handle serves one host thread at a time; its calls are
+ *    serialised on the handle's stream.  For concurrent queries use one
+ *    replica per thread or dbl_query_multi.  Queries are read-only and may
+ *    not overlap an insertion (reference contract: pkg/README.md:179-183).
  *  - Label bit i lives in bit (i % 64) of word (i / 64), least-significant
  *    word first (pkg/docs/snapshot-format.md:38-42).
  */

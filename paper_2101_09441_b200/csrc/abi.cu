@@ -803,6 +803,8 @@ extern "C" dbl_status dbl_query_multi(const dbl_index *const *idx, const dbl_gra
         dbl_status s = check_pair(idx[d], g[d]);
         if (s) return s;
         if (idx[d]->n != idx[0]->n) { set_error("replicas differ in vertex count"); return DBL_E_MISMATCH; }
+        for (uint32_t e = 0; e < d; ++e)   // a handle serves one host thread at a time
+            if (g[e] == g[d]) { set_error("dbl_query_multi needs distinct graph handles per slice"); return DBL_E_ARG; }
     }
     const uint64_t chunk = ndev ? (count + ndev - 1) / ndev : count;
     std::vector<dbl_status> st(ndev, DBL_OK);

@@ -83,6 +83,8 @@ def test_query_multi_errors():
     g2 = E.DynamicGraph.from_edges(101, src, dst)
     with pytest.raises(E.IndexGraphMismatchError):
         P.query_batch_sharded([reps[0], (g2, reps[1][1])], [(0, 1)] * 10)
+    with pytest.raises(TypeError):   # one handle twice would be driven from two threads (DBL_E_ARG)
+        P.query_batch_sharded([reps[0], reps[0]], [(0, 1)] * 10)
 
 
 def _bench_json(out: str) -> dict:
