@@ -61,6 +61,8 @@ def replicate(n: int, src, dst, devices: Sequence[int], config=None):
     """
     from .graph import DynamicGraph
     from .labels import build_index
+    if hasattr(src, "is_cuda"):   # device tensors live on one GPU: replicate from host copies
+        src, dst = src.cpu().numpy(), dst.cpu().numpy()
     out = []
     for d in devices:
         g = DynamicGraph.from_edges(n, src, dst, device=d)
