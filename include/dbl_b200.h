@@ -230,8 +230,10 @@ dbl_status dbl_sync(const dbl_graph *g);
  * slices of ceil(count / ndev) pairs (queries.py:231-232) and slice d is
  * answered by (idx[d], g[d]) -- identical replicas, one per device -- on its
  * own host thread, all slices concurrently.  Results land in input order.
- * mem must be DBL_MEM_HOST (device-resident batches: dbl_query per handle).
- * Errors name the failing slice. */
+ * DBL_MEM_HOST: pinned or pageable host buffers.  DBL_MEM_DEVICE: u, v,
+ * codes (and visited) all on one GPU; the other devices access them by peer
+ * access over NVLink (enabled here; the producer of u / v must be finished).
+ * Each graph handle may appear once.  Errors name the failing slice. */
 dbl_status dbl_query_multi(const dbl_index *const *idx, const dbl_graph *const *g, uint32_t ndev,
                            const uint32_t *u, const uint32_t *v, uint64_t count, uint32_t flags,
                            uint8_t *codes, uint32_t *visited, dbl_mem mem);

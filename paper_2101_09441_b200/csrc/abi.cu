@@ -790,15 +790,45 @@ extern "C" dbl_status dbl_query_async(const dbl_index *idx, const dbl_graph *g, 
 // One batch split across several devices: contiguous,
 // order-preserving slices as in the reference's worker pool
 // (queries.py:224-232: chunk = ceil(count / parts)), each answered on its
-// own handle pair from one host thread per device, so the slices' PCIe
-// transfers and kernels run concurrently.  The replicas must be identical
-// (same graph and index built on every device); host memory only.
+// own handle pair from one host thread per device, so the slices' transfers
+// and kernels run concurrently.  The replicas must be identical (same graph
+// and index built on every device).  Host batches: every slice crosses PCIe
+// to its own GPU.  Device batches (all buffers on one GPU): the other GPUs
+// read their slices and write their codes over NVLink by peer access.
 extern "C" dbl_status dbl_query_multi(const dbl_index *const *idx, const dbl_graph *const *g, uint32_t ndev,
                                       const uint32_t *u, const uint32_t *v, uint64_t count, uint32_t flags,
                                       uint8_t *codes, uint32_t *visited, dbl_mem mem) {
     if (!idx || !g || ndev == 0) { set_error("null handle list"); return DBL_E_ARG; }
-    if (mem != DBL_MEM_HOST) { set_error("dbl_query_multi takes host buffers (device batches: dbl_query per handle)"); return DBL_E_ARG; }
     if (count && (!u || !v || !codes)) { set_error("null argument"); return DBL_E_ARG; }
+    if (mem == DBL_MEM_DEVICE && count) {
+        // a batch resident on one GPU: every other GPU reads its slice of the
+        // pairs and writes its codes over NVLink (peer access), inside its
+        // query kernel -- no staging copies, no collective
+        cudaPointerAttributes at{};
+        const void *bufs[4] = {u, v, codes, visited};
+        int owner = -1;
+        for (const void *b : bufs) {
+            if (!b) continue;
+            if (cudaPointerGetAttributes(&at, b) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+                cudaGetLastError();
+                set_error("dbl_query_multi with DBL_MEM_DEVICE needs device buffers");
+                return DBL_E_ARG;
+            }
+            if (owner < 0) owner = at.device;
+            if (at.device != owner) { set_error("the batch's buffers live on different devices"); return DBL_E_ARG; }
+        }
+        for (uint32_t d = 0; d < ndev; ++d) {
+            const int dev = g[d]->device;
+            if (dev == owner) continue;
+            int can = 0;
+            DBL_CUDA(cudaDeviceCanAccessPeer(&can, dev, owner));
+            if (!can) { set_error("device " + std::to_string(dev) + " has no peer access to the batch's device"); return DBL_E_ARG; }
+            DBL_CUDA(cudaSetDevice(dev));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(owner, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+            cudaGetLastError();
+        }
+    }
     for (uint32_t d = 0; d < ndev; ++d) {
         dbl_status s = check_pair(idx[d], g[d]);
         if (s) return s;
@@ -813,7 +843,7 @@ extern "C" dbl_status dbl_query_multi(const dbl_index *const *idx, const dbl_gra
         const uint64_t lo = d * chunk < count ? d * chunk : count;
         const uint64_t hi = lo + chunk < count ? lo + chunk : count;
         st[d] = query_impl(idx[d], g[d], u + lo, v + lo, hi - lo, flags, codes + lo, visited ? visited + lo : nullptr,
-                           DBL_MEM_HOST, true);
+                           mem, true);
         if (st[d]) msg[d] = g_last_error;
     };
     if (ndev == 1 || count < 2 * (uint64_t)ndev) {

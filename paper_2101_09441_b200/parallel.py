@@ -76,7 +76,9 @@ def query_batch_sharded(replicas, queries, flags=None):
     `replicas` is a list of (graph, index) pairs with identical contents
     (see replicate()).  The batch is split into the reference's contiguous
     slices, answered concurrently by dbl_query_multi, and returned in input
-    order as (Outcomes, BatchStats), exactly like query_batch.
+    order as (Outcomes, BatchStats), exactly like query_batch.  `queries`
+    may be a (u, v) pair of CUDA tensors on one GPU: the other GPUs then read
+    their slices and write their answers over NVLink (peer access).
     """
     from . import _native as N
     from .queries import DEFAULT_FLAGS, BatchStats, Outcomes, _check_consistent, _pairs_to_arrays
@@ -91,11 +93,25 @@ def query_batch_sharded(replicas, queries, flags=None):
         _check_consistent(g, idx)
         gs.append(g.handle)
         ids.append(idx.handle)
+    garr = (ctypes.c_void_p * len(gs))(*[h.value for h in gs])
+    iarr = (ctypes.c_void_p * len(ids))(*[h.value for h in ids])
+    if isinstance(queries, tuple) and len(queries) == 2 and all(getattr(q, "is_cuda", False) for q in queries):
+        # a batch resident on one GPU: slices read and codes written over NVLink
+        import torch
+        u, v = queries
+        N.check_device_ids(u, v, u.device.index)
+        torch.cuda.current_stream(u.device).synchronize()
+        codes = torch.empty(u.numel(), dtype=torch.uint8, device=u.device)
+        vis = torch.empty(u.numel(), dtype=torch.int32, device=u.device)
+        t0 = time.perf_counter()
+        N.call("dbl_query_multi", iarr, garr, len(gs), N.ptr(u), N.ptr(v), u.numel(), flags.bits(),
+               N.ptr(codes), N.ptr(vis), N.MEM_DEVICE)
+        elapsed_ms = (time.perf_counter() - t0) * 1e3
+        out = Outcomes(codes.cpu().numpy(), vis.cpu().numpy().view(np.uint32))
+        return out, BatchStats.collect(out, elapsed_ms)
     u, v = _pairs_to_arrays(queries)
     codes = np.zeros(len(u), np.uint8)
     vis = np.zeros(len(u), np.uint32)
-    garr = (ctypes.c_void_p * len(gs))(*[h.value for h in gs])
-    iarr = (ctypes.c_void_p * len(ids))(*[h.value for h in ids])
     t0 = time.perf_counter()
     N.call("dbl_query_multi", iarr, garr, len(gs), N.ptr(u), N.ptr(v), len(u), flags.bits(),
            N.ptr(codes), N.ptr(vis), N.MEM_HOST)

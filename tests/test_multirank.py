@@ -64,6 +64,13 @@ def test_query_multi_two_handles_one_gpu():
         assert np.array_equal(out.codes, one.codes)
         assert np.array_equal(out.visited == 0, one.visited == 0)
         assert st.query_count == s1.query_count and st.label_answered == s1.label_answered
+    # a batch resident on the GPU (the peer-access path; one device here)
+    import torch
+    du = torch.from_numpy(qu.view(np.int32)).cuda()
+    dv = torch.from_numpy(qv.view(np.int32)).cuda()
+    for k in (1, 2):
+        out, _ = P.query_batch_sharded(reps[:k], (du, dv))
+        assert np.array_equal(out.codes, one.codes)
     # tiny and empty batches take the serial path
     out, _ = P.query_batch_sharded(reps, [(0, 1), (2, 2), (5, 3)])
     assert np.array_equal(out.codes, E.query_batch(reps[0][0], reps[0][1], [(0, 1), (2, 2), (5, 3)])[0].codes)

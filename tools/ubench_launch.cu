@@ -77,6 +77,53 @@ int main() {
                                "two small kernels", "no kernel (event pair)"};
         std::printf("%-50s median %6.2f us  mean %6.2f us\n", names[variant], ts[ts.size() / 2], mean);
     }
+    // the same empty kernel as a one-node CUDA graph
+    {
+        cudaGraph_t gr;
+        cudaGraphExec_t ge;
+        cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal);
+        small_kernel<<<1184, 256, 0, s>>>(flag);
+        cudaStreamEndCapture(s, &gr);
+        cudaGraphInstantiate(&ge, gr, 0);
+        std::vector<float> ts;
+        for (int i = 0; i < 220; ++i) {
+            busy_kernel<<<1, 32, 0, s>>>(50000);
+            cudaEventRecord(e0, s);
+            cudaGraphLaunch(ge, s);
+            cudaEventRecord(e1, s);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (i >= 20) ts.push_back(ms * 1e3f);
+        }
+        std::sort(ts.begin(), ts.end());
+        std::printf("small kernel as a CUDA graph                      median %6.2f us\n", ts[ts.size() / 2]);
+    }
+    // programmatic dependent launch after the busy kernel (the event pair still around it)
+    {
+        std::vector<float> ts;
+        for (int i = 0; i < 220; ++i) {
+            busy_kernel<<<1, 32, 0, s>>>(50000);
+            cudaEventRecord(e0, s);
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(1184);
+            cfg.blockDim = dim3(256);
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, small_kernel, flag);
+            cudaEventRecord(e1, s);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (i >= 20) ts.push_back(ms * 1e3f);
+        }
+        std::sort(ts.begin(), ts.end());
+        std::printf("small kernel with PDL attribute                   median %6.2f us\n", ts[ts.size() / 2]);
+    }
     // CTA count vs fixed cost: same thread count, different CTA sizes
     const int cfgs[][2] = {{1184, 256}, {592, 512}, {296, 1024}, {148, 1024}, {2368, 128}, {148, 256}};
     for (auto &c : cfgs) {

@@ -102,5 +102,26 @@ int main() {
         cudaStreamWaitEvent(s0, ej, 0);
         cudaEventDestroy(ej);
     }, (bytes + obytes) / 1e6);
+    // hybrid: a share of the 8 MB read zero-copy by a kernel while the copy
+    // engine moves the rest (both on the same link)
+    for (int pct : {30, 40, 50, 60}) {
+        const size_t zc = (bytes * pct / 100) & ~(size_t)255;
+        char name[64];
+        std::snprintf(name, sizeof name, "hybrid: %d%% zero-copy + rest by DMA", pct);
+        timeit(name, [&] {
+            cudaEvent_t es;
+            cudaEventCreateWithFlags(&es, cudaEventDisableTiming);
+            cudaEventRecord(es, s0);
+            cudaStreamWaitEvent(s1, es, 0);
+            cudaEventDestroy(es);
+            cudaMemcpyAsync((char *)d + zc, (char *)h + zc, bytes - zc, cudaMemcpyHostToDevice, s1);
+            zc_read<uint4><<<sms * 4, 256, 0, s0>>>((const uint4 *)hd, zc / 16, out);
+            cudaEvent_t ej;
+            cudaEventCreateWithFlags(&ej, cudaEventDisableTiming);
+            cudaEventRecord(ej, s1);
+            cudaStreamWaitEvent(s0, ej, 0);
+            cudaEventDestroy(ej);
+        }, bytes / 1e6);
+    }
     return 0;
 }
