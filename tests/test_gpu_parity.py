@@ -693,3 +693,48 @@ def test_label_tests_random_pairs_vs_oracle(k, kp):
     odl, obl = O.label_tests({f: getattr(oidx, f) for f in FAMS}, x, y)
     np.testing.assert_array_equal(dl, odl)
     np.testing.assert_array_equal(bl, obl)
+
+
+def test_dense_workspace_lazy_paths():
+    """The dense BFS workspace is allocated on first need: a batch that needs it
+    is re-run by whichever path issued it -- the staged small host batch, the
+    chunked pageable pipeline (> 64k pairs), the device-resident synchronous
+    call, and dbl_query_async completed by dbl_sync."""
+    import torch
+    from paper_2101_09441_b200 import _native as N
+    # no labels to prune with, and targets with no in-edges: every such BFS
+    # exhausts the giant component (thousands of vertices), overflowing the
+    # 64-query groups' shared tables
+    nn = 12_000
+    src, dst = W.gen_random_graph(nn, 2.0, seed=5)
+    og = O.OracleGraph(nn, src, dst)
+    oidx = og.build(0, 1)
+    qu, qv = W.uniform_queries(nn, 70_000, 3)
+    sources = np.setdiff1d(np.arange(nn, dtype=np.uint32), dst)
+    qv[::2] = sources[np.arange(len(qv[::2])) % len(sources)]
+    fl = E.QueryFlags(prune_dl=False, prune_bl=False)   # unpruned cones outgrow the shared tables
+    oc, _ = og.query_batch(oidx, qu, qv, fl.bits(), threads=8)
+    for path in ("staged", "pipelined", "device", "async"):
+        g = E.DynamicGraph.from_edges(nn, src, dst)   # fresh graph: no dense workspace yet
+        idx = E.build_index(g, E.IndexConfig(k=0, k_prime=1))
+        if path == "staged":
+            codes, _ = E.query_codes(g, idx, qu[:30_000], qv[:30_000], fl)
+            np.testing.assert_array_equal(codes, oc[:30_000], err_msg=path)
+        elif path == "pipelined":
+            codes, _ = E.query_codes(g, idx, qu, qv, fl)
+            np.testing.assert_array_equal(codes, oc, err_msg=path)
+        else:
+            du = torch.from_numpy(qu.view(np.int32)).cuda()
+            dv = torch.from_numpy(qv.view(np.int32)).cuda()
+            if path == "device":
+                codes, _ = E.query_codes(g, idx, du, dv, fl)
+            else:
+                torch.cuda.synchronize()
+                codes = torch.empty(len(qu), dtype=torch.uint8, device="cuda")
+                N.call("dbl_query_async", idx.handle, g.handle, N.ptr(du), N.ptr(dv), len(qu), fl.bits(),
+                       N.ptr(codes), None)
+                N.call("dbl_sync", g.handle)
+            np.testing.assert_array_equal(codes.cpu().numpy(), oc, err_msg=path)
+        qc = np.zeros(8, np.uint32)
+        N.call("dbl_query_counters", g.handle, N.ptr(qc))
+        assert qc[3] > 0, f"{path}: the batch did not need the dense kernel"

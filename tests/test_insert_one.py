@@ -57,11 +57,12 @@ def run_sequence(n, src, dst, iu, iv, k=64, kp=64, query_every=0, seed=0):
     return g, idx, og, oidx
 
 
-def test_rmat_sequence_with_queries():
+@pytest.mark.parametrize("k,kp", [(64, 64), (256, 64), (0, 200)])
+def test_rmat_sequence_with_queries(k, kp):
     n = 1 << 12
     src, dst = W.rmat_edges(12, 4, seed=31)
     iu, iv = W.gen_insert_workload(src, dst, n, 400, seed=32)
-    run_sequence(n, src, dst, iu, iv, query_every=50)
+    run_sequence(n, src, dst, iu, iv, k=k, kp=kp, query_every=50)
 
 
 def test_pending_log_overflow_and_repeats():
