@@ -944,7 +944,8 @@ struct ReachParams {
     uint32_t *nb[2][3];      // per direction: vertices newly marked in step s go to nb[d][s % 3]
     unsigned int *changed;   // [step % 3]: marks made in step s (read after its barrier, cleared in s + 2);
                              // [3]: set when the step cap stopped the search (no head start then);
-                             // [4]: steps run, [5]: bottom-up sweeps among them (trace)
+                             // [4]: steps run, [5]: bottom-up sweeps among them (trace);
+                             // [6]: apply CTAs done
     uint32_t max_sweeps;     // cap on bottom-up sweeps (each O(n))
     uint32_t max_steps;      // cap on all steps
     uint32_t td_switch;      // switch to top-down once a step marks fewer vertices than this
@@ -957,6 +958,8 @@ struct ReachParams {
     const uint32_t *bucket;
     bool write_rec;          // records not seeded yet (full build): write seeds | head start, whole lines
     uint32_t n, nwords;
+    uint32_t kp;             // k_prime (bucket bits per BL half)
+    bool fused_apply;        // apply the head start inside reach_kernel (small graphs)
 };
 
 __device__ __forceinline__ bool vis_test_ca(const uint32_t *vis, uint32_t x) {
@@ -988,6 +991,130 @@ __device__ __forceinline__ bool any_marked(const Adj &a, const uint32_t *vis, ui
 #ifndef DBL_BU_ILP
 #define DBL_BU_ILP 1
 #endif
+// The head start into the records (after the unions): vertices of h's SCC
+// leave the level-0 frontier, then every record takes L_in(h) / L_out(h) by
+// membership (and, in write mode, its seeds).  FAST adds the write-mode path
+// for strides dividing 64 words (more registers: used by the stand-alone
+// apply kernel; the fused small-graph variant inside reach_kernel keeps the
+// general loop and the sweeps' register budget).
+template <bool WORK, bool FAST>
+__device__ __forceinline__ void apply_head_start(const ReachParams &P, uint64_t tid, uint64_t nth,
+                                                 const unsigned long long *acc, bool drop, bool capped) {
+    const uint32_t H = P.H, rw = 2 * H, rs = rec_stride(H);
+    // a vertex of h's SCC (in D(h) and A(h)) now holds L_in(h) / L_out(h),
+    // which every successor / predecessor also holds: it leaves the level-0
+    // frontier (on R-MAT that drops the landmarks, the hubs of that frontier)
+    for (uint64_t w = tid; w < P.nwords && !drop; w += nth) {
+        if (capped) {   // partial sets: every marked vertex propagates its head start
+            P.front[0][w] |= P.vis[0][w];
+            P.front[1][w] |= P.vis[1][w];
+            continue;
+        }
+        const uint32_t scc = P.vis[0][w] & P.vis[1][w];
+        if (scc) {
+            if (P.front[0]) P.front[0][w] &= ~scc;
+            if (P.front[1]) P.front[1][w] &= ~scc;
+        }
+    }
+    // apply: a warp takes 32 consecutive records (one bitmap word per
+    // direction) and ORs the unions in with 512-byte coalesced
+    // read-modify-writes, instead of 8-byte accesses at the record stride.
+    // In write mode (full build, prep skipped the records) it writes every
+    // record whole instead -- seeds from the metadata | the unions, pad words
+    // zero -- with no read at all, and the landmark bits follow.
+    {
+        const int lane = threadIdx.x & 31;
+        const uint32_t wdl = P.wdl;
+        const uint64_t nblk = P.nwords, gw = tid >> 5, nw = nth >> 5;
+        unsigned long long touched = 0;
+        // lane's first (record, word) in a block and the step per 64 words,
+        // so the store loop needs no division by the runtime stride
+        const uint32_t r0 = (2 * lane) / rs, w0 = (2 * lane) % rs, q64 = 64 / rs, m64 = 64 % rs;
+        if (FAST && P.write_rec && m64 == 0) {
+            // write mode, stride dividing 64 words (every stride up to
+            // k = 448): a lane's word pair w0 is the same in every store, so
+            // its union words are fixed; the next block's bitmap words, flags
+            // and buckets load while this block's records are stored
+            const uint32_t w = w0;
+            const uint64_t A0 = w < rw ? acc[w] : 0ull, A1 = w + 1 < rw ? acc[w + 1] : 0ull;
+            const bool h0 = w < H, h1 = w + 1 < H;
+            uint32_t fb = 0, bb = 0, f = 0, b = 0;
+            auto fetch = [&](uint64_t blk) {
+                fb = drop ? 0u : P.vis[0][blk];
+                bb = drop ? 0u : P.vis[1][blk];
+                const uint64_t v = blk * 32 + lane;
+                f = v < P.n ? P.flags[v] : 0u;
+                b = v < P.n ? P.bucket[v] : 0u;
+            };
+            if (gw < nblk) fetch(gw);
+            for (uint64_t blk = gw; blk < nblk; blk += nw) {
+                const uint32_t cfb = fb, cbb = bb, cf = f, cbk = b;
+                if (blk + nw < nblk) fetch(blk + nw);
+                if (WORK && lane == 0) touched += __popc(cfb | cbb);
+                const uint32_t sb = cbk % 64;
+                const uint32_t win = (cf & 1) ? wdl + cbk / 64 : 0xffffffffu;
+                const uint32_t wout = (cf & 2) ? H + wdl + cbk / 64 : 0xffffffffu;
+                uint64_t *base = P.rec + blk * 32 * rs;
+                uint32_t r = r0;
+                for (uint32_t t = 0; t < rs * 32; t += 64, r += q64) {
+                    const uint32_t swin = __shfl_sync(FULL, win, r), swout = __shfl_sync(FULL, wout, r);
+                    const uint64_t sbit = 1ull << __shfl_sync(FULL, sb, r);
+                    const bool in_d = (cfb >> r) & 1u, in_a = (cbb >> r) & 1u;
+                    if (blk * 32 + r >= P.n) continue;
+                    ulonglong2 val;
+                    val.x = ((h0 ? in_d : in_a) ? A0 : 0ull) | ((w == swin || w == swout) ? sbit : 0ull);
+                    val.y = ((h1 ? in_d : in_a) ? A1 : 0ull) | ((w + 1 == swin || w + 1 == swout) ? sbit : 0ull);
+                    *reinterpret_cast<ulonglong2 *>(base + t + 2 * lane) = val;
+                }
+            }
+        } else
+        for (uint64_t blk = gw; blk < nblk; blk += nw) {
+            const uint32_t fb = drop ? 0u : P.vis[0][blk], bb = drop ? 0u : P.vis[1][blk];
+            if (WORK && lane == 0) touched += __popc(fb | bb);
+            if (!(fb | bb) && !P.write_rec) continue;
+            uint64_t *base = P.rec + blk * 32 * rs;
+            uint32_t win = 0xffffffffu, wout = 0xffffffffu, sb = 0;
+            if (P.write_rec) {
+                const uint64_t v = blk * 32 + lane;
+                if (v < P.n) {
+                    const uint8_t f = P.flags[v];
+                    if (f) {
+                        const uint32_t b = P.bucket[v];
+                        sb = b % 64;
+                        if (f & 1) win = wdl + b / 64;
+                        if (f & 2) wout = H + wdl + b / 64;
+                    }
+                }
+            }
+            uint32_t r = r0, w = w0;
+            for (uint32_t t = 0; t < rs * 32; t += 64, r += q64, w += m64) {
+                if (w >= rs) { w -= rs; ++r; }
+                const uint32_t wi = t + 2 * lane;
+                const bool in_d = (fb >> r) & 1u, in_a = (bb >> r) & 1u;
+                const uint64_t a0 = (w < H ? in_d : (w < rw && in_a)) ? acc[w] : 0ull;
+                const uint64_t a1 = (w + 1 < H ? in_d : (w + 1 < rw && in_a)) ? acc[w + 1] : 0ull;
+                if (P.write_rec) {
+                    const uint32_t swin = __shfl_sync(FULL, win, r), swout = __shfl_sync(FULL, wout, r);
+                    const uint64_t sbit = 1ull << __shfl_sync(FULL, sb, r);
+                    if (blk * 32 + r >= P.n) continue;
+                    ulonglong2 val;
+                    val.x = a0 | ((w == swin || w == swout) ? sbit : 0ull);
+                    val.y = a1 | ((w + 1 == swin || w + 1 == swout) ? sbit : 0ull);
+                    *reinterpret_cast<ulonglong2 *>(base + wi) = val;
+                } else if (a0 | a1) {
+                    if (blk * 32 + r >= P.n) continue;
+                    ulonglong2 *p = reinterpret_cast<ulonglong2 *>(base + wi);
+                    ulonglong2 val = *p;
+                    val.x |= a0;
+                    val.y |= a1;
+                    *p = val;
+                }
+            }
+        }
+        if (WORK && lane == 0 && touched) atomicAdd(&P.work[4], touched);
+    }
+}
+
 template <int MINB, bool WORK>
 __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
     cg::grid_group grid = cg::this_grid();
@@ -1235,6 +1362,7 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
                 }
             }
             if (!__any_sync(FULL, qin != 0xffffffffu || qout != 0xffffffffu)) continue;
+            bool full = true;
             for (uint32_t q = 0; q < wbl; ++q) {
                 const uint64_t vi = qin == q ? 1ull << bb : 0ull, vo = qout == q ? 1ull << bb : 0ull;
                 const uint64_t ri = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(vi >> 32)) << 32) |
@@ -1242,10 +1370,19 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
                 const uint64_t ro = ((uint64_t)__reduce_or_sync(FULL, (uint32_t)(vo >> 32)) << 32) |
                                     __reduce_or_sync(FULL, (uint32_t)vo);
                 if (lane == 0) {
-                    if (ri && ((wm >> (wdl + q)) & 1u)) atomicOr(&acc[wdl + q], (unsigned long long)ri);
-                    if (ro && ((wm >> (H + wdl + q)) & 1u)) atomicOr(&acc[H + wdl + q], (unsigned long long)ro);
+                    // every bucket bit of the word present: this CTA's share
+                    // of the union is complete (R-MAT: after a few hundred
+                    // leaves of its ~57k vertices at cfg5)
+                    const uint64_t fm = (q == wbl - 1 && P.kp % 64) ? (1ull << (P.kp % 64)) - 1 : ~0ull;
+                    uint64_t got_in = fm, got_out = fm;
+                    if ((wm >> (wdl + q)) & 1u)
+                        got_in = (ri ? atomicOr(&acc[wdl + q], (unsigned long long)ri) : acc[wdl + q]) | ri;
+                    if ((wm >> (H + wdl + q)) & 1u)
+                        got_out = (ro ? atomicOr(&acc[H + wdl + q], (unsigned long long)ro) : acc[H + wdl + q]) | ro;
+                    full = full && (got_in & fm) == fm && (got_out & fm) == fm;
                 }
             }
+            if (__shfl_sync(FULL, full, 0)) break;
         }
         for (uint64_t i = tid; i < P.k; i += nth) {
             const uint32_t x = P.lm[i], w = (uint32_t)(i / 64);
@@ -1258,87 +1395,60 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x)
         if (acc[i]) atomicOr(&P.L[i], acc[i]);
+    // large graphs: the unions are complete when the kernel ends, and
+    // reach_apply_kernel (launched behind it) writes them into the records;
+    // small ones apply here (a launch costs more than their apply)
+    if (!P.fused_apply) return;
     grid.sync();
     for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = *(volatile unsigned long long *)&P.L[i];
     __syncthreads();
-    // a vertex of h's SCC (in D(h) and A(h)) now holds L_in(h) / L_out(h),
-    // which every successor / predecessor also holds: it leaves the level-0
-    // frontier (on R-MAT that drops the landmarks, the hubs of that frontier)
-    for (uint64_t w = tid; w < P.nwords && !drop; w += nth) {
-        if (capped) {   // partial sets: every marked vertex propagates its head start
-            P.front[0][w] |= P.vis[0][w];
-            P.front[1][w] |= P.vis[1][w];
-            continue;
-        }
-        const uint32_t scc = P.vis[0][w] & P.vis[1][w];
-        if (scc) {
-            if (P.front[0]) P.front[0][w] &= ~scc;
-            if (P.front[1]) P.front[1][w] &= ~scc;
+    apply_head_start<WORK, false>(P, tid, nth, acc, drop, capped);
+    if (P.write_rec) {   // landmark i seeds bit i of both DL halves (labels.py:291-293)
+        grid.sync();
+        for (uint64_t i = tid; i < P.k; i += nth) {
+            const uint32_t x = P.lm[i];
+            if (x >= P.n) continue;
+            const unsigned long long bit = 1ull << (i % 64);
+            atomicOr(reinterpret_cast<unsigned long long *>(P.rec + (uint64_t)x * rs + i / 64), bit);
+            atomicOr(reinterpret_cast<unsigned long long *>(P.rec + (uint64_t)x * rs + H + i / 64), bit);
         }
     }
-    // apply: a warp takes 32 consecutive records (one bitmap word per
-    // direction) and ORs the unions in with 512-byte coalesced
-    // read-modify-writes, instead of 8-byte accesses at the record stride.
-    // In write mode (full build, prep skipped the records) it writes every
-    // record whole instead -- seeds from the metadata | the unions, pad words
-    // zero -- with no read at all, and the landmark bits follow.
-    {
-        const int lane = threadIdx.x & 31;
-        const uint32_t wdl = P.wdl;
-        const uint64_t nblk = P.nwords, gw = tid >> 5, nw = nth >> 5;
-        unsigned long long touched = 0;
-        for (uint64_t blk = gw; blk < nblk; blk += nw) {
-            const uint32_t fb = drop ? 0u : P.vis[0][blk], bb = drop ? 0u : P.vis[1][blk];
-            if (WORK && lane == 0) touched += __popc(fb | bb);
-            if (!(fb | bb) && !P.write_rec) continue;
-            uint64_t *base = P.rec + blk * 32 * rs;
-            uint32_t win = 0xffffffffu, wout = 0xffffffffu, sb = 0;
-            if (P.write_rec) {
-                const uint64_t v = blk * 32 + lane;
-                if (v < P.n) {
-                    const uint8_t f = P.flags[v];
-                    if (f) {
-                        const uint32_t b = P.bucket[v];
-                        sb = b % 64;
-                        if (f & 1) win = wdl + b / 64;
-                        if (f & 2) wout = H + wdl + b / 64;
-                    }
-                }
-            }
-            for (uint32_t t = 0; t < rs * 32; t += 64) {
-                const uint32_t wi = t + 2 * lane, r = wi / rs, w = wi % rs;
-                const bool in_d = (fb >> r) & 1u, in_a = (bb >> r) & 1u;
-                const uint64_t a0 = (w < H ? in_d : (w < rw && in_a)) ? acc[w] : 0ull;
-                const uint64_t a1 = (w + 1 < H ? in_d : (w + 1 < rw && in_a)) ? acc[w + 1] : 0ull;
-                if (P.write_rec) {
-                    const uint32_t swin = __shfl_sync(FULL, win, r), swout = __shfl_sync(FULL, wout, r);
-                    const uint64_t sbit = 1ull << __shfl_sync(FULL, sb, r);
-                    if (blk * 32 + r >= P.n) continue;
-                    ulonglong2 val;
-                    val.x = a0 | ((w == swin || w == swout) ? sbit : 0ull);
-                    val.y = a1 | ((w + 1 == swin || w + 1 == swout) ? sbit : 0ull);
-                    *reinterpret_cast<ulonglong2 *>(base + wi) = val;
-                } else if (a0 | a1) {
-                    if (blk * 32 + r >= P.n) continue;
-                    ulonglong2 *p = reinterpret_cast<ulonglong2 *>(base + wi);
-                    ulonglong2 val = *p;
-                    val.x |= a0;
-                    val.y |= a1;
-                    *p = val;
-                }
-            }
-        }
-        if (WORK && lane == 0 && touched) atomicAdd(&P.work[4], touched);
-        if (P.write_rec) {   // landmark i seeds bit i of both DL halves (labels.py:291-293)
-            grid.sync();
-            for (uint64_t i = tid; i < P.k; i += nth) {
-                const uint32_t x = P.lm[i];
-                if (x >= P.n) continue;
-                const unsigned long long bit = 1ull << (i % 64);
-                atomicOr(reinterpret_cast<unsigned long long *>(P.rec + (uint64_t)x * rs + i / 64), bit);
-                atomicOr(reinterpret_cast<unsigned long long *>(P.rec + (uint64_t)x * rs + H + i / 64), bit);
-            }
-        }
+}
+
+// Apply the head start (after reach_kernel; a plain launch at full occupancy,
+// no grid barrier: the records stream out at HBM write rate).
+template <bool WORK>
+__global__ void __launch_bounds__(256) reach_apply_kernel(ReachParams P) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    const bool have = P.lm[0] < P.n;
+    if (!have && !P.write_rec) return;
+    const bool capped = *(volatile unsigned int *)&P.changed[3] != 0;
+    const bool drop = capped && !(P.front[0] && P.front[1]);
+    if (drop && !P.write_rec) return;
+    __shared__ unsigned long long acc[2 * MAX_SHARD_WORDS];
+    const uint32_t H = P.H, rw = 2 * H, rs = rec_stride(H);
+    for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = drop ? 0ull : P.L[i];
+    __syncthreads();
+    apply_head_start<WORK, true>(P, tid, nth, acc, drop, capped);
+    if (!P.write_rec) return;
+    // landmark i seeds bit i of both DL halves (labels.py:291-293) once every
+    // record is written whole: the last CTA to finish ORs them in
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&P.changed[6], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (uint32_t i = threadIdx.x; i < P.k; i += blockDim.x) {
+        const uint32_t x = P.lm[i];
+        if (x >= P.n) continue;
+        const unsigned long long bit = 1ull << (i % 64);
+        atomicOr(reinterpret_cast<unsigned long long *>(P.rec + (uint64_t)x * rs + i / 64), bit);
+        atomicOr(reinterpret_cast<unsigned long long *>(P.rec + (uint64_t)x * rs + H + i / 64), bit);
     }
 }
 
@@ -1351,7 +1461,7 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     const size_t bmw = ((size_t)n + 31) / 32;
     const size_t bbytes = ((bmw * 4 + 255) / 256) * 256;
     dbl_status s;
-    const size_t rbytes = 8 * bbytes + 2 * MAX_SHARD_WORDS * 8 + 64 + 66 * 8 + 8 * 8;
+    const size_t rbytes = 8 * bbytes + 2 * MAX_SHARD_WORDS * 8 + 64 + 66 * 8 + 16 * 8;
     if ((s = g->reach.ensure(rbytes))) return s;
     uint32_t *vf = g->reach.as<uint32_t>();
     uint32_t *vb = reinterpret_cast<uint32_t *>(g->reach.as<char>() + bbytes);
@@ -1366,6 +1476,7 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     R.front[0] = front0;
     R.front[1] = front1;
     R.k = idx->cfg.k;
+    R.kp = idx->cfg.k_prime;
     R.wdl = idx->wdl;
     R.dmask_out = nullptr;
     R.scc_out = nullptr;
@@ -1398,7 +1509,10 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     // in ~5; deep sparse ones stop here and hand the partial sets to the
     // label fixpoint's frontier
     R.max_sweeps = 12;
-    R.max_steps = 64;
+#ifndef DBL_REACH_MAX_STEPS
+#define DBL_REACH_MAX_STEPS 64
+#endif
+    R.max_steps = DBL_REACH_MAX_STEPS;
     R.td_switch = DBL_TD_DIV ? (uint32_t)(n / DBL_TD_DIV) : 0u;
     constexpr bool tr = DBL_TRACE;
     unsigned long long *trb = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(chg) + 64);
@@ -1414,9 +1528,27 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
                            : (wk ? (const void *)reach_kernel<6, true> : (const void *)reach_kernel<6, false>);
     int bps = 1;
     if ((s = kernel_occupancy(kern, 256, 0, &bps))) return s;
+    // the records stream out faster from a separate full-occupancy kernel
+    // once they are large (cfg5: 1.64 vs ~2.2 ms); a small graph's apply is
+    // cheaper than a launch (cfg2: ~14 us either way)
+    R.fused_apply = (uint64_t)n * idx->rs * 8 < (256ull << 20);
     void *args[] = {(void *)&R};
     DBL_CUDA(cudaLaunchCooperativeKernel(kern, dim3(g->sm_count * bps), dim3(256), args, 0, g->stream));
     DBL_LAUNCHED();
+    if (!R.fused_apply) {
+        // one resident wave (grid-stride over the 32-vertex blocks)
+        const void *ak = wk ? (const void *)reach_apply_kernel<true> : (const void *)reach_apply_kernel<false>;
+        int abps = 1;
+        if ((s = kernel_occupancy(ak, 256, 0, &abps))) return s;
+        const uint64_t blocks_needed = ((uint64_t)bmw * 32 + 255) / 256;
+        const uint64_t full = (uint64_t)g->sm_count * abps;
+        const int ag = (int)(blocks_needed < full ? (blocks_needed ? blocks_needed : 1) : full);
+        if (wk)
+            reach_apply_kernel<true><<<ag, 256, 0, g->stream>>>(R);
+        else
+            reach_apply_kernel<false><<<ag, 256, 0, g->stream>>>(R);
+        DBL_CHECK_LAUNCH("reach_apply_kernel");
+    }
     if (DBL_TRACE) {
         unsigned int hc[6];
         DBL_CUDA(cudaMemcpyAsync(hc, chg, sizeof(hc), cudaMemcpyDeviceToHost, g->stream));

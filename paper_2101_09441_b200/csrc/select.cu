@@ -24,6 +24,22 @@ __host__ __device__ __forceinline__ uint32_t leaf_hash_u64(uint64_t v, uint32_t 
     return (uint32_t)(x % (uint64_t)k_prime);
 }
 
+// The same hash with the final 64-bit modulo as a multiply-high by
+// magic = floor((2^64 - 1) / k') and one correction (the quotient estimate
+// is at most one short), exact for every x and k' >= 1: the general 64-bit
+// division is the most expensive part of the build's prep pass.
+__device__ __forceinline__ uint32_t leaf_hash_magic(uint64_t v, uint32_t k_prime, uint64_t magic, uint64_t seed_mix) {
+    uint64_t x = v * 0x9E3779B97F4A7C15ull + seed_mix;
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    uint64_t r = x - __umul64hi(x, magic) * k_prime;
+    if (r >= k_prime) r -= k_prime;
+    return (uint32_t)r;
+}
+
 __global__ void leaf_hash_kernel(const uint64_t *__restrict__ ids, uint64_t count, uint32_t k_prime,
                                  uint64_t seed, uint32_t *__restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
@@ -209,10 +225,11 @@ struct PrepArgs {
     uint32_t n;
     int strategy;
     int do_lm, do_leaves;
-    uint64_t *score;
     uint64_t threshold;
     uint32_t k_prime;
     uint64_t seed;
+    uint64_t kp_magic, seed_mix;   // leaf_hash_magic constants
+    uint8_t *bins;                 // score bin per vertex (landmark candidates)
     const uint32_t *ovr;
     uint8_t *flags;
     uint32_t *bucket;
@@ -233,83 +250,82 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
     const uint64_t nr = ((uint64_t)A.n + 31) & ~31ull;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
-    // the next vertex's row pointers are loaded while this one is processed
-    // (one dependent round trip per vertex instead of two)
+    // A warp takes 32 consecutive vertices per step; each lane loads row
+    // pointer i and takes i + 1 from its neighbour (lane 31 loads it), and
+    // the next step's pointers load while this step is processed.
     const bool degs = A.do_lm || A.do_leaves;
     const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     uint32_t nf0 = 0, nf1 = 0, nr0 = 0, nr1 = 0;
-    if (degs && i0 < A.n) {
-        nf0 = __ldg(A.f.ptr + i0); nf1 = __ldg(A.f.ptr + i0 + 1);
-        nr0 = __ldg(A.r.ptr + i0); nr1 = __ldg(A.r.ptr + i0 + 1);
-    }
+    auto fetch = [&](uint64_t i) {
+        nf0 = i <= A.n ? __ldg(A.f.ptr + i) : 0u;
+        nr0 = i <= A.n ? __ldg(A.r.ptr + i) : 0u;
+        if (lane == 31 && i < A.n) {
+            nf1 = __ldg(A.f.ptr + i + 1);
+            nr1 = __ldg(A.r.ptr + i + 1);
+        }
+    };
+    if (degs && i0 < nr) fetch(i0);
     for (uint64_t i = i0; i < nr; i += stride) {
-        bool p0 = false, p1 = false;
-        uint32_t win = 0xffffffffu, wout = 0xffffffffu;
-        uint64_t bit = 0;
-        const uint32_t cf0 = nf0, cf1 = nf1, cr0 = nr0, cr1 = nr1;
-        if (degs && i + stride < A.n) {
-            nf0 = __ldg(A.f.ptr + i + stride); nf1 = __ldg(A.f.ptr + i + stride + 1);
-            nr0 = __ldg(A.r.ptr + i + stride); nr1 = __ldg(A.r.ptr + i + stride + 1);
-        }
-        if (i < A.n) {
-            const uint32_t v = (uint32_t)i;
-            uint8_t f;
-            uint32_t b;
-            if (degs) {
-                uint64_t out = cf1 - cf0, in = cr1 - cr0;
-                if (A.f.dptr) { out += A.f.dptr[v + 1] - A.f.dptr[v]; in += A.r.dptr[v + 1] - A.r.dptr[v]; }
-                if (A.do_lm) {
-                    const uint64_t sc = strategy_score(A.strategy, in, out);
-                    A.score[v] = sc;
-                    // warp-aggregated: ~70% of R-MAT scores fall in bin 0
-                    // (degree-0 ends), so per-thread shared atomics serialise
-                    const int bin = score_bin(sc);
-                    const unsigned peers = __match_any_sync(__activemask(), bin);
-                    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+        const bool valid = i < A.n;
+        const uint32_t v = (uint32_t)i;
+        uint32_t cf0 = nf0, cf1 = __shfl_down_sync(FULL, nf0, 1), cr0 = nr0, cr1 = __shfl_down_sync(FULL, nr0, 1);
+        if (lane == 31) { cf1 = nf1; cr1 = nr1; }
+        if (degs && i + stride < nr) fetch(i + stride);
+        uint8_t f = 0;
+        uint32_t b = 0;
+        if (degs) {
+            uint64_t out = cf1 - cf0, in = cr1 - cr0;
+            if (A.f.dptr && valid) { out += A.f.dptr[v + 1] - A.f.dptr[v]; in += A.r.dptr[v + 1] - A.r.dptr[v]; }
+            if (A.do_lm) {
+                // bin 0 (a degree-0 end: ~70% of R-MAT vertices) counted by
+                // one ballot; the other lanes aggregate per bin
+                const int bin = valid ? score_bin(strategy_score(A.strategy, in, out)) : 0;
+                if (valid) A.bins[v] = (uint8_t)bin;
+                const unsigned z = __ballot_sync(FULL, valid && bin == 0);
+                const unsigned nz = __ballot_sync(FULL, valid && bin != 0);
+                if (lane == 0 && z) atomicAdd(&h[0], (uint32_t)__popc(z));
+                if (valid && bin != 0) {
+                    const unsigned peers = __match_any_sync(nz, bin);
+                    if (lane == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
                 }
-                if (A.do_leaves) {
-                    f = 0;
-                    if (in == 0) f |= 1;
-                    if (out == 0) f |= 2;
-                    if (A.threshold > 0 && in * out <= A.threshold) f |= 3;
-                    b = 0;
-                    if (f) {
-                        const uint32_t o = A.ovr ? A.ovr[v] : 0xffffffffu;
-                        if (o != 0xffffffffu) {
-                            if (o >= A.k_prime) atomicOr(&A.st->err, 1ull);
-                            b = o;
-                        } else {
-                            b = leaf_hash_u64(v, A.k_prime, A.seed);
-                        }
+            }
+            if (A.do_leaves && valid) {
+                if (in == 0) f |= 1;
+                if (out == 0) f |= 2;
+                if (A.threshold > 0 && in * out <= A.threshold) f |= 3;
+                if (f) {
+                    const uint32_t o = A.ovr ? A.ovr[v] : 0xffffffffu;
+                    if (o != 0xffffffffu) {
+                        if (o >= A.k_prime) atomicOr(&A.st->err, 1ull);
+                        b = o;
+                    } else {
+                        b = leaf_hash_magic(v, A.k_prime, A.kp_magic, A.seed_mix);
                     }
-                    A.flags[v] = f;
-                    A.bucket[v] = b;
                 }
+                A.flags[v] = f;
+                A.bucket[v] = b;
             }
-            if (!A.do_leaves) {
-                f = A.flags[v];
-                b = A.bucket[v];
-            }
-            // seeds: bl_in bit for source leaves, bl_out bit for sinks, dl words 0
-            const uint32_t bw = A.wdl + b / 64;
-            win = (f & 1) ? bw : 0xffffffffu;
-            wout = (f & 2) ? H + bw : 0xffffffffu;
-            bit = 1ull << (b % 64);
-            p0 = (f & 1) && bw >= A.a0 && bw < A.e0;
-            p1 = (f & 2) && H + bw >= A.a1 && H + bw < A.e1;
         }
+        if (!A.do_leaves && valid) {
+            f = A.flags[v];
+            b = A.bucket[v];
+        }
+        // seeds: bl_in bit for source leaves, bl_out bit for sinks, dl words 0
+        const uint32_t bw = A.wdl + b / 64;
+        const uint32_t win = (f & 1) ? bw : 0xffffffffu;
+        const uint32_t wout = (f & 2) ? H + bw : 0xffffffffu;
+        const uint64_t bit = 1ull << (b % 64);
+        const bool p0 = (f & 1) && bw >= A.a0 && bw < A.e0;
+        const bool p1 = (f & 2) && H + bw >= A.a1 && H + bw < A.e1;
         // the warp's 32 records (pad words included) as one contiguous block
         // (skipped when the pivot pass writes the records: A.rec == nullptr):
         // each store instruction covers 512 bytes, whole sectors and lines
         // (per-record 16-byte stores at the record stride are partial-sector
         // writes, which cost L2 read-fills)
-#ifndef DBL_PREP_COALESCED_ALL
-#define DBL_PREP_COALESCED_ALL 0
-#endif
-        if (A.rec && !DBL_PREP_COALESCED_ALL && rs <= 4) {
+        if (A.rec && rs <= 4) {
             // one-sector records: the thread's own two 16-byte stores complete
             // its sector (no partial-sector fills)
-            if (i < A.n) {
+            if (valid) {
                 uint64_t *r = A.rec + i * rs;
                 for (uint32_t w = 0; w < rw; w += 2) {
                     ulonglong2 val;
@@ -335,7 +351,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
             }
         }
         const unsigned b0 = __ballot_sync(FULL, p0), b1 = __ballot_sync(FULL, p1);
-        if ((threadIdx.x & 31) == 0) {
+        if (lane == 0) {
             if (A.bits0) A.bits0[i >> 5] = b0;
             if (A.bits1) A.bits1[i >> 5] = b1;
         }
@@ -351,7 +367,8 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
 // lowest bin that still holds the k-th best score (bins from the histogram;
 // each CTA derives the threshold itself).  Unordered; at most
 // PREP_CAND_CAP are stored, the count is exact.
-__global__ void __launch_bounds__(256) topk_candidates_kernel(const uint64_t *__restrict__ score, uint32_t n,
+__global__ void __launch_bounds__(256) topk_candidates_kernel(const Adj f, const Adj r, int strategy,
+                                                              const uint8_t *__restrict__ bins, uint32_t n,
                                                               uint32_t k, PrepState *st,
                                                               uint64_t *__restrict__ cs, uint32_t *__restrict__ ci) {
     __shared__ int tbin;
@@ -365,25 +382,40 @@ __global__ void __launch_bounds__(256) topk_candidates_kernel(const uint64_t *__
         tbin = bin < 0 ? 0 : bin;
     }
     __syncthreads();
-    const int t = tbin;
-    const uint64_t nr = ((uint64_t)n + 31) & ~31ull;
+    const uint32_t t = (uint32_t)tbin;
     const int lane = threadIdx.x & 31;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t sc = 0;
-        bool take = false;
-        if (i < n) {
-            sc = score[i];
-            take = score_bin(sc) >= t;
+    // 16 bins per thread per step (one 16-byte load); a warp reserves the
+    // slots of all its candidates with one atomicAdd, and a candidate's score
+    // is recomputed from its degrees (there are at most a few thousand)
+    const uint64_t n16 = ((uint64_t)n + 15) / 16, n16r = (n16 + 31) & ~31ull;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n16r; j += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t take = 0;
+        if (j < n16) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4 *>(bins) + j);
+            const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                if (((wv[e >> 2] >> (8 * (e & 3))) & 0xffu) >= t && j * 16 + e < n) take |= 1u << e;
         }
-        const unsigned m = __ballot_sync(FULL, take);
-        if (!m) continue;
+        const uint32_t cnt = __popc(take);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t tot = __shfl_sync(FULL, incl, 31);
+        if (!tot) continue;
         uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&st->n_above, (uint32_t)__popc(m));
-        base = __shfl_sync(FULL, base, 0);
-        const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-        if (take && pos < PREP_CAND_CAP) {
-            cs[pos] = sc;
-            ci[pos] = (uint32_t)i;
+        if (lane == 31) base = atomicAdd(&st->n_above, tot);
+        uint32_t pos = __shfl_sync(FULL, base, 31) + incl - cnt;
+        for (; take; take &= take - 1, ++pos) {
+            if (pos >= PREP_CAND_CAP) break;
+            const uint32_t v = (uint32_t)(j * 16 + __ffs(take) - 1);
+            uint64_t out = f.ptr[v + 1] - f.ptr[v], in = r.ptr[v + 1] - r.ptr[v];
+            if (f.dptr) { out += f.dptr[v + 1] - f.dptr[v]; in += r.dptr[v + 1] - r.dptr[v]; }
+            cs[pos] = strategy_score(strategy, in, out);
+            ci[pos] = v;
         }
     }
 }
@@ -473,8 +505,12 @@ dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_
     if (idx->sel_leaves && idx->cfg.k_prime < 1) { set_error("k_prime must be >= 1"); return DBL_E_CONFIG; }
     dbl_status s;
     const size_t cand_bytes = (size_t)PREP_CAND_CAP * 12;
-    if ((s = g->prep.ensure(sizeof(PrepState) + 16 + cand_bytes))) return s;
+    // the bins need n bytes; the buffer keeps the n x 8 bytes of the former
+    // score array: the pivot sweeps behind this pass measured 26 vs 33 us at
+    // cfg2 with the smaller allocation (a buffer-placement effect on the
+    // later reach buffer, not explained; tools/ab_build.sh)
     if (do_lm && (s = g->scratch_a.ensure((size_t)n * 8 + 64))) return s;
+    if ((s = g->prep.ensure(sizeof(PrepState) + 16 + cand_bytes))) return s;
     PrepState *st = g->prep.as<PrepState>();
     uint64_t *cs = reinterpret_cast<uint64_t *>(g->prep.as<char>() + ((sizeof(PrepState) + 15) & ~15ull));
     uint32_t *ci = reinterpret_cast<uint32_t *>(cs + PREP_CAND_CAP);
@@ -486,10 +522,12 @@ dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_
     A.strategy = idx->cfg.strategy;
     A.do_lm = do_lm;
     A.do_leaves = idx->sel_leaves;
-    A.score = do_lm ? g->scratch_a.as<uint64_t>() : nullptr;
     A.threshold = idx->cfg.leaf_threshold;
     A.k_prime = idx->cfg.k_prime;
     A.seed = idx->cfg.hash_seed;
+    A.kp_magic = A.k_prime ? ~0ull / A.k_prime : 0ull;
+    A.seed_mix = A.seed * 0xD1B54A32D192ED03ull;
+    A.bins = do_lm ? g->scratch_a.as<uint8_t>() : nullptr;
     A.ovr = idx->ovr.p ? idx->ovr.as<uint32_t>() : nullptr;
     A.flags = idx->leaf_flags.as<uint8_t>();
     A.bucket = idx->bucket.as<uint32_t>();
@@ -507,7 +545,7 @@ dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_
     DBL_CHECK_LAUNCH("prep_kernel");
     const uint32_t H = idx->wdl + idx->wbl;
     if (do_lm) {
-        topk_candidates_kernel<<<blocks, 256, 0, g->stream>>>(A.score, n, k, st, cs, ci);
+        topk_candidates_kernel<<<blocks, 256, 0, g->stream>>>(A.f, A.r, A.strategy, A.bins, n, k, st, cs, ci);
         DBL_CHECK_LAUNCH("topk_candidates_kernel");
         const int fsmem = (int)cand_bytes;
         int fbps = 1;
