@@ -44,6 +44,9 @@ namespace cg = cooperative_groups;
 #ifndef DBL_TD_DIV
 #define DBL_TD_DIV 64u           // pivot reach: top-down once a step marks < n / d
 #endif
+#ifndef DBL_COMPACT_SLICES
+#define DBL_COMPACT_SLICES 0     // 1: each warp compacts one contiguous slice of the bitmap
+#endif
 #ifndef DBL_PREP_RECORDS
 #define DBL_PREP_RECORDS 0       // 1: prep writes the seeded records even when the pivot could
 #endif
@@ -394,6 +397,10 @@ __device__ __forceinline__ void pull_range(const DirParams &D, const uint32_t *_
     }
 }
 
+#if DBL_TRACE
+__device__ unsigned long long g_compact_prof[5];   // SM cycles per compaction section, summed over warps
+#endif
+
 // Phase B: turn the direction's next-frontier bitmap into the current
 // frontier (copied to D.cur) and work items, clearing it.  Each warp owns an
 // equal slice of the bitmap; set bits are spread across lanes (32 vertices per
@@ -408,9 +415,25 @@ __device__ __forceinline__ void compact_bitmap(const DirParams &D, uint32_t nwor
 #endif
     constexpr int R = DBL_COMPACT_R;
     const int lane = threadIdx.x & 31;
+#if DBL_COMPACT_SLICES
     const uint32_t per = (nwords + nwarps - 1) / nwarps;
-    const uint32_t w0 = gwarp * per, w1 = min(w0 + per, nwords);
-    for (uint32_t g0 = w0; g0 < w1; g0 += 32) {
+    const uint32_t w0 = gwarp * per, w1 = min(w0 + per, nwords), gstep = 32;
+#else
+    // 32-word groups dealt round-robin over the warps: a frontier whose
+    // density varies along the id range (R-MAT leaves gather in the
+    // high-id, low-degree part) still gives every warp the same share
+    // (contiguous slices: cfg5 level-0 compaction 716 us, mostly warps
+    // waiting at the barrier for the densest slices)
+    const uint32_t w0 = gwarp * 32, w1 = nwords, gstep = nwarps * 32;
+#endif
+#if DBL_TRACE
+    long long tsec[5] = {0, 0, 0, 0, 0};
+    long long tq = clock64();
+#define DBL_TSEC(i) do { const long long tn = clock64(); tsec[i] += tn - tq; tq = tn; } while (0)
+#else
+#define DBL_TSEC(i) do { } while (0)
+#endif
+    for (uint32_t g0 = w0; g0 < w1; g0 += gstep) {
         const uint32_t wi = g0 + lane;
         const uint32_t bits = wi < w1 ? ld_cg32(D.bits + wi) : 0u;
         if (wi < w1) {
@@ -419,6 +442,7 @@ __device__ __forceinline__ void compact_bitmap(const DirParams &D, uint32_t nwor
         }
         uint32_t tot = 0;
         const uint32_t excl = warp_excl_scan_u32(__popc(bits), tot);
+        DBL_TSEC(0);
         for (uint32_t t0 = 0; t0 < tot; t0 += 32 * R) {
             uint32_t ys[R], b0[R], b1[R], d0[R], d1[R];
             bool val[R];
@@ -436,6 +460,7 @@ __device__ __forceinline__ void compact_bitmap(const DirParams &D, uint32_t nwor
                 val[r] = t < tot;
                 ys[r] = val[r] ? (g0 + k) * 32 + select_bit(ob, t - oe) : 0u;
             }
+            DBL_TSEC(1);
             uint32_t ni = 0, ne = 0;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -460,12 +485,14 @@ __device__ __forceinline__ void compact_bitmap(const DirParams &D, uint32_t nwor
                 }
             }
             const uint32_t ii = warp_incl_scan(ni), ei = warp_incl_scan(ne);
+            DBL_TSEC(2);
             const uint32_t ti = __shfl_sync(FULL, ii, 31), te = __shfl_sync(FULL, ei, 31);
             if (ti == 0) continue;
             unsigned long long base = 0;
             if (lane == 31) base = atomicAdd(cnt_ptr, ((unsigned long long)ti << 32) | te);
             base = __shfl_sync(FULL, base, 31);
             const uint32_t ibase = (uint32_t)(base >> 32), ebase = (uint32_t)base;
+            DBL_TSEC(3);
             if ((uint64_t)ibase + ti > D.cap) {
                 if (lane == 0) atomicOr(&ctrl->overflow, 1u);
                 continue;
@@ -485,8 +512,14 @@ __device__ __forceinline__ void compact_bitmap(const DirParams &D, uint32_t nwor
                     eo += d1[r] - d0[r];
                 }
             }
+            DBL_TSEC(4);
         }
     }
+#if DBL_TRACE
+    if (lane == 0)
+        for (int i = 0; i < 5; ++i) atomicAdd(&g_compact_prof[i], (unsigned long long)tsec[i]);
+#endif
+#undef DBL_TSEC
 }
 
 template <int NW, bool VEC>
@@ -525,9 +558,18 @@ __global__ void __launch_bounds__(FIX_THREADS, DBL_FMINB) fixpoint_kernel(FixPar
         const int cb = L & 1;
         stamp_time(2 * L);
         // phase B: next-frontier bitmaps -> current frontier + work items
+        unsigned long long tc0 = 0;
+        if (DBL_TRACE && L == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tc0));
 #pragma unroll
         for (int d = 0; d < 2; ++d)
             if ((P.active >> d) & 1) compact_bitmap<COUNT>(P.d[d], nwords, warp, nwarps, &ctrl->cnt[cb][d], ctrl, nchanged[d]);
+        if (DBL_TRACE && L == 0 && lane == 0) {
+            unsigned long long tc1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tc1));
+            atomicMax(&ctrl->dbg[0], tc1 - tc0);
+            atomicAdd(&ctrl->dbg[1], tc1 - tc0);
+            atomicMax(&ctrl->dbg[3], tc0);
+        }
         grid.sync();
         const unsigned long long q0 = *(volatile unsigned long long *)&ctrl->cnt[cb][0];
         const unsigned long long q1 = *(volatile unsigned long long *)&ctrl->cnt[cb][1];
@@ -648,7 +690,7 @@ __global__ void landmark_bits_kernel(uint64_t *__restrict__ rec, uint32_t rs, ui
 __global__ void leaf_frontier_kernel(uint32_t *__restrict__ bits0, uint32_t *__restrict__ bits1, uint32_t n,
                                      uint32_t wdl, uint32_t H, const uint8_t *__restrict__ flags,
                                      const uint32_t *__restrict__ bucket, uint32_t a0, uint32_t e0, uint32_t a1,
-                                     uint32_t e1) {
+                                     uint32_t e1, const Adj fwd, const Adj rev) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t nr = ((uint64_t)n + 31) & ~31ull;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nr; i += stride) {
@@ -659,6 +701,9 @@ __global__ void leaf_frontier_kernel(uint32_t *__restrict__ bits0, uint32_t *__r
                 const uint32_t bw = wdl + bucket[i] / 64;
                 p0 = (f & 1) && bw >= a0 && bw < e0;
                 p1 = (f & 2) && H + bw >= a1 && H + bw < e1;
+                // only with edges to push along (as in prep_kernel)
+                if (p0) p0 = fwd.ptr[i + 1] > fwd.ptr[i] || (fwd.dptr && fwd.dptr[i + 1] > fwd.dptr[i]);
+                if (p1) p1 = rev.ptr[i + 1] > rev.ptr[i] || (rev.dptr && rev.dptr[i + 1] > rev.dptr[i]);
             }
         }
         const unsigned b0 = __ballot_sync(FULL, p0), b1 = __ballot_sync(FULL, p1);
@@ -778,7 +823,8 @@ static dbl_status launch_init_frontier(dbl_graph *g, dbl_index *idx, const Group
     if (blocks > g->sm_count * 8) blocks = g->sm_count * 8;
     if (blocks < 1) blocks = 1;
     leaf_frontier_kernel<<<blocks, 256, 0, g->stream>>>(b0, b1, g->n, idx->wdl, H, idx->leaf_flags.as<uint8_t>(),
-                                                         idx->bucket.as<uint32_t>(), a0, e0, a1, e1);
+                                                         idx->bucket.as<uint32_t>(), a0, e0, a1, e1, graph_fwd(g),
+                                                         graph_rev(g));
     DBL_CHECK_LAUNCH("leaf_frontier_kernel");
     if (idx->cfg.k) {
         landmark_frontier_kernel<<<(idx->cfg.k + 255) / 256, 256, 0, g->stream>>>(
@@ -1686,7 +1732,19 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
             idx->sel_landmarks = false;
         }
         if (DBL_TRACE) {
-            std::fprintf(stderr, "[dbl] fixpoint levels=%u nw=%u\n", h.levels, nw);
+#if DBL_TRACE
+            {
+                unsigned long long cp[5] = {0, 0, 0, 0, 0};
+                cudaMemcpyFromSymbol(cp, g_compact_prof, sizeof(cp));
+                unsigned long long z[5] = {0, 0, 0, 0, 0};
+                cudaMemcpyToSymbol(g_compact_prof, z, sizeof(z));
+                const double tot = (double)(cp[0] + cp[1] + cp[2] + cp[3] + cp[4]) + 1;
+                std::fprintf(stderr, "[dbl] compaction cycles (all levels): bits+scan %.0f%%, select %.0f%%, row ptrs %.0f%%, reserve %.0f%%, stores %.0f%%  (%.3g warp-cycles)\n",
+                             100 * cp[0] / tot, 100 * cp[1] / tot, 100 * cp[2] / tot, 100 * cp[3] / tot, 100 * cp[4] / tot, tot);
+            }
+#endif
+            std::fprintf(stderr, "[dbl] fixpoint levels=%u nw=%u  level-0 compaction per warp: max %.1f us, mean %.1f us, last start %.1f us after level start\n",
+                         h.levels, nw, h.dbg[0] / 1e3, h.dbg[1] / 1e3 / (g->sm_count * 8.0 * 4), (h.dbg[3] - h.level_t[0]) / 1e3);
             for (uint32_t l = 0; l < h.levels && l < 31; ++l)
                 std::fprintf(stderr, "[dbl]   level %2u items %9llu edges %10llu pull %llu compact %7.1f us  relax %7.1f us\n",
                              l, h.level_items[l] & ((1ull << 60) - 1), h.level_edges[l], h.level_items[l] >> 60,

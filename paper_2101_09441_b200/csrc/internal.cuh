@@ -190,6 +190,7 @@ struct Ctrl {
     unsigned long long level_edges[32];  // edges expanded per level (first 32 levels, both directions)
     unsigned long long level_items[32];
     unsigned long long level_t[64];       // globaltimer at each phase boundary (block 0)
+    unsigned long long dbg[4];            // trace builds: level-0 compaction per warp (max, sum, min, start spread)
 };
 
 // One direction of a fixpoint: label words [lab + v*stride, +nw) propagate

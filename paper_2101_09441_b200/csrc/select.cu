@@ -240,9 +240,13 @@ struct PrepArgs {
     PrepState *st;
 };
 
+// LM: landmark scores + histogram; LV: leaf selection (else the flags and
+// buckets are read); DL: the graph has delta adjacency.  Warp-uniform
+// switches as template parameters: the pass is issue-bound, not HBM-bound.
+template <bool LM, bool LV, bool DL>
 __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
     __shared__ uint32_t h[65];
-    if (A.do_lm) {
+    if (LM) {
         for (int i = threadIdx.x; i < 65; i += blockDim.x) h[i] = 0;
         __syncthreads();
     }
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
     // A warp takes 32 consecutive vertices per step; each lane loads row
     // pointer i and takes i + 1 from its neighbour (lane 31 loads it), and
     // the next step's pointers load while this step is processed.
-    const bool degs = A.do_lm || A.do_leaves;
+    constexpr bool degs = LM || LV;
     const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     uint32_t nf0 = 0, nf1 = 0, nr0 = 0, nr1 = 0;
     auto fetch = [&](uint64_t i) {
@@ -268,15 +272,17 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
     for (uint64_t i = i0; i < nr; i += stride) {
         const bool valid = i < A.n;
         const uint32_t v = (uint32_t)i;
-        uint32_t cf0 = nf0, cf1 = __shfl_down_sync(FULL, nf0, 1), cr0 = nr0, cr1 = __shfl_down_sync(FULL, nr0, 1);
-        if (lane == 31) { cf1 = nf1; cr1 = nr1; }
-        if (degs && i + stride < nr) fetch(i + stride);
         uint8_t f = 0;
         uint32_t b = 0;
+        uint32_t out = 1, in = 1;   // (unknown without degs: every leaf joins the frontier)
         if (degs) {
-            uint64_t out = cf1 - cf0, in = cr1 - cr0;
-            if (A.f.dptr && valid) { out += A.f.dptr[v + 1] - A.f.dptr[v]; in += A.r.dptr[v + 1] - A.r.dptr[v]; }
-            if (A.do_lm) {
+            uint32_t cf1 = __shfl_down_sync(FULL, nf0, 1), cr1 = __shfl_down_sync(FULL, nr0, 1);
+            if (lane == 31) { cf1 = nf1; cr1 = nr1; }
+            out = cf1 - nf0;
+            in = cr1 - nr0;
+            if (i + stride < nr) fetch(i + stride);
+            if (DL && valid) { out += A.f.dptr[v + 1] - A.f.dptr[v]; in += A.r.dptr[v + 1] - A.r.dptr[v]; }
+            if (LM) {
                 // bin 0 (a degree-0 end: ~70% of R-MAT vertices) counted by
                 // one ballot; the other lanes aggregate per bin
                 const int bin = valid ? score_bin(strategy_score(A.strategy, in, out)) : 0;
@@ -289,10 +295,9 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
                     if (lane == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
                 }
             }
-            if (A.do_leaves && valid) {
-                if (in == 0) f |= 1;
-                if (out == 0) f |= 2;
-                if (A.threshold > 0 && in * out <= A.threshold) f |= 3;
+            if (LV && valid) {
+                f = (in == 0 ? 1 : 0) | (out == 0 ? 2 : 0);
+                if (A.threshold > 0 && (uint64_t)in * out <= A.threshold) f = 3;
                 if (f) {
                     const uint32_t o = A.ovr ? A.ovr[v] : 0xffffffffu;
                     if (o != 0xffffffffu) {
@@ -306,7 +311,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
                 A.bucket[v] = b;
             }
         }
-        if (!A.do_leaves && valid) {
+        if (!LV && valid) {
             f = A.flags[v];
             b = A.bucket[v];
         }
@@ -315,8 +320,11 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
         const uint32_t win = (f & 1) ? bw : 0xffffffffu;
         const uint32_t wout = (f & 2) ? H + bw : 0xffffffffu;
         const uint64_t bit = 1ull << (b % 64);
-        const bool p0 = (f & 1) && bw >= A.a0 && bw < A.e0;
-        const bool p1 = (f & 2) && H + bw >= A.a1 && H + bw < A.e1;
+        // a leaf joins the level-0 frontier of a direction only if it has
+        // edges to push along (R-MAT: 57% of the vertices are source leaves,
+        // 10% have out-edges; the rest would only cost compaction work)
+        const bool p0 = (f & 1) && out > 0 && bw >= A.a0 && bw < A.e0;
+        const bool p1 = (f & 2) && in > 0 && H + bw >= A.a1 && H + bw < A.e1;
         // the warp's 32 records (pad words included) as one contiguous block
         // (skipped when the pivot pass writes the records: A.rec == nullptr):
         // each store instruction covers 512 bytes, whole sectors and lines
@@ -356,7 +364,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
             if (A.bits1) A.bits1[i >> 5] = b1;
         }
     }
-    if (A.do_lm) {
+    if (LM) {
         __syncthreads();
         for (int i = threadIdx.x; i < 65; i += blockDim.x)
             if (h[i]) atomicAdd(&A.st->hist[i], h[i]);
@@ -541,8 +549,15 @@ dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_
     int blocks = (int)(((uint64_t)n + 255) / 256);
     if (blocks > g->sm_count * 8) blocks = g->sm_count * 8;
     if (blocks < 1) blocks = 1;
-    prep_kernel<<<blocks, 256, 0, g->stream>>>(A);
-    DBL_CHECK_LAUNCH("prep_kernel");
+    {
+        const int sel = (A.do_lm ? 4 : 0) | (A.do_leaves ? 2 : 0) | (A.f.dptr ? 1 : 0);
+        void (*kerns[8])(const PrepArgs) = {prep_kernel<false, false, false>, prep_kernel<false, false, true>,
+                                            prep_kernel<false, true, false>,  prep_kernel<false, true, true>,
+                                            prep_kernel<true, false, false>,  prep_kernel<true, false, true>,
+                                            prep_kernel<true, true, false>,   prep_kernel<true, true, true>};
+        kerns[sel]<<<blocks, 256, 0, g->stream>>>(A);
+        DBL_CHECK_LAUNCH("prep_kernel");
+    }
     const uint32_t H = idx->wdl + idx->wbl;
     if (do_lm) {
         topk_candidates_kernel<<<blocks, 256, 0, g->stream>>>(A.f, A.r, A.strategy, A.bins, n, k, st, cs, ci);
