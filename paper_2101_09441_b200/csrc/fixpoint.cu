@@ -1043,7 +1043,7 @@ __device__ __forceinline__ bool any_marked(const Adj &a, const uint32_t *vis, ui
 // for strides dividing 64 words (more registers: used by the stand-alone
 // apply kernel; the fused small-graph variant inside reach_kernel keeps the
 // general loop and the sweeps' register budget).
-template <bool WORK, bool FAST>
+template <bool WORK, int FAST>
 __device__ __forceinline__ void apply_head_start(const ReachParams &P, uint64_t tid, uint64_t nth,
                                                  const unsigned long long *acc, bool drop, bool capped) {
     const uint32_t H = P.H, rw = 2 * H, rs = rec_stride(H);
@@ -1076,7 +1076,54 @@ __device__ __forceinline__ void apply_head_start(const ReachParams &P, uint64_t 
         // lane's first (record, word) in a block and the step per 64 words,
         // so the store loop needs no division by the runtime stride
         const uint32_t r0 = (2 * lane) / rs, w0 = (2 * lane) % rs, q64 = 64 / rs, m64 = 64 % rs;
-        if (FAST && P.write_rec && m64 == 0) {
+        if (FAST == 2 && P.write_rec) {
+            // write mode, stride dividing 128 words (k <= 960 at k' = 64):
+            // 32-byte stores (a warp instruction covers 1 KB, 128 / rs
+            // records); a lane's 4 words w..w+3 are the same in every store,
+            // so its union words are fixed; the next block's bitmap words,
+            // flags and buckets load while this block's records are stored
+            const uint32_t w = (4 * lane) % rs, rq0 = (4 * lane) / rs, q = 128 / rs;
+            uint64_t Aw[4];
+            bool hw[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                Aw[j] = w + j < rw ? acc[w + j] : 0ull;
+                hw[j] = w + j < H;
+            }
+            uint32_t fb = 0, bb = 0, f = 0, b = 0;
+            auto fetch = [&](uint64_t blk) {
+                fb = drop ? 0u : P.vis[0][blk];
+                bb = drop ? 0u : P.vis[1][blk];
+                const uint64_t v = blk * 32 + lane;
+                f = v < P.n ? P.flags[v] : 0u;
+                b = v < P.n ? P.bucket[v] : 0u;
+            };
+            if (gw < nblk) fetch(gw);
+            for (uint64_t blk = gw; blk < nblk; blk += nw) {
+                const uint32_t cfb = fb, cbb = bb, cf = f, cbk = b;
+                if (blk + nw < nblk) fetch(blk + nw);
+                if (WORK && lane == 0) touched += __popc(cfb | cbb);
+                const uint32_t sb = cbk % 64;
+                const uint32_t win = (cf & 1) ? wdl + cbk / 64 : 0xffffffffu;
+                const uint32_t wout = (cf & 2) ? H + wdl + cbk / 64 : 0xffffffffu;
+                uint64_t *base = P.rec + blk * 32 * rs;
+                uint32_t r = rq0;
+                for (uint32_t t = 0; t < rs * 32; t += 128, r += q) {
+                    const uint32_t swin = __shfl_sync(FULL, win, r), swout = __shfl_sync(FULL, wout, r);
+                    const uint64_t sbit = 1ull << __shfl_sync(FULL, sb, r);
+                    const bool in_d = (cfb >> r) & 1u, in_a = (cbb >> r) & 1u;
+                    if (blk * 32 + r >= P.n) continue;
+                    uint64_t val[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        val[j] = ((hw[j] ? in_d : in_a) ? Aw[j] : 0ull) |
+                                 ((w + j == swin || w + j == swout) ? sbit : 0ull);
+                    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(base + t + 4 * lane), "l"(val[0]),
+                                 "l"(val[1]), "l"(val[2]), "l"(val[3])
+                                 : "memory");
+                }
+            }
+        } else if (FAST == 1 && P.write_rec && m64 == 0) {
             // write mode, stride dividing 64 words (every stride up to
             // k = 448): a lane's word pair w0 is the same in every store, so
             // its union words are fixed; the next block's bitmap words, flags
@@ -1448,7 +1495,7 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
     grid.sync();
     for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = *(volatile unsigned long long *)&P.L[i];
     __syncthreads();
-    apply_head_start<WORK, false>(P, tid, nth, acc, drop, capped);
+    apply_head_start<WORK, 0>(P, tid, nth, acc, drop, capped);
     if (P.write_rec) {   // landmark i seeds bit i of both DL halves (labels.py:291-293)
         grid.sync();
         for (uint64_t i = tid; i < P.k; i += nth) {
@@ -1463,7 +1510,7 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
 
 // Apply the head start (after reach_kernel; a plain launch at full occupancy,
 // no grid barrier: the records stream out at HBM write rate).
-template <bool WORK>
+template <bool WORK, int MODE>
 __global__ void __launch_bounds__(256) reach_apply_kernel(ReachParams P) {
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
@@ -1476,7 +1523,7 @@ __global__ void __launch_bounds__(256) reach_apply_kernel(ReachParams P) {
     const uint32_t H = P.H, rw = 2 * H, rs = rec_stride(H);
     for (uint32_t i = threadIdx.x; i < rw; i += blockDim.x) acc[i] = drop ? 0ull : P.L[i];
     __syncthreads();
-    apply_head_start<WORK, true>(P, tid, nth, acc, drop, capped);
+    apply_head_start<WORK, MODE>(P, tid, nth, acc, drop, capped);
     if (!P.write_rec) return;
     // landmark i seeds bit i of both DL halves (labels.py:291-293) once every
     // record is written whole: the last CTA to finish ORs them in
@@ -1583,16 +1630,18 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     DBL_LAUNCHED();
     if (!R.fused_apply) {
         // one resident wave (grid-stride over the 32-vertex blocks)
-        const void *ak = wk ? (const void *)reach_apply_kernel<true> : (const void *)reach_apply_kernel<false>;
+        // write mode with a stride dividing 128 words: 32-byte stores (own
+        // kernel: the path's extra registers cost the 16-byte path occupancy)
+        const bool v32 = write_rec && idx->rs >= 8 && 128 % idx->rs == 0;
+        const void *ak = wk ? (v32 ? (const void *)reach_apply_kernel<true, 2> : (const void *)reach_apply_kernel<true, 1>)
+                            : (v32 ? (const void *)reach_apply_kernel<false, 2> : (const void *)reach_apply_kernel<false, 1>);
         int abps = 1;
         if ((s = kernel_occupancy(ak, 256, 0, &abps))) return s;
         const uint64_t blocks_needed = ((uint64_t)bmw * 32 + 255) / 256;
         const uint64_t full = (uint64_t)g->sm_count * abps;
         const int ag = (int)(blocks_needed < full ? (blocks_needed ? blocks_needed : 1) : full);
-        if (wk)
-            reach_apply_kernel<true><<<ag, 256, 0, g->stream>>>(R);
-        else
-            reach_apply_kernel<false><<<ag, 256, 0, g->stream>>>(R);
+        void *aargs[] = {(void *)&R};
+        DBL_CUDA(cudaLaunchKernel(ak, dim3(ag), dim3(256), aargs, 0, g->stream));
         DBL_CHECK_LAUNCH("reach_apply_kernel");
     }
     if (DBL_TRACE) {
