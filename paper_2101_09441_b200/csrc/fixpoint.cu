@@ -1005,6 +1005,8 @@ struct ReachParams {
     bool write_rec;          // records not seeded yet (full build): write seeds | head start, whole lines
     uint32_t n, nwords;
     uint32_t kp;             // k_prime (bucket bits per BL half)
+    const uint32_t *haspred[2];   // vertices with a predecessor along adj[d] (prep), or nullptr
+    uint32_t sparse_g;            // bitmap words per warp step in the sparse sweeps (power of 2, <= 32)
     bool fused_apply;        // apply the head start inside reach_kernel (small graphs)
 };
 
@@ -1267,7 +1269,55 @@ __global__ void __launch_bounds__(256, MINB) reach_kernel(ReachParams P) {
         }
         const int cb = step % 3;
         unsigned marks = 0;
-        if (!td) {
+        if (!td && bu > 0 && P.haspred[0]) {
+            // later bottom-up sweeps: only the vertices still unmarked that
+            // have a predecessor at all (cfg2 after the first sweep: ~170k of
+            // the 1.3M unmarked vertex-directions), picked from the bitmaps
+            // 32 words per warp step and spread over the lanes
+            const int lane = threadIdx.x & 31;
+#pragma unroll 1
+            for (int d = 0; d < 2; ++d) {
+                const Adj &a = P.adj[d];
+                // G words per warp step (host: enough groups for every warp)
+                const uint32_t G = P.sparse_g;
+                for (uint64_t g0 = (tid >> 5) * G; g0 < P.nwords; g0 += (nth >> 5) * G) {
+                    const uint64_t wi = g0 + lane;
+                    const uint32_t cand =
+                        lane < G && wi < P.nwords ? ~*(volatile uint32_t *)&P.vis[d][wi] & P.haspred[d][wi] : 0u;
+                    uint32_t tot = 0;
+                    const uint32_t excl = warp_excl_scan_u32(__popc(cand), tot);
+                    for (uint32_t t0 = 0; t0 < tot; t0 += 32) {
+                        const uint32_t t = t0 + lane;
+                        int k = 0;
+#pragma unroll
+                        for (int st = 16; st >= 1; st >>= 1) {
+                            const uint32_t v = __shfl_sync(FULL, excl, (k + st) & 31);
+                            if (k + st < 32 && v <= t) k += st;
+                        }
+                        const uint32_t ob = __shfl_sync(FULL, cand, k), oe = __shfl_sync(FULL, excl, k);
+                        if (t >= tot) continue;
+                        const uint32_t x = (uint32_t)(g0 + k) * 32 + select_bit(ob, t - oe);
+                        if (WORK) ++w_tests;
+                        bool hit = false;
+                        uint32_t s0 = __ldg(a.ptr + x), s1 = __ldg(a.ptr + x + 1), j = s0;
+                        for (; j < s1 && !hit; ++j) hit = vis_test_ca(P.vis[d], __ldg(a.col + j));
+                        if (WORK) w_probes += j - s0;
+                        if (!hit && a.dptr) {
+                            s0 = __ldg(a.dptr + x);
+                            s1 = __ldg(a.dptr + x + 1);
+                            for (j = s0; j < s1 && !hit; ++j) hit = vis_test_ca(P.vis[d], __ldg(a.dcol + j));
+                            if (WORK) w_probes += j - s0;
+                        }
+                        if (hit) {
+                            atomicOr(&P.vis[d][x >> 5], 1u << (x & 31));
+                            atomicOr(&P.nb[d][cb][x >> 5], 1u << (x & 31));
+                            ++marks;
+                        }
+                    }
+                }
+            }
+            ++bu;
+        } else if (!td) {
 #if DBL_BU_ILP
             // two vertices x both directions per iteration: the four
             // dependent chains (bitmap word -> row pointers -> first
@@ -1549,7 +1599,8 @@ static bool pivot_on() { return !DBL_NO_PIVOT; }
 
 // Head start from the pivot's reachability (all record words; after prep).
 static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask, uint32_t *front0,
-                                   uint32_t *front1, uint64_t cap_wmask, bool write_rec) {
+                                   uint32_t *front1, uint64_t cap_wmask, bool write_rec,
+                                   const uint32_t *haspred = nullptr) {
     const uint32_t n = g->n, H = idx->wdl + idx->wbl;
     const size_t bmw = ((size_t)n + 31) / 32;
     const size_t bbytes = ((bmw * 4 + 255) / 256) * 256;
@@ -1570,6 +1621,8 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
     R.front[1] = front1;
     R.k = idx->cfg.k;
     R.kp = idx->cfg.k_prime;
+    R.haspred[0] = haspred;
+    R.haspred[1] = haspred ? haspred + bmw : nullptr;
     R.wdl = idx->wdl;
     R.dmask_out = nullptr;
     R.scc_out = nullptr;
@@ -1621,6 +1674,12 @@ static dbl_status pivot_head_start(dbl_graph *g, dbl_index *idx, uint64_t wmask,
                            : (wk ? (const void *)reach_kernel<6, true> : (const void *)reach_kernel<6, false>);
     int bps = 1;
     if ((s = kernel_occupancy(kern, 256, 0, &bps))) return s;
+    {   // at least ~2 word groups per warp and direction (cfg2: 4 words, cfg5: 32)
+        const uint64_t warps = (uint64_t)g->sm_count * bps * 8;
+        uint32_t gsz = 32;
+        while (gsz > 1 && (uint64_t)bmw < warps * gsz * 2) gsz >>= 1;
+        R.sparse_g = gsz;
+    }
     // the records stream out faster from a separate full-occupancy kernel
     // once they are large (cfg5: 1.64 vs ~2.2 ms); a small graph's apply is
     // cheaper than a launch (cfg2: ~14 us either way)
@@ -1710,12 +1769,19 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
     g->last_build.flags = (prep && !pivot_writes ? 1u : 0u) | (pivot_writes ? 2u : 0u) |
                           (pivot && !pivot_writes ? 4u : 0u) | (prep ? 0u : 16u);
     g->last_build.rs = idx->rs;
+    bool haspred_ok = false;
     if (prep) {
         const Group **p0 = pairs[0];
         uint32_t *b0 = p0[0] ? g->stamp[0].as<uint32_t>() : nullptr;
         uint32_t *b1 = p0[1] ? g->stamp[1].as<uint32_t>() : nullptr;
+        // has-predecessor bitmaps for the sparse later sweeps: they pay from
+        // 2^21 vertices on (2^24: 1.32 -> 1.22 ms per build, cfg5 5.51 ->
+        // 5.07 ms); on cfg2 the dense sweep is faster (13.4 vs 15.4 us)
+        const bool want_hp = pivot && g->n >= (1u << 21);
+        if (want_hp && (s = g->haspred.ensure((((size_t)g->n + 31) / 32) * 8 + 64))) return s;
         if ((s = prep_build_dev(g, idx, b0, b1, p0[0] ? p0[0]->w0 : 0, p0[0] ? p0[0]->w0 + p0[0]->nw : 0,
-                                p0[1] ? p0[1]->w0 : 0, p0[1] ? p0[1]->w0 + p0[1]->nw : 0, !pivot_writes)))
+                                p0[1] ? p0[1]->w0 : 0, p0[1] ? p0[1]->w0 + p0[1]->nw : 0, !pivot_writes,
+                                want_hp ? g->haspred.as<uint32_t>() : nullptr, &haspred_ok)))
             return s;
     } else {
         uint64_t wmask = 0;
@@ -1740,7 +1806,9 @@ dbl_status run_build(dbl_graph *g, dbl_index *idx, const uint32_t *words, uint32
                 if (pairs[0][d])
                     for (uint32_t w = pairs[0][d]->w0; w < pairs[0][d]->w0 + pairs[0][d]->nw; ++w) cap_wmask |= 1ull << w;
         }
-        if ((s = pivot_head_start(g, idx, wmask, f0, f1, cap_wmask, pivot_writes))) return s;
+        if ((s = pivot_head_start(g, idx, wmask, f0, f1, cap_wmask, pivot_writes,
+                                  haspred_ok ? g->haspred.as<uint32_t>() : nullptr)))
+            return s;
         // (the capped case needs both bitmaps; with a one-direction first
         // group the kernel drops the head start instead)
         trace("build: pivot head start", g->stream);

@@ -560,7 +560,7 @@ extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
                       &g->drcol, &g->dkeys_f, &g->dkeys_r, &g->dmerge, &g->stamp[0], &g->stamp[1],
                       &g->qbuf[0][0], &g->qbuf[0][1], &g->qbuf[1][0], &g->qbuf[1][1], &g->ctrl,
                       &g->changed_bits, &g->cub_tmp, &g->scratch_a, &g->scratch_b, &g->scratch_c,
-                      &g->scratch_d, &g->prep, &g->q_in, &g->q_codes, &g->q_vis, &g->q_pending,
+                      &g->scratch_d, &g->prep, &g->haspred, &g->q_in, &g->q_codes, &g->q_vis, &g->q_pending,
                       &g->q_counters, &g->q_dense};
     set_stream(nullptr);
     for (auto *b : bufs) b->release();

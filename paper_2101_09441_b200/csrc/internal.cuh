@@ -235,6 +235,7 @@ struct dbl_graph {
     dbl::DevBuf qbuf[2][2];   // [direction][0] work-item queue storage
     uint32_t qcap = 0;
     dbl::DevBuf ctrl;
+    dbl::DevBuf haspred;      // build: per direction, vertices with predecessors (prep -> pivot sweeps)
     dbl::DevBuf reach;        // pivot reachability: n x {from pivot, to pivot} u64 + 2 bitmaps + unions
     unsigned long long *reach_work = nullptr;   // the last pivot pass's work counters (in `reach`)
     unsigned int *reach_chg = nullptr;          // its step words: [3] capped, [4] steps, [5] sweeps
@@ -340,7 +341,7 @@ dbl_status leaf_hash_dev(const uint64_t *ids, uint64_t count, uint32_t k_prime, 
 // then the landmark top-k runs on the device and ORs the landmark bits into
 // the records and the bitmaps.  No host synchronisation.
 dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_t *bits1, uint32_t a0,
-                          uint32_t e0, uint32_t a1, uint32_t e1, bool write_rec = true);
+                          uint32_t e0, uint32_t a1, uint32_t e1, bool write_rec = true, uint32_t *haspred = nullptr, bool *haspred_written = nullptr);
 // Enqueue the D2H copy of the prep state (read after the build's sync):
 // err = bucket override outside [0, k'); fallback = the device top-k
 // overflowed its candidate table (the caller re-selects and rebuilds).

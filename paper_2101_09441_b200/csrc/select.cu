@@ -230,6 +230,7 @@ struct PrepArgs {
     uint64_t seed;
     uint64_t kp_magic, seed_mix;   // leaf_hash_magic constants
     uint8_t *bins;                 // score bin per vertex (landmark candidates)
+    uint32_t *hp0, *hp1;           // has-predecessor bitmaps (in-degree > 0, out-degree > 0), or nullptr
     const uint32_t *ovr;
     uint8_t *flags;
     uint32_t *bucket;
@@ -359,9 +360,18 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs A) {
             }
         }
         const unsigned b0 = __ballot_sync(FULL, p0), b1 = __ballot_sync(FULL, p1);
+        unsigned h0 = 0, h1 = 0;
+        if (degs) {
+            h0 = __ballot_sync(FULL, valid && in > 0);
+            h1 = __ballot_sync(FULL, valid && out > 0);
+        }
         if (lane == 0) {
             if (A.bits0) A.bits0[i >> 5] = b0;
             if (A.bits1) A.bits1[i >> 5] = b1;
+            if (degs && A.hp0) {
+                A.hp0[i >> 5] = h0;
+                A.hp1[i >> 5] = h1;
+            }
         }
     }
     if (LM) {
@@ -506,7 +516,8 @@ __global__ void landmark_seed_kernel(const uint32_t *__restrict__ lm, uint32_t k
 }
 
 dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_t *bits1, uint32_t a0,
-                          uint32_t e0, uint32_t a1, uint32_t e1, bool write_rec) {
+                          uint32_t e0, uint32_t a1, uint32_t e1, bool write_rec, uint32_t *haspred,
+                          bool *haspred_written) {
     const uint32_t n = g->n, k = idx->cfg.k;
     const bool do_lm = idx->sel_landmarks && k > 0;
     if (k > n) { set_error("k exceeds vertex count"); return DBL_E_CONFIG; }
@@ -536,6 +547,10 @@ dbl_status prep_build_dev(dbl_graph *g, dbl_index *idx, uint32_t *bits0, uint32_
     A.kp_magic = A.k_prime ? ~0ull / A.k_prime : 0ull;
     A.seed_mix = A.seed * 0xD1B54A32D192ED03ull;
     A.bins = do_lm ? g->scratch_a.as<uint8_t>() : nullptr;
+    const bool degs = do_lm || idx->sel_leaves;
+    A.hp0 = degs ? haspred : nullptr;
+    A.hp1 = degs && haspred ? haspred + (n + 31) / 32 : nullptr;
+    if (haspred_written) *haspred_written = A.hp0 != nullptr;
     A.ovr = idx->ovr.p ? idx->ovr.as<uint32_t>() : nullptr;
     A.flags = idx->leaf_flags.as<uint8_t>();
     A.bucket = idx->bucket.as<uint32_t>();

@@ -272,6 +272,23 @@ def test_rmat_build_and_queries_vs_oracle(scale, ef):
         np.testing.assert_array_equal(out.visited == 0, ov == 0)
 
 
+@pytest.mark.parametrize("k", [64, 256])
+def test_large_graph_build_paths_vs_oracle(k):
+    """2^21 vertices: the build paths that only large graphs take -- the
+    has-predecessor bitmaps and sparse later pivot sweeps (n >= 2^21), the
+    stand-alone record-apply kernel (records >= 256 MB at k = 256: 32-byte
+    stores) -- against the oracle's labels, and against a rebuild (frozen
+    metadata: dense sweeps, no prep degrees)."""
+    n, src, dst = rmat_case(21, 4, 21)
+    g = E.DynamicGraph.from_edges(n, src, dst)
+    og = O.OracleGraph(n, src, dst)
+    idx = E.build_index(g, E.IndexConfig(k=k, k_prime=64))
+    oidx = og.build(k, 64, threads=16)
+    np.testing.assert_array_equal(np.array(idx.landmark_set.landmarks), oidx.landmarks)
+    assert_labels_equal_oracle(idx, oidx)
+    assert idx.labels_equal(E.rebuild_index(g, idx))
+
+
 def test_rmat_insert_batches_vs_rebuild():
     n, src, dst = rmat_case(16, 8, 11)
     g = E.DynamicGraph.from_edges(n, src, dst)
