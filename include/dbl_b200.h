@@ -198,7 +198,7 @@ dbl_status dbl_label_tests(const dbl_index *idx, const uint32_t *x, const uint32
 /* Device pointer to the AoS record table and its record stride in words:
  * record v starts at word v * stride and holds dl_in|bl_in|dl_out|bl_out
  * (2*(ceil(k/64)+ceil(k'/64)) words; records wider than 32 bytes are padded
- * with zero words to 64 or a multiple of 128 bytes), for zero-copy
+ * to 64 or a multiple of 128 bytes, pad words unspecified), for zero-copy
  * consumers. */
 dbl_status dbl_index_records(const dbl_index *idx, uint64_t **dev_records,
                              uint32_t *words_per_record);

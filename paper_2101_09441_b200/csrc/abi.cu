@@ -245,12 +245,13 @@ __global__ void scatter_family_kernel(uint64_t *__restrict__ rec, uint32_t rs, u
         rec[(i / w) * rs + off + i % w] = in[i];
 }
 
+// label words only: a record's pad words past 2H are unspecified
 __global__ void diff_kernel(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b, uint64_t count,
-                            unsigned long long *out) {
+                            uint32_t rs, uint32_t rw, unsigned long long *out) {
     unsigned long long c = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
          i += (uint64_t)gridDim.x * blockDim.x)
-        c |= a[i] != b[i];
+        c |= (i % rs < rw) && a[i] != b[i];
     if (__any_sync(FULL, c) && (threadIdx.x & 31) == 0) atomicOr(out, 1ull);
 }
 
@@ -524,8 +525,8 @@ extern "C" dbl_status dbl_index_equal(const dbl_index *a, const dbl_index *b, in
     cudaMemset(flag.p, 0, 8);
     const uint64_t cnt = (uint64_t)a->n * a->rs;
     if (cnt) {
-        diff_kernel<<<grid_for(cnt), 256>>>(a->rec.as<uint64_t>(), b->rec.as<uint64_t>(), cnt,
-                                            flag.as<unsigned long long>());
+        diff_kernel<<<grid_for(cnt), 256>>>(a->rec.as<uint64_t>(), b->rec.as<uint64_t>(), cnt, a->rs,
+                                            2 * (a->wdl + a->wbl), flag.as<unsigned long long>());
         DBL_LAUNCHED();
     }
     unsigned long long h = 1;

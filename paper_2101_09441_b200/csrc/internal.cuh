@@ -282,7 +282,7 @@ struct dbl_index {
     uint32_t n = 0;
     dbl_config cfg{};
     uint32_t wdl = 0, wbl = 0, rw = 0;  // words: dl, bl, per record (2H)
-    uint32_t rs = 0;                     // record stride in words (rec_stride(H) >= rw; pad words stay 0)
+    uint32_t rs = 0;                     // record stride in words (rec_stride(H) >= rw; pad words unspecified)
     dbl::DevBuf rec;                     // n * rs u64
     dbl::DevBuf landmarks;               // k u32
     dbl::DevBuf leaf_flags;              // n u8

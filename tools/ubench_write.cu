@@ -24,6 +24,18 @@ __global__ void st32(uint64_t *p, size_t n32) {
     }
 }
 
+// 32-byte stores covering only the first 3 sectors of every 128-byte line
+// (records of 80 bytes at a 128-byte stride with the pad sector skipped)
+__global__ void st32_skip(uint64_t *p, size_t n32) {
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x, s = (size_t)gridDim.x * blockDim.x;
+    for (; i < n32; i += s) {
+        if ((i & 3) == 3) continue;
+        uint64_t *q = p + 4 * i;
+        asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(q), "l"((uint64_t)i), "l"(0ull), "l"(0ull),
+                     "l"(0ull) : "memory");
+    }
+}
+
 // the apply pattern: a warp per 32-vertex block; read vis word + 32 flag
 // bytes, then 8 x 512-byte stores of the block's 32 x 128-byte records
 template <bool CS>
@@ -86,6 +98,8 @@ int main() {
         rep(name, gb, [&] { st16<<<sms * per, 256>>>((uint4 *)rec, bytes / 16); });
         snprintf(name, sizeof name, "st32 grid %d x 256", sms * per);
         rep(name, gb, [&] { st32<<<sms * per, 256>>>(rec, bytes / 32); });
+        snprintf(name, sizeof name, "st32 3-of-4 sectors grid %d x 256", sms * per);
+        rep(name, gb, [&] { st32_skip<<<sms * per, 256>>>(rec, bytes / 32); });
         snprintf(name, sizeof name, "apply-like grid %d x 256", sms * per);
         rep(name, gb, [&] { apply_like<false><<<sms * per, 256>>>(rec, vis, flags, n, 7); });
         snprintf(name, sizeof name, "apply-like .cs grid %d x 256", sms * per);
