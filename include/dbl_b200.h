@@ -199,9 +199,19 @@ dbl_status dbl_label_tests(const dbl_index *idx, const uint32_t *x, const uint32
  * record v starts at word v * stride and holds dl_in|bl_in|dl_out|bl_out
  * (2*(ceil(k/64)+ceil(k'/64)) words; records wider than 32 bytes are padded
  * to 64 or a multiple of 128 bytes, pad words unspecified), for zero-copy
- * consumers. */
+ * consumers.  Read-only: the index keeps derived state (the query digest)
+ * that only its own entry points keep in step with the records. */
 dbl_status dbl_index_records(const dbl_index *idx, uint64_t **dev_records,
                              uint32_t *words_per_record);
+
+/* Query digest (no reference counterpart: derived state of this engine):
+ * out[x] (n u32, host) summarises x's labels -- bit 0/1: dl_out has
+ * landmark 0 / any other landmark, bit 2/3: the same for dl_in, bits 4..17 /
+ * 18..31: bl_in / bl_out with bucket b folded onto bit (b % 64) % 14.  Query
+ * batches decide a pair from the two digests when they prove rule 1 or rule
+ * 2 of queries.py:102-108 and read the records otherwise.  Recomputed here
+ * first if the labels changed since it was last built. */
+dbl_status dbl_index_digest(const dbl_index *idx, const dbl_graph *g, uint32_t *out);
 
 /* -------------------------------------------------------------- queries */
 /* query_batch, queries.py:94-142, 210-249: label rules 0..4 on every

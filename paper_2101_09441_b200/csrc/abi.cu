@@ -397,7 +397,9 @@ extern "C" dbl_status dbl_index_build(const dbl_graph *gc, const dbl_config *cfg
     dbl_index *idx = nullptr;
     dbl_status s = index_create(gc, cfg, landmarks, leaf_flags, bucket, ovr_ids, ovr_buckets, n_ovr, &idx, false);
     if (s) return s;
-    if ((s = run_build(const_cast<dbl_graph *>(gc), idx, nullptr, 0))) {
+    // the digest is part of the built index (its pass is inside the build's time)
+    if ((s = run_build(const_cast<dbl_graph *>(gc), idx, nullptr, 0)) ||
+        (s = digest_refresh(idx, const_cast<dbl_graph *>(gc)))) {
         dbl_index_free(idx);
         return s;
     }
@@ -412,7 +414,9 @@ extern "C" dbl_status dbl_index_rebuild(const dbl_graph *gc, dbl_index *idx) {
     DBL_CUDA(cudaSetDevice(g->device));
     if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
-    return run_build(g, idx, nullptr, 0);
+    ++idx->version;
+    if ((s = run_build(g, idx, nullptr, 0))) return s;
+    return digest_refresh(idx, g);
 }
 
 extern "C" dbl_status dbl_index_build_words(const dbl_graph *gc, dbl_index *idx, const uint32_t *words,
@@ -425,6 +429,7 @@ extern "C" dbl_status dbl_index_build_words(const dbl_graph *gc, dbl_index *idx,
     DBL_CUDA(cudaSetDevice(g->device));
     if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
+    ++idx->version;
     return run_build(g, idx, words, nwords);
 }
 
@@ -434,6 +439,7 @@ extern "C" dbl_status dbl_index_free(dbl_index *idx) {
     cudaDeviceSynchronize();
     set_stream_synced();
     idx->rec.release();
+    idx->digest.release();
     idx->landmarks.release();
     idx->leaf_flags.release();
     idx->bucket.release();
@@ -491,6 +497,7 @@ extern "C" dbl_status dbl_index_import(dbl_index *idx, const uint64_t *dl_in, co
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(idx->device));
     set_stream(nullptr);
+    ++idx->version;
     const uint64_t *ins[4] = {dl_in, dl_out, bl_in, bl_out};
     DevBuf tmp;
     for (int f = 0; f < 4; ++f) {
@@ -560,6 +567,7 @@ extern "C" dbl_status dbl_index_grow(dbl_index *idx, uint32_t n) {
         (s = grow_buf(idx->bucket, (size_t)idx->n * 4, (size_t)n * 4 + 16, 0)))
         return s;
     idx->n = n;
+    ++idx->version;
     return DBL_OK;
 }
 
@@ -903,6 +911,7 @@ extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, 
     }
     DBL_CUDA(cudaSetDevice(g->device));
     set_stream(g->stream);
+    ++idx->version;
     dbl_update_stats st{};
     // one launch + one sync: pre-check, add_edge into the pending log, both
     // propagations (insert_one.cu)
@@ -948,6 +957,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     DBL_CUDA(cudaSetDevice(g->device));
     if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
+    ++idx->version;
     trace("insert: enter", g->stream);
     DevBuf in, keys, alt, newk, err;
     auto cleanup = [&]() { in.release(); keys.release(); alt.release(); newk.release(); err.release(); };
@@ -1107,6 +1117,7 @@ extern "C" dbl_status dbl_index_unpack_words(dbl_index *idx, const uint32_t *wor
     if (s) return s;
     cudaStream_t st = (cudaStream_t)stream;
     set_stream(st);
+    ++idx->version;
     DBL_CUDA(cudaMemcpyAsync(w.p, words, nw * 4, cudaMemcpyHostToDevice, st));
     unpack_words_kernel<<<grid_for((uint64_t)idx->n * nw), 256, 0, st>>>(idx->rec.as<uint64_t>(), idx->rs, idx->n,
                                                                          w.as<uint32_t>(), nw, dev_slab);

@@ -298,6 +298,14 @@ struct dbl_index {
     dbl::DevBuf dmask, sccmask;
     uint32_t dmask_n = 0;                // vertices covered by dmask
     bool has_scc = false;
+    // Label digest (query.cu): one u32 per vertex summarising its four label
+    // families, n x 4 bytes, so a query batch decides most pairs from an
+    // L2-resident table and reads the full records only for the rest.
+    // `version` moves on every label change (each ABI entry that writes
+    // records); the digest is current iff digest_version == version.
+    uint64_t version = 1;
+    mutable dbl::DevBuf digest;
+    mutable uint64_t digest_version = 0;
 };
 
 namespace dbl {
@@ -368,4 +376,6 @@ dbl_status query_finish(dbl_graph *g, uint32_t *err_out, bool *dense_out);
 dbl_status query_err_to(dbl_graph *g, uint32_t *dst4);
 bool chunk_needs_dense(const uint32_t *w4);
 dbl_status query_sync(dbl_graph *g);
+// (Re)compute idx's digest on g's stream if it is stale (no host sync).
+dbl_status digest_refresh(const dbl_index *idx, dbl_graph *g);
 }  // namespace dbl
