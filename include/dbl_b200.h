@@ -209,9 +209,12 @@ dbl_status dbl_index_records(const dbl_index *idx, uint64_t **dev_records,
  * landmark 0 / any other landmark, bit 2/3: the same for dl_in, bits 4..17 /
  * 18..31: bl_in / bl_out with bucket b folded onto bit (b % 64) % 14.  Query
  * batches decide a pair from the two digests when they prove rule 1 or rule
- * 2 of queries.py:102-108 and read the records otherwise.  Recomputed here
- * first if the labels changed since it was last built. */
-dbl_status dbl_index_digest(const dbl_index *idx, const dbl_graph *g, uint32_t *out);
+ * 2 of queries.py:102-108 and read the records otherwise.  Builds compute
+ * it; inserts keep a current digest current (single inserts OR the new
+ * label bits' digest bits in, batches recompute the changed vertices); other
+ * label writes leave it stale until a batch of >= 64k pairs or this call
+ * recomputes it.  *was_current (optional) tells whether it was current. */
+dbl_status dbl_index_digest(const dbl_index *idx, const dbl_graph *g, uint32_t *out, int *was_current);
 
 /* -------------------------------------------------------------- queries */
 /* query_batch, queries.py:94-142, 210-249: label rules 0..4 on every

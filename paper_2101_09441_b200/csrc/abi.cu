@@ -911,14 +911,19 @@ extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, 
     }
     DBL_CUDA(cudaSetDevice(g->device));
     set_stream(g->stream);
+    // the fast path ORs each written label delta's digest bits into the
+    // digest (digest bits are ORs of label bits), the fallback refreshes the
+    // changed vertices, so a current digest stays current
+    const bool dig_ok = idx->digest_version == idx->version;
     ++idx->version;
     dbl_update_stats st{};
     // one launch + one sync: pre-check, add_edge into the pending log, both
     // propagations (insert_one.cu)
     bool done = false;
     uint32_t dirs_done = 0;
-    if ((s = insert_edge_fast(idx, g, u, v, &st, &done, &dirs_done))) return s;
+    if ((s = insert_edge_fast(idx, g, u, v, &st, &done, &dirs_done, dig_ok))) return s;
     if (done) {
+        if (dig_ok) idx->digest_version = idx->version;
         if (stats) *stats = st;
         return DBL_OK;
     }
@@ -933,7 +938,7 @@ extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, 
     uint32_t changed[2], seedc[2], levels = 0;
     s = run_insert(g, idx, kb.as<uint64_t>(), 1, true, changed, seedc, &levels);
     kb.release();
-    if (s) return s;
+    if (s || (s = digest_after_insert(idx, g, dig_ok))) return s;
     // _propagate_union dequeues the seed plus every changed non-seed vertex;
     // a direction the fast path already finished (its labels are final, so
     // the fixpoint changes nothing there) keeps the fast path's counts
@@ -957,6 +962,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     DBL_CUDA(cudaSetDevice(g->device));
     if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
+    const bool dig_ok = idx->digest_version == idx->version;   // kept current by the change bitmaps
     ++idx->version;
     trace("insert: enter", g->stream);
     DevBuf in, keys, alt, newk, err;
@@ -1025,6 +1031,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
             return s;
         }
         range_error = hx[0] != 0;
+        if (!range_error && (s = digest_after_insert(idx, g, dig_ok))) { cleanup(); return s; }
         st.certified = hx[1];
         nnew = hx[2];
         cert_read = true;

@@ -199,20 +199,41 @@ __device__ uint32_t one_direction(OneShared &S, const uint64_t *rec, uint32_t rs
     return S.found;
 }
 
-// OR S.add into the discovered vertices' halves (and the seed's).
-__device__ void one_apply(OneShared &S, uint64_t *rec, uint32_t rs, uint32_t off, uint32_t H, int h) {
+__device__ __forceinline__ uint32_t fold14_one(uint64_t x) {
+    return (uint32_t)((x | (x >> 14) | (x >> 28) | (x >> 42) | (x >> 56)) & 0x3fffu);
+}
+
+// OR S.add into the discovered vertices' halves (and the seed's).  With a
+// query digest (query.cu: each digest bit is the OR of a fixed set of label
+// bits), the digest bits of S.add are ORed into the same vertices' digests,
+// which keeps a current digest exact.
+__device__ void one_apply(OneShared &S, uint64_t *rec, uint32_t rs, uint32_t off, uint32_t H, uint32_t wdl,
+                          uint32_t *dig, int h) {
+    uint32_t dm = 0;
+    if (dig) {
+        if (wdl) {
+            uint64_t rest = S.add[0] & ~1ull;
+            for (uint32_t j = 1; j < wdl; ++j) rest |= S.add[j];
+            dm = (uint32_t)(S.add[0] & 1u) | (rest ? 2u : 0u);
+        }
+        uint32_t f = 0;
+        for (uint32_t j = wdl; j < H; ++j) f |= fold14_one(S.add[j]);
+        // in-half (h = 0): dl_in -> bits 2, 3, bl_in -> 4..17; out-half: dl_out -> 0, 1, bl_out -> 18..31
+        dm = h == 0 ? (dm << 2) | (f << 4) : dm | (f << 18);
+    }
     for (int i = threadIdx.x - h * ONE_HALF; i < ONE_HCAP; i += ONE_HALF) {
         const uint32_t x = S.key[i];
         if (x == ONE_EMPTY) continue;
         uint64_t *p = rec + (uint64_t)x * rs + off;
         for (uint32_t j = 0; j < H; ++j) p[j] |= S.add[j];
+        if (dm) atomicOr(dig + x, dm);
     }
     half_sync(h);
 }
 
 __global__ void __launch_bounds__(ONE_THREADS, 1)
 insert_one_kernel(uint64_t *rec, uint32_t rs, uint32_t H, uint32_t wdl, uint32_t n, uint32_t u, uint32_t v,
-                  Adj fwd, Adj rev, uint64_t *pend, uint32_t npend, uint32_t pcap, OneOut *out) {
+                  Adj fwd, Adj rev, uint64_t *pend, uint32_t npend, uint32_t pcap, OneOut *out, uint32_t *dig) {
     extern __shared__ __align__(16) unsigned char smem[];
     OneShared *S2 = reinterpret_cast<OneShared *>(smem);   // one table set per direction
     const int tid = threadIdx.x;
@@ -257,7 +278,7 @@ insert_one_kernel(uint64_t *rec, uint32_t rs, uint32_t H, uint32_t wdl, uint32_t
         const uint32_t found = one_direction(S, rec, rs, off, H, n, h == 0 ? fwd : rev, pend,
                                              npend + ((is_new && npend < pcap) ? 1 : 0), h == 0, seed, &range, h);
         const bool ok = !S.overflow;
-        if (ok) one_apply(S, rec, rs, off, H, h);
+        if (ok) one_apply(S, rec, rs, off, H, wdl, dig, h);
         if (ltid == 0) {
             rok[h] = ok;
             rvis[h] = 1 + found;
@@ -295,7 +316,7 @@ namespace dbl {
 // edge is in the pending log, direction d is finished (labels written, its
 // counts in *st) iff bit d of *dirs_done is set, the other is untouched.
 dbl_status insert_edge_fast(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, dbl_update_stats *st,
-                            bool *done, uint32_t *dirs_done) {
+                            bool *done, uint32_t *dirs_done, bool digest_current) {
     *done = false;
     *dirs_done = 0;
     dbl_status s;
@@ -307,7 +328,7 @@ dbl_status insert_edge_fast(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v
     OneOut *out = reinterpret_cast<OneOut *>(g->one_out.p);
     insert_one_kernel<<<1, ONE_THREADS, 2 * sizeof(OneShared), g->stream>>>(
         idx->rec.as<uint64_t>(), idx->rs, idx->wdl + idx->wbl, idx->wdl, g->n, u, v, graph_fwd(g), graph_rev(g),
-        g->pend.as<uint64_t>(), g->n_pend, PEND_CAP, out);
+        g->pend.as<uint64_t>(), g->n_pend, PEND_CAP, out, digest_current ? idx->digest.as<uint32_t>() : nullptr);
     DBL_CHECK_LAUNCH("insert_one_kernel");
     DBL_CUDA(cudaStreamSynchronize(g->stream));
     OneOut o;

@@ -335,7 +335,7 @@ dbl_status graph_flush_pending(dbl_graph *g);
 // insert_one.cu: single-edge insert in one launch (done = false: the caller
 // finishes with the batch fixpoint; the edge is already in the pending log)
 dbl_status insert_edge_fast(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, dbl_update_stats *st,
-                            bool *done, uint32_t *dirs_done);
+                            bool *done, uint32_t *dirs_done, bool digest_current = false);
 // select.cu
 dbl_status select_landmarks_dev(dbl_graph *g, uint32_t k, int strategy, uint32_t *dev_out);
 dbl_status select_leaves_dev(dbl_graph *g, uint64_t threshold, uint32_t k_prime, uint64_t seed,
@@ -378,4 +378,8 @@ bool chunk_needs_dense(const uint32_t *w4);
 dbl_status query_sync(dbl_graph *g);
 // (Re)compute idx's digest on g's stream if it is stale (no host sync).
 dbl_status digest_refresh(const dbl_index *idx, dbl_graph *g);
+// After run_insert (count_changes): if the digest was current before the
+// batch, recompute it for the vertices in the change bitmaps and mark it
+// current again.
+dbl_status digest_after_insert(dbl_index *idx, dbl_graph *g, bool was_current);
 }  // namespace dbl

@@ -129,27 +129,47 @@ __device__ __forceinline__ uint32_t fold14(uint64_t x) {
     return (uint32_t)((x | (x >> 14) | (x >> 28) | (x >> 42) | (x >> 56)) & 0x3fffu);
 }
 
+__device__ __forceinline__ uint32_t digest_of(const uint64_t *__restrict__ r, uint32_t wdl, uint32_t wbl) {
+    const uint32_t H = wdl + wbl;
+    uint32_t d = 0;
+    if (wdl) {
+        const uint64_t in0 = __ldg(r), out0 = __ldg(r + H);
+        uint64_t in_rest = in0 & ~1ull, out_rest = out0 & ~1ull;
+        for (uint32_t k = 1; k < wdl; ++k) {
+            in_rest |= __ldg(r + k);
+            out_rest |= __ldg(r + H + k);
+        }
+        d = (uint32_t)(out0 & 1u) | (out_rest ? 2u : 0u) | ((uint32_t)(in0 & 1u) << 2) | (in_rest ? 8u : 0u);
+    }
+    uint32_t fi = 0, fo = 0;
+    for (uint32_t k = 0; k < wbl; ++k) {
+        fi |= fold14(__ldg(r + wdl + k));
+        fo |= fold14(__ldg(r + H + wdl + k));
+    }
+    return d | (fi << 4) | (fo << 18);
+}
+
 __global__ void __launch_bounds__(256) digest_kernel(const uint64_t *__restrict__ rec, uint32_t n, uint32_t rs,
                                                      uint32_t wdl, uint32_t wbl, uint32_t *__restrict__ dig) {
-    const uint32_t H = wdl + wbl;
-    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-        const uint64_t *r = rec + (size_t)x * rs;
-        uint32_t d = 0;
-        if (wdl) {
-            const uint64_t in0 = __ldg(r), out0 = __ldg(r + H);
-            uint64_t in_rest = in0 & ~1ull, out_rest = out0 & ~1ull;
-            for (uint32_t k = 1; k < wdl; ++k) {
-                in_rest |= __ldg(r + k);
-                out_rest |= __ldg(r + H + k);
-            }
-            d = (uint32_t)(out0 & 1u) | (out_rest ? 2u : 0u) | ((uint32_t)(in0 & 1u) << 2) | (in_rest ? 8u : 0u);
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
+        dig[x] = digest_of(rec + (size_t)x * rs, wdl, wbl);
+}
+
+// After an insert batch: recompute the digests of the vertices whose labels
+// grew (the fixpoint's per-direction change bitmaps; seeds included).
+__global__ void __launch_bounds__(256) digest_changed_kernel(const uint64_t *__restrict__ rec, uint32_t n,
+                                                             uint32_t rs, uint32_t wdl, uint32_t wbl,
+                                                             const uint32_t *__restrict__ bits0,
+                                                             const uint32_t *__restrict__ bits1,
+                                                             uint32_t *__restrict__ dig) {
+    const uint32_t nw = (n + 31) / 32;
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
+        uint32_t m = bits0[w] | bits1[w];
+        while (m) {
+            const uint32_t x = w * 32 + (uint32_t)(__ffs(m) - 1);
+            m &= m - 1;
+            if (x < n) dig[x] = digest_of(rec + (size_t)x * rs, wdl, wbl);
         }
-        uint32_t fi = 0, fo = 0;
-        for (uint32_t k = 0; k < wbl; ++k) {
-            fi |= fold14(__ldg(r + wdl + k));
-            fo |= fold14(__ldg(r + H + wdl + k));
-        }
-        dig[x] = d | (fi << 4) | (fo << 18);
     }
 }
 
@@ -162,16 +182,41 @@ __device__ __forceinline__ uint8_t digest_decide(uint32_t du, uint32_t dv, bool 
     return 0xff;
 }
 
+template <int WDL, int WBL>
+__global__ void digest_kernel_t(const uint64_t *__restrict__ rec, uint32_t n, uint32_t *__restrict__ dig);
+
 dbl_status digest_refresh(const dbl_index *idx, dbl_graph *g) {
     if (!DBL_DIGEST || idx->digest_version == idx->version) return DBL_OK;
     dbl_status s = idx->digest.ensure((size_t)idx->n * 4 + 16);
     if (s) return s;
     if (idx->n) {
-        uint32_t blocks = (idx->n + 255) / 256;
-        if (blocks > (uint32_t)g->sm_count * 8) blocks = g->sm_count * 8;
-        digest_kernel<<<blocks, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, idx->rs, idx->wdl, idx->wbl,
-                                                     idx->digest.as<uint32_t>());
+        const uint32_t blocks = (idx->n + 255) / 256;
+        const uint64_t *rec = idx->rec.as<uint64_t>();
+        uint32_t *dig = idx->digest.as<uint32_t>();
+        // one vertex per thread; the common widths load the record with
+        // vector loads (templated), the rest word by word
+#define DBL_DG(A, B) if (idx->wdl == A && idx->wbl == B) digest_kernel_t<A, B><<<blocks, 256, 0, g->stream>>>(rec, idx->n, dig); else
+        DBL_DG(1, 1) DBL_DG(2, 1) DBL_DG(4, 1) DBL_DG(1, 2) DBL_DG(2, 2) DBL_DG(0, 1)
+            digest_kernel<<<blocks < (uint32_t)g->sm_count * 8 ? blocks : g->sm_count * 8, 256, 0, g->stream>>>(
+                rec, idx->n, idx->rs, idx->wdl, idx->wbl, dig);
+#undef DBL_DG
         DBL_CHECK_LAUNCH("digest_kernel");
+    }
+    idx->digest_version = idx->version;
+    return DBL_OK;
+}
+
+dbl_status digest_after_insert(dbl_index *idx, dbl_graph *g, bool was_current) {
+    if (!DBL_DIGEST || !was_current) return DBL_OK;
+    if (idx->n) {
+        const size_t nw = ((size_t)idx->n + 31) / 32;
+        if (g->changed_bits.bytes < nw * 8) return DBL_OK;   // no change bitmaps: stays stale
+        uint32_t blocks = (uint32_t)((nw + 255) / 256);
+        if (blocks > (uint32_t)g->sm_count * 4) blocks = g->sm_count * 4;
+        const uint32_t *b0 = g->changed_bits.as<uint32_t>();
+        digest_changed_kernel<<<blocks, 256, 0, g->stream>>>(idx->rec.as<uint64_t>(), idx->n, idx->rs, idx->wdl,
+                                                             idx->wbl, b0, b0 + nw, idx->digest.as<uint32_t>());
+        DBL_CHECK_LAUNCH("digest_changed_kernel");
     }
     idx->digest_version = idx->version;
     return DBL_OK;
@@ -572,6 +617,33 @@ __device__ __forceinline__ void load_record(const uint64_t *p, uint64_t (&r)[RW]
     for (int k = V4; k < RW; k += 2)
         asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
                      : "=l"(r[k]), "=l"(r[k + 1]) : "l"(p + k));
+}
+
+template <int WDL, int WBL>
+__global__ void __launch_bounds__(256) digest_kernel_t(const uint64_t *__restrict__ rec, uint32_t n,
+                                                       uint32_t *__restrict__ dig) {
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H);
+    const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n) return;
+    uint64_t r[RW];
+    load_record<RW, RS>(rec + (size_t)x * RS, r);
+    uint32_t d = 0;
+    if (WDL) {
+        uint64_t in_rest = r[0] & ~1ull, out_rest = r[H] & ~1ull;
+#pragma unroll
+        for (int k = 1; k < WDL; ++k) {
+            in_rest |= r[k];
+            out_rest |= r[H + k];
+        }
+        d = (uint32_t)(r[H] & 1u) | (out_rest ? 2u : 0u) | ((uint32_t)(r[0] & 1u) << 2) | (in_rest ? 8u : 0u);
+    }
+    uint32_t fi = 0, fo = 0;
+#pragma unroll
+    for (int k = 0; k < WBL; ++k) {
+        fi |= fold14(r[WDL + k]);
+        fo |= fold14(r[H + WDL + k]);
+    }
+    dig[x] = d | (fi << 4) | (fo << 18);
 }
 
 __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t &total) {
@@ -1685,8 +1757,10 @@ dbl_status query_sync(dbl_graph *g) {
 using namespace dbl;
 
 // The index's query digest (n u32, host), recomputed first if stale.
-extern "C" dbl_status dbl_index_digest(const dbl_index *idx, const dbl_graph *gc, uint32_t *out) {
+extern "C" dbl_status dbl_index_digest(const dbl_index *idx, const dbl_graph *gc, uint32_t *out,
+                                       int *was_current) {
     if (!idx || !gc || (!out && idx->n)) { set_error("null argument"); return DBL_E_ARG; }
+    if (was_current) *was_current = idx->digest_version == idx->version;
     if (idx->n != gc->n) { set_error("graph and index vertex counts differ"); return DBL_E_MISMATCH; }
     dbl_graph *g = const_cast<dbl_graph *>(gc);
     DBL_CUDA(cudaSetDevice(g->device));

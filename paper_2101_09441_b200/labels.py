@@ -290,14 +290,16 @@ class DblIndex:
         N.call("dbl_index_equal", self._h, other._h, ctypes.byref(eq))
         return bool(eq.value)
 
-    def digest(self, g=None) -> np.ndarray:
-        """The query digest (u32 per vertex, dbl_index_digest), recomputed if stale."""
+    def digest(self, g=None, *, with_state: bool = False):
+        """The query digest (u32 per vertex, dbl_index_digest), recomputed if stale;
+        with_state=True also returns whether it was current before the call."""
         g = g if g is not None else self._graph_ref()
         if g is None:
             raise ValueError("the index's graph is gone: pass it explicitly")
         out = np.zeros(max(self._n, 1), np.uint32)
-        N.call("dbl_index_digest", self._h, g.handle, N.ptr(out))
-        return out[:self._n]
+        cur = ctypes.c_int()
+        N.call("dbl_index_digest", self._h, g.handle, N.ptr(out), ctypes.byref(cur))
+        return (out[:self._n], bool(cur.value)) if with_state else out[:self._n]
 
     def records(self) -> tuple[int, int]:
         """(device pointer, words per record) of the AoS label table."""

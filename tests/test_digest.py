@@ -109,28 +109,31 @@ def test_device_digest_equals_numpy(E, k, kp):
     np.testing.assert_array_equal(idx.digest(), np_digest(idx.export_words()))
 
 
+def oracle_codes(g, idx, qu, qv):
+    fptr, fcol = g.adjacency(False)
+    return O.csr_query_batch(g.vertex_count, fptr.astype(np.uint64), fcol, idx.config.k, idx.config.k_prime,
+                             idx.export_words(), qu, qv, threads=4)
+
+
 @gpu
-def test_digest_tracks_label_changes(E):
+def test_digest_maintained_through_inserts(E):
+    """Batch inserts recompute the changed vertices' digests, single inserts OR
+    the new label bits' digest bits in: the digest stays current and exact."""
     scale = 14
     n = 1 << scale
     src, dst = W.rmat_edges(scale, 8, 9)
     g = E.DynamicGraph.from_edges(n, src, dst)
     idx = E.build_index(g)
     rng = np.random.default_rng(4)
-    big = 1 << 17   # above the refresh threshold: a stale digest is recomputed
-    qu = rng.integers(0, n, big, dtype=np.uint32)
-    qv = rng.integers(0, n, big, dtype=np.uint32)
+    qu = rng.integers(0, n, 20_000, dtype=np.uint32)
+    qv = rng.integers(0, n, 20_000, dtype=np.uint32)
 
     def check(tag):
-        w = idx.export_words()
-        fptr, fcol = g.adjacency(False)
-        small, _ = E.query_codes(g, idx, qu[:5000], qv[:5000])     # stale digest: records
-        large, _ = E.query_codes(g, idx, qu, qv)                   # refreshes the digest
-        ref = O.csr_query_batch(n, fptr.astype(np.uint64), fcol, idx.config.k, idx.config.k_prime, w,
-                                qu, qv, threads=4)
-        np.testing.assert_array_equal(small, ref[:5000], err_msg=tag)
-        np.testing.assert_array_equal(large, ref, err_msg=tag)
-        np.testing.assert_array_equal(idx.digest(), np_digest(w), err_msg=tag)
+        dig, current = idx.digest(with_state=True)
+        assert current, f"{tag}: digest went stale"
+        np.testing.assert_array_equal(dig, np_digest(idx.export_words()), err_msg=tag)
+        codes, _ = E.query_codes(g, idx, qu, qv)
+        np.testing.assert_array_equal(codes, oracle_codes(g, idx, qu, qv), err_msg=tag)
 
     check("build")
     for b in range(3):
@@ -138,28 +141,47 @@ def test_digest_tracks_label_changes(E):
         iv = rng.integers(0, n, 3000, dtype=np.uint32)
         E.insert_edges(g, idx, iu, iv)
         check(f"batch {b}")
-    for _ in range(20):
-        E.insert_edge(g, idx, int(rng.integers(0, n)), int(rng.integers(0, n)))
+    changed = 0
+    for _ in range(40):
+        changed += E.insert_edge(g, idx, int(rng.integers(0, n)), int(rng.integers(0, n))).labels_changed
+    assert changed > 0
     check("single inserts")
+    # a hub-to-hub edge: its cones outgrow the single-edge kernel's tables
+    # (fallback to the batch fixpoint + change-bitmap refresh)
+    E.insert_edge(g, idx, int(n - 1), 0)
+    E.insert_edge(g, idx, 1, int(n - 2))
+    check("large cones")
     E.rebuild_in_place(g, idx)
     check("rebuild")
 
 
 @gpu
-def test_digest_after_import_and_growth(E):
+def test_stale_digest_takes_the_record_path(E):
+    """Label writes other than inserts (snapshot import, growth) leave the
+    digest stale: small batches read the records, a batch of >= 64k pairs
+    recomputes it first."""
     from paper_2101_09441_b200 import snapshot
-    n = 1 << 12
-    src, dst = W.rmat_edges(12, 8, 21)
+    import io
+    n = 1 << 13
+    src, dst = W.rmat_edges(13, 8, 21)
     g = E.DynamicGraph.from_edges(n, src, dst)
     idx = E.build_index(g)
     d0 = idx.digest()
-    # a snapshot round trip imports the labels into a fresh index
-    import io
+    rng = np.random.default_rng(8)
+    qu = rng.integers(0, n, 1 << 17, dtype=np.uint32)
+    qv = rng.integers(0, n, 1 << 17, dtype=np.uint32)
+    ref = oracle_codes(g, idx, qu, qv)
     buf = io.BytesIO()
     snapshot.save_index(idx, buf)
     buf.seek(0)
     idx2 = snapshot.load_index(buf, g)
-    np.testing.assert_array_equal(idx2.digest(), d0)
-    # growth: new vertices have empty labels except their own leaf bits
+    small, _ = E.query_codes(g, idx2, qu[:5000], qv[:5000])
+    np.testing.assert_array_equal(small, ref[:5000])
+    large, _ = E.query_codes(g, idx2, qu, qv)      # recomputes the digest
+    np.testing.assert_array_equal(large, ref)
+    dig, current = idx2.digest(with_state=True)
+    assert current
+    np.testing.assert_array_equal(dig, d0)
+    # growth: the new vertex's record is written by insert_vertex
     E.insert_vertex(g, idx, out_edges=[0], in_edges=[1])
     np.testing.assert_array_equal(idx.digest(), np_digest(idx.export_words()))
