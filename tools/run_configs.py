@@ -75,7 +75,8 @@ def build_time(g, cfg=None, reps=3):
 
 def query_rate(g, idx, qu, qv, reps=5):
     """query_qps: device-resident batch timed with CUDA events on the engine
-    stream (the bench's definition; codes + visited written); api_qps: the
+    stream after a 256 MB L2-flushing write (the bench's definition; codes +
+    visited written); api_qps: the
     same batch through E.query_codes (allocation, call and sync included)."""
     du = torch.from_numpy(qu.view(np.int32)).cuda()
     dv = torch.from_numpy(qv.view(np.int32)).cuda()
@@ -91,7 +92,9 @@ def query_rate(g, idx, qu, qv, reps=5):
     dvis = torch.empty(len(qu), dtype=torch.int32, device="cuda")
     flags = E.DEFAULT_FLAGS.bits()
     ts = []
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for i in range(reps + 1):
+        flush.fill_(1)   # L2 flushed before every timed batch, as bench.py times
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
