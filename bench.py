@@ -143,6 +143,20 @@ def ncu_traffic(kernel: str):
         return None
 
 
+# L2 request ceiling of a random 32-byte gather (8 CTAs/SM, 64 MB table, warm):
+# 205.3 G requests/s, tools/ubench_gather.cu -> profiles/r01_ubench_gather.txt
+L2_REQ_CEILING_G = 205.3
+
+
+def ncu_l2req(kernel: str):
+    """SM->L2 requests per launch of `kernel` from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_l2req.json")) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
 def make_workload(rank: int, scale: int):
     from paper_2101_09441_b200 import workload as W
     src, dst = W.rmat_edges(scale, EDGE_FACTOR, GRAPH_SEED)
@@ -429,6 +443,7 @@ def run_ours(args, rank, world, local_rank, gloo):
     k6_ms = statistics.mean(step_ms)   # average launch duration (the event timer is quantized)
     achieved = BATCH * q_bytes / (k6_ms / 1e3) / 1e9
     traffic = ncu_traffic("label_lean_kernel")
+    l2req = ncu_l2req("label_lean_kernel")
     build_achieved = exec_bytes["total"] / (build_ms_max / 1e3) / 1e9
     model_achieved = model_bytes / (build_ms_max / 1e3) / 1e9
     result = {
@@ -442,7 +457,14 @@ def run_ours(args, rank, world, local_rank, gloo):
                      "traffic": traffic, "peak_source": peak_src,
                      "bytes_per_query": q_bytes, "kernel_ms": k6_ms,
                      "digest_undecided_fraction": f_rec,
-                     "bytes_per_query_without_digest": 8 + 1 + 4 + 2 * rec_bytes},
+                     "bytes_per_query_without_digest": 8 + 1 + 4 + 2 * rec_bytes,
+                     # what binds this kernel: SM->L2 requests (ncu count per launch) per
+                     # event-timed launch against the random-gather request ceiling
+                     "l2_requests": None if not l2req else {
+                         "per_launch": l2req, "achieved_G_per_s": l2req / (k6_ms / 1e3) / 1e9,
+                         "ceiling_G_per_s": L2_REQ_CEILING_G,
+                         "frac": l2req / (k6_ms / 1e3) / 1e9 / L2_REQ_CEILING_G,
+                         "ceiling_source": "tools/ubench_gather.cu, profiles/r01_ubench_gather.txt"}},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": 8 * BATCH,
                 "d2h_bytes_per_step": BATCH, "api": "dbl_query(mem=DBL_MEM_HOST) on pinned buffers: the kernels "
                 "read the pairs and write the codes over PCIe (zero-copy); answer codes returned",

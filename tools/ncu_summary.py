@@ -19,6 +19,7 @@ METRICS = [
     ("dram__bytes_write.sum", "dram write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram % peak"),
     ("lts__t_bytes.sum", "L2 bytes"),
+    ("lts__t_requests_srcunit_tex.sum", "L2 requests (SM)"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
     ("launch__registers_per_thread", "regs"),
@@ -51,7 +52,7 @@ def main(rep, launches, out_md):
     kn = h.index("Kernel Name")
     lines = ["| kernel | " + " | ".join(lbl for m, lbl in METRICS if m in col) + " |",
              "|---|" + "---|" * len(col)]
-    traffic = {}
+    traffic, l2req = {}, {}
     for r in rows[2:]:
         cells = []
         for m, _ in METRICS:
@@ -63,6 +64,8 @@ def main(rep, launches, out_md):
         wb = to_bytes(r[col["dram__bytes_write.sum"]].replace(",", ""), units[col["dram__bytes_write.sum"]])
         key = short(r[kn]).split("<")[0]
         traffic.setdefault(key, []).append(rb + wb)
+        if "lts__t_requests_srcunit_tex.sum" in col:
+            l2req.setdefault(key, []).append(float(r[col["lts__t_requests_srcunit_tex.sum"]].replace(",", "")))
     # launch list shares
     share = defaultdict(float)
     total = 0.0
@@ -91,6 +94,11 @@ def main(rep, launches, out_md):
     for k, v in traffic.items():
         old[k] = sum(v) / len(v)
     json.dump(old, open(tj, "w"), indent=1, sort_keys=True)
+    lj = os.path.join(os.path.dirname(out_md), "ncu_l2req.json")
+    old = json.load(open(lj)) if os.path.exists(lj) else {}
+    for k, v in l2req.items():
+        old[k] = sum(v) / len(v)
+    json.dump(old, open(lj, "w"), indent=1, sort_keys=True)
     print("\n".join(md))
 
 

@@ -13,6 +13,31 @@
 
 __global__ void empty_kernel() {}
 
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Mailbox ping-pong over pinned host memory: one thread polls mb[0] and
+// echoes each new value into resp[0] (the floor of a persistent "query
+// server" kernel).  Exits after `iters` requests or 2 s, whichever first.
+__global__ void pingpong(volatile uint32_t *mb, volatile uint32_t *resp, int iters) {
+    if (threadIdx.x) return;
+    const unsigned long long t0 = gtime();
+    uint32_t last = 0;
+    for (int i = 0; i < iters; ++i) {
+        uint32_t s;
+        do {
+            s = mb[0];
+            if (gtime() - t0 > 2000000000ull) return;
+        } while (s == last);
+        last = s;
+        resp[0] = s;
+        __threadfence_system();
+    }
+}
+
 template <typename F>
 static double med_us(F f, int n = 400) {
     std::vector<double> t;
@@ -50,6 +75,35 @@ int main() {
     std::printf("dbl_query, device, 1 query:       %6.1f us\n", med_us([&] { dbl_query(idx, g, du, dv, 1, 0x3f, dc, nullptr, DBL_MEM_DEVICE); }));
     std::printf("dbl_query, host (pageable), 1 q:  %6.1f us\n", med_us([&] { dbl_query(idx, g, &hu, &hv, 1, 0x3f, &hc, nullptr, DBL_MEM_HOST); }));
     std::printf("dbl_query_async + dbl_sync, 1 q:  %6.1f us\n", med_us([&] { dbl_query_async(idx, g, du, dv, 1, 0x3f, dc, nullptr); dbl_sync(g); }));
+    {
+        uint32_t *mb, *resp;
+        cudaHostAlloc(&mb, 64, cudaHostAllocMapped);
+        cudaHostAlloc(&resp, 64, cudaHostAllocMapped);
+        mb[0] = 0;
+        resp[0] = 0;
+        cudaStream_t s2;
+        cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+        const int iters = 2000;
+        pingpong<<<1, 32, 0, s2>>>(mb, resp, iters);
+        std::vector<double> t;
+        bool ok = true;
+        for (int i = 1; i <= iters && ok; ++i) {
+            auto a = std::chrono::steady_clock::now();
+            *(volatile uint32_t *)mb = (uint32_t)i;
+            while (*(volatile uint32_t *)resp != (uint32_t)i) {
+                if (std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count() > 1.0) { ok = false; break; }
+            }
+            auto b = std::chrono::steady_clock::now();
+            if (i > 20) t.push_back(std::chrono::duration<double, std::micro>(b - a).count());
+        }
+        cudaStreamSynchronize(s2);
+        std::sort(t.begin(), t.end());
+        if (ok && !t.empty())
+            std::printf("mailbox ping-pong (pinned):       %6.2f us (p10 %.2f, p90 %.2f)\n", t[t.size() / 2],
+                        t[t.size() / 10], t[t.size() * 9 / 10]);
+        else
+            std::printf("mailbox ping-pong: timed out\n");
+    }
     uint32_t *pu, *pv;
     uint8_t *pc;
     const size_t Q = 1 << 20;
