@@ -269,6 +269,7 @@ extern "C" const char *dbl_last_error(void) { return g_last_error.c_str(); }
 extern "C" int dbl_version(void) { return 1; }
 extern "C" uint64_t dbl_kernel_launches(void) { return g_launches.load(); }
 extern "C" dbl_status dbl_release_cached_memory(void) {
+    serve_quiesce();   // no per-call query service runs beside this call
     pool_trim();
     return DBL_OK;
 }
@@ -386,6 +387,7 @@ static dbl_status index_create(const dbl_graph *gc, const dbl_config *cfg, const
 extern "C" dbl_status dbl_index_create(const dbl_graph *gc, const dbl_config *cfg, const uint32_t *landmarks,
                                        const uint8_t *leaf_flags, const uint32_t *bucket, const uint32_t *ovr_ids,
                                        const uint32_t *ovr_buckets, uint32_t n_ovr, dbl_index **out) {
+    serve_quiesce();   // no per-call query service runs beside this call
     return index_create(gc, cfg, landmarks, leaf_flags, bucket, ovr_ids, ovr_buckets, n_ovr, out);
 }
 
@@ -393,6 +395,7 @@ extern "C" dbl_status dbl_index_build(const dbl_graph *gc, const dbl_config *cfg
                                       const uint8_t *leaf_flags, const uint32_t *bucket,
                                       const uint32_t *ovr_ids, const uint32_t *ovr_buckets, uint32_t n_ovr,
                                       dbl_index **out) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (out) *out = nullptr;
     dbl_index *idx = nullptr;
     dbl_status s = index_create(gc, cfg, landmarks, leaf_flags, bucket, ovr_ids, ovr_buckets, n_ovr, &idx, false);
@@ -408,6 +411,7 @@ extern "C" dbl_status dbl_index_build(const dbl_graph *gc, const dbl_config *cfg
 }
 
 extern "C" dbl_status dbl_index_rebuild(const dbl_graph *gc, dbl_index *idx) {
+    serve_quiesce();   // no per-call query service runs beside this call
     dbl_status s = check_pair(idx, gc);
     if (s) return s;
     dbl_graph *g = const_cast<dbl_graph *>(gc);
@@ -421,6 +425,7 @@ extern "C" dbl_status dbl_index_rebuild(const dbl_graph *gc, dbl_index *idx) {
 
 extern "C" dbl_status dbl_index_build_words(const dbl_graph *gc, dbl_index *idx, const uint32_t *words,
                                             uint32_t nwords) {
+    serve_quiesce();   // no per-call query service runs beside this call
     dbl_status s = check_pair(idx, gc);
     if (s) return s;
     for (uint32_t i = 0; i < nwords; ++i)
@@ -434,6 +439,7 @@ extern "C" dbl_status dbl_index_build_words(const dbl_graph *gc, dbl_index *idx,
 }
 
 extern "C" dbl_status dbl_index_free(dbl_index *idx) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!idx) return DBL_OK;
     cudaSetDevice(idx->device);
     cudaDeviceSynchronize();
@@ -459,6 +465,7 @@ extern "C" dbl_status dbl_index_info(const dbl_index *idx, uint32_t *n, dbl_conf
 
 extern "C" dbl_status dbl_index_metadata(const dbl_index *idx, uint32_t *landmarks, uint8_t *leaf_flags,
                                          uint32_t *bucket) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(idx->device));
     set_stream(nullptr);
@@ -470,6 +477,7 @@ extern "C" dbl_status dbl_index_metadata(const dbl_index *idx, uint32_t *landmar
 
 extern "C" dbl_status dbl_index_export(const dbl_index *idx, uint64_t *dl_in, uint64_t *dl_out, uint64_t *bl_in,
                                        uint64_t *bl_out) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(idx->device));
     set_stream(nullptr);
@@ -494,6 +502,7 @@ extern "C" dbl_status dbl_index_export(const dbl_index *idx, uint64_t *dl_in, ui
 
 extern "C" dbl_status dbl_index_import(dbl_index *idx, const uint64_t *dl_in, const uint64_t *dl_out,
                                        const uint64_t *bl_in, const uint64_t *bl_out) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(idx->device));
     set_stream(nullptr);
@@ -520,6 +529,7 @@ extern "C" dbl_status dbl_index_import(dbl_index *idx, const uint64_t *dl_in, co
 }
 
 extern "C" dbl_status dbl_index_equal(const dbl_index *a, const dbl_index *b, int *out_equal) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!a || !b || !out_equal) { set_error("null argument"); return DBL_E_ARG; }
     *out_equal = 0;
     if (a->n != b->n || a->cfg.k != b->cfg.k || a->cfg.k_prime != b->cfg.k_prime) return DBL_OK;
@@ -556,6 +566,7 @@ static dbl_status grow_buf(DevBuf &b, size_t old_bytes, size_t new_bytes, int fi
 }
 
 extern "C" dbl_status dbl_index_grow(dbl_index *idx, uint32_t n) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     if (n < idx->n) { set_error("index cannot shrink"); return DBL_E_CONFIG; }
     if (n == idx->n) return DBL_OK;
@@ -572,6 +583,7 @@ extern "C" dbl_status dbl_index_grow(dbl_index *idx, uint32_t n) {
 }
 
 extern "C" dbl_status dbl_graph_add_vertices(dbl_graph *g, uint32_t count) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!g) { set_error("null graph"); return DBL_E_ARG; }
     if (!count) return DBL_OK;
     if ((uint64_t)g->n + count >= 0xffffffffull) { set_error("vertex count overflow"); return DBL_E_CONFIG; }
@@ -739,6 +751,16 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
     if (s) return s;
     if (count && (!u || !v || !codes)) { set_error("null argument"); return DBL_E_ARG; }
     dbl_graph *g = const_cast<dbl_graph *>(gc);
+    if (count == 1 && mem == DBL_MEM_HOST && sync) {
+        // a single query() call: the resident service warp answers it
+        // (query.cu K6s), no launch or stream sync per call
+        const uint32_t hu = u[0], hv = v[0];
+        if (hu >= g->n || hv >= g->n) { set_error("query vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
+        bool served = false;
+        if ((s = serve_query(idx, g, hu, hv, flags, codes, visited, &served))) return s;
+        if (served) return DBL_OK;
+    }
+    serve_quiesce();
     DBL_CUDA(cudaSetDevice(g->device));
     if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
@@ -793,6 +815,7 @@ extern "C" dbl_status dbl_query(const dbl_index *idx, const dbl_graph *g, const 
 extern "C" dbl_status dbl_query_async(const dbl_index *idx, const dbl_graph *g, const uint32_t *u,
                                       const uint32_t *v, uint64_t count, uint32_t flags, uint8_t *codes,
                                       uint32_t *visited) {
+    serve_quiesce();   // no per-call query service runs beside this call
     return query_impl(idx, g, u, v, count, flags, codes, visited, DBL_MEM_DEVICE, false);
 }
 
@@ -807,6 +830,7 @@ extern "C" dbl_status dbl_query_async(const dbl_index *idx, const dbl_graph *g, 
 extern "C" dbl_status dbl_query_multi(const dbl_index *const *idx, const dbl_graph *const *g, uint32_t ndev,
                                       const uint32_t *u, const uint32_t *v, uint64_t count, uint32_t flags,
                                       uint8_t *codes, uint32_t *visited, dbl_mem mem) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!idx || !g || ndev == 0) { set_error("null handle list"); return DBL_E_ARG; }
     if (count && (!u || !v || !codes)) { set_error("null argument"); return DBL_E_ARG; }
     if (mem == DBL_MEM_DEVICE && count) {
@@ -903,6 +927,7 @@ static dbl_status count_certified_async(dbl_graph *g, const dbl_index *idx, cons
 
 extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v,
                                       dbl_update_stats *stats) {
+    serve_quiesce();   // no per-call query service runs beside this call
     dbl_status s = check_pair(idx, g);
     if (s) return s;
     if (u >= g->n || v >= g->n) {
@@ -953,6 +978,7 @@ extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, 
 
 extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
                                        uint64_t count, dbl_mem mem, dbl_batch_stats *stats) {
+    serve_quiesce();   // no per-call query service runs beside this call
     dbl_status s = check_pair(idx, g);
     if (s) return s;
     dbl_batch_stats st{};
@@ -1060,6 +1086,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
 
 extern "C" dbl_status dbl_work_model(const dbl_index *idx, const dbl_graph *gc, uint64_t *V, uint64_t *E,
                                      uint32_t *levels) {
+    serve_quiesce();   // no per-call query service runs beside this call
     dbl_status s = check_pair(idx, gc);
     if (s) return s;
     if (!V || !E || !levels) { set_error("null argument"); return DBL_E_ARG; }
@@ -1094,6 +1121,7 @@ __global__ void unpack_words_kernel(uint64_t *__restrict__ rec, uint32_t rs, uin
 // slab (nw x n u64, device memory) -- the unit of the NCCL allgather.
 extern "C" dbl_status dbl_index_pack_words(const dbl_index *idx, const uint32_t *words, uint32_t nw,
                                            uint64_t *dev_slab, void *stream) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!idx || (nw && (!words || !dev_slab))) { set_error("null argument"); return DBL_E_ARG; }
     if (!nw || !idx->n) return DBL_OK;
     DBL_CUDA(cudaSetDevice(idx->device));
@@ -1115,6 +1143,7 @@ extern "C" dbl_status dbl_index_pack_words(const dbl_index *idx, const uint32_t 
 // Inverse of dbl_index_pack_words: scatter a slab (K5 record interleave).
 extern "C" dbl_status dbl_index_unpack_words(dbl_index *idx, const uint32_t *words, uint32_t nw,
                                              const uint64_t *dev_slab, void *stream) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!idx || (nw && (!words || !dev_slab))) { set_error("null argument"); return DBL_E_ARG; }
     if (!nw || !idx->n) return DBL_OK;
     DBL_CUDA(cudaSetDevice(idx->device));
@@ -1141,6 +1170,7 @@ extern "C" dbl_status dbl_index_unpack_words(dbl_index *idx, const uint32_t *wor
 // call and not repeated earlier in the batch.
 extern "C" dbl_status dbl_graph_add_edges(dbl_graph *g, const uint32_t *u, const uint32_t *v, uint64_t count,
                                           uint64_t *out_inserted) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!g || (count && (!u || !v))) { set_error("null argument"); return DBL_E_ARG; }
     if (out_inserted) *out_inserted = 0;
     if (!count) return DBL_OK;
@@ -1210,6 +1240,7 @@ __global__ void label_tests_kernel(const uint64_t *__restrict__ rec, uint32_t wd
 // batch of (x, y) pairs, host in/out.
 extern "C" dbl_status dbl_label_tests(const dbl_index *idx, const uint32_t *x, const uint32_t *y, uint64_t count,
                                       uint8_t *out_dl_intersec, uint8_t *out_bl_contain) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!idx || (count && (!x || !y || !out_dl_intersec || !out_bl_contain))) {
         set_error("null argument");
         return DBL_E_ARG;

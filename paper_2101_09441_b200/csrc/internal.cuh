@@ -266,6 +266,14 @@ struct dbl_graph {
     cudaEvent_t ev[6] = {};
     cudaEvent_t ev_in = nullptr;   // orders the engine stream after the caller's (order_after_caller)
     float t_fix = 0, t_label = 0, t_bfs = 0;
+    // per-call query service (query.cu): one resident warp answering single
+    // query() calls through a mailbox in pinned host memory
+    cudaStream_t sstream = nullptr;
+    dbl::HostBuf sbox;
+    const dbl_index *s_idx = nullptr;   // index the running service reads
+    uint64_t s_ver = 0;                 // its label version at launch
+    uint32_t s_seq = 0;                 // last request number posted
+    bool s_running = false;
 };
 
 // Record stride (u64 words) for half-width H = wdl + wbl.  L2 fills whole
@@ -376,6 +384,14 @@ dbl_status query_finish(dbl_graph *g, uint32_t *err_out, bool *dense_out);
 dbl_status query_err_to(dbl_graph *g, uint32_t *dst4);
 bool chunk_needs_dense(const uint32_t *w4);
 dbl_status query_sync(dbl_graph *g);
+// Stop every running per-call query service (each ABI entry that may write
+// labels or adjacency, launch a cooperative kernel or free a handle calls
+// this first; a no-op while none runs).
+void serve_quiesce();
+// Answer one host query through the service; *served = false: take the batch path.
+dbl_status serve_query(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, uint32_t flags, uint8_t *code,
+                       uint32_t *visited, bool *served);
+void serve_release(dbl_graph *g);
 // (Re)compute idx's digest on g's stream if it is stale (no host sync).
 dbl_status digest_refresh(const dbl_index *idx, dbl_graph *g);
 // After run_insert (count_changes): if the digest was current before the

@@ -22,7 +22,11 @@
 // 64 queries' DL/BL words staged in shared memory.  A group whose BFS
 // outgrows the table is re-run by the dense variant (direct-mapped global
 // arrays), so no query is ever answered on the CPU.
+#include <atomic>
+#include <chrono>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -1752,6 +1756,281 @@ dbl_status query_sync(dbl_graph *g) {
     return DBL_OK;
 }
 
+// ------------------------------------------------- per-call service (K6s) --
+//
+// A single query() call used to pay a kernel launch and a stream sync
+// (10.1 us on this box for an empty kernel, tools/ubench_api.cu) on top of
+// about a microsecond of work.  The service keeps one warp resident that
+// polls a mailbox in pinned host memory (round trip 2.4 us, same tool): the
+// host writes (u, v, flags) and a sequence number; the warp answers with the
+// same rules as K6 (digest, then both records, rules 1-4 in order,
+// queries.py:96-114) and, if they leave the query open, the bounded warp BFS
+// (queries.py:116-142); a query that outgrows it is handed back and answered
+// by the batch path.  The warp exits after SERVE_IDLE_NS without a request;
+// every other entry point of the library stops it first (serve_quiesce), so
+// it never runs beside a label or adjacency write or a cooperative launch.
+struct ServeBox {
+    uint32_t seq, op, u, v, flags, pad0[11];           // host -> device
+    uint32_t rseq, status, code, visited, alive, pad1[11];   // device -> host (own line)
+};
+enum { SERVE_QUERY = 1, SERVE_STOP = 2 };
+enum { SERVE_OK = 0, SERVE_FALLBACK = 1 };
+#ifndef DBL_SERVE
+#define DBL_SERVE 1                 // 0: single queries take the launch + sync path
+#endif
+constexpr uint64_t SERVE_IDLE_NS = 2000000;   // the warp exits after 2 ms without a request
+
+__device__ __forceinline__ uint64_t serve_clock() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int WDL, int WBL>
+__global__ void __launch_bounds__(32, 1) serve_kernel(const uint64_t *__restrict__ rec,
+                                                      const uint32_t *__restrict__ dig, uint32_t n, const Adj adj,
+                                                      ServeBox *box, uint32_t start_seq) {
+    constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H), WD = WDL > 0 ? WDL : 1;
+    __shared__ uint32_t wq[TB_Q];
+    __shared__ uint64_t sdlo[WD], sbli[WBL], sblo[WBL];
+    const int lane = threadIdx.x & 31;
+    uint32_t last = start_seq;
+    uint64_t t_idle = serve_clock();
+    for (;;) {
+        uint32_t seq = last;
+        if (lane == 0) {
+            for (;;) {
+                seq = ld_acquire_sys(&box->seq);
+                if (seq != last || serve_clock() - t_idle > SERVE_IDLE_NS) break;
+            }
+        }
+        seq = __shfl_sync(FULL, seq, 0);
+        if (seq == last) break;   // idle
+        uint32_t op = 0, u = 0, v = 0, flags = 0;
+        if (lane == 0) {
+            const volatile ServeBox *vb = box;
+            op = vb->op;
+            u = vb->u;
+            v = vb->v;
+            flags = vb->flags;
+        }
+        op = __shfl_sync(FULL, op, 0);
+        if (op != SERVE_QUERY) break;
+        u = __shfl_sync(FULL, u, 0);
+        v = __shfl_sync(FULL, v, 0);
+        flags = __shfl_sync(FULL, flags, 0);
+        const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
+        const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
+        const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
+        uint32_t code = UNRESOLVED, vc = 0, status = SERVE_OK;
+        if (u >= n || v >= n) {
+            status = SERVE_FALLBACK;   // (the host checks the range first)
+        } else if (u == v) {
+            code = DBL_REFLEXIVE;
+        } else {
+            if (dig) code = digest_decide(__ldg(dig + u), __ldg(dig + v), use_dl, use_bl);
+            if (code == UNRESOLVED) {
+                uint64_t a[RW], b[RW];
+                load_record<RW, RS>(rec + (size_t)u * RS, a);
+                load_record<RW, RS>(rec + (size_t)v * RS, b);
+                uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
+#pragma unroll
+                for (int k = 0; k < WDL; ++k) {
+                    r1 |= a[H + k] & b[k];
+                    r3 |= b[H + k] & a[k];
+                    r4 |= (a[H + k] & a[k]) | (b[H + k] & b[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < WBL; ++k) r2 |= (a[WDL + k] & ~b[WDL + k]) | (b[H + WDL + k] & ~a[H + WDL + k]);
+                if (use_dl && r1) code = DBL_DL_POSITIVE;
+                else if (use_bl && r2) code = DBL_BL_NEGATIVE;
+                else if (thm1 && r3) code = DBL_THM1_NEGATIVE;
+                else if (thm2 && r4) code = DBL_THM2_NEGATIVE;
+                if (code == UNRESOLVED) {
+                    if (lane == 0) {
+#pragma unroll
+                        for (int k = 0; k < WDL; ++k) sdlo[k] = a[H + k];
+#pragma unroll
+                        for (int k = 0; k < WBL; ++k) {
+                            sbli[k] = b[WDL + k];
+                            sblo[k] = b[H + WDL + k];
+                        }
+                    }
+                    __syncwarp();
+                    const int r = warp_query_bfs<WDL, WBL>(rec, adj, u, v, sdlo, sbli, sblo, prune_dl, prune_bl,
+                                                           Pivot{}, wq, &vc);
+                    if (r == 2) status = SERVE_FALLBACK;
+                    else code = r ? DBL_BFS_POSITIVE : DBL_BFS_NEGATIVE;
+                    __syncwarp();
+                }
+            }
+        }
+        if (lane == 0) {
+            volatile ServeBox *vb = box;
+            vb->code = code;
+            vb->visited = vc;
+            vb->status = status;
+            st_release_sys(&box->rseq, seq);
+        }
+        last = seq;
+        t_idle = serve_clock();
+    }
+    if (lane == 0) st_release_sys(&box->alive, 0u);
+}
+
+typedef void (*serve_fn)(const uint64_t *, const uint32_t *, uint32_t, const Adj, ServeBox *, uint32_t);
+
+static serve_fn pick_serve(uint32_t wdl, uint32_t wbl) {
+#define DBL_SV(A, B) if (wdl == A && wbl == B) return serve_kernel<A, B>;
+    DBL_SV(0, 1) DBL_SV(1, 1) DBL_SV(2, 1) DBL_SV(4, 1) DBL_SV(0, 2) DBL_SV(1, 2) DBL_SV(2, 2)
+#undef DBL_SV
+    return nullptr;
+}
+
+// One service at a time per process (it holds one SM); the mutex also
+// serialises concurrent single-query calls, which share the mailbox.
+static std::mutex g_srv_mu;
+static dbl_graph *g_srv = nullptr;
+static std::atomic<int> g_srv_on{0};
+
+static void serve_stop_locked() {
+    dbl_graph *g = g_srv;
+    if (!g) return;
+    g_srv = nullptr;
+    g_srv_on.store(0, std::memory_order_release);
+    if (!g->s_running) return;
+    volatile ServeBox *vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
+    vb->op = SERVE_STOP;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    vb->seq = ++g->s_seq;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaSetDevice(g->device);
+    cudaStreamSynchronize(g->sstream);
+    cudaSetDevice(dev);
+    g->s_running = false;
+}
+
+void serve_quiesce() {
+    if (g_srv_on.load(std::memory_order_acquire) == 0) return;
+    std::lock_guard<std::mutex> lk(g_srv_mu);
+    serve_stop_locked();
+}
+
+// Release the graph's service resources (dbl_graph_free, after serve_quiesce).
+void serve_release(dbl_graph *g) {
+    if (g->sstream) {
+        cudaStreamSynchronize(g->sstream);
+        cudaStreamDestroy(g->sstream);
+        g->sstream = nullptr;
+    }
+    g->sbox.release();
+}
+
+static dbl_status serve_start_locked(const dbl_index *idx, dbl_graph *g, serve_fn fn) {
+    if (g_srv != g) serve_stop_locked();
+    DBL_CUDA(cudaSetDevice(g->device));
+    dbl_status s;
+    if (g->s_running) {   // an exited (idle) or outdated service of this graph
+        volatile ServeBox *vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
+        vb->op = SERVE_STOP;
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        vb->seq = ++g->s_seq;
+        DBL_CUDA(cudaStreamSynchronize(g->sstream));
+        g->s_running = false;
+    }
+    // BFS fallbacks read the adjacency: fold the single-edge log in first,
+    // and let the engine stream's queued work (builds, inserts) finish
+    if ((s = graph_flush_pending(g))) return s;
+    DBL_CUDA(cudaStreamSynchronize(g->stream));
+    if ((s = g->sbox.ensure(sizeof(ServeBox) + 64))) return s;
+    if (!g->sstream) DBL_CUDA(cudaStreamCreateWithFlags(&g->sstream, cudaStreamNonBlocking));
+    ServeBox *hb = reinterpret_cast<ServeBox *>(g->sbox.p);
+    ServeBox *db = nullptr;
+    DBL_CUDA(cudaHostGetDevicePointer((void **)&db, hb, 0));
+    volatile ServeBox *vb = hb;
+    vb->rseq = g->s_seq;
+    vb->seq = g->s_seq;
+    vb->alive = 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    const uint32_t *dig = DBL_DIGEST && idx->digest_version == idx->version ? idx->digest.as<uint32_t>() : nullptr;
+    fn<<<1, 32, 0, g->sstream>>>(idx->rec.as<uint64_t>(), dig, idx->n, graph_fwd(g), db, g->s_seq);
+    DBL_CHECK_LAUNCH("serve_kernel");
+    g->s_running = true;
+    g->s_idx = idx;
+    g->s_ver = idx->version;
+    g_srv = g;
+    g_srv_on.store(1, std::memory_order_release);
+    return DBL_OK;
+}
+
+// Answer one query through the service.  *served = false: the service cannot
+// take it (label widths without a service kernel, or a BFS beyond its
+// bounds); the caller answers it on the batch path.
+dbl_status serve_query(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, uint32_t flags, uint8_t *code,
+                       uint32_t *visited, bool *served) {
+    *served = false;
+    const serve_fn fn = DBL_SERVE ? pick_serve(idx->wdl, idx->wbl) : nullptr;
+    if (!fn) return DBL_OK;
+    std::lock_guard<std::mutex> lk(g_srv_mu);
+    dbl_status s;
+    volatile ServeBox *vb = nullptr;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        if (g_srv != g || !g->s_running || g->s_idx != idx || g->s_ver != idx->version ||
+            reinterpret_cast<volatile ServeBox *>(g->sbox.p)->alive == 0) {
+            if ((s = serve_start_locked(idx, g, fn))) return s;
+        }
+        vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
+        vb->u = u;
+        vb->v = v;
+        vb->flags = flags;
+        vb->op = SERVE_QUERY;
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        const uint32_t seq = ++g->s_seq;
+        vb->seq = seq;
+        const auto t0 = std::chrono::steady_clock::now();
+        bool done = false, exited = false;
+        for (uint32_t it = 0;; ++it) {
+            if (vb->rseq == seq) { done = true; break; }
+            if (vb->alive == 0) {   // went idle just before the request: relaunch, post again
+                exited = vb->rseq != seq;
+                if (!exited) done = true;
+                break;
+            }
+            if ((it & 1023) == 1023 &&
+                std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+                serve_stop_locked();
+                set_error("query service did not answer within 2 s");
+                return DBL_E_CUDA;
+            }
+        }
+        if (exited) {
+            g->s_running = false;
+            cudaStreamSynchronize(g->sstream);
+            continue;
+        }
+        if (done) break;
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    if (!vb || vb->rseq != g->s_seq) { set_error("query service failed to start"); return DBL_E_CUDA; }
+    if (vb->status != SERVE_OK) {
+        serve_stop_locked();   // the batch path takes this query (its BFS stages run on the engine stream)
+        return DBL_OK;
+    }
+    *code = (uint8_t)vb->code;
+    if (visited) *visited = vb->visited;
+    *served = true;
+    return DBL_OK;
+}
+
 }  // namespace dbl
 
 using namespace dbl;
@@ -1759,6 +2038,7 @@ using namespace dbl;
 // The index's query digest (n u32, host), recomputed first if stale.
 extern "C" dbl_status dbl_index_digest(const dbl_index *idx, const dbl_graph *gc, uint32_t *out,
                                        int *was_current) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!idx || !gc || (!out && idx->n)) { set_error("null argument"); return DBL_E_ARG; }
     if (was_current) *was_current = idx->digest_version == idx->version;
     if (idx->n != gc->n) { set_error("graph and index vertex counts differ"); return DBL_E_MISMATCH; }
@@ -1778,6 +2058,7 @@ extern "C" dbl_status dbl_index_digest(const dbl_index *idx, const dbl_graph *gc
 // kernels (per-warp BFS table overflow or generic widths), [1] range-error
 // flag, [3] groups re-run densely.
 extern "C" dbl_status dbl_query_counters(const dbl_graph *g, uint32_t *out8) {
+    serve_quiesce();   // no per-call query service runs beside this call
     if (!g || !out8) { set_error("null argument"); return DBL_E_ARG; }
     if (!g->q_counters.p) { for (int i = 0; i < 8; ++i) out8[i] = 0; return DBL_OK; }
     DBL_CUDA(cudaSetDevice(g->device));
