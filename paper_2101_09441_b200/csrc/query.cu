@@ -22,6 +22,8 @@
 // 64 queries' DL/BL words staged in shared memory.  A group whose BFS
 // outgrows the table is re-run by the dense variant (direct-mapped global
 // arrays), so no query is ever answered on the CPU.
+#include <emmintrin.h>
+
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
@@ -1769,9 +1771,14 @@ dbl_status query_sync(dbl_graph *g) {
 // by the batch path.  The warp exits after SERVE_IDLE_NS without a request;
 // every other entry point of the library stops it first (serve_quiesce), so
 // it never runs beside a label or adjacency write or a cooperative launch.
-struct ServeBox {
-    uint32_t seq, op, u, v, flags, pad0[11];           // host -> device
-    uint32_t rseq, status, code, visited, alive, pad1[11];   // device -> host (own line)
+// Request and answer are one 16-byte word each, written and read with single
+// vector accesses (one PCIe transaction each way); the sequence number is
+// the last word the host writes (x86 keeps store order), so a request read
+// with the new sequence number also holds its own (u, v, flags).
+struct alignas(64) ServeBox {
+    uint32_t u, v, opflags, seq, pad0[12];              // host -> device: opflags = op << 16 | flags
+    uint32_t code, visited, status, rseq, pad1[12];     // device -> host (own line)
+    uint32_t alive, pad2[15];
 };
 enum { SERVE_QUERY = 1, SERVE_STOP = 2 };
 enum { SERVE_OK = 0, SERVE_FALLBACK = 1 };
@@ -1784,11 +1791,6 @@ __device__ __forceinline__ uint64_t serve_clock() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
 }
 __device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -1805,28 +1807,21 @@ __global__ void __launch_bounds__(32, 1) serve_kernel(const uint64_t *__restrict
     uint32_t last = start_seq;
     uint64_t t_idle = serve_clock();
     for (;;) {
-        uint32_t seq = last;
+        uint32_t seq = last, u = 0, v = 0, opflags = 0;
         if (lane == 0) {
             for (;;) {
-                seq = ld_acquire_sys(&box->seq);
+                asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(u), "=r"(v), "=r"(opflags), "=r"(seq) : "l"(box) : "memory");
                 if (seq != last || serve_clock() - t_idle > SERVE_IDLE_NS) break;
             }
         }
         seq = __shfl_sync(FULL, seq, 0);
         if (seq == last) break;   // idle
-        uint32_t op = 0, u = 0, v = 0, flags = 0;
-        if (lane == 0) {
-            const volatile ServeBox *vb = box;
-            op = vb->op;
-            u = vb->u;
-            v = vb->v;
-            flags = vb->flags;
-        }
-        op = __shfl_sync(FULL, op, 0);
-        if (op != SERVE_QUERY) break;
+        opflags = __shfl_sync(FULL, opflags, 0);
+        if ((opflags >> 16) != SERVE_QUERY) break;
         u = __shfl_sync(FULL, u, 0);
         v = __shfl_sync(FULL, v, 0);
-        flags = __shfl_sync(FULL, flags, 0);
+        const uint32_t flags = opflags & 0xffffu;
         const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
         const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
         const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
@@ -1873,13 +1868,9 @@ __global__ void __launch_bounds__(32, 1) serve_kernel(const uint64_t *__restrict
                 }
             }
         }
-        if (lane == 0) {
-            volatile ServeBox *vb = box;
-            vb->code = code;
-            vb->visited = vc;
-            vb->status = status;
-            st_release_sys(&box->rseq, seq);
-        }
+        if (lane == 0)
+            asm volatile("st.relaxed.sys.global.v4.u32 [%0], {%1, %2, %3, %4};"
+                         ::"l"(&box->code), "r"(code), "r"(vc), "r"(status), "r"(seq) : "memory");
         last = seq;
         t_idle = serve_clock();
     }
@@ -1908,7 +1899,7 @@ static void serve_stop_locked() {
     g_srv_on.store(0, std::memory_order_release);
     if (!g->s_running) return;
     volatile ServeBox *vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
-    vb->op = SERVE_STOP;
+    vb->opflags = SERVE_STOP << 16;
     std::atomic_thread_fence(std::memory_order_seq_cst);
     vb->seq = ++g->s_seq;
     int dev = 0;
@@ -1941,7 +1932,7 @@ static dbl_status serve_start_locked(const dbl_index *idx, dbl_graph *g, serve_f
     dbl_status s;
     if (g->s_running) {   // an exited (idle) or outdated service of this graph
         volatile ServeBox *vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
-        vb->op = SERVE_STOP;
+        vb->opflags = SERVE_STOP << 16;
         std::atomic_thread_fence(std::memory_order_seq_cst);
         vb->seq = ++g->s_seq;
         DBL_CUDA(cudaStreamSynchronize(g->sstream));
@@ -1960,6 +1951,8 @@ static dbl_status serve_start_locked(const dbl_index *idx, dbl_graph *g, serve_f
     vb->rseq = g->s_seq;
     vb->seq = g->s_seq;
     vb->alive = 1;
+    static_assert(offsetof(ServeBox, code) % 16 == 0 && offsetof(ServeBox, rseq) == offsetof(ServeBox, code) + 12,
+                  "the answer is one 16-byte word");
     std::atomic_thread_fence(std::memory_order_seq_cst);
     const uint32_t *dig = DBL_DIGEST && idx->digest_version == idx->version ? idx->digest.as<uint32_t>() : nullptr;
     fn<<<1, 32, 0, g->sstream>>>(idx->rec.as<uint64_t>(), dig, idx->n, graph_fwd(g), db, g->s_seq);
@@ -1983,7 +1976,9 @@ dbl_status serve_query(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t 
     std::lock_guard<std::mutex> lk(g_srv_mu);
     dbl_status s;
     volatile ServeBox *vb = nullptr;
-    for (int attempt = 0; attempt < 3; ++attempt) {
+    uint32_t ans[3] = {0, 0, 0};   // code, visited, status
+    bool answered = false;
+    for (int attempt = 0; attempt < 3 && !answered; ++attempt) {
         if (g_srv != g || !g->s_running || g->s_idx != idx || g->s_ver != idx->version ||
             reinterpret_cast<volatile ServeBox *>(g->sbox.p)->alive == 0) {
             if ((s = serve_start_locked(idx, g, fn))) return s;
@@ -1991,18 +1986,26 @@ dbl_status serve_query(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t 
         vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
         vb->u = u;
         vb->v = v;
-        vb->flags = flags;
-        vb->op = SERVE_QUERY;
-        std::atomic_thread_fence(std::memory_order_seq_cst);
+        vb->opflags = (SERVE_QUERY << 16) | (flags & 0xffffu);
+        std::atomic_signal_fence(std::memory_order_seq_cst);   // the sequence number is stored last
         const uint32_t seq = ++g->s_seq;
         vb->seq = seq;
         const auto t0 = std::chrono::steady_clock::now();
         bool done = false, exited = false;
         for (uint32_t it = 0;; ++it) {
-            if (vb->rseq == seq) { done = true; break; }
+            alignas(16) uint32_t w[4];   // one 16-byte load: the answer and its sequence number together
+            _mm_store_si128(reinterpret_cast<__m128i *>(w),
+                            _mm_load_si128(reinterpret_cast<const __m128i *>(const_cast<uint32_t *>(&vb->code))));
+            if (w[3] == seq) {
+                ans[0] = w[0];
+                ans[1] = w[1];
+                ans[2] = w[2];
+                done = true;
+                break;
+            }
             if (vb->alive == 0) {   // went idle just before the request: relaunch, post again
                 exited = vb->rseq != seq;
-                if (!exited) done = true;
+                if (!exited) { ans[0] = vb->code; ans[1] = vb->visited; ans[2] = vb->status; done = true; }
                 break;
             }
             if ((it & 1023) == 1023 &&
@@ -2017,16 +2020,15 @@ dbl_status serve_query(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t 
             cudaStreamSynchronize(g->sstream);
             continue;
         }
-        if (done) break;
+        answered = done;
     }
-    std::atomic_thread_fence(std::memory_order_acquire);
-    if (!vb || vb->rseq != g->s_seq) { set_error("query service failed to start"); return DBL_E_CUDA; }
-    if (vb->status != SERVE_OK) {
+    if (!answered) { set_error("query service failed to start"); return DBL_E_CUDA; }
+    if (ans[2] != SERVE_OK) {
         serve_stop_locked();   // the batch path takes this query (its BFS stages run on the engine stream)
         return DBL_OK;
     }
-    *code = (uint8_t)vb->code;
-    if (visited) *visited = vb->visited;
+    *code = (uint8_t)ans[0];
+    if (visited) *visited = ans[1];
     *served = true;
     return DBL_OK;
 }
