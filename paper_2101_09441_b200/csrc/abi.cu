@@ -927,31 +927,37 @@ static dbl_status count_certified_async(dbl_graph *g, const dbl_index *idx, cons
 
 extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v,
                                       dbl_update_stats *stats) {
-    serve_quiesce();   // no per-call query service runs beside this call
     dbl_status s = check_pair(idx, g);
     if (s) return s;
     if (u >= g->n || v >= g->n) {
         set_error("vertex " + std::to_string(u >= g->n ? u : v) + " outside [0, " + std::to_string(g->n) + ")");
         return DBL_E_VERTEX_RANGE;
     }
-    DBL_CUDA(cudaSetDevice(g->device));
-    set_stream(g->stream);
-    // the fast path ORs each written label delta's digest bits into the
-    // digest (digest bits are ORs of label bits), the fallback refreshes the
-    // changed vertices, so a current digest stays current
-    const bool dig_ok = idx->digest_version == idx->version;
-    ++idx->version;
     dbl_update_stats st{};
-    // one launch + one sync: pre-check, add_edge into the pending log, both
-    // propagations (insert_one.cu)
-    bool done = false;
+    bool done = false, dig_ok = false, served = false;
     uint32_t dirs_done = 0;
-    if ((s = insert_edge_fast(idx, g, u, v, &st, &done, &dirs_done, dig_ok))) return s;
+    // the per-call service runs K9 in its resident CTA (no launch, no sync)
+    if ((s = serve_insert(idx, g, u, v, &st, &done, &dirs_done, &dig_ok, &served))) return s;
+    if (!served) {
+        serve_quiesce();
+        DBL_CUDA(cudaSetDevice(g->device));
+        set_stream(g->stream);
+        // the fast path ORs each written label delta's digest bits into the
+        // digest (digest bits are ORs of label bits), the fallback refreshes
+        // the changed vertices, so a current digest stays current
+        dig_ok = idx->digest_version == idx->version;
+        ++idx->version;
+        // one launch + one sync: pre-check, add_edge into the pending log,
+        // both propagations (insert_one.cu)
+        if ((s = insert_edge_fast(idx, g, u, v, &st, &done, &dirs_done, dig_ok))) return s;
+        if (done && dig_ok) idx->digest_version = idx->version;
+    }
     if (done) {
-        if (dig_ok) idx->digest_version = idx->version;
         if (stats) *stats = st;
         return DBL_OK;
     }
+    DBL_CUDA(cudaSetDevice(g->device));
+    set_stream(g->stream);
     // a cone outgrew the single-CTA tables (no label was written; the edge is
     // in the graph): fold the log into the delta adjacency and run the batch
     // fixpoint from this edge's seeds

@@ -274,6 +274,7 @@ struct dbl_graph {
     uint64_t s_ver = 0;                 // its label version at launch
     uint32_t s_seq = 0;                 // last request number posted
     bool s_running = false;
+    bool s_dig = false;                 // the service keeps the digest current (it was at launch)
 };
 
 // Record stride (u64 words) for half-width H = wdl + wbl.  L2 fills whole
@@ -344,6 +345,9 @@ dbl_status graph_flush_pending(dbl_graph *g);
 // finishes with the batch fixpoint; the edge is already in the pending log)
 dbl_status insert_edge_fast(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, dbl_update_stats *st,
                             bool *done, uint32_t *dirs_done, bool digest_current = false);
+struct OneOut;
+dbl_status insert_edge_outcome(dbl_graph *g, const OneOut &o, dbl_update_stats *st, bool *done,
+                               uint32_t *dirs_done);
 // select.cu
 dbl_status select_landmarks_dev(dbl_graph *g, uint32_t k, int strategy, uint32_t *dev_out);
 dbl_status select_leaves_dev(dbl_graph *g, uint64_t threshold, uint32_t k_prime, uint64_t seed,
@@ -392,6 +396,12 @@ void serve_quiesce();
 dbl_status serve_query(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, uint32_t flags, uint8_t *code,
                        uint32_t *visited, bool *served);
 void serve_release(dbl_graph *g);
+// Run one single-edge insert (K9) on the service.  *served = false: the
+// caller launches K9 itself.  Otherwise the label version has moved, the
+// outcome is in st / done / dirs_done as from insert_edge_fast, and *dig_ok
+// tells whether the digest was current before the edge (for the fallback).
+dbl_status serve_insert(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, dbl_update_stats *st, bool *done,
+                        uint32_t *dirs_done, bool *dig_ok, bool *served);
 // (Re)compute idx's digest on g's stream if it is stale (no host sync).
 dbl_status digest_refresh(const dbl_index *idx, dbl_graph *g);
 // After run_insert (count_changes): if the digest was current before the

@@ -27,10 +27,11 @@
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
-#include "internal.cuh"
+#include "insert_one.cuh"
 
 namespace dbl {
 
@@ -1760,32 +1761,40 @@ dbl_status query_sync(dbl_graph *g) {
 
 // ------------------------------------------------- per-call service (K6s) --
 //
-// A single query() call used to pay a kernel launch and a stream sync
-// (10.1 us on this box for an empty kernel, tools/ubench_api.cu) on top of
-// about a microsecond of work.  The service keeps one warp resident that
-// polls a mailbox in pinned host memory (round trip 2.4 us, same tool): the
-// host writes (u, v, flags) and a sequence number; the warp answers with the
-// same rules as K6 (digest, then both records, rules 1-4 in order,
-// queries.py:96-114) and, if they leave the query open, the bounded warp BFS
-// (queries.py:116-142); a query that outgrows it is handed back and answered
-// by the batch path.  The warp exits after SERVE_IDLE_NS without a request;
-// every other entry point of the library stops it first (serve_quiesce), so
-// it never runs beside a label or adjacency write or a cooperative launch.
+// A single query() or insert_edge() call used to pay a kernel launch and a
+// stream sync (10.1 us on this box for an empty kernel, tools/ubench_api.cu)
+// on top of a few microseconds of work.  The service keeps one CTA resident
+// that polls a mailbox in pinned host memory (round trip 2.4 us, same tool):
+//   * a query (u, v, flags): warp 0 applies K6's rules (digest, then both
+//     records, rules 1-4 in order, queries.py:96-114) and, if they leave it
+//     open, the bounded warp BFS (queries.py:116-142); a query that outgrows
+//     the BFS, or needs one after the service inserted edges (they sit in the
+//     pending log, which the BFS does not read), is handed back to the batch
+//     path;
+//   * an insert (u, v): the whole CTA runs K9 (insert_one.cuh,
+//     updates.py:112-137) against the pending log; a cone beyond K9's tables
+//     is handed back to the batch fixpoint, as from the K9 launch.
+// The CTA exits after SERVE_IDLE_NS without a request; every other entry
+// point of the library stops it first (serve_quiesce), so it never runs
+// beside another label or adjacency write or a cooperative launch.  Records
+// and digests are read L2-coherently (.cg): the service writes them itself.
+//
 // Request and answer are one 16-byte word each, written and read with single
 // vector accesses (one PCIe transaction each way); the sequence number is
 // the last word the host writes (x86 keeps store order), so a request read
-// with the new sequence number also holds its own (u, v, flags).
+// with the new sequence number also holds its own fields.
 struct alignas(64) ServeBox {
-    uint32_t u, v, opflags, seq, pad0[12];              // host -> device: opflags = op << 16 | flags
+    uint32_t u, v, opflags, seq, pad0[12];              // host -> device: op << 16 | (flags or pending count)
     uint32_t code, visited, status, rseq, pad1[12];     // device -> host (own line)
-    uint32_t alive, pad2[15];
+    OneOut ins;                                         // insert result (written before the answer word)
+    uint32_t alive, pad2[3];
 };
-enum { SERVE_QUERY = 1, SERVE_STOP = 2 };
+enum { SERVE_QUERY = 1, SERVE_STOP = 2, SERVE_INSERT = 3 };
 enum { SERVE_OK = 0, SERVE_FALLBACK = 1 };
 #ifndef DBL_SERVE
-#define DBL_SERVE 1                 // 0: single queries take the launch + sync path
+#define DBL_SERVE 1                 // 0: single calls take the launch + sync path
 #endif
-constexpr uint64_t SERVE_IDLE_NS = 2000000;   // the warp exits after 2 ms without a request
+constexpr uint64_t SERVE_IDLE_NS = 2000000;   // the CTA exits after 2 ms without a request
 
 __device__ __forceinline__ uint64_t serve_clock() {
     uint64_t t;
@@ -1796,88 +1805,129 @@ __device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+template <int RW, int RS>
+__device__ __forceinline__ void load_record_cg(const uint64_t *p, uint64_t (&r)[RW]) {
+    constexpr int V4 = RS % 4 == 0 ? RW / 4 * 4 : 0;
+#pragma unroll
+    for (int k = 0; k < V4; k += 4)
+        asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(r[k]), "=l"(r[k + 1]), "=l"(r[k + 2]), "=l"(r[k + 3]) : "l"(p + k));
+#pragma unroll
+    for (int k = V4; k < RW; k += 2)
+        asm volatile("ld.global.cg.v2.u64 {%0,%1}, [%2];" : "=l"(r[k]), "=l"(r[k + 1]) : "l"(p + k));
+}
+
+struct ServeArgs {
+    uint64_t *rec;
+    const uint32_t *dig;    // current digest or nullptr (inserts keep it current)
+    uint32_t n;
+    Adj fwd, rev;
+    uint64_t *pend;         // single-edge log (device)
+    ServeBox *box;          // device address of the pinned mailbox
+    uint32_t start_seq;
+};
+
 template <int WDL, int WBL>
-__global__ void __launch_bounds__(32, 1) serve_kernel(const uint64_t *__restrict__ rec,
-                                                      const uint32_t *__restrict__ dig, uint32_t n, const Adj adj,
-                                                      ServeBox *box, uint32_t start_seq) {
+__global__ void __launch_bounds__(ONE_THREADS, 1) serve_kernel(const ServeArgs A) {
     constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H), WD = WDL > 0 ? WDL : 1;
+    extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t wq[TB_Q];
     __shared__ uint64_t sdlo[WD], sbli[WBL], sblo[WBL];
-    const int lane = threadIdx.x & 31;
-    uint32_t last = start_seq;
+    __shared__ uint32_t req[4];
+    ServeBox *box = A.box;
+    const int tid = threadIdx.x, lane = tid & 31;
+    uint32_t last = A.start_seq;
+    bool dirty = false;   // the service inserted edges: its BFS would miss the pending ones
     uint64_t t_idle = serve_clock();
     for (;;) {
-        uint32_t seq = last, u = 0, v = 0, opflags = 0;
-        if (lane == 0) {
+        if (tid == 0) {
+            uint32_t u, v, opflags, seq;
             for (;;) {
                 asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(u), "=r"(v), "=r"(opflags), "=r"(seq) : "l"(box) : "memory");
                 if (seq != last || serve_clock() - t_idle > SERVE_IDLE_NS) break;
             }
+            req[0] = u; req[1] = v; req[2] = seq == last ? (SERVE_STOP << 16) : opflags; req[3] = seq;
         }
-        seq = __shfl_sync(FULL, seq, 0);
-        if (seq == last) break;   // idle
-        opflags = __shfl_sync(FULL, opflags, 0);
-        if ((opflags >> 16) != SERVE_QUERY) break;
-        u = __shfl_sync(FULL, u, 0);
-        v = __shfl_sync(FULL, v, 0);
-        const uint32_t flags = opflags & 0xffffu;
-        const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
-        const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
-        const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
-        uint32_t code = UNRESOLVED, vc = 0, status = SERVE_OK;
-        if (u >= n || v >= n) {
-            status = SERVE_FALLBACK;   // (the host checks the range first)
-        } else if (u == v) {
-            code = DBL_REFLEXIVE;
-        } else {
-            if (dig) code = digest_decide(__ldg(dig + u), __ldg(dig + v), use_dl, use_bl);
-            if (code == UNRESOLVED) {
-                uint64_t a[RW], b[RW];
-                load_record<RW, RS>(rec + (size_t)u * RS, a);
-                load_record<RW, RS>(rec + (size_t)v * RS, b);
-                uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
+        __syncthreads();
+        const uint32_t u = req[0], v = req[1], opflags = req[2], seq = req[3], op = opflags >> 16;
+        __syncthreads();
+        if (op == SERVE_INSERT) {
+            insert_one_body(A.rec, RS, H, WDL, A.n, u, v, A.fwd, A.rev, A.pend, opflags & 0xffffu, PEND_CAP,
+                            &box->ins, const_cast<uint32_t *>(A.dig), reinterpret_cast<OneShared *>(smem));
+            dirty = true;
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence_system();   // the OneOut lands before the answer word
+                asm volatile("st.relaxed.sys.global.v4.u32 [%0], {%1, %2, %3, %4};"
+                             ::"l"(&box->code), "r"(0u), "r"(0u), "r"((uint32_t)SERVE_OK), "r"(seq) : "memory");
+            }
+        } else if (op == SERVE_QUERY) {
+            if (tid < 32) {
+                const uint32_t flags = opflags & 0xffffu;
+                const bool use_dl = flags & DBL_F_USE_DL, use_bl = flags & DBL_F_USE_BL;
+                const bool thm1 = use_dl && (flags & DBL_F_THM1), thm2 = use_dl && (flags & DBL_F_THM2);
+                const bool prune_dl = use_dl && (flags & DBL_F_PRUNE_DL), prune_bl = use_bl && (flags & DBL_F_PRUNE_BL);
+                uint32_t code = UNRESOLVED, vc = 0, status = SERVE_OK;
+                if (u >= A.n || v >= A.n) {
+                    status = SERVE_FALLBACK;   // (the host checks the range first)
+                } else if (u == v) {
+                    code = DBL_REFLEXIVE;
+                } else {
+                    if (A.dig) code = digest_decide(__ldcg(A.dig + u), __ldcg(A.dig + v), use_dl, use_bl);
+                    if (code == UNRESOLVED) {
+                        uint64_t a[RW], b[RW];
+                        load_record_cg<RW, RS>(A.rec + (size_t)u * RS, a);
+                        load_record_cg<RW, RS>(A.rec + (size_t)v * RS, b);
+                        uint64_t r1 = 0, r2 = 0, r3 = 0, r4 = 0;
 #pragma unroll
-                for (int k = 0; k < WDL; ++k) {
-                    r1 |= a[H + k] & b[k];
-                    r3 |= b[H + k] & a[k];
-                    r4 |= (a[H + k] & a[k]) | (b[H + k] & b[k]);
-                }
+                        for (int k = 0; k < WDL; ++k) {
+                            r1 |= a[H + k] & b[k];
+                            r3 |= b[H + k] & a[k];
+                            r4 |= (a[H + k] & a[k]) | (b[H + k] & b[k]);
+                        }
 #pragma unroll
-                for (int k = 0; k < WBL; ++k) r2 |= (a[WDL + k] & ~b[WDL + k]) | (b[H + WDL + k] & ~a[H + WDL + k]);
-                if (use_dl && r1) code = DBL_DL_POSITIVE;
-                else if (use_bl && r2) code = DBL_BL_NEGATIVE;
-                else if (thm1 && r3) code = DBL_THM1_NEGATIVE;
-                else if (thm2 && r4) code = DBL_THM2_NEGATIVE;
-                if (code == UNRESOLVED) {
-                    if (lane == 0) {
+                        for (int k = 0; k < WBL; ++k)
+                            r2 |= (a[WDL + k] & ~b[WDL + k]) | (b[H + WDL + k] & ~a[H + WDL + k]);
+                        if (use_dl && r1) code = DBL_DL_POSITIVE;
+                        else if (use_bl && r2) code = DBL_BL_NEGATIVE;
+                        else if (thm1 && r3) code = DBL_THM1_NEGATIVE;
+                        else if (thm2 && r4) code = DBL_THM2_NEGATIVE;
+                        if (code == UNRESOLVED && dirty) {
+                            status = SERVE_FALLBACK;
+                        } else if (code == UNRESOLVED) {
+                            if (lane == 0) {
 #pragma unroll
-                        for (int k = 0; k < WDL; ++k) sdlo[k] = a[H + k];
+                                for (int k = 0; k < WDL; ++k) sdlo[k] = a[H + k];
 #pragma unroll
-                        for (int k = 0; k < WBL; ++k) {
-                            sbli[k] = b[WDL + k];
-                            sblo[k] = b[H + WDL + k];
+                                for (int k = 0; k < WBL; ++k) {
+                                    sbli[k] = b[WDL + k];
+                                    sblo[k] = b[H + WDL + k];
+                                }
+                            }
+                            __syncwarp();
+                            const int r = warp_query_bfs<WDL, WBL>(A.rec, A.fwd, u, v, sdlo, sbli, sblo, prune_dl,
+                                                                   prune_bl, Pivot{}, wq, &vc);
+                            if (r == 2) status = SERVE_FALLBACK;
+                            else code = r ? DBL_BFS_POSITIVE : DBL_BFS_NEGATIVE;
+                            __syncwarp();
                         }
                     }
-                    __syncwarp();
-                    const int r = warp_query_bfs<WDL, WBL>(rec, adj, u, v, sdlo, sbli, sblo, prune_dl, prune_bl,
-                                                           Pivot{}, wq, &vc);
-                    if (r == 2) status = SERVE_FALLBACK;
-                    else code = r ? DBL_BFS_POSITIVE : DBL_BFS_NEGATIVE;
-                    __syncwarp();
                 }
+                if (lane == 0)
+                    asm volatile("st.relaxed.sys.global.v4.u32 [%0], {%1, %2, %3, %4};"
+                                 ::"l"(&box->code), "r"(code), "r"(vc), "r"(status), "r"(seq) : "memory");
             }
+        } else {
+            break;   // stop, idle, or an unknown request
         }
-        if (lane == 0)
-            asm volatile("st.relaxed.sys.global.v4.u32 [%0], {%1, %2, %3, %4};"
-                         ::"l"(&box->code), "r"(code), "r"(vc), "r"(status), "r"(seq) : "memory");
         last = seq;
         t_idle = serve_clock();
     }
-    if (lane == 0) st_release_sys(&box->alive, 0u);
+    if (tid == 0) st_release_sys(&box->alive, 0u);
 }
 
-typedef void (*serve_fn)(const uint64_t *, const uint32_t *, uint32_t, const Adj, ServeBox *, uint32_t);
+typedef void (*serve_fn)(const ServeArgs);
 
 static serve_fn pick_serve(uint32_t wdl, uint32_t wbl) {
 #define DBL_SV(A, B) if (wdl == A && wbl == B) return serve_kernel<A, B>;
@@ -1887,10 +1937,17 @@ static serve_fn pick_serve(uint32_t wdl, uint32_t wbl) {
 }
 
 // One service at a time per process (it holds one SM); the mutex also
-// serialises concurrent single-query calls, which share the mailbox.
+// serialises concurrent single calls, which share the mailbox.
 static std::mutex g_srv_mu;
 static dbl_graph *g_srv = nullptr;
 static std::atomic<int> g_srv_on{0};
+
+static void post_stop(dbl_graph *g) {
+    volatile ServeBox *vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
+    vb->opflags = SERVE_STOP << 16;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    vb->seq = ++g->s_seq;
+}
 
 static void serve_stop_locked() {
     dbl_graph *g = g_srv;
@@ -1898,10 +1955,7 @@ static void serve_stop_locked() {
     g_srv = nullptr;
     g_srv_on.store(0, std::memory_order_release);
     if (!g->s_running) return;
-    volatile ServeBox *vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
-    vb->opflags = SERVE_STOP << 16;
-    std::atomic_thread_fence(std::memory_order_seq_cst);
-    vb->seq = ++g->s_seq;
+    post_stop(g);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaSetDevice(g->device);
@@ -1931,18 +1985,19 @@ static dbl_status serve_start_locked(const dbl_index *idx, dbl_graph *g, serve_f
     DBL_CUDA(cudaSetDevice(g->device));
     dbl_status s;
     if (g->s_running) {   // an exited (idle) or outdated service of this graph
-        volatile ServeBox *vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
-        vb->opflags = SERVE_STOP << 16;
-        std::atomic_thread_fence(std::memory_order_seq_cst);
-        vb->seq = ++g->s_seq;
+        post_stop(g);
         DBL_CUDA(cudaStreamSynchronize(g->sstream));
         g->s_running = false;
     }
-    // BFS fallbacks read the adjacency: fold the single-edge log in first,
+    // the query BFS reads the adjacency: fold the single-edge log in first,
     // and let the engine stream's queued work (builds, inserts) finish
+    set_stream(g->stream);
     if ((s = graph_flush_pending(g))) return s;
     DBL_CUDA(cudaStreamSynchronize(g->stream));
-    if ((s = g->sbox.ensure(sizeof(ServeBox) + 64))) return s;
+    const size_t smem = 2 * sizeof(OneShared);
+    int bps = 0;
+    if ((s = kernel_occupancy((const void *)fn, ONE_THREADS, smem, &bps))) return s;
+    if ((s = g->sbox.ensure(sizeof(ServeBox) + 64)) || (s = g->pend.ensure(PEND_CAP * 8 + 64))) return s;
     if (!g->sstream) DBL_CUDA(cudaStreamCreateWithFlags(&g->sstream, cudaStreamNonBlocking));
     ServeBox *hb = reinterpret_cast<ServeBox *>(g->sbox.p);
     ServeBox *db = nullptr;
@@ -1954,8 +2009,11 @@ static dbl_status serve_start_locked(const dbl_index *idx, dbl_graph *g, serve_f
     static_assert(offsetof(ServeBox, code) % 16 == 0 && offsetof(ServeBox, rseq) == offsetof(ServeBox, code) + 12,
                   "the answer is one 16-byte word");
     std::atomic_thread_fence(std::memory_order_seq_cst);
-    const uint32_t *dig = DBL_DIGEST && idx->digest_version == idx->version ? idx->digest.as<uint32_t>() : nullptr;
-    fn<<<1, 32, 0, g->sstream>>>(idx->rec.as<uint64_t>(), dig, idx->n, graph_fwd(g), db, g->s_seq);
+    ServeArgs A{const_cast<uint64_t *>(idx->rec.as<uint64_t>()),
+                DBL_DIGEST && idx->digest_version == idx->version ? idx->digest.as<uint32_t>() : nullptr,
+                idx->n, graph_fwd(g), graph_rev(g), g->pend.as<uint64_t>(), db, g->s_seq};
+    g->s_dig = A.dig != nullptr;
+    fn<<<1, ONE_THREADS, smem, g->sstream>>>(A);
     DBL_CHECK_LAUNCH("serve_kernel");
     g->s_running = true;
     g->s_idx = idx;
@@ -1965,33 +2023,30 @@ static dbl_status serve_start_locked(const dbl_index *idx, dbl_graph *g, serve_f
     return DBL_OK;
 }
 
-// Answer one query through the service.  *served = false: the service cannot
-// take it (label widths without a service kernel, or a BFS beyond its
-// bounds); the caller answers it on the batch path.
-dbl_status serve_query(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, uint32_t flags, uint8_t *code,
-                       uint32_t *visited, bool *served) {
+// Post one request and wait for its answer word (code, visited, status).
+// op = SERVE_INSERT sends the pending-log length (read after any restart,
+// which folds the log in).  *served = false: no service kernel for these
+// label widths.
+static dbl_status serve_call(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, uint32_t op,
+                             uint32_t flags, uint32_t ans[3], bool *served) {
     *served = false;
     const serve_fn fn = DBL_SERVE ? pick_serve(idx->wdl, idx->wbl) : nullptr;
     if (!fn) return DBL_OK;
-    std::lock_guard<std::mutex> lk(g_srv_mu);
     dbl_status s;
-    volatile ServeBox *vb = nullptr;
-    uint32_t ans[3] = {0, 0, 0};   // code, visited, status
-    bool answered = false;
-    for (int attempt = 0; attempt < 3 && !answered; ++attempt) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
         if (g_srv != g || !g->s_running || g->s_idx != idx || g->s_ver != idx->version ||
+            (op == SERVE_INSERT && g->n_pend >= PEND_CAP) ||
             reinterpret_cast<volatile ServeBox *>(g->sbox.p)->alive == 0) {
             if ((s = serve_start_locked(idx, g, fn))) return s;
         }
-        vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
+        volatile ServeBox *vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
         vb->u = u;
         vb->v = v;
-        vb->opflags = (SERVE_QUERY << 16) | (flags & 0xffffu);
+        vb->opflags = (op << 16) | ((op == SERVE_INSERT ? g->n_pend : flags) & 0xffffu);
         std::atomic_signal_fence(std::memory_order_seq_cst);   // the sequence number is stored last
         const uint32_t seq = ++g->s_seq;
         vb->seq = seq;
         const auto t0 = std::chrono::steady_clock::now();
-        bool done = false, exited = false;
         for (uint32_t it = 0;; ++it) {
             alignas(16) uint32_t w[4];   // one 16-byte load: the answer and its sequence number together
             _mm_store_si128(reinterpret_cast<__m128i *>(w),
@@ -2000,37 +2055,67 @@ dbl_status serve_query(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t 
                 ans[0] = w[0];
                 ans[1] = w[1];
                 ans[2] = w[2];
-                done = true;
-                break;
+                std::atomic_thread_fence(std::memory_order_acquire);
+                *served = true;
+                return DBL_OK;
             }
             if (vb->alive == 0) {   // went idle just before the request: relaunch, post again
-                exited = vb->rseq != seq;
-                if (!exited) { ans[0] = vb->code; ans[1] = vb->visited; ans[2] = vb->status; done = true; }
+                if (vb->rseq == seq) continue;
+                g->s_running = false;
+                cudaStreamSynchronize(g->sstream);
                 break;
             }
-            if ((it & 1023) == 1023 &&
-                std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+            if ((it & 1023) == 1023 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
                 serve_stop_locked();
-                set_error("query service did not answer within 2 s");
+                set_error("per-call service did not answer within 2 s");
                 return DBL_E_CUDA;
             }
         }
-        if (exited) {
-            g->s_running = false;
-            cudaStreamSynchronize(g->sstream);
-            continue;
-        }
-        answered = done;
     }
-    if (!answered) { set_error("query service failed to start"); return DBL_E_CUDA; }
+    set_error("per-call service failed to start");
+    return DBL_E_CUDA;
+}
+
+// Answer one query through the service.  *served = false: the caller answers
+// it on the batch path (no service kernel for these widths, or the service
+// handed it back).
+dbl_status serve_query(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, uint32_t flags, uint8_t *code,
+                       uint32_t *visited, bool *served) {
+    std::lock_guard<std::mutex> lk(g_srv_mu);
+    uint32_t ans[3];
+    dbl_status s = serve_call(idx, g, u, v, SERVE_QUERY, flags, ans, served);
+    if (s || !*served) return s;
     if (ans[2] != SERVE_OK) {
-        serve_stop_locked();   // the batch path takes this query (its BFS stages run on the engine stream)
+        *served = false;
+        serve_stop_locked();   // the batch path takes it (its BFS stages run on the engine stream)
         return DBL_OK;
     }
     *code = (uint8_t)ans[0];
     if (visited) *visited = ans[1];
-    *served = true;
     return DBL_OK;
+}
+
+dbl_status serve_insert(dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, dbl_update_stats *st, bool *done,
+                        uint32_t *dirs_done, bool *dig_ok, bool *served) {
+    std::lock_guard<std::mutex> lk(g_srv_mu);
+    *served = false;
+    if (idx->wdl + idx->wbl > (uint32_t)MAX_SHARD_WORDS) return DBL_OK;
+    uint32_t ans[3];
+    dbl_status s = serve_call(idx, g, u, v, SERVE_INSERT, 0, ans, served);
+    if (s || !*served) return s;
+    OneOut o;
+    const volatile OneOut *vo = &reinterpret_cast<volatile ServeBox *>(g->sbox.p)->ins;
+    std::memcpy(&o, const_cast<const OneOut *>(vo), sizeof(o));
+    // labels may have changed: the version moves; the service wrote the
+    // digest bits too iff it holds the digest, and it reads the new labels
+    // itself, so it stays valid for the next call
+    *dig_ok = g->s_dig;
+    ++idx->version;
+    if (g->s_dig) idx->digest_version = idx->version;
+    g->s_ver = idx->version;
+    s = insert_edge_outcome(g, o, st, done, dirs_done);
+    if (s || !*done) serve_stop_locked();   // the batch fixpoint finishes it (cooperative launch)
+    return s;
 }
 
 }  // namespace dbl
