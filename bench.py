@@ -423,7 +423,7 @@ def run_ours(args, rank, world, local_rank, gloo):
     ins_achieved = statistics.mean(b / (t / 1e3) / 1e9 for b, t in zip(ins_bytes, ins_ms))
 
     # single-edge insert_edge (updates.py:112-137) through the shim, per call
-    su, sv = W.gen_insert_workload(src, dst, n, 300, 90, exclude=prev)
+    su, sv = W.gen_insert_workload(src, dst, n, 2020, 90, exclude=prev)
     for u_, v_ in zip(su[:20].tolist(), sv[:20].tolist()):
         E.insert_edge(g, idx, u_, v_)
     barrier()
@@ -752,7 +752,33 @@ def python_reference(n, src, dst, oidx, qu, qv, cores) -> dict:
     names = [a.value for a in R.AnsweredBy]
     codes = np.array([names.index(o.answered_by.value) for o in outs], np.uint8)
     oc, _ = O.OracleGraph(n, src, dst).query_batch(oidx, qu, qv, threads=cores)
+    # the per-call API: query() and insert_edge() one call at a time (the
+    # engine's api_paths.single_query / inserts.single_insert_edge), at most
+    # ~10 s each; the inserts come last (they change the reference's graph)
+    t0 = time.perf_counter()
+    nq = 0
+    for u, v in pairs[:50_000]:
+        R.query(g, idx, u, v)
+        nq += 1
+        if nq % 1000 == 0 and time.perf_counter() - t0 > 10:
+            break
+    single_q = nq / (time.perf_counter() - t0)
+    from paper_2101_09441_b200 import workload as W
+    su, sv = W.gen_insert_workload(src, dst, n, 2300, 90)
+    t0 = time.perf_counter()
+    ni = 0
+    for u, v in zip(su.tolist(), sv.tolist()):
+        R.insert_edge(g, idx, u, v)
+        ni += 1
+        if time.perf_counter() - t0 > 10:
+            break
+    single_ins = ni / (time.perf_counter() - t0)
     return {"value_workers_1": one, "value_workers_all": many, "unit": "queries/s", "cores": cores,
+            "single_query": {"value": single_q, "unit": "queries/s", "calls": nq,
+                             "api": "dblreach.query(g, idx, u, v) per call"},
+            "single_insert_edge": {"value": single_ins, "unit": "edges/s", "calls": ni,
+                                   "api": "dblreach.insert_edge(g, idx, u, v) per call, edges of "
+                                          "workload.gen_insert_workload(seed 90) on the base cfg2 graph"},
             "codes_equal_port": bool(np.array_equal(codes, oc)),
             "sample": f"dblreach 0.1.0 (unmodified, baseline/_ref): query_batch workers=1 on {k} pairs, "
                       f"workers={cores} on the 1M batch; labels via load_index of a DBLIDX01 snapshot of "
