@@ -269,7 +269,7 @@ extern "C" const char *dbl_last_error(void) { return g_last_error.c_str(); }
 extern "C" int dbl_version(void) { return 1; }
 extern "C" uint64_t dbl_kernel_launches(void) { return g_launches.load(); }
 extern "C" dbl_status dbl_release_cached_memory(void) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     pool_trim();
     return DBL_OK;
 }
@@ -387,7 +387,7 @@ static dbl_status index_create(const dbl_graph *gc, const dbl_config *cfg, const
 extern "C" dbl_status dbl_index_create(const dbl_graph *gc, const dbl_config *cfg, const uint32_t *landmarks,
                                        const uint8_t *leaf_flags, const uint32_t *bucket, const uint32_t *ovr_ids,
                                        const uint32_t *ovr_buckets, uint32_t n_ovr, dbl_index **out) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     return index_create(gc, cfg, landmarks, leaf_flags, bucket, ovr_ids, ovr_buckets, n_ovr, out);
 }
 
@@ -395,7 +395,7 @@ extern "C" dbl_status dbl_index_build(const dbl_graph *gc, const dbl_config *cfg
                                       const uint8_t *leaf_flags, const uint32_t *bucket,
                                       const uint32_t *ovr_ids, const uint32_t *ovr_buckets, uint32_t n_ovr,
                                       dbl_index **out) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (out) *out = nullptr;
     dbl_index *idx = nullptr;
     dbl_status s = index_create(gc, cfg, landmarks, leaf_flags, bucket, ovr_ids, ovr_buckets, n_ovr, &idx, false);
@@ -411,7 +411,7 @@ extern "C" dbl_status dbl_index_build(const dbl_graph *gc, const dbl_config *cfg
 }
 
 extern "C" dbl_status dbl_index_rebuild(const dbl_graph *gc, dbl_index *idx) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     dbl_status s = check_pair(idx, gc);
     if (s) return s;
     dbl_graph *g = const_cast<dbl_graph *>(gc);
@@ -425,7 +425,7 @@ extern "C" dbl_status dbl_index_rebuild(const dbl_graph *gc, dbl_index *idx) {
 
 extern "C" dbl_status dbl_index_build_words(const dbl_graph *gc, dbl_index *idx, const uint32_t *words,
                                             uint32_t nwords) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     dbl_status s = check_pair(idx, gc);
     if (s) return s;
     for (uint32_t i = 0; i < nwords; ++i)
@@ -439,7 +439,7 @@ extern "C" dbl_status dbl_index_build_words(const dbl_graph *gc, dbl_index *idx,
 }
 
 extern "C" dbl_status dbl_index_free(dbl_index *idx) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx) return DBL_OK;
     cudaSetDevice(idx->device);
     cudaDeviceSynchronize();
@@ -465,7 +465,7 @@ extern "C" dbl_status dbl_index_info(const dbl_index *idx, uint32_t *n, dbl_conf
 
 extern "C" dbl_status dbl_index_metadata(const dbl_index *idx, uint32_t *landmarks, uint8_t *leaf_flags,
                                          uint32_t *bucket) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(idx->device));
     set_stream(nullptr);
@@ -477,7 +477,7 @@ extern "C" dbl_status dbl_index_metadata(const dbl_index *idx, uint32_t *landmar
 
 extern "C" dbl_status dbl_index_export(const dbl_index *idx, uint64_t *dl_in, uint64_t *dl_out, uint64_t *bl_in,
                                        uint64_t *bl_out) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(idx->device));
     set_stream(nullptr);
@@ -502,7 +502,7 @@ extern "C" dbl_status dbl_index_export(const dbl_index *idx, uint64_t *dl_in, ui
 
 extern "C" dbl_status dbl_index_import(dbl_index *idx, const uint64_t *dl_in, const uint64_t *dl_out,
                                        const uint64_t *bl_in, const uint64_t *bl_out) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(idx->device));
     set_stream(nullptr);
@@ -529,7 +529,7 @@ extern "C" dbl_status dbl_index_import(dbl_index *idx, const uint64_t *dl_in, co
 }
 
 extern "C" dbl_status dbl_index_equal(const dbl_index *a, const dbl_index *b, int *out_equal) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!a || !b || !out_equal) { set_error("null argument"); return DBL_E_ARG; }
     *out_equal = 0;
     if (a->n != b->n || a->cfg.k != b->cfg.k || a->cfg.k_prime != b->cfg.k_prime) return DBL_OK;
@@ -566,7 +566,7 @@ static dbl_status grow_buf(DevBuf &b, size_t old_bytes, size_t new_bytes, int fi
 }
 
 extern "C" dbl_status dbl_index_grow(dbl_index *idx, uint32_t n) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx) { set_error("null index"); return DBL_E_ARG; }
     if (n < idx->n) { set_error("index cannot shrink"); return DBL_E_CONFIG; }
     if (n == idx->n) return DBL_OK;
@@ -583,7 +583,7 @@ extern "C" dbl_status dbl_index_grow(dbl_index *idx, uint32_t n) {
 }
 
 extern "C" dbl_status dbl_graph_add_vertices(dbl_graph *g, uint32_t count) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g) { set_error("null graph"); return DBL_E_ARG; }
     if (!count) return DBL_OK;
     if ((uint64_t)g->n + count >= 0xffffffffull) { set_error("vertex count overflow"); return DBL_E_CONFIG; }
@@ -760,7 +760,7 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
         if ((s = serve_query(idx, g, hu, hv, flags, codes, visited, &served))) return s;
         if (served) return DBL_OK;
     }
-    serve_quiesce();
+    ServeBlock no_service_;   // batch path: no per-call service runs during it
     DBL_CUDA(cudaSetDevice(g->device));
     if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
     set_stream(g->stream);
@@ -815,7 +815,7 @@ extern "C" dbl_status dbl_query(const dbl_index *idx, const dbl_graph *g, const 
 extern "C" dbl_status dbl_query_async(const dbl_index *idx, const dbl_graph *g, const uint32_t *u,
                                       const uint32_t *v, uint64_t count, uint32_t flags, uint8_t *codes,
                                       uint32_t *visited) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     return query_impl(idx, g, u, v, count, flags, codes, visited, DBL_MEM_DEVICE, false);
 }
 
@@ -830,7 +830,7 @@ extern "C" dbl_status dbl_query_async(const dbl_index *idx, const dbl_graph *g, 
 extern "C" dbl_status dbl_query_multi(const dbl_index *const *idx, const dbl_graph *const *g, uint32_t ndev,
                                       const uint32_t *u, const uint32_t *v, uint64_t count, uint32_t flags,
                                       uint8_t *codes, uint32_t *visited, dbl_mem mem) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx || !g || ndev == 0) { set_error("null handle list"); return DBL_E_ARG; }
     if (count && (!u || !v || !codes)) { set_error("null argument"); return DBL_E_ARG; }
     if (mem == DBL_MEM_DEVICE && count) {
@@ -938,8 +938,12 @@ extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, 
     uint32_t dirs_done = 0;
     // the per-call service runs K9 in its resident CTA (no launch, no sync)
     if ((s = serve_insert(idx, g, u, v, &st, &done, &dirs_done, &dig_ok, &served))) return s;
+    if (served && done) {
+        if (stats) *stats = st;
+        return DBL_OK;
+    }
+    ServeBlock no_service_;   // K9 launch and the batch fixpoint: no per-call service runs during them
     if (!served) {
-        serve_quiesce();
         DBL_CUDA(cudaSetDevice(g->device));
         set_stream(g->stream);
         // the fast path ORs each written label delta's digest bits into the
@@ -984,7 +988,7 @@ extern "C" dbl_status dbl_insert_edge(dbl_index *idx, dbl_graph *g, uint32_t u, 
 
 extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
                                        uint64_t count, dbl_mem mem, dbl_batch_stats *stats) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     dbl_status s = check_pair(idx, g);
     if (s) return s;
     dbl_batch_stats st{};
@@ -1092,7 +1096,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
 
 extern "C" dbl_status dbl_work_model(const dbl_index *idx, const dbl_graph *gc, uint64_t *V, uint64_t *E,
                                      uint32_t *levels) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     dbl_status s = check_pair(idx, gc);
     if (s) return s;
     if (!V || !E || !levels) { set_error("null argument"); return DBL_E_ARG; }
@@ -1127,7 +1131,7 @@ __global__ void unpack_words_kernel(uint64_t *__restrict__ rec, uint32_t rs, uin
 // slab (nw x n u64, device memory) -- the unit of the NCCL allgather.
 extern "C" dbl_status dbl_index_pack_words(const dbl_index *idx, const uint32_t *words, uint32_t nw,
                                            uint64_t *dev_slab, void *stream) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx || (nw && (!words || !dev_slab))) { set_error("null argument"); return DBL_E_ARG; }
     if (!nw || !idx->n) return DBL_OK;
     DBL_CUDA(cudaSetDevice(idx->device));
@@ -1149,7 +1153,7 @@ extern "C" dbl_status dbl_index_pack_words(const dbl_index *idx, const uint32_t 
 // Inverse of dbl_index_pack_words: scatter a slab (K5 record interleave).
 extern "C" dbl_status dbl_index_unpack_words(dbl_index *idx, const uint32_t *words, uint32_t nw,
                                              const uint64_t *dev_slab, void *stream) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx || (nw && (!words || !dev_slab))) { set_error("null argument"); return DBL_E_ARG; }
     if (!nw || !idx->n) return DBL_OK;
     DBL_CUDA(cudaSetDevice(idx->device));
@@ -1176,7 +1180,7 @@ extern "C" dbl_status dbl_index_unpack_words(dbl_index *idx, const uint32_t *wor
 // call and not repeated earlier in the batch.
 extern "C" dbl_status dbl_graph_add_edges(dbl_graph *g, const uint32_t *u, const uint32_t *v, uint64_t count,
                                           uint64_t *out_inserted) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g || (count && (!u || !v))) { set_error("null argument"); return DBL_E_ARG; }
     if (out_inserted) *out_inserted = 0;
     if (!count) return DBL_OK;
@@ -1246,7 +1250,7 @@ __global__ void label_tests_kernel(const uint64_t *__restrict__ rec, uint32_t wd
 // batch of (x, y) pairs, host in/out.
 extern "C" dbl_status dbl_label_tests(const dbl_index *idx, const uint32_t *x, const uint32_t *y, uint64_t count,
                                       uint8_t *out_dl_intersec, uint8_t *out_bl_contain) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx || (count && (!x || !y || !out_dl_intersec || !out_bl_contain))) {
         set_error("null argument");
         return DBL_E_ARG;

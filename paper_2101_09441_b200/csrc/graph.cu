@@ -489,7 +489,7 @@ using namespace dbl;
 
 extern "C" dbl_status dbl_graph_create(uint32_t n, const uint32_t *src, const uint32_t *dst,
                                        uint64_t m, dbl_mem mem, int device, dbl_graph **out) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!out || (m && (!src || !dst))) { set_error("null argument"); return DBL_E_ARG; }
     *out = nullptr;
     DBL_CUDA(cudaSetDevice(device));
@@ -553,7 +553,7 @@ extern "C" dbl_status dbl_graph_create(uint32_t n, const uint32_t *src, const ui
 }
 
 extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g) return DBL_OK;
     cudaSetDevice(g->device);
     serve_release(g);
@@ -590,7 +590,7 @@ extern "C" dbl_status dbl_graph_info(const dbl_graph *g, uint32_t *n, uint64_t *
 }
 
 extern "C" dbl_status dbl_graph_degrees(const dbl_graph *g, uint32_t *indeg, uint32_t *outdeg) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g || !indeg || !outdeg) { set_error("null argument"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
     if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
@@ -622,7 +622,7 @@ __global__ void has_edges_kernel(const uint32_t *__restrict__ u, const uint32_t 
 
 extern "C" dbl_status dbl_graph_has_edges(const dbl_graph *g, const uint32_t *u, const uint32_t *v,
                                           uint64_t count, uint8_t *out) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g || (count && (!u || !v || !out))) { set_error("null argument"); return DBL_E_ARG; }
     if (!count) return DBL_OK;
     DBL_CUDA(cudaSetDevice(g->device));
@@ -663,7 +663,7 @@ __global__ void split_keys_kernel(const uint64_t *__restrict__ keys, uint64_t m,
 }
 
 extern "C" dbl_status dbl_graph_edges(const dbl_graph *g, uint32_t *src, uint32_t *dst) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g) { set_error("null graph"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
     if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;
@@ -698,7 +698,7 @@ extern "C" dbl_status dbl_graph_edges(const dbl_graph *g, uint32_t *src, uint32_
 }
 
 extern "C" dbl_status dbl_sync(const dbl_graph *g) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g) { set_error("null graph"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
     set_stream(g->stream);
@@ -749,7 +749,7 @@ __global__ void add_ptr_kernel(const uint32_t *__restrict__ a, const uint32_t *_
 }
 
 extern "C" dbl_status dbl_graph_adjacency(const dbl_graph *g, int reverse, uint32_t *ptr, uint32_t *col) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g || !ptr) { set_error("null argument"); return DBL_E_ARG; }
     DBL_CUDA(cudaSetDevice(g->device));
     if (dbl_status fs = graph_flush_pending(const_cast<dbl_graph *>(g))) return fs;

@@ -388,10 +388,18 @@ dbl_status query_finish(dbl_graph *g, uint32_t *err_out, bool *dense_out);
 dbl_status query_err_to(dbl_graph *g, uint32_t *dst4);
 bool chunk_needs_dense(const uint32_t *w4);
 dbl_status query_sync(dbl_graph *g);
-// Stop every running per-call query service (each ABI entry that may write
-// labels or adjacency, launch a cooperative kernel or free a handle calls
-// this first; a no-op while none runs).
+// Stop every running per-call service (a no-op while none runs).
 void serve_quiesce();
+// While one exists (any thread), no per-call service runs or starts: every
+// ABI entry except the single-call paths holds one for its duration, so no
+// service runs beside a label or adjacency write, a cooperative launch or a
+// handle release.
+struct ServeBlock {
+    ServeBlock();
+    ~ServeBlock();
+    ServeBlock(const ServeBlock &) = delete;
+    ServeBlock &operator=(const ServeBlock &) = delete;
+};
 // Answer one host query through the service; *served = false: take the batch path.
 dbl_status serve_query(const dbl_index *idx, dbl_graph *g, uint32_t u, uint32_t v, uint32_t flags, uint8_t *code,
                        uint32_t *visited, bool *served);

@@ -53,6 +53,10 @@ constexpr uint8_t UNRESOLVED = 0xff;
 #ifndef DBL_NO_PIVOT_PRUNE
 #define DBL_NO_PIVOT_PRUNE 0   // 1: BFS fallbacks ignore the pivot sets
 #endif
+#ifndef DBL_LEAN_THREADS
+#define DBL_LEAN_THREADS 256   // K6 CTA size
+#endif
+constexpr int LEAN_THREADS = DBL_LEAN_THREADS;
 #ifndef DBL_DIGEST
 #define DBL_DIGEST 1           // 0: query kernels never read the label digest
 #endif
@@ -1289,7 +1293,7 @@ __device__ __forceinline__ void lean_pend(bool unres, uint32_t i, uint32_t *__re
 // (2 x 80 bytes at k = 256) spill at that cap, so they trade occupancy for
 // registers
 template <int WDL, int WBL, int QPT>
-__global__ void __launch_bounds__(256, (QPT > 1 ? 4 : (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_WIDE)))
+__global__ void __launch_bounds__(LEAN_THREADS, (QPT > 1 ? 4 : (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_WIDE)) * 256 / LEAN_THREADS)
 label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj, const QueryDesc qd,
                   uint32_t *__restrict__ pending, uint32_t *__restrict__ counters, const HardArgs ha) {
     // the per-thread BFS pays off for k <= 64; with wider labels (cfg5:
@@ -1398,7 +1402,7 @@ label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj, c
         // (the pivot prune is left out here: these BFS expand <= 3 vertices
         // on R-MAT, and its bitmap test adds a dependent load before each
         // record read -- measured 24.2 vs 23.1 us per 1M batch on cfg2)
-        __shared__ uint32_t wq[256 / 32][TB_Q];
+        __shared__ uint32_t wq[LEAN_THREADS / 32][TB_Q];
         auto answer = [&](uint32_t t) {   // one warp per queued query, neighbours in parallel
             const uint32_t i = dq.i[t];
             uint32_t vc = 0;
@@ -1651,17 +1655,17 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     if (count && (DBL_TBFS_ALL || DBL_LEAN_WIDE || idx->wdl <= 1 || qd.dig) &&
         pick_lean(idx->wdl, idx->wbl, qpt4, lean, bfsw, wsmem)) {
         int lbps = 1, wbps = 1;
-        if ((s = kernel_occupancy((const void *)lean, 256, 0, &lbps)) ||
+        if ((s = kernel_occupancy((const void *)lean, LEAN_THREADS, 0, &lbps)) ||
             (s = kernel_occupancy((const void *)bfsw, FUSED_THREADS, wsmem, &wbps)))
             return s;
         uint32_t *wovf = pending + 2 * g->q_pending_cap + 32;
         const HardArgs ha{hp.grid, hp.dctas, (uint32_t)hp.smem, (uint32_t)hp.dsmem, idx->wdl, idx->wbl, ovf,
                           hp.ws, g->sm_count * wbps, (uint32_t)wsmem, wovf};
-        const uint64_t per = qpt4 ? DBL_QPT_HOST * 256 : 256;   // queries per CTA per step
+        const uint64_t per = qpt4 ? DBL_QPT_HOST * LEAN_THREADS : LEAN_THREADS;   // queries per CTA per step
         uint32_t lgrid = (uint32_t)((count + per - 1) / per);
         if (lgrid > (uint32_t)(g->sm_count * lbps)) lgrid = (uint32_t)(g->sm_count * lbps);
         if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
-        lean<<<lgrid, 256, 0, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);
+        lean<<<lgrid, LEAN_THREADS, 0, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);
         DBL_CHECK_LAUNCH("label_lean_kernel");
         if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[3], g->stream));
         g->q_timed_bfs = false;
@@ -1970,6 +1974,13 @@ void serve_quiesce() {
     serve_stop_locked();
 }
 
+static std::atomic<int> g_srv_block{0};
+ServeBlock::ServeBlock() {
+    g_srv_block.fetch_add(1, std::memory_order_acq_rel);
+    serve_quiesce();
+}
+ServeBlock::~ServeBlock() { g_srv_block.fetch_sub(1, std::memory_order_acq_rel); }
+
 // Release the graph's service resources (dbl_graph_free, after serve_quiesce).
 void serve_release(dbl_graph *g) {
     if (g->sstream) {
@@ -2031,7 +2042,9 @@ static dbl_status serve_call(const dbl_index *idx, dbl_graph *g, uint32_t u, uin
                              uint32_t flags, uint32_t ans[3], bool *served) {
     *served = false;
     const serve_fn fn = DBL_SERVE ? pick_serve(idx->wdl, idx->wbl) : nullptr;
-    if (!fn) return DBL_OK;
+    // another thread is inside a library call: take the launch path (a
+    // service started now would be stopped by it anyway)
+    if (!fn || g_srv_block.load(std::memory_order_acquire) > 0) return DBL_OK;
     dbl_status s;
     for (int attempt = 0; attempt < 3; ++attempt) {
         if (g_srv != g || !g->s_running || g->s_idx != idx || g->s_ver != idx->version ||
@@ -2125,7 +2138,7 @@ using namespace dbl;
 // The index's query digest (n u32, host), recomputed first if stale.
 extern "C" dbl_status dbl_index_digest(const dbl_index *idx, const dbl_graph *gc, uint32_t *out,
                                        int *was_current) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx || !gc || (!out && idx->n)) { set_error("null argument"); return DBL_E_ARG; }
     if (was_current) *was_current = idx->digest_version == idx->version;
     if (idx->n != gc->n) { set_error("graph and index vertex counts differ"); return DBL_E_MISMATCH; }
@@ -2145,7 +2158,7 @@ extern "C" dbl_status dbl_index_digest(const dbl_index *idx, const dbl_graph *gc
 // kernels (per-warp BFS table overflow or generic widths), [1] range-error
 // flag, [3] groups re-run densely.
 extern "C" dbl_status dbl_query_counters(const dbl_graph *g, uint32_t *out8) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g || !out8) { set_error("null argument"); return DBL_E_ARG; }
     if (!g->q_counters.p) { for (int i = 0; i < 8; ++i) out8[i] = 0; return DBL_OK; }
     DBL_CUDA(cudaSetDevice(g->device));

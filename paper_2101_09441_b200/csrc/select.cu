@@ -603,7 +603,7 @@ using namespace dbl;
 
 extern "C" dbl_status dbl_leaf_hash(const uint64_t *ids, uint64_t count, uint32_t k_prime,
                                     uint64_t seed, uint32_t *out, int device) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (k_prime < 1) { set_error("k_prime must be >= 1"); return DBL_E_CONFIG; }
     if (!count) return DBL_OK;
     if (!ids || !out) { set_error("null argument"); return DBL_E_ARG; }
@@ -626,7 +626,7 @@ extern "C" dbl_status dbl_leaf_hash(const uint64_t *ids, uint64_t count, uint32_
 
 extern "C" dbl_status dbl_select_landmarks(const dbl_graph *g, uint32_t k, int32_t strategy,
                                            uint32_t *out_ids) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g || (k && !out_ids)) { set_error("null argument"); return DBL_E_ARG; }
     if (k > g->n) { set_error("k exceeds vertex count"); return DBL_E_CONFIG; }
     if (!k) return DBL_OK;
@@ -681,7 +681,7 @@ extern "C" dbl_status dbl_select_leaves(const dbl_graph *g, uint64_t threshold, 
                                         uint64_t hash_seed, const uint32_t *ovr_ids,
                                         const uint32_t *ovr_buckets, uint32_t n_ovr,
                                         uint8_t *out_flags, uint32_t *out_bucket) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!g || (g->n && (!out_flags || !out_bucket)) || (n_ovr && (!ovr_ids || !ovr_buckets))) {
         set_error("null argument");
         return DBL_E_ARG;
@@ -752,7 +752,7 @@ __global__ void rmat_kernel(uint32_t scale, uint64_t m, uint64_t seed, uint32_t 
 
 extern "C" dbl_status dbl_rmat_generate(uint32_t scale, uint64_t m, uint64_t seed, double a, double b, double c,
                                         uint32_t *dev_src, uint32_t *dev_dst, int device) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (scale < 1 || scale > 31 || (m && (!dev_src || !dev_dst))) { set_error("bad R-MAT arguments"); return DBL_E_ARG; }
     if (!m) return DBL_OK;
     DBL_CUDA(cudaSetDevice(device));

@@ -107,7 +107,7 @@ using namespace dbl;
 extern "C" dbl_status dbl_verify(const dbl_index *idx, const dbl_graph *gc, int exhaustive, uint64_t max_out,
                                  uint64_t *out_count, uint32_t *out_vertex, uint8_t *out_half,
                                  uint64_t *out_expected, uint64_t *out_actual) {
-    serve_quiesce();   // no per-call query service runs beside this call
+    ServeBlock no_service_;   // no per-call service runs during this call
     if (!idx || !gc || !out_count) { set_error("null argument"); return DBL_E_ARG; }
     if (idx->n != gc->n) {
         set_error("graph and index vertex counts differ");

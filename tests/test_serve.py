@@ -96,3 +96,37 @@ def test_single_call_range_error(E):
     with pytest.raises(E.VertexRangeError):
         E.query(g, idx, 1, n)
     assert code_of(E, E.query(g, idx, 3, 3)) == 0
+
+
+def test_single_calls_beside_other_threads(E):
+    """Single queries on one thread while another thread builds and inserts on
+    another graph (cooperative launches): the service never runs beside them
+    (every other call blocks it), answers stay exact, nothing stalls."""
+    import threading
+    n = 1 << 12
+    g = E.DynamicGraph.from_edges(n, *W.rmat_edges(12, 8, 35))
+    idx = E.build_index(g)
+    rng = np.random.default_rng(6)
+    qu = rng.integers(0, n, 4000, dtype=np.uint32)
+    qv = rng.integers(0, n, 4000, dtype=np.uint32)
+    ref, _ = E.query_codes(g, idx, qu, qv)
+    g2 = E.DynamicGraph.from_edges(n, *W.rmat_edges(12, 8, 36))
+    errors = []
+
+    def writer():
+        try:
+            r = np.random.default_rng(7)
+            for _ in range(15):
+                i2 = E.build_index(g2)
+                E.insert_edges(g2, i2, r.integers(0, n, 500, dtype=np.uint32), r.integers(0, n, 500, dtype=np.uint32))
+                assert i2.labels_equal(E.rebuild_index(g2, i2))
+        except Exception as e:   # noqa: BLE001
+            errors.append(e)
+
+    t = threading.Thread(target=writer)
+    t.start()
+    got = np.array([code_of(E, E.query(g, idx, u, v)) for u, v in zip(qu.tolist(), qv.tolist())], np.uint8)
+    t.join(timeout=120)
+    assert not t.is_alive(), "writer thread stalled"
+    assert not errors, errors
+    np.testing.assert_array_equal(got, ref)
