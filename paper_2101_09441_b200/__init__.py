@@ -9,7 +9,7 @@ missing library or device raises DeviceError.
 from .errors import (ConfigError, DblError, DeviceError, EdgeListFormatError,
                      IndexGraphMismatchError, MissingEdgeError, NotFittedError,
                      VertexRangeError, WorkloadExhaustedError)
-from .graph import DynamicGraph, as_device_graph
+from .graph import DynamicGraph, as_device_graph, load_edge_list
 from .labels import (DblIndex, IndexConfig, LandmarkSet, LandmarkStrategy, LeafSets,
                      bl_contain, build_index, dl_intersec, leaf_hash, leaf_hash_batch,
                      rebuild_in_place, rebuild_index, select_landmarks, select_leaves)
@@ -30,7 +30,7 @@ __all__ = [
     "DL_ONLY", "DblError", "DblIndex", "DeviceError", "DynamicGraph", "EdgeListFormatError",
     "IndexConfig", "IndexGraphMismatchError", "LandmarkSet", "LandmarkStrategy", "LeafSets",
     "MissingEdgeError", "NotFittedError", "Outcomes", "QueryFlags", "QueryOutcome",
-    "UpdateStats", "VertexRangeError", "WorkloadExhaustedError", "as_device_graph",
+    "UpdateStats", "VertexRangeError", "WorkloadExhaustedError", "as_device_graph", "load_edge_list",
     "bl_contain", "build_index", "default_workers", "dl_intersec", "explain", "insert_edge",
     "insert_edges", "insert_vertex", "leaf_hash", "leaf_hash_batch", "query", "query_batch",
     "query_codes", "rebuild_in_place", "rebuild_index", "select_landmarks", "select_leaves",

@@ -213,6 +213,34 @@ class DynamicGraph:
     def vertices(self) -> range:
         return range(self._n)
 
+    def _lists(self, reverse: bool) -> list[list[int]]:
+        key = (self._n, self.edge_count, self.version, reverse)
+        cache = getattr(self, "_list_cache", None)
+        if cache is not None and cache[0] == key:
+            return cache[1]
+        if self._h is None:
+            lists: list[list[int]] = [[] for _ in range(self._n)]
+            for u, v in self._pending:
+                (lists[v] if reverse else lists[u]).append(u if reverse else v)
+        else:
+            ptr, col = self.adjacency(reverse)
+            cl = col.tolist()
+            p = ptr.tolist()
+            lists = [cl[p[i]:p[i + 1]] for i in range(self._n)]
+        self._list_cache = (key, lists)
+        return lists
+
+    @property
+    def forward(self) -> list[list[int]]:
+        """Out-adjacency lists (graph.py:36), a read-only host copy sorted by id
+        (the reference keeps insertion order; reachability is the same)."""
+        return self._lists(False)
+
+    @property
+    def reverse(self) -> list[list[int]]:
+        """In-adjacency lists (graph.py:37), read-only host copy."""
+        return self._lists(True)
+
     def to_original(self, dense: int) -> int:
         self._check_vertex(dense)
         return self.original_ids[dense] if self.original_ids else dense
@@ -260,6 +288,11 @@ def load_edge_list(source, gzipped: bool | None = None, *, device: int = 0) -> D
     elif isinstance(source, bytes):
         raw = gzip.decompress(source) if (gzipped or (gzipped is None and source[:2] == b"\x1f\x8b")) else source
         stream = io.StringIO(raw.decode("utf-8"))
+    elif hasattr(source, "read") and isinstance(source.read(0), bytes):
+        # binary stream (graph.py:162-169): gzip by flag or magic bytes
+        if gzipped is None and hasattr(source, "peek"):
+            gzipped = source.peek(2)[:2] == b"\x1f\x8b"
+        stream = io.TextIOWrapper(gzip.GzipFile(fileobj=source) if gzipped else source, encoding="utf-8")
     else:
         stream = source
     flat: list[int] = []
@@ -326,6 +359,23 @@ def as_device_graph(g, device: int = 0) -> DynamicGraph:
             pass
         return dg
     raise TypeError(f"expected a DynamicGraph, got {type(g)!r}")
+
+
+def sync_reference_graph(orig, dg: DynamicGraph, pairs=(), new_vertices: int = 0) -> None:
+    """Mirror an engine-side mutation into the reference DynamicGraph the caller
+    passed (insert_edge adds its edge to g, updates.py:124; insert_vertex adds
+    the vertex, :255-271), and re-key the cached device copy so it is kept."""
+    if isinstance(orig, DynamicGraph) or not hasattr(orig, "add_edge"):
+        return
+    for _ in range(new_vertices):
+        orig.add_vertex()
+    for u, v in pairs:
+        orig.add_edge(int(u), int(v))
+    key = (orig.vertex_count, getattr(orig, "edge_count", None), getattr(orig, "version", None), dg.device)
+    try:
+        _converted[orig] = (key, dg)
+    except TypeError:
+        pass
 
 
 def forget_device_graph(g) -> None:

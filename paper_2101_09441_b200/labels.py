@@ -255,21 +255,36 @@ class DblIndex:
         N.call("dbl_index_import", self._h, *[N.ptr(a) for a in arrs])
         self._invalidate()
 
-    @property
-    def dl_in(self) -> list[int]:
-        return _words_to_ints(self.export_words()["dl_in"])
+    def _family(self, fam: str) -> "_LabelList":
+        return _LabelList(self, fam, _words_to_ints(self.export_words()[fam]))
+
+    def _write_family(self, fam: str, values: Sequence[int]) -> None:
+        """Write one family's labels (ints, LSW first) back to the device."""
+        w = self.wdl if fam.startswith("dl") else self.wbl
+        arr = np.zeros((self._n, w), np.uint64)
+        mask = (1 << 64) - 1
+        for x, val in enumerate(values):
+            for k in range(w):
+                arr[x, k] = (int(val) >> (64 * k)) & mask
+        ptrs = [N.ptr(arr) if f == fam else None for f in ("dl_in", "dl_out", "bl_in", "bl_out")]
+        N.call("dbl_index_import", self._h, *ptrs)
+        self._invalidate()
 
     @property
-    def dl_out(self) -> list[int]:
-        return _words_to_ints(self.export_words()["dl_out"])
+    def dl_in(self) -> "_LabelList":
+        return self._family("dl_in")
 
     @property
-    def bl_in(self) -> list[int]:
-        return _words_to_ints(self.export_words()["bl_in"])
+    def dl_out(self) -> "_LabelList":
+        return self._family("dl_out")
 
     @property
-    def bl_out(self) -> list[int]:
-        return _words_to_ints(self.export_words()["bl_out"])
+    def bl_in(self) -> "_LabelList":
+        return self._family("bl_in")
+
+    @property
+    def bl_out(self) -> "_LabelList":
+        return self._family("bl_out")
 
     def _check_vertex(self, v: int) -> None:
         if not 0 <= v < self._n:
@@ -310,6 +325,21 @@ class DblIndex:
 
     def __repr__(self) -> str:
         return f"DblIndex(n={self._n}, k={self.config.k}, k_prime={self.config.k_prime})"
+
+
+class _LabelList(list):
+    """One label family as ints, one per vertex (labels.py:194-207).  Item
+    assignment writes the family back to the device, so code that edits a
+    label in place (`idx.dl_in[x] &= ~1`, as the reference's tests do to
+    forge or drop a bit) changes the index the engine uses."""
+
+    def __init__(self, idx: "DblIndex", fam: str, values: list[int]):
+        super().__init__(values)
+        self._idx, self._fam = idx, fam
+
+    def __setitem__(self, i, value):
+        super().__setitem__(i, value)
+        self._idx._write_family(self._fam, self)
 
 
 def leaf_hash(v: int, k_prime: int, seed: int = 0, *, device: int = 0) -> int:

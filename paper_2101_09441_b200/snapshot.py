@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native as N
 from .errors import DblError
-from .graph import as_device_graph
+from .graph import DynamicGraph, as_device_graph
 from .labels import DblIndex, IndexConfig, LandmarkStrategy
 
 MAGIC = b"DBLIDX01"
@@ -121,11 +121,12 @@ def save_index(idx: DblIndex, sink: Union[str, IO[bytes]]) -> None:
         sink.write(data)
 
 
-def load_index(source: Union[str, IO[bytes]], g) -> DblIndex:
+def load_index(source: Union[str, IO[bytes]], g=None) -> DblIndex:
     """Load a snapshot onto g's device (snapshot.py:104-148).
 
-    Unlike the reference, the device index is attached to a graph (the BFS
-    fallback needs it anyway); g must have the snapshot's vertex count.
+    g (optional) must have the snapshot's vertex count.  Without it, as in the
+    reference, the index gets a vertex-only device graph of its own (kept
+    alive by the index); queries and updates take the caller's graph as usual.
     """
     if isinstance(source, str):
         with open(source, "rb") as fh:
@@ -133,7 +134,8 @@ def load_index(source: Union[str, IO[bytes]], g) -> DblIndex:
     else:
         data = source.read()
     d = decode_snapshot(data)
-    g = as_device_graph(g)
+    own = g is None
+    g = DynamicGraph(d["n"]) if own else as_device_graph(g)
     if g.vertex_count != d["n"]:
         from .errors import IndexGraphMismatchError
         raise IndexGraphMismatchError(f"graph has {g.vertex_count} vertices but snapshot has {d['n']}")
@@ -143,6 +145,8 @@ def load_index(source: Union[str, IO[bytes]], g) -> DblIndex:
     N.call("dbl_index_create", g.handle, ctypes.byref(cfg.to_c()), N.ptr(lm), N.ptr(d["leaf_flags"]),
            N.ptr(d["bucket"]), None, None, 0, ctypes.byref(h))
     idx = DblIndex(h, g, cfg)
+    if own:
+        idx._own_graph = g
     idx.import_words(d)
     return idx
 

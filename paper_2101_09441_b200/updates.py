@@ -23,8 +23,10 @@ import ctypes
 from dataclasses import dataclass
 from typing import Iterable
 
+import numpy as np
+
 from . import _native as N
-from .graph import as_device_graph
+from .graph import as_device_graph, sync_reference_graph
 from .labels import DblIndex
 from .queries import _check_consistent
 
@@ -67,7 +69,7 @@ class BatchUpdateStats:
 
 def insert_edge(g, idx: DblIndex, u: int, v: int) -> UpdateStats:
     """Insert (u, v) and repair all four label families (updates.py:112-137)."""
-    g = as_device_graph(g)
+    orig, g = g, as_device_graph(g)
     _check_consistent(g, idx)
     g._check_vertex(u)
     g._check_vertex(v)
@@ -76,6 +78,7 @@ def insert_edge(g, idx: DblIndex, u: int, v: int) -> UpdateStats:
     g._m_dev += int(st.inserted)   # add_edge's return (the C side counts it the same way)
     g.version += 1
     idx._invalidate()
+    sync_reference_graph(orig, g, ((u, v),))
     return UpdateStats(int(st.visited), int(st.labels_changed), bool(st.early_terminated))
 
 
@@ -84,7 +87,7 @@ def insert_edges(g, idx: DblIndex, u, v) -> BatchUpdateStats:
 
     u/v are host arrays or CUDA tensors (device pointers) of equal length.
     """
-    g = as_device_graph(g)
+    orig, g = g, as_device_graph(g)
     _check_consistent(g, idx)
     st = N.BatchStatsC()
     if (hasattr(u, "is_cuda") and u.is_cuda) or (hasattr(v, "is_cuda") and v.is_cuda):
@@ -101,6 +104,10 @@ def insert_edges(g, idx: DblIndex, u, v) -> BatchUpdateStats:
     g._refresh_count()
     g.version += 1
     idx._invalidate()
+    if orig is not g:
+        hu = u.cpu().numpy() if hasattr(u, "cpu") else np.asarray(u)
+        hv = v.cpu().numpy() if hasattr(v, "cpu") else np.asarray(v)
+        sync_reference_graph(orig, g, zip(hu.tolist(), hv.tolist()))
     return BatchUpdateStats(int(st.requested), int(st.inserted), int(st.certified),
                             int(st.labels_changed), int(st.levels), bool(st.delta_merged),
                             int(st.fix_items), int(st.fix_edges))
@@ -109,13 +116,15 @@ def insert_edges(g, idx: DblIndex, u, v) -> BatchUpdateStats:
 def insert_vertex(g, idx: DblIndex, out_edges: Iterable[int] = (),
                   in_edges: Iterable[int] = ()) -> UpdateStats:
     """Add a vertex with empty labels and wire its edges (updates.py:255-271)."""
-    g = as_device_graph(g)
+    orig, g = g, as_device_graph(g)
     _check_consistent(g, idx)
     vid = g.add_vertex()
     idx.grow_to(g.vertex_count)
     stats = UpdateStats()
-    for w in out_edges:
+    outs, ins = list(out_edges), list(in_edges)
+    for w in outs:
         stats.absorb(insert_edge(g, idx, vid, w))
-    for w in in_edges:
+    for w in ins:
         stats.absorb(insert_edge(g, idx, w, vid))
+    sync_reference_graph(orig, g, [(vid, w) for w in outs] + [(w, vid) for w in ins], new_vertices=1)
     return stats
