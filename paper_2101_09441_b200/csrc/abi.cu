@@ -128,7 +128,7 @@ static auto g_trace_t0 = std::chrono::steady_clock::now();
 
 void trace(const char *what, cudaStream_t s) {
     if (!DBL_TRACE) return;
-    cudaStreamSynchronize(s);
+    if (DBL_TRACE == 1) cudaStreamSynchronize(s);   // 2: host enqueue times only
     auto now = std::chrono::steady_clock::now();
     double us = std::chrono::duration<double, std::micro>(now - g_trace_t0).count();
     std::fprintf(stderr, "[dbl] %-28s +%9.1f us\n", what, us);
@@ -1001,10 +1001,13 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     const bool dig_ok = idx->digest_version == idx->version;   // kept current by the change bitmaps
     ++idx->version;
     trace("insert: enter", g->stream);
-    DevBuf in, keys, alt, newk, err;
-    auto cleanup = [&]() { in.release(); keys.release(); alt.release(); newk.release(); err.release(); };
+    // the batch's workspaces stay with the graph (grow-only): no pool round
+    // trips per batch
+    DevBuf &in = g->ins_in, &keys = g->ins_keys, &alt = g->ins_alt, &newk = g->ins_newk, &err = g->ins_err;
+    auto cleanup = [&]() {};
     if ((s = keys.ensure(count * 8)) || (s = alt.ensure(count * 8)) || (s = newk.ensure(count * 8)) ||
         (s = err.ensure(32))) { cleanup(); return s; }
+    trace("insert: workspaces", g->stream);
     const uint32_t *du = u, *dv = v;
     if (mem == DBL_MEM_HOST) {
         if ((s = in.ensure(count * 8))) { cleanup(); return s; }
@@ -1021,29 +1024,33 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     // trip: counts stay on the device (the batch size bounds every launch)
     // and a range error turns the batch into a no-op (no new edges), reported
     // after the single readback -- the graph and labels are left as they were.
+    trace("insert: ordered", g->stream);
     unsigned long long *st4 = err.as<unsigned long long>();
     DBL_CUDA(cudaMemsetAsync(st4, 0, 32, g->stream));
+    trace("insert: memset", g->stream);
     // the batch is sorted on (u << b | v), b = vertex-id bits: 2b radix bits
     // instead of 32 + b (5 onesweep passes instead of 7 at n = 2^20)
     const uint32_t shift = (uint32_t)key_end_bit(g->n) - 32;
     pack_pairs_kernel<<<grid_for(count), 256, 0, g->stream>>>(du, dv, count, g->n, keys.as<uint64_t>(), st4, shift);
     DBL_LAUNCHED();
     uint64_t *sorted = nullptr;
+    trace("insert: packed", g->stream);
     if ((s = sort_keys(g, keys.as<uint64_t>(), alt.as<uint64_t>(), count, (int)(2 * shift), &sorted))) {
         cleanup();
         return s;
     }
+    trace("insert: sorted", g->stream);
     // unique (into the other buffer); its count goes to st4[3]
     uint64_t *uniq = sorted == keys.as<uint64_t>() ? alt.as<uint64_t>() : keys.as<uint64_t>();
     const uint64_t *dnu = reinterpret_cast<const uint64_t *>(st4 + 3);
     {
-        size_t tmp = 0;
-        DBL_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted, uniq, (uint64_t *)(st4 + 3), (int64_t)count,
-                                           g->stream));
-        if ((s = g->cub_tmp.ensure(tmp))) { cleanup(); return s; }
-        DBL_CUDA(cub::DeviceSelect::Unique(g->cub_tmp.p, tmp, sorted, uniq, (uint64_t *)(st4 + 3), (int64_t)count,
-                                           g->stream));
-        DBL_LAUNCHED();
+        if ((s = cub_cached(g, CUB_UNIQUE, count, 0, [&](void *t, size_t &bytes) {
+                 return cub::DeviceSelect::Unique(t, bytes, sorted, uniq, (uint64_t *)(st4 + 3), (int64_t)count,
+                                                  g->stream);
+             }))) {
+            cleanup();
+            return s;
+        }
         widen_keys_kernel<<<grid_for(count), 256, 0, g->stream>>>(uniq, count, shift, dnu);
         DBL_LAUNCHED();
     }
@@ -1082,6 +1089,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
             st.delta_merged = 1;
         }
     }
+    trace("insert: done", g->stream);
     if (range_error) { cleanup(); set_error("insert vertex outside [0, n)"); return DBL_E_VERTEX_RANGE; }
     if (!cert_read) {
         unsigned long long hcert = 0;

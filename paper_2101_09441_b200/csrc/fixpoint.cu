@@ -1902,12 +1902,15 @@ dbl_status run_insert(dbl_graph *g, dbl_index *idx, const uint64_t *new_keys, ui
         bool vec = true;
         dbl_status s = prepare_params(g, idx, pair, P, nw, vec, count_changes, i == 0);
         if (s) return s;
+        trace("insert: params", g->stream);
         if ((s = launch_insert_seed(g, P, nw, vec, count_changes, new_keys, count, dcount))) return s;
+        trace("insert: seed launched", g->stream);
         if (count_changes) {
             if ((s = launch_fixpoint<true>(g, P, nw, vec))) return s;
         } else {
             if ((s = launch_fixpoint<false>(g, P, nw, vec))) return s;
         }
+        trace("insert: fixpoint launched", g->stream);
         Ctrl h{};
         // the caller's extra device word (batch stats) rides on the last sync
         const bool last = i == half - 1;

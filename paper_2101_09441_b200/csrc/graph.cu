@@ -70,12 +70,10 @@ dbl_status sort_keys(dbl_graph *g, uint64_t *keys, uint64_t *alt, uint64_t m, in
                      uint64_t **sorted) {
     if (m == 0) { *sorted = keys; return DBL_OK; }
     cub::DoubleBuffer<uint64_t> db(keys, alt);
-    size_t tmp = 0;
-    DBL_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, (int64_t)m, 0, end_bit, g->stream));
-    dbl_status s = g->cub_tmp.ensure(tmp);
+    dbl_status s = cub_cached(g, CUB_SORT, m, (uint64_t)end_bit, [&](void *t, size_t &bytes) {
+        return cub::DeviceRadixSort::SortKeys(t, bytes, db, (int64_t)m, 0, end_bit, g->stream);
+    });
     if (s) return s;
-    DBL_CUDA(cub::DeviceRadixSort::SortKeys(g->cub_tmp.p, tmp, db, (int64_t)m, 0, end_bit, g->stream));
-    DBL_LAUNCHED();
     *sorted = db.Current();
     return DBL_OK;
 }
@@ -91,12 +89,10 @@ dbl_status build_csr_from_sorted(dbl_graph *g, const uint64_t *keys, uint64_t m,
         count_rows_kernel<<<grid_for(m + madd_ub), 256, 0, g->stream>>>(keys, m, cnt, col, madd);
         DBL_CHECK_LAUNCH("count_rows_kernel");
     }
-    size_t tmp = 0;
-    DBL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, ptr, (int64_t)n + 1, g->stream));
-    s = g->cub_tmp.ensure(tmp);
+    s = cub_cached(g, CUB_SCAN, (uint64_t)n + 1, 0, [&](void *t, size_t &bytes) {
+        return cub::DeviceScan::ExclusiveSum(t, bytes, cnt, ptr, (int64_t)n + 1, g->stream);
+    });
     if (s) return s;
-    DBL_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.p, tmp, cnt, ptr, (int64_t)n + 1, g->stream));
-    DBL_LAUNCHED();
     return DBL_OK;
 }
 
@@ -131,11 +127,10 @@ static dbl_status build_csc_by_scatter(dbl_graph *g, const uint64_t *fkeys, uint
         count_dst_kernel<<<grid_for(m + madd_ub), 256, 0, g->stream>>>(fkeys, m, cnt, madd);
         DBL_CHECK_LAUNCH("count_dst_kernel");
     }
-    size_t tmp = 0;
-    DBL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, ptr, (int64_t)n + 1, g->stream));
-    if ((s = g->cub_tmp.ensure(tmp))) return s;
-    DBL_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.p, tmp, cnt, ptr, (int64_t)n + 1, g->stream));
-    DBL_LAUNCHED();
+    if ((s = cub_cached(g, CUB_SCAN, (uint64_t)n + 1, 0, [&](void *t, size_t &bytes) {
+             return cub::DeviceScan::ExclusiveSum(t, bytes, cnt, ptr, (int64_t)n + 1, g->stream);
+         })))
+        return s;
     if (m + madd_ub) {
         DBL_CUDA(cudaMemcpyAsync(cursor, ptr, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, g->stream));
         scatter_src_kernel<<<grid_for(m + madd_ub), 256, 0, g->stream>>>(fkeys, m, cursor, col, madd);
@@ -307,11 +302,10 @@ dbl_status graph_filter_new(dbl_graph *g, const uint64_t *keys, uint64_t count, 
                                                              g->dkeys_f.as<uint64_t>(), g->m_delta, flag,
                                                              valid_dev, abort_dev);
     DBL_CHECK_LAUNCH("flag_new_kernel");
-    size_t tmp = 0;
-    DBL_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, keys, flag, out, d_n, (int64_t)count, g->stream));
-    if ((s = g->cub_tmp.ensure(tmp))) return s;
-    DBL_CUDA(cub::DeviceSelect::Flagged(g->cub_tmp.p, tmp, keys, flag, out, d_n, (int64_t)count, g->stream));
-    DBL_LAUNCHED();
+    if ((s = cub_cached(g, CUB_FLAGGED, count, 0, [&](void *t, size_t &bytes) {
+             return cub::DeviceSelect::Flagged(t, bytes, keys, flag, out, d_n, (int64_t)count, g->stream);
+         })))
+        return s;
     if (dcount) {   // caller keeps the count on the device (read back with its final sync)
         *dcount = d_n;
         *nout = count;   // upper bound
@@ -564,7 +558,8 @@ extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
                       &g->qbuf[0][0], &g->qbuf[0][1], &g->qbuf[1][0], &g->qbuf[1][1], &g->ctrl,
                       &g->changed_bits, &g->cub_tmp, &g->scratch_a, &g->scratch_b, &g->scratch_c,
                       &g->scratch_d, &g->prep, &g->haspred, &g->q_in, &g->q_codes, &g->q_vis, &g->q_pending,
-                      &g->q_counters, &g->q_dense};
+                      &g->q_counters, &g->q_dense, &g->ins_in, &g->ins_keys, &g->ins_alt, &g->ins_newk,
+                      &g->ins_err};
     set_stream(nullptr);
     for (auto *b : bufs) b->release();
     g->q_errs.release();

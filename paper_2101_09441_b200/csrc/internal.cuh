@@ -4,7 +4,9 @@
 #include <cstdint>
 #include <cstddef>
 #include <atomic>
+#include <map>
 #include <string>
+#include <tuple>
 
 #include "dbl_b200.h"
 
@@ -249,6 +251,8 @@ struct dbl_graph {
     dbl::DevBuf changed_bits;
     // generic scratch
     dbl::DevBuf cub_tmp, scratch_a, scratch_b, scratch_c, scratch_d;
+    dbl::DevBuf ins_in, ins_keys, ins_alt, ins_newk, ins_err;   // insert-batch workspaces
+    std::map<std::tuple<int, uint64_t, uint64_t>, size_t> cub_sizes;   // cub_cached
     dbl::DevBuf prep;                     // PrepState + top-k candidates
     dbl::HostBuf host_stage;
     dbl::HostBuf q_host_res;              // pinned result words of the last query batch
@@ -318,6 +322,33 @@ struct dbl_index {
 };
 
 namespace dbl {
+// A CUB device call is two calls: a temporary-storage size query, which runs
+// the whole host-side dispatch (occupancy queries; ~40 us of host time for a
+// radix sort on this box), then the real one.  The size depends only on the
+// call and its sizes, so it is cached per graph under (tag, a, b):
+// call(tmp, bytes) must issue the CUB call.
+template <class F>
+dbl_status cub_cached(dbl_graph *g, int tag, uint64_t a, uint64_t b, F &&call) {
+    const auto key = std::make_tuple(tag, a, b);
+    size_t tmp = 0;
+    auto it = g->cub_sizes.find(key);
+    if (it == g->cub_sizes.end()) {
+        cudaError_t e = call((void *)nullptr, tmp);
+        if (e != cudaSuccess) return cuda_fail(e, "CUB temporary-size query");
+        if (g->cub_sizes.size() > 4096) g->cub_sizes.clear();
+        g->cub_sizes[key] = tmp;
+    } else {
+        tmp = it->second;
+    }
+    dbl_status s = g->cub_tmp.ensure(tmp);
+    if (s) return s;
+    cudaError_t e = call(g->cub_tmp.p, tmp);
+    if (e != cudaSuccess) return cuda_fail(e, "CUB call");
+    DBL_LAUNCHED();
+    return DBL_OK;
+}
+enum { CUB_SORT = 1, CUB_UNIQUE = 2, CUB_FLAGGED = 3, CUB_SCAN = 4 };
+
 // graph.cu
 dbl_status graph_ensure_traversal(dbl_graph *g);
 dbl_status graph_degrees_dev(const dbl_graph *g, uint32_t *indeg, uint32_t *outdeg);
