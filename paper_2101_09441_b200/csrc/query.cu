@@ -53,6 +53,9 @@ constexpr uint8_t UNRESOLVED = 0xff;
 #ifndef DBL_NO_PIVOT_PRUNE
 #define DBL_NO_PIVOT_PRUNE 0   // 1: BFS fallbacks ignore the pivot sets
 #endif
+#ifndef DBL_LEAN_WAVES
+#define DBL_LEAN_WAVES 1       // K6 grid cap in waves of resident CTAs
+#endif
 #ifndef DBL_LEAN_THREADS
 #define DBL_LEAN_THREADS 256   // K6 CTA size
 #endif
@@ -1663,7 +1666,7 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
                           hp.ws, g->sm_count * wbps, (uint32_t)wsmem, wovf};
         const uint64_t per = qpt4 ? DBL_QPT_HOST * LEAN_THREADS : LEAN_THREADS;   // queries per CTA per step
         uint32_t lgrid = (uint32_t)((count + per - 1) / per);
-        if (lgrid > (uint32_t)(g->sm_count * lbps)) lgrid = (uint32_t)(g->sm_count * lbps);
+        if (lgrid > (uint32_t)(g->sm_count * lbps * DBL_LEAN_WAVES)) lgrid = (uint32_t)(g->sm_count * lbps * DBL_LEAN_WAVES);
         if (g->instrument) DBL_CUDA(cudaEventRecord(g->ev[2], g->stream));
         lean<<<lgrid, LEAN_THREADS, 0, g->stream>>>(rec, idx->n, adj, qd, pending, counters, ha);
         DBL_CHECK_LAUNCH("label_lean_kernel");
