@@ -302,6 +302,7 @@ struct BfsShared {
     uint32_t tkey[TCAP];
     unsigned long long tmask[TCAP];
     unsigned long long done;
+    unsigned long long dstart;   // done at the start of the current level (visited counts)
     unsigned long long active;
     unsigned long long sccq;   // queries taking the pivot prune
     uint32_t nlist[2];
@@ -420,6 +421,7 @@ bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_
         for (int s = tid; s < TCAP; s += blockDim.x) { S.tkey[s] = EMPTY; S.tmask[s] = 0; }
         if (tid == 0) {
             S.done = 0;
+            S.dstart = 0;
             S.sccq = 0;
             S.active = nq == 64 ? ~0ull : ((1ull << nq) - 1);
             S.nlist[0] = 0;
@@ -473,20 +475,22 @@ bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_
                 const int slot = (int)T.list[cur][e];
                 unsigned long long fw = 0;
                 if (lane == 0) {
-                    fw = T.fr[cur][slot] & ~*(volatile unsigned long long *)&S.done;
+                    const unsigned long long raw = T.fr[cur][slot];
+                    fw = raw & ~*(volatile unsigned long long *)&S.done;
                     T.fr[cur][slot] = 0;
-                }
-                fw = __shfl_sync(FULL, fw, 0);
-                if (fw == 0) continue;
-                const uint32_t w = tab_vertex<DENSE>(T, slot);
-                if (lane == 0) {
-                    unsigned long long m = fw;
+                    // visited: every vertex of each level a query starts
+                    // (levels 0..d-1 of a positive, all reached vertices of a
+                    // negative), independent of the order within the level
+                    unsigned long long m = raw & ~S.dstart;
                     while (m) {
                         const int b = __ffsll((long long)m) - 1;
                         m &= m - 1;
                         atomicAdd(&S.vcount[b], 1u);
                     }
                 }
+                fw = __shfl_sync(FULL, fw, 0);
+                if (fw == 0) continue;
+                const uint32_t w = tab_vertex<DENSE>(T, slot);
 #pragma unroll 1
                 for (int seg = 0; seg < 2; ++seg) {
                     uint32_t s0, s1;
@@ -550,7 +554,10 @@ bfs_kernel(const uint64_t *__restrict__ rec, uint32_t WDL, uint32_t WBL, uint32_
                 }
             }
             __syncthreads();
-            if (tid == 0) S.nlist[cur] = 0;
+            if (tid == 0) {
+                S.nlist[cur] = 0;
+                S.dstart = S.done;
+            }
             cur = nxt;
             __syncthreads();
         }
@@ -734,11 +741,13 @@ __device__ void warp_bfs(WarpBfs<WDL, WBL> &B, uint32_t nb, const uint64_t *__re
         for (uint32_t base = 0; base < ncur; base += 32) {
             // lane j takes frontier entry base + j
             const uint32_t ej = base + lane;
-            uint32_t fw = 0, w = 0, b0 = 0, bl = 0, d0 = 0, dl = 0;
+            uint32_t fw = 0, fc = 0, w = 0, b0 = 0, bl = 0, d0 = 0, dl = 0;
             if (ej < ncur) {
                 const uint32_t sl = B.hlist[cur][ej];
                 w = B.hkey[sl];
-                fw = B.hfr[cur][sl] & ~*(volatile uint32_t *)&B.done;
+                const uint32_t raw = B.hfr[cur][sl];
+                fw = raw & ~*(volatile uint32_t *)&B.done;
+                fc = raw & ~dn;   // visited: the whole level for every query active at its start
                 B.hfr[cur][sl] = 0;
                 if (fw) {
                     b0 = __ldg(adj.ptr + w);
@@ -752,7 +761,7 @@ __device__ void warp_bfs(WarpBfs<WDL, WBL> &B, uint32_t nb, const uint64_t *__re
             // per-query expansion counts: lane q counts the entries holding bit q
             {
                 for (int j = 0; j < 32; ++j) {
-                    const uint32_t fj = __shfl_sync(FULL, fw, j);
+                    const uint32_t fj = __shfl_sync(FULL, fc, j);
                     if ((fj >> lane) & 1) B.vcnt[lane] += 1;
                 }
             }
@@ -1153,10 +1162,11 @@ __device__ __forceinline__ int warp_query_bfs(const uint64_t *__restrict__ rec, 
     const int lane = threadIdx.x & 31;
     if (lane == 0) wq[0] = u;
     __syncwarp();
-    uint32_t qn = 1;
+    uint32_t qn = 1, lvl_end = 1;   // wq[0, lvl_end): the levels up to the one being expanded
     for (uint32_t head = 0; head < qn; ++head) {
+        if (head == lvl_end) lvl_end = qn;
         const uint32_t w = wq[head];
-        *vcount = head + 1;
+        *vcount = lvl_end;
         for (int seg = 0; seg < 2; ++seg) {
             const uint32_t *ptr = seg ? adj.dptr : adj.ptr;
             if (!ptr) break;
@@ -1196,6 +1206,7 @@ __device__ __forceinline__ int warp_query_bfs(const uint64_t *__restrict__ rec, 
             }
         }
     }
+    *vcount = qn;
     return 0;
 }
 
