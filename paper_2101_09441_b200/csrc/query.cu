@@ -1959,6 +1959,11 @@ static serve_fn pick_serve(uint32_t wdl, uint32_t wbl) {
 static std::mutex g_srv_mu;
 static dbl_graph *g_srv = nullptr;
 static std::atomic<int> g_srv_on{0};
+// A service launched for a request that exits without answering it means
+// kernel launches block until the kernel ends (a profiler or sanitizer
+// serialising launches, CUDA_LAUNCH_BLOCKING): single calls then take the
+// launch path for the rest of the process.
+static bool g_srv_off = false;
 
 static void post_stop(dbl_graph *g) {
     volatile ServeBox *vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
@@ -2058,13 +2063,15 @@ static dbl_status serve_call(const dbl_index *idx, dbl_graph *g, uint32_t u, uin
     const serve_fn fn = DBL_SERVE ? pick_serve(idx->wdl, idx->wbl) : nullptr;
     // another thread is inside a library call: take the launch path (a
     // service started now would be stopped by it anyway)
-    if (!fn || g_srv_block.load(std::memory_order_acquire) > 0) return DBL_OK;
+    if (!fn || g_srv_off || g_srv_block.load(std::memory_order_acquire) > 0) return DBL_OK;
     dbl_status s;
     for (int attempt = 0; attempt < 3; ++attempt) {
+        bool fresh = false;
         if (g_srv != g || !g->s_running || g->s_idx != idx || g->s_ver != idx->version ||
             (op == SERVE_INSERT && g->n_pend >= PEND_CAP) ||
             reinterpret_cast<volatile ServeBox *>(g->sbox.p)->alive == 0) {
             if ((s = serve_start_locked(idx, g, fn))) return s;
+            fresh = true;
         }
         volatile ServeBox *vb = reinterpret_cast<volatile ServeBox *>(g->sbox.p);
         vb->u = u;
@@ -2090,6 +2097,11 @@ static dbl_status serve_call(const dbl_index *idx, dbl_graph *g, uint32_t u, uin
                 if (vb->rseq == seq) continue;
                 g->s_running = false;
                 cudaStreamSynchronize(g->sstream);
+                if (fresh) {   // a fresh service never saw its first request: launches block
+                    g_srv_off = true;
+                    serve_stop_locked();
+                    return DBL_OK;
+                }
                 break;
             }
             if ((it & 1023) == 1023 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
@@ -2099,8 +2111,7 @@ static dbl_status serve_call(const dbl_index *idx, dbl_graph *g, uint32_t u, uin
             }
         }
     }
-    set_error("per-call service failed to start");
-    return DBL_E_CUDA;
+    return DBL_OK;   // (not reached in practice) the launch path answers it
 }
 
 // Answer one query through the service.  *served = false: the caller answers

@@ -130,3 +130,31 @@ def test_single_calls_beside_other_threads(E):
     assert not t.is_alive(), "writer thread stalled"
     assert not errors, errors
     np.testing.assert_array_equal(got, ref)
+
+
+def test_single_calls_when_launches_block(E):
+    """Under CUDA_LAUNCH_BLOCKING (as under a profiler or sanitizer, which
+    serialise launches) a service kernel cannot see the request posted after
+    its launch: the library notices the unanswered first request and answers
+    single calls on the launch path from then on."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, paper_2101_09441_b200 as E\n"
+        "from paper_2101_09441_b200 import workload as W\n"
+        "n = 1 << 11\n"
+        "g = E.DynamicGraph.from_edges(n, *W.rmat_edges(11, 8, 37))\n"
+        "idx = E.build_index(g)\n"
+        "r = np.random.default_rng(1)\n"
+        "qu = r.integers(0, n, 300, dtype=np.uint32); qv = r.integers(0, n, 300, dtype=np.uint32)\n"
+        "ref, _ = E.query_codes(g, idx, qu, qv)\n"
+        "order = list(E.AnsweredBy)\n"
+        "got = [order.index(E.query(g, idx, int(a), int(b)).answered_by) for a, b in zip(qu, qv)]\n"
+        "E.insert_edge(g, idx, 5, 9)\n"
+        "assert got == ref.tolist()\n"
+        "print('ok')\n")
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
