@@ -286,7 +286,7 @@ def cfg5(scale=26, ef=16, nq=64_000_000):
     codes, qps, st = query_rate(g, idx, qu, qv, reps=3)
     rep = E.verify_labels(g, idx, exhaustive=False)
     assert rep.ok, rep.violations[:3]
-    cols = label_columns_check(g, idx, n_lm=32, n_bk=32, seed=5)
+    cols = label_columns_check(g, idx, n_lm=256, n_bk=64, seed=5)   # every bit column: the full labels
     sample = rng.choice(nq, 200_000, replace=False)
     nchk = csr_codes_check(g, idx, qu[sample], qv[sample], codes[sample])
     return {"n": n, "m": g.edge_count, "k": 256, "k_prime": 64, "build_s": tb, "query_batch": nq,
