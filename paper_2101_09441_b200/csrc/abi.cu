@@ -719,6 +719,31 @@ static dbl_status query_host_pipelined(const dbl_index *idx, dbl_graph *g, const
 // which also writes the codes there; one launch and one stream sync instead
 // of the copy pipeline's seven operations (a single query() call).
 constexpr uint64_t STAGE_MAX = 1ull << 16;
+#ifndef DBL_STAGE_ALL
+#define DBL_STAGE_ALL 1   // 1: large pageable batches are staged too (parallel host copies), 0: copy pipeline
+#endif
+
+// memcpy split over host threads for large buffers (pageable <-> pinned
+// staging runs at one core's copy bandwidth otherwise)
+static void par_memcpy(void *dst, const void *src, size_t bytes) {
+    constexpr size_t MIN_PART = 1u << 20;
+    const unsigned hw = std::thread::hardware_concurrency();
+    size_t parts = bytes / MIN_PART;
+    if (parts > 8) parts = 8;
+    if (hw && parts > hw) parts = hw;
+    if (parts < 2) { std::memcpy(dst, src, bytes); return; }
+    const size_t chunk = (bytes / parts + 63) & ~(size_t)63;
+    std::vector<std::thread> ts;
+    ts.reserve(parts - 1);
+    for (size_t i = 1; i < parts; ++i) {
+        const size_t lo = i * chunk;
+        if (lo >= bytes) break;
+        const size_t len = lo + chunk <= bytes ? chunk : bytes - lo;
+        ts.emplace_back([=] { std::memcpy((char *)dst + lo, (const char *)src + lo, len); });
+    }
+    std::memcpy(dst, src, chunk < bytes ? chunk : bytes);
+    for (auto &t : ts) t.join();
+}
 
 static dbl_status query_host_staged(const dbl_index *idx, dbl_graph *g, const uint32_t *u, const uint32_t *v,
                                     uint64_t count, uint32_t flags, uint8_t *codes, uint32_t *visited) {
@@ -728,8 +753,8 @@ static dbl_status query_host_staged(const dbl_index *idx, dbl_graph *g, const ui
     uint32_t *su = reinterpret_cast<uint32_t *>(g->q_stage.p), *sv = su + cpad;
     uint32_t *svis = sv + cpad;
     uint8_t *sc = reinterpret_cast<uint8_t *>(svis + cpad);
-    std::memcpy(su, u, count * 4);
-    std::memcpy(sv, v, count * 4);
+    par_memcpy(su, u, count * 4);
+    par_memcpy(sv, v, count * 4);
     if ((s = run_query(idx, g, su, sv, count, flags, sc, visited ? svis : nullptr, true, true))) return s;
     uint32_t err = 0;
     bool dense = false;
@@ -739,8 +764,8 @@ static dbl_status query_host_staged(const dbl_index *idx, dbl_graph *g, const ui
         if ((s = ensure_dense(idx, g))) return s;
         return query_host_staged(idx, g, u, v, count, flags, codes, visited);
     }
-    std::memcpy(codes, sc, count);
-    if (visited) std::memcpy(visited, svis, count * 4);
+    par_memcpy(codes, sc, count);
+    if (visited) par_memcpy(visited, svis, count * 4);
     return DBL_OK;
 }
 
@@ -784,8 +809,9 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
             }
         }
         if (!pinned)
-            return count <= STAGE_MAX ? query_host_staged(idx, g, u, v, count, flags, codes, visited)
-                                      : query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
+            return (DBL_STAGE_ALL || count <= STAGE_MAX)
+                       ? query_host_staged(idx, g, u, v, count, flags, codes, visited)
+                       : query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
         if ((s = run_query(idx, g, (const uint32_t *)dptr[0], (const uint32_t *)dptr[1], count, flags,
                            (uint8_t *)dptr[2], (uint32_t *)dptr[3], sync, true)))
             return s;

