@@ -225,6 +225,11 @@ dbl_status dbl_index_digest(const dbl_index *idx, const dbl_graph *g, uint32_t *
 dbl_status dbl_query(const dbl_index *idx, const dbl_graph *g, const uint32_t *u,
                      const uint32_t *v, uint64_t count, uint32_t flags, uint8_t *codes,
                      uint32_t *visited, dbl_mem mem);
+/* query, queries.py:94-142, for one pair with scalar arguments (the
+ * per-call path: a resident service answers it without a kernel launch,
+ * see DESIGN.md §4): out[0] = AnsweredBy code, out[1] = visited. */
+dbl_status dbl_query_one(const dbl_index *idx, const dbl_graph *g, uint32_t u, uint32_t v, uint32_t flags,
+                         uint32_t *out);
 /* Same as dbl_query but enqueued on the handle's stream without a final
  * synchronisation (device memory only); dbl_sync waits for it.  Unlike the
  * synchronous calls it does not order itself after the legacy default

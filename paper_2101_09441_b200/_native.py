@@ -76,6 +76,7 @@ _SIGS = {
     "dbl_index_unpack_words": [P, P, u32, P, P],
     "dbl_label_tests": [P, P, P, u64, P, P],
     "dbl_index_digest": [P, P, P, P],
+    "dbl_query_one": [P, P, u32, u32, u32, P],
     "dbl_query": [P, P, P, P, u64, u32, P, P, i32],
     "dbl_query_async": [P, P, P, P, u64, u32, P, P],
     "dbl_query_multi": [P, P, u32, P, P, u64, u32, P, P, i32],

@@ -838,6 +838,20 @@ extern "C" dbl_status dbl_query(const dbl_index *idx, const dbl_graph *g, const 
     return query_impl(idx, g, u, v, count, flags, codes, visited, mem, true);
 }
 
+// query() for one pair with scalar arguments (the per-call path):
+// out[0] = AnsweredBy code, out[1] = visited.
+extern "C" dbl_status dbl_query_one(const dbl_index *idx, const dbl_graph *g, uint32_t u, uint32_t v,
+                                    uint32_t flags, uint32_t *out) {
+    if (!out) { set_error("null argument"); return DBL_E_ARG; }
+    uint8_t code = 0;
+    uint32_t visited = 0;
+    dbl_status s = query_impl(idx, g, &u, &v, 1, flags, &code, &visited, DBL_MEM_HOST, true);
+    if (s) return s;
+    out[0] = code;
+    out[1] = visited;
+    return DBL_OK;
+}
+
 extern "C" dbl_status dbl_query_async(const dbl_index *idx, const dbl_graph *g, const uint32_t *u,
                                       const uint32_t *v, uint64_t count, uint32_t flags, uint8_t *codes,
                                       uint32_t *visited) {

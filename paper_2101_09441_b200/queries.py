@@ -219,25 +219,39 @@ def query_codes(g, idx: DblIndex, u, v, flags: QueryFlags = DEFAULT_FLAGS,
 
 
 _ONE = threading.local()
+_DEFAULT_BITS = DEFAULT_FLAGS.bits()
+# outcomes are immutable: one shared instance per label-answered code
+_LABEL_OUTCOMES = tuple(QueryOutcome(c in REACHABLE_CODES, ANSWER_ORDER[c], 0) for c in range(len(ANSWER_ORDER)))
 
 
 def query(g, idx: DblIndex, u: int, v: int, flags: QueryFlags = DEFAULT_FLAGS) -> QueryOutcome:
-    """Answer q(u, v) (queries.py:94-142): one staged launch and one sync."""
+    """Answer q(u, v) (queries.py:94-142) through the per-call service
+    (dbl_query_one: no kernel launch per call)."""
     g = as_device_graph(g)
     _check_consistent(g, idx)
     g._check_vertex(u)
     g._check_vertex(v)
-    buf = getattr(_ONE, "buf", None)
-    if buf is None:   # per-thread 1-query buffers (u, v, visited | code) and their addresses
-        arr = np.zeros(4, np.uint32)
-        code = np.zeros(8, np.uint8)
-        buf = _ONE.buf = (arr, code, N.ptr(arr[0:1]), N.ptr(arr[1:2]), N.ptr(code),
-                          ctypes.c_void_p(arr.ctypes.data + 8))
-    arr, code, pu, pv, pc, pvis = buf
-    arr[0], arr[1] = u, v
-    N.check(N.lib().dbl_query(idx.handle, g.handle, pu, pv, 1, flags.bits(), pc, pvis, N.MEM_HOST))
-    c = int(code[0])
-    return QueryOutcome(c in REACHABLE_CODES, ANSWER_ORDER[c], int(arr[2]))
+    out = getattr(_ONE, "out", None)
+    if out is None:   # per-thread result words (code, visited)
+        out = _ONE.out = (ctypes.c_uint32 * 2)()
+    fb = _DEFAULT_BITS if flags is DEFAULT_FLAGS else flags.bits()
+    st = _query_one()(idx.handle, g.handle, u, v, fb, out)
+    if st:
+        N.check(st)
+    c, vis = out[0], out[1]
+    if vis == 0:   # label-answered (BFS answers expand at least the source)
+        return _LABEL_OUTCOMES[c]
+    return QueryOutcome(c in REACHABLE_CODES, ANSWER_ORDER[c], vis)
+
+
+_QUERY_ONE = None
+
+
+def _query_one():
+    global _QUERY_ONE
+    if _QUERY_ONE is None:
+        _QUERY_ONE = N.lib().dbl_query_one
+    return _QUERY_ONE
 
 
 def query_batch(g, idx: DblIndex, queries: Iterable[tuple[int, int]], workers: int = 1,
