@@ -458,6 +458,13 @@ def run_ours(args, rank, world, local_rank, gloo):
                      "bytes_per_query": q_bytes, "kernel_ms": k6_ms,
                      "digest_undecided_fraction": f_rec,
                      "bytes_per_query_without_digest": 8 + 1 + 4 + 2 * rec_bytes,
+                     # SURVEY.md §8(d)'s B_q (+4 B visited) over the same launch time: a
+                     # work-equivalent rate (the digest skips most record reads), not a
+                     # bandwidth claim -- as the build's survey_model below
+                     "survey_model": {"bytes_per_query": 8 + 1 + 4 + 2 * rec_bytes,
+                                      "achieved": BATCH * (13 + 2 * rec_bytes) / (k6_ms / 1e3) / 1e9,
+                                      "frac": BATCH * (13 + 2 * rec_bytes) / (k6_ms / 1e3) / 1e9 / peak,
+                                      "basis": "SURVEY.md §8(d) B_q = 8 + 1 + 2R, plus the 4-byte visited store"},
                      # what binds this kernel: SM->L2 requests (ncu count per launch) per
                      # event-timed launch against the random-gather request ceiling
                      "l2_requests": None if not l2req else {

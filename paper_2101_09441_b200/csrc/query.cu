@@ -1228,6 +1228,12 @@ constexpr uint8_t QUEUED = 0xfc;   // in the CTA's BFS queue (code written later
 #ifndef DBL_QPT_HOST
 #define DBL_QPT_HOST 4   // pairs per thread per step when they are read over PCIe (4 or 8)
 #endif
+#ifndef DBL_QPT_DEV
+#define DBL_QPT_DEV 0    // 1: device-resident pairs take the DBL_QPT_HOST kernel too
+#endif
+#ifndef DBL_QPT_MINB
+#define DBL_QPT_MINB 4   // resident 256-thread CTAs per SM of the multi-pair kernel
+#endif
 
 // Rules 0-4 for pair i = (u, v) (queries.py:94-114).  Returns the code, or
 // QUEUED if the query went to the CTA's BFS queue, or UNRESOLVED if it is
@@ -1236,7 +1242,8 @@ template <int WDL, int WBL, bool TBFS>
 __device__ __forceinline__ uint8_t lean_eval(const uint64_t *__restrict__ rec, const uint32_t *__restrict__ dig,
                                              uint32_t n, const Adj &adj, uint32_t i,
                                              uint32_t u, uint32_t v, bool use_dl, bool use_bl, bool thm1, bool thm2,
-                                             DeferQ<WDL, WBL> &dq, uint32_t *__restrict__ counters) {
+                                             DeferQ<WDL, WBL> &dq, uint32_t *__restrict__ counters,
+                                             uint32_t du = 0, uint32_t dv = 0, bool dpre = false) {
     constexpr int H = WDL + WBL, RW = 2 * H, RS = (int)rec_stride(H);
     if (u >= n || v >= n) {
         atomicOr(&counters[CNT_ERR], 1u);
@@ -1244,7 +1251,10 @@ __device__ __forceinline__ uint8_t lean_eval(const uint64_t *__restrict__ rec, c
     }
     if (u == v) return DBL_REFLEXIVE;
     if (dig) {
-        const uint8_t c = digest_decide(__ldg(dig + u), __ldg(dig + v), use_dl, use_bl);
+        // dpre: the caller loaded both digest words ahead (all of its pairs'
+        // loads in flight at once)
+        const uint8_t c = dpre ? digest_decide(du, dv, use_dl, use_bl)
+                               : digest_decide(__ldg(dig + u), __ldg(dig + v), use_dl, use_bl);
         if (c != 0xff) return c;
     }
     uint64_t a[RW], b[RW];
@@ -1307,7 +1317,7 @@ __device__ __forceinline__ void lean_pend(bool unres, uint32_t i, uint32_t *__re
 // (2 x 80 bytes at k = 256) spill at that cap, so they trade occupancy for
 // registers
 template <int WDL, int WBL, int QPT>
-__global__ void __launch_bounds__(LEAN_THREADS, (QPT > 1 ? 4 : (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_WIDE)) * 256 / LEAN_THREADS)
+__global__ void __launch_bounds__(LEAN_THREADS, (QPT > 1 ? DBL_QPT_MINB : (WDL + WBL <= 3 ? DBL_LMINB : DBL_LMINB_WIDE)) * 256 / LEAN_THREADS)
 label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj, const QueryDesc qd,
                   uint32_t *__restrict__ pending, uint32_t *__restrict__ counters, const HardArgs ha) {
     // the per-thread BFS pays off for k <= 64; with wider labels (cfg5:
@@ -1378,13 +1388,21 @@ label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj, c
                 }
             }
             uint8_t cs[QPT];
+            uint32_t dus[QPT], dvs[QPT];
+            if (qd.dig) {
+#pragma unroll
+                for (int j = 0; j < QPT; ++j) {
+                    dus[j] = bi < nblk && us[j] < n ? __ldg(qd.dig + us[j]) : 0;
+                    dvs[j] = bi < nblk && vs[j] < n ? __ldg(qd.dig + vs[j]) : 0;
+                }
+            }
 #pragma unroll
             for (int j = 0; j < QPT; ++j) {
                 bool unres = false;
                 cs[j] = QUEUED;
                 if (bi < nblk && q0 + j < count) {
                     cs[j] = lean_eval<WDL, WBL, TBFS>(rec, qd.dig, n, adj, q0 + j, us[j], vs[j], use_dl, use_bl, thm1, thm2,
-                                                      dq, counters);
+                                                      dq, counters, dus[j], dvs[j], true);
                     unres = cs[j] == UNRESOLVED;
                 }
                 lean_pend(unres, q0 + j, pending, counters);
@@ -1664,7 +1682,7 @@ dbl_status run_query(const dbl_index *idx, dbl_graph *g, const uint32_t *u, cons
     // cfg5 without the digest: 4.6 vs 3.7 G q/s for the lean gather)
     // pairs in pinned host memory (zero-copy): 4 pairs per thread per step
     // when the buffers allow the vector loads and stores
-    const bool qpt4 = host_inputs && ((((uintptr_t)u) | ((uintptr_t)v)) & 15) == 0 && (((uintptr_t)codes) & 3) == 0 &&
+    const bool qpt4 = (host_inputs || DBL_QPT_DEV) && ((((uintptr_t)u) | ((uintptr_t)v)) & 15) == 0 && (((uintptr_t)codes) & 3) == 0 &&
                       (!visited || (((uintptr_t)visited) & 15) == 0);
     if (count && (DBL_TBFS_ALL || DBL_LEAN_WIDE || idx->wdl <= 1 || qd.dig) &&
         pick_lean(idx->wdl, idx->wbl, qpt4, lean, bfsw, wsmem)) {

@@ -81,6 +81,9 @@ def main():
                 kern.append(tl.value + tb.value)
                 lab.append(tl.value)
     c = codes.cpu().numpy()
+    vv = vis.cpu().numpy()
+    import hashlib
+    chash = hashlib.sha1(c.tobytes() + (b"" if a.novis else vv.tobytes())).hexdigest()[:12]
     iu, iv = W.gen_insert_workload(src, dst, n, 100_000, 50)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -92,7 +95,8 @@ def main():
         "Gq_s": round(a.batch / statistics.mean(step) / 1e6, 2),
         "build_ms": round(statistics.mean(bt), 4), "fixpoint_ms": round(statistics.mean(ft), 4),
         "insert_edges_s": round(st.inserted / ins / 1e6, 1),
-        "unanswered": int(np.count_nonzero(c > 6)), "bfs_frac": float(np.mean((c >= 5) & (c <= 6)))}))
+        "unanswered": int(np.count_nonzero(c > 6)), "bfs_frac": float(np.mean((c >= 5) & (c <= 6))),
+        "codes_sha1": chash}))
 
 
 if __name__ == "__main__":
