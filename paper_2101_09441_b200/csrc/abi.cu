@@ -655,6 +655,13 @@ extern "C" dbl_status dbl_build_work_stats(const dbl_graph *g, dbl_build_work *o
 
 // ---------------------------------------------------------------- queries --
 
+#ifndef DBL_PIPE_CHUNK_LOG2
+#define DBL_PIPE_CHUNK_LOG2 18   // pairs per chunk of the copy pipeline (log2)
+#endif
+#ifndef DBL_PINNED_DMA
+#define DBL_PINNED_DMA 0         // > 0: pinned batches of >= 2^DBL_PINNED_DMA pairs take the copy pipeline
+#endif
+
 // Host-memory batches are pipelined in chunks: the H2D copy of chunk i+1
 // (copy stream), the query kernels of chunk i (engine stream) and the D2H copy
 // of chunk i-1 (second copy stream) overlap, so PCIe traffic in both
@@ -671,7 +678,7 @@ static dbl_status query_host_pipelined(const dbl_index *idx, dbl_graph *g, const
         DBL_CUDA(cudaStreamCreateWithFlags(&g->cstream[1], cudaStreamNonBlocking));
         for (auto &e : g->cev) DBL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    const uint64_t target = 1ull << 18;
+    const uint64_t target = 1ull << DBL_PIPE_CHUNK_LOG2;
     uint64_t nch = (count + target - 1) / target;
     if (nch < 1) nch = 1;
     if (nch > 16) nch = 16;
@@ -808,6 +815,8 @@ static dbl_status query_impl(const dbl_index *idx, const dbl_graph *gc, const ui
                 dptr[i] = at.devicePointer;
             }
         }
+        if (pinned && DBL_PINNED_DMA && count >= (1ull << DBL_PINNED_DMA))
+            return query_host_pipelined(idx, g, u, v, count, flags, codes, visited);
         if (!pinned)
             return (DBL_STAGE_ALL || count <= STAGE_MAX)
                        ? query_host_staged(idx, g, u, v, count, flags, codes, visited)

@@ -1231,6 +1231,9 @@ constexpr uint8_t QUEUED = 0xfc;   // in the CTA's BFS queue (code written later
 #ifndef DBL_QPT_DEV
 #define DBL_QPT_DEV 0    // 1: device-resident pairs take the DBL_QPT_HOST kernel too
 #endif
+#ifndef DBL_QPT_DPRE
+#define DBL_QPT_DPRE 1   // multi-pair kernel: every digest load of a thread's pairs issued first
+#endif
 #ifndef DBL_QPT_MINB
 #define DBL_QPT_MINB 4   // resident 256-thread CTAs per SM of the multi-pair kernel
 #endif
@@ -1389,7 +1392,7 @@ label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj, c
             }
             uint8_t cs[QPT];
             uint32_t dus[QPT], dvs[QPT];
-            if (qd.dig) {
+            if (DBL_QPT_DPRE && qd.dig) {
 #pragma unroll
                 for (int j = 0; j < QPT; ++j) {
                     dus[j] = bi < nblk && us[j] < n ? __ldg(qd.dig + us[j]) : 0;
@@ -1402,7 +1405,7 @@ label_lean_kernel(const uint64_t *__restrict__ rec, uint32_t n, const Adj adj, c
                 cs[j] = QUEUED;
                 if (bi < nblk && q0 + j < count) {
                     cs[j] = lean_eval<WDL, WBL, TBFS>(rec, qd.dig, n, adj, q0 + j, us[j], vs[j], use_dl, use_bl, thm1, thm2,
-                                                      dq, counters, dus[j], dvs[j], true);
+                                                      dq, counters, dus[j], dvs[j], DBL_QPT_DPRE);
                     unres = cs[j] == UNRESOLVED;
                 }
                 lean_pend(unres, q0 + j, pending, counters);
