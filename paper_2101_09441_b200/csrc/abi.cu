@@ -1084,7 +1084,7 @@ extern "C" dbl_status dbl_insert_edges(dbl_index *idx, dbl_graph *g, const uint3
     DBL_LAUNCHED();
     uint64_t *sorted = nullptr;
     trace("insert: packed", g->stream);
-    if ((s = sort_keys(g, keys.as<uint64_t>(), alt.as<uint64_t>(), count, (int)(2 * shift), &sorted))) {
+    if ((s = sort_keys_replay(g, keys.as<uint64_t>(), alt.as<uint64_t>(), count, (int)(2 * shift), &sorted))) {
         cleanup();
         return s;
     }

@@ -78,6 +78,71 @@ dbl_status sort_keys(dbl_graph *g, uint64_t *keys, uint64_t *alt, uint64_t m, in
     return DBL_OK;
 }
 
+#ifndef DBL_SORT_GRAPH
+#define DBL_SORT_GRAPH 1
+#endif
+// The insert batch's sort, replayed from a captured CUDA graph: CUB's radix
+// sort costs ~49 us of host time per call to enqueue (dispatch, occupancy
+// queries, one launch per onesweep pass; profiles/r02_ubench_cub.md), during
+// which the GPU idles between the batch's small kernels.  From the second
+// consecutive batch of the same size on the same (grow-only) workspaces, the
+// sort is one graph launch.
+// Any capture failure turns the replay off for this graph (direct calls).
+dbl_status sort_keys_replay(dbl_graph *g, uint64_t *keys, uint64_t *alt, uint64_t m, int end_bit,
+                            uint64_t **sorted) {
+    if (!DBL_SORT_GRAPH || g->sort_graph_off || m == 0 || g->instrument)
+        return sort_keys(g, keys, alt, m, end_bit, sorted);
+    // the temporary storage must exist at its final address before capture
+    size_t tmp = 0;
+    {
+        const auto ck = std::make_tuple((int)CUB_SORT, m, (uint64_t)end_bit);
+        auto it = g->cub_sizes.find(ck);
+        if (it == g->cub_sizes.end()) {
+            cub::DoubleBuffer<uint64_t> q(keys, alt);
+            cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, tmp, q, (int64_t)m, 0, end_bit, g->stream);
+            if (e != cudaSuccess) return cuda_fail(e, "CUB temporary-size query");
+            if (g->cub_sizes.size() > 4096) g->cub_sizes.clear();
+            g->cub_sizes[ck] = tmp;
+        } else {
+            tmp = it->second;
+        }
+        if (dbl_status s = g->cub_tmp.ensure(tmp)) return s;
+    }
+    const auto key = std::make_tuple((const void *)keys, (const void *)alt, m, end_bit, (const void *)g->cub_tmp.p);
+    if (!g->sort_exec || g->sort_key != key) {
+        // capture only when the previous batch had the same key (a stream of
+        // equal-size batches): a one-off size is cheaper called directly
+        if (g->sort_seen != key) {
+            g->sort_seen = key;
+            return sort_keys(g, keys, alt, m, end_bit, sorted);
+        }
+        if (g->sort_exec) { cudaGraphExecDestroy(g->sort_exec); g->sort_exec = nullptr; }
+        cub::DoubleBuffer<uint64_t> db(keys, alt);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+            const cudaError_t ec = cub::DeviceRadixSort::SortKeys(g->cub_tmp.p, tmp, db, (int64_t)m, 0, end_bit,
+                                                                  g->stream);
+            e = cudaStreamEndCapture(g->stream, &graph);
+            if (ec != cudaSuccess) e = ec;
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&g->sort_exec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            if (g->sort_exec) { cudaGraphExecDestroy(g->sort_exec); g->sort_exec = nullptr; }
+            g->sort_graph_off = true;
+            return sort_keys(g, keys, alt, m, end_bit, sorted);
+        }
+        g->sort_key = key;
+        g->sort_out = db.Current();
+    }
+    DBL_CUDA(cudaGraphLaunch(g->sort_exec, g->stream));
+    DBL_LAUNCHED();
+    *sorted = g->sort_out;
+    return DBL_OK;
+}
+
 // ptr[0..n] and col[0..m) from keys sorted by (src, dst).
 dbl_status build_csr_from_sorted(dbl_graph *g, const uint64_t *keys, uint64_t m, uint32_t n,
                                  uint32_t *ptr, uint32_t *col, const uint64_t *madd, uint64_t madd_ub) {
@@ -571,6 +636,7 @@ extern "C" dbl_status dbl_graph_free(dbl_graph *g) {
     g->q_stage.release();
     g->one_out.release();
     for (auto &ev : g->ev) if (ev) cudaEventDestroy(ev);
+    if (g->sort_exec) cudaGraphExecDestroy(g->sort_exec);
     if (g->ev_in) cudaEventDestroy(g->ev_in);
     if (g->stream) cudaStreamDestroy(g->stream);
     delete g;

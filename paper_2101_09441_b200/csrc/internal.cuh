@@ -253,6 +253,12 @@ struct dbl_graph {
     dbl::DevBuf cub_tmp, scratch_a, scratch_b, scratch_c, scratch_d;
     dbl::DevBuf ins_in, ins_keys, ins_alt, ins_newk, ins_err;   // insert-batch workspaces
     std::map<std::tuple<int, uint64_t, uint64_t>, size_t> cub_sizes;   // cub_cached
+    // the insert batch's radix sort replayed as a captured CUDA graph
+    // (graph.cu sort_keys_replay): key = buffers, size, bits, temporary storage
+    cudaGraphExec_t sort_exec = nullptr;
+    std::tuple<const void *, const void *, uint64_t, int, const void *> sort_key{}, sort_seen{};
+    uint64_t *sort_out = nullptr;
+    bool sort_graph_off = false;
     dbl::DevBuf prep;                     // PrepState + top-k candidates
     dbl::HostBuf host_stage;
     dbl::HostBuf q_host_res;              // pinned result words of the last query batch
@@ -357,6 +363,8 @@ Adj graph_rev(const dbl_graph *g);
 dbl_status build_csr_from_sorted(dbl_graph *g, const uint64_t *keys, uint64_t m, uint32_t n,
                                  uint32_t *ptr, uint32_t *col, const uint64_t *madd = nullptr,
                                  uint64_t madd_ub = 0);
+dbl_status sort_keys_replay(dbl_graph *g, uint64_t *keys, uint64_t *alt, uint64_t m, int end_bit,
+                            uint64_t **sorted);
 dbl_status sort_keys(dbl_graph *g, uint64_t *keys, uint64_t *alt, uint64_t m, int end_bit,
                      uint64_t **sorted);
 int key_end_bit(uint32_t n);
