@@ -154,6 +154,20 @@ def test_pairs_tuple_of_pairs_is_pairs():
         _pairs_to_arrays((np.array([0, 3, 4]), np.array([5, 7])))
     u, v = _pairs_to_arrays(np.array([[1, 2], [3, 4]]))
     assert u.tolist() == [1, 3] and v.tolist() == [2, 4]
+    # the fromiter fast path (a list of 2-tuples) equals np.array's on a large
+    # list, on numpy scalars and on a generator; ragged pairs still raise
+    rng = np.random.default_rng(0)
+    big = [(int(a), int(b)) for a, b in rng.integers(0, 2**32, size=(5000, 2))]
+    u, v = _pairs_to_arrays(big)
+    ref = np.array(big, dtype=np.int64)
+    assert np.array_equal(u, ref[:, 0]) and np.array_equal(v, ref[:, 1])
+    u, v = _pairs_to_arrays((p for p in [(np.uint32(4), 5), (6, np.int64(7))]))
+    assert u.tolist() == [4, 6] and v.tolist() == [5, 7]
+    for bad in ([(1, 2), (3,)], [(1, 2, 3), (4,)], [(1, 2), 3]):
+        with pytest.raises(Exception):
+            _pairs_to_arrays(bad)
+    with pytest.raises(Exception):
+        _pairs_to_arrays([(0, 2**32)])
 
 
 def test_slice_bounds_match_reference_pool():
